@@ -1,0 +1,146 @@
+/*
+ * libdashgpu — B200-native LabelTensor garble/evaluate engine for the
+ * arithmetic garbled-circuit scheme of arXiv 2302.06361 ("Dash").
+ *
+ * C-ABI drop-in boundary.  Each entry point replaces one call of the
+ * reference's dash:: C++ API (paths under /root/reference/proj/core/):
+ *
+ *   dashgpu_garble          <- dash::garble          include/dash/garble.hpp:93-94
+ *   dashgpu_garble_inputs   <- dash::garble_inputs   include/dash/garble.hpp:97-99
+ *   dashgpu_evaluate        <- dash::evaluate        include/dash/garble.hpp:103-105
+ *   dashgpu_decode_outputs  <- dash::decode_outputs  include/dash/garble.hpp:110-112
+ *   dashgpu_export_gc       <- dash::serialize_garbled_circuit  garble.hpp:116
+ *   dashgpu_export_encoding <- dash::serialize_encoding         garble.hpp:119
+ *   dashgpu_export_decoding <- dash::serialize_decoding         garble.hpp:122
+ *   dashgpu_export_bundle   <- dash::bundle_payload             garble.hpp:131
+ *   dashgpu_import_bundle   <- dash::bundle_from_payload        garble.hpp:132-134
+ *   dashgpu_circuit_create  <- dash::validate_circuit + circuit_layout   circuit.hpp:26, garble.hpp:86-88
+ *   dashgpu_circuit_info    <- dash::count_circuit / GarbleStats         circuit.hpp:61-62, garble.hpp:36-41
+ *
+ * Differences by design: every call is batched over `batch` independent
+ * inferences (one 16-byte seed each, garbled circuits are single-use), all
+ * label material stays resident in HBM (one structure-of-arrays buffer per
+ * CRT modulus), and errors are status codes instead of exceptions:
+ * DASHGPU_ERR_DATA <-> dash::DataError (CLI exit 3), DASHGPU_ERR_AUTH <->
+ * dash::AuthenticityError (exit 4), DASHGPU_ERR_OVERFLOW <-> dash::OverflowError.
+ * dashgpu_last_error() returns the thread-local message of the last failure.
+ * There is no CPU fallback: without a CUDA device every call returns
+ * DASHGPU_ERR_CUDA.
+ */
+#ifndef DASHGPU_H
+#define DASHGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "dash_circuit_desc.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DASHGPU_OK 0
+#define DASHGPU_ERR 1
+#define DASHGPU_ERR_CUDA 2
+#define DASHGPU_ERR_DATA 3
+#define DASHGPU_ERR_AUTH 4
+#define DASHGPU_ERR_OVERFLOW 5
+
+typedef struct dashgpu_circuit dashgpu_circuit;
+typedef struct dashgpu_network dashgpu_network;
+typedef struct dashgpu_bundle dashgpu_bundle;
+
+typedef struct dashgpu_circuit_info {
+    int32_t k;
+    uint32_t n_layers;
+    uint64_t n_in, n_out;
+    uint64_t cts, gates, wires;      /* per inference (GarbleStats, garble.hpp:36-41) */
+    uint32_t sign_t;                 /* mixed-radix digits (0 when no activation) */
+    uint16_t radices[32];
+    uint64_t relu_elements;          /* activation elements per inference */
+    uint64_t linear_macs;            /* digit multiply-accumulates per inference and pass */
+    uint64_t act_uc_cts;             /* ciphertexts per activation element */
+    uint32_t max_slots;
+} dashgpu_circuit_info;
+
+typedef struct dashgpu_timing {
+    double ms_garble, ms_encode, ms_evaluate, ms_decode, ms_total;
+    uint64_t h2d_bytes, d2h_bytes;
+    uint32_t sub_batches;
+} dashgpu_timing;
+
+const char* dashgpu_last_error(void);
+int dashgpu_version(void);
+/* Selects the CUDA device and uploads the constant tables. */
+int dashgpu_init(int device);
+/* Stream all work is enqueued on (a cudaStream_t; NULL = legacy default). */
+int dashgpu_set_stream(void* stream);
+
+/* ---- circuits (host) ---- */
+int dashgpu_circuit_create(const dash_circuit_desc* desc, dashgpu_circuit** out);
+void dashgpu_circuit_destroy(dashgpu_circuit* c);
+int dashgpu_circuit_info_get(const dashgpu_circuit* c, dashgpu_circuit_info* out);
+/* Deterministic synthetic models: the reference test builders
+ * (tests/support/test_models.hpp: model_a, model_c, model_d, model_f_dims,
+ * model_tiny) plus "lenet5", "minionn" (paper Model F) and "relu<N>" /
+ * "sign<N>" single-layer sweeps. */
+int dashgpu_model_build(const char* name, uint32_t seed, int k, int private_weights,
+                        dashgpu_circuit** out);
+/* View of the circuit's quantized parameters (valid while c lives). */
+int dashgpu_circuit_desc_view(const dashgpu_circuit* c, dash_circuit_desc* out);
+/* testsupport::random_input(c, rng(seed), lo, hi) */
+int dashgpu_random_input(const dashgpu_circuit* c, uint32_t seed, int lo, int hi, int64_t* out);
+/* circuit_plain_forward (circuit.hpp:48-50), host reference semantics. */
+int dashgpu_plain_forward(const dashgpu_circuit* c, const int64_t* in, int64_t* out);
+
+/* ---- garbling / evaluation (device) ---- */
+/* seeds: batch*16 bytes (host).  The network keeps the garbled circuit,
+ * encoding and decoding information of every inference in HBM. */
+int dashgpu_garble(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
+                   dashgpu_network** out);
+void dashgpu_network_destroy(dashgpu_network* n);
+/* values: host [batch][n_in] signed quantized inputs */
+int dashgpu_garble_inputs(dashgpu_network* n, const int64_t* values, dashgpu_bundle** out);
+int dashgpu_evaluate(dashgpu_network* n, const dashgpu_bundle* in, dashgpu_bundle** out);
+/* values: host [batch][n_out]; DASHGPU_ERR_AUTH if any label misses its table */
+int dashgpu_decode_outputs(dashgpu_network* n, const dashgpu_bundle* out, int64_t* values);
+void dashgpu_bundle_destroy(dashgpu_bundle* b);
+
+/* ---- reference wire formats (byte-identical to the reference) ---- */
+int dashgpu_export_gc(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len);
+int dashgpu_export_encoding(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len);
+int dashgpu_export_decoding(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len);
+int dashgpu_export_bundle(const dashgpu_bundle* bd, uint32_t b, uint8_t* buf, size_t cap, size_t* len);
+/* payload of every inference concatenated ([batch][k][n][16] bytes) */
+int dashgpu_import_bundle(dashgpu_network* n, const uint8_t* data, size_t len, int output,
+                          dashgpu_bundle** out);
+/* fault injection for tests: XOR `mask` (16 bytes) into ciphertext `index` of inference b */
+int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint8_t* mask16);
+
+/* ---- fused pipeline: garble + garble_inputs + evaluate + decode_outputs ----
+ * inputs [batch][n_in], outputs [batch][n_out].  on_device=0: host buffers
+ * (copies inside the call); on_device=1: device pointers (seeds too).
+ * Sub-batches automatically when the garbled circuits exceed free HBM. */
+int dashgpu_infer(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
+                  const int64_t* inputs, int64_t* outputs, int on_device, dashgpu_timing* t);
+
+/* ---- per-kernel CUDA-event timing on the launching stream ---- */
+int dashgpu_profile(int enable);
+/* kinds: 0 act-garble 1 act-eval 2 linear 3 priv-garble 4 priv-eval 5 setup 6 encode 7 decode 8 misc */
+int dashgpu_profile_read(double* ms, uint64_t* launches, int max_kinds);
+
+/* ---- primitive kernels (parity tests) ----
+ * op 0: decompress_mod(in[i], m) -> digits (u16), then compress -> out[i]
+ * op 1: AES-128 under the all-zero key (fixed permutation pi)
+ * op 2: AES-128 under key16
+ * op 3: LabelPrf::draw(wires[i], stream=q, m) -> digits
+ * op 4: out[i] = encrypt_label(key=decompress(in[i], m), tweak{gate, i%7, i%3}, msg=decompress(out[i], q))
+ * op 5: digits = decrypt_label(key=decompress(in[i], m), tweak{gate, i%7, i%3}, ct=out[i], q)
+ * in/out: n u128 as (lo, hi) u64 pairs; digits: n*128 u16. */
+int dashgpu_prim(int op, uint32_t n, int m, int q, const uint64_t* in, uint64_t* out, uint16_t* digits,
+                 const uint8_t* key16, const uint64_t* wires, uint64_t gate);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,349 @@
+// Per-thread logic of the non-tape kernels: public-weight linear lanes,
+// private-weight (projection) linear lanes, PRF setup, input encoding,
+// decoding tables / decode and label export.
+#pragma once
+
+#include "dash_device.cuh"
+
+namespace dashgpu {
+
+// ---------------------------------------------------------------------------
+// Public-weight linear lane (reference layer.cpp:122-191):
+//   out[u][d] = (sum_{i: w!=0 mod p} (w mod p) x_i[d] + z_u zero[d] - [garbler] b_u R_p[d]) mod p
+// One thread = four digits (one word w) of one output unit of one inference.
+struct LinParams {
+    int conv;
+    uint32_t K;          // in_dim or in_ch*f*f
+    uint32_t M;          // output units
+    uint32_t E_in;
+    uint32_t in_ch, H, W, f, stride, OH, OW;
+    const uint8_t* wres; // dense: [K][M]; conv: [out_ch][K]   (w mod p)
+    const uint8_t* zt;   // [M] (dense) / [out_ch] (conv): #zero-residue weights mod p
+    const uint8_t* bres; // [M] / [out_ch]: bias residue (garbler only)
+    const uint32_t* in;  // [B][nw][E_in]
+    uint32_t* out;       // [B][nw][M]
+    const uint32_t* zero;// zero-wire label of this lane (byte digits), inference b at zero[b*zstride]
+    const uint32_t* R;   // offset R_p (byte digits), garbler only, same stride
+    uint32_t zstride;
+    uint32_t p, nw, B;
+    int garbler;
+};
+
+DASH_HD void linear_thread(const LinParams& L, uint32_t b, uint32_t w, uint32_t u) {
+    const ModC& M = c_mod[L.p];
+    uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    const uint32_t* xin = L.in + ((uint64_t)b * L.nw + w) * L.E_in;
+    uint32_t oc = 0;
+    if (!L.conv) {
+        for (uint32_t i = 0; i < L.K; ++i) {
+            const uint32_t wv = L.wres[(uint64_t)i * L.M + u];
+            const uint32_t x = xin[i];
+            acc0 += wv * (x & 0xffu);
+            acc1 += wv * ((x >> 8) & 0xffu);
+            acc2 += wv * ((x >> 16) & 0xffu);
+            acc3 += wv * (x >> 24);
+        }
+    } else {
+        oc = u / (L.OH * L.OW);
+        const uint32_t oy = (u / L.OW) % L.OH, ox = u % L.OW;
+        const uint8_t* wr = L.wres + (uint64_t)oc * L.K;
+        uint32_t i = 0;
+        for (uint32_t ic = 0; ic < L.in_ch; ++ic)
+            for (uint32_t ky = 0; ky < L.f; ++ky) {
+                const uint32_t* row = xin + ((uint64_t)ic * L.H + (oy * L.stride + ky)) * L.W + ox * L.stride;
+                for (uint32_t kx = 0; kx < L.f; ++kx, ++i) {
+                    const uint32_t wv = wr[i];
+                    const uint32_t x = row[kx];
+                    acc0 += wv * (x & 0xffu);
+                    acc1 += wv * ((x >> 8) & 0xffu);
+                    acc2 += wv * ((x >> 16) & 0xffu);
+                    acc3 += wv * (x >> 24);
+                }
+            }
+    }
+    const uint32_t idx = L.conv ? oc : u;
+    const uint32_t z = L.zt[idx];
+    const uint32_t nb = L.garbler ? (L.bres[idx] ? L.p - L.bres[idx] : 0u) : 0u;
+    const uint32_t zw = L.zero[(uint64_t)b * L.zstride + w];
+    const uint32_t rw = L.garbler ? L.R[(uint64_t)b * L.zstride + w] : 0u;
+    uint32_t accs[4] = {acc0, acc1, acc2, acc3};
+    uint32_t o = 0;
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t s = accs[j] - fdiv(accs[j], M.mag_m, M.sh_m) * L.p;
+        const uint32_t t = s + z * ((zw >> (8 * j)) & 0xffu) + nb * ((rw >> (8 * j)) & 0xffu);
+        const uint32_t d = t - fdiv(t, M.mag_m, M.sh_m) * L.p;
+        o |= d << (8 * j);
+    }
+    // digits beyond n in the top word stay zero (inputs are zero there)
+    if (4 * w + 4 > M.n) o &= 0xffffffffu >> (8 * (4 * w + 4 - M.n));
+    L.out[((uint64_t)b * L.nw + w) * L.M + u] = o;
+}
+
+// ---------------------------------------------------------------------------
+// Private-weight linear lane (layer.cpp:195-212, 456-507): per weight one
+// projection x -> w*x mod p, free add, then add_public_constant(bias).
+struct PrivParams {
+    int conv;
+    uint32_t win;            // window
+    uint32_t M;              // units
+    uint32_t E_in;
+    uint32_t in_ch, H, W, f, stride, OH, OW;
+    const uint8_t* wres;     // [M][win] (dense) / [out_ch][win] (conv)
+    const uint8_t* bres;     // [M] / [out_ch]
+    const uint32_t* in;      // [B][nw][E_in]
+    uint32_t* out;           // [B][nw][M]
+    uint32_t p, B;
+    uint64_t gate_base, wire_base;   // layer base + lane offset
+    U4* blob;                // layer blob of inference 0, already offset by the lane's ct offset
+    uint64_t blob_stride;
+    const uint32_t* rk;      // [B][44]
+    const uint32_t* mult;    // [B][...]
+    uint64_t mult_stride;
+    int garbler;
+};
+
+DASH_HD void private_thread(const PrivParams& P, uint32_t b, uint32_t u, const AesTab& t) {
+    const ModC& M = c_mod[P.p];
+    const uint32_t p = P.p;
+    Elt e;
+    e.b = b;
+    e.u = u;
+    e.rk = P.rk + (uint64_t)b * 44;
+    e.mult = P.mult + (uint64_t)b * P.mult_stride;
+    e.t = t;
+    U4* rows = P.blob + (uint64_t)b * P.blob_stride + (uint64_t)u * P.win * p;
+    uint32_t oc = 0, oy = 0, ox = 0;
+    if (P.conv) {
+        oc = u / (P.OH * P.OW);
+        oy = (u / P.OW) % P.OH;
+        ox = u % P.OW;
+    }
+    const uint8_t* wr = P.wres + (uint64_t)(P.conv ? oc : u) * P.win;
+    const uint32_t* Rp = P.garbler ? mult_row(e, p, 1) : nullptr;
+    Lab sum;
+    lab_zero(sum);
+    for (uint32_t j = 0; j < P.win; ++j) {
+        uint64_t xi;
+        if (!P.conv) {
+            xi = j;
+        } else {
+            const uint32_t ic = j / (P.f * P.f), ky = (j / P.f) % P.f, kx = j % P.f;
+            xi = ((uint64_t)ic * P.H + (oy * P.stride + ky)) * P.W + (ox * P.stride + kx);
+        }
+        Lab x, term;
+        lab_load_rows(x, P.in + ((uint64_t)b * M.nw) * P.E_in + xi, P.E_in, M);
+        const uint64_t g = P.gate_base + (uint64_t)u * P.win + j;
+        U4* R = rows + (uint64_t)j * p;
+        const uint32_t c = color(x, M);
+        if (P.garbler) {
+            prf_label(term, P.wire_base + (uint64_t)u * P.win + j, 0, M, e.rk, t);
+            const uint32_t w = wr[j];
+            for (uint32_t a = 0; a < p; ++a) {
+                uint32_t row = c + a;
+                row = row >= p ? row - p : row;
+                const U4 H = hash_tw(compress(x, M), g, row, 0, t);
+                Lab pay = term;
+                lab_add_g(pay, mult_row(e, p, (w * a) % p), M);
+                R[row] = enc_with(H, pay, M);
+                lab_add_g(x, Rp, M);
+            }
+        } else {
+            dec_row(term, x, M, g, c, 0, R[c], M, t);
+        }
+        if (j == 0) sum = term;
+        else lab_add(sum, term, M);
+    }
+    if (P.garbler) {
+        const uint32_t bb = P.bres[P.conv ? oc : u];
+        if (bb) lab_sub_g(sum, mult_row(e, p, bb), M);
+    }
+    lab_store_rows(sum, P.out + ((uint64_t)b * M.nw) * P.M + u, P.M, M);
+}
+
+// ---------------------------------------------------------------------------
+// Garbling setup: offsets R_m and their multiples v*R_m (prf.hpp:28-32,
+// gadgets.hpp:20-34), zero-wire / input base labels (garble.cpp:155-173) and
+// the seed commitment (garble.cpp:199-204).
+struct SetupParams {
+    uint32_t B;
+    int k;
+    uint16_t primes[MAXK];
+    uint32_t nslot;
+    uint16_t slot_mod[MAXMOD + 1];
+    const uint32_t* rk;        // [B][44]
+    const uint8_t* seeds;      // [B][16]
+    uint32_t* mult;            // [B][nslot][128][NWMAX]
+    uint64_t mult_stride;
+    uint32_t n_in;
+    uint32_t* base_planes[MAXK]; // [B][nw][n_in] input base labels (encoding info)
+    uint32_t* zero;            // [B][k][LABW] byte-digit words
+    uint32_t* Rb;              // [B][k][LABW] offsets of the primes, byte-digit words
+    U4* commit;                // [B]
+};
+
+DASH_HD void setup_offsets_thread(const SetupParams& S, uint32_t b, uint32_t si, const AesTab& t) {
+    const uint32_t m = S.slot_mod[si];
+    const ModC& M = c_mod[m];
+    Lab R, v;
+    prf_label(R, m, 1, M, S.rk + (uint64_t)b * 44, t);
+    // digit 0 forced to 1 (prf.hpp:28-32)
+    if (M.pow2) R.w[0] = (R.w[0] & ~(M.m - 1u)) | 1u;
+    else R.w[0] = (R.w[0] & ~0xffu) | 1u;
+    uint32_t* base = S.mult + (uint64_t)b * S.mult_stride + (uint64_t)c_modslot[m] * 128 * NWMAX;
+    for (uint32_t x = 0; x < m; ++x) {
+        lab_scale(v, R, x, M);
+        for (int w = 0; w < NWMAX; ++w) base[(uint64_t)x * NWMAX + w] = v.w[w];
+    }
+    for (int i = 0; i < S.k; ++i)
+        if (S.primes[i] == m) lab_store_rows(R, S.Rb + ((uint64_t)b * S.k + i) * LABW, 1, M);
+}
+
+DASH_HD void setup_labels_thread(const SetupParams& S, uint32_t b, uint32_t e, int i, const AesTab& t) {
+    // e < n_in: input base of element e, lane i (wire k + e*k + i); e == n_in: zero wire i
+    const uint32_t p = S.primes[i];
+    const ModC& M = c_mod[p];
+    Lab L;
+    const uint32_t* rk = S.rk + (uint64_t)b * 44;
+    if (e < S.n_in) {
+        prf_label(L, (uint64_t)S.k + (uint64_t)e * S.k + (uint64_t)i, 0, M, rk, t);
+        lab_store_rows(L, S.base_planes[i] + ((uint64_t)b * M.nw) * S.n_in + e, S.n_in, M);
+    } else {
+        prf_label(L, (uint64_t)i, 0, M, rk, t);
+        lab_store_rows(L, S.zero + ((uint64_t)b * S.k + i) * LABW, 1, M);
+    }
+    if (e == S.n_in && i == 0) {
+        // seed commitment = davies_meyer(seed bytes read little-endian)
+        const uint8_t* sd = S.seeds + (uint64_t)b * 16;
+        U4 v;
+        for (int j = 0; j < 4; ++j)
+            v.x[j] = (uint32_t)sd[4 * j] | ((uint32_t)sd[4 * j + 1] << 8) | ((uint32_t)sd[4 * j + 2] << 16) |
+                     ((uint32_t)sd[4 * j + 3] << 24);
+        U4 h = aes_pi(v, t);
+        for (int j = 0; j < 4; ++j) h.x[j] ^= v.x[j];
+        S.commit[b] = h;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// garble_inputs (garble.cpp:242-263): label = base + (enc(v) mod p) R_p
+struct EncodeParams {
+    uint32_t B, n_in;
+    int k;
+    uint16_t primes[MAXK];
+    const int64_t* values;     // [B][n_in]
+    const uint32_t* base[MAXK];// [B][nw][n_in]
+    uint32_t* out[MAXK];       // [B][nw][n_in]
+    const uint32_t* mult;
+    uint64_t mult_stride;
+    uint64_t half_up_lo, half_up_hi;  // ceil(P/2) as u128
+    uint64_t half_dn_lo, half_dn_hi;  // floor(P/2)
+    int* err;
+};
+
+DASH_HD void encode_thread(const EncodeParams& P, uint32_t b, uint32_t e, int i) {
+    const uint32_t p = P.primes[i];
+    const ModC& M = c_mod[p];
+    const int64_t v = P.values[(uint64_t)b * P.n_in + e];
+    const u128 half_up = ((u128)P.half_up_hi << 64) | P.half_up_lo;
+    const u128 half_dn = ((u128)P.half_dn_hi << 64) | P.half_dn_lo;
+    uint32_t r;
+    if (v >= 0) {
+        if ((u128)(uint64_t)v >= half_up) {
+            *P.err = ST_DATA;
+            return;
+        }
+        r = (uint32_t)((uint64_t)v % p);
+    } else {
+        const uint64_t mag = (uint64_t)(-(v + 1)) + 1;
+        if ((u128)mag > half_dn) {
+            *P.err = ST_DATA;
+            return;
+        }
+        const uint32_t mr = (uint32_t)(mag % p);
+        r = mr ? p - mr : 0;
+    }
+    Lab L;
+    lab_load_rows(L, P.base[i] + ((uint64_t)b * M.nw) * P.n_in + e, P.n_in, M);
+    Elt ex;
+    ex.mult = P.mult + (uint64_t)b * P.mult_stride;
+    lab_add_g(L, mult_row(ex, p, r), M);
+    lab_store_rows(L, P.out[i] + ((uint64_t)b * M.nw) * P.n_in + e, P.n_in, M);
+}
+
+// ---------------------------------------------------------------------------
+// Decoding tables (garble.cpp:208-231) and decode_outputs (314-343)
+struct DecodeParams {
+    uint32_t B, n_out;
+    int k;
+    uint16_t primes[MAXK];
+    uint16_t poff[MAXK + 1];   // prefix sums of the primes
+    const uint32_t* lanes[MAXK];  // [B][nw][n_out] base (tables) or active (decode) labels
+    U4* table;                 // [B][n_out][sum_p]
+    const uint32_t* mult;
+    uint64_t mult_stride;
+    uint8_t* residues;         // [B][n_out][k]
+    int* err;
+};
+
+DASH_HD void dectable_thread(const DecodeParams& P, uint32_t b, uint32_t e, int i) {
+    const uint32_t p = P.primes[i];
+    const ModC& M = c_mod[p];
+    Lab base;
+    lab_load_rows(base, P.lanes[i] + ((uint64_t)b * M.nw) * P.n_out + e, P.n_out, M);
+    Elt ex;
+    ex.mult = P.mult + (uint64_t)b * P.mult_stride;
+    U4* row = P.table + ((uint64_t)b * P.n_out + e) * P.poff[P.k] + P.poff[i];
+    for (uint32_t v = 0; v < p; ++v) {
+        Lab c = base;
+        lab_add_g(c, mult_row(ex, p, v), M);
+        row[v] = compress(c, M);
+    }
+}
+
+DASH_HD void decode_thread(const DecodeParams& P, uint32_t b, uint32_t e) {
+    for (int i = 0; i < P.k; ++i) {
+        const uint32_t p = P.primes[i];
+        const ModC& M = c_mod[p];
+        Lab L;
+        lab_load_rows(L, P.lanes[i] + ((uint64_t)b * M.nw) * P.n_out + e, P.n_out, M);
+        const U4 c = compress(L, M);
+        const U4* row = P.table + ((uint64_t)b * P.n_out + e) * P.poff[P.k] + P.poff[i];
+        int found = -1;
+        for (uint32_t v = 0; v < p; ++v) {
+            const U4 t = row[v];
+            if (found < 0 && t.x[0] == c.x[0] && t.x[1] == c.x[1] && t.x[2] == c.x[2] && t.x[3] == c.x[3])
+                found = (int)v;
+        }
+        if (found < 0) {
+            *P.err = ST_AUTH;
+            found = 0;
+        }
+        P.residues[((uint64_t)b * P.n_out + e) * P.k + i] = (uint8_t)found;
+    }
+}
+
+// compress every label of a lane plane: out[b][e] (bundle payload / tensor_write)
+struct CompressParams {
+    uint32_t B, n;
+    uint32_t p;
+    const uint32_t* lane;  // [B][nw][n]
+    U4* out;               // [B][n] strided: out[b*ostride + e]
+    uint64_t ostride;
+};
+
+DASH_HD void compress_thread(const CompressParams& P, uint32_t b, uint32_t e) {
+    const ModC& M = c_mod[P.p];
+    Lab L;
+    lab_load_rows(L, P.lane + ((uint64_t)b * M.nw) * P.n + e, P.n, M);
+    P.out[(uint64_t)b * P.ostride + e] = compress(L, M);
+}
+
+// parse side of the bundle format: decompress_mod every chunk into a lane plane
+DASH_HD void decompress_thread(const CompressParams& P, uint32_t b, uint32_t e, uint32_t* lane_out) {
+    const ModC& M = c_mod[P.p];
+    Lab L;
+    decompress(L, P.out[(uint64_t)b * P.ostride + e], M);
+    lab_store_rows(L, lane_out + ((uint64_t)b * M.nw) * P.n + e, P.n, M);
+}
+
+}  // namespace dashgpu

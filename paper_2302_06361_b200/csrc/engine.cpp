@@ -1,0 +1,2027 @@
+// Host engine of the B200 Dash garble/evaluate path (plain C++; all device
+// work goes through launch.hpp).
+//
+//  * host math: digit capacities / codec constants (reference label.cpp:15-64),
+//    AES key schedule (aes.cpp:32-46), CRT base (crt.cpp:38-101), mixed-radix
+//    spec search and sign tables (mixed_radix.cpp:59-212), sign plan
+//    (gadgets.cpp:5-28);
+//  * the activation "gadget tape": the reference's t_approx_sign_bit /
+//    relu_element / sign_act_element (gadgets.hpp:382-481, layer.cpp:214-236)
+//    recorded once in reference order so every gate / fresh wire / ciphertext
+//    gets the reference's per-element offset, then re-scheduled depth-first
+//    to keep few labels live and mapped onto per-thread label slots;
+//  * circuit preparation and layout (circuit.cpp, garble.cpp:16-42);
+//  * the batched network driver: garble / garble_inputs / evaluate /
+//    decode_outputs over B inferences resident in HBM (garble.cpp:134-343);
+//  * reference wire formats (garble.cpp:347-526) and the C ABI (dashgpu.h).
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dashgpu.h"
+#include "launch.hpp"
+
+namespace dashgpu {
+
+struct DataError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct OverflowErr : DataError {
+    using DataError::DataError;
+};
+struct AuthError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+static const int kPrimes[MAXK] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53};
+
+// =========================================================== host math
+
+// n_m = max{n : m^n <= 2^128} (label.cpp:15-29)
+static int n_digits_host(int m) {
+    const u128 limit = ((u128)0 - 1) / (u128)m;
+    u128 acc = 1;
+    int n = 0;
+    while (acc <= limit) {
+        acc *= (u128)m;
+        ++n;
+    }
+    if ((m & (m - 1)) == 0) {
+        int e = 0;
+        while ((1 << e) < m) ++e;
+        if (e * (n + 1) == 128) ++n;
+    }
+    return n;
+}
+
+static int bitlen(u128 x) {
+    int b = 0;
+    while (x) {
+        ++b;
+        x >>= 1;
+    }
+    return b;
+}
+
+// floor(x / d) = umulhi(x, mag) >> sh for 0 <= x < 2^31 (Granlund-Montgomery)
+static void magic31(uint64_t d, uint32_t& mag, uint32_t& sh) {
+    int l = 0;
+    while (((uint64_t)1 << l) < d) ++l;
+    if (l == 0) l = 1;
+    const u128 num = (u128)1 << (31 + l);
+    const u128 M = (num + d - 1) / d;
+    if (M >> 32) throw std::logic_error("magic31 overflow");
+    mag = (uint32_t)M;
+    sh = (uint32_t)(l - 1);
+    // spot-check exactness at the range edges
+    const uint64_t probes[] = {0, 1, d - 1, d, d + 1, (1u << 31) - 1, (1u << 31) - d, 12345677};
+    for (uint64_t x : probes) {
+        if (x >= (1ull << 31)) continue;
+        if ((((uint64_t)x * mag) >> 32 >> sh) != x / d) throw std::logic_error("magic31 inexact");
+    }
+}
+
+static ModC make_modc(int m) {
+    ModC c;
+    std::memset(&c, 0, sizeof c);
+    c.m = (uint16_t)m;
+    c.n = (uint8_t)n_digits_host(m);
+    c.nw = (uint8_t)((c.n + 3) / 4);
+    c.pow2 = (m & (m - 1)) == 0;
+    c.e = 0;
+    if (c.pow2)
+        while ((1 << (c.e + 1)) <= m) ++c.e;
+    c.full = c.pow2 && c.e * c.n == 128;
+    magic31((uint64_t)m, c.mag_m, c.sh_m);
+    c.mag64 = (uint64_t)(~0ull / (uint64_t)m) + 1;
+    c.spread = (uint32_t)m * 0x01010101u;
+    c.addc = (uint32_t)(128 - (m < 128 ? m : 127)) * 0x01010101u;
+    if (c.pow2) {
+        u128 bits = 0, hi = 0, lo = 0;
+        for (int i = 0; i < c.n; ++i) {
+            lo |= (u128)1 << (c.e * i);
+            hi |= (u128)1 << (c.e * i + c.e - 1);
+        }
+        bits = c.e * c.n >= 128 ? ~(u128)0 : (((u128)1 << (c.e * c.n)) - 1);
+        for (int j = 0; j < 4; ++j) {
+            c.bits[j] = (uint32_t)(bits >> (32 * j));
+            c.hi[j] = (uint32_t)(hi >> (32 * j));
+            c.lo[j] = (uint32_t)(lo >> (32 * j));
+        }
+        c.m4 = (uint32_t)m * m * m * m;
+        return c;
+    }
+    c.m4 = (uint32_t)m * m * m * m;
+    int W = 1;
+    while (true) {
+        u128 p = 1;
+        for (int i = 0; i < 4 * (W + 1); ++i) p *= (u128)m;
+        if (p > ((u128)1 << 31)) break;
+        ++W;
+    }
+    c.W = (uint8_t)W;
+    u128 D = 1;
+    for (int i = 0; i < 4 * W; ++i) D *= (u128)m;
+    c.D = (uint32_t)D;
+    c.nchunks = (uint8_t)((c.nw + W - 1) / W);
+    u128 bound = ~(u128)0;
+    for (int j = 0; j < c.nchunks && j < 21; ++j) {
+        const int b = bitlen(bound);
+        c.limbs[j] = (uint8_t)((b + 31) / 32);
+        if (c.limbs[j] == 0) c.limbs[j] = 1;
+        bound /= D;
+    }
+    magic31(c.m4, c.mag_m4, c.sh_m4);
+    c.invD = ~0ull / (uint64_t)c.D;
+    return c;
+}
+
+// ---- AES-128 key schedule + T0 table (FIPS-197; aes.cpp:32-46) ----
+static uint8_t g_sbox[256];
+static void sbox_init() {
+    static bool done = false;
+    if (done) return;
+    auto gmul = [](uint8_t a, uint8_t b) {
+        uint8_t r = 0;
+        while (b) {
+            if (b & 1) r ^= a;
+            a = (uint8_t)((a << 1) ^ ((a & 0x80) ? 0x1b : 0));
+            b >>= 1;
+        }
+        return r;
+    };
+    auto rotl8 = [](uint8_t x, int s) { return (uint8_t)((x << s) | (x >> (8 - s))); };
+    for (int x = 0; x < 256; ++x) {
+        uint8_t inv = 0;
+        for (int y = 1; x && y < 256; ++y)
+            if (gmul((uint8_t)x, (uint8_t)y) == 1) {
+                inv = (uint8_t)y;
+                break;
+            }
+        g_sbox[x] = (uint8_t)(inv ^ rotl8(inv, 1) ^ rotl8(inv, 2) ^ rotl8(inv, 3) ^ rotl8(inv, 4) ^ 0x63);
+    }
+    done = true;
+}
+
+static void aes_expand_host(const uint8_t key[16], uint32_t rk[44]) {
+    static const uint8_t rcon[10] = {1, 2, 4, 8, 16, 32, 64, 128, 0x1b, 0x36};
+    sbox_init();
+    uint8_t w[176];
+    std::memcpy(w, key, 16);
+    for (int i = 4; i < 44; ++i) {
+        uint8_t t[4];
+        std::memcpy(t, w + 4 * (i - 1), 4);
+        if (i % 4 == 0) {
+            const uint8_t t0 = t[0];
+            t[0] = (uint8_t)(g_sbox[t[1]] ^ rcon[i / 4 - 1]);
+            t[1] = g_sbox[t[2]];
+            t[2] = g_sbox[t[3]];
+            t[3] = g_sbox[t0];
+        }
+        for (int j = 0; j < 4; ++j) w[4 * i + j] = (uint8_t)(w[4 * (i - 4) + j] ^ t[j]);
+    }
+    for (int i = 0; i < 44; ++i)
+        rk[i] = (uint32_t)w[4 * i] | ((uint32_t)w[4 * i + 1] << 8) | ((uint32_t)w[4 * i + 2] << 16) |
+                ((uint32_t)w[4 * i + 3] << 24);
+}
+
+static void t0_table(uint32_t T0[256]) {
+    sbox_init();
+    for (int x = 0; x < 256; ++x) {
+        const uint32_t s = g_sbox[x];
+        const uint32_t s2 = ((s << 1) ^ ((s & 0x80) ? 0x1b : 0)) & 0xff;
+        const uint32_t s3 = s2 ^ s;
+        T0[x] = s2 | (s << 8) | (s << 16) | (s3 << 24);
+    }
+}
+
+// ---- CRT base (crt.cpp:38-101) ----
+struct Crt {
+    int k = 0;
+    std::vector<int> primes;
+    u128 P = 0;
+    std::vector<u128> coeffs;
+};
+
+static Crt crt_base(int k) {
+    if (k < 1 || k > MAXK) throw DataError("crt_base: k must be in [1, 16]");
+    Crt b;
+    b.k = k;
+    b.P = 1;
+    for (int i = 0; i < k; ++i) {
+        b.primes.push_back(kPrimes[i]);
+        b.P *= (u128)kPrimes[i];
+    }
+    for (int p : b.primes) {
+        const u128 A = b.P / (u128)p;
+        uint64_t base = (uint64_t)(A % (u128)p), r = 1;
+        for (int e = p - 2; e > 0; e >>= 1) {
+            if (e & 1) r = r * base % (uint64_t)p;
+            base = base * base % (uint64_t)p;
+        }
+        b.coeffs.push_back(A * (u128)r);
+    }
+    return b;
+}
+
+static int64_t max_signed(const Crt& b) {
+    const u128 hi = (b.P + 1) / 2 - 1;
+    return hi > (u128)INT64_MAX ? INT64_MAX : (int64_t)hi;
+}
+static int64_t min_signed(const Crt& b) {
+    const u128 mag = b.P / 2;
+    return mag > (u128)INT64_MAX ? INT64_MIN : -(int64_t)mag;
+}
+
+// ---- mixed radix (mixed_radix.cpp) ----
+using Spec = std::vector<int>;
+
+static u128 spec_M(const Spec& s) {
+    u128 M = 1;
+    for (int r : s) M *= (u128)r;
+    return M;
+}
+
+// round-half-away(M*y/P) = floor((2My + P) / (2P)) with a 256-bit numerator
+static u128 round_scaled(u128 M, u128 y, u128 P) {
+    const u128 a = 2 * M;
+    const u128 al = (uint64_t)a, ah = a >> 64, bl = (uint64_t)y, bh = y >> 64;
+    const u128 ll = al * bl, lh = al * bh, hl = ah * bl, hh = ah * bh;
+    u128 lo = ll + (lh << 64);
+    u128 carry = lo < ll;
+    const u128 lo2 = lo + (hl << 64);
+    carry += lo2 < lo;
+    lo = lo2;
+    u128 hi = hh + (lh >> 64) + (hl >> 64) + carry;
+    const u128 lo3 = lo + P;
+    hi += lo3 < lo;
+    lo = lo3;
+    const u128 d = 2 * P;
+    u128 q = 0, rem = 0;
+    for (int i = 255; i >= 0; --i) {
+        const u128 bit = i >= 128 ? (hi >> (i - 128)) & 1 : (lo >> i) & 1;
+        rem = (rem << 1) | bit;
+        if (rem >= d) {
+            rem -= d;
+            if (i < 128) q |= (u128)1 << i;
+        }
+    }
+    return q;
+}
+
+static std::vector<std::vector<u128>> d_tables(const Crt& b, u128 M) {
+    std::vector<std::vector<u128>> d(b.k);
+    for (int i = 0; i < b.k; ++i) {
+        const u128 alpha = b.coeffs[i] % b.P;
+        for (int x = 0; x < b.primes[i]; ++x) d[i].push_back(round_scaled(M, alpha * (u128)x % b.P, b.P) % M);
+    }
+    return d;
+}
+
+static uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+static double sign_accuracy(const Crt& b, const Spec& s) {
+    const u128 M = spec_M(s);
+    const auto d = d_tables(b, M);
+    uint64_t ok = 0, total;
+    auto cls = [&](u128 x) {
+        u128 sum = 0;
+        for (int i = 0; i < b.k; ++i) sum += d[i][(int)(x % (u128)b.primes[i])];
+        sum %= M;
+        return (2 * sum >= M) == (2 * x >= b.P);
+    };
+    if (b.P <= ((u128)1 << 20)) {
+        total = (uint64_t)b.P;
+        for (u128 x = 0; x < b.P; ++x) ok += cls(x);
+    } else {
+        total = 100000;
+        for (uint64_t i = 0; i < total; ++i)
+            ok += cls((((u128)splitmix64(2 * i) << 64) | splitmix64(2 * i + 1)) % b.P);
+    }
+    return (double)ok / (double)total;
+}
+
+struct SpecSearch {
+    bool found = false;
+    u128 M = 0;
+    int t = 0, m1 = 0;
+    Spec spec;
+    void consider(int m1v, const std::vector<int>& tr, u128 bound) {
+        u128 Mv = (u128)m1v;
+        for (int x : tr) Mv *= (u128)x;
+        if (Mv <= bound) return;
+        const int tv = 1 + (int)tr.size();
+        const bool better = !found || Mv < M || (Mv == M && tv < t) || (Mv == M && tv == t && m1v > m1);
+        if (!better) return;
+        found = true;
+        M = Mv;
+        t = tv;
+        m1 = m1v;
+        spec.assign(1, m1v);
+        spec.insert(spec.end(), tr.begin(), tr.end());
+    }
+    void dfs(std::vector<int>& seq, u128 q, int last, u128 bound, u128 qmax) {
+        if (!seq.empty()) {
+            const u128 need = bound / q + 1;
+            u128 m1v = need + (need & 1);
+            if (m1v < 50) m1v = 50;
+            if (m1v <= 128) consider((int)m1v, seq, bound);
+        }
+        for (int d = std::min(last, 8); d >= 2; --d)
+            if (q * (u128)d <= qmax) {
+                seq.push_back(d);
+                dfs(seq, q * (u128)d, d, bound, qmax);
+                seq.pop_back();
+            }
+    }
+};
+
+// choose_mixed_radix (mixed_radix.cpp:153-189)
+static Spec choose_spec(const Crt& b, double target) {
+    const u128 bound = (u128)b.k * b.P / 2;
+    SpecSearch s;
+    for (int m1 = 2; m1 <= 128; m1 += 2) s.consider(m1, {}, bound);
+    std::vector<int> seq;
+    s.dfs(seq, 1, 8, bound, bound / 25 + 1);
+    if (!s.found) throw DataError("no mixed-radix spec reaches the required M");
+    Spec cur = s.spec;
+    if (target >= 1.0) return cur;
+    if (sign_accuracy(b, cur) < target) return cur;
+    Spec last = cur;
+    while (true) {
+        Spec next = cur;
+        if (next.size() > 1) next.pop_back();
+        else if (next[0] > 2) next[0] -= 2;
+        else return last;
+        if (sign_accuracy(b, next) < target) return last;
+        last = next;
+        cur = next;
+    }
+}
+
+struct Pos {
+    int m, b_mod, carry_in, carry_out;
+};
+struct SignCtx {
+    Spec spec;
+    std::vector<Pos> positions;  // make_sign_plan (gadgets.cpp:5-28)
+    int msd_carry = 0;
+    std::vector<std::vector<std::vector<int>>> digits;  // [i][j][x]
+};
+
+static SignCtx make_sign(const Crt& b, const Spec& spec) {
+    if (spec.empty() || spec[0] % 2) throw DataError("mixed-radix m_1 must be even");
+    for (int r : spec)
+        if (r < 2 || r > 128) throw DataError("mixed-radix digit modulus out of range");
+    SignCtx s;
+    s.spec = spec;
+    const int t = (int)spec.size();
+    if (b.k > 1 && t > 1) {
+        int carry = 0;
+        for (int j = t - 1; j >= 1; --j) {
+            Pos p;
+            p.m = spec[j];
+            p.carry_in = carry;
+            p.b_mod = b.k * (p.m - 1) + (carry ? carry - 1 : 0) + 1;
+            if (p.b_mod > MAXMOD) throw DataError("mixed-radix digit sum exceeds the modulus limit");
+            const int maxcarry = (p.b_mod - 1) / p.m;
+            p.carry_out = maxcarry > 0 ? maxcarry + 1 : 0;
+            carry = p.carry_out;
+            s.positions.push_back(p);
+        }
+        s.msd_carry = carry;
+    }
+    const auto d = d_tables(b, spec_M(spec));
+    s.digits.assign(b.k, std::vector<std::vector<int>>(t));
+    for (int i = 0; i < b.k; ++i)
+        for (int x = 0; x < b.primes[i]; ++x) {
+            u128 v = d[i][x];
+            for (int j = t - 1; j >= 0; --j) {
+                s.digits[i][j].resize(b.primes[i]);
+                s.digits[i][j][x] = (int)(v % (u128)spec[j]);
+                v /= (u128)spec[j];
+            }
+        }
+    return s;
+}
+
+// ======================================================= activation tape
+
+struct Tape {
+    std::vector<TapeOp> ops;
+    std::vector<uint8_t> phi;
+    uint64_t cts = 0, gates = 0, wires = 0;
+    int nslots = 0;
+    std::set<int> moduli;
+};
+
+// Records the gadget DAG in reference order (CountCtx semantics,
+// gadgets.hpp:82-98): gate ids, fresh wires and ciphertext positions advance
+// exactly as in the reference.
+class Recorder {
+  public:
+    struct ROp {
+        int kind;
+        int a = -1, b = -1, out = -1;
+        int pm = 0, qm = 0, cst = 0;
+        uint64_t gate = 0, wire = 0, ct = 0;
+        uint32_t phi = 0;
+    };
+    std::vector<int> vmod;  // modulus per value; values 0..k-1 are the inputs
+    std::vector<int> producer;
+    std::vector<ROp> ops;
+    std::vector<uint8_t> phi;
+    uint64_t cts = 0, gates = 0, wires = 0;
+    std::set<int> moduli;
+    int k;
+
+    explicit Recorder(const Crt& b) : k(b.k) {
+        for (int p : b.primes) {
+            vmod.push_back(p);
+            producer.push_back(-1);
+        }
+    }
+    int newval(int m, int op) {
+        vmod.push_back(m);
+        producer.push_back(op);
+        return (int)vmod.size() - 1;
+    }
+    uint32_t addphi(const std::vector<int>& f, int q) {
+        const uint32_t off = (uint32_t)phi.size();
+        for (int v : f) phi.push_back((uint8_t)(v % q));
+        return off;
+    }
+    int proj(int in, int q, const std::vector<int>& f) {  // t_proj
+        const int p = vmod[in];
+        ROp o;
+        o.kind = OP_PROJ;
+        o.a = in;
+        o.pm = p;
+        o.qm = q;
+        o.gate = gates++;
+        o.ct = cts;
+        cts += (uint64_t)p;
+        moduli.insert(p);
+        o.wire = wires++;
+        moduli.insert(q);
+        o.phi = addphi(f, q);
+        ops.push_back(o);
+        return ops.back().out = newval(q, (int)ops.size() - 1);
+    }
+    int grr(int in, int q, const std::vector<int>& f) {  // t_proj_grr
+        const int p = vmod[in];
+        ROp o;
+        o.kind = OP_GRR;
+        o.a = in;
+        o.pm = p;
+        o.qm = q;
+        o.gate = gates++;
+        o.ct = cts;
+        cts += (uint64_t)(p - 1);
+        moduli.insert(p);
+        moduli.insert(q);
+        o.phi = addphi(f, q);
+        ops.push_back(o);
+        return ops.back().out = newval(q, (int)ops.size() - 1);
+    }
+    int half(int x, int y) {  // t_half_gate
+        const int p = vmod[x];
+        if (vmod[y] != p) throw DataError("half gate modulus mismatch");
+        ROp o;
+        o.kind = OP_HALF;
+        o.a = x;
+        o.b = y;
+        o.pm = p;
+        o.qm = p;
+        o.gate = gates++;
+        o.ct = cts;
+        cts += 2u * (uint64_t)p;
+        moduli.insert(p);
+        o.wire = wires;
+        wires += 2;
+        ops.push_back(o);
+        return ops.back().out = newval(p, (int)ops.size() - 1);
+    }
+    int mmhalf(int x, int y) {  // t_mm_half_gate
+        const int p = vmod[x], q = vmod[y];
+        if (q > p) throw DataError("mixed-modulus half gate needs q <= p");
+        int w = 0;
+        while ((1 << w) < p) ++w;
+        if (w == 0) w = 1;
+        if (q * w > 128) throw DataError("mixed-modulus short block exceeds 128 bits");
+        ROp o;
+        o.kind = OP_MMHALF;
+        o.a = x;
+        o.b = y;
+        o.pm = p;
+        o.qm = q;
+        o.gate = gates++;
+        o.ct = cts;
+        cts += (uint64_t)p + (uint64_t)q + 1;
+        moduli.insert(p);
+        moduli.insert(q);
+        o.wire = wires;
+        wires += 2;
+        ops.push_back(o);
+        return ops.back().out = newval(p, (int)ops.size() - 1);
+    }
+    int add(int a, int b) {  // free_add (one binary step)
+        if (vmod[a] != vmod[b]) throw DataError("free_add modulus mismatch");
+        ROp o;
+        o.kind = OP_ADD;
+        o.a = a;
+        o.b = b;
+        o.pm = o.qm = vmod[a];
+        ops.push_back(o);
+        return ops.back().out = newval(vmod[a], (int)ops.size() - 1);
+    }
+    int addconst(int a, int c) {  // add_public_constant
+        ROp o;
+        o.kind = OP_ADDCONST;
+        o.a = a;
+        o.pm = o.qm = vmod[a];
+        o.cst = c;
+        moduli.insert(vmod[a]);
+        ops.push_back(o);
+        return ops.back().out = newval(vmod[a], (int)ops.size() - 1);
+    }
+    void output(int v, int lane) {
+        ROp o;
+        o.kind = OP_OUTPUT;
+        o.a = v;
+        o.pm = o.qm = vmod[v];
+        o.cst = lane;
+        ops.push_back(o);
+    }
+};
+
+static std::vector<int> tabulate(int n, const std::function<int(int)>& f) {
+    std::vector<int> v(n);
+    for (int i = 0; i < n; ++i) v[i] = f(i);
+    return v;
+}
+
+// t_approx_sign_bit (gadgets.hpp:442-481) with t_mixed_radix_add (382-435)
+static int record_sign_bit(Recorder& r, const Crt& b, const SignCtx& s) {
+    const int k = b.k, t = (int)s.spec.size();
+    std::vector<std::vector<int>> bundles(k, std::vector<int>(t));
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < t; ++j) bundles[i][j] = r.proj(i, s.spec[j], s.digits[i][j]);
+    int msd;
+    if (k == 1) {
+        msd = bundles[0][0];
+    } else {
+        int carry = -1;
+        for (size_t pi = 0; pi < s.positions.size(); ++pi) {
+            const Pos& pos = s.positions[pi];
+            const int j = t - 1 - (int)pi;
+            auto lift = [&](int m) { return tabulate(m, [](int a) { return a; }); };
+            int sum = -1;
+            for (int si = 0; si < k; ++si) {
+                const int term = r.proj(bundles[si][j], pos.b_mod, lift(s.spec[j]));
+                sum = sum < 0 ? term : r.add(sum, term);
+            }
+            if (pos.carry_in) {
+                const int term = r.proj(carry, pos.b_mod, lift(pos.carry_in));
+                sum = r.add(sum, term);
+            }
+            if (pos.carry_out) {
+                const int m = pos.m;
+                carry = r.proj(sum, pos.carry_out, tabulate(pos.b_mod, [m](int a) { return a / m; }));
+            } else {
+                carry = -1;
+            }
+        }
+        const int m1 = s.spec[0];
+        msd = bundles[0][0];
+        for (int si = 1; si < k; ++si) msd = r.add(msd, bundles[si][0]);
+        if (s.msd_carry) {
+            const int term = r.proj(carry, m1, tabulate(s.msd_carry, [m1](int c) { return c % m1; }));
+            msd = r.add(msd, term);
+        }
+    }
+    const int m1 = s.spec[0], half = m1 / 2;
+    const int negative = r.grr(msd, 2, tabulate(m1, [half](int v) { return v >= half ? 1 : 0; }));
+    const int nonneg = r.addconst(negative, 1);
+    int count = -1;
+    for (int i = 0; i < k; ++i) {
+        const int nz = r.proj(i, k + 1, tabulate(b.primes[i], [](int a) { return a != 0 ? 1 : 0; }));
+        count = count < 0 ? nz : r.add(count, nz);
+    }
+    const int nonzero = r.proj(count, 2, tabulate(k + 1, [](int c) { return c >= 1 ? 1 : 0; }));
+    return r.half(nonneg, nonzero);
+}
+
+// Depth-first schedule from the outputs + linear-scan slot assignment.
+static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
+    Recorder r(b);
+    const int bit = record_sign_bit(r, b, s);
+    for (int i = 0; i < b.k; ++i) {
+        if (kind == DASH_LAYER_RELU) {
+            r.output(r.mmhalf(i, bit), i);
+        } else {
+            const int p = b.primes[i];
+            r.output(r.proj(bit, p, tabulate(2, [p](int v) { return v != 0 ? 1 : p - 1; })), i);
+        }
+    }
+    const int nops = (int)r.ops.size();
+    std::vector<int> order;
+    std::vector<char> done(nops, 0);
+    std::function<void(int)> dfs = [&](int v) {
+        if (v < 0 || v < b.k) return;
+        const int op = r.producer[v];
+        if (done[op]) return;
+        dfs(r.ops[op].a);
+        dfs(r.ops[op].b);
+        done[op] = 1;
+        order.push_back(op);
+    };
+    for (int i = 0; i < nops; ++i)
+        if (r.ops[i].kind == OP_OUTPUT) {
+            dfs(r.ops[i].a);
+            done[i] = 1;
+            order.push_back(i);
+        }
+    for (int i = 0; i < nops; ++i)
+        if (!done[i]) throw std::logic_error("tape: unreachable gadget");
+    std::vector<int> last(r.vmod.size(), -1);
+    for (int t = 0; t < (int)order.size(); ++t) {
+        const auto& o = r.ops[order[t]];
+        if (o.a >= 0) last[o.a] = t;
+        if (o.b >= 0) last[o.b] = t;
+    }
+    std::vector<int> slot(r.vmod.size(), -1);
+    std::vector<int> freelist;
+    int nslots = 0;
+    Tape tp;
+    for (int t = 0; t < (int)order.size(); ++t) {
+        const auto& o = r.ops[order[t]];
+        TapeOp d;
+        std::memset(&d, 0, sizeof d);
+        d.kind = (uint8_t)o.kind;
+        auto enc = [&](int v) -> uint8_t {
+            if (v < 0) return 0;
+            if (v < b.k) return (uint8_t)(IN_LANE + v);
+            if (slot[v] < 0) throw std::logic_error("tape: operand without slot");
+            return (uint8_t)slot[v];
+        };
+        d.a = enc(o.a);
+        d.b = enc(o.b);
+        d.pm = (uint16_t)o.pm;
+        d.qm = (uint16_t)o.qm;
+        d.cst = (uint16_t)o.cst;
+        d.gate_off = (uint32_t)o.gate;
+        d.wire_off = (uint32_t)o.wire;
+        d.ct_off = (uint32_t)o.ct;
+        d.phi_off = o.phi;
+        for (int v : {o.a, o.b})
+            if (v >= b.k && last[v] == t && slot[v] >= 0) {
+                freelist.push_back(slot[v]);
+                slot[v] = -1;
+            }
+        if (o.out >= 0) {
+            int sidx;
+            if (!freelist.empty()) {
+                sidx = freelist.back();
+                freelist.pop_back();
+            } else {
+                sidx = nslots++;
+            }
+            slot[o.out] = sidx;
+            d.out = (uint8_t)sidx;
+            if (last[o.out] < 0) {  // dead value
+                freelist.push_back(sidx);
+                slot[o.out] = -1;
+            }
+        }
+        tp.ops.push_back(d);
+    }
+    if (nslots > MAXSLOTS) throw DataError("activation gadget needs too many label slots");
+    tp.nslots = nslots;
+    tp.phi = r.phi;
+    if (tp.phi.empty()) tp.phi.push_back(0);
+    tp.cts = r.cts;
+    tp.gates = r.gates;
+    tp.wires = r.wires;
+    tp.moduli = r.moduli;
+    return tp;
+}
+
+// ============================================================== circuits
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { dev::release(p); }
+    void ensure(size_t bytes) {
+        if (bytes <= n && p) return;
+        dev::release(p);
+        p = dev::alloc(bytes);
+        n = bytes;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+static void* g_stream = nullptr;
+
+struct HLayer {
+    int kind = 0;
+    bool priv = false;
+    uint32_t in_dim = 0, out_dim = 0, in_ch = 0, out_ch = 0, filter = 0, stride = 0;
+    std::vector<int64_t> w, bias;
+    std::vector<uint32_t> in_shape, out_shape;
+    uint64_t E_in = 0, E_out = 0;
+    // layout (per inference)
+    uint64_t gate_base = 0, wire_base = 0, ct_base = 0, cts = 0, gates = 0, wires = 0;
+    // public / private linear: per-lane device residues
+    std::vector<std::shared_ptr<DevBuf>> wres, zt, bres;
+    std::vector<uint64_t> lane_ct_off, lane_gate_off, lane_wire_off;  // private
+    uint32_t K = 0;  // window
+    // activation
+    std::shared_ptr<Tape> tape;
+    std::shared_ptr<DevBuf> tape_d, phi_d;
+    bool linear() const { return kind == DASH_LAYER_DENSE || kind == DASH_LAYER_CONV2D; }
+    uint64_t weight_count() const {
+        if (kind == DASH_LAYER_DENSE) return (uint64_t)in_dim * out_dim;
+        if (kind == DASH_LAYER_CONV2D) return (uint64_t)out_ch * in_ch * filter * filter;
+        return 0;
+    }
+    uint64_t bias_count() const {
+        if (kind == DASH_LAYER_DENSE) return out_dim;
+        if (kind == DASH_LAYER_CONV2D) return out_ch;
+        return 0;
+    }
+};
+
+struct Network;
+
+}  // namespace dashgpu
+
+struct dashgpu_circuit {
+    int k = 8;
+    std::vector<uint32_t> input_shape;
+    double sign_target = 1.0, alpha = 1.0;
+    std::vector<dashgpu::HLayer> layers;
+    dashgpu::Crt base;
+    bool needs_sign = false;
+    dashgpu::SignCtx sign;
+    std::shared_ptr<dashgpu::Tape> relu_tape, sign_tape;
+    uint64_t n_in = 0, n_out = 0;
+    uint64_t total_cts = 0, total_gates = 0, total_wires = 0, wire0 = 0;
+    std::set<int> moduli;
+    uint64_t relu_elements = 0, linear_macs = 0;
+    std::vector<dash_layer_desc> desc_layers;  // for dashgpu_circuit_desc_view
+    std::unique_ptr<dashgpu::Network> workspace;  // dashgpu_infer cache
+    std::mutex mu;
+    ~dashgpu_circuit();
+};
+
+namespace dashgpu {
+
+static void check_constants();
+
+static uint64_t shape_size(const std::vector<uint32_t>& s) {
+    uint64_t n = 1;
+    for (auto x : s) n *= x;
+    return n;
+}
+
+static uint32_t conv_extent(uint32_t in, uint32_t f, uint32_t s) {
+    if (f == 0 || s == 0 || f > in) throw DataError("convolution filter does not fit the input");
+    return (in - f) / s + 1;
+}
+
+// layer_out_shape (layer.cpp:320-344)
+static std::vector<uint32_t> out_shape_of(const HLayer& l, const std::vector<uint32_t>& in) {
+    switch (l.kind) {
+        case DASH_LAYER_DENSE:
+            if (in.size() != 1 || in[0] != l.in_dim) throw DataError("dense layer input shape mismatch");
+            return {l.out_dim};
+        case DASH_LAYER_CONV2D:
+            if (in.size() != 3 || in[0] != l.in_ch) throw DataError("conv layer input shape mismatch");
+            return {l.out_ch, conv_extent(in[1], l.filter, l.stride), conv_extent(in[2], l.filter, l.stride)};
+        case DASH_LAYER_RELU:
+        case DASH_LAYER_SIGNACT:
+            return in;
+        case DASH_LAYER_FLATTEN:
+            return {(uint32_t)shape_size(in)};
+    }
+    throw DataError("unknown layer kind");
+}
+
+static std::shared_ptr<DevBuf> upload(const void* data, size_t bytes) {
+    auto b = std::make_shared<DevBuf>();
+    b->ensure(bytes ? bytes : 16);
+    dev::h2d(b->p, data, bytes, g_stream);
+    return b;
+}
+
+static int64_t resid(int64_t w, int p) { return ((w % p) + p) % p; }
+
+// validate_circuit + circuit_layout + per-layer device preparation
+static void prepare_circuit(dashgpu_circuit& c) {
+    check_constants();
+    c.base = crt_base(c.k);
+    if (c.input_shape.empty() || c.input_shape.size() > 8 || shape_size(c.input_shape) == 0)
+        throw DataError("circuit has an empty input shape");
+    c.n_in = shape_size(c.input_shape);
+    std::vector<uint32_t> shape = c.input_shape;
+    c.needs_sign = false;
+    for (auto& l : c.layers) {
+        if (l.kind < 1 || l.kind > 5) throw DataError("bad layer kind");
+        l.in_shape = shape;
+        l.out_shape = out_shape_of(l, shape);
+        l.E_in = shape_size(l.in_shape);
+        l.E_out = shape_size(l.out_shape);
+        if (l.linear()) {
+            if (l.w.size() != l.weight_count()) throw DataError("circuit must be quantized before garbling");
+            if (!l.bias.empty() && l.bias.size() != l.bias_count()) throw DataError("quantized bias count mismatch");
+        }
+        if (l.kind == DASH_LAYER_RELU || l.kind == DASH_LAYER_SIGNACT) c.needs_sign = true;
+        shape = l.out_shape;
+    }
+    c.n_out = shape_size(shape);
+    if (c.n_in > (1u << 26) || c.n_out > (1u << 26)) throw DataError("tensor too large");
+    if (c.needs_sign) {
+        c.sign = make_sign(c.base, choose_spec(c.base, c.sign_target));
+        c.relu_tape = std::make_shared<Tape>(build_tape(DASH_LAYER_RELU, c.base, c.sign));
+        c.sign_tape = std::make_shared<Tape>(build_tape(DASH_LAYER_SIGNACT, c.base, c.sign));
+    }
+    const int k = c.k;
+    c.wire0 = (uint64_t)k * (1 + c.n_in);
+    uint64_t g = 0, w = c.wire0, ct = 0;
+    c.moduli.clear();
+    for (int p : c.base.primes) c.moduli.insert(p);
+    c.relu_elements = 0;
+    c.linear_macs = 0;
+    for (auto& l : c.layers) {
+        l.gate_base = g;
+        l.wire_base = w;
+        l.ct_base = ct;
+        l.cts = l.gates = l.wires = 0;
+        l.wres.clear();
+        l.zt.clear();
+        l.bres.clear();
+        l.lane_ct_off.clear();
+        l.lane_gate_off.clear();
+        l.lane_wire_off.clear();
+        if (l.linear()) {
+            const bool dense = l.kind == DASH_LAYER_DENSE;
+            l.K = dense ? l.in_dim : l.in_ch * l.filter * l.filter;
+            const uint64_t M = l.E_out;
+            const uint64_t nrow = dense ? M : l.out_ch;
+            for (int i = 0; i < k; ++i) {
+                const int p = c.base.primes[i];
+                if (!l.priv) {
+                    std::vector<uint8_t> wr(l.w.size()), zt(nrow), br(nrow);
+                    for (uint64_t row = 0; row < nrow; ++row) {
+                        uint32_t z = 0;
+                        for (uint32_t j = 0; j < l.K; ++j) {
+                            const int64_t wv = resid(l.w[row * l.K + j], p);
+                            if (wv == 0) ++z;
+                            if (dense) wr[(uint64_t)j * M + row] = (uint8_t)wv;
+                            else wr[row * l.K + j] = (uint8_t)wv;
+                        }
+                        zt[row] = (uint8_t)(z % (uint32_t)p);
+                        br[row] = (uint8_t)resid(l.bias.empty() ? 0 : l.bias[row], p);
+                    }
+                    l.wres.push_back(upload(wr.data(), wr.size()));
+                    l.zt.push_back(upload(zt.data(), zt.size()));
+                    l.bres.push_back(upload(br.data(), br.size()));
+                } else {
+                    std::vector<uint8_t> wr(l.w.size()), br(nrow);
+                    for (uint64_t row = 0; row < nrow; ++row) {
+                        for (uint32_t j = 0; j < l.K; ++j) wr[row * l.K + j] = (uint8_t)resid(l.w[row * l.K + j], p);
+                        br[row] = (uint8_t)resid(l.bias.empty() ? 0 : l.bias[row], p);
+                    }
+                    l.wres.push_back(upload(wr.data(), wr.size()));
+                    l.bres.push_back(upload(br.data(), br.size()));
+                    // count_layer order (layer.cpp:393-404): lane after lane
+                    l.lane_ct_off.push_back(l.cts);
+                    l.lane_gate_off.push_back(l.gates);
+                    l.lane_wire_off.push_back(l.wires);
+                    l.cts += (uint64_t)l.K * p * M;
+                    l.gates += (uint64_t)l.K * M;
+                    l.wires += (uint64_t)l.K * M;
+                }
+            }
+        } else if (l.kind == DASH_LAYER_RELU || l.kind == DASH_LAYER_SIGNACT) {
+            l.tape = l.kind == DASH_LAYER_RELU ? c.relu_tape : c.sign_tape;
+            l.tape_d = upload(l.tape->ops.data(), l.tape->ops.size() * sizeof(TapeOp));
+            l.phi_d = upload(l.tape->phi.data(), l.tape->phi.size());
+            l.cts = l.tape->cts * l.E_out;
+            l.gates = l.tape->gates * l.E_out;
+            l.wires = l.tape->wires * l.E_out;
+            for (int m : l.tape->moduli) c.moduli.insert(m);
+            c.relu_elements += l.E_out;
+        }
+        g += l.gates;
+        w += l.wires;
+        ct += l.cts;
+    }
+    c.linear_macs = 0;  // digit multiply-accumulates of the public linear lanes
+    for (auto& l : c.layers)
+        if (l.linear() && !l.priv) {
+            uint64_t sum_n = 0;
+            for (int p : c.base.primes) sum_n += (uint64_t)n_digits_host(p);
+            c.linear_macs += (uint64_t)l.K * l.E_out * sum_n;
+        }
+    c.total_cts = ct;
+    c.total_gates = g;
+    c.total_wires = w - c.wire0;
+    dev::sync(g_stream);
+}
+
+// ================================================================ network
+
+struct Lanes {
+    std::vector<std::unique_ptr<DevBuf>> lane;  // [k] of [B][nw][E] u32
+    uint64_t E = 0;
+    void ensure(const Crt& b, uint32_t B, uint64_t E_) {
+        E = E_;
+        lane.resize(b.k);
+        for (int i = 0; i < b.k; ++i) {
+            if (!lane[i]) lane[i] = std::make_unique<DevBuf>();
+            const uint64_t nw = (n_digits_host(b.primes[i]) + 3) / 4;
+            lane[i]->ensure((size_t)B * nw * E * 4);
+        }
+    }
+};
+
+struct Network {
+    dashgpu_circuit* c = nullptr;
+    uint32_t B = 0, cap = 0;
+    std::vector<uint8_t> seeds;
+    DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err;
+    Lanes base;  // encoding info: input base labels
+    Lanes ping, pong;    // garbling planes
+    Lanes eping, epong;  // evaluation planes
+    uint64_t mult_stride = 0;
+    uint32_t sum_p = 0;
+};
+
+struct Bundle {
+    Network* net = nullptr;
+    uint32_t B = 0;
+    bool output = false;
+    Lanes lanes;
+};
+
+static void make_lane_ptrs(const Lanes& L, int k, const uint32_t** out) {
+    for (int i = 0; i < k; ++i) out[i] = L.lane[i]->as<uint32_t>();
+}
+
+static void fill_primes(const Crt& b, uint16_t* out) {
+    for (int i = 0; i < b.k; ++i) out[i] = (uint16_t)b.primes[i];
+}
+
+// Runs one layer over B inferences.  garbler: base labels; else active.
+static void run_layer(Network& n, const HLayer& l, bool garbler, Lanes& in, Lanes& out) {
+    dashgpu_circuit& c = *n.c;
+    const int k = c.k;
+    if (l.kind == DASH_LAYER_FLATTEN) {
+        std::swap(in, out);  // metadata-only reshape: the planes are already flat
+        out.E = l.E_out;
+        return;
+    }
+    out.ensure(c.base, n.B, l.E_out);
+    if (l.linear() && !l.priv) {
+        for (int i = 0; i < k; ++i) {
+            LinParams L;
+            std::memset(&L, 0, sizeof L);
+            L.conv = l.kind == DASH_LAYER_CONV2D;
+            L.K = l.K;
+            L.M = (uint32_t)l.E_out;
+            L.E_in = (uint32_t)l.E_in;
+            if (L.conv) {
+                L.in_ch = l.in_ch;
+                L.H = l.in_shape[1];
+                L.W = l.in_shape[2];
+                L.f = l.filter;
+                L.stride = l.stride;
+                L.OH = l.out_shape[1];
+                L.OW = l.out_shape[2];
+            }
+            L.wres = l.wres[i]->as<uint8_t>();
+            L.zt = l.zt[i]->as<uint8_t>();
+            L.bres = l.bres[i]->as<uint8_t>();
+            L.in = in.lane[i]->as<uint32_t>();
+            L.out = out.lane[i]->as<uint32_t>();
+            L.zero = n.zero.as<uint32_t>() + (uint64_t)i * LABW;
+            L.R = n.Rb.as<uint32_t>() + (uint64_t)i * LABW;
+            L.p = (uint32_t)c.base.primes[i];
+            L.nw = (uint32_t)(n_digits_host(L.p) + 3) / 4;
+            L.B = n.B;
+            L.zstride = (uint32_t)(k * LABW);  // zero / R rows are [B][k][LABW]
+            L.garbler = garbler;
+            launch_linear(L, g_stream);
+        }
+        return;
+    }
+    if (l.linear()) {
+        for (int i = 0; i < k; ++i) {
+            PrivParams P;
+            std::memset(&P, 0, sizeof P);
+            P.conv = l.kind == DASH_LAYER_CONV2D;
+            P.win = l.K;
+            P.M = (uint32_t)l.E_out;
+            P.E_in = (uint32_t)l.E_in;
+            if (P.conv) {
+                P.in_ch = l.in_ch;
+                P.H = l.in_shape[1];
+                P.W = l.in_shape[2];
+                P.f = l.filter;
+                P.stride = l.stride;
+                P.OH = l.out_shape[1];
+                P.OW = l.out_shape[2];
+            }
+            P.wres = l.wres[i]->as<uint8_t>();
+            P.bres = l.bres[i]->as<uint8_t>();
+            P.in = in.lane[i]->as<uint32_t>();
+            P.out = out.lane[i]->as<uint32_t>();
+            P.p = (uint32_t)c.base.primes[i];
+            P.B = n.B;
+            P.gate_base = l.gate_base + l.lane_gate_off[i];
+            P.wire_base = l.wire_base + l.lane_wire_off[i];
+            P.blob = n.blob.as<U4>() + l.ct_base + l.lane_ct_off[i];
+            P.blob_stride = c.total_cts;
+            P.rk = n.rk.as<uint32_t>();
+            P.mult = n.mult.as<uint32_t>();
+            P.mult_stride = n.mult_stride;
+            P.garbler = garbler;
+            launch_private(P, g_stream);
+        }
+        return;
+    }
+    ActParams P;
+    std::memset(&P, 0, sizeof P);
+    P.tape = l.tape_d->as<TapeOp>();
+    P.n_ops = (int)l.tape->ops.size();
+    P.phi = l.phi_d->as<uint8_t>();
+    P.k = k;
+    P.E = (uint32_t)l.E_out;
+    P.B = n.B;
+    P.gate_base = l.gate_base;
+    P.wire_base = l.wire_base;
+    P.uc_cts = l.tape->cts;
+    P.uc_gates = l.tape->gates;
+    P.uc_wires = l.tape->wires;
+    P.blob = n.blob.as<U4>() + l.ct_base;
+    P.blob_stride = c.total_cts;
+    for (int i = 0; i < k; ++i) {
+        P.in[i] = in.lane[i]->as<uint32_t>();
+        P.out[i] = out.lane[i]->as<uint32_t>();
+        P.lane_mod[i] = (uint16_t)c.base.primes[i];
+    }
+    P.rk = n.rk.as<uint32_t>();
+    P.mult = n.mult.as<uint32_t>();
+    P.mult_stride = n.mult_stride;
+    launch_act(P, garbler, l.tape->nslots, g_stream);
+}
+
+static void network_reserve(Network& n, uint32_t B) {
+    dashgpu_circuit& c = *n.c;
+    const int k = c.k;
+    if (B <= n.cap && n.cap) {
+        n.B = B;
+        return;
+    }
+    n.cap = B;
+    n.B = B;
+    n.mult_stride = (uint64_t)(MAXMOD - 1) * 128 * NWMAX;
+    n.seeds_d.ensure((size_t)B * 16);
+    n.rk.ensure((size_t)B * 44 * 4);
+    n.mult.ensure((size_t)B * n.mult_stride * 4);
+    n.zero.ensure((size_t)B * k * LABW * 4);
+    n.Rb.ensure((size_t)B * k * LABW * 4);
+    n.commit.ensure((size_t)B * 16);
+    n.blob.ensure((size_t)B * std::max<uint64_t>(c.total_cts, 1) * 16);
+    n.sum_p = 0;
+    for (int p : c.base.primes) n.sum_p += (uint32_t)p;
+    n.dec.ensure((size_t)B * c.n_out * n.sum_p * 16);
+    n.vals.ensure((size_t)B * std::max(c.n_in, c.n_out) * 8);
+    n.resid.ensure((size_t)B * c.n_out * k);
+    n.err.ensure(16);
+    n.base.ensure(c.base, B, c.n_in);
+}
+
+// garble (garble.cpp:134-240), batched: inference b uses seeds[b]
+static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
+    dashgpu_circuit& c = *n.c;
+    const int k = c.k;
+    network_reserve(n, B);
+    n.seeds.assign(16 * (size_t)B, 0);
+    std::vector<uint32_t> rk((size_t)B * 44);
+    if (seeds_on_device) {
+        dev::d2h(n.seeds.data(), seeds, 16 * (size_t)B, g_stream);
+        dev::sync(g_stream);
+    } else {
+        std::memcpy(n.seeds.data(), seeds, 16 * (size_t)B);
+    }
+    for (uint32_t b = 0; b < B; ++b) aes_expand_host(n.seeds.data() + 16 * (size_t)b, rk.data() + 44 * (size_t)b);
+    dev::h2d(n.rk.p, rk.data(), rk.size() * 4, g_stream);
+    dev::h2d(n.seeds_d.p, n.seeds.data(), n.seeds.size(), g_stream);
+    // zero / Rb rows are addressed per lane with stride LABW between inferences
+    // in linear_thread; store them lane-major: [k][B][LABW]
+    SetupParams S;
+    std::memset(&S, 0, sizeof S);
+    S.B = B;
+    S.k = k;
+    fill_primes(c.base, S.primes);
+    S.nslot = 0;
+    for (int m : c.moduli) S.slot_mod[S.nslot++] = (uint16_t)m;
+    S.rk = n.rk.as<uint32_t>();
+    S.seeds = n.seeds_d.as<uint8_t>();
+    S.mult = n.mult.as<uint32_t>();
+    S.mult_stride = n.mult_stride;
+    S.n_in = (uint32_t)c.n_in;
+    for (int i = 0; i < k; ++i) S.base_planes[i] = n.base.lane[i]->as<uint32_t>();
+    S.zero = n.zero.as<uint32_t>();
+    S.Rb = n.Rb.as<uint32_t>();
+    S.commit = n.commit.as<U4>();
+    launch_setup(S, g_stream);
+    // copy the input base planes into the working planes and run the layers
+    n.ping.ensure(c.base, B, c.n_in);
+    for (int i = 0; i < k; ++i)
+        dev::d2d(n.ping.lane[i]->p, n.base.lane[i]->p,
+                 (size_t)B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_in * 4, g_stream);
+    Lanes* cur = &n.ping;
+    Lanes* nxt = &n.pong;
+    for (const auto& l : c.layers) {
+        run_layer(n, l, true, *cur, *nxt);
+        std::swap(cur, nxt);
+    }
+    // decoding tables from the final base labels
+    DecodeParams D;
+    std::memset(&D, 0, sizeof D);
+    D.B = B;
+    D.n_out = (uint32_t)c.n_out;
+    D.k = k;
+    fill_primes(c.base, D.primes);
+    D.poff[0] = 0;
+    for (int i = 0; i < k; ++i) D.poff[i + 1] = (uint16_t)(D.poff[i] + c.base.primes[i]);
+    make_lane_ptrs(*cur, k, D.lanes);
+    D.table = n.dec.as<U4>();
+    D.mult = n.mult.as<uint32_t>();
+    D.mult_stride = n.mult_stride;
+    launch_dectable(D, g_stream);
+}
+
+static void encode_into(Network& n, const int64_t* values, bool on_device, Bundle& out) {
+    dashgpu_circuit& c = *n.c;
+    const int k = c.k;
+    const int64_t* vd = values;
+    if (!on_device) {
+        dev::h2d(n.vals.p, values, (size_t)n.B * c.n_in * 8, g_stream);
+        vd = n.vals.as<int64_t>();
+    }
+    out.net = &n;
+    out.B = n.B;
+    out.output = false;
+    out.lanes.ensure(c.base, n.B, c.n_in);
+    dev::memset0(n.err.p, 4, g_stream);
+    EncodeParams P;
+    std::memset(&P, 0, sizeof P);
+    P.B = n.B;
+    P.n_in = (uint32_t)c.n_in;
+    P.k = k;
+    fill_primes(c.base, P.primes);
+    P.values = vd;
+    for (int i = 0; i < k; ++i) {
+        P.base[i] = n.base.lane[i]->as<uint32_t>();
+        P.out[i] = out.lanes.lane[i]->as<uint32_t>();
+    }
+    P.mult = n.mult.as<uint32_t>();
+    P.mult_stride = n.mult_stride;
+    const u128 half_up = (c.base.P + 1) / 2, half_dn = c.base.P / 2;
+    P.half_up_lo = (uint64_t)half_up;
+    P.half_up_hi = (uint64_t)(half_up >> 64);
+    P.half_dn_lo = (uint64_t)half_dn;
+    P.half_dn_hi = (uint64_t)(half_dn >> 64);
+    P.err = n.err.as<int>();
+    launch_encode(P, g_stream);
+    int err = 0;
+    dev::d2h(&err, n.err.p, 4, g_stream);
+    dev::sync(g_stream);
+    if (err) throw DataError("encode_signed: value outside the representable range");
+}
+
+// evaluate (garble.cpp:265-312)
+static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
+    dashgpu_circuit& c = *n.c;
+    const int k = c.k;
+    if (in.B != n.B || in.output) throw DataError("garbled input bundle does not match the network");
+    n.eping.ensure(c.base, n.B, c.n_in);
+    for (int i = 0; i < k; ++i)
+        dev::d2d(n.eping.lane[i]->p, in.lanes.lane[i]->p,
+                 (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_in * 4, g_stream);
+    Lanes* cur = &n.eping;
+    Lanes* nxt = &n.epong;
+    for (const auto& l : c.layers) {
+        run_layer(n, l, false, *cur, *nxt);
+        std::swap(cur, nxt);
+    }
+    out.net = &n;
+    out.B = n.B;
+    out.output = true;
+    out.lanes.ensure(c.base, n.B, c.n_out);
+    for (int i = 0; i < k; ++i)
+        dev::d2d(out.lanes.lane[i]->p, cur->lane[i]->p,
+                 (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_out * 4, g_stream);
+}
+
+// decode_outputs (garble.cpp:314-343); CRT reconstruction on the host
+static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool values_on_device) {
+    dashgpu_circuit& c = *n.c;
+    const int k = c.k;
+    if (!outb.output || outb.B != n.B) throw DataError("output lane count mismatch");
+    DecodeParams D;
+    std::memset(&D, 0, sizeof D);
+    D.B = n.B;
+    D.n_out = (uint32_t)c.n_out;
+    D.k = k;
+    fill_primes(c.base, D.primes);
+    for (int i = 0; i < k; ++i) D.poff[i + 1] = (uint16_t)(D.poff[i] + c.base.primes[i]);
+    make_lane_ptrs(outb.lanes, k, D.lanes);
+    D.table = n.dec.as<U4>();
+    D.residues = n.resid.as<uint8_t>();
+    D.err = n.err.as<int>();
+    dev::memset0(n.err.p, 4, g_stream);
+    launch_decode(D, g_stream);
+    std::vector<uint8_t> res((size_t)n.B * c.n_out * k);
+    int err = 0;
+    dev::d2h(res.data(), n.resid.p, res.size(), g_stream);
+    dev::d2h(&err, n.err.p, 4, g_stream);
+    dev::sync(g_stream);
+    if (err) throw AuthError("output label not present in the decoding table");
+    std::vector<int64_t> host;
+    int64_t* dst = values;
+    if (values_on_device) {
+        host.resize((size_t)n.B * c.n_out);
+        dst = host.data();
+    }
+    for (uint64_t e = 0; e < (uint64_t)n.B * c.n_out; ++e) {
+        u128 acc = 0;
+        for (int i = 0; i < k; ++i) acc += c.base.coeffs[i] % c.base.P * res[e * k + i] % c.base.P;
+        acc %= c.base.P;
+        const u128 half_up = (c.base.P + 1) / 2;
+        int64_t v;
+        if (acc < half_up) {
+            if (acc > (u128)INT64_MAX) throw DataError("decode_signed: value exceeds 64-bit signed range");
+            v = (int64_t)acc;
+        } else {
+            const u128 mag = c.base.P - acc;
+            if (mag > (u128)INT64_MAX) throw DataError("decode_signed: value exceeds 64-bit signed range");
+            v = -(int64_t)mag;
+        }
+        dst[e] = v;
+    }
+    if (values_on_device) dev::h2d(values, host.data(), host.size() * 8, g_stream);
+}
+
+// ============================================================ exports
+
+struct Writer {
+    std::vector<uint8_t> b;
+    void le(uint64_t v, int n) {
+        for (int i = 0; i < n; ++i) b.push_back((uint8_t)(v >> (8 * i)));
+    }
+    void u128v(u128 v) {
+        le((uint64_t)v, 8);
+        le((uint64_t)(v >> 64), 8);
+    }
+    void bytes(const void* p, size_t n) {
+        const uint8_t* q = (const uint8_t*)p;
+        b.insert(b.end(), q, q + n);
+    }
+    void header(int kind) {
+        bytes("DASH", 4);
+        le(1, 2);
+        le((uint64_t)kind, 1);
+    }
+    void shape(const std::vector<uint32_t>& s) {
+        le(s.size(), 1);
+        for (auto d : s) le(d, 4);
+    }
+};
+
+// compress of a byte-digit row (label.cpp:208-219), host side for exports
+static u128 host_compress(const uint32_t* words, int m) {
+    const int n = n_digits_host(m);
+    u128 acc = 0;
+    const bool pow2 = (m & (m - 1)) == 0;
+    int e = 0;
+    while ((1 << e) < m) ++e;
+    for (int i = n - 1; i >= 0; --i) {
+        const uint32_t d = (words[i / 4] >> (8 * (i % 4))) & 0xff;
+        acc = pow2 ? ((acc << e) | d) : (acc * (u128)m + d);
+    }
+    return acc;
+}
+
+static u128 u4_to_u128(const U4& v) {
+    return ((u128)v.x[3] << 96) | ((u128)v.x[2] << 64) | ((u128)v.x[1] << 32) | v.x[0];
+}
+
+static size_t out_bytes(const std::vector<uint8_t>& v, uint8_t* buf, size_t cap, size_t* len) {
+    if (len) *len = v.size();
+    if (buf && cap >= v.size()) std::memcpy(buf, v.data(), v.size());
+    return v.size();
+}
+
+static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
+    const dashgpu_circuit& c = *n.c;
+    if (b >= n.B) throw DataError("inference index out of range");
+    Writer w;
+    w.header(1);
+    w.le((uint64_t)c.k, 1);
+    w.shape(c.input_shape);
+    uint64_t bits;
+    std::memcpy(&bits, &c.alpha, 8);
+    w.le(bits, 8);
+    std::memcpy(&bits, &c.sign_target, 8);
+    w.le(bits, 8);
+    const auto& radices = c.needs_sign ? c.sign.spec : Spec{};
+    w.le(radices.size(), 1);
+    for (int r : radices) w.le((uint64_t)r, 2);
+    w.le(c.layers.size(), 2);
+    for (const auto& l : c.layers) {
+        w.le((uint64_t)l.kind, 1);
+        w.le(l.priv ? 1 : 0, 1);
+        for (uint32_t v : {l.in_dim, l.out_dim, l.in_ch, l.out_ch, l.filter, l.stride}) w.le(v, 4);
+        const bool ww = l.linear() && !l.priv;
+        w.le(ww ? 1 : 0, 1);
+        if (ww) {
+            w.le(l.w.size(), 8);
+            for (int64_t v : l.w) w.le((uint64_t)v, 8);
+        }
+    }
+    std::vector<uint32_t> zero((size_t)c.k * LABW);
+    dev::d2h(zero.data(), n.zero.as<uint32_t>() + (uint64_t)b * c.k * LABW, zero.size() * 4, g_stream);
+    std::vector<U4> cts(c.total_cts);
+    dev::d2h(cts.data(), n.blob.as<U4>() + (uint64_t)b * c.total_cts, cts.size() * 16, g_stream);
+    U4 commit;
+    dev::d2h(&commit, n.commit.as<U4>() + b, 16, g_stream);
+    dev::sync(g_stream);
+    for (int i = 0; i < c.k; ++i) w.u128v(host_compress(zero.data() + (size_t)i * LABW, c.base.primes[i]));
+    w.le(c.layers.size() + 1, 8);
+    for (const auto& l : c.layers) w.le(l.ct_base, 8);
+    w.le(c.total_cts, 8);
+    w.le(c.total_cts, 8);
+    for (const auto& v : cts) w.u128v(u4_to_u128(v));
+    w.u128v(u4_to_u128(commit));
+    return w.b;
+}
+
+static std::vector<U4> compress_lanes(const Lanes& L, const Crt& base, uint32_t B, uint32_t b) {
+    const uint64_t n = L.E;
+    DevBuf tmp;
+    tmp.ensure((size_t)B * n * 16);
+    std::vector<U4> out((size_t)base.k * n);
+    for (int i = 0; i < base.k; ++i) {
+        CompressParams P;
+        std::memset(&P, 0, sizeof P);
+        P.B = B;
+        P.n = (uint32_t)n;
+        P.p = (uint32_t)base.primes[i];
+        P.lane = L.lane[i]->as<uint32_t>();
+        P.out = tmp.as<U4>();
+        P.ostride = n;
+        launch_compress(P, g_stream);
+        dev::d2h(out.data() + (size_t)i * n, tmp.as<U4>() + (uint64_t)b * n, n * 16, g_stream);
+        dev::sync(g_stream);
+    }
+    return out;
+}
+
+static std::vector<uint8_t> export_encoding(const Network& n, uint32_t b) {
+    const dashgpu_circuit& c = *n.c;
+    if (b >= n.B) throw DataError("inference index out of range");
+    Writer w;
+    w.header(2);
+    w.le((uint64_t)c.k, 1);
+    w.shape(c.input_shape);
+    std::vector<uint32_t> R((size_t)c.k * LABW);
+    dev::d2h(R.data(), n.Rb.as<uint32_t>() + (uint64_t)b * c.k * LABW, R.size() * 4, g_stream);
+    dev::sync(g_stream);
+    for (int i = 0; i < c.k; ++i) w.u128v(host_compress(R.data() + (size_t)i * LABW, c.base.primes[i]));
+    const auto lanes = compress_lanes(n.base, c.base, n.B, b);
+    for (int i = 0; i < c.k; ++i) {  // tensor_write (label_tensor.cpp:95-101)
+        w.le((uint64_t)c.base.primes[i], 2);
+        w.shape(c.input_shape);
+        for (uint64_t e = 0; e < c.n_in; ++e) w.u128v(u4_to_u128(lanes[(size_t)i * c.n_in + e]));
+    }
+    return w.b;
+}
+
+static std::vector<uint8_t> export_decoding(const Network& n, uint32_t b) {
+    const dashgpu_circuit& c = *n.c;
+    if (b >= n.B) throw DataError("inference index out of range");
+    Writer w;
+    w.header(3);
+    w.le((uint64_t)c.k, 1);
+    w.shape(c.layers.empty() ? c.input_shape : c.layers.back().out_shape);
+    std::vector<U4> t((size_t)c.n_out * n.sum_p);
+    dev::d2h(t.data(), n.dec.as<U4>() + (uint64_t)b * t.size(), t.size() * 16, g_stream);
+    dev::sync(g_stream);
+    for (const auto& v : t) w.u128v(u4_to_u128(v));
+    return w.b;
+}
+
+// ============================================================ models
+
+namespace models {
+using Rng = std::mt19937;
+
+static std::vector<int64_t> random_ints(Rng& g, size_t n, int lo, int hi) {
+    std::uniform_int_distribution<int> d(lo, hi);
+    std::vector<int64_t> v(n);
+    for (auto& x : v) x = d(g);
+    return v;
+}
+static HLayer dense(uint32_t in, uint32_t out, Rng& g, bool priv = false, int wmax = 2, int bmax = 10) {
+    HLayer l;
+    l.kind = DASH_LAYER_DENSE;
+    l.priv = priv;
+    l.in_dim = in;
+    l.out_dim = out;
+    l.w = random_ints(g, (size_t)in * out, -wmax, wmax);
+    l.bias = random_ints(g, out, -bmax, bmax);
+    return l;
+}
+static HLayer conv2d(uint32_t ic, uint32_t oc, uint32_t f, uint32_t s, Rng& g, bool priv = false, int wmax = 2,
+                     int bmax = 10) {
+    HLayer l;
+    l.kind = DASH_LAYER_CONV2D;
+    l.priv = priv;
+    l.in_ch = ic;
+    l.out_ch = oc;
+    l.filter = f;
+    l.stride = s;
+    l.w = random_ints(g, (size_t)oc * ic * f * f, -wmax, wmax);
+    l.bias = random_ints(g, oc, -bmax, bmax);
+    return l;
+}
+static HLayer simple(int kind) {
+    HLayer l;
+    l.kind = kind;
+    return l;
+}
+
+// Builders mirror the reference's tests/support/test_models.hpp:79-145 (same
+// mt19937 stream, same draw order) plus the benchmark configurations of
+// SURVEY.md section 8(d).
+static void build(dashgpu_circuit& c, const std::string& name, uint32_t seed, int k, bool priv) {
+    Rng g(seed);
+    c.k = k;
+    c.layers.clear();
+    const HLayer R = simple(DASH_LAYER_RELU), F = simple(DASH_LAYER_FLATTEN), SA = simple(DASH_LAYER_SIGNACT);
+    if (name == "model_a") {
+        c.input_shape = {784};
+        c.layers.push_back(dense(784, 128, g));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(dense(128, 128, g));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(dense(128, 10, g));
+    } else if (name == "model_c") {
+        c.input_shape = {1, 28, 28};
+        c.layers.push_back(conv2d(1, 5, 4, 2, g));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(simple(DASH_LAYER_FLATTEN));
+        c.layers.push_back(dense(845, 100, g));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(dense(100, 10, g));
+    } else if (name == "model_d") {
+        c.input_shape = {1, 28, 28};
+        c.layers.push_back(conv2d(1, 16, 6, 2, g));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(conv2d(16, 16, 6, 2, g));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(simple(DASH_LAYER_FLATTEN));
+        c.layers.push_back(dense(256, 100, g));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(dense(100, 10, g));
+    } else if (name == "model_f_dims") {
+        c.input_shape = {3, 32, 32};
+        c.layers.push_back(simple(DASH_LAYER_FLATTEN));
+        c.layers.push_back(dense(3072, 16, g));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(dense(16, 10, g));
+    } else if (name == "model_tiny") {
+        c.input_shape = {2, 6, 6};
+        c.layers.push_back(conv2d(2, 3, 3, 1, g, priv));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(conv2d(3, 2, 2, 2, g, priv));
+        c.layers.push_back(simple(DASH_LAYER_SIGNACT));
+        c.layers.push_back(simple(DASH_LAYER_FLATTEN));
+        c.layers.push_back(dense(8, 5, g, priv));
+        c.layers.push_back(simple(DASH_LAYER_RELU));
+        c.layers.push_back(dense(5, 3, g, priv));
+    } else if (name == "lenet5") {
+        // LeNet-5 restated in reference ops (pooling -> strided 2x2 conv)
+        c.input_shape = {1, 28, 28};
+        c.layers.push_back(conv2d(1, 6, 5, 1, g, priv));
+        c.layers.push_back(R);
+        c.layers.push_back(conv2d(6, 6, 2, 2, g, priv));
+        c.layers.push_back(conv2d(6, 16, 5, 1, g, priv));
+        c.layers.push_back(R);
+        c.layers.push_back(conv2d(16, 16, 2, 2, g, priv));
+        c.layers.push_back(F);
+        c.layers.push_back(dense(256, 120, g, priv));
+        c.layers.push_back(R);
+        c.layers.push_back(dense(120, 84, g, priv));
+        c.layers.push_back(R);
+        c.layers.push_back(dense(84, 10, g, priv));
+    } else if (name == "minionn") {
+        // paper Model F, Tanh -> ReLU, padding-free
+        c.input_shape = {3, 32, 32};
+        const uint32_t spec[8][4] = {{3, 32, 3, 1},  {32, 32, 3, 1}, {32, 32, 2, 2},  {32, 64, 3, 1},
+                                     {64, 64, 3, 1}, {64, 64, 2, 2}, {64, 128, 3, 1}, {128, 128, 3, 1}};
+        for (auto& s : spec) {
+            c.layers.push_back(conv2d(s[0], s[1], s[2], s[3], g, priv));
+            c.layers.push_back(R);
+        }
+        c.layers.push_back(F);
+        c.layers.push_back(dense(128, 10, g, priv));
+    } else if (name.rfind("relu", 0) == 0 || name.rfind("sign", 0) == 0) {
+        const long n = std::stol(name.substr(4));
+        if (n <= 0) throw DataError("bad sweep size");
+        c.input_shape = {(uint32_t)n};
+        c.layers.push_back(name[0] == 'r' ? R : SA);
+    } else if (name.rfind("dense", 0) == 0) {
+        const long n = std::stol(name.substr(5));
+        c.input_shape = {(uint32_t)n};
+        c.layers.push_back(dense((uint32_t)n, (uint32_t)n, g));
+    } else {
+        throw DataError("unknown model " + name);
+    }
+}
+}  // namespace models
+
+// ============================================================ constants
+
+static bool g_constants = false;
+static std::mutex g_init_mu;
+
+static void check_constants() {
+    if (!g_constants) throw std::runtime_error("dashgpu_init() has not been called");
+}
+
+static void init_device(int device) {
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    dev::set_device(device);
+    static std::vector<ModC> mods(MAXMOD + 1);
+    for (int m = 2; m <= MAXMOD; ++m) mods[m] = make_modc(m);
+    uint32_t pi_rk[44];
+    const uint8_t zero[16] = {0};
+    aes_expand_host(zero, pi_rk);
+    uint16_t modslot[MAXMOD + 1] = {0};
+    for (int m = 2; m <= MAXMOD; ++m) modslot[m] = (uint16_t)(m - 2);
+    uint32_t T0[256];
+    t0_table(T0);
+    dev::upload_constants(mods.data(), pi_rk, modslot, T0);
+    g_constants = true;
+}
+
+// plain_forward (layer.cpp:346-376, 56-109) with OverflowError range checks
+static std::vector<int64_t> plain_forward(const dashgpu_circuit& c, std::vector<int64_t> x) {
+    const int64_t hi = max_signed(c.base), lo = min_signed(c.base);
+    for (const auto& l : c.layers) {
+        std::vector<int64_t> y(l.E_out);
+        if (l.linear()) {
+            for (uint64_t u = 0; u < l.E_out; ++u) {
+                __int128 acc;
+                if (l.kind == DASH_LAYER_DENSE) {
+                    acc = l.bias.empty() ? 0 : l.bias[u];
+                    for (uint32_t i = 0; i < l.in_dim; ++i) acc += (__int128)l.w[u * l.in_dim + i] * x[i];
+                } else {
+                    const uint32_t H = l.in_shape[1], W = l.in_shape[2], OH = l.out_shape[1], OW = l.out_shape[2];
+                    const uint32_t oc = (uint32_t)(u / ((uint64_t)OH * OW)), oy = (uint32_t)((u / OW) % OH),
+                                   ox = (uint32_t)(u % OW);
+                    acc = l.bias.empty() ? 0 : l.bias[oc];
+                    for (uint32_t ic = 0; ic < l.in_ch; ++ic)
+                        for (uint32_t ky = 0; ky < l.filter; ++ky)
+                            for (uint32_t kx = 0; kx < l.filter; ++kx)
+                                acc += (__int128)l.w[(((uint64_t)oc * l.in_ch + ic) * l.filter + ky) * l.filter + kx] *
+                                       x[((uint64_t)ic * H + (oy * l.stride + ky)) * W + (ox * l.stride + kx)];
+                }
+                if (acc > hi || acc < lo) throw OverflowErr("intermediate value left the signed range of the base");
+                y[u] = (int64_t)acc;
+            }
+        } else {
+            for (uint64_t u = 0; u < l.E_out; ++u) {
+                if (l.kind == DASH_LAYER_RELU) y[u] = x[u] > 0 ? x[u] : 0;
+                else if (l.kind == DASH_LAYER_SIGNACT) y[u] = x[u] > 0 ? 1 : -1;
+                else y[u] = x[u];
+            }
+        }
+        x = std::move(y);
+    }
+    return x;
+}
+
+}  // namespace dashgpu
+
+dashgpu_circuit::~dashgpu_circuit() = default;
+
+struct dashgpu_network {
+    std::unique_ptr<dashgpu::Network> net;
+};
+struct dashgpu_bundle {
+    std::unique_ptr<dashgpu::Bundle> b;
+};
+
+// ================================================================ C ABI
+
+using namespace dashgpu;
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        f();
+        return DASHGPU_OK;
+    } catch (const OverflowErr& e) {
+        g_err = e.what();
+        return DASHGPU_ERR_OVERFLOW;
+    } catch (const DataError& e) {
+        g_err = e.what();
+        return DASHGPU_ERR_DATA;
+    } catch (const AuthError& e) {
+        g_err = e.what();
+        return DASHGPU_ERR_AUTH;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return std::string(e.what()).rfind("CUDA", 0) == 0 ? DASHGPU_ERR_CUDA : DASHGPU_ERR;
+    }
+}
+
+extern "C" {
+
+const char* dashgpu_last_error(void) { return g_err.c_str(); }
+int dashgpu_version(void) { return 1; }
+
+int dashgpu_init(int device) {
+    return guarded([&] { init_device(device); });
+}
+
+int dashgpu_set_stream(void* stream) {
+    g_stream = stream;
+    return DASHGPU_OK;
+}
+
+int dashgpu_circuit_create(const dash_circuit_desc* d, dashgpu_circuit** out) {
+    return guarded([&] {
+        if (!d || !out) throw DataError("null argument");
+        if (d->k < 1 || d->k > MAXK) throw DataError("CRT base size out of range");
+        if (d->rank < 1 || d->rank > 8) throw DataError("bad tensor rank");
+        auto c = std::make_unique<dashgpu_circuit>();
+        c->k = d->k;
+        c->input_shape.assign(d->input_shape, d->input_shape + d->rank);
+        c->sign_target = d->sign_target;
+        c->alpha = d->alpha;
+        for (uint32_t i = 0; i < d->n_layers; ++i) {
+            const dash_layer_desc& s = d->layers[i];
+            HLayer l;
+            l.kind = s.kind;
+            l.priv = s.private_weights != 0;
+            l.in_dim = s.in_dim;
+            l.out_dim = s.out_dim;
+            l.in_ch = s.in_ch;
+            l.out_ch = s.out_ch;
+            l.filter = s.filter;
+            l.stride = s.stride;
+            if (s.q_weights) l.w.assign(s.q_weights, s.q_weights + s.n_weights);
+            if (s.q_biases) l.bias.assign(s.q_biases, s.q_biases + s.n_biases);
+            c->layers.push_back(std::move(l));
+        }
+        prepare_circuit(*c);
+        *out = c.release();
+    });
+}
+
+void dashgpu_circuit_destroy(dashgpu_circuit* c) { delete c; }
+
+int dashgpu_model_build(const char* name, uint32_t seed, int k, int priv, dashgpu_circuit** out) {
+    return guarded([&] {
+        auto c = std::make_unique<dashgpu_circuit>();
+        models::build(*c, name, seed, k, priv != 0);
+        prepare_circuit(*c);
+        *out = c.release();
+    });
+}
+
+int dashgpu_circuit_info_get(const dashgpu_circuit* c, dashgpu_circuit_info* o) {
+    return guarded([&] {
+        std::memset(o, 0, sizeof *o);
+        o->k = c->k;
+        o->n_layers = (uint32_t)c->layers.size();
+        o->n_in = c->n_in;
+        o->n_out = c->n_out;
+        o->cts = c->total_cts;
+        o->gates = c->total_gates;
+        o->wires = c->total_wires + c->wire0;
+        if (c->needs_sign) {
+            o->sign_t = (uint32_t)c->sign.spec.size();
+            for (size_t j = 0; j < c->sign.spec.size() && j < 32; ++j) o->radices[j] = (uint16_t)c->sign.spec[j];
+            o->act_uc_cts = c->relu_tape->cts;
+            o->max_slots = (uint32_t)std::max(c->relu_tape->nslots, c->sign_tape->nslots);
+        }
+        o->relu_elements = c->relu_elements;
+        o->linear_macs = c->linear_macs;
+    });
+}
+
+int dashgpu_circuit_desc_view(const dashgpu_circuit* cc, dash_circuit_desc* out) {
+    return guarded([&] {
+        auto* c = const_cast<dashgpu_circuit*>(cc);
+        c->desc_layers.clear();
+        for (const auto& l : c->layers) {
+            dash_layer_desc s;
+            std::memset(&s, 0, sizeof s);
+            s.kind = l.kind;
+            s.private_weights = l.priv;
+            s.in_dim = l.in_dim;
+            s.out_dim = l.out_dim;
+            s.in_ch = l.in_ch;
+            s.out_ch = l.out_ch;
+            s.filter = l.filter;
+            s.stride = l.stride;
+            s.q_weights = l.w.empty() ? nullptr : l.w.data();
+            s.n_weights = l.w.size();
+            s.q_biases = l.bias.empty() ? nullptr : l.bias.data();
+            s.n_biases = l.bias.size();
+            c->desc_layers.push_back(s);
+        }
+        std::memset(out, 0, sizeof *out);
+        out->k = c->k;
+        out->rank = (uint32_t)c->input_shape.size();
+        for (size_t i = 0; i < c->input_shape.size(); ++i) out->input_shape[i] = c->input_shape[i];
+        out->sign_target = c->sign_target;
+        out->alpha = c->alpha;
+        out->n_layers = (uint32_t)c->desc_layers.size();
+        out->layers = c->desc_layers.data();
+    });
+}
+
+int dashgpu_random_input(const dashgpu_circuit* c, uint32_t seed, int lo, int hi, int64_t* out) {
+    return guarded([&] {
+        models::Rng g(seed);
+        auto v = models::random_ints(g, c->n_in, lo, hi);
+        std::copy(v.begin(), v.end(), out);
+    });
+}
+
+int dashgpu_plain_forward(const dashgpu_circuit* c, const int64_t* in, int64_t* out) {
+    return guarded([&] {
+        auto y = plain_forward(*c, std::vector<int64_t>(in, in + c->n_in));
+        std::copy(y.begin(), y.end(), out);
+    });
+}
+
+int dashgpu_garble(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch, dashgpu_network** out) {
+    return guarded([&] {
+        if (batch == 0) throw DataError("empty batch");
+        auto n = std::make_unique<dashgpu_network>();
+        n->net = std::make_unique<Network>();
+        n->net->c = const_cast<dashgpu_circuit*>(c);
+        garble_into(*n->net, seeds, batch, false);
+        dev::sync(g_stream);
+        *out = n.release();
+    });
+}
+
+void dashgpu_network_destroy(dashgpu_network* n) { delete n; }
+
+int dashgpu_garble_inputs(dashgpu_network* n, const int64_t* values, dashgpu_bundle** out) {
+    return guarded([&] {
+        auto b = std::make_unique<dashgpu_bundle>();
+        b->b = std::make_unique<Bundle>();
+        encode_into(*n->net, values, false, *b->b);
+        *out = b.release();
+    });
+}
+
+int dashgpu_evaluate(dashgpu_network* n, const dashgpu_bundle* in, dashgpu_bundle** out) {
+    return guarded([&] {
+        auto b = std::make_unique<dashgpu_bundle>();
+        b->b = std::make_unique<Bundle>();
+        evaluate_into(*n->net, *in->b, *b->b);
+        dev::sync(g_stream);
+        *out = b.release();
+    });
+}
+
+int dashgpu_decode_outputs(dashgpu_network* n, const dashgpu_bundle* out, int64_t* values) {
+    return guarded([&] { decode_into(*n->net, *out->b, values, false); });
+}
+
+void dashgpu_bundle_destroy(dashgpu_bundle* b) { delete b; }
+
+int dashgpu_export_gc(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
+    return guarded([&] { out_bytes(export_gc(*n->net, b), buf, cap, len); });
+}
+int dashgpu_export_encoding(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
+    return guarded([&] { out_bytes(export_encoding(*n->net, b), buf, cap, len); });
+}
+int dashgpu_export_decoding(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
+    return guarded([&] { out_bytes(export_decoding(*n->net, b), buf, cap, len); });
+}
+int dashgpu_export_bundle(const dashgpu_bundle* bd, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
+    return guarded([&] {
+        const Bundle& B = *bd->b;
+        if (b >= B.B) throw DataError("inference index out of range");
+        const auto v = compress_lanes(B.lanes, B.net->c->base, B.B, b);
+        Writer w;
+        for (const auto& x : v) w.u128v(u4_to_u128(x));
+        out_bytes(w.b, buf, cap, len);
+    });
+}
+
+int dashgpu_import_bundle(dashgpu_network* n, const uint8_t* data, size_t len, int output, dashgpu_bundle** out) {
+    return guarded([&] {
+        Network& N = *n->net;
+        const dashgpu_circuit& c = *N.c;
+        const uint64_t E = output ? c.n_out : c.n_in;
+        if (len != (size_t)N.B * c.k * E * 16) throw DataError("wire payload size mismatch");
+        auto bd = std::make_unique<dashgpu_bundle>();
+        bd->b = std::make_unique<Bundle>();
+        Bundle& B = *bd->b;
+        B.net = &N;
+        B.B = N.B;
+        B.output = output != 0;
+        B.lanes.ensure(c.base, N.B, E);
+        DevBuf tmp;
+        tmp.ensure((size_t)N.B * E * 16);
+        for (int i = 0; i < c.k; ++i) {
+            std::vector<uint8_t> lane((size_t)N.B * E * 16);
+            for (uint32_t b = 0; b < N.B; ++b)
+                std::memcpy(lane.data() + (size_t)b * E * 16, data + ((size_t)b * c.k + i) * E * 16, E * 16);
+            dev::h2d(tmp.p, lane.data(), lane.size(), g_stream);
+            CompressParams P;
+            std::memset(&P, 0, sizeof P);
+            P.B = N.B;
+            P.n = (uint32_t)E;
+            P.p = (uint32_t)c.base.primes[i];
+            P.out = tmp.as<U4>();
+            P.ostride = E;
+            launch_decompress(P, B.lanes.lane[i]->as<uint32_t>(), g_stream);
+            dev::sync(g_stream);
+        }
+        *out = bd.release();
+    });
+}
+
+int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint8_t* mask16) {
+    return guarded([&] {
+        Network& N = *n->net;
+        if (b >= N.B || index >= N.c->total_cts) throw DataError("ciphertext index out of range");
+        U4 v;
+        U4* p = N.blob.as<U4>() + (uint64_t)b * N.c->total_cts + index;
+        dev::d2h(&v, p, 16, g_stream);
+        dev::sync(g_stream);
+        uint8_t* vb = reinterpret_cast<uint8_t*>(&v);
+        for (int i = 0; i < 16; ++i) vb[i] ^= mask16[i];
+        dev::h2d(p, &v, 16, g_stream);
+        dev::sync(g_stream);
+    });
+}
+
+int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batch, const int64_t* inputs,
+                  int64_t* outputs, int on_device, dashgpu_timing* t) {
+    return guarded([&] {
+        auto* c = const_cast<dashgpu_circuit*>(cc);
+        std::lock_guard<std::mutex> lk(c->mu);
+        using clk = std::chrono::steady_clock;
+        const auto t0 = clk::now();
+        // per-inference device bytes: ciphertexts + multiples + decode table + planes
+        uint64_t planes = 0;
+        {
+            uint64_t maxE = c->n_in;
+            for (const auto& l : c->layers) maxE = std::max(maxE, l.E_out);
+            for (int p : c->base.primes) planes += (uint64_t)((n_digits_host(p) + 3) / 4) * maxE * 4;
+        }
+        const uint64_t per = c->total_cts * 16 + (uint64_t)(MAXMOD - 1) * 128 * NWMAX * 4 + planes * 5 +
+                             c->n_out * 600 * 16 + 4096;
+        if (!c->workspace) {
+            c->workspace = std::make_unique<Network>();
+            c->workspace->c = c;
+        }
+        Network& n = *c->workspace;
+        uint32_t chunk = batch;
+        if (n.cap < batch) {
+            const uint64_t budget = (uint64_t)(dev::free_bytes() * 0.85) + (uint64_t)n.cap * per;
+            chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(batch, budget / per));
+        }
+        dashgpu_timing tm;
+        std::memset(&tm, 0, sizeof tm);
+        Bundle in, out;
+        for (uint32_t b0 = 0; b0 < batch; b0 += chunk) {
+            const uint32_t B = std::min(chunk, batch - b0);
+            const auto a = clk::now();
+            garble_into(n, seeds + (size_t)16 * b0, B, on_device != 0);
+            dev::sync(g_stream);
+            const auto b = clk::now();
+            encode_into(n, inputs + (size_t)b0 * c->n_in, on_device != 0, in);
+            const auto d = clk::now();
+            evaluate_into(n, in, out);
+            dev::sync(g_stream);
+            const auto e = clk::now();
+            decode_into(n, out, outputs + (size_t)b0 * c->n_out, on_device != 0);
+            dev::sync(g_stream);
+            const auto f = clk::now();
+            tm.ms_garble += std::chrono::duration<double, std::milli>(b - a).count();
+            tm.ms_encode += std::chrono::duration<double, std::milli>(d - b).count();
+            tm.ms_evaluate += std::chrono::duration<double, std::milli>(e - d).count();
+            tm.ms_decode += std::chrono::duration<double, std::milli>(f - e).count();
+            tm.sub_batches += 1;
+        }
+        if (!on_device) {
+            tm.h2d_bytes = (uint64_t)batch * (c->n_in * 8 + 16 + 44 * 4);
+            tm.d2h_bytes = (uint64_t)batch * c->n_out * c->k;
+        }
+        tm.ms_total = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+        if (t) *t = tm;
+    });
+}
+
+int dashgpu_profile(int enable) {
+    return guarded([&] {
+        dev::prof_enable(enable);
+        dev::prof_reset();
+    });
+}
+
+int dashgpu_profile_read(double* ms, uint64_t* launches, int max_kinds) {
+    int k = 0;
+    int rc = guarded([&] { k = dev::prof_read(ms, launches, max_kinds); });
+    return rc ? -rc : k;
+}
+
+int dashgpu_prim(int op, uint32_t n, int m, int q, const uint64_t* in, uint64_t* out, uint16_t* digits,
+                 const uint8_t* key16, const uint64_t* wires, uint64_t gate) {
+    return guarded([&] {
+        check_constants();
+        if (m < 2 || m > MAXMOD || ((op == 4 || op == 5) && (q < 2 || q > MAXMOD)))
+            throw DataError("modulus out of range");
+        DevBuf din, dout, ddig, drk, dw;
+        din.ensure((size_t)n * 16);
+        dout.ensure((size_t)n * 16);
+        ddig.ensure((size_t)n * LABW * 4);
+        drk.ensure(44 * 4);
+        dw.ensure((size_t)n * 8);
+        if (in) dev::h2d(din.p, in, (size_t)n * 16, g_stream);
+        if (out && (op == 4 || op == 5)) dev::h2d(dout.p, out, (size_t)n * 16, g_stream);
+        if (key16) {
+            uint32_t rk[44];
+            aes_expand_host(key16, rk);
+            dev::h2d(drk.p, rk, sizeof rk, g_stream);
+        }
+        if (wires) dev::h2d(dw.p, wires, (size_t)n * 8, g_stream);
+        dev::memset0(ddig.p, (size_t)n * LABW * 4, g_stream);
+        PrimParams P;
+        std::memset(&P, 0, sizeof P);
+        P.op = op;
+        P.n = n;
+        P.m = (uint32_t)m;
+        P.q = (uint32_t)q;
+        P.in = din.as<U4>();
+        P.out = dout.as<U4>();
+        P.digits = ddig.as<uint32_t>();
+        P.rk = drk.as<uint32_t>();
+        P.wires = dw.as<uint64_t>();
+        P.gate = gate;
+        launch_prim(P, g_stream);
+        if (out) dev::d2h(out, dout.p, (size_t)n * 16, g_stream);
+        std::vector<uint32_t> dg((size_t)n * LABW);
+        dev::d2h(dg.data(), ddig.p, dg.size() * 4, g_stream);
+        dev::sync(g_stream);
+        if (digits)
+            for (size_t i = 0; i < (size_t)n * 128; ++i) digits[i] = (uint16_t)((dg[i / 4] >> (8 * (i % 4))) & 0xff);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,238 @@
+// CUDA side of the B200 Dash engine (sm_100a), non-activation kernels:
+// public/private linear lanes, garbling setup (offsets, PRF labels), input
+// encoding, decoding tables / decode, label export and primitive parity
+// kernels.  Owns device memory, streams and per-kernel event timing.
+#include "dash_common.hpp"
+
+namespace dashgpu {
+__constant__ ModC c_mod[MAXMOD + 1];
+__constant__ uint32_t c_pi_rk[44];
+__constant__ uint16_t c_modslot[MAXMOD + 1];
+__device__ uint32_t g_T0[256];
+}  // namespace dashgpu
+#define DASH_CONST_DEFINED 1
+#include "dash_prim.cuh"
+#include "kernels_common.cuh"
+
+namespace dashgpu {
+
+void upload_act(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot, const uint32_t* T0);
+
+ProfData& prof() {
+    static ProfData p;
+    return p;
+}
+
+namespace {
+
+void prof_drain() {
+    for (auto& p : prof().pending) {
+        cudaEventSynchronize(p.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        prof().ms[p.kind] += ms;
+        prof().n[p.kind] += 1;
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    prof().pending.clear();
+}
+
+__global__ void __launch_bounds__(128) linear_kernel(LinParams L) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= L.M) return;
+    linear_thread(L, blockIdx.z, blockIdx.y, u);
+}
+
+__global__ void __launch_bounds__(128) private_kernel(PrivParams P) {
+    __shared__ uint32_t T[kTWords];
+    fill_T(T, g_T0);
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= P.M) return;
+    private_thread(P, blockIdx.y, u, AesTab{T, threadIdx.x & 31u});
+}
+
+__global__ void __launch_bounds__(128) setup_offsets_kernel(SetupParams Sp) {
+    __shared__ uint32_t T[kTWords];
+    fill_T(T, g_T0);
+    const uint32_t si = blockIdx.x * blockDim.x + threadIdx.x;
+    if (si >= Sp.nslot) return;
+    setup_offsets_thread(Sp, blockIdx.y, si, AesTab{T, threadIdx.x & 31u});
+}
+
+__global__ void __launch_bounds__(128) setup_labels_kernel(SetupParams Sp) {
+    __shared__ uint32_t T[kTWords];
+    fill_T(T, g_T0);
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e > Sp.n_in) return;
+    setup_labels_thread(Sp, blockIdx.z, e, (int)blockIdx.y, AesTab{T, threadIdx.x & 31u});
+}
+
+__global__ void __launch_bounds__(128) encode_kernel(EncodeParams P) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= P.n_in) return;
+    encode_thread(P, blockIdx.z, e, (int)blockIdx.y);
+}
+
+__global__ void __launch_bounds__(128) dectable_kernel(DecodeParams P) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= P.n_out) return;
+    dectable_thread(P, blockIdx.z, e, (int)blockIdx.y);
+}
+
+__global__ void __launch_bounds__(128) decode_kernel(DecodeParams P) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= P.n_out) return;
+    decode_thread(P, blockIdx.y, e);
+}
+
+__global__ void __launch_bounds__(128) compress_kernel(CompressParams P) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= P.n) return;
+    compress_thread(P, blockIdx.y, e);
+}
+
+__global__ void __launch_bounds__(128) decompress_kernel(CompressParams P, uint32_t* lane_out) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= P.n) return;
+    decompress_thread(P, blockIdx.y, e, lane_out);
+}
+
+__global__ void __launch_bounds__(128) prim_kernel(PrimParams P) {
+    __shared__ uint32_t T[kTWords];
+    fill_T(T, g_T0);
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    prim_thread(P, i, AesTab{T, threadIdx.x & 31u});
+}
+
+}  // namespace
+
+namespace dev {
+
+void set_device(int d) { ck(cudaSetDevice(d), "cudaSetDevice"); }
+int backend() { return 1; }
+void* alloc(size_t n) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, n ? n : 16), "cudaMalloc");
+    return p;
+}
+void release(void* p) {
+    if (p) cudaFree(p);
+}
+void* host_alloc(size_t n) {
+    void* p = nullptr;
+    ck(cudaMallocHost(&p, n ? n : 16), "cudaMallocHost");
+    return p;
+}
+void host_release(void* p) {
+    if (p) cudaFreeHost(p);
+}
+void h2d(void* d, const void* s, size_t n, void* st) {
+    if (n) ck(cudaMemcpyAsync(d, s, n, cudaMemcpyHostToDevice, S(st)), "h2d");
+}
+void d2h(void* d, const void* s, size_t n, void* st) {
+    if (n) ck(cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToHost, S(st)), "d2h");
+}
+void d2d(void* d, const void* s, size_t n, void* st) {
+    if (n) ck(cudaMemcpyAsync(d, s, n, cudaMemcpyDeviceToDevice, S(st)), "d2d");
+}
+void memset0(void* p, size_t n, void* st) {
+    if (n) ck(cudaMemsetAsync(p, 0, n, S(st)), "memset");
+}
+void sync(void* st) {
+    ck(cudaStreamSynchronize(S(st)), "sync");
+    if (prof().on) prof_drain();
+}
+void check() { ck(cudaGetLastError(), "launch"); }
+size_t free_bytes() {
+    size_t f = 0, t = 0;
+    ck(cudaMemGetInfo(&f, &t), "cudaMemGetInfo");
+    return f;
+}
+void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot, const uint32_t* T0) {
+    ck(cudaMemcpyToSymbol(c_mod, mods, sizeof(ModC) * (MAXMOD + 1)), "c_mod");
+    ck(cudaMemcpyToSymbol(c_pi_rk, pi_rk, sizeof(uint32_t) * 44), "c_pi_rk");
+    ck(cudaMemcpyToSymbol(c_modslot, modslot, sizeof(uint16_t) * (MAXMOD + 1)), "c_modslot");
+    ck(cudaMemcpyToSymbol(g_T0, T0, sizeof(uint32_t) * 256), "g_T0");
+    upload_act(mods, pi_rk, modslot, T0);
+}
+void prof_enable(int on) { prof().on = on; }
+void prof_reset() {
+    prof_drain();
+    for (int i = 0; i < K_NKINDS; ++i) {
+        prof().ms[i] = 0;
+        prof().n[i] = 0;
+    }
+}
+int prof_read(double* ms, uint64_t* n, int maxk) {
+    prof_drain();
+    const int k = maxk < K_NKINDS ? maxk : K_NKINDS;
+    for (int i = 0; i < k; ++i) {
+        ms[i] = prof().ms[i];
+        n[i] = prof().n[i];
+    }
+    return k;
+}
+
+}  // namespace dev
+
+void launch_linear(const LinParams& L, void* st) {
+    if (L.B == 0 || L.M == 0) return;
+    ProfScope ps(K_LINEAR, S(st));
+    dim3 grid(cdiv(L.M, 128), L.nw, L.B);
+    linear_kernel<<<grid, 128, 0, S(st)>>>(L);
+    dev::check();
+}
+
+void launch_private(const PrivParams& P, void* st) {
+    if (P.B == 0 || P.M == 0) return;
+    ProfScope ps(P.garbler ? K_PRIV_GARBLE : K_PRIV_EVAL, S(st));
+    private_kernel<<<dim3(cdiv(P.M, 128), P.B), 128, 0, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_setup(const SetupParams& Sp, void* st) {
+    ProfScope ps(K_SETUP, S(st));
+    setup_offsets_kernel<<<dim3(cdiv(Sp.nslot, 128), Sp.B), 128, 0, S(st)>>>(Sp);
+    dev::check();
+    setup_labels_kernel<<<dim3(cdiv(Sp.n_in + 1, 128), Sp.k, Sp.B), 128, 0, S(st)>>>(Sp);
+    dev::check();
+}
+
+void launch_encode(const EncodeParams& P, void* st) {
+    ProfScope ps(K_ENCODE, S(st));
+    encode_kernel<<<dim3(cdiv(P.n_in, 128), P.k, P.B), 128, 0, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_dectable(const DecodeParams& P, void* st) {
+    ProfScope ps(K_DECODE, S(st));
+    dectable_kernel<<<dim3(cdiv(P.n_out, 128), P.k, P.B), 128, 0, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_decode(const DecodeParams& P, void* st) {
+    ProfScope ps(K_DECODE, S(st));
+    decode_kernel<<<dim3(cdiv(P.n_out, 128), P.B), 128, 0, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_compress(const CompressParams& P, void* st) {
+    ProfScope ps(K_MISC, S(st));
+    compress_kernel<<<dim3(cdiv(P.n, 128), P.B), 128, 0, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_decompress(const CompressParams& P, uint32_t* lane_out, void* st) {
+    ProfScope ps(K_MISC, S(st));
+    decompress_kernel<<<dim3(cdiv(P.n, 128), P.B), 128, 0, S(st)>>>(P, lane_out);
+    dev::check();
+}
+
+void launch_prim(const PrimParams& P, void* st) {
+    prim_kernel<<<cdiv(P.n, 128), 128, 0, S(st)>>>(P);
+    dev::check();
+}
+
+}  // namespace dashgpu

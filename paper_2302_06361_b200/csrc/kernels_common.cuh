@@ -1,0 +1,63 @@
+// Helpers shared by the CUDA translation units (kernels.cu, kernels_act.cu).
+// Each TU defines its own copy of the constant tables (no relocatable device
+// code) before including this header; dev::upload_constants() fills both.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "launch.hpp"
+
+namespace dashgpu {
+
+constexpr int kActWarps = 8;  // warps per CTA of the activation kernels
+constexpr int kTWords = 256 * 32;
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA ") + what + ": " + cudaGetErrorString(e));
+}
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+inline uint32_t cdiv(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
+
+// ---- per-kind CUDA-event timing on the launching stream (kernels.cu owns it)
+struct ProfData {
+    int on = 0;
+    double ms[K_NKINDS] = {};
+    uint64_t n[K_NKINDS] = {};
+    struct Pending {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+};
+ProfData& prof();
+
+struct ProfScope {
+    int kind;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(int k, cudaStream_t st) : kind(k), s(st) {
+        if (prof().on) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~ProfScope() {
+        if (prof().on) {
+            cudaEventRecord(b, s);
+            prof().pending.push_back({kind, a, b});
+        }
+    }
+};
+
+// Replicates T0 32x into shared memory: entry x of lane l at T[x*32 + l].
+__device__ __forceinline__ void fill_T(uint32_t* T, const uint32_t* T0) {
+    for (int i = threadIdx.x; i < kTWords; i += blockDim.x) T[i] = T0[i >> 5];
+    __syncthreads();
+}
+
+}  // namespace dashgpu

@@ -1,0 +1,75 @@
+// Seam between the host engine (engine.cpp, plain C++) and the device side
+// (kernels.cu: CUDA for sm_100a).  The engine never includes CUDA headers; all
+// device memory, streams and kernel launches go through these functions.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "dash_layers.cuh"
+
+namespace dashgpu {
+namespace dev {
+
+void set_device(int device);
+int backend();  // 1 = CUDA
+void* alloc(size_t bytes);
+void release(void* p);
+void* host_alloc(size_t bytes);  // pinned
+void host_release(void* p);
+void h2d(void* dst, const void* src, size_t n, void* stream);
+void d2h(void* dst, const void* src, size_t n, void* stream);
+void d2d(void* dst, const void* src, size_t n, void* stream);
+void memset0(void* p, size_t n, void* stream);
+void sync(void* stream);
+void check();  // raise on a pending device error
+size_t free_bytes();
+void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot, const uint32_t* T0);
+
+// per-kernel-kind event timing on the launching stream (bench roofline)
+void prof_enable(int on);
+void prof_reset();
+int prof_read(double* ms, uint64_t* launches, int max_kinds);
+
+}  // namespace dev
+
+enum KernelKind {
+    K_ACT_GARBLE = 0,
+    K_ACT_EVAL = 1,
+    K_LINEAR = 2,
+    K_PRIV_GARBLE = 3,
+    K_PRIV_EVAL = 4,
+    K_SETUP = 5,
+    K_ENCODE = 6,
+    K_DECODE = 7,
+    K_MISC = 8,
+    K_NKINDS = 9
+};
+
+void launch_act(const ActParams& P, bool garble, int nslots, void* stream);
+void launch_linear(const LinParams& L, void* stream);
+void launch_private(const PrivParams& P, void* stream);
+void launch_setup(const SetupParams& S, void* stream);
+void launch_encode(const EncodeParams& P, void* stream);
+void launch_dectable(const DecodeParams& P, void* stream);
+void launch_decode(const DecodeParams& P, void* stream);
+void launch_compress(const CompressParams& P, void* stream);
+void launch_decompress(const CompressParams& P, uint32_t* lane_out, void* stream);
+
+// primitive kernels for parity tests: op 0 decompress+compress, 1 aes_pi,
+// 2 aes with key, 3 prf label, 4 encrypt_label, 5 decrypt_label
+struct PrimParams {
+    int op;
+    uint32_t n;
+    uint32_t m, q;
+    const U4* in;       // [n]
+    U4* out;            // [n]
+    uint32_t* digits;   // [n][LABW] byte-digit words
+    const uint32_t* rk; // [44]
+    const uint64_t* wires;
+    uint64_t gate;
+};
+void launch_prim(const PrimParams& P, void* stream);
+
+}  // namespace dashgpu

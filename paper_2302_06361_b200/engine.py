@@ -1,0 +1,307 @@
+"""Python mirror of the reference's whole-network API over the C ABI.
+
+Names and argument meaning follow ``dash::garble`` / ``garble_inputs`` /
+``evaluate`` / ``decode_outputs`` (reference
+``proj/core/include/dash/garble.hpp:93-112``); errors follow
+``proj/core/include/dash/errors.hpp:9-34`` (``DataError``, ``OverflowError``
+(a DataError), ``AuthenticityError``).  Every call is batched over
+independent inferences, one 16-byte seed each.
+
+The compute path is libdashgpu.so (CUDA, sm_100a).  There is no CPU fallback:
+constructing ``Dash()`` without the built library or without a CUDA device
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .circuit import Circuit, CircuitDesc
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdashgpu.so")
+
+vp = ctypes.c_void_p
+u8p = ctypes.POINTER(ctypes.c_uint8)
+u16p = ctypes.POINTER(ctypes.c_uint16)
+u64p = ctypes.POINTER(ctypes.c_uint64)
+i64p = ctypes.POINTER(ctypes.c_int64)
+f64p = ctypes.POINTER(ctypes.c_double)
+
+
+class Error(RuntimeError):
+    """dash::Error"""
+
+
+class DataError(Error):
+    """dash::DataError (CLI exit 3)"""
+
+
+class OverflowError_(DataError):
+    """dash::OverflowError"""
+
+
+class AuthenticityError(Error):
+    """dash::AuthenticityError (CLI exit 4)"""
+
+
+class CudaError(Error):
+    """CUDA runtime failure (no device, launch failure, out of memory)."""
+
+
+_CODES = {1: Error, 2: CudaError, 3: DataError, 4: AuthenticityError, 5: OverflowError_}
+
+
+class CircuitInfo(ctypes.Structure):
+    _fields_ = [
+        ("k", ctypes.c_int32),
+        ("n_layers", ctypes.c_uint32),
+        ("n_in", ctypes.c_uint64),
+        ("n_out", ctypes.c_uint64),
+        ("cts", ctypes.c_uint64),
+        ("gates", ctypes.c_uint64),
+        ("wires", ctypes.c_uint64),
+        ("sign_t", ctypes.c_uint32),
+        ("radices", ctypes.c_uint16 * 32),
+        ("relu_elements", ctypes.c_uint64),
+        ("linear_macs", ctypes.c_uint64),
+        ("act_uc_cts", ctypes.c_uint64),
+        ("max_slots", ctypes.c_uint32),
+    ]
+
+
+class Timing(ctypes.Structure):
+    _fields_ = [
+        ("ms_garble", ctypes.c_double),
+        ("ms_encode", ctypes.c_double),
+        ("ms_evaluate", ctypes.c_double),
+        ("ms_decode", ctypes.c_double),
+        ("ms_total", ctypes.c_double),
+        ("h2d_bytes", ctypes.c_uint64),
+        ("d2h_bytes", ctypes.c_uint64),
+        ("sub_batches", ctypes.c_uint32),
+    ]
+
+
+KERNEL_KINDS = ["act_garble", "act_eval", "linear", "priv_garble", "priv_eval", "setup", "encode", "decode", "misc"]
+
+
+def _declare(L):
+    L.dashgpu_last_error.restype = ctypes.c_char_p
+    L.dashgpu_init.argtypes = [ctypes.c_int]
+    L.dashgpu_set_stream.argtypes = [vp]
+    L.dashgpu_circuit_create.argtypes = [vp, ctypes.POINTER(vp)]
+    L.dashgpu_circuit_destroy.argtypes = [vp]
+    L.dashgpu_circuit_info_get.argtypes = [vp, ctypes.POINTER(CircuitInfo)]
+    L.dashgpu_model_build.argtypes = [ctypes.c_char_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(vp)]
+    L.dashgpu_circuit_desc_view.argtypes = [vp, ctypes.POINTER(CircuitDesc)]
+    L.dashgpu_random_input.argtypes = [vp, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, i64p]
+    L.dashgpu_plain_forward.argtypes = [vp, i64p, i64p]
+    L.dashgpu_garble.argtypes = [vp, u8p, ctypes.c_uint32, ctypes.POINTER(vp)]
+    L.dashgpu_network_destroy.argtypes = [vp]
+    L.dashgpu_garble_inputs.argtypes = [vp, i64p, ctypes.POINTER(vp)]
+    L.dashgpu_evaluate.argtypes = [vp, vp, ctypes.POINTER(vp)]
+    L.dashgpu_decode_outputs.argtypes = [vp, vp, i64p]
+    L.dashgpu_bundle_destroy.argtypes = [vp]
+    for n in ("dashgpu_export_gc", "dashgpu_export_encoding", "dashgpu_export_decoding", "dashgpu_export_bundle"):
+        getattr(L, n).argtypes = [vp, ctypes.c_uint32, u8p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    L.dashgpu_import_bundle.argtypes = [vp, u8p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(vp)]
+    L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
+    L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
+    L.dashgpu_profile.argtypes = [ctypes.c_int]
+    L.dashgpu_profile_read.argtypes = [f64p, u64p, ctypes.c_int]
+    L.dashgpu_prim.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u64p, u64p, u16p, u8p,
+                               u64p, ctypes.c_uint64]
+
+
+class Dash:
+    """Handle to the device engine (one CUDA device)."""
+
+    def __init__(self, device: int = 0, lib_path: Optional[str] = None):
+        path = lib_path or LIB_PATH
+        if not os.path.exists(path):
+            raise CudaError(f"{path} is not built; run __graft_entry__.build()")
+        self.lib = ctypes.CDLL(path)
+        _declare(self.lib)
+        self._check(self.lib.dashgpu_init(device))
+
+    def _check(self, rc: int):
+        if rc:
+            raise _CODES.get(rc, Error)(self.lib.dashgpu_last_error().decode())
+
+    def set_stream(self, stream_ptr: int):
+        self.lib.dashgpu_set_stream(vp(stream_ptr))
+
+    # ---- circuits ----
+    def circuit(self, c: Circuit) -> "GpuCircuit":
+        desc = c.to_desc()
+        h = vp()
+        self._check(self.lib.dashgpu_circuit_create(ctypes.byref(desc), ctypes.byref(h)))
+        return GpuCircuit(self, h)
+
+    def model(self, name: str, seed: int, k: int = 8, private: bool = False) -> "GpuCircuit":
+        h = vp()
+        self._check(self.lib.dashgpu_model_build(name.encode(), seed, k, 1 if private else 0, ctypes.byref(h)))
+        return GpuCircuit(self, h)
+
+    # ---- whole-network API (garble.hpp:93-112), batched ----
+    def garble(self, c: "GpuCircuit", seeds: bytes) -> "GarbledNetwork":
+        if len(seeds) == 0 or len(seeds) % 16:
+            raise DataError("seeds must be a non-empty multiple of 16 bytes")
+        h = vp()
+        buf = (ctypes.c_uint8 * len(seeds)).from_buffer_copy(seeds)
+        self._check(self.lib.dashgpu_garble(c.h, buf, len(seeds) // 16, ctypes.byref(h)))
+        return GarbledNetwork(self, h, c, len(seeds) // 16)
+
+    def garble_inputs(self, net: "GarbledNetwork", values) -> "Bundle":
+        v = np.ascontiguousarray(values, np.int64).reshape(net.batch, net.circuit.info.n_in)
+        h = vp()
+        self._check(self.lib.dashgpu_garble_inputs(net.h, v.ctypes.data_as(i64p), ctypes.byref(h)))
+        return Bundle(self, h, net, False)
+
+    def evaluate(self, net: "GarbledNetwork", inputs: "Bundle") -> "Bundle":
+        h = vp()
+        self._check(self.lib.dashgpu_evaluate(net.h, inputs.h, ctypes.byref(h)))
+        return Bundle(self, h, net, True)
+
+    def decode_outputs(self, net: "GarbledNetwork", outputs: "Bundle") -> np.ndarray:
+        out = np.zeros((net.batch, net.circuit.info.n_out), np.int64)
+        self._check(self.lib.dashgpu_decode_outputs(net.h, outputs.h, out.ctypes.data_as(i64p)))
+        return out
+
+    def import_bundle(self, net: "GarbledNetwork", payload: bytes, output: bool) -> "Bundle":
+        h = vp()
+        buf = (ctypes.c_uint8 * len(payload)).from_buffer_copy(payload)
+        self._check(self.lib.dashgpu_import_bundle(net.h, buf, len(payload), 1 if output else 0, ctypes.byref(h)))
+        return Bundle(self, h, net, output)
+
+    def infer(self, c: "GpuCircuit", seeds, inputs, outputs=None, on_device: bool = False):
+        """garble + garble_inputs + evaluate + decode_outputs for every inference.
+
+        Host mode: seeds bytes / numpy inputs.  Device mode: pass raw device
+        pointers (ints) for seeds, inputs and outputs."""
+        t = Timing()
+        if on_device:
+            batch = outputs[1]
+            self._check(self.lib.dashgpu_infer(c.h, vp(seeds), batch, vp(inputs), vp(outputs[0]), 1, ctypes.byref(t)))
+            return None, t
+        batch = len(seeds) // 16
+        sbuf = (ctypes.c_uint8 * len(seeds)).from_buffer_copy(seeds)
+        x = np.ascontiguousarray(inputs, np.int64).reshape(batch, c.info.n_in)
+        out = np.zeros((batch, c.info.n_out), np.int64)
+        self._check(self.lib.dashgpu_infer(c.h, ctypes.cast(sbuf, vp), batch, vp(x.ctypes.data),
+                                           vp(out.ctypes.data), 0, ctypes.byref(t)))
+        return out, t
+
+    # ---- profiling ----
+    def profile(self, enable: bool):
+        self._check(self.lib.dashgpu_profile(1 if enable else 0))
+
+    def profile_read(self):
+        ms = (ctypes.c_double * 16)()
+        n = (ctypes.c_uint64 * 16)()
+        k = self.lib.dashgpu_profile_read(ms, n, 16)
+        return {KERNEL_KINDS[i]: (ms[i], int(n[i])) for i in range(max(k, 0))}
+
+    # ---- primitives (parity tests) ----
+    def prim(self, op: int, m: int, q: int = 0, inp=None, out=None, key: bytes = None, wires=None, gate: int = 0,
+             n: int = None):
+        n = n if n is not None else (len(inp) if inp is not None else len(wires))
+        ia = np.zeros((n, 2), np.uint64) if inp is None else np.ascontiguousarray(inp, np.uint64).reshape(n, 2)
+        oa = np.zeros((n, 2), np.uint64) if out is None else np.ascontiguousarray(out, np.uint64).reshape(n, 2).copy()
+        dg = np.zeros((n, 128), np.uint16)
+        kb = (ctypes.c_uint8 * 16)(*key) if key is not None else None
+        wa = None if wires is None else np.ascontiguousarray(wires, np.uint64)
+        self._check(self.lib.dashgpu_prim(op, n, m, q, ia.ctypes.data_as(u64p), oa.ctypes.data_as(u64p),
+                                          dg.ctypes.data_as(u16p), kb,
+                                          None if wa is None else wa.ctypes.data_as(u64p), gate))
+        return oa, dg
+
+
+class GpuCircuit:
+    def __init__(self, eng: Dash, h):
+        self.eng, self.h = eng, h
+        self.info = CircuitInfo()
+        eng._check(eng.lib.dashgpu_circuit_info_get(h, ctypes.byref(self.info)))
+
+    def __del__(self):
+        try:
+            self.eng.lib.dashgpu_circuit_destroy(self.h)
+        except Exception:
+            pass
+
+    def to_circuit(self) -> Circuit:
+        d = CircuitDesc()
+        self.eng._check(self.eng.lib.dashgpu_circuit_desc_view(self.h, ctypes.byref(d)))
+        return Circuit.from_desc(d)
+
+    def random_input(self, seed: int, lo: int = -7, hi: int = 7) -> np.ndarray:
+        out = np.zeros(self.info.n_in, np.int64)
+        self.eng._check(self.eng.lib.dashgpu_random_input(self.h, seed, lo, hi, out.ctypes.data_as(i64p)))
+        return out
+
+    def plain_forward(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.int64)
+        out = np.zeros(self.info.n_out, np.int64)
+        self.eng._check(self.eng.lib.dashgpu_plain_forward(self.h, x.ctypes.data_as(i64p), out.ctypes.data_as(i64p)))
+        return out
+
+    @property
+    def radices(self):
+        return list(self.info.radices[: self.info.sign_t])
+
+
+class GarbledNetwork:
+    def __init__(self, eng: Dash, h, circuit: GpuCircuit, batch: int):
+        self.eng, self.h, self.circuit, self.batch = eng, h, circuit, batch
+
+    def __del__(self):
+        try:
+            self.eng.lib.dashgpu_network_destroy(self.h)
+        except Exception:
+            pass
+
+    def _export(self, fn, b: int) -> bytes:
+        n = ctypes.c_size_t()
+        self.eng._check(fn(self.h, b, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_uint8 * n.value)()
+        self.eng._check(fn(self.h, b, buf, n.value, ctypes.byref(n)))
+        return bytes(buf)
+
+    def export_gc(self, b: int = 0) -> bytes:
+        """serialize_garbled_circuit (garble.cpp:347-370) of inference b."""
+        return self._export(self.eng.lib.dashgpu_export_gc, b)
+
+    def export_encoding(self, b: int = 0) -> bytes:
+        return self._export(self.eng.lib.dashgpu_export_encoding, b)
+
+    def export_decoding(self, b: int = 0) -> bytes:
+        return self._export(self.eng.lib.dashgpu_export_decoding, b)
+
+    def tamper(self, b: int, index: int, mask: bytes):
+        self.eng._check(self.eng.lib.dashgpu_tamper_ct(self.h, b, index, (ctypes.c_uint8 * 16)(*mask)))
+
+
+class Bundle:
+    def __init__(self, eng: Dash, h, net: GarbledNetwork, output: bool):
+        self.eng, self.h, self.net, self.output = eng, h, net, output
+
+    def __del__(self):
+        try:
+            self.eng.lib.dashgpu_bundle_destroy(self.h)
+        except Exception:
+            pass
+
+    def payload(self, b: int = 0) -> bytes:
+        """bundle_payload (garble.cpp:465-472) of inference b."""
+        fn = self.eng.lib.dashgpu_export_bundle
+        n = ctypes.c_size_t()
+        self.eng._check(fn(self.h, b, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_uint8 * n.value)()
+        self.eng._check(fn(self.h, b, buf, n.value, ctypes.byref(n)))
+        return bytes(buf)

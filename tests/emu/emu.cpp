@@ -1,0 +1,130 @@
+// TEST INFRASTRUCTURE ONLY — CPU emulation of the device side of libdashgpu.
+//
+// Compiles the *same* per-thread kernel logic (dash_device.cuh,
+// dash_layers.cuh, dash_prim.cuh) with g++ and runs every "launch" as a host
+// loop over the grid, so kernel logic can be debugged against the oracle on a
+// machine without a GPU.  Linked with engine.cpp into tests/emu/libdashemu.so.
+// The product package never loads this library; on a GPU box the tests run
+// the real CUDA library (paper_2302_06361_b200/libdashgpu.so).
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+
+#include "dash_common.hpp"
+
+namespace dashgpu {
+ModC c_mod[MAXMOD + 1];
+uint32_t c_pi_rk[44];
+uint16_t c_modslot[MAXMOD + 1];
+}  // namespace dashgpu
+#define DASH_CONST_DEFINED 1
+#include "dash_prim.cuh"
+
+namespace dashgpu {
+
+static uint32_t g_T[256 * 32];
+
+static AesTab tab() { return AesTab{g_T, 0}; }
+
+namespace dev {
+void set_device(int) {}
+int backend() { return 2; }
+void* alloc(size_t n) {
+    void* p = std::calloc(1, n ? n : 16);
+    if (!p) throw std::runtime_error("emu alloc failed");
+    return p;
+}
+void release(void* p) { std::free(p); }
+void* host_alloc(size_t n) { return alloc(n); }
+void host_release(void* p) { std::free(p); }
+void h2d(void* d, const void* s, size_t n, void*) { std::memcpy(d, s, n); }
+void d2h(void* d, const void* s, size_t n, void*) { std::memcpy(d, s, n); }
+void d2d(void* d, const void* s, size_t n, void*) { std::memmove(d, s, n); }
+void memset0(void* p, size_t n, void*) { std::memset(p, 0, n); }
+void sync(void*) {}
+void check() {}
+size_t free_bytes() { return (size_t)8 << 30; }
+void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot, const uint32_t* T0) {
+    std::memcpy(c_mod, mods, sizeof(ModC) * (MAXMOD + 1));
+    std::memcpy(c_pi_rk, pi_rk, sizeof(uint32_t) * 44);
+    std::memcpy(c_modslot, modslot, sizeof(uint16_t) * (MAXMOD + 1));
+    for (int i = 0; i < 256 * 32; ++i) g_T[i] = T0[i >> 5];
+}
+void prof_enable(int) {}
+void prof_reset() {}
+int prof_read(double*, uint64_t*, int) { return 0; }
+}  // namespace dev
+
+void launch_act(const ActParams& P, bool garble, int nslots, void*) {
+    (void)nslots;
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+    for (int64_t b = 0; b < (int64_t)P.B; ++b)
+        for (int64_t u = 0; u < (int64_t)P.E; ++u) {
+            U4 slots[MAXSLOTS];
+            Elt e;
+            e.b = (uint32_t)b;
+            e.u = (uint32_t)u;
+            e.slots = slots;
+            e.sstride = 1;
+            e.t = tab();
+            e.rk = nullptr;
+            e.mult = nullptr;
+            if (garble) act_element<true>(P, e);
+            else act_element<false>(P, e);
+        }
+}
+
+void launch_linear(const LinParams& L, void*) {
+#pragma omp parallel for collapse(3)
+    for (int64_t b = 0; b < (int64_t)L.B; ++b)
+        for (int64_t w = 0; w < (int64_t)L.nw; ++w)
+            for (int64_t u = 0; u < (int64_t)L.M; ++u) linear_thread(L, (uint32_t)b, (uint32_t)w, (uint32_t)u);
+}
+
+void launch_private(const PrivParams& P, void*) {
+#pragma omp parallel for collapse(2)
+    for (int64_t b = 0; b < (int64_t)P.B; ++b)
+        for (int64_t u = 0; u < (int64_t)P.M; ++u) private_thread(P, (uint32_t)b, (uint32_t)u, tab());
+}
+
+void launch_setup(const SetupParams& S, void*) {
+    for (uint32_t b = 0; b < S.B; ++b)
+        for (uint32_t si = 0; si < S.nslot; ++si) setup_offsets_thread(S, b, si, tab());
+#pragma omp parallel for collapse(2)
+    for (int64_t b = 0; b < (int64_t)S.B; ++b)
+        for (int64_t e = 0; e <= (int64_t)S.n_in; ++e)
+            for (int i = 0; i < S.k; ++i) setup_labels_thread(S, (uint32_t)b, (uint32_t)e, i, tab());
+}
+
+void launch_encode(const EncodeParams& P, void*) {
+    for (uint32_t b = 0; b < P.B; ++b)
+        for (uint32_t e = 0; e < P.n_in; ++e)
+            for (int i = 0; i < P.k; ++i) encode_thread(P, b, e, i);
+}
+
+void launch_dectable(const DecodeParams& P, void*) {
+    for (uint32_t b = 0; b < P.B; ++b)
+        for (uint32_t e = 0; e < P.n_out; ++e)
+            for (int i = 0; i < P.k; ++i) dectable_thread(P, b, e, i);
+}
+
+void launch_decode(const DecodeParams& P, void*) {
+    for (uint32_t b = 0; b < P.B; ++b)
+        for (uint32_t e = 0; e < P.n_out; ++e) decode_thread(P, b, e);
+}
+
+void launch_compress(const CompressParams& P, void*) {
+    for (uint32_t b = 0; b < P.B; ++b)
+        for (uint32_t e = 0; e < P.n; ++e) compress_thread(P, b, e);
+}
+
+void launch_decompress(const CompressParams& P, uint32_t* lane_out, void*) {
+    for (uint32_t b = 0; b < P.B; ++b)
+        for (uint32_t e = 0; e < P.n; ++e) decompress_thread(P, b, e, lane_out);
+}
+
+void launch_prim(const PrimParams& P, void*) {
+    for (uint32_t i = 0; i < P.n; ++i) prim_thread(P, i, tab());
+}
+
+}  // namespace dashgpu
