@@ -1,0 +1,341 @@
+#!/usr/bin/env python3
+"""Benchmark: garbled inferences/s (garble + garble_inputs + evaluate + decode).
+
+Workload (BASELINE.json configs[1]): LeNet-5 restated in reference ops on
+synthetic 28x28 inputs, batch 64 per GPU, k = 8 CRT primes, one fresh seed per
+inference per step (garbled circuits are single-use).  A step garbles,
+encodes, evaluates and decodes the whole batch; the per-step garbled tables
+(8 GB at batch 64) are far larger than L2, so no explicit flush is needed.
+
+  value   inputs (seeds + quantized inputs) already in HBM, outputs left in HBM,
+          CUDA events on the stream the library launches on, max over ranks.
+  e2e     the same metric through the C-ABI call dashgpu_infer with HOST
+          buffers: H2D of seeds + inputs and D2H of the decoded outputs inside
+          the timed region.
+  --impl reference: the reference's own CPU implementation (oracle/_ref, the
+          unmodified dash_core sources) on the host cores, rank 0 only.
+
+Multi-GPU (torchrun): inferences are sharded across ranks (weak scaling), the
+decoded outputs are all-gathered over NCCL once per step.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODEL, SEED, K = "lenet5", 2001, 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--model", default=MODEL)
+    ap.add_argument("--k", type=int, default=K)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="inferences in the CPU-baseline sample")
+    return ap.parse_args()
+
+
+def seeds_for(step, rank, batch):
+    # hex(0x5eed0000 + global index), big-endian 16 bytes (seed_from_string)
+    base = (step * 4096 + rank) * batch
+    return b"".join(int(0x5EED0000 + base + b).to_bytes(16, "big") for b in range(batch))
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline(circuit_desc_c, n_in, n_out, sample):
+    """Reference CPU path (oracle/_ref) on the host cores, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    cores = os.cpu_count() or 1
+    if pyoracle.have_ref():
+        R = pyoracle.RefLib()
+        kind = "reference"
+        ch = R.circuit(circuit_desc_c)
+        seeds = b"".join(int(0x5EED0000 + b).to_bytes(16, "big") for b in range(sample))
+        rng = np.random.default_rng(7)
+        x = rng.integers(-7, 8, size=(sample, n_in)).astype(np.int64)
+        best = None
+        for mode in (1, 0):  # inference-parallel, then intra-layer OpenMP
+            sec, _ = R.bench_infer(ch, seeds, x, mode, cores)
+            v = sample / sec
+            if best is None or v > best[0]:
+                best = (v, mode, sec)
+        return {"value": best[0], "unit": "inferences/s", "cores": cores, "kind": kind,
+                "sample": f"{sample} {MODEL_NAME[0]} inferences (garble+garble_inputs+evaluate+decode_outputs), "
+                          f"{'inference-parallel' if best[1] == 1 else 'OpenMP intra-layer'} on {cores} threads, "
+                          f"{best[2]:.1f} s"}
+    O = pyoracle.Oracle()
+    ch = O.circuit(circuit_desc_c)
+    seeds = b"".join(int(0x5EED0000 + b).to_bytes(16, "big") for b in range(sample))
+    x = np.random.default_rng(7).integers(-7, 8, size=(sample, n_in)).astype(np.int64)
+    sec, _ = O.bench_infer(ch, seeds, x, cores)
+    return {"value": sample / sec, "unit": "inferences/s", "cores": cores, "kind": "port",
+            "sample": f"{sample} inferences, C oracle port, inference-parallel on {cores} threads, {sec:.1f} s"}
+
+
+MODEL_NAME = [MODEL]
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation, rank 0 only."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    from paper_2302_06361_b200.circuit import Circuit
+    from paper_2302_06361_b200 import models
+
+    c = models.build(args.model, SEED, args.k)
+    cores = os.cpu_count() or 1
+    n_in = c.n_in
+    per_step = max(1, min(args.batch, cores))
+    if pyoracle.have_ref():
+        R = pyoracle.RefLib()
+        ch = R.circuit(c)
+        kind = "reference"
+
+        def step(i):
+            seeds = b"".join(int(0x5EED0000 + i * per_step + b).to_bytes(16, "big") for b in range(per_step))
+            x = np.random.default_rng(i).integers(-7, 8, size=(per_step, n_in)).astype(np.int64)
+            return R.bench_infer(ch, seeds, x, 1, cores)[0]
+    else:
+        O = pyoracle.Oracle()
+        ch = O.circuit(c)
+        kind = "port"
+
+        def step(i):
+            seeds = b"".join(int(0x5EED0000 + i * per_step + b).to_bytes(16, "big") for b in range(per_step))
+            x = np.random.default_rng(i).integers(-7, 8, size=(per_step, n_in)).astype(np.int64)
+            return O.bench_infer(ch, seeds, x, cores)[0]
+    for i in range(args.warmup):
+        step(i)
+    total = 0.0
+    for i in range(args.steps):
+        total += step(args.warmup + i)
+    value = per_step * args.steps / total
+    line = {"metric": "garbled inferences/sec (garble+eval)", "value": value, "unit": "inferences/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"{args.model} k={args.k}, reference CPU path, {per_step} inferences per step "
+                                   f"(one per core, inference-parallel)", "global_batch": per_step,
+                       "inferences_per_gpu": per_step},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "inferences/s", "cores": cores, "kind": kind,
+                             "sample": f"{per_step} inferences per step x {args.steps} steps"},
+            "e2e": {"value": value, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    MODEL_NAME[0] = args.model
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_06361_b200.engine import Dash
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    eng = Dash(local)
+    eng.set_stream(stream.cuda_stream)
+    g = eng.model(args.model, SEED, args.k)
+    info = g.info
+    B = args.batch
+    n_in, n_out = info.n_in, info.n_out
+    rng = np.random.default_rng(1234 + rank)
+    host_x = rng.integers(-7, 8, size=(B, n_in)).astype(np.int64)
+    dev_x = torch.from_numpy(host_x).cuda()
+    dev_out = torch.zeros((B, n_out), dtype=torch.int64, device="cuda")
+    steps_seeds = [seeds_for(s, rank, B) for s in range(args.warmup + args.steps)]
+    dev_seeds = [torch.frombuffer(bytearray(s), dtype=torch.uint8).cuda() for s in steps_seeds]
+    gathered = torch.zeros((world * B, n_out), dtype=torch.int64, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step_device(i):
+        eng.infer(g, dev_seeds[i].data_ptr(), dev_x.data_ptr(), (dev_out.data_ptr(), B), on_device=True)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, dev_out)
+
+    # ---- value: HBM-resident inputs ----
+    for i in range(args.warmup):
+        step_device(i)
+    barrier()
+    eng.profile(True)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record(stream)
+        for i in range(args.steps):
+            step_device(args.warmup + i)
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end)
+    prof = eng.profile_read()
+    eng.profile(False)
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * B * args.steps / (ms / 1e3)
+
+    # ---- e2e: host buffers through the C ABI (dashgpu_infer) ----
+    out_host = None
+    h2d = d2h = 0
+    barrier()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for i in range(args.steps):
+        out_host, tm = eng.infer(g, steps_seeds[args.warmup + i], host_x)
+        h2d, d2h = tm.h2d_bytes, tm.d2h_bytes
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, torch.from_numpy(out_host).cuda())
+    e_end.record(stream)
+    barrier()
+    ems = e_start.elapsed_time(e_end)
+    t = torch.tensor([ems], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ems = float(t.item())
+    e2e = world * B * args.steps / (ems / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (activation garbling) ----
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback"
+    if os.path.exists(peaks_path):
+        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured"
+    sum_n = sum(n for n in [128, 80, 55, 45, 37, 34, 31, 30, 28, 26, 25, 24, 23, 23, 23, 22][: args.k])
+    act_ms, act_n = prof.get("act_garble", (0.0, 0))
+    bytes_per_elem = 16 * info.act_uc_cts + 2 * sum_n  # table writes + label bundle read/write (u8)
+    elems_per_launch = (info.relu_elements * B) / max(1, act_n / max(1, args.steps)) if act_n else 0
+    achieved = (bytes_per_elem * elems_per_launch) / ((act_ms / act_n) / 1e3) / 1e9 if act_n else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "act_garble_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    launches = sum(v[1] for v in prof.values())
+
+    cpu = None
+    sample = args.cpu_sample or min(B, max(8, os.cpu_count() or 8))
+    try:
+        cpu = cpu_baseline(g.to_circuit(), n_in, n_out, sample)
+    except Exception as e:  # the CPU baseline must not hide the GPU line
+        cpu = {"value": None, "unit": "inferences/s", "cores": os.cpu_count(), "kind": "unavailable",
+               "sample": str(e)[:200]}
+
+    line = {
+        "metric": "garbled inferences/sec (garble+eval)",
+        "value": value,
+        "unit": "inferences/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": f"{args.model} (LeNet-5 restated in reference ops) k={args.k}, synthetic 1x28x28 "
+                               f"inputs U[-7,7], batch {B} per GPU, fresh seed per inference per step",
+                   "global_batch": world * B, "inferences_per_gpu": B, "parallelism": f"inference-sharded x{world}",
+                   "l2": "per-step garbled tables (%.1f GB) exceed L2; no flush needed" % (info.cts * 16 * B / 1e9),
+                   "ciphertexts_per_inference": info.cts, "relu_elements_per_inference": info.relu_elements},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "kernel": "act_kernel<garble> (ReLU gadget tape)", "peak_source": peak_src,
+                     "bytes_per_element": bytes_per_elem,
+                     "kernel_ms_per_step": act_ms / args.steps,
+                     "kernel_share_of_step": (act_ms / args.steps) / (ms / args.steps)},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": "inferences/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

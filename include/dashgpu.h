@@ -59,7 +59,8 @@ typedef struct dashgpu_circuit_info {
     uint16_t radices[32];
     uint64_t relu_elements;          /* activation elements per inference */
     uint64_t linear_macs;            /* digit multiply-accumulates per inference and pass */
-    uint64_t act_uc_cts;             /* ciphertexts per activation element */
+    uint64_t act_uc_cts;             /* ciphertexts per ReLU element (garbler writes) */
+    uint64_t act_eval_rows;          /* ciphertext rows one ReLU evaluation reads */
     uint32_t max_slots;
 } dashgpu_circuit_info;
 

@@ -42,9 +42,6 @@ extern DASH_CONST uint32_t c_pi_rk[44];           // all-zero-key AES schedule
 extern DASH_CONST uint16_t c_modslot[MAXMOD + 1];  // modulus -> mult-table slot
 #endif
 
-struct Lab {
-    uint32_t w[NWMAX];
-};
 
 struct U4 {
     uint32_t x[4];
@@ -54,12 +51,38 @@ struct U4 {
 // T0[x] = (2S, S, S, 3S) as little-endian bytes; T1..T3 are byte rotations.
 // The table is replicated 32x in shared memory (entry x of lane l at
 // T[x*32 + l]) so the 32 lanes of a warp never bank-conflict.
+#if defined(__CUDACC__)
+// The replicated T-table lives at a link-time-constant shared address, so a
+// lookup is SHF + LOP3 (byte -> row offset | lane*4) + LDS [R + imm].
+__shared__ uint32_t s_T[256 * 32];
+#endif
+
 struct AesTab {
-    const uint32_t* T;
-    uint32_t lane;
+    const uint32_t* T;  // host emulation only
+    uint32_t l4;        // 4 * lane
 };
 
-DASH_HD uint32_t tl(const AesTab& t, uint32_t x) { return t.T[(x << 5) | t.lane]; }
+DASH_HD AesTab make_tab(const uint32_t* T, uint32_t lane) {
+    AesTab t;
+    t.T = T;
+    t.l4 = 4u * lane;
+    return t;
+}
+
+// Entry at byte offset `off` = x * 128 + 4 * lane (x = table index).
+DASH_HD uint32_t tlo(const AesTab& t, uint32_t off) {
+#if defined(__CUDA_ARCH__)
+    (void)t;
+    return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(s_T) + off);
+#else
+    return t.T[off >> 2];
+#endif
+}
+
+#define ob0(s) ((((s) << 7) & 0x7F80u) | t.l4)
+#define ob1(s) ((((s) >> 1) & 0x7F80u) | t.l4)
+#define ob2(s) ((((s) >> 9) & 0x7F80u) | t.l4)
+#define ob3(s) ((((s) >> 17) & 0x7F80u) | t.l4)
 
 template <class RK>
 DASH_HD U4 aes_core(U4 s, const RK& rk, const AesTab& t) {
@@ -68,35 +91,33 @@ DASH_HD U4 aes_core(U4 s, const RK& rk, const AesTab& t) {
 #pragma unroll
 #endif
     for (int r = 1; r < 10; ++r) {
-        const uint32_t t0 = tl(t, s0 & 0xff) ^ rotl32(tl(t, (s1 >> 8) & 0xff), 8) ^
-                            rotl32(tl(t, (s2 >> 16) & 0xff), 16) ^ rotl32(tl(t, s3 >> 24), 24) ^ rk(4 * r);
-        const uint32_t t1 = tl(t, s1 & 0xff) ^ rotl32(tl(t, (s2 >> 8) & 0xff), 8) ^
-                            rotl32(tl(t, (s3 >> 16) & 0xff), 16) ^ rotl32(tl(t, s0 >> 24), 24) ^
-                            rk(4 * r + 1);
-        const uint32_t t2 = tl(t, s2 & 0xff) ^ rotl32(tl(t, (s3 >> 8) & 0xff), 8) ^
-                            rotl32(tl(t, (s0 >> 16) & 0xff), 16) ^ rotl32(tl(t, s1 >> 24), 24) ^
-                            rk(4 * r + 2);
-        const uint32_t t3 = tl(t, s3 & 0xff) ^ rotl32(tl(t, (s0 >> 8) & 0xff), 8) ^
-                            rotl32(tl(t, (s1 >> 16) & 0xff), 16) ^ rotl32(tl(t, s2 >> 24), 24) ^
-                            rk(4 * r + 3);
+        const uint32_t t0 = tlo(t, ob0(s0)) ^ rotl32(tlo(t, ob1(s1)), 8) ^ rotl32(tlo(t, ob2(s2)), 16) ^
+                            rotl32(tlo(t, ob3(s3)), 24) ^ rk(4 * r);
+        const uint32_t t1 = tlo(t, ob0(s1)) ^ rotl32(tlo(t, ob1(s2)), 8) ^ rotl32(tlo(t, ob2(s3)), 16) ^
+                            rotl32(tlo(t, ob3(s0)), 24) ^ rk(4 * r + 1);
+        const uint32_t t2 = tlo(t, ob0(s2)) ^ rotl32(tlo(t, ob1(s3)), 8) ^ rotl32(tlo(t, ob2(s0)), 16) ^
+                            rotl32(tlo(t, ob3(s1)), 24) ^ rk(4 * r + 2);
+        const uint32_t t3 = tlo(t, ob0(s3)) ^ rotl32(tlo(t, ob1(s0)), 8) ^ rotl32(tlo(t, ob2(s1)), 16) ^
+                            rotl32(tlo(t, ob3(s2)), 24) ^ rk(4 * r + 3);
         s0 = t0;
         s1 = t1;
         s2 = t2;
         s3 = t3;
     }
-#define DASH_SB(v) ((tl(t, (v)) >> 8) & 0xff)
+    // last round: S-box = byte 1 of T0 (no MixColumns)
+#define DASH_SB(o) ((tlo(t, (o)) >> 8) & 0xffu)
     U4 o;
-    o.x[0] = (DASH_SB(s0 & 0xff) | (DASH_SB((s1 >> 8) & 0xff) << 8) | (DASH_SB((s2 >> 16) & 0xff) << 16) |
-              (DASH_SB(s3 >> 24) << 24)) ^ rk(40);
-    o.x[1] = (DASH_SB(s1 & 0xff) | (DASH_SB((s2 >> 8) & 0xff) << 8) | (DASH_SB((s3 >> 16) & 0xff) << 16) |
-              (DASH_SB(s0 >> 24) << 24)) ^ rk(41);
-    o.x[2] = (DASH_SB(s2 & 0xff) | (DASH_SB((s3 >> 8) & 0xff) << 8) | (DASH_SB((s0 >> 16) & 0xff) << 16) |
-              (DASH_SB(s1 >> 24) << 24)) ^ rk(42);
-    o.x[3] = (DASH_SB(s3 & 0xff) | (DASH_SB((s0 >> 8) & 0xff) << 8) | (DASH_SB((s1 >> 16) & 0xff) << 16) |
-              (DASH_SB(s2 >> 24) << 24)) ^ rk(43);
+    o.x[0] = (DASH_SB(ob0(s0)) | (DASH_SB(ob1(s1)) << 8) | (DASH_SB(ob2(s2)) << 16) | (DASH_SB(ob3(s3)) << 24)) ^ rk(40);
+    o.x[1] = (DASH_SB(ob0(s1)) | (DASH_SB(ob1(s2)) << 8) | (DASH_SB(ob2(s3)) << 16) | (DASH_SB(ob3(s0)) << 24)) ^ rk(41);
+    o.x[2] = (DASH_SB(ob0(s2)) | (DASH_SB(ob1(s3)) << 8) | (DASH_SB(ob2(s0)) << 16) | (DASH_SB(ob3(s1)) << 24)) ^ rk(42);
+    o.x[3] = (DASH_SB(ob0(s3)) | (DASH_SB(ob1(s0)) << 8) | (DASH_SB(ob2(s1)) << 16) | (DASH_SB(ob3(s2)) << 24)) ^ rk(43);
 #undef DASH_SB
     return o;
 }
+#undef ob0
+#undef ob1
+#undef ob2
+#undef ob3
 
 struct RkConst {
     DASH_HD uint32_t operator()(int i) const { return c_pi_rk[i]; }
@@ -172,49 +193,6 @@ DASH_HD uint32_t split4(uint32_t v, const ModC& M) {
     return d0 | (d1 << 8) | (d2 << 16) | (q3 << 24);
 }
 
-// decompress_mod (label.cpp:228-232): the first n base-m digits of c.
-DASH_HD void decompress(Lab& L, const U4& cin, const ModC& M) {
-    if (M.pow2) {
-        L.w[0] = cin.x[0] & M.bits[0];
-        L.w[1] = cin.x[1] & M.bits[1];
-        L.w[2] = cin.x[2] & M.bits[2];
-        L.w[3] = cin.x[3] & M.bits[3];
-        return;
-    }
-    uint32_t c[4] = {cin.x[0], cin.x[1], cin.x[2], cin.x[3]};
-    uint32_t chunk = 0;
-    int left = 0, j = 0;
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = 0; w < NWMAX; ++w) {
-        if (w < M.nw) {
-            if (left == 0) {
-                chunk = divmod_D(c, M, M.limbs[j]);
-                ++j;
-                left = M.W;
-            }
-            --left;
-            const uint32_t q = fdiv(chunk, M.mag_m4, M.sh_m4);
-            const uint32_t v = chunk - q * M.m4;
-            chunk = q;
-            L.w[w] = split4(v, M);
-        } else {
-            L.w[w] = 0;
-        }
-    }
-    // digits beyond n in the top word must be zero
-    const int extra = M.nw * 4 - M.n;
-    if (extra) {
-        const uint32_t keep = 0xffffffffu >> (8 * extra);
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-        for (int w = 0; w < NWMAX; ++w)
-            if (w == M.nw - 1) L.w[w] &= keep;
-    }
-}
-
 DASH_HD void mul_add_128(uint32_t c[4], uint32_t m, uint32_t add) {
     uint64_t t = (uint64_t)c[0] * m + add;
     c[0] = (uint32_t)t;
@@ -227,34 +205,6 @@ DASH_HD void mul_add_128(uint32_t c[4], uint32_t m, uint32_t add) {
 }
 
 // compress (label.cpp:208-219): Horner, one word (four digits) per step.
-DASH_HD U4 compress(const Lab& L, const ModC& M) {
-    U4 o;
-    if (M.pow2) {
-        o.x[0] = L.w[0];
-        o.x[1] = L.w[1];
-        o.x[2] = L.w[2];
-        o.x[3] = L.w[3];
-        return o;
-    }
-    uint32_t c[4] = {0, 0, 0, 0};
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = NWMAX - 1; w >= 0; --w) {
-        if (w < M.nw) {
-            const uint32_t x = L.w[w];
-            const uint32_t cv = (x & 0xff) + M.m * (((x >> 8) & 0xff) + M.m * (((x >> 16) & 0xff) + M.m * (x >> 24)));
-            mul_add_128(c, M.m4, cv);
-        }
-    }
-    o.x[0] = c[0];
-    o.x[1] = c[1];
-    o.x[2] = c[2];
-    o.x[3] = c[3];
-    return o;
-}
-
-DASH_HD uint32_t color(const Lab& L, const ModC& M) { return M.pow2 ? (L.w[0] & (M.m - 1u)) : (L.w[0] & 0xffu); }
 
 // ---- componentwise arithmetic (label.cpp:144-206) ----
 DASH_HD uint32_t swar_add(uint32_t a, uint32_t b, const ModC& M) {
@@ -294,271 +244,6 @@ DASH_HD void p2_neg(uint32_t a[4], const ModC& M) {
     for (int i = 0; i < 4; ++i) a[i] = n[i];
 }
 
-DASH_HD void lab_add(Lab& a, const Lab& b, const ModC& M) {
-    if (M.pow2) {
-        p2_add(a.w, b.w, M);
-        return;
-    }
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = 0; w < NWMAX; ++w)
-        if (w < M.nw) a.w[w] = swar_add(a.w[w], b.w[w], M);
-}
-
-// a += label stored in global memory (word form)
-DASH_HD void lab_add_g(Lab& a, const uint32_t* g, const ModC& M) {
-    if (M.pow2) {
-        uint32_t b[4] = {g[0], g[1], g[2], g[3]};
-        p2_add(a.w, b, M);
-        return;
-    }
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = 0; w < NWMAX; ++w)
-        if (w < M.nw) a.w[w] = swar_add(a.w[w], g[w], M);
-}
-
-DASH_HD void lab_neg(Lab& a, const ModC& M) {
-    if (M.pow2) {
-        p2_neg(a.w, M);
-        return;
-    }
-    // (m - d) mod m per digit: m - d, then fold m -> 0 via the SWAR add of 0
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = 0; w < NWMAX; ++w)
-        if (w < M.nw) a.w[w] = swar_add(M.spread - a.w[w], 0u, M);
-    const int extra = M.nw * 4 - M.n;
-    if (extra) {
-        const uint32_t keep = 0xffffffffu >> (8 * extra);
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-        for (int w = 0; w < NWMAX; ++w)
-            if (w == M.nw - 1) a.w[w] &= keep;
-    }
-}
-
-DASH_HD void lab_sub(Lab& a, const Lab& b, const ModC& M) {
-    if (M.pow2) {
-        uint32_t n[4] = {b.w[0], b.w[1], b.w[2], b.w[3]};
-        p2_neg(n, M);
-        p2_add(a.w, n, M);
-        return;
-    }
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = 0; w < NWMAX; ++w)
-        if (w < M.nw) a.w[w] = swar_add(a.w[w], M.spread - b.w[w], M);
-    // padding digits: 0 + (m - 0) folds to 0 in swar_add
-}
-
-DASH_HD void lab_sub_g(Lab& a, const uint32_t* g, const ModC& M) {
-    if (M.pow2) {
-        uint32_t n[4] = {g[0], g[1], g[2], g[3]};
-        p2_neg(n, M);
-        p2_add(a.w, n, M);
-        return;
-    }
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = 0; w < NWMAX; ++w)
-        if (w < M.nw) a.w[w] = swar_add(a.w[w], M.spread - g[w], M);
-}
-
-// s*a mod m componentwise, s per lane (label.cpp:167-175)
-DASH_HD void lab_scale(Lab& o, const Lab& a, uint32_t s, const ModC& M) {
-    if (M.pow2) {
-        uint32_t acc[4] = {0, 0, 0, 0};
-        uint32_t x[4] = {a.w[0], a.w[1], a.w[2], a.w[3]};
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-        for (int bit = 0; bit < 7; ++bit) {
-            if ((s >> bit) & 1u) p2_add(acc, x, M);
-            // double each field: shift left, drop bits that crossed a field boundary
-            const uint32_t c0 = x[0] >> 31, c1 = x[1] >> 31, c2 = x[2] >> 31;
-            x[0] = (x[0] << 1) & ~M.lo[0] & M.bits[0];
-            x[1] = ((x[1] << 1) | c0) & ~M.lo[1] & M.bits[1];
-            x[2] = ((x[2] << 1) | c1) & ~M.lo[2] & M.bits[2];
-            x[3] = ((x[3] << 1) | c2) & ~M.lo[3] & M.bits[3];
-        }
-        o.w[0] = acc[0];
-        o.w[1] = acc[1];
-        o.w[2] = acc[2];
-        o.w[3] = acc[3];
-        return;
-    }
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = 0; w < NWMAX; ++w) {
-        if (w < M.nw) {
-            const uint32_t x = a.w[w];
-            uint32_t r = 0;
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t t = ((x >> (8 * j)) & 0xffu) * s;
-                const uint32_t q = fdiv(t, M.mag_m, M.sh_m);
-                r |= (t - q * M.m) << (8 * j);
-            }
-            o.w[w] = r;
-        } else {
-            o.w[w] = 0;
-        }
-    }
-}
-
-DASH_HD void lab_zero(Lab& a) {
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-    for (int w = 0; w < NWMAX; ++w) a.w[w] = 0;
-}
-
-// ---- global label rows: u8 digits, four per word, word stride `stride` ----
-DASH_HD void lab_load_rows(Lab& L, const uint32_t* p, uint64_t stride, const ModC& M) {
-    if (!M.pow2) {
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-        for (int w = 0; w < NWMAX; ++w) L.w[w] = (w < M.nw) ? p[(uint64_t)w * stride] : 0u;
-        return;
-    }
-    uint32_t acc[4] = {0, 0, 0, 0};
-    for (int w = 0; w < M.nw; ++w) {
-        const uint32_t x = p[(uint64_t)w * stride];
-        for (int j = 0; j < 4; ++j) {
-            const int i = 4 * w + j;
-            if (i < M.n) {
-                const uint32_t d = (x >> (8 * j)) & 0xffu;
-                const int pos = M.e * i;
-                const int limb = pos >> 5, off = pos & 31;
-                const uint32_t lo = d << off;
-                const uint32_t hi = off ? (d >> (32 - off)) : 0u;
-                acc[0] |= limb == 0 ? lo : 0u;
-                acc[1] |= limb == 1 ? lo : (limb == 0 ? hi : 0u);
-                acc[2] |= limb == 2 ? lo : (limb == 1 ? hi : 0u);
-                acc[3] |= limb == 3 ? lo : (limb == 2 ? hi : 0u);
-            }
-        }
-    }
-    L.w[0] = acc[0];
-    L.w[1] = acc[1];
-    L.w[2] = acc[2];
-    L.w[3] = acc[3];
-}
-
-DASH_HD void lab_store_rows(const Lab& L, uint32_t* p, uint64_t stride, const ModC& M) {
-    if (!M.pow2) {
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-        for (int w = 0; w < NWMAX; ++w)
-            if (w < M.nw) p[(uint64_t)w * stride] = L.w[w];
-        return;
-    }
-    const uint32_t mask = M.m - 1u;
-    for (int w = 0; w < M.nw; ++w) {
-        uint32_t x = 0;
-        for (int j = 0; j < 4; ++j) {
-            const int i = 4 * w + j;
-            if (i < M.n) {
-                const int pos = M.e * i;
-                const int limb = pos >> 5, off = pos & 31;
-                uint32_t v = L.w[0];
-                v = limb == 1 ? L.w[1] : v;
-                v = limb == 2 ? L.w[2] : v;
-                v = limb == 3 ? L.w[3] : v;
-                uint32_t nx = limb == 0 ? L.w[1] : (limb == 1 ? L.w[2] : (limb == 2 ? L.w[3] : 0u));
-                uint32_t d = (v >> off) | (off ? (nx << (32 - off)) : 0u);
-                x |= (d & mask) << (8 * j);
-            }
-        }
-        p[(uint64_t)w * stride] = x;
-    }
-}
-
-// ---- PRF (prf.cpp:11-27): digit i = (u32 word i of AES_seed(wire|stream<<64|(i/4)<<96)) mod m
-DASH_HD uint32_t mod32(uint32_t x, const ModC& M) {
-    const uint64_t q = umulhi64((uint64_t)x, M.mag64);
-    return x - (uint32_t)q * M.m;
-}
-
-DASH_HD void prf_label(Lab& L, uint64_t wire, uint32_t stream, const ModC& M, const uint32_t* rk, const AesTab& t) {
-    if (!M.pow2) {
-        uint32_t tmp[NWMAX];
-        for (int w = 0; w < M.nw; ++w) {
-            U4 s;
-            s.x[0] = (uint32_t)wire;
-            s.x[1] = (uint32_t)(wire >> 32);
-            s.x[2] = stream;
-            s.x[3] = (uint32_t)w;
-            const U4 o = aes_key(s, rk, t);
-            uint32_t x = 0;
-            for (int j = 0; j < 4; ++j)
-                if (4 * w + j < M.n) x |= mod32(o.x[j], M) << (8 * j);
-            tmp[w] = x;
-        }
-#if defined(__CUDA_ARCH__)
-#pragma unroll
-#endif
-        for (int w = 0; w < NWMAX; ++w) L.w[w] = (w < M.nw) ? tmp[w] : 0u;
-        return;
-    }
-    uint32_t acc[4] = {0, 0, 0, 0};
-    const int nb = (M.n + 3) / 4;
-    const uint32_t mask = M.m - 1u;
-    for (int b = 0; b < nb; ++b) {
-        U4 s;
-        s.x[0] = (uint32_t)wire;
-        s.x[1] = (uint32_t)(wire >> 32);
-        s.x[2] = stream;
-        s.x[3] = (uint32_t)b;
-        const U4 o = aes_key(s, rk, t);
-        for (int j = 0; j < 4; ++j) {
-            const int i = 4 * b + j;
-            if (i < M.n) {
-                const uint32_t d = o.x[j] & mask;
-                const int pos = M.e * i;
-                const int limb = pos >> 5, off = pos & 31;
-                const uint32_t lo = d << off;
-                const uint32_t hi = off ? (d >> (32 - off)) : 0u;
-                acc[0] |= limb == 0 ? lo : 0u;
-                acc[1] |= limb == 1 ? lo : (limb == 0 ? hi : 0u);
-                acc[2] |= limb == 2 ? lo : (limb == 1 ? hi : 0u);
-                acc[3] |= limb == 3 ? lo : (limb == 2 ? hi : 0u);
-            }
-        }
-    }
-    L.w[0] = acc[0] & M.bits[0];
-    L.w[1] = acc[1] & M.bits[1];
-    L.w[2] = acc[2] & M.bits[2];
-    L.w[3] = acc[3] & M.bits[3];
-}
-
-// ---- row encryption (cipher.cpp:27-43) ----
-// ct = compress(payload + decompress_mod(H, q))
-DASH_HD U4 enc_with(const U4& H, const Lab& payload, const ModC& Q) {
-    Lab pad;
-    decompress(pad, H, Q);
-    lab_add(pad, payload, Q);
-    return compress(pad, Q);
-}
-// m = decompress_mod(ct, q) - decompress_mod(H, q)
-DASH_HD void dec_with(Lab& out, const U4& ct, const U4& H, const ModC& Q) {
-    Lab pad;
-    decompress(out, ct, Q);
-    decompress(pad, H, Q);
-    lab_sub(out, pad, Q);
-}
 
 DASH_HD uint32_t field_width(uint32_t p) {
     uint32_t w = 0;
@@ -586,6 +271,332 @@ DASH_HD uint32_t u4_shr_low(const U4& a, uint32_t sh) {
     return (v >> off) | (off ? (nx << (32 - off)) : 0u);
 }
 
+
+// ---- PRF (prf.cpp:11-27): digit i = (u32 word i of AES_seed(wire|stream<<64|(i/4)<<96)) mod m
+DASH_HD uint32_t mod32(uint32_t x, const ModC& M) {
+    const uint64_t q = umulhi64((uint64_t)x, M.mag64);
+    return x - (uint32_t)q * M.m;
+}
+
+
+// =================================================== label buffers
+// A label lives in a per-lane buffer: word w at p[w * s].  In the
+// activation kernel the buffers are in shared memory, lane-interleaved
+// (s = 32), so a warp touching word w of its 32 labels hits 32 banks once.
+// Non-power-of-two moduli: u8 digits, four per word (nw words).  Powers of
+// two: the packed-bit form in 4 words, which equals the compressed value.
+// All loops are runtime loops: one compact copy of every routine.
+struct LB {
+    uint32_t* p;
+    uint32_t s;
+    DASH_HD uint32_t& operator[](int w) const { return p[(uint32_t)w * s]; }
+};
+
+DASH_HD int lb_words(const ModC& M) { return M.pow2 ? 4 : M.nw; }
+
+DASH_HD U4 lb_u4(LB a) {
+    U4 r;
+    r.x[0] = a[0];
+    r.x[1] = a[1];
+    r.x[2] = a[2];
+    r.x[3] = a[3];
+    return r;
+}
+DASH_HD void lb_set_u4(LB a, const U4& v) {
+    a[0] = v.x[0];
+    a[1] = v.x[1];
+    a[2] = v.x[2];
+    a[3] = v.x[3];
+}
+
+DASH_HD void lb_copy(LB d, LB s, const ModC& M) {
+    const int n = lb_words(M);
+    for (int w = 0; w < n; ++w) d[w] = s[w];
+}
+
+DASH_HD uint32_t lb_color(LB a, const ModC& M) { return M.pow2 ? (a[0] & (M.m - 1u)) : (a[0] & 0xffu); }
+
+DASH_HD uint32_t top_keep(const ModC& M) {
+    const int extra = M.nw * 4 - M.n;
+    return extra ? (0xffffffffu >> (8 * extra)) : 0xffffffffu;
+}
+
+// digit-wise (x * s) mod m of one word (non-pow2)
+DASH_HD uint32_t scale_word(uint32_t x, uint32_t s, const ModC& M) {
+    uint32_t r = 0;
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t t = ((x >> (8 * j)) & 0xffu) * s;
+        r |= (t - fdiv(t, M.mag_m, M.sh_m) * M.m) << (8 * j);
+    }
+    return r;
+}
+
+DASH_HD U4 p2_scale(U4 x, uint32_t s, const ModC& M) {
+    uint32_t acc[4] = {0, 0, 0, 0};
+    for (int bit = 0; bit < 7; ++bit) {
+        if ((s >> bit) & 1u) p2_add(acc, x.x, M);
+        const uint32_t c0 = x.x[0] >> 31, c1 = x.x[1] >> 31, c2 = x.x[2] >> 31;
+        x.x[0] = (x.x[0] << 1) & ~M.lo[0] & M.bits[0];
+        x.x[1] = ((x.x[1] << 1) | c0) & ~M.lo[1] & M.bits[1];
+        x.x[2] = ((x.x[2] << 1) | c1) & ~M.lo[2] & M.bits[2];
+        x.x[3] = ((x.x[3] << 1) | c2) & ~M.lo[3] & M.bits[3];
+    }
+    U4 r;
+    r.x[0] = acc[0];
+    r.x[1] = acc[1];
+    r.x[2] = acc[2];
+    r.x[3] = acc[3];
+    return r;
+}
+
+DASH_HD U4 p2_sub(U4 a, U4 b, const ModC& M) {
+    p2_neg(b.x, M);
+    p2_add(a.x, b.x, M);
+    return a;
+}
+
+// a += b
+DASH_HD void lb_add(LB a, LB b, const ModC& M) {
+    if (M.pow2) {
+        U4 x = lb_u4(a), y = lb_u4(b);
+        p2_add(x.x, y.x, M);
+        lb_set_u4(a, x);
+        return;
+    }
+    for (int w = 0; w < M.nw; ++w) a[w] = swar_add(a[w], b[w], M);
+}
+// a += g (label words in global memory, same form)
+DASH_HD void lb_add_g(LB a, const uint32_t* g, const ModC& M) {
+    if (M.pow2) {
+        U4 x = lb_u4(a);
+        uint32_t y[4] = {g[0], g[1], g[2], g[3]};
+        p2_add(x.x, y, M);
+        lb_set_u4(a, x);
+        return;
+    }
+    for (int w = 0; w < M.nw; ++w) a[w] = swar_add(a[w], g[w], M);
+}
+DASH_HD void lb_sub(LB a, LB b, const ModC& M) {
+    if (M.pow2) {
+        lb_set_u4(a, p2_sub(lb_u4(a), lb_u4(b), M));
+        return;
+    }
+    for (int w = 0; w < M.nw; ++w) a[w] = swar_add(a[w], M.spread - b[w], M);
+}
+DASH_HD void lb_sub_g(LB a, const uint32_t* g, const ModC& M) {
+    if (M.pow2) {
+        U4 y;
+        y.x[0] = g[0];
+        y.x[1] = g[1];
+        y.x[2] = g[2];
+        y.x[3] = g[3];
+        lb_set_u4(a, p2_sub(lb_u4(a), y, M));
+        return;
+    }
+    for (int w = 0; w < M.nw; ++w) a[w] = swar_add(a[w], M.spread - g[w], M);
+}
+DASH_HD void lb_neg(LB a, const ModC& M) {
+    if (M.pow2) {
+        U4 x = lb_u4(a);
+        p2_neg(x.x, M);
+        lb_set_u4(a, x);
+        return;
+    }
+    for (int w = 0; w < M.nw; ++w) a[w] = swar_add(M.spread - a[w], 0u, M);
+}
+// o = s * a (o may alias a)
+DASH_HD void lb_scale(LB o, LB a, uint32_t s, const ModC& M) {
+    if (M.pow2) {
+        lb_set_u4(o, p2_scale(lb_u4(a), s, M));
+        return;
+    }
+    for (int w = 0; w < M.nw; ++w) o[w] = scale_word(a[w], s, M);
+}
+
+// compress (label.cpp:208-219): Horner in base m^4, one word per step
+DASH_HD U4 lb_compress(LB a, const ModC& M) {
+    if (M.pow2) return lb_u4(a);
+    uint32_t c[4] = {0, 0, 0, 0};
+    for (int w = M.nw - 1; w >= 0; --w) {
+        const uint32_t x = a[w];
+        const uint32_t cv = (x & 0xff) + M.m * (((x >> 8) & 0xff) + M.m * (((x >> 16) & 0xff) + M.m * (x >> 24)));
+        mul_add_128(c, M.m4, cv);
+    }
+    U4 o;
+    o.x[0] = c[0];
+    o.x[1] = c[1];
+    o.x[2] = c[2];
+    o.x[3] = c[3];
+    return o;
+}
+
+// Returns compress(key), then key += R (the per-row key step of every
+// garbling loop: rows a and a+1 use keys in + aR and in + (a+1)R).
+DASH_HD U4 lb_key_step(LB key, const uint32_t* R, const ModC& M) {
+    if (M.pow2) {
+        U4 k = lb_u4(key), r = k;
+        uint32_t y[4] = {R[0], R[1], R[2], R[3]};
+        p2_add(k.x, y, M);
+        lb_set_u4(key, k);
+        return r;
+    }
+    uint32_t c[4] = {0, 0, 0, 0};
+    for (int w = M.nw - 1; w >= 0; --w) {
+        const uint32_t x = key[w];
+        const uint32_t cv = (x & 0xff) + M.m * (((x >> 8) & 0xff) + M.m * (((x >> 16) & 0xff) + M.m * (x >> 24)));
+        mul_add_128(c, M.m4, cv);
+        key[w] = swar_add(x, R[w], M);
+    }
+    U4 o;
+    o.x[0] = c[0];
+    o.x[1] = c[1];
+    o.x[2] = c[2];
+    o.x[3] = c[3];
+    return o;
+}
+
+// Streams the base-m words of decompress_mod(cin, m) (label.cpp:228-232)
+// to f(word_index, packed_digits); digits beyond n are zeroed.
+template <class F>
+DASH_HD void digits_stream(const U4& cin, const ModC& M, F&& f) {
+    uint32_t c[4] = {cin.x[0], cin.x[1], cin.x[2], cin.x[3]};
+    const uint32_t keep = top_keep(M);
+    int w = 0;
+    for (int j = 0; j < M.nchunks; ++j) {
+        uint32_t chunk = divmod_D(c, M, M.limbs[j]);
+        for (int ww = 0; ww < M.W && w < M.nw; ++ww, ++w) {
+            const uint32_t q = fdiv(chunk, M.mag_m4, M.sh_m4);
+            uint32_t v = split4(chunk - q * M.m4, M);
+            chunk = q;
+            if (w == M.nw - 1) v &= keep;
+            f(w, v);
+        }
+    }
+}
+
+DASH_HD void lb_decompress(LB out, const U4& c, const ModC& M) {
+    if (M.pow2) {
+        U4 v;
+        for (int i = 0; i < 4; ++i) v.x[i] = c.x[i] & M.bits[i];
+        lb_set_u4(out, v);
+        return;
+    }
+    digits_stream(c, M, [&](int w, uint32_t v) { out[w] = v; });
+}
+
+// Row encryption (cipher.cpp:27-29 with the payload of gadgets.hpp):
+//   ct = compress(decompress_mod(H, q) + base [+ g] [- s*sub])
+// tmp is scratch (may not alias base/sub).
+DASH_HD U4 lb_enc(const U4& H, LB base, const uint32_t* g, LB* sub, uint32_t s, LB tmp, const ModC& M) {
+    if (M.pow2) {
+        U4 t;
+        for (int i = 0; i < 4; ++i) t.x[i] = H.x[i] & M.bits[i];
+        U4 b = lb_u4(base);
+        p2_add(t.x, b.x, M);
+        if (g) {
+            uint32_t y[4] = {g[0], g[1], g[2], g[3]};
+            p2_add(t.x, y, M);
+        }
+        if (sub) t = p2_sub(t, p2_scale(lb_u4(*sub), s, M), M);
+        return t;
+    }
+    digits_stream(H, M, [&](int w, uint32_t v) {
+        uint32_t t = swar_add(v, base[w], M);
+        if (g) t = swar_add(t, g[w], M);
+        if (sub) t = swar_add(t, M.spread - scale_word((*sub)[w], s, M), M);
+        tmp[w] = t;
+    });
+    return lb_compress(tmp, M);
+}
+
+// Row decryption (cipher.cpp:36-38): out = decompress_mod(ct) - decompress_mod(H)
+DASH_HD void lb_dec(LB out, const U4& ct, const U4& H, const ModC& M) {
+    if (M.pow2) {
+        U4 a, b;
+        for (int i = 0; i < 4; ++i) {
+            a.x[i] = ct.x[i] & M.bits[i];
+            b.x[i] = H.x[i] & M.bits[i];
+        }
+        lb_set_u4(out, p2_sub(a, b, M));
+        return;
+    }
+    lb_decompress(out, ct, M);
+    digits_stream(H, M, [&](int w, uint32_t v) { out[w] = swar_add(out[w], M.spread - v, M); });
+}
+
+// ---- global label rows: u8 digits, four per word, word stride `stride` ----
+DASH_HD void lb_load_rows(LB L, const uint32_t* p, uint64_t stride, const ModC& M) {
+    if (!M.pow2) {
+        for (int w = 0; w < M.nw; ++w) L[w] = p[(uint64_t)w * stride];
+        return;
+    }
+    U4 acc;
+    acc.x[0] = acc.x[1] = acc.x[2] = acc.x[3] = 0;
+    for (int w = 0; w < M.nw; ++w) {
+        const uint32_t x = p[(uint64_t)w * stride];
+        for (int j = 0; j < 4; ++j) {
+            const int i = 4 * w + j;
+            if (i < M.n) {
+                const uint32_t d = (x >> (8 * j)) & 0xffu;
+                u4_or_shl(acc, d, (uint32_t)(M.e * i));
+            }
+        }
+    }
+    lb_set_u4(L, acc);
+}
+
+DASH_HD void lb_store_rows(LB L, uint32_t* p, uint64_t stride, const ModC& M) {
+    if (!M.pow2) {
+        for (int w = 0; w < M.nw; ++w) p[(uint64_t)w * stride] = L[w];
+        return;
+    }
+    const U4 v = lb_u4(L);
+    const uint32_t mask = M.m - 1u;
+    for (int w = 0; w < M.nw; ++w) {
+        uint32_t x = 0;
+        for (int j = 0; j < 4; ++j) {
+            const int i = 4 * w + j;
+            if (i < M.n) x |= (u4_shr_low(v, (uint32_t)(M.e * i)) & mask) << (8 * j);
+        }
+        p[(uint64_t)w * stride] = x;
+    }
+}
+
+// LabelPrf::draw (prf.cpp:11-27): digit i = (u32 word i of
+// AES_seed(wire | stream<<64 | (i/4)<<96)) mod m; one AES block per word.
+DASH_HD void lb_prf(LB L, uint64_t wire, uint32_t stream, const ModC& M, const uint32_t* rk, const AesTab& t) {
+    const int nb = (M.n + 3) / 4;
+    U4 acc;
+    acc.x[0] = acc.x[1] = acc.x[2] = acc.x[3] = 0;
+    const uint32_t mask = M.m - 1u;
+    for (int b = 0; b < nb; ++b) {
+        U4 s;
+        s.x[0] = (uint32_t)wire;
+        s.x[1] = (uint32_t)(wire >> 32);
+        s.x[2] = stream;
+        s.x[3] = (uint32_t)b;
+        const U4 o = aes_key(s, rk, t);
+        if (!M.pow2) {
+            uint32_t x = 0;
+            for (int j = 0; j < 4; ++j)
+                if (4 * b + j < M.n) x |= mod32(o.x[j], M) << (8 * j);
+            L[b] = x;
+        } else {
+            for (int j = 0; j < 4; ++j) {
+                const int i = 4 * b + j;
+                if (i < M.n) u4_or_shl(acc, o.x[j] & mask, (uint32_t)(M.e * i));
+            }
+        }
+    }
+    if (M.pow2) {
+        for (int i = 0; i < 4; ++i) acc.x[i] &= M.bits[i];
+        lb_set_u4(L, acc);
+    }
+}
+
 // ------------------------------------------------------------ element tape
 struct ActParams {
     const TapeOp* tape;
@@ -600,20 +611,23 @@ struct ActParams {
     uint64_t blob_stride;      // ciphertexts between inferences
     const uint32_t* in[MAXK];  // input lane planes [B][nw][E]
     uint32_t* out[MAXK];       // output lane planes [B][nw][E]
-    uint16_t lane_mod[MAXK];
     const uint32_t* rk;        // PRF round keys [B][44] (garble)
-    const uint32_t* mult;      // multiples v*R_m [B][nslot][128][NWMAX] (garble)
+    const uint32_t* mult;      // multiples v*R_m [B][127][128][NWMAX] (garble)
     uint64_t mult_stride;      // words per inference
+    U4* slots;                 // compressed label slots [nslots][B*E]
 };
 
+// Working buffers of one element: X (first operand / key), K (second key),
+// A (fresh / accumulated label), T (scratch).
 struct Elt {
     uint32_t b, u;
     uint64_t gate0, wire0;
     U4* rows;
     const uint32_t* rk;
     const uint32_t* mult;
-    U4* slots;      // slot s at slots[s * sstride]
-    uint32_t sstride;
+    U4* slot0;          // slot s at slot0[s * sstride]
+    uint64_t sstride;
+    LB X, K, A, T;
     AesTab t;
 };
 
@@ -621,18 +635,17 @@ DASH_HD const uint32_t* mult_row(const Elt& e, uint32_t m, uint32_t v) {
     return e.mult + ((uint64_t)c_modslot[m] * 128u + v) * NWMAX;
 }
 
-DASH_HD void load_operand(Lab& L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M) {
+DASH_HD void load_operand(LB L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M) {
     if (v >= IN_LANE) {
         const int lane = v - IN_LANE;
-        const uint32_t* base = P.in[lane] + ((uint64_t)e.b * M.nw) * P.E + e.u;
-        lab_load_rows(L, base, P.E, M);
+        lb_load_rows(L, P.in[lane] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, M);
     } else {
-        decompress(L, e.slots[(uint32_t)v * e.sstride], M);
+        lb_decompress(L, e.slot0[(uint64_t)v * e.sstride], M);
     }
 }
 
-DASH_HD void store_slot(const Elt& e, uint8_t s, const Lab& L, const ModC& M) {
-    e.slots[(uint32_t)s * e.sstride] = compress(L, M);
+DASH_HD void store_slot(const Elt& e, uint8_t s, LB L, const ModC& M) {
+    e.slot0[(uint64_t)s * e.sstride] = lb_compress(L, M);
 }
 
 // ---- garbling of one op (gadgets.hpp) ----
@@ -646,177 +659,107 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const uint64_t g = e.gate0 + op.gate_off;
             const uint8_t* phi = P.phi + op.phi_off;
             U4* R = e.rows + op.ct_off;
-            Lab x;
-            load_operand(x, P, e, op.a, Mp);
-            const uint32_t cin = color(x, Mp);
-            Lab out0;
+            load_operand(e.X, P, e, op.a, Mp);
+            const uint32_t cin = lb_color(e.X, Mp);
             if (op.kind == OP_PROJ) {
-                prf_label(out0, e.wire0 + op.wire_off, 0, Mq, e.rk, e.t);
+                lb_prf(e.A, e.wire0 + op.wire_off, 0, Mq, e.rk, e.t);
             } else {
                 // out0 = -pad(key0, {g,0,0}) - phi(a0) R_q, key0 = in + a0 R_p
                 const uint32_t a0 = cin == 0 ? 0 : p - cin;
-                Lab key0 = x;
-                lab_add_g(key0, mult_row(e, p, a0), Mp);
-                const U4 H0 = hash_tw(compress(key0, Mp), g, 0, 0, e.t);
-                decompress(out0, H0, Mq);
-                lab_neg(out0, Mq);
-                lab_sub_g(out0, mult_row(e, op.qm, phi[a0]), Mq);
+                lb_copy(e.T, e.X, Mp);
+                lb_add_g(e.T, mult_row(e, p, a0), Mp);
+                const U4 H0 = hash_tw(lb_compress(e.T, Mp), g, 0, 0, e.t);
+                lb_decompress(e.A, H0, Mq);
+                lb_neg(e.A, Mq);
+                lb_sub_g(e.A, mult_row(e, op.qm, phi[a0]), Mq);
             }
             const uint32_t* Rp = mult_row(e, p, 1);
             for (uint32_t a = 0; a < p; ++a) {
                 uint32_t row = cin + a;
                 row = row >= p ? row - p : row;
-                const U4 H = hash_tw(compress(x, Mp), g, row, 0, e.t);
-                Lab pay = out0;
-                lab_add_g(pay, mult_row(e, op.qm, phi[a]), Mq);
-                const U4 ct = enc_with(H, pay, Mq);
+                const U4 H = hash_tw(lb_key_step(e.X, Rp, Mp), g, row, 0, e.t);
+                const U4 ct = lb_enc(H, e.A, mult_row(e, op.qm, phi[a]), nullptr, 0, e.T, Mq);
                 if (op.kind == OP_PROJ) R[row] = ct;
                 else if (row != 0) R[row - 1] = ct;
-                lab_add_g(x, Rp, Mp);
             }
-            store_slot(e, op.out, out0, Mq);
+            store_slot(e, op.out, e.A, Mq);
             break;
         }
-        case OP_HALF: {  // t_half_gate (gadgets.hpp:230-282)
-            const ModC& M = c_mod[op.pm];
-            const uint32_t p = op.pm;
-            const uint64_t g = e.gate0 + op.gate_off;
-            U4* R = e.rows + op.ct_off;
-            Lab x, key;
-            load_operand(x, P, e, op.a, M);
-            const uint32_t* Rp = mult_row(e, p, 1);
-            const uint32_t cx = color(x, M);
-            uint32_t r;
-            {
-                Lab y;
-                load_operand(y, P, e, op.b, M);
-                r = color(y, M);
-                key = y;
-            }
-            Lab u0;
-            prf_label(u0, e.wire0 + op.wire_off, 0, M, e.rk, e.t);
-            const U4 u0c = compress(u0, M);
-            {
-                Lab kx = x;
-                for (uint32_t a = 0; a < p; ++a) {
-                    uint32_t row = cx + a;
-                    row = row >= p ? row - p : row;
-                    const U4 H = hash_tw(compress(kx, M), g, row, 0, e.t);
-                    Lab pay = u0;
-                    lab_add_g(pay, mult_row(e, p, (a * r) % p), M);
-                    R[row] = enc_with(H, pay, M);
-                    lab_add_g(kx, Rp, M);
-                }
-            }
-            Lab v0;
-            prf_label(v0, e.wire0 + op.wire_off + 1, 0, M, e.rk, e.t);
-            for (uint32_t b = 0; b < p; ++b) {
-                uint32_t row = r + b;
-                row = row >= p ? row - p : row;
-                const U4 H = hash_tw(compress(key, M), g, row, 1, e.t);
-                Lab pay = v0, sx;
-                lab_scale(sx, x, row, M);
-                lab_sub(pay, sx, M);
-                R[p + row] = enc_with(H, pay, M);
-                lab_add_g(key, Rp, M);
-            }
-            decompress(u0, u0c, M);
-            lab_sub(v0, u0, M);
-            store_slot(e, op.out, v0, M);
-            break;
-        }
-        case OP_MMHALF: {  // t_mm_half_gate (gadgets.hpp:292-358)
+        case OP_HALF:      // t_half_gate (gadgets.hpp:230-282): x, y mod p
+        case OP_MMHALF: {  // t_mm_half_gate (gadgets.hpp:292-358): x mod p, y mod q
+            const bool mm = op.kind == OP_MMHALF;
             const ModC& Mp = c_mod[op.pm];
-            const ModC& Mq = c_mod[op.qm];
-            const uint32_t p = op.pm, q = op.qm;
+            const ModC& Mq = c_mod[mm ? op.qm : op.pm];
+            const uint32_t p = op.pm, q = mm ? op.qm : op.pm;
             const uint64_t g = e.gate0 + op.gate_off;
             U4* R = e.rows + op.ct_off;
-            Lab x;
-            load_operand(x, P, e, op.a, Mp);
-            const uint32_t r = color(x, Mp);
-            Lab u0;
-            prf_label(u0, e.wire0 + op.wire_off, 0, Mp, e.rk, e.t);
-            const U4 u0c = compress(u0, Mp);
-            {
-                const uint32_t* Rp = mult_row(e, p, 1);
-                Lab kx = x;
-                for (uint32_t a = 0; a < p; ++a) {
-                    uint32_t row = r + a;
-                    row = row >= p ? row - p : row;
-                    const U4 H = hash_tw(compress(kx, Mp), g, row, 0, e.t);
-                    Lab pay = u0;
-                    lab_add_g(pay, mult_row(e, p, (a * r) % p), Mp);
-                    R[row] = enc_with(H, pay, Mp);
-                    lab_add_g(kx, Rp, Mp);
-                }
+            load_operand(e.K, P, e, op.b, Mq);
+            const uint32_t cy = lb_color(e.K, Mq);
+            load_operand(e.X, P, e, op.a, Mp);
+            const uint32_t cx = lb_color(e.X, Mp);
+            const uint32_t r = mm ? cx : cy;
+            // garbler rows: key x + aR_p, payload u0 + (a r mod p) R_p, slot 0
+            lb_prf(e.A, e.wire0 + op.wire_off, 0, Mp, e.rk, e.t);
+            const U4 u0c = lb_compress(e.A, Mp);
+            const uint32_t* Rp = mult_row(e, p, 1);
+            lb_copy(e.K, e.X, Mp);
+            for (uint32_t a = 0; a < p; ++a) {
+                uint32_t row = cx + a;
+                row = row >= p ? row - p : row;
+                const U4 H = hash_tw(lb_key_step(e.K, Rp, Mp), g, row, 0, e.t);
+                R[row] = lb_enc(H, e.A, mult_row(e, p, (a * r) % p), nullptr, 0, e.T, Mp);
             }
-            Lab v0;
-            prf_label(v0, e.wire0 + op.wire_off + 1, 0, Mp, e.rk, e.t);
+            // evaluator rows: key y + bR_q, payload v0 - s x, slot 1
+            lb_prf(e.A, e.wire0 + op.wire_off + 1, 0, Mp, e.rk, e.t);
+            load_operand(e.K, P, e, op.b, Mq);
+            const uint32_t* Rq = mult_row(e, q, 1);
             const uint32_t fw = field_width(p);
             const uint32_t fmask = (1u << fw) - 1u;
             U4 sb;
             sb.x[0] = sb.x[1] = sb.x[2] = sb.x[3] = 0;
-            {
-                Lab key;
-                load_operand(key, P, e, op.b, Mq);
-                const uint32_t cy = color(key, Mq);
-                const uint32_t* Rq = mult_row(e, q, 1);
-                for (uint32_t b = 0; b < q; ++b) {
-                    uint32_t row = cy + b;
-                    row = row >= q ? row - q : row;
-                    uint32_t s = r + b;
-                    s = s >= p ? s - p : s;
-                    const U4 Kc = compress(key, Mq);
-                    const U4 H = hash_tw(Kc, g, row, 1, e.t);
-                    Lab pay = v0, sx;
-                    lab_scale(sx, x, s, Mp);
-                    lab_sub(pay, sx, Mp);
-                    R[p + row] = enc_with(H, pay, Mp);
+            for (uint32_t b = 0; b < q; ++b) {
+                uint32_t row = cy + b;
+                row = row >= q ? row - q : row;
+                uint32_t s = r + b;
+                s = s >= p ? s - p : s;
+                const U4 Kc = lb_key_step(e.K, Rq, Mq);
+                const U4 H = hash_tw(Kc, g, row, 1, e.t);
+                LB X = e.X;
+                R[p + row] = lb_enc(H, e.A, nullptr, &X, mm ? s : row, e.T, Mp);
+                if (mm) {  // encrypt_short field of this row (cipher.cpp:45-60)
                     const U4 Hs = hash_tw(Kc, g, 0, 2, e.t);
                     u4_or_shl(sb, (s ^ (Hs.x[0] & fmask)) & fmask, fw * row);
-                    lab_add_g(key, Rq, Mq);
                 }
             }
-            R[p + q] = sb;
-            decompress(u0, u0c, Mp);
-            lab_sub(v0, u0, Mp);
-            store_slot(e, op.out, v0, Mp);
+            if (mm) R[p + q] = sb;
+            lb_decompress(e.T, u0c, Mp);
+            lb_sub(e.A, e.T, Mp);
+            store_slot(e, op.out, e.A, Mp);
             break;
         }
         case OP_ADD: {
             const ModC& M = c_mod[op.qm];
-            Lab a, b;
-            load_operand(a, P, e, op.a, M);
-            load_operand(b, P, e, op.b, M);
-            lab_add(a, b, M);
-            store_slot(e, op.out, a, M);
+            load_operand(e.A, P, e, op.a, M);
+            load_operand(e.T, P, e, op.b, M);
+            lb_add(e.A, e.T, M);
+            store_slot(e, op.out, e.A, M);
             break;
         }
         case OP_ADDCONST: {  // add_public_constant (gadgets.hpp:127-139)
             const ModC& M = c_mod[op.qm];
-            Lab a;
-            load_operand(a, P, e, op.a, M);
+            load_operand(e.A, P, e, op.a, M);
             const uint32_t c = op.cst % op.qm;
-            if (c) lab_sub_g(a, mult_row(e, op.qm, c), M);
-            store_slot(e, op.out, a, M);
+            if (c) lb_sub_g(e.A, mult_row(e, op.qm, c), M);
+            store_slot(e, op.out, e.A, M);
             break;
         }
         case OP_OUTPUT: {
             const ModC& M = c_mod[op.qm];
-            Lab a;
-            load_operand(a, P, e, op.a, M);
-            uint32_t* base = P.out[op.cst] + ((uint64_t)e.b * M.nw) * P.E + e.u;
-            lab_store_rows(a, base, P.E, M);
+            load_operand(e.A, P, e, op.a, M);
+            lb_store_rows(e.A, P.out[op.cst] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, M);
             break;
         }
     }
-}
-
-// decrypt_label (cipher.cpp:36-38): key label -> payload label mod q
-DASH_HD void dec_row(Lab& out, const Lab& key, const ModC& Mk, uint64_t g, uint32_t row, uint32_t slot,
-                     const U4& ct, const ModC& Mq, const AesTab& t) {
-    const U4 H = hash_tw(compress(key, Mk), g, row, slot, t);
-    dec_with(out, ct, H, Mq);
 }
 
 // ---- evaluation of one op ----
@@ -828,9 +771,8 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const ModC& Mq = c_mod[op.qm];
             const uint64_t g = e.gate0 + op.gate_off;
             const U4* R = e.rows + op.ct_off;
-            Lab x, out;
-            load_operand(x, P, e, op.a, Mp);
-            const uint32_t row = color(x, Mp);
+            load_operand(e.X, P, e, op.a, Mp);
+            const uint32_t row = lb_color(e.X, Mp);
             U4 ct;
             if (op.kind == OP_PROJ) {
                 ct = R[row];
@@ -839,77 +781,60 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             } else {
                 ct = R[row - 1];
             }
-            dec_row(out, x, Mp, g, row, 0, ct, Mq, e.t);
-            store_slot(e, op.out, out, Mq);
+            const U4 H = hash_tw(lb_compress(e.X, Mp), g, row, 0, e.t);
+            lb_dec(e.A, ct, H, Mq);
+            store_slot(e, op.out, e.A, Mq);
             break;
         }
-        case OP_HALF: {
-            const ModC& M = c_mod[op.pm];
-            const uint32_t p = op.pm;
-            const uint64_t g = e.gate0 + op.gate_off;
-            const U4* R = e.rows + op.ct_off;
-            Lab x, y, u, out, sx;
-            load_operand(x, P, e, op.a, M);
-            load_operand(y, P, e, op.b, M);
-            const uint32_t cx = color(x, M), cy = color(y, M);
-            dec_row(u, x, M, g, cx, 0, R[cx], M, e.t);
-            dec_row(out, y, M, g, cy, 1, R[p + cy], M, e.t);
-            lab_scale(sx, x, cy, M);
-            lab_add(out, sx, M);
-            lab_sub(out, u, M);
-            store_slot(e, op.out, out, M);
-            break;
-        }
+        case OP_HALF:
         case OP_MMHALF: {
+            const bool mm = op.kind == OP_MMHALF;
             const ModC& Mp = c_mod[op.pm];
-            const ModC& Mq = c_mod[op.qm];
-            const uint32_t p = op.pm, q = op.qm;
+            const ModC& Mq = c_mod[mm ? op.qm : op.pm];
+            const uint32_t p = op.pm, q = mm ? op.qm : op.pm;
             const uint64_t g = e.gate0 + op.gate_off;
             const U4* R = e.rows + op.ct_off;
-            Lab x, y, u, out, sx;
-            load_operand(x, P, e, op.a, Mp);
-            load_operand(y, P, e, op.b, Mq);
-            const uint32_t cx = color(x, Mp), cy = color(y, Mq);
-            dec_row(u, x, Mp, g, cx, 0, R[cx], Mp, e.t);
-            const U4 Ky = compress(y, Mq);
-            const U4 H = hash_tw(Ky, g, cy, 1, e.t);
-            dec_with(out, R[p + cy], H, Mp);
-            // decrypt_short (cipher.cpp:62-69)
-            const uint32_t fw = field_width(p);
-            const uint32_t fmask = (1u << fw) - 1u;
-            const U4 Hs = hash_tw(Ky, g, 0, 2, e.t);
-            const uint32_t field = u4_shr_low(R[p + q], fw * cy) & fmask;
-            const uint32_t s = ((field ^ (Hs.x[0] & fmask)) & fmask) % p;
-            lab_scale(sx, x, s, Mp);
-            lab_add(out, sx, Mp);
-            lab_sub(out, u, Mp);
-            store_slot(e, op.out, out, Mp);
+            load_operand(e.X, P, e, op.a, Mp);
+            load_operand(e.K, P, e, op.b, Mq);
+            const uint32_t cx = lb_color(e.X, Mp), cy = lb_color(e.K, Mq);
+            // u = Dec(x, {g,cx,0}); out = Dec(y, {g,cy,1}) (+ s x) - u
+            lb_dec(e.T, R[cx], hash_tw(lb_compress(e.X, Mp), g, cx, 0, e.t), Mp);
+            const U4 Ky = lb_compress(e.K, Mq);
+            lb_dec(e.A, R[p + cy], hash_tw(Ky, g, cy, 1, e.t), Mp);
+            uint32_t s = cy;
+            if (mm) {  // decrypt_short (cipher.cpp:62-69)
+                const uint32_t fw = field_width(p);
+                const uint32_t fmask = (1u << fw) - 1u;
+                const U4 Hs = hash_tw(Ky, g, 0, 2, e.t);
+                const uint32_t field = u4_shr_low(R[p + q], fw * cy) & fmask;
+                s = ((field ^ (Hs.x[0] & fmask)) & fmask) % p;
+            }
+            lb_sub(e.A, e.T, Mp);
+            lb_scale(e.T, e.X, s, Mp);
+            lb_add(e.A, e.T, Mp);
+            store_slot(e, op.out, e.A, Mp);
             break;
         }
         case OP_ADD: {
             const ModC& M = c_mod[op.qm];
-            Lab a, b;
-            load_operand(a, P, e, op.a, M);
-            load_operand(b, P, e, op.b, M);
-            lab_add(a, b, M);
-            store_slot(e, op.out, a, M);
+            load_operand(e.A, P, e, op.a, M);
+            load_operand(e.T, P, e, op.b, M);
+            lb_add(e.A, e.T, M);
+            store_slot(e, op.out, e.A, M);
             break;
         }
         case OP_ADDCONST: {
             if (op.a != op.out) {
                 const ModC& M = c_mod[op.qm];
-                Lab a;
-                load_operand(a, P, e, op.a, M);
-                store_slot(e, op.out, a, M);
+                load_operand(e.A, P, e, op.a, M);
+                store_slot(e, op.out, e.A, M);
             }
             break;
         }
         case OP_OUTPUT: {
             const ModC& M = c_mod[op.qm];
-            Lab a;
-            load_operand(a, P, e, op.a, M);
-            uint32_t* base = P.out[op.cst] + ((uint64_t)e.b * M.nw) * P.E + e.u;
-            lab_store_rows(a, base, P.E, M);
+            load_operand(e.A, P, e, op.a, M);
+            lb_store_rows(e.A, P.out[op.cst] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, M);
             break;
         }
     }
@@ -920,6 +845,8 @@ DASH_HD void act_element(const ActParams& P, Elt& e) {
     e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
     e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
     e.rows = P.blob + (uint64_t)e.b * P.blob_stride + (uint64_t)e.u * P.uc_cts;
+    e.sstride = (uint64_t)P.B * P.E;
+    e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
     if (GARBLE) {
         e.rk = P.rk + (uint64_t)e.b * 44;
         e.mult = P.mult + (uint64_t)e.b * P.mult_stride;

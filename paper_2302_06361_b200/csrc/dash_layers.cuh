@@ -120,8 +120,8 @@ DASH_HD void private_thread(const PrivParams& P, uint32_t b, uint32_t u, const A
     }
     const uint8_t* wr = P.wres + (uint64_t)(P.conv ? oc : u) * P.win;
     const uint32_t* Rp = P.garbler ? mult_row(e, p, 1) : nullptr;
-    Lab sum;
-    lab_zero(sum);
+    uint32_t buf[4][NWMAX];
+    const LB X{buf[0], 1}, term{buf[1], 1}, sum{buf[2], 1}, tmp{buf[3], 1};
     for (uint32_t j = 0; j < P.win; ++j) {
         uint64_t xi;
         if (!P.conv) {
@@ -130,34 +130,30 @@ DASH_HD void private_thread(const PrivParams& P, uint32_t b, uint32_t u, const A
             const uint32_t ic = j / (P.f * P.f), ky = (j / P.f) % P.f, kx = j % P.f;
             xi = ((uint64_t)ic * P.H + (oy * P.stride + ky)) * P.W + (ox * P.stride + kx);
         }
-        Lab x, term;
-        lab_load_rows(x, P.in + ((uint64_t)b * M.nw) * P.E_in + xi, P.E_in, M);
+        lb_load_rows(X, P.in + ((uint64_t)b * M.nw) * P.E_in + xi, P.E_in, M);
         const uint64_t g = P.gate_base + (uint64_t)u * P.win + j;
         U4* R = rows + (uint64_t)j * p;
-        const uint32_t c = color(x, M);
+        const uint32_t c = lb_color(X, M);
         if (P.garbler) {
-            prf_label(term, P.wire_base + (uint64_t)u * P.win + j, 0, M, e.rk, t);
+            lb_prf(term, P.wire_base + (uint64_t)u * P.win + j, 0, M, e.rk, t);
             const uint32_t w = wr[j];
             for (uint32_t a = 0; a < p; ++a) {
                 uint32_t row = c + a;
                 row = row >= p ? row - p : row;
-                const U4 H = hash_tw(compress(x, M), g, row, 0, t);
-                Lab pay = term;
-                lab_add_g(pay, mult_row(e, p, (w * a) % p), M);
-                R[row] = enc_with(H, pay, M);
-                lab_add_g(x, Rp, M);
+                const U4 H = hash_tw(lb_key_step(X, Rp, M), g, row, 0, t);
+                R[row] = lb_enc(H, term, mult_row(e, p, (w * a) % p), nullptr, 0, tmp, M);
             }
         } else {
-            dec_row(term, x, M, g, c, 0, R[c], M, t);
+            lb_dec(term, R[c], hash_tw(lb_compress(X, M), g, c, 0, t), M);
         }
-        if (j == 0) sum = term;
-        else lab_add(sum, term, M);
+        if (j == 0) lb_copy(sum, term, M);
+        else lb_add(sum, term, M);
     }
     if (P.garbler) {
         const uint32_t bb = P.bres[P.conv ? oc : u];
-        if (bb) lab_sub_g(sum, mult_row(e, p, bb), M);
+        if (bb) lb_sub_g(sum, mult_row(e, p, bb), M);
     }
-    lab_store_rows(sum, P.out + ((uint64_t)b * M.nw) * P.M + u, P.M, M);
+    lb_store_rows(sum, P.out + ((uint64_t)b * M.nw) * P.M + u, P.M, M);
 }
 
 // ---------------------------------------------------------------------------
@@ -184,32 +180,34 @@ struct SetupParams {
 DASH_HD void setup_offsets_thread(const SetupParams& S, uint32_t b, uint32_t si, const AesTab& t) {
     const uint32_t m = S.slot_mod[si];
     const ModC& M = c_mod[m];
-    Lab R, v;
-    prf_label(R, m, 1, M, S.rk + (uint64_t)b * 44, t);
+    uint32_t buf[2][NWMAX] = {};
+    const LB R{buf[0], 1}, v{buf[1], 1};
+    lb_prf(R, m, 1, M, S.rk + (uint64_t)b * 44, t);
     // digit 0 forced to 1 (prf.hpp:28-32)
-    if (M.pow2) R.w[0] = (R.w[0] & ~(M.m - 1u)) | 1u;
-    else R.w[0] = (R.w[0] & ~0xffu) | 1u;
+    if (M.pow2) R[0] = (R[0] & ~(M.m - 1u)) | 1u;
+    else R[0] = (R[0] & ~0xffu) | 1u;
     uint32_t* base = S.mult + (uint64_t)b * S.mult_stride + (uint64_t)c_modslot[m] * 128 * NWMAX;
     for (uint32_t x = 0; x < m; ++x) {
-        lab_scale(v, R, x, M);
-        for (int w = 0; w < NWMAX; ++w) base[(uint64_t)x * NWMAX + w] = v.w[w];
+        lb_scale(v, R, x, M);
+        for (int w = 0; w < NWMAX; ++w) base[(uint64_t)x * NWMAX + w] = v[w];
     }
     for (int i = 0; i < S.k; ++i)
-        if (S.primes[i] == m) lab_store_rows(R, S.Rb + ((uint64_t)b * S.k + i) * LABW, 1, M);
+        if (S.primes[i] == m) lb_store_rows(R, S.Rb + ((uint64_t)b * S.k + i) * LABW, 1, M);
 }
 
 DASH_HD void setup_labels_thread(const SetupParams& S, uint32_t b, uint32_t e, int i, const AesTab& t) {
     // e < n_in: input base of element e, lane i (wire k + e*k + i); e == n_in: zero wire i
     const uint32_t p = S.primes[i];
     const ModC& M = c_mod[p];
-    Lab L;
+    uint32_t buf[NWMAX];
+    const LB L{buf, 1};
     const uint32_t* rk = S.rk + (uint64_t)b * 44;
     if (e < S.n_in) {
-        prf_label(L, (uint64_t)S.k + (uint64_t)e * S.k + (uint64_t)i, 0, M, rk, t);
-        lab_store_rows(L, S.base_planes[i] + ((uint64_t)b * M.nw) * S.n_in + e, S.n_in, M);
+        lb_prf(L, (uint64_t)S.k + (uint64_t)e * S.k + (uint64_t)i, 0, M, rk, t);
+        lb_store_rows(L, S.base_planes[i] + ((uint64_t)b * M.nw) * S.n_in + e, S.n_in, M);
     } else {
-        prf_label(L, (uint64_t)i, 0, M, rk, t);
-        lab_store_rows(L, S.zero + ((uint64_t)b * S.k + i) * LABW, 1, M);
+        lb_prf(L, (uint64_t)i, 0, M, rk, t);
+        lb_store_rows(L, S.zero + ((uint64_t)b * S.k + i) * LABW, 1, M);
     }
     if (e == S.n_in && i == 0) {
         // seed commitment = davies_meyer(seed bytes read little-endian)
@@ -262,12 +260,13 @@ DASH_HD void encode_thread(const EncodeParams& P, uint32_t b, uint32_t e, int i)
         const uint32_t mr = (uint32_t)(mag % p);
         r = mr ? p - mr : 0;
     }
-    Lab L;
-    lab_load_rows(L, P.base[i] + ((uint64_t)b * M.nw) * P.n_in + e, P.n_in, M);
+    uint32_t buf[NWMAX];
+    const LB L{buf, 1};
+    lb_load_rows(L, P.base[i] + ((uint64_t)b * M.nw) * P.n_in + e, P.n_in, M);
     Elt ex;
     ex.mult = P.mult + (uint64_t)b * P.mult_stride;
-    lab_add_g(L, mult_row(ex, p, r), M);
-    lab_store_rows(L, P.out[i] + ((uint64_t)b * M.nw) * P.n_in + e, P.n_in, M);
+    lb_add_g(L, mult_row(ex, p, r), M);
+    lb_store_rows(L, P.out[i] + ((uint64_t)b * M.nw) * P.n_in + e, P.n_in, M);
 }
 
 // ---------------------------------------------------------------------------
@@ -288,25 +287,27 @@ struct DecodeParams {
 DASH_HD void dectable_thread(const DecodeParams& P, uint32_t b, uint32_t e, int i) {
     const uint32_t p = P.primes[i];
     const ModC& M = c_mod[p];
-    Lab base;
-    lab_load_rows(base, P.lanes[i] + ((uint64_t)b * M.nw) * P.n_out + e, P.n_out, M);
+    uint32_t buf[2][NWMAX];
+    const LB base{buf[0], 1}, c{buf[1], 1};
+    lb_load_rows(base, P.lanes[i] + ((uint64_t)b * M.nw) * P.n_out + e, P.n_out, M);
     Elt ex;
     ex.mult = P.mult + (uint64_t)b * P.mult_stride;
     U4* row = P.table + ((uint64_t)b * P.n_out + e) * P.poff[P.k] + P.poff[i];
     for (uint32_t v = 0; v < p; ++v) {
-        Lab c = base;
-        lab_add_g(c, mult_row(ex, p, v), M);
-        row[v] = compress(c, M);
+        lb_copy(c, base, M);
+        lb_add_g(c, mult_row(ex, p, v), M);
+        row[v] = lb_compress(c, M);
     }
 }
 
 DASH_HD void decode_thread(const DecodeParams& P, uint32_t b, uint32_t e) {
+    uint32_t buf[NWMAX];
+    const LB L{buf, 1};
     for (int i = 0; i < P.k; ++i) {
         const uint32_t p = P.primes[i];
         const ModC& M = c_mod[p];
-        Lab L;
-        lab_load_rows(L, P.lanes[i] + ((uint64_t)b * M.nw) * P.n_out + e, P.n_out, M);
-        const U4 c = compress(L, M);
+        lb_load_rows(L, P.lanes[i] + ((uint64_t)b * M.nw) * P.n_out + e, P.n_out, M);
+        const U4 c = lb_compress(L, M);
         const U4* row = P.table + ((uint64_t)b * P.n_out + e) * P.poff[P.k] + P.poff[i];
         int found = -1;
         for (uint32_t v = 0; v < p; ++v) {
@@ -333,17 +334,19 @@ struct CompressParams {
 
 DASH_HD void compress_thread(const CompressParams& P, uint32_t b, uint32_t e) {
     const ModC& M = c_mod[P.p];
-    Lab L;
-    lab_load_rows(L, P.lane + ((uint64_t)b * M.nw) * P.n + e, P.n, M);
-    P.out[(uint64_t)b * P.ostride + e] = compress(L, M);
+    uint32_t buf[NWMAX];
+    const LB L{buf, 1};
+    lb_load_rows(L, P.lane + ((uint64_t)b * M.nw) * P.n + e, P.n, M);
+    P.out[(uint64_t)b * P.ostride + e] = lb_compress(L, M);
 }
 
 // parse side of the bundle format: decompress_mod every chunk into a lane plane
 DASH_HD void decompress_thread(const CompressParams& P, uint32_t b, uint32_t e, uint32_t* lane_out) {
     const ModC& M = c_mod[P.p];
-    Lab L;
-    decompress(L, P.out[(uint64_t)b * P.ostride + e], M);
-    lab_store_rows(L, lane_out + ((uint64_t)b * M.nw) * P.n + e, P.n, M);
+    uint32_t buf[NWMAX];
+    const LB L{buf, 1};
+    lb_decompress(L, P.out[(uint64_t)b * P.ostride + e], M);
+    lb_store_rows(L, lane_out + ((uint64_t)b * M.nw) * P.n + e, P.n, M);
 }
 
 }  // namespace dashgpu

@@ -7,15 +7,15 @@
 namespace dashgpu {
 
 DASH_HD void prim_thread(const PrimParams& P, uint32_t i, const AesTab& t) {
+    uint32_t buf[3][NWMAX] = {};
+    const LB A{buf[0], 1}, B{buf[1], 1}, T{buf[2], 1};
     switch (P.op) {
         case 0: {  // decompress_mod + compress (label.cpp:208-232)
             const ModC& M = c_mod[P.m];
-            Lab L;
-            decompress(L, P.in[i], M);
-            lab_store_rows(L, P.digits + (uint64_t)i * LABW, 1, M);
-            Lab R;
-            lab_load_rows(R, P.digits + (uint64_t)i * LABW, 1, M);
-            P.out[i] = compress(R, M);
+            lb_decompress(A, P.in[i], M);
+            lb_store_rows(A, P.digits + (uint64_t)i * LABW, 1, M);
+            lb_load_rows(B, P.digits + (uint64_t)i * LABW, 1, M);
+            P.out[i] = lb_compress(B, M);
             break;
         }
         case 1:
@@ -24,30 +24,28 @@ DASH_HD void prim_thread(const PrimParams& P, uint32_t i, const AesTab& t) {
         case 2:
             P.out[i] = aes_key(P.in[i], P.rk, t);
             break;
-        case 3: {  // LabelPrf::label / offset (prf.cpp:11-27)
+        case 3: {  // LabelPrf::label / offset draw (prf.cpp:11-27)
             const ModC& M = c_mod[P.m];
-            Lab L;
-            prf_label(L, P.wires[i], P.q, M, P.rk, t);
-            lab_store_rows(L, P.digits + (uint64_t)i * LABW, 1, M);
+            lb_prf(A, P.wires[i], P.q, M, P.rk, t);
+            lb_store_rows(A, P.digits + (uint64_t)i * LABW, 1, M);
             break;
         }
         case 4: {  // encrypt_label with key = decompress(in, m), msg = decompress(out, q)
             const ModC& Mk = c_mod[P.m];
             const ModC& Mq = c_mod[P.q];
-            Lab key, msg;
-            decompress(key, P.in[i], Mk);
-            decompress(msg, P.out[i], Mq);
-            const U4 H = hash_tw(compress(key, Mk), P.gate, i % 7u, i % 3u, t);
-            P.out[i] = enc_with(H, msg, Mq);
+            lb_decompress(A, P.in[i], Mk);
+            lb_decompress(B, P.out[i], Mq);
+            const U4 H = hash_tw(lb_compress(A, Mk), P.gate, i % 7u, i % 3u, t);
+            P.out[i] = lb_enc(H, B, nullptr, nullptr, 0, T, Mq);
             break;
         }
         case 5: {  // decrypt_label
             const ModC& Mk = c_mod[P.m];
             const ModC& Mq = c_mod[P.q];
-            Lab key, msg;
-            decompress(key, P.in[i], Mk);
-            dec_row(msg, key, Mk, P.gate, i % 7u, i % 3u, P.out[i], Mq, t);
-            lab_store_rows(msg, P.digits + (uint64_t)i * LABW, 1, Mq);
+            lb_decompress(A, P.in[i], Mk);
+            const U4 H = hash_tw(lb_compress(A, Mk), P.gate, i % 7u, i % 3u, t);
+            lb_dec(B, P.out[i], H, Mq);
+            lb_store_rows(B, P.digits + (uint64_t)i * LABW, 1, Mq);
             break;
         }
     }

@@ -427,6 +427,7 @@ struct Tape {
     std::vector<TapeOp> ops;
     std::vector<uint8_t> phi;
     uint64_t cts = 0, gates = 0, wires = 0;
+    uint64_t eval_rows = 0;  // ciphertext rows one evaluation reads
     int nslots = 0;
     std::set<int> moduli;
 };
@@ -717,6 +718,8 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
     tp.phi = r.phi;
     if (tp.phi.empty()) tp.phi.push_back(0);
     tp.cts = r.cts;
+    for (const auto& o : r.ops)
+        tp.eval_rows += o.kind == OP_PROJ || o.kind == OP_GRR ? 1 : o.kind == OP_HALF ? 2 : o.kind == OP_MMHALF ? 3 : 0;
     tp.gates = r.gates;
     tp.wires = r.wires;
     tp.moduli = r.moduli;
@@ -755,7 +758,8 @@ struct HLayer {
     uint64_t E_in = 0, E_out = 0;
     // layout (per inference)
     uint64_t gate_base = 0, wire_base = 0, ct_base = 0, cts = 0, gates = 0, wires = 0;
-    // public / private linear: per-lane device residues
+    // public / private linear: per-lane residues (host) and their device copies
+    std::vector<std::vector<uint8_t>> wres_h, zt_h, bres_h;
     std::vector<std::shared_ptr<DevBuf>> wres, zt, bres;
     std::vector<uint64_t> lane_ct_off, lane_gate_off, lane_wire_off;  // private
     uint32_t K = 0;  // window
@@ -794,6 +798,7 @@ struct dashgpu_circuit {
     uint64_t relu_elements = 0, linear_macs = 0;
     std::vector<dash_layer_desc> desc_layers;  // for dashgpu_circuit_desc_view
     std::unique_ptr<dashgpu::Network> workspace;  // dashgpu_infer cache
+    bool uploaded = false;  // per-layer device buffers created (upload_circuit)
     std::mutex mu;
     ~dashgpu_circuit();
 };
@@ -840,9 +845,10 @@ static std::shared_ptr<DevBuf> upload(const void* data, size_t bytes) {
 
 static int64_t resid(int64_t w, int p) { return ((w % p) + p) % p; }
 
-// validate_circuit + circuit_layout + per-layer device preparation
+// validate_circuit + circuit_layout + per-layer residues and tapes (host only;
+// device copies are made lazily by upload_circuit at the first garble)
 static void prepare_circuit(dashgpu_circuit& c) {
-    check_constants();
+    c.uploaded = false;
     c.base = crt_base(c.k);
     if (c.input_shape.empty() || c.input_shape.size() > 8 || shape_size(c.input_shape) == 0)
         throw DataError("circuit has an empty input shape");
@@ -881,9 +887,9 @@ static void prepare_circuit(dashgpu_circuit& c) {
         l.wire_base = w;
         l.ct_base = ct;
         l.cts = l.gates = l.wires = 0;
-        l.wres.clear();
-        l.zt.clear();
-        l.bres.clear();
+        l.wres_h.clear();
+        l.zt_h.clear();
+        l.bres_h.clear();
         l.lane_ct_off.clear();
         l.lane_gate_off.clear();
         l.lane_wire_off.clear();
@@ -907,17 +913,17 @@ static void prepare_circuit(dashgpu_circuit& c) {
                         zt[row] = (uint8_t)(z % (uint32_t)p);
                         br[row] = (uint8_t)resid(l.bias.empty() ? 0 : l.bias[row], p);
                     }
-                    l.wres.push_back(upload(wr.data(), wr.size()));
-                    l.zt.push_back(upload(zt.data(), zt.size()));
-                    l.bres.push_back(upload(br.data(), br.size()));
+                    l.wres_h.push_back(std::move(wr));
+                    l.zt_h.push_back(std::move(zt));
+                    l.bres_h.push_back(std::move(br));
                 } else {
                     std::vector<uint8_t> wr(l.w.size()), br(nrow);
                     for (uint64_t row = 0; row < nrow; ++row) {
                         for (uint32_t j = 0; j < l.K; ++j) wr[row * l.K + j] = (uint8_t)resid(l.w[row * l.K + j], p);
                         br[row] = (uint8_t)resid(l.bias.empty() ? 0 : l.bias[row], p);
                     }
-                    l.wres.push_back(upload(wr.data(), wr.size()));
-                    l.bres.push_back(upload(br.data(), br.size()));
+                    l.wres_h.push_back(std::move(wr));
+                    l.bres_h.push_back(std::move(br));
                     // count_layer order (layer.cpp:393-404): lane after lane
                     l.lane_ct_off.push_back(l.cts);
                     l.lane_gate_off.push_back(l.gates);
@@ -929,8 +935,6 @@ static void prepare_circuit(dashgpu_circuit& c) {
             }
         } else if (l.kind == DASH_LAYER_RELU || l.kind == DASH_LAYER_SIGNACT) {
             l.tape = l.kind == DASH_LAYER_RELU ? c.relu_tape : c.sign_tape;
-            l.tape_d = upload(l.tape->ops.data(), l.tape->ops.size() * sizeof(TapeOp));
-            l.phi_d = upload(l.tape->phi.data(), l.tape->phi.size());
             l.cts = l.tape->cts * l.E_out;
             l.gates = l.tape->gates * l.E_out;
             l.wires = l.tape->wires * l.E_out;
@@ -951,7 +955,25 @@ static void prepare_circuit(dashgpu_circuit& c) {
     c.total_cts = ct;
     c.total_gates = g;
     c.total_wires = w - c.wire0;
+}
+
+static void upload_circuit(dashgpu_circuit& c) {
+    check_constants();
+    if (c.uploaded) return;
+    for (auto& l : c.layers) {
+        l.wres.clear();
+        l.zt.clear();
+        l.bres.clear();
+        for (auto& v : l.wres_h) l.wres.push_back(upload(v.data(), v.size()));
+        for (auto& v : l.zt_h) l.zt.push_back(upload(v.data(), v.size()));
+        for (auto& v : l.bres_h) l.bres.push_back(upload(v.data(), v.size()));
+        if (l.tape) {
+            l.tape_d = upload(l.tape->ops.data(), l.tape->ops.size() * sizeof(TapeOp));
+            l.phi_d = upload(l.tape->phi.data(), l.tape->phi.size());
+        }
+    }
     dev::sync(g_stream);
+    c.uploaded = true;
 }
 
 // ================================================================ network
@@ -974,7 +996,7 @@ struct Network {
     dashgpu_circuit* c = nullptr;
     uint32_t B = 0, cap = 0;
     std::vector<uint8_t> seeds;
-    DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err;
+    DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err, slots;
     Lanes base;  // encoding info: input base labels
     Lanes ping, pong;    // garbling planes
     Lanes eping, epong;  // evaluation planes
@@ -1093,11 +1115,12 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, Lanes& in, Lane
     for (int i = 0; i < k; ++i) {
         P.in[i] = in.lane[i]->as<uint32_t>();
         P.out[i] = out.lane[i]->as<uint32_t>();
-        P.lane_mod[i] = (uint16_t)c.base.primes[i];
     }
     P.rk = n.rk.as<uint32_t>();
     P.mult = n.mult.as<uint32_t>();
     P.mult_stride = n.mult_stride;
+    n.slots.ensure((size_t)l.tape->nslots * n.B * l.E_out * 16);
+    P.slots = n.slots.as<U4>();
     launch_act(P, garbler, l.tape->nslots, g_stream);
 }
 
@@ -1131,6 +1154,7 @@ static void network_reserve(Network& n, uint32_t B) {
 static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
+    upload_circuit(c);
     network_reserve(n, B);
     n.seeds.assign(16 * (size_t)B, 0);
     std::vector<uint32_t> rk((size_t)B * 44);
@@ -1748,6 +1772,7 @@ int dashgpu_circuit_info_get(const dashgpu_circuit* c, dashgpu_circuit_info* o) 
             o->sign_t = (uint32_t)c->sign.spec.size();
             for (size_t j = 0; j < c->sign.spec.size() && j < 32; ++j) o->radices[j] = (uint16_t)c->sign.spec[j];
             o->act_uc_cts = c->relu_tape->cts;
+            o->act_eval_rows = c->relu_tape->eval_rows;
             o->max_slots = (uint32_t)std::max(c->relu_tape->nslots, c->sign_tape->nslots);
         }
         o->relu_elements = c->relu_elements;

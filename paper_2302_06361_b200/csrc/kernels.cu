@@ -45,27 +45,24 @@ __global__ void __launch_bounds__(128) linear_kernel(LinParams L) {
 }
 
 __global__ void __launch_bounds__(128) private_kernel(PrivParams P) {
-    __shared__ uint32_t T[kTWords];
-    fill_T(T, g_T0);
+    fill_T(s_T, g_T0);
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= P.M) return;
-    private_thread(P, blockIdx.y, u, AesTab{T, threadIdx.x & 31u});
+    private_thread(P, blockIdx.y, u, make_tab(s_T, threadIdx.x & 31u));
 }
 
 __global__ void __launch_bounds__(128) setup_offsets_kernel(SetupParams Sp) {
-    __shared__ uint32_t T[kTWords];
-    fill_T(T, g_T0);
+    fill_T(s_T, g_T0);
     const uint32_t si = blockIdx.x * blockDim.x + threadIdx.x;
     if (si >= Sp.nslot) return;
-    setup_offsets_thread(Sp, blockIdx.y, si, AesTab{T, threadIdx.x & 31u});
+    setup_offsets_thread(Sp, blockIdx.y, si, make_tab(s_T, threadIdx.x & 31u));
 }
 
 __global__ void __launch_bounds__(128) setup_labels_kernel(SetupParams Sp) {
-    __shared__ uint32_t T[kTWords];
-    fill_T(T, g_T0);
+    fill_T(s_T, g_T0);
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e > Sp.n_in) return;
-    setup_labels_thread(Sp, blockIdx.z, e, (int)blockIdx.y, AesTab{T, threadIdx.x & 31u});
+    setup_labels_thread(Sp, blockIdx.z, e, (int)blockIdx.y, make_tab(s_T, threadIdx.x & 31u));
 }
 
 __global__ void __launch_bounds__(128) encode_kernel(EncodeParams P) {
@@ -99,11 +96,10 @@ __global__ void __launch_bounds__(128) decompress_kernel(CompressParams P, uint3
 }
 
 __global__ void __launch_bounds__(128) prim_kernel(PrimParams P) {
-    __shared__ uint32_t T[kTWords];
-    fill_T(T, g_T0);
+    fill_T(s_T, g_T0);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.n) return;
-    prim_thread(P, i, AesTab{T, threadIdx.x & 31u});
+    prim_thread(P, i, make_tab(s_T, threadIdx.x & 31u));
 }
 
 }  // namespace

@@ -18,25 +18,30 @@ namespace dashgpu {
 
 namespace {
 
+// Shared memory per CTA: static T-table s_T (32 KB) + dynamic: 4 label buffers of NWMAX words
+// per lane (word w of buffer j for lane l at L[((warp*4 + j)*NWMAX + w)*32 + l]).
+constexpr int kBufWords = 4 * NWMAX * 32;
+
 template <bool G>
-__global__ void __launch_bounds__(kActWarps * 32, 2) act_kernel(ActParams P, int nslots) {
+__global__ void __launch_bounds__(kActWarps * 32, 2) act_kernel(ActParams P) {
     extern __shared__ uint4 smem4[];
-    uint32_t* T = reinterpret_cast<uint32_t*>(smem4);
-    U4* slots = reinterpret_cast<U4*>(T + kTWords);
-    fill_T(T, g_T0);
+    uint32_t* L = reinterpret_cast<uint32_t*>(smem4);
+    fill_T(s_T, g_T0);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t wpi = (P.E + 31) / 32;
     const uint64_t gw = (uint64_t)blockIdx.x * kActWarps + warp;
     const uint32_t b = (uint32_t)(gw / wpi);
     const uint32_t u = (uint32_t)(gw % wpi) * 32 + lane;
     if (b >= P.B || u >= P.E) return;
+    uint32_t* lb = L + (uint64_t)warp * kBufWords + lane;
     Elt e;
     e.b = b;
     e.u = u;
-    e.slots = slots + (uint64_t)warp * nslots * 32 + lane;
-    e.sstride = 32;
-    e.t.T = T;
-    e.t.lane = lane;
+    e.X = LB{lb, 32};
+    e.K = LB{lb + NWMAX * 32, 32};
+    e.A = LB{lb + 2 * NWMAX * 32, 32};
+    e.T = LB{lb + 3 * NWMAX * 32, 32};
+    e.t = make_tab(s_T, lane);
     e.rk = nullptr;
     e.mult = nullptr;
     act_element<G>(P, e);
@@ -56,13 +61,14 @@ void launch_act(const ActParams& P, bool garble, int nslots, void* st) {
     ProfScope ps(garble ? K_ACT_GARBLE : K_ACT_EVAL, S(st));
     const uint64_t warps = (uint64_t)P.B * ((P.E + 31) / 32);
     const uint32_t grid = cdiv(warps, kActWarps);
-    const size_t smem = sizeof(uint32_t) * kTWords + sizeof(U4) * (size_t)kActWarps * nslots * 32;
+    (void)nslots;  // slots live in global memory (P.slots)
+    const size_t smem = sizeof(uint32_t) * (size_t)kActWarps * kBufWords;  // + static s_T (32 KB)
     if (garble) {
         ck(cudaFuncSetAttribute(act_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_kernel<true><<<grid, kActWarps * 32, smem, S(st)>>>(P, nslots);
+        act_kernel<true><<<grid, kActWarps * 32, smem, S(st)>>>(P);
     } else {
         ck(cudaFuncSetAttribute(act_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_kernel<false><<<grid, kActWarps * 32, smem, S(st)>>>(P, nslots);
+        act_kernel<false><<<grid, kActWarps * 32, smem, S(st)>>>(P);
     }
     ck(cudaGetLastError(), "act launch");
 }

@@ -70,6 +70,7 @@ class CircuitInfo(ctypes.Structure):
         ("relu_elements", ctypes.c_uint64),
         ("linear_macs", ctypes.c_uint64),
         ("act_uc_cts", ctypes.c_uint64),
+        ("act_eval_rows", ctypes.c_uint64),
         ("max_slots", ctypes.c_uint32),
     ]
 

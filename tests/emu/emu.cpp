@@ -24,7 +24,7 @@ namespace dashgpu {
 
 static uint32_t g_T[256 * 32];
 
-static AesTab tab() { return AesTab{g_T, 0}; }
+static AesTab tab() { return make_tab(g_T, 0); }
 
 namespace dev {
 void set_device(int) {}
@@ -60,12 +60,14 @@ void launch_act(const ActParams& P, bool garble, int nslots, void*) {
 #pragma omp parallel for collapse(2) schedule(dynamic, 16)
     for (int64_t b = 0; b < (int64_t)P.B; ++b)
         for (int64_t u = 0; u < (int64_t)P.E; ++u) {
-            U4 slots[MAXSLOTS];
+            uint32_t buf[4][NWMAX];
             Elt e;
             e.b = (uint32_t)b;
             e.u = (uint32_t)u;
-            e.slots = slots;
-            e.sstride = 1;
+            e.X = LB{buf[0], 1};
+            e.K = LB{buf[1], 1};
+            e.A = LB{buf[2], 1};
+            e.T = LB{buf[3], 1};
             e.t = tab();
             e.rk = nullptr;
             e.mult = nullptr;
