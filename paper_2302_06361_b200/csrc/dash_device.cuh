@@ -615,6 +615,19 @@ struct ActParams {
     const uint32_t* mult;      // multiples v*R_m [B][127][128][NWMAX] (garble)
     uint64_t mult_stride;      // words per inference
     U4* slots;                 // compressed label slots [nslots][B*E]
+    // garble-side outputs are pure PRF functions of the element's wire ids:
+    // ReLU lane i = v0 - u0 of its mm half gate, SignAct lane i = out0 of its
+    // projection; act_output_thread writes them before the tape runs.
+    uint8_t out_kind[MAXK];    // OP_MMHALF or OP_PROJ
+    uint32_t out_wire[MAXK];   // wire offset of that gadget within the element
+};
+
+// Work map of a multi-layer launch: layer li owns items [base[li], base[li+1]),
+// item -> (b, 32-element block) with wpi[li] blocks per inference.
+struct ItemMap {
+    uint32_t n;
+    uint32_t base[MAXK + 1];
+    uint32_t wpi[MAXK];
 };
 
 // Working buffers of one element: X (first operand / key), K (second key),
@@ -702,14 +715,15 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             lb_prf(e.A, e.wire0 + op.wire_off, 0, Mp, e.rk, e.t);
             const U4 u0c = lb_compress(e.A, Mp);
             const uint32_t* Rp = mult_row(e, p, 1);
-            lb_copy(e.K, e.X, Mp);
+            // X is the running key here (K only holds the Z_2-sized y operand)
             for (uint32_t a = 0; a < p; ++a) {
                 uint32_t row = cx + a;
                 row = row >= p ? row - p : row;
-                const U4 H = hash_tw(lb_key_step(e.K, Rp, Mp), g, row, 0, e.t);
+                const U4 H = hash_tw(lb_key_step(e.X, Rp, Mp), g, row, 0, e.t);
                 R[row] = lb_enc(H, e.A, mult_row(e, p, (a * r) % p), nullptr, 0, e.T, Mp);
             }
             // evaluator rows: key y + bR_q, payload v0 - s x, slot 1
+            load_operand(e.X, P, e, op.a, Mp);
             lb_prf(e.A, e.wire0 + op.wire_off + 1, 0, Mp, e.rk, e.t);
             load_operand(e.K, P, e, op.b, Mq);
             const uint32_t* Rq = mult_row(e, q, 1);
@@ -753,12 +767,27 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             store_slot(e, op.out, e.A, M);
             break;
         }
-        case OP_OUTPUT: {
-            const ModC& M = c_mod[op.qm];
-            load_operand(e.A, P, e, op.a, M);
-            lb_store_rows(e.A, P.out[op.cst] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, M);
+        case OP_OUTPUT:  // written up front by act_output_thread (same value)
             break;
-        }
+    }
+}
+
+// Garbler-side output base label of lane i of element (b, u): for ReLU the
+// mm half gate's v0 - u0 (gadgets.hpp:354), for SignAct the fresh out0 of the
+// Z_2 -> Z_p projection (gadgets.hpp:172).  Both depend only on wire ids, so
+// every activation layer's outputs exist before any gadget is garbled.
+DASH_HD void act_output_thread(const ActParams& P, uint32_t b, uint32_t u, int i, uint32_t p, LB A, LB T,
+                               const AesTab& t) {
+    const ModC& M = c_mod[p];
+    const uint32_t* rk = P.rk + (uint64_t)b * 44;
+    const uint64_t w = P.wire_base + (uint64_t)u * P.uc_wires + P.out_wire[i];
+    lb_prf(A, w, 0, M, rk, t);
+    if (P.out_kind[i] == OP_MMHALF) {  // out = v0 - u0, v0 drawn at the next wire id
+        lb_prf(T, w + 1, 0, M, rk, t);
+        lb_sub(T, A, M);
+        lb_store_rows(T, P.out[i] + ((uint64_t)b * M.nw) * P.E + u, P.E, M);
+    } else {
+        lb_store_rows(A, P.out[i] + ((uint64_t)b * M.nw) * P.E + u, P.E, M);
     }
 }
 

@@ -430,6 +430,8 @@ struct Tape {
     uint64_t eval_rows = 0;  // ciphertext rows one evaluation reads
     int nslots = 0;
     std::set<int> moduli;
+    uint8_t out_kind[MAXK] = {};   // gadget producing output lane i (OP_MMHALF / OP_PROJ)
+    uint32_t out_wire[MAXK] = {};  // its first fresh wire offset
 };
 
 // Records the gadget DAG in reference order (CountCtx semantics,
@@ -696,6 +698,10 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
                 freelist.push_back(slot[v]);
                 slot[v] = -1;
             }
+        if ((o.kind == OP_HALF || o.kind == OP_MMHALF) && (o.qm & (o.qm - 1)) != 0)
+            throw DataError("half-gate selector wire must have a power-of-two modulus <= 16");
+        if ((o.kind == OP_HALF || o.kind == OP_MMHALF) && o.qm > 16)
+            throw DataError("half-gate selector wire must have a power-of-two modulus <= 16");
         if (o.out >= 0) {
             int sidx;
             if (!freelist.empty()) {
@@ -717,6 +723,13 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
     tp.nslots = nslots;
     tp.phi = r.phi;
     if (tp.phi.empty()) tp.phi.push_back(0);
+    for (const auto& o : r.ops)
+        if (o.kind == OP_OUTPUT) {
+            const auto& prod = r.ops[r.producer[o.a]];
+            if (prod.kind != OP_MMHALF && prod.kind != OP_PROJ) throw std::logic_error("tape: unexpected output gadget");
+            tp.out_kind[o.cst] = (uint8_t)prod.kind;
+            tp.out_wire[o.cst] = (uint32_t)prod.wire;
+        }
     tp.cts = r.cts;
     for (const auto& o : r.ops)
         tp.eval_rows += o.kind == OP_PROJ || o.kind == OP_GRR ? 1 : o.kind == OP_HALF ? 2 : o.kind == OP_MMHALF ? 3 : 0;
@@ -1000,6 +1013,13 @@ struct Network {
     Lanes base;  // encoding info: input base labels
     Lanes ping, pong;    // garbling planes
     Lanes eping, epong;  // evaluation planes
+    std::unique_ptr<struct Bundle> bin, bout;  // dashgpu_infer's cached bundles
+    // garbling of every activation layer is one launch over these
+    std::vector<std::unique_ptr<Lanes>> act_in;
+    std::vector<ActParams> act_host;
+    DevBuf act_dev;        // [act_cap] ActParams (last entry: evaluation scratch)
+    size_t act_cap = 0;
+    size_t slot_used = 0;  // U4 entries of `slots` handed out to garbled layers
     uint64_t mult_stride = 0;
     uint32_t sum_p = 0;
 };
@@ -1113,15 +1133,38 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, Lanes& in, Lane
     P.blob = n.blob.as<U4>() + l.ct_base;
     P.blob_stride = c.total_cts;
     for (int i = 0; i < k; ++i) {
-        P.in[i] = in.lane[i]->as<uint32_t>();
         P.out[i] = out.lane[i]->as<uint32_t>();
+        P.out_kind[i] = l.tape->out_kind[i];
+        P.out_wire[i] = l.tape->out_wire[i];
     }
     P.rk = n.rk.as<uint32_t>();
     P.mult = n.mult.as<uint32_t>();
     P.mult_stride = n.mult_stride;
-    n.slots.ensure((size_t)l.tape->nslots * n.B * l.E_out * 16);
+    const size_t slot_words = (size_t)l.tape->nslots * n.B * l.E_out;
+    if (garbler) {
+        // Inputs stay resident until the combined tape launch; the outputs
+        // (pure PRF functions) are written now so the next layer can proceed.
+        const size_t j = n.act_host.size();
+        if (n.act_in.size() <= j) n.act_in.emplace_back(std::make_unique<Lanes>());
+        Lanes& keep = *n.act_in[j];
+        keep.ensure(c.base, n.B, l.E_out);
+        for (int i = 0; i < k; ++i) {
+            dev::d2d(keep.lane[i]->p, in.lane[i]->p,
+                     (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * l.E_out * 4, g_stream);
+            P.in[i] = keep.lane[i]->as<uint32_t>();
+        }
+        P.slots = n.slots.as<U4>() + n.slot_used;
+        n.slot_used += slot_words;
+        uint16_t primes[MAXK];
+        fill_primes(c.base, primes);
+        launch_act_outputs(P, primes, g_stream);
+        n.act_host.push_back(P);
+        return;
+    }
+    for (int i = 0; i < k; ++i) P.in[i] = in.lane[i]->as<uint32_t>();
     P.slots = n.slots.as<U4>();
-    launch_act(P, garbler, l.tape->nslots, g_stream);
+    dev::h2d(n.act_dev.as<ActParams>() + n.act_cap - 1, &P, sizeof P, g_stream);
+    launch_act_multi(n.act_dev.as<ActParams>() + n.act_cap - 1, &P, 1, false, g_stream);
 }
 
 static void network_reserve(Network& n, uint32_t B) {
@@ -1148,6 +1191,15 @@ static void network_reserve(Network& n, uint32_t B) {
     n.resid.ensure((size_t)B * c.n_out * k);
     n.err.ensure(16);
     n.base.ensure(c.base, B, c.n_in);
+    size_t slot_total = 0, nact = 0;
+    for (const auto& l : c.layers)
+        if (l.tape) {
+            slot_total += (size_t)l.tape->nslots * B * l.E_out;
+            ++nact;
+        }
+    n.slots.ensure(std::max<size_t>(slot_total, 1) * 16);
+    n.act_cap = nact + 1;
+    n.act_dev.ensure(n.act_cap * sizeof(ActParams));
 }
 
 // garble (garble.cpp:134-240), batched: inference b uses seeds[b]
@@ -1193,9 +1245,15 @@ static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds
                  (size_t)B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_in * 4, g_stream);
     Lanes* cur = &n.ping;
     Lanes* nxt = &n.pong;
+    n.act_host.clear();
+    n.slot_used = 0;
     for (const auto& l : c.layers) {
         run_layer(n, l, true, *cur, *nxt);
         std::swap(cur, nxt);
+    }
+    if (!n.act_host.empty()) {
+        dev::h2d(n.act_dev.p, n.act_host.data(), n.act_host.size() * sizeof(ActParams), g_stream);
+        launch_act_multi(n.act_dev.as<ActParams>(), n.act_host.data(), (int)n.act_host.size(), true, g_stream);
     }
     // decoding tables from the final base labels
     DecodeParams D;
@@ -1954,6 +2012,8 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
         if (!c->workspace) {
             c->workspace = std::make_unique<Network>();
             c->workspace->c = c;
+            c->workspace->bin = std::make_unique<Bundle>();
+            c->workspace->bout = std::make_unique<Bundle>();
         }
         Network& n = *c->workspace;
         uint32_t chunk = batch;
@@ -1963,7 +2023,8 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
         }
         dashgpu_timing tm;
         std::memset(&tm, 0, sizeof tm);
-        Bundle in, out;
+        Bundle& in = *n.bin;
+        Bundle& out = *n.bout;
         for (uint32_t b0 = 0; b0 < batch; b0 += chunk) {
             const uint32_t B = std::min(chunk, batch - b0);
             const auto a = clk::now();

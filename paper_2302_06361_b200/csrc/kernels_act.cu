@@ -12,39 +12,65 @@ __constant__ uint16_t c_modslot[MAXMOD + 1];
 __device__ uint32_t g_T0[256];
 }  // namespace dashgpu
 #define DASH_CONST_DEFINED 1
+#include <algorithm>
+#include <cstring>
+
 #include "kernels_common.cuh"
 
 namespace dashgpu {
 
 namespace {
 
-// Shared memory per CTA: static T-table s_T (32 KB) + dynamic: 4 label buffers of NWMAX words
-// per lane (word w of buffer j for lane l at L[((warp*4 + j)*NWMAX + w)*32 + l]).
-constexpr int kBufWords = 4 * NWMAX * 32;
+// Shared memory per CTA: static T-table s_T (32 KB) + dynamic per-lane label
+// buffers X (NWMAX words), K (4 words: the Z_2-sized y operand of half
+// gates, checked by the tape builder), A, T (NWMAX words each); word w of a
+// buffer at base + w*32 + lane.  24 warps x 8 KB + 32 KB = 224 KB.
+constexpr int kLaneWords = 3 * NWMAX + 4;
+constexpr int kBufWords = kLaneWords * 32;
 
 template <bool G>
-__global__ void __launch_bounds__(kActWarps * 32, 2) act_kernel(ActParams P) {
+__global__ void __launch_bounds__(kActWarps * 32, 1)
+    act_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
     extern __shared__ uint4 smem4[];
     uint32_t* L = reinterpret_cast<uint32_t*>(smem4);
     fill_T(s_T, g_T0);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t wpi = (P.E + 31) / 32;
-    const uint64_t gw = (uint64_t)blockIdx.x * kActWarps + warp;
-    const uint32_t b = (uint32_t)(gw / wpi);
-    const uint32_t u = (uint32_t)(gw % wpi) * 32 + lane;
-    if (b >= P.B || u >= P.E) return;
+    const uint32_t total = map.base[map.n];
     uint32_t* lb = L + (uint64_t)warp * kBufWords + lane;
     Elt e;
-    e.b = b;
-    e.u = u;
     e.X = LB{lb, 32};
     e.K = LB{lb + NWMAX * 32, 32};
-    e.A = LB{lb + 2 * NWMAX * 32, 32};
-    e.T = LB{lb + 3 * NWMAX * 32, 32};
+    e.A = LB{lb + (NWMAX + 4) * 32, 32};
+    e.T = LB{lb + (2 * NWMAX + 4) * 32, 32};
     e.t = make_tab(s_T, lane);
-    e.rk = nullptr;
-    e.mult = nullptr;
-    act_element<G>(P, e);
+    // first round: item = warp * grid + cta spreads small launches over all
+    // SMs; afterwards warps pull items from the counter (balanced tail)
+    uint32_t item = warp * gridDim.x + blockIdx.x;
+    const uint32_t first = kActWarps * gridDim.x;
+    for (;;) {
+        if (item >= total) break;
+        uint32_t li = 0;
+        while (li + 1 < map.n && item >= map.base[li + 1]) ++li;
+        const uint32_t local = item - map.base[li];
+        const ActParams& P = layers[li];
+        e.b = local / map.wpi[li];
+        e.u = (local % map.wpi[li]) * 32 + lane;
+        e.rk = nullptr;
+        e.mult = nullptr;
+        if (e.u < P.E) act_element<G>(P, e);
+        __syncwarp();
+        uint32_t next = 0;
+        if (lane == 0) next = first + atomicAdd(counter, 1u);
+        item = __shfl_sync(0xffffffffu, next, 0);
+    }
+}
+
+__global__ void __launch_bounds__(128) act_out_kernel(ActParams P, uint32_t p, int lane_i) {
+    fill_T(s_T, g_T0);
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= P.E) return;
+    uint32_t buf[2][NWMAX];
+    act_output_thread(P, blockIdx.y, u, lane_i, p, LB{buf[0], 1}, LB{buf[1], 1}, make_tab(s_T, threadIdx.x & 31u));
 }
 
 }  // namespace
@@ -56,21 +82,53 @@ void upload_act(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot
     ck(cudaMemcpyToSymbol(g_T0, T0, sizeof(uint32_t) * 256), "g_T0(act)");
 }
 
-void launch_act(const ActParams& P, bool garble, int nslots, void* st) {
-    if (P.B == 0 || P.E == 0) return;
+static uint32_t* act_counter() {
+    static uint32_t* counter = nullptr;
+    if (!counter) ck(cudaMalloc(&counter, 64 * sizeof(uint32_t)), "counter");
+    return counter;
+}
+
+static int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "dev");
+        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+    }
+    return sms;
+}
+
+void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* st) {
+    ItemMap map;
+    std::memset(&map, 0, sizeof map);
+    map.n = (uint32_t)n;
+    for (int i = 0; i < n; ++i) {
+        map.wpi[i] = (host_layers[i].E + 31) / 32;
+        map.base[i + 1] = map.base[i] + host_layers[i].B * map.wpi[i];
+    }
+    if (map.base[n] == 0) return;
     ProfScope ps(garble ? K_ACT_GARBLE : K_ACT_EVAL, S(st));
-    const uint64_t warps = (uint64_t)P.B * ((P.E + 31) / 32);
-    const uint32_t grid = cdiv(warps, kActWarps);
-    (void)nslots;  // slots live in global memory (P.slots)
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), cdiv(map.base[n], kActWarps));
     const size_t smem = sizeof(uint32_t) * (size_t)kActWarps * kBufWords;  // + static s_T (32 KB)
+    uint32_t* counter = act_counter();
+    ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
     if (garble) {
         ck(cudaFuncSetAttribute(act_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_kernel<true><<<grid, kActWarps * 32, smem, S(st)>>>(P);
+        act_kernel<true><<<grid, kActWarps * 32, smem, S(st)>>>(dev_layers, map, counter);
     } else {
         ck(cudaFuncSetAttribute(act_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_kernel<false><<<grid, kActWarps * 32, smem, S(st)>>>(P);
+        act_kernel<false><<<grid, kActWarps * 32, smem, S(st)>>>(dev_layers, map, counter);
     }
     ck(cudaGetLastError(), "act launch");
+}
+
+void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* st) {
+    if (P.B == 0 || P.E == 0) return;
+    ProfScope ps(K_SETUP, S(st));
+    for (int i = 0; i < P.k; ++i) {
+        act_out_kernel<<<dim3(cdiv(P.E, 128), P.B), 128, 0, S(st)>>>(P, primes[i], i);
+        ck(cudaGetLastError(), "act outputs launch");
+    }
 }
 
 }  // namespace dashgpu

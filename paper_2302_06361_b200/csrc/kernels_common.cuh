@@ -13,7 +13,7 @@
 
 namespace dashgpu {
 
-constexpr int kActWarps = 8;  // warps per CTA of the activation kernels
+constexpr int kActWarps = 24;  // warps per CTA of the activation kernels (one CTA per SM)
 constexpr int kTWords = 256 * 32;
 
 inline void ck(cudaError_t e, const char* what) {

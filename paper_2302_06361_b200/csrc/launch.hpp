@@ -47,7 +47,11 @@ enum KernelKind {
     K_NKINDS = 9
 };
 
-void launch_act(const ActParams& P, bool garble, int nslots, void* stream);
+// Activation tapes of n layers in one persistent launch (dev_layers: the same
+// ActParams array in device memory).
+void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* stream);
+// Garbler-side output labels of an activation layer (pure PRF functions).
+void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* stream);
 void launch_linear(const LinParams& L, void* stream);
 void launch_private(const PrivParams& P, void* stream);
 void launch_setup(const SetupParams& S, void* stream);

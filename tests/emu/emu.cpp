@@ -55,8 +55,7 @@ void prof_reset() {}
 int prof_read(double*, uint64_t*, int) { return 0; }
 }  // namespace dev
 
-void launch_act(const ActParams& P, bool garble, int nslots, void*) {
-    (void)nslots;
+static void act_layer(const ActParams& P, bool garble) {
 #pragma omp parallel for collapse(2) schedule(dynamic, 16)
     for (int64_t b = 0; b < (int64_t)P.B; ++b)
         for (int64_t u = 0; u < (int64_t)P.E; ++u) {
@@ -73,6 +72,21 @@ void launch_act(const ActParams& P, bool garble, int nslots, void*) {
             e.mult = nullptr;
             if (garble) act_element<true>(P, e);
             else act_element<false>(P, e);
+        }
+}
+
+void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void*) {
+    (void)host_layers;
+    for (int i = 0; i < n; ++i) act_layer(dev_layers[i], garble);
+}
+
+void launch_act_outputs(const ActParams& P, const uint16_t* primes, void*) {
+#pragma omp parallel for collapse(2)
+    for (int64_t b = 0; b < (int64_t)P.B; ++b)
+        for (int64_t u = 0; u < (int64_t)P.E; ++u) {
+            uint32_t buf[2][NWMAX];
+            for (int i = 0; i < P.k; ++i)
+                act_output_thread(P, (uint32_t)b, (uint32_t)u, i, primes[i], LB{buf[0], 1}, LB{buf[1], 1}, tab());
         }
 }
 
