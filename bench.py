@@ -48,10 +48,12 @@ def parse():
     return ap.parse_args()
 
 
-def seeds_for(step, rank, batch):
-    # hex(0x5eed0000 + global index), big-endian 16 bytes (seed_from_string)
-    base = (step * 4096 + rank) * batch
-    return b"".join(int(0x5EED0000 + base + b).to_bytes(16, "big") for b in range(batch))
+def seeds_for(step, rank, world, batch):
+    """This rank's shard of the step's fresh seeds (paper_2302_06361_b200.shard)."""
+    from paper_2302_06361_b200.shard import shard_range, step_seeds
+
+    a, b = shard_range(world * batch, world, rank)
+    return b"".join(step_seeds(step, world * batch)[a:b])
 
 
 class ClockSampler:
@@ -215,7 +217,7 @@ def main():
     host_x = rng.integers(-7, 8, size=(B, n_in)).astype(np.int64)
     dev_x = torch.from_numpy(host_x).cuda()
     dev_out = torch.zeros((B, n_out), dtype=torch.int64, device="cuda")
-    steps_seeds = [seeds_for(s, rank, B) for s in range(args.warmup + args.steps)]
+    steps_seeds = [seeds_for(s, rank, world, B) for s in range(args.warmup + args.steps)]
     dev_seeds = [torch.frombuffer(bytearray(s), dtype=torch.uint8).cuda() for s in steps_seeds]
     gathered = torch.zeros((world * B, n_out), dtype=torch.int64, device="cuda")
 

@@ -1,0 +1,65 @@
+"""N>1 path on CPU: two gloo ranks shard a batch of inferences, each garbles /
+evaluates its shard (CPU emulation of the device code), and the decoded
+outputs are all-gathered; the result must equal one process doing the whole
+batch.  On the GPU box the same code path runs with NCCL (bench.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import EMU_LIB, ROOT
+from paper_2302_06361_b200.shard import shard_range, step_seeds
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, B, out_path):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2302_06361_b200.engine import Dash
+    from paper_2302_06361_b200.shard import gather_outputs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    eng = Dash(lib_path=EMU_LIB)
+    g = eng.model("model_tiny", 1000, 8)
+    seeds = step_seeds(0, B)
+    a, b = shard_range(B, world, rank)
+    x = np.stack([g.random_input(4000 + i) for i in range(a, b)])
+    out, _ = eng.infer(g, b"".join(seeds[a:b]), x)
+    full = gather_outputs(out, B, g.info.n_out)
+    if rank == 0:
+        np.save(out_path, full)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_ranges_cover_batch():
+    for B in (1, 7, 64, 65):
+        for world in (1, 2, 3, 8):
+            rs = [shard_range(B, world, r) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == B
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+
+
+@pytest.mark.skipif(not os.path.exists(EMU_LIB), reason="emulation library not built")
+def test_two_rank_gloo_gather_equals_single_process(tmp_path, emu):
+    B = 5
+    out_path = str(tmp_path / "gathered.npy")
+    mp.spawn(_worker, args=(2, _free_port(), B, out_path), nprocs=2, join=True)
+    gathered = np.load(out_path)
+    g = emu.model("model_tiny", 1000, 8)
+    x = np.stack([g.random_input(4000 + i) for i in range(B)])
+    single, _ = emu.infer(g, b"".join(step_seeds(0, B)), x)
+    assert gathered.shape == single.shape
+    assert (gathered == single).all()
