@@ -88,7 +88,7 @@ template <class RK>
 DASH_HD U4 aes_core(U4 s, const RK& rk, const AesTab& t) {
     uint32_t s0 = s.x[0] ^ rk(0), s1 = s.x[1] ^ rk(1), s2 = s.x[2] ^ rk(2), s3 = s.x[3] ^ rk(3);
 #if defined(__CUDA_ARCH__)
-#pragma unroll
+#pragma unroll 1
 #endif
     for (int r = 1; r < 10; ++r) {
         const uint32_t t0 = tlo(t, ob0(s0)) ^ rotl32(tlo(t, ob1(s1)), 8) ^ rotl32(tlo(t, ob2(s2)), 16) ^
@@ -648,17 +648,54 @@ DASH_HD const uint32_t* mult_row(const Elt& e, uint32_t m, uint32_t v) {
     return e.mult + ((uint64_t)c_modslot[m] * 128u + v) * NWMAX;
 }
 
+#if defined(__CUDA_ARCH__)
+#define DASH_NI __device__ __noinline__
+#else
+#define DASH_NI static inline
+#endif
+DASH_NI void operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m);
+DASH_NI void store_n(U4* slot, LB L, uint32_t m);
+
 DASH_HD void load_operand(LB L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M) {
-    if (v >= IN_LANE) {
-        const int lane = v - IN_LANE;
-        lb_load_rows(L, P.in[lane] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, M);
-    } else {
-        lb_decompress(L, e.slot0[(uint64_t)v * e.sstride], M);
-    }
+    if (v >= IN_LANE) operand_n(L, P.in[v - IN_LANE] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, nullptr, M.m);
+    else operand_n(L, nullptr, 0, e.slot0 + (uint64_t)v * e.sstride, M.m);
 }
 
 DASH_HD void store_slot(const Elt& e, uint8_t s, LB L, const ModC& M) {
-    e.slot0[(uint64_t)s * e.sstride] = lb_compress(L, M);
+    store_n(e.slot0 + (uint64_t)s * e.sstride, L, M.m);
+}
+
+// Single-copy helpers (called once per gadget, not per row): keeps the
+// instruction working set of 24 co-resident warps inside the I-cache.
+DASH_NI void prf_n(LB L, uint64_t wire, uint32_t stream, uint32_t m, const uint32_t* rk, AesTab t) {
+    lb_prf(L, wire, stream, c_mod[m], rk, t);
+}
+// operand from an input lane (row pointer of this element) or from a slot
+DASH_NI void operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m) {
+    if (rows) lb_load_rows(L, rows, E, c_mod[m]);
+    else lb_decompress(L, *slot, c_mod[m]);
+}
+DASH_NI void store_n(U4* slot, LB L, uint32_t m) { *slot = lb_compress(L, c_mod[m]); }
+
+// The garbling row loop of every projection / half gate (one copy):
+// row(a) = (cin + a) mod p, key X + aR_p (X advances), payload
+// base + phi(a) R_q (phi table) or base + (a r mod p) R_p (phi == nullptr);
+// GRR stores row j at R[j-1] and drops row 0 (gadgets.hpp:156-175, 195-219, 244-252).
+DASH_NI void garble_rows_n(LB X, LB base, LB T, AesTab t, const uint32_t* mult, uint32_t p, uint32_t q, uint32_t cin,
+                           uint64_t g, const uint8_t* phi, uint32_t r, U4* R, int grr) {
+    const ModC& Mp = c_mod[p];
+    const ModC& Mq = c_mod[q];
+    const uint32_t* Rp = mult + ((uint64_t)c_modslot[p] * 128u + 1) * NWMAX;
+    const uint32_t* Mrow = mult + (uint64_t)c_modslot[q] * 128u * NWMAX;
+    for (uint32_t a = 0; a < p; ++a) {
+        uint32_t row = cin + a;
+        row = row >= p ? row - p : row;
+        const U4 H = hash_tw(lb_key_step(X, Rp, Mp), g, row, 0, t);
+        const uint32_t v = phi ? phi[a] : (a * r) % p;
+        const U4 ct = lb_enc(H, base, Mrow + (uint64_t)v * NWMAX, nullptr, 0, T, Mq);
+        if (!grr) R[row] = ct;
+        else if (row != 0) R[row - 1] = ct;
+    }
 }
 
 // ---- garbling of one op (gadgets.hpp) ----
@@ -675,7 +712,7 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             load_operand(e.X, P, e, op.a, Mp);
             const uint32_t cin = lb_color(e.X, Mp);
             if (op.kind == OP_PROJ) {
-                lb_prf(e.A, e.wire0 + op.wire_off, 0, Mq, e.rk, e.t);
+                prf_n(e.A, e.wire0 + op.wire_off, 0, op.qm, e.rk, e.t);
             } else {
                 // out0 = -pad(key0, {g,0,0}) - phi(a0) R_q, key0 = in + a0 R_p
                 const uint32_t a0 = cin == 0 ? 0 : p - cin;
@@ -686,15 +723,7 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
                 lb_neg(e.A, Mq);
                 lb_sub_g(e.A, mult_row(e, op.qm, phi[a0]), Mq);
             }
-            const uint32_t* Rp = mult_row(e, p, 1);
-            for (uint32_t a = 0; a < p; ++a) {
-                uint32_t row = cin + a;
-                row = row >= p ? row - p : row;
-                const U4 H = hash_tw(lb_key_step(e.X, Rp, Mp), g, row, 0, e.t);
-                const U4 ct = lb_enc(H, e.A, mult_row(e, op.qm, phi[a]), nullptr, 0, e.T, Mq);
-                if (op.kind == OP_PROJ) R[row] = ct;
-                else if (row != 0) R[row - 1] = ct;
-            }
+            garble_rows_n(e.X, e.A, e.T, e.t, e.mult, p, op.qm, cin, g, phi, 0, R, op.kind == OP_GRR);
             store_slot(e, op.out, e.A, Mq);
             break;
         }
@@ -712,19 +741,13 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const uint32_t cx = lb_color(e.X, Mp);
             const uint32_t r = mm ? cx : cy;
             // garbler rows: key x + aR_p, payload u0 + (a r mod p) R_p, slot 0
-            lb_prf(e.A, e.wire0 + op.wire_off, 0, Mp, e.rk, e.t);
+            prf_n(e.A, e.wire0 + op.wire_off, 0, op.pm, e.rk, e.t);
             const U4 u0c = lb_compress(e.A, Mp);
-            const uint32_t* Rp = mult_row(e, p, 1);
             // X is the running key here (K only holds the Z_2-sized y operand)
-            for (uint32_t a = 0; a < p; ++a) {
-                uint32_t row = cx + a;
-                row = row >= p ? row - p : row;
-                const U4 H = hash_tw(lb_key_step(e.X, Rp, Mp), g, row, 0, e.t);
-                R[row] = lb_enc(H, e.A, mult_row(e, p, (a * r) % p), nullptr, 0, e.T, Mp);
-            }
+            garble_rows_n(e.X, e.A, e.T, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0);
             // evaluator rows: key y + bR_q, payload v0 - s x, slot 1
             load_operand(e.X, P, e, op.a, Mp);
-            lb_prf(e.A, e.wire0 + op.wire_off + 1, 0, Mp, e.rk, e.t);
+            prf_n(e.A, e.wire0 + op.wire_off + 1, 0, op.pm, e.rk, e.t);
             load_operand(e.K, P, e, op.b, Mq);
             const uint32_t* Rq = mult_row(e, q, 1);
             const uint32_t fw = field_width(p);
