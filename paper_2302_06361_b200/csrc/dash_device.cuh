@@ -51,10 +51,18 @@ struct U4 {
 // T0[x] = (2S, S, S, 3S) as little-endian bytes; T1..T3 are byte rotations.
 // The table is replicated 32x in shared memory (entry x of lane l at
 // T[x*32 + l]) so the 32 lanes of a warp never bank-conflict.
+// T-tables in shared memory, 256-byte rows: row x holds 32 lane replicas of
+// T0[x] (bytes 0..127) and of T2[x] = rot16(T0[x]) (bytes 128..255), so
+//  * one PRMT turns state byte r into the row offset (byte << 8) | lane*4
+//    (| 128 for T2) -- no shift/mask pair per lookup;
+//  * T0[a] ^ T1[b] ^ T2[c] ^ T3[d] = T0[a] ^ T2[c] ^ rot8(T0[b] ^ T2[d]),
+//    one rotation per column instead of three;
+//  * the 32 replicas keep every warp-wide lookup bank-conflict free.
+// The table is the first 64 KB of dynamic shared memory of every kernel
+// that hashes (link-time-constant base: LDS [R + 0]).
+constexpr int kTabWords = 256 * 64;
 #if defined(__CUDACC__)
-// The replicated T-table lives at a link-time-constant shared address, so a
-// lookup is SHF + LOP3 (byte -> row offset | lane*4) + LDS [R + imm].
-__shared__ uint32_t s_T[256 * 32];
+extern __shared__ uint32_t s_dyn[];
 #endif
 
 struct AesTab {
@@ -69,55 +77,60 @@ DASH_HD AesTab make_tab(const uint32_t* T, uint32_t lane) {
     return t;
 }
 
-// Entry at byte offset `off` = x * 128 + 4 * lane (x = table index).
+DASH_HD uint32_t bperm(uint32_t x, uint32_t y, uint32_t sel) {
+#if defined(__CUDA_ARCH__)
+    return __byte_perm(x, y, sel);
+#else
+    const uint64_t v = ((uint64_t)y << 32) | x;
+    uint32_t r = 0;
+    for (int i = 0; i < 4; ++i) r |= (uint32_t)((v >> (8 * ((sel >> (4 * i)) & 7))) & 0xff) << (8 * i);
+    return r;
+#endif
+}
+
 DASH_HD uint32_t tlo(const AesTab& t, uint32_t off) {
 #if defined(__CUDA_ARCH__)
     (void)t;
-    return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(s_T) + off);
+    return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(s_dyn) + off);
 #else
     return t.T[off >> 2];
 #endif
 }
 
-#define ob0(s) ((((s) << 7) & 0x7F80u) | t.l4)
-#define ob1(s) ((((s) >> 1) & 0x7F80u) | t.l4)
-#define ob2(s) ((((s) >> 9) & 0x7F80u) | t.l4)
-#define ob3(s) ((((s) >> 17) & 0x7F80u) | t.l4)
-
 template <class RK>
 DASH_HD U4 aes_core(U4 s, const RK& rk, const AesTab& t) {
+    const uint32_t L0 = t.l4, L2 = t.l4 | 0x80u;
+#define P0(v, r) bperm((v), L0, 0x5504u | ((r) << 4))
+#define P2(v, r) bperm((v), L2, 0x5504u | ((r) << 4))
+#define COL(a, b, c, d, k) \
+    (tlo(t, P0(a, 0)) ^ tlo(t, P2(c, 2)) ^ rotl32(tlo(t, P0(b, 1)) ^ tlo(t, P2(d, 3)), 8) ^ (k))
     uint32_t s0 = s.x[0] ^ rk(0), s1 = s.x[1] ^ rk(1), s2 = s.x[2] ^ rk(2), s3 = s.x[3] ^ rk(3);
 #if defined(__CUDA_ARCH__)
 #pragma unroll 1
 #endif
     for (int r = 1; r < 10; ++r) {
-        const uint32_t t0 = tlo(t, ob0(s0)) ^ rotl32(tlo(t, ob1(s1)), 8) ^ rotl32(tlo(t, ob2(s2)), 16) ^
-                            rotl32(tlo(t, ob3(s3)), 24) ^ rk(4 * r);
-        const uint32_t t1 = tlo(t, ob0(s1)) ^ rotl32(tlo(t, ob1(s2)), 8) ^ rotl32(tlo(t, ob2(s3)), 16) ^
-                            rotl32(tlo(t, ob3(s0)), 24) ^ rk(4 * r + 1);
-        const uint32_t t2 = tlo(t, ob0(s2)) ^ rotl32(tlo(t, ob1(s3)), 8) ^ rotl32(tlo(t, ob2(s0)), 16) ^
-                            rotl32(tlo(t, ob3(s1)), 24) ^ rk(4 * r + 2);
-        const uint32_t t3 = tlo(t, ob0(s3)) ^ rotl32(tlo(t, ob1(s0)), 8) ^ rotl32(tlo(t, ob2(s1)), 16) ^
-                            rotl32(tlo(t, ob3(s2)), 24) ^ rk(4 * r + 3);
+        const uint32_t t0 = COL(s0, s1, s2, s3, rk(4 * r));
+        const uint32_t t1 = COL(s1, s2, s3, s0, rk(4 * r + 1));
+        const uint32_t t2 = COL(s2, s3, s0, s1, rk(4 * r + 2));
+        const uint32_t t3 = COL(s3, s0, s1, s2, rk(4 * r + 3));
         s0 = t0;
         s1 = t1;
         s2 = t2;
         s3 = t3;
     }
     // last round: S-box = byte 1 of T0 (no MixColumns)
-#define DASH_SB(o) ((tlo(t, (o)) >> 8) & 0xffu)
+#define SB(v, r) ((tlo(t, P0(v, r)) >> 8) & 0xffu)
     U4 o;
-    o.x[0] = (DASH_SB(ob0(s0)) | (DASH_SB(ob1(s1)) << 8) | (DASH_SB(ob2(s2)) << 16) | (DASH_SB(ob3(s3)) << 24)) ^ rk(40);
-    o.x[1] = (DASH_SB(ob0(s1)) | (DASH_SB(ob1(s2)) << 8) | (DASH_SB(ob2(s3)) << 16) | (DASH_SB(ob3(s0)) << 24)) ^ rk(41);
-    o.x[2] = (DASH_SB(ob0(s2)) | (DASH_SB(ob1(s3)) << 8) | (DASH_SB(ob2(s0)) << 16) | (DASH_SB(ob3(s1)) << 24)) ^ rk(42);
-    o.x[3] = (DASH_SB(ob0(s3)) | (DASH_SB(ob1(s0)) << 8) | (DASH_SB(ob2(s1)) << 16) | (DASH_SB(ob3(s2)) << 24)) ^ rk(43);
-#undef DASH_SB
+    o.x[0] = (SB(s0, 0) | (SB(s1, 1) << 8) | (SB(s2, 2) << 16) | (SB(s3, 3) << 24)) ^ rk(40);
+    o.x[1] = (SB(s1, 0) | (SB(s2, 1) << 8) | (SB(s3, 2) << 16) | (SB(s0, 3) << 24)) ^ rk(41);
+    o.x[2] = (SB(s2, 0) | (SB(s3, 1) << 8) | (SB(s0, 2) << 16) | (SB(s1, 3) << 24)) ^ rk(42);
+    o.x[3] = (SB(s3, 0) | (SB(s0, 1) << 8) | (SB(s1, 2) << 16) | (SB(s2, 3) << 24)) ^ rk(43);
+#undef SB
+#undef COL
+#undef P2
+#undef P0
     return o;
 }
-#undef ob0
-#undef ob1
-#undef ob2
-#undef ob3
 
 struct RkConst {
     DASH_HD uint32_t operator()(int i) const { return c_pi_rk[i]; }
@@ -487,10 +500,22 @@ DASH_HD void lb_decompress(LB out, const U4& c, const ModC& M) {
     digits_stream(c, M, [&](int w, uint32_t v) { out[w] = v; });
 }
 
+// c += v * pw (4-limb accumulator, v < 2^28)
+DASH_HD void mac_128(uint32_t c[4], const uint32_t pw[4], uint32_t v) {
+    uint64_t t = (uint64_t)pw[0] * v + c[0];
+    c[0] = (uint32_t)t;
+    t = (uint64_t)pw[1] * v + c[1] + (t >> 32);
+    c[1] = (uint32_t)t;
+    t = (uint64_t)pw[2] * v + c[2] + (t >> 32);
+    c[2] = (uint32_t)t;
+    c[3] = (uint32_t)((uint64_t)pw[3] * v + c[3] + (t >> 32));
+}
+
 // Row encryption (cipher.cpp:27-29 with the payload of gadgets.hpp):
 //   ct = compress(decompress_mod(H, q) + base [+ g] [- s*sub])
-// tmp is scratch (may not alias base/sub).
-DASH_HD U4 lb_enc(const U4& H, LB base, const uint32_t* g, LB* sub, uint32_t s, LB tmp, const ModC& M) {
+// The pad digits stream out low word first; the ciphertext is accumulated
+// low-first as sum_w value(word_w) * (m^4)^w, so no scratch label is needed.
+DASH_HD U4 lb_enc(const U4& H, LB base, const uint32_t* g, LB* sub, uint32_t s, const ModC& M) {
     if (M.pow2) {
         U4 t;
         for (int i = 0; i < 4; ++i) t.x[i] = H.x[i] & M.bits[i];
@@ -503,13 +528,55 @@ DASH_HD U4 lb_enc(const U4& H, LB base, const uint32_t* g, LB* sub, uint32_t s, 
         if (sub) t = p2_sub(t, p2_scale(lb_u4(*sub), s, M), M);
         return t;
     }
+    uint32_t c[4] = {0, 0, 0, 0}, pw[4] = {1, 0, 0, 0};
     digits_stream(H, M, [&](int w, uint32_t v) {
         uint32_t t = swar_add(v, base[w], M);
         if (g) t = swar_add(t, g[w], M);
         if (sub) t = swar_add(t, M.spread - scale_word((*sub)[w], s, M), M);
-        tmp[w] = t;
+        const uint32_t cv = (t & 0xff) + M.m * (((t >> 8) & 0xff) + M.m * (((t >> 16) & 0xff) + M.m * (t >> 24)));
+        mac_128(c, pw, cv);
+        mul_add_128(pw, M.m4, 0);
     });
-    return lb_compress(tmp, M);
+    U4 o;
+    o.x[0] = c[0];
+    o.x[1] = c[1];
+    o.x[2] = c[2];
+    o.x[3] = c[3];
+    return o;
+}
+
+// out += digits(c)  (componentwise, streamed: no scratch label)
+DASH_HD void lb_add_c(LB out, const U4& c, const ModC& M) {
+    if (M.pow2) {
+        U4 a = lb_u4(out);
+        uint32_t y[4];
+        for (int i = 0; i < 4; ++i) y[i] = c.x[i] & M.bits[i];
+        p2_add(a.x, y, M);
+        lb_set_u4(out, a);
+        return;
+    }
+    digits_stream(c, M, [&](int w, uint32_t v) { out[w] = swar_add(out[w], v, M); });
+}
+// out -= digits(c)
+DASH_HD void lb_sub_c(LB out, const U4& c, const ModC& M) {
+    if (M.pow2) {
+        U4 y;
+        for (int i = 0; i < 4; ++i) y.x[i] = c.x[i] & M.bits[i];
+        lb_set_u4(out, p2_sub(lb_u4(out), y, M));
+        return;
+    }
+    digits_stream(c, M, [&](int w, uint32_t v) { out[w] = swar_add(out[w], M.spread - v, M); });
+}
+// out += s * x
+DASH_HD void lb_add_scaled(LB out, LB x, uint32_t s, const ModC& M) {
+    if (M.pow2) {
+        U4 a = lb_u4(out);
+        const U4 y = p2_scale(lb_u4(x), s, M);
+        p2_add(a.x, y.x, M);
+        lb_set_u4(out, a);
+        return;
+    }
+    for (int w = 0; w < M.nw; ++w) out[w] = swar_add(out[w], scale_word(x[w], s, M), M);
 }
 
 // Row decryption (cipher.cpp:36-38): out = decompress_mod(ct) - decompress_mod(H)
@@ -630,8 +697,8 @@ struct ItemMap {
     uint32_t wpi[MAXK];
 };
 
-// Working buffers of one element: X (first operand / key), K (second key),
-// A (fresh / accumulated label), T (scratch).
+// Working buffers of one element: X (first operand / running key), K (the
+// Z_2-sized second operand of half gates), A (fresh / accumulated label).
 struct Elt {
     uint32_t b, u;
     uint64_t gate0, wire0;
@@ -640,7 +707,7 @@ struct Elt {
     const uint32_t* mult;
     U4* slot0;          // slot s at slot0[s * sstride]
     uint64_t sstride;
-    LB X, K, A, T;
+    LB X, K, A;
     AesTab t;
 };
 
@@ -665,6 +732,25 @@ DASH_HD void store_slot(const Elt& e, uint8_t s, LB L, const ModC& M) {
     store_n(e.slot0 + (uint64_t)s * e.sstride, L, M.m);
 }
 
+// L += operand v (streamed, no scratch label)
+DASH_NI void add_operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m) {
+    const ModC& M = c_mod[m];
+    if (!rows) {
+        lb_add_c(L, *slot, M);
+    } else if (!M.pow2) {
+        for (int w = 0; w < M.nw; ++w) L[w] = swar_add(L[w], rows[(uint64_t)w * E], M);
+    } else {
+        uint32_t tmp[4];
+        const LB T{tmp, 1};
+        lb_load_rows(T, rows, E, M);
+        lb_add(L, T, M);
+    }
+}
+DASH_HD void add_operand(LB L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M) {
+    if (v >= IN_LANE) add_operand_n(L, P.in[v - IN_LANE] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, nullptr, M.m);
+    else add_operand_n(L, nullptr, 0, e.slot0 + (uint64_t)v * e.sstride, M.m);
+}
+
 // Single-copy helpers (called once per gadget, not per row): keeps the
 // instruction working set of 24 co-resident warps inside the I-cache.
 DASH_NI void prf_n(LB L, uint64_t wire, uint32_t stream, uint32_t m, const uint32_t* rk, AesTab t) {
@@ -681,7 +767,7 @@ DASH_NI void store_n(U4* slot, LB L, uint32_t m) { *slot = lb_compress(L, c_mod[
 // row(a) = (cin + a) mod p, key X + aR_p (X advances), payload
 // base + phi(a) R_q (phi table) or base + (a r mod p) R_p (phi == nullptr);
 // GRR stores row j at R[j-1] and drops row 0 (gadgets.hpp:156-175, 195-219, 244-252).
-DASH_NI void garble_rows_n(LB X, LB base, LB T, AesTab t, const uint32_t* mult, uint32_t p, uint32_t q, uint32_t cin,
+DASH_NI void garble_rows_n(LB X, LB base, AesTab t, const uint32_t* mult, uint32_t p, uint32_t q, uint32_t cin,
                            uint64_t g, const uint8_t* phi, uint32_t r, U4* R, int grr) {
     const ModC& Mp = c_mod[p];
     const ModC& Mq = c_mod[q];
@@ -692,7 +778,7 @@ DASH_NI void garble_rows_n(LB X, LB base, LB T, AesTab t, const uint32_t* mult, 
         row = row >= p ? row - p : row;
         const U4 H = hash_tw(lb_key_step(X, Rp, Mp), g, row, 0, t);
         const uint32_t v = phi ? phi[a] : (a * r) % p;
-        const U4 ct = lb_enc(H, base, Mrow + (uint64_t)v * NWMAX, nullptr, 0, T, Mq);
+        const U4 ct = lb_enc(H, base, Mrow + (uint64_t)v * NWMAX, nullptr, 0, Mq);
         if (!grr) R[row] = ct;
         else if (row != 0) R[row - 1] = ct;
     }
@@ -716,14 +802,14 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             } else {
                 // out0 = -pad(key0, {g,0,0}) - phi(a0) R_q, key0 = in + a0 R_p
                 const uint32_t a0 = cin == 0 ? 0 : p - cin;
-                lb_copy(e.T, e.X, Mp);
-                lb_add_g(e.T, mult_row(e, p, a0), Mp);
-                const U4 H0 = hash_tw(lb_compress(e.T, Mp), g, 0, 0, e.t);
+                lb_copy(e.A, e.X, Mp);
+                lb_add_g(e.A, mult_row(e, p, a0), Mp);
+                const U4 H0 = hash_tw(lb_compress(e.A, Mp), g, 0, 0, e.t);
                 lb_decompress(e.A, H0, Mq);
                 lb_neg(e.A, Mq);
                 lb_sub_g(e.A, mult_row(e, op.qm, phi[a0]), Mq);
             }
-            garble_rows_n(e.X, e.A, e.T, e.t, e.mult, p, op.qm, cin, g, phi, 0, R, op.kind == OP_GRR);
+            garble_rows_n(e.X, e.A, e.t, e.mult, p, op.qm, cin, g, phi, 0, R, op.kind == OP_GRR);
             store_slot(e, op.out, e.A, Mq);
             break;
         }
@@ -744,7 +830,7 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             prf_n(e.A, e.wire0 + op.wire_off, 0, op.pm, e.rk, e.t);
             const U4 u0c = lb_compress(e.A, Mp);
             // X is the running key here (K only holds the Z_2-sized y operand)
-            garble_rows_n(e.X, e.A, e.T, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0);
+            garble_rows_n(e.X, e.A, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0);
             // evaluator rows: key y + bR_q, payload v0 - s x, slot 1
             load_operand(e.X, P, e, op.a, Mp);
             prf_n(e.A, e.wire0 + op.wire_off + 1, 0, op.pm, e.rk, e.t);
@@ -762,23 +848,21 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
                 const U4 Kc = lb_key_step(e.K, Rq, Mq);
                 const U4 H = hash_tw(Kc, g, row, 1, e.t);
                 LB X = e.X;
-                R[p + row] = lb_enc(H, e.A, nullptr, &X, mm ? s : row, e.T, Mp);
+                R[p + row] = lb_enc(H, e.A, nullptr, &X, mm ? s : row, Mp);
                 if (mm) {  // encrypt_short field of this row (cipher.cpp:45-60)
                     const U4 Hs = hash_tw(Kc, g, 0, 2, e.t);
                     u4_or_shl(sb, (s ^ (Hs.x[0] & fmask)) & fmask, fw * row);
                 }
             }
             if (mm) R[p + q] = sb;
-            lb_decompress(e.T, u0c, Mp);
-            lb_sub(e.A, e.T, Mp);
+            lb_sub_c(e.A, u0c, Mp);  // out = v0 - u0
             store_slot(e, op.out, e.A, Mp);
             break;
         }
         case OP_ADD: {
             const ModC& M = c_mod[op.qm];
             load_operand(e.A, P, e, op.a, M);
-            load_operand(e.T, P, e, op.b, M);
-            lb_add(e.A, e.T, M);
+            add_operand(e.A, P, e, op.b, M);
             store_slot(e, op.out, e.A, M);
             break;
         }
@@ -849,8 +933,8 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             load_operand(e.X, P, e, op.a, Mp);
             load_operand(e.K, P, e, op.b, Mq);
             const uint32_t cx = lb_color(e.X, Mp), cy = lb_color(e.K, Mq);
-            // u = Dec(x, {g,cx,0}); out = Dec(y, {g,cy,1}) (+ s x) - u
-            lb_dec(e.T, R[cx], hash_tw(lb_compress(e.X, Mp), g, cx, 0, e.t), Mp);
+            // u = Dec(x, {g,cx,0}); out = Dec(y, {g,cy,1}) (+ s x) - u, all streamed
+            const U4 Hx = hash_tw(lb_compress(e.X, Mp), g, cx, 0, e.t);
             const U4 Ky = lb_compress(e.K, Mq);
             lb_dec(e.A, R[p + cy], hash_tw(Ky, g, cy, 1, e.t), Mp);
             uint32_t s = cy;
@@ -861,17 +945,16 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
                 const uint32_t field = u4_shr_low(R[p + q], fw * cy) & fmask;
                 s = ((field ^ (Hs.x[0] & fmask)) & fmask) % p;
             }
-            lb_sub(e.A, e.T, Mp);
-            lb_scale(e.T, e.X, s, Mp);
-            lb_add(e.A, e.T, Mp);
+            lb_add_scaled(e.A, e.X, s, Mp);
+            lb_sub_c(e.A, R[cx], Mp);  // - u = - (decompress(ct_x) - pad_x)
+            lb_add_c(e.A, Hx, Mp);
             store_slot(e, op.out, e.A, Mp);
             break;
         }
         case OP_ADD: {
             const ModC& M = c_mod[op.qm];
             load_operand(e.A, P, e, op.a, M);
-            load_operand(e.T, P, e, op.b, M);
-            lb_add(e.A, e.T, M);
+            add_operand(e.A, P, e, op.b, M);
             store_slot(e, op.out, e.A, M);
             break;
         }

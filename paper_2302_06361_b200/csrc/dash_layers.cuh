@@ -141,7 +141,7 @@ DASH_HD void private_thread(const PrivParams& P, uint32_t b, uint32_t u, const A
                 uint32_t row = c + a;
                 row = row >= p ? row - p : row;
                 const U4 H = hash_tw(lb_key_step(X, Rp, M), g, row, 0, t);
-                R[row] = lb_enc(H, term, mult_row(e, p, (w * a) % p), nullptr, 0, tmp, M);
+                R[row] = lb_enc(H, term, mult_row(e, p, (w * a) % p), nullptr, 0, M);
             }
         } else {
             lb_dec(term, R[c], hash_tw(lb_compress(X, M), g, c, 0, t), M);

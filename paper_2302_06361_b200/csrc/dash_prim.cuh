@@ -36,7 +36,7 @@ DASH_HD void prim_thread(const PrimParams& P, uint32_t i, const AesTab& t) {
             lb_decompress(A, P.in[i], Mk);
             lb_decompress(B, P.out[i], Mq);
             const U4 H = hash_tw(lb_compress(A, Mk), P.gate, i % 7u, i % 3u, t);
-            P.out[i] = lb_enc(H, B, nullptr, nullptr, 0, T, Mq);
+            P.out[i] = lb_enc(H, B, nullptr, nullptr, 0, Mq);
             break;
         }
         case 5: {  // decrypt_label

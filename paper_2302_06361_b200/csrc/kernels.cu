@@ -45,24 +45,24 @@ __global__ void __launch_bounds__(128) linear_kernel(LinParams L) {
 }
 
 __global__ void __launch_bounds__(128) private_kernel(PrivParams P) {
-    fill_T(s_T, g_T0);
+    fill_T(g_T0);
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= P.M) return;
-    private_thread(P, blockIdx.y, u, make_tab(s_T, threadIdx.x & 31u));
+    private_thread(P, blockIdx.y, u, make_tab(nullptr, threadIdx.x & 31u));
 }
 
 __global__ void __launch_bounds__(128) setup_offsets_kernel(SetupParams Sp) {
-    fill_T(s_T, g_T0);
+    fill_T(g_T0);
     const uint32_t si = blockIdx.x * blockDim.x + threadIdx.x;
     if (si >= Sp.nslot) return;
-    setup_offsets_thread(Sp, blockIdx.y, si, make_tab(s_T, threadIdx.x & 31u));
+    setup_offsets_thread(Sp, blockIdx.y, si, make_tab(nullptr, threadIdx.x & 31u));
 }
 
 __global__ void __launch_bounds__(128) setup_labels_kernel(SetupParams Sp) {
-    fill_T(s_T, g_T0);
+    fill_T(g_T0);
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e > Sp.n_in) return;
-    setup_labels_thread(Sp, blockIdx.z, e, (int)blockIdx.y, make_tab(s_T, threadIdx.x & 31u));
+    setup_labels_thread(Sp, blockIdx.z, e, (int)blockIdx.y, make_tab(nullptr, threadIdx.x & 31u));
 }
 
 __global__ void __launch_bounds__(128) encode_kernel(EncodeParams P) {
@@ -96,10 +96,10 @@ __global__ void __launch_bounds__(128) decompress_kernel(CompressParams P, uint3
 }
 
 __global__ void __launch_bounds__(128) prim_kernel(PrimParams P) {
-    fill_T(s_T, g_T0);
+    fill_T(g_T0);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.n) return;
-    prim_thread(P, i, make_tab(s_T, threadIdx.x & 31u));
+    prim_thread(P, i, make_tab(nullptr, threadIdx.x & 31u));
 }
 
 }  // namespace
@@ -184,15 +184,18 @@ void launch_linear(const LinParams& L, void* st) {
 void launch_private(const PrivParams& P, void* st) {
     if (P.B == 0 || P.M == 0) return;
     ProfScope ps(P.garbler ? K_PRIV_GARBLE : K_PRIV_EVAL, S(st));
-    private_kernel<<<dim3(cdiv(P.M, 128), P.B), 128, 0, S(st)>>>(P);
+    ck(cudaFuncSetAttribute(private_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    private_kernel<<<dim3(cdiv(P.M, 128), P.B), 128, kTabBytes, S(st)>>>(P);
     dev::check();
 }
 
 void launch_setup(const SetupParams& Sp, void* st) {
     ProfScope ps(K_SETUP, S(st));
-    setup_offsets_kernel<<<dim3(cdiv(Sp.nslot, 128), Sp.B), 128, 0, S(st)>>>(Sp);
+    ck(cudaFuncSetAttribute(setup_offsets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    setup_offsets_kernel<<<dim3(cdiv(Sp.nslot, 128), Sp.B), 128, kTabBytes, S(st)>>>(Sp);
     dev::check();
-    setup_labels_kernel<<<dim3(cdiv(Sp.n_in + 1, 128), Sp.k, Sp.B), 128, 0, S(st)>>>(Sp);
+    ck(cudaFuncSetAttribute(setup_labels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    setup_labels_kernel<<<dim3(cdiv(Sp.n_in + 1, 128), Sp.k, Sp.B), 128, kTabBytes, S(st)>>>(Sp);
     dev::check();
 }
 
@@ -227,7 +230,8 @@ void launch_decompress(const CompressParams& P, uint32_t* lane_out, void* st) {
 }
 
 void launch_prim(const PrimParams& P, void* st) {
-    prim_kernel<<<cdiv(P.n, 128), 128, 0, S(st)>>>(P);
+    ck(cudaFuncSetAttribute(prim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    prim_kernel<<<cdiv(P.n, 128), 128, kTabBytes, S(st)>>>(P);
     dev::check();
 }
 

@@ -21,19 +21,18 @@ namespace dashgpu {
 
 namespace {
 
-// Shared memory per CTA: static T-table s_T (32 KB) + dynamic per-lane label
+// Dynamic shared memory per CTA: AES tables (64 KB) + per-lane label
 // buffers X (NWMAX words), K (4 words: the Z_2-sized y operand of half
-// gates, checked by the tape builder), A, T (NWMAX words each); word w of a
-// buffer at base + w*32 + lane.  24 warps x 8 KB + 32 KB = 224 KB.
-constexpr int kLaneWords = 3 * NWMAX + 4;
+// gates, checked by the tape builder), A (NWMAX words); word w of a buffer at
+// base + w*32 + lane.  28 warps x 5.5 KB + 64 KB = 218 KB.
+constexpr int kLaneWords = 2 * NWMAX + 4;
 constexpr int kBufWords = kLaneWords * 32;
 
 template <bool G>
 __global__ void __launch_bounds__(kActWarps * 32, 1)
     act_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
-    extern __shared__ uint4 smem4[];
-    uint32_t* L = reinterpret_cast<uint32_t*>(smem4);
-    fill_T(s_T, g_T0);
+    uint32_t* L = s_dyn + kTabWords;
+    fill_T(g_T0);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t total = map.base[map.n];
     uint32_t* lb = L + (uint64_t)warp * kBufWords + lane;
@@ -41,8 +40,7 @@ __global__ void __launch_bounds__(kActWarps * 32, 1)
     e.X = LB{lb, 32};
     e.K = LB{lb + NWMAX * 32, 32};
     e.A = LB{lb + (NWMAX + 4) * 32, 32};
-    e.T = LB{lb + (2 * NWMAX + 4) * 32, 32};
-    e.t = make_tab(s_T, lane);
+    e.t = make_tab(nullptr, lane);
     // first round: item = warp * grid + cta spreads small launches over all
     // SMs; afterwards warps pull items from the counter (balanced tail)
     uint32_t item = warp * gridDim.x + blockIdx.x;
@@ -66,11 +64,11 @@ __global__ void __launch_bounds__(kActWarps * 32, 1)
 }
 
 __global__ void __launch_bounds__(128) act_out_kernel(ActParams P, uint32_t p, int lane_i) {
-    fill_T(s_T, g_T0);
+    fill_T(g_T0);
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= P.E) return;
     uint32_t buf[2][NWMAX];
-    act_output_thread(P, blockIdx.y, u, lane_i, p, LB{buf[0], 1}, LB{buf[1], 1}, make_tab(s_T, threadIdx.x & 31u));
+    act_output_thread(P, blockIdx.y, u, lane_i, p, LB{buf[0], 1}, LB{buf[1], 1}, make_tab(nullptr, threadIdx.x & 31u));
 }
 
 }  // namespace
@@ -109,7 +107,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     if (map.base[n] == 0) return;
     ProfScope ps(garble ? K_ACT_GARBLE : K_ACT_EVAL, S(st));
     const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), cdiv(map.base[n], kActWarps));
-    const size_t smem = sizeof(uint32_t) * (size_t)kActWarps * kBufWords;  // + static s_T (32 KB)
+    const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kActWarps * kBufWords;
     uint32_t* counter = act_counter();
     ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
     if (garble) {
@@ -126,7 +124,8 @@ void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* st) {
     if (P.B == 0 || P.E == 0) return;
     ProfScope ps(K_SETUP, S(st));
     for (int i = 0; i < P.k; ++i) {
-        act_out_kernel<<<dim3(cdiv(P.E, 128), P.B), 128, 0, S(st)>>>(P, primes[i], i);
+        ck(cudaFuncSetAttribute(act_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+        act_out_kernel<<<dim3(cdiv(P.E, 128), P.B), 128, kTabBytes, S(st)>>>(P, primes[i], i);
         ck(cudaGetLastError(), "act outputs launch");
     }
 }

@@ -9,7 +9,7 @@
 #include <string>
 #include <vector>
 
-#include "launch.hpp"
+#include "dash_prim.cuh"
 
 namespace dashgpu {
 
@@ -54,10 +54,15 @@ struct ProfScope {
     }
 };
 
-// Replicates T0 32x into shared memory: entry x of lane l at T[x*32 + l].
-__device__ __forceinline__ void fill_T(uint32_t* T, const uint32_t* T0) {
-    for (int i = threadIdx.x; i < kTWords; i += blockDim.x) T[i] = T0[i >> 5];
+// Fills the AES tables at the start of dynamic shared memory (layout in
+// dash_device.cuh: 256-byte rows of 32 T0 replicas then 32 T2 replicas).
+__device__ __forceinline__ void fill_T(const uint32_t* T0) {
+    for (int i = threadIdx.x; i < kTabWords; i += blockDim.x) {
+        const uint32_t v = T0[i >> 6];
+        s_dyn[i] = (i & 32) ? __funnelshift_l(v, v, 16) : v;
+    }
     __syncthreads();
 }
+constexpr size_t kTabBytes = sizeof(uint32_t) * kTabWords;
 
 }  // namespace dashgpu

@@ -22,7 +22,7 @@ uint16_t c_modslot[MAXMOD + 1];
 
 namespace dashgpu {
 
-static uint32_t g_T[256 * 32];
+static uint32_t g_T[256 * 64];
 
 static AesTab tab() { return make_tab(g_T, 0); }
 
@@ -48,7 +48,10 @@ void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* m
     std::memcpy(c_mod, mods, sizeof(ModC) * (MAXMOD + 1));
     std::memcpy(c_pi_rk, pi_rk, sizeof(uint32_t) * 44);
     std::memcpy(c_modslot, modslot, sizeof(uint16_t) * (MAXMOD + 1));
-    for (int i = 0; i < 256 * 32; ++i) g_T[i] = T0[i >> 5];
+    for (int i = 0; i < 256 * 64; ++i) {
+        const uint32_t v = T0[i >> 6];
+        g_T[i] = (i & 32) ? ((v << 16) | (v >> 16)) : v;
+    }
 }
 void prof_enable(int) {}
 void prof_reset() {}
@@ -59,14 +62,13 @@ static void act_layer(const ActParams& P, bool garble) {
 #pragma omp parallel for collapse(2) schedule(dynamic, 16)
     for (int64_t b = 0; b < (int64_t)P.B; ++b)
         for (int64_t u = 0; u < (int64_t)P.E; ++u) {
-            uint32_t buf[4][NWMAX];
+            uint32_t buf[3][NWMAX];
             Elt e;
             e.b = (uint32_t)b;
             e.u = (uint32_t)u;
             e.X = LB{buf[0], 1};
             e.K = LB{buf[1], 1};
             e.A = LB{buf[2], 1};
-            e.T = LB{buf[3], 1};
             e.t = tab();
             e.rk = nullptr;
             e.mult = nullptr;
