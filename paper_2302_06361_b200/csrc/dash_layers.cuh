@@ -29,6 +29,12 @@ struct LinParams {
     int garbler;
 };
 
+struct LinMulti {
+    LinParams L[MAXK];
+    uint32_t wbase[MAXK];
+    int n;
+};
+
 DASH_HD void linear_thread(const LinParams& L, uint32_t b, uint32_t w, uint32_t u) {
     const ModC& M = c_mod[L.p];
     uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
@@ -120,8 +126,8 @@ DASH_HD void private_thread(const PrivParams& P, uint32_t b, uint32_t u, const A
     }
     const uint8_t* wr = P.wres + (uint64_t)(P.conv ? oc : u) * P.win;
     const uint32_t* Rp = P.garbler ? mult_row(e, p, 1) : nullptr;
-    uint32_t buf[4][NWMAX];
-    const LB X{buf[0], 1}, term{buf[1], 1}, sum{buf[2], 1}, tmp{buf[3], 1};
+    uint32_t buf[3][NWMAX];
+    const LB X{buf[0], 1}, term{buf[1], 1}, sum{buf[2], 1};
     for (uint32_t j = 0; j < P.win; ++j) {
         uint64_t xi;
         if (!P.conv) {

@@ -7,8 +7,8 @@
 namespace dashgpu {
 
 DASH_HD void prim_thread(const PrimParams& P, uint32_t i, const AesTab& t) {
-    uint32_t buf[3][NWMAX] = {};
-    const LB A{buf[0], 1}, B{buf[1], 1}, T{buf[2], 1};
+    uint32_t buf[2][NWMAX] = {};
+    const LB A{buf[0], 1}, B{buf[1], 1};
     switch (P.op) {
         case 0: {  // decompress_mod + compress (label.cpp:208-232)
             const ModC& M = c_mod[P.m];

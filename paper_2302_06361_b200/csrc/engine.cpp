@@ -1050,8 +1050,9 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, Lanes& in, Lane
     }
     out.ensure(c.base, n.B, l.E_out);
     if (l.linear() && !l.priv) {
+        LinParams Ls[MAXK];
         for (int i = 0; i < k; ++i) {
-            LinParams L;
+            LinParams& L = Ls[i];
             std::memset(&L, 0, sizeof L);
             L.conv = l.kind == DASH_LAYER_CONV2D;
             L.K = l.K;
@@ -1078,8 +1079,8 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, Lanes& in, Lane
             L.B = n.B;
             L.zstride = (uint32_t)(k * LABW);  // zero / R rows are [B][k][LABW]
             L.garbler = garbler;
-            launch_linear(L, g_stream);
         }
+        launch_linear(Ls, k, g_stream);
         return;
     }
     if (l.linear()) {

@@ -38,10 +38,15 @@ void prof_drain() {
     prof().pending.clear();
 }
 
-__global__ void __launch_bounds__(128) linear_kernel(LinParams L) {
+// All k residue lanes of one linear layer in one launch: blockIdx.y walks the
+// (lane, word) pairs, lane boundaries in LinMulti::wbase.
+__global__ void __launch_bounds__(128) linear_kernel(const __grid_constant__ LinMulti Lm) {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    int i = 0;
+    while (i + 1 < Lm.n && blockIdx.y >= Lm.wbase[i + 1]) ++i;
+    const LinParams& L = Lm.L[i];
     if (u >= L.M) return;
-    linear_thread(L, blockIdx.z, blockIdx.y, u);
+    linear_thread(L, blockIdx.z, blockIdx.y - Lm.wbase[i], u);
 }
 
 __global__ void __launch_bounds__(128) private_kernel(PrivParams P) {
@@ -173,11 +178,19 @@ int prof_read(double* ms, uint64_t* n, int maxk) {
 
 }  // namespace dev
 
-void launch_linear(const LinParams& L, void* st) {
-    if (L.B == 0 || L.M == 0) return;
+void launch_linear(const LinParams* Ls, int n, void* st) {
+    if (n <= 0 || Ls[0].B == 0 || Ls[0].M == 0) return;
     ProfScope ps(K_LINEAR, S(st));
-    dim3 grid(cdiv(L.M, 128), L.nw, L.B);
-    linear_kernel<<<grid, 128, 0, S(st)>>>(L);
+    LinMulti Lm;
+    Lm.n = n;
+    uint32_t w = 0;
+    for (int i = 0; i < n; ++i) {
+        Lm.L[i] = Ls[i];
+        Lm.wbase[i] = w;
+        w += Ls[i].nw;
+    }
+    dim3 grid(cdiv(Ls[0].M, 128), w, Ls[0].B);
+    linear_kernel<<<grid, 128, 0, S(st)>>>(Lm);
     dev::check();
 }
 

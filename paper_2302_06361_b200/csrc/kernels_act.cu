@@ -63,12 +63,20 @@ __global__ void __launch_bounds__(kActWarps * 32, 1)
     }
 }
 
-__global__ void __launch_bounds__(128) act_out_kernel(ActParams P, uint32_t p, int lane_i) {
+// All k lanes of one layer in one launch: thread (lane i, element u) of
+// inference blockIdx.y; elements are padded to whole warps per lane so the
+// modulus is warp-uniform.
+struct Primes {
+    uint16_t p[MAXK];
+};
+__global__ void __launch_bounds__(256) act_out_kernel(ActParams P, Primes pr, uint32_t epad) {
     fill_T(g_T0);
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= P.E) return;
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t i = idx / epad, u = idx % epad;
+    if (i >= (uint32_t)P.k || u >= P.E) return;
     uint32_t buf[2][NWMAX];
-    act_output_thread(P, blockIdx.y, u, lane_i, p, LB{buf[0], 1}, LB{buf[1], 1}, make_tab(nullptr, threadIdx.x & 31u));
+    act_output_thread(P, blockIdx.y, u, (int)i, pr.p[i], LB{buf[0], 1}, LB{buf[1], 1},
+                      make_tab(nullptr, threadIdx.x & 31u));
 }
 
 }  // namespace
@@ -106,7 +114,9 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     }
     if (map.base[n] == 0) return;
     ProfScope ps(garble ? K_ACT_GARBLE : K_ACT_EVAL, S(st));
-    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), cdiv(map.base[n], kActWarps));
+    // one CTA per SM (the first round strides items across SMs), never fewer
+    // CTAs than needed to give every item its own SM when items < #SMs
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), map.base[n]);
     const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kActWarps * kBufWords;
     uint32_t* counter = act_counter();
     ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
@@ -123,11 +133,12 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
 void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* st) {
     if (P.B == 0 || P.E == 0) return;
     ProfScope ps(K_SETUP, S(st));
-    for (int i = 0; i < P.k; ++i) {
-        ck(cudaFuncSetAttribute(act_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
-        act_out_kernel<<<dim3(cdiv(P.E, 128), P.B), 128, kTabBytes, S(st)>>>(P, primes[i], i);
-        ck(cudaGetLastError(), "act outputs launch");
-    }
+    Primes pr;
+    for (int i = 0; i < MAXK; ++i) pr.p[i] = i < P.k ? primes[i] : 0;
+    const uint32_t epad = (P.E + 31) / 32 * 32;
+    ck(cudaFuncSetAttribute(act_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    act_out_kernel<<<dim3(cdiv((uint64_t)epad * P.k, 256), P.B), 256, kTabBytes, S(st)>>>(P, pr, epad);
+    ck(cudaGetLastError(), "act outputs launch");
 }
 
 }  // namespace dashgpu

@@ -52,7 +52,7 @@ enum KernelKind {
 void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* stream);
 // Garbler-side output labels of an activation layer (pure PRF functions).
 void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* stream);
-void launch_linear(const LinParams& L, void* stream);
+void launch_linear(const LinParams* Ls, int n, void* stream);  // all lanes of a layer
 void launch_private(const PrivParams& P, void* stream);
 void launch_setup(const SetupParams& S, void* stream);
 void launch_encode(const EncodeParams& P, void* stream);

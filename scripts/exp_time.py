@@ -18,4 +18,5 @@ for path in sys.argv[1:]:
     dt = (time.time() - t) / 4
     p = E.profile_read()
     print(f"{os.path.basename(path)}: {B/dt:.1f} inf/s  act_garble {p['act_garble'][0]/4:.2f} ms  act_eval {p['act_eval'][0]/4:.2f} ms  out0={out[0][:3]}", flush=True)
+    print("   " + "  ".join(f"{k} {v[0]/4:.2f}ms/{v[1]//4}" for k, v in p.items() if v[1]), flush=True)
     del E

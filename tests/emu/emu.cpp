@@ -92,11 +92,14 @@ void launch_act_outputs(const ActParams& P, const uint16_t* primes, void*) {
         }
 }
 
-void launch_linear(const LinParams& L, void*) {
+void launch_linear(const LinParams* Ls, int n, void*) {
+    for (int i = 0; i < n; ++i) {
+        const LinParams& L = Ls[i];
 #pragma omp parallel for collapse(3)
-    for (int64_t b = 0; b < (int64_t)L.B; ++b)
-        for (int64_t w = 0; w < (int64_t)L.nw; ++w)
-            for (int64_t u = 0; u < (int64_t)L.M; ++u) linear_thread(L, (uint32_t)b, (uint32_t)w, (uint32_t)u);
+        for (int64_t b = 0; b < (int64_t)L.B; ++b)
+            for (int64_t w = 0; w < (int64_t)L.nw; ++w)
+                for (int64_t u = 0; u < (int64_t)L.M; ++u) linear_thread(L, (uint32_t)b, (uint32_t)w, (uint32_t)u);
+    }
 }
 
 void launch_private(const PrivParams& P, void*) {
