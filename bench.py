@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--model", default=MODEL)
     ap.add_argument("--k", type=int, default=K)
     ap.add_argument("--cpu-sample", type=int, default=0, help="inferences in the CPU-baseline sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (config sweeps)")
     return ap.parse_args()
 
 
@@ -135,6 +136,12 @@ def cpu_baseline(circuit_desc_c, n_in, n_out, sample):
 
 
 MODEL_NAME = [MODEL]
+WORKLOADS = {
+    "lenet5": "LeNet-5 restated in reference ops, 1x28x28",
+    "model_a": "784-128-128-10 ReLU MLP, testsupport::model_a",
+    "minionn": "paper Model F, MiniONN-style 7-conv CIFAR CNN, 3x32x32, ReLU",
+    "model_c": "testsupport::model_c", "model_d": "testsupport::model_d",
+}
 
 
 def run_reference(args, rank, world):
@@ -294,11 +301,24 @@ def main():
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
     launches = sum(v[1] for v in prof.values())
+    # public linear lanes on the tensor cores (tcgen05 kind::i8): algorithmic
+    # digit-MACs (K * units * sum n_p per pass, garble + eval) vs the nominal
+    # dense int8 peak; the kernel executes 4x these MACs (digit-word expansion,
+    # tc_linear.cuh) and its ncu tensor-pipe share is in profiles/.
+    lin_ms, lin_n = prof.get("linear", (0.0, 0))
+    roof_lin = None
+    if lin_n and info.linear_macs:
+        tops = 2 * 2 * info.linear_macs * B * args.steps / (lin_ms / 1e3) / 1e12
+        roof_lin = {"bound": "tensor", "achieved": tops, "peak": 4500.0, "unit": "TOPS (int8)", "frac": tops / 4500.0,
+                    "peak_source": "nominal B200 dense int8 (no measured int8 peak in MEASURED_PEAKS.json)",
+                    "kernel": "tc_linear_kernel (tcgen05.mma kind::i8, TMA weights)",
+                    "digit_macs_per_inference_pass": int(info.linear_macs),
+                    "kernel_ms_per_step": lin_ms / args.steps}
 
     cpu = None
     sample = args.cpu_sample or min(B, max(8, os.cpu_count() or 8))
     try:
-        cpu = cpu_baseline(g.to_circuit(), n_in, n_out, sample)
+        cpu = None if args.no_cpu else cpu_baseline(g.to_circuit(), n_in, n_out, sample)
     except Exception as e:  # the CPU baseline must not hide the GPU line
         cpu = {"value": None, "unit": "inferences/s", "cores": os.cpu_count(), "kind": "unavailable",
                "sample": str(e)[:200]}
@@ -316,8 +336,8 @@ def main():
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": f"{args.model} (LeNet-5 restated in reference ops) k={args.k}, synthetic 1x28x28 "
-                               f"inputs U[-7,7], batch {B} per GPU, fresh seed per inference per step",
+        "config": {"workload": f"{args.model} ({WORKLOADS.get(args.model, 'single-layer sweep')}) k={args.k}, "
+                               f"synthetic inputs U[-7,7], batch {B} per GPU, fresh seed per inference per step",
                    "global_batch": world * B, "inferences_per_gpu": B, "parallelism": f"inference-sharded x{world}",
                    "l2": "per-step garbled tables (%.1f GB) exceed L2; no flush needed" % (info.cts * 16 * B / 1e9),
                    "ciphertexts_per_inference": info.cts, "relu_elements_per_inference": info.relu_elements},
@@ -327,6 +347,7 @@ def main():
                      "bytes_per_element": bytes_per_elem,
                      "kernel_ms_per_step": act_ms / args.steps,
                      "kernel_share_of_step": (act_ms / args.steps) / (ms / args.steps)},
+        "roofline_linear": roof_lin,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "inferences/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "clocks": clk.summary(),

@@ -26,13 +26,8 @@ struct LinParams {
     const uint32_t* R;   // offset R_p (byte digits), garbler only, same stride
     uint32_t zstride;
     uint32_t p, nw, B;
+    uint32_t n, mag, sh;  // digits n_p and the x/p magic (tensor-core epilogue)
     int garbler;
-};
-
-struct LinMulti {
-    LinParams L[MAXK];
-    uint32_t wbase[MAXK];
-    int n;
 };
 
 DASH_HD void linear_thread(const LinParams& L, uint32_t b, uint32_t w, uint32_t u) {

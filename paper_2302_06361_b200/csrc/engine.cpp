@@ -774,6 +774,11 @@ struct HLayer {
     // public / private linear: per-lane residues (host) and their device copies
     std::vector<std::vector<uint8_t>> wres_h, zt_h, bres_h;
     std::vector<std::shared_ptr<DevBuf>> wres, zt, bres;
+    // public linear on the tensor cores: expanded weights + window offsets
+    std::vector<uint8_t> wexp_h;
+    std::vector<int32_t> koff_h;
+    std::shared_ptr<DevBuf> wexp, koff;
+    TcLinear tc;
     std::vector<uint64_t> lane_ct_off, lane_gate_off, lane_wire_off;  // private
     uint32_t K = 0;  // window
     // activation
@@ -858,6 +863,43 @@ static std::shared_ptr<DevBuf> upload(const void* data, size_t bytes) {
 
 static int64_t resid(int64_t w, int p) { return ((w % p) + p) % p; }
 
+// Tensor-core operands of a public linear layer (tc_linear.cuh): expanded
+// weights W'[(lane, oc, j')][(i, j)] = wres[oc][i] if j == j', zero padded to
+// whole 128-byte K stages and N tiles, and the im2col window offsets
+// koff[i] = ic*H*W + ky*W + kx (dense: i).
+static void build_tc_linear(HLayer& l, int k) {
+    const bool dense = l.kind == DASH_LAYER_DENSE;
+    const uint32_t nout = dense ? l.out_dim : l.out_ch, K = l.K;
+    TcLinear& T = l.tc;
+    T.k = (uint32_t)k;
+    T.nout = nout;
+    T.kblocks = (K + 31) / 32;
+    T.Kpad = T.kblocks * 128;
+    const uint32_t n4 = 4 * nout;
+    T.BN = n4 <= 32 ? 32 : n4 <= 64 ? 64 : n4 <= 128 ? 128 : 256;
+    T.Npad = (n4 + T.BN - 1) / T.BN * T.BN;
+    l.wexp_h.assign((size_t)k * T.Npad * T.Kpad, 0);
+    const uint64_t M = l.E_out;
+    for (int i = 0; i < k; ++i) {
+        const std::vector<uint8_t>& wr = l.wres_h[i];
+        for (uint32_t oc = 0; oc < nout; ++oc)
+            for (uint32_t j = 0; j < 4; ++j) {
+                uint8_t* row = &l.wexp_h[((size_t)i * T.Npad + 4 * oc + j) * T.Kpad];
+                for (uint32_t kw = 0; kw < K; ++kw)
+                    row[4 * kw + j] = dense ? wr[(uint64_t)kw * M + oc] : wr[(uint64_t)oc * K + kw];
+            }
+    }
+    l.koff_h.assign((size_t)T.kblocks * 32, -1);
+    for (uint32_t kw = 0; kw < K; ++kw) {
+        if (dense) {
+            l.koff_h[kw] = (int32_t)kw;
+        } else {
+            const uint32_t f = l.filter, ic = kw / (f * f), ky = (kw / f) % f, kx = kw % f;
+            l.koff_h[kw] = (int32_t)((ic * l.in_shape[1] + ky) * l.in_shape[2] + kx);
+        }
+    }
+}
+
 // validate_circuit + circuit_layout + per-layer residues and tapes (host only;
 // device copies are made lazily by upload_circuit at the first garble)
 static void prepare_circuit(dashgpu_circuit& c) {
@@ -901,6 +943,8 @@ static void prepare_circuit(dashgpu_circuit& c) {
         l.ct_base = ct;
         l.cts = l.gates = l.wires = 0;
         l.wres_h.clear();
+        l.wexp_h.clear();
+        l.koff_h.clear();
         l.zt_h.clear();
         l.bres_h.clear();
         l.lane_ct_off.clear();
@@ -929,6 +973,7 @@ static void prepare_circuit(dashgpu_circuit& c) {
                     l.wres_h.push_back(std::move(wr));
                     l.zt_h.push_back(std::move(zt));
                     l.bres_h.push_back(std::move(br));
+                    if (i == k - 1) build_tc_linear(l, k);
                 } else {
                     std::vector<uint8_t> wr(l.w.size()), br(nrow);
                     for (uint64_t row = 0; row < nrow; ++row) {
@@ -980,6 +1025,13 @@ static void upload_circuit(dashgpu_circuit& c) {
         for (auto& v : l.wres_h) l.wres.push_back(upload(v.data(), v.size()));
         for (auto& v : l.zt_h) l.zt.push_back(upload(v.data(), v.size()));
         for (auto& v : l.bres_h) l.bres.push_back(upload(v.data(), v.size()));
+        if (!l.wexp_h.empty()) {
+            l.wexp = upload(l.wexp_h.data(), l.wexp_h.size());
+            l.koff = upload(l.koff_h.data(), l.koff_h.size() * sizeof(int32_t));
+            l.tc.wexp = l.wexp->as<uint8_t>();
+            l.tc.koff = l.koff->as<int32_t>();
+            make_weight_map(l.tc);
+        }
         if (l.tape) {
             l.tape_d = upload(l.tape->ops.data(), l.tape->ops.size() * sizeof(TapeOp));
             l.phi_d = upload(l.tape->phi.data(), l.tape->phi.size());
@@ -1075,12 +1127,14 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, Lanes& in, Lane
             L.zero = n.zero.as<uint32_t>() + (uint64_t)i * LABW;
             L.R = n.Rb.as<uint32_t>() + (uint64_t)i * LABW;
             L.p = (uint32_t)c.base.primes[i];
-            L.nw = (uint32_t)(n_digits_host(L.p) + 3) / 4;
+            L.n = (uint32_t)n_digits_host(L.p);
+            L.nw = (L.n + 3) / 4;
+            magic31(L.p, L.mag, L.sh);
             L.B = n.B;
             L.zstride = (uint32_t)(k * LABW);  // zero / R rows are [B][k][LABW]
             L.garbler = garbler;
         }
-        launch_linear(Ls, k, g_stream);
+        launch_linear(Ls, k, l.tc, g_stream);
         return;
     }
     if (l.linear()) {

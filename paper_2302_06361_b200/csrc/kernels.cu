@@ -11,8 +11,11 @@ __constant__ uint16_t c_modslot[MAXMOD + 1];
 __device__ uint32_t g_T0[256];
 }  // namespace dashgpu
 #define DASH_CONST_DEFINED 1
+#include <cudaTypedefs.h>
+
 #include "dash_prim.cuh"
 #include "kernels_common.cuh"
+#include "tc_linear.cuh"
 
 namespace dashgpu {
 
@@ -36,17 +39,6 @@ void prof_drain() {
         cudaEventDestroy(p.b);
     }
     prof().pending.clear();
-}
-
-// All k residue lanes of one linear layer in one launch: blockIdx.y walks the
-// (lane, word) pairs, lane boundaries in LinMulti::wbase.
-__global__ void __launch_bounds__(128) linear_kernel(const __grid_constant__ LinMulti Lm) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    int i = 0;
-    while (i + 1 < Lm.n && blockIdx.y >= Lm.wbase[i + 1]) ++i;
-    const LinParams& L = Lm.L[i];
-    if (u >= L.M) return;
-    linear_thread(L, blockIdx.z, blockIdx.y - Lm.wbase[i], u);
 }
 
 __global__ void __launch_bounds__(128) private_kernel(PrivParams P) {
@@ -178,19 +170,78 @@ int prof_read(double* ms, uint64_t* n, int maxk) {
 
 }  // namespace dev
 
-void launch_linear(const LinParams* Ls, int n, void* st) {
+void make_weight_map(TcLinear& T) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q),
+           "cuTensorMapEncodeTiled entry point");
+        if (q != cudaDriverEntryPointSuccess || !encode) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {T.Kpad, (cuuint64_t)T.k * T.Npad};
+    const cuuint64_t strides[1] = {T.Kpad};
+    const cuuint32_t box[2] = {(cuuint32_t)tc::BKB, T.BN};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)T.wexp, dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    static_assert(sizeof(CUtensorMap) == sizeof(T.tmap), "tensor map size");
+    memcpy(T.tmap, &m, sizeof m);
+}
+
+void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     if (n <= 0 || Ls[0].B == 0 || Ls[0].M == 0) return;
     ProfScope ps(K_LINEAR, S(st));
-    LinMulti Lm;
-    Lm.n = n;
-    uint32_t w = 0;
-    for (int i = 0; i < n; ++i) {
-        Lm.L[i] = Ls[i];
-        Lm.wbase[i] = w;
-        w += Ls[i].nw;
+    tc::TcParams P;
+    memset(&P, 0, sizeof P);
+    const LinParams& L0 = Ls[0];
+    P.nl = n;
+    P.kblocks = T.kblocks;
+    P.BN = T.BN;
+    P.tiles_n = T.Npad / T.BN;
+    P.nout = T.nout;
+    if (L0.conv) {
+        P.P = L0.OH * L0.OW;
+        P.OW = L0.OW;
+        P.s = L0.stride;
+        P.W = L0.W;
+    } else {
+        P.P = 1;
+        P.OW = 1;
     }
-    dim3 grid(cdiv(Ls[0].M, 128), w, Ls[0].B);
-    linear_kernel<<<grid, 128, 0, S(st)>>>(Lm);
+    P.E_in = L0.E_in;
+    P.M = L0.M;
+    P.stages = tc::stages_for(T.BN);
+    P.zstride = L0.zstride;
+    P.garbler = L0.garbler;
+    P.koff = T.koff;
+    uint32_t tiles = 0;
+    for (int i = 0; i < n; ++i) {
+        const LinParams& L = Ls[i];
+        tc::TcLane& l = P.L[i];
+        l.in = L.in;
+        l.out = L.out;
+        l.zt = L.zt;
+        l.bres = L.bres;
+        l.zero = L.zero;
+        l.R = L.R;
+        l.p = L.p;
+        l.n = L.n;
+        l.nw = L.nw;
+        l.mag = L.mag;
+        l.sh = L.sh;
+        l.rows = L.B * L.nw * P.P;
+        l.tile_base = tiles;
+        l.wrow = (uint32_t)i * T.Npad;
+        tiles += cdiv(l.rows, tc::BM) * P.tiles_n;
+    }
+    const size_t smem = tc::smem_bytes(T.BN);
+    ck(cudaFuncSetAttribute(tc::tc_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    CUtensorMap map;
+    memcpy(&map, T.tmap, sizeof map);
+    tc::tc_linear_kernel<<<tiles, tc::kThreads, smem, S(st)>>>(map, P);
     dev::check();
 }
 

@@ -52,7 +52,19 @@ enum KernelKind {
 void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* stream);
 // Garbler-side output labels of an activation layer (pure PRF functions).
 void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* stream);
-void launch_linear(const LinParams* Ls, int n, void* stream);  // all lanes of a layer
+// Tensor-core form of one public linear layer (tc_linear.cuh): the expanded
+// weight residues of all k lanes, [k][Npad][Kpad] u8 K-major (row (oc, j'),
+// column (window index i, byte j), nonzero only for j == j'), the window
+// offset table and the TMA descriptor of the weights.
+struct TcLinear {
+    alignas(64) uint8_t tmap[128];
+    const uint8_t* wexp = nullptr;
+    const int32_t* koff = nullptr;  // [kblocks * 32] element offsets, -1 = padding
+    uint32_t kblocks = 0, Npad = 0, Kpad = 0, BN = 0, nout = 0, k = 0;
+};
+void make_weight_map(TcLinear& t);  // encodes t.tmap for t.wexp
+// all lanes of a public linear layer in one launch
+void launch_linear(const LinParams* Ls, int n, const TcLinear& tc, void* stream);
 void launch_private(const PrivParams& P, void* stream);
 void launch_setup(const SetupParams& S, void* stream);
 void launch_encode(const EncodeParams& P, void* stream);

@@ -92,7 +92,11 @@ void launch_act_outputs(const ActParams& P, const uint16_t* primes, void*) {
         }
 }
 
-void launch_linear(const LinParams* Ls, int n, void*) {
+void make_weight_map(TcLinear&) {}
+
+// the tensor-core GEMM (tc_linear.cuh) has no CPU emulation; the emulation
+// runs the same arithmetic per output word (dash_layers.cuh linear_thread)
+void launch_linear(const LinParams* Ls, int n, const TcLinear&, void*) {
     for (int i = 0; i < n; ++i) {
         const LinParams& L = Ls[i];
 #pragma omp parallel for collapse(3)

@@ -274,3 +274,47 @@ def test_sign_sweep_k2_to_k9(gpu):
         x[:, :3] = [0, 1, -1]
         out, _ = gpu.infer(g, seed_hex(0xB0 + k) + seed_hex(0xC0 + k), x)
         assert (out == np.where(x > 0, 1, -1)).all(), k
+
+
+# ------------------------------------------------- tensor-core linear lanes
+
+def _linear_case(kind):
+    """Circuits that stress the tcgen05 GEMM tiling (tc_linear.cuh): several N
+    tiles (4*out_ch > 256), many K stages, strided windows, ragged row tiles."""
+    from paper_2302_06361_b200.circuit import Circuit, conv2d, dense, flatten, relu
+
+    r = np.random.default_rng({"wide": 11, "deep": 12, "strided": 13}[kind])
+    w = lambda *s: r.integers(-2, 3, size=s)  # noqa: E731
+    b = lambda n: r.integers(-10, 11, size=n)  # noqa: E731
+    if kind == "wide":   # conv N = 512 (2 tiles), dense N = 280 (BN 256, 2 tiles)
+        L = [conv2d(3, 128, 3, 1, w(128, 3, 3, 3), b(128)), flatten(), dense(2048, 70, w(70, 2048), b(70)), relu(),
+             dense(70, 10, w(10, 70), b(10))]
+        return Circuit([3, 6, 6], 9, L)
+    if kind == "deep":   # K = 3000 window elements: 94 K stages, zero-padded tail
+        L = [dense(3000, 20, w(20, 3000), b(20)), relu(), dense(20, 3, w(3, 20), b(3))]
+        return Circuit([3000], 8, L)
+    # strided / non-square windows over ragged planes (E_in = 5*13*11)
+    L = [conv2d(5, 7, 4, 3, w(7, 5, 4, 4), b(7)), relu(), conv2d(7, 9, 2, 1, w(9, 7, 2, 2), b(9)), flatten(),
+         dense(9 * 3 * 2, 5, w(5, 54), b(5))]
+    return Circuit([5, 13, 11], 7, L)
+
+
+@pytest.mark.parametrize("kind", ["wide", "deep", "strided"])
+def test_tensor_core_linear_vs_oracle(eng, oracle, kind):
+    gpu = eng
+    c = _linear_case(kind)
+    g = gpu.circuit(c)
+    B = 5  # rows per lane = B * nw * positions: ragged 128-row tiles
+    seeds = b"".join(seed_hex(0x7C0 + i) for i in range(B))
+    x = np.random.default_rng(21).integers(-7, 8, size=(B, c.n_in)).astype(np.int64)
+    net = gpu.garble(g, seeds)
+    bo = gpu.evaluate(net, gpu.garble_inputs(net, x))
+    out = gpu.decode_outputs(net, bo)
+    for i in (0, B - 1):
+        onet = oracle.garble(c, seed_hex(0x7C0 + i))
+        assert net.export_gc(i) == onet.gc_bytes(), (kind, i)
+        assert net.export_decoding(i) == onet.dec_bytes(), (kind, i)
+        ob = oracle.evaluate(onet, oracle.garble_inputs(onet, x[i]))
+        assert bo.payload(i) == ob.payload(), (kind, i)
+        assert out[i].tolist() == oracle.decode(onet, ob).tolist()
+        assert out[i].tolist() == g.plain_forward(x[i]).tolist()
