@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--k", type=int, default=K)
     ap.add_argument("--cpu-sample", type=int, default=0, help="inferences in the CPU-baseline sample")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (config sweeps)")
+    ap.add_argument("--sweep", default="", help="label-ops sweep (BASELINE configs[4]): 'proj' and/or 'linear', "
+                                                "comma separated; --sweep-log2 / --sweep-k select the grid")
+    ap.add_argument("--sweep-log2", default="16,18,20,22,24,26")
+    ap.add_argument("--sweep-k", default="2,4,6,8")
     return ap.parse_args()
 
 
@@ -195,8 +199,78 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_sweep(args):
+    """Label-ops sweep (BASELINE configs[4]).
+
+    proj:   one ReLU layer of N = 2^j elements ({input_shape={N}, layers={relu()}},
+            reference bench_main.cpp:156-162), garbled + evaluated + decoded in
+            element chunks through dashgpu_infer_stream; a projection label-op is
+            one garbled row (garble) or one decrypted row (eval).
+    linear: Dense(1024 -> 1024) over B = N / 1024 inferences through
+            dashgpu_infer; a linear label-op is one label x scalar MAC (n_p digit
+            MACs), timed on the tcgen05 linear kernel's CUDA events.
+    One JSON line per grid point, all on one GPU (the sweep shards by element
+    range / CRT lane with no exchange)."""
+    import torch
+    from paper_2302_06361_b200.engine import Dash
+
+    eng = Dash(0)
+    eng.set_stream(torch.cuda.current_stream().cuda_stream)
+    kinds = [s for s in args.sweep.split(",") if s]
+    for kind in kinds:
+        for j in [int(v) for v in args.sweep_log2.split(",")]:
+            for k in [int(v) for v in args.sweep_k.split(",")]:
+                N = 1 << j
+                if kind == "proj":
+                    g = eng.model(f"relu{N}", 0, k)
+                    info = g.info
+                    P = 1
+                    for p in [2, 3, 5, 7, 11, 13, 17, 19][:k]:
+                        P *= p
+                    x = np.random.default_rng(j * 16 + k).integers(-(P // 2), (P + 1) // 2, size=(1, N))
+                    chunk = max(1 << 14, int(24e9 // (16 * info.act_uc_cts)))
+                    gw = eng.model("relu16384", 0, k)  # warm-up: same kernels, small layer
+                    eng.infer_stream(gw, (0x5EED).to_bytes(16, "big"), x[:, :16384] if N >= 16384 else
+                                     np.zeros((1, 16384), np.int64), 1 << 14)
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    out, tm, _ = eng.infer_stream(g, (0x5EED0001).to_bytes(16, "big"), x, chunk)
+                    sec = time.perf_counter() - t0
+                    assert (out[0] == np.maximum(x[0], 0)).all(), "ReLU sweep mismatch"
+                    rows = N * (info.act_uc_cts + info.act_eval_rows)
+                    line = {"sweep": "proj", "labels": N, "k": k, "label_ops_per_s": rows / sec,
+                            "elements_per_s": N / sec, "seconds": sec, "garbled_rows": N * info.act_uc_cts,
+                            "eval_rows": N * info.act_eval_rows, "table_bytes": 16 * N * info.act_uc_cts,
+                            "table_GBps": 16 * N * info.act_uc_cts / sec / 1e9, "chunk_elements": chunk,
+                            "chunks": tm.sub_batches, "ms_garble": tm.ms_garble, "ms_evaluate": tm.ms_evaluate}
+                else:
+                    g = eng.model("dense1024", 0, k)
+                    info = g.info
+                    B = max(1, N // 1024)
+                    seeds = b"".join(int(0x5EED0000 + b).to_bytes(16, "big") for b in range(B))
+                    x = np.random.default_rng(k).integers(-7, 8, size=(B, 1024))
+                    eng.infer(g, seeds[:16 * min(B, 4)], x[: min(B, 4)])
+                    eng.profile(True)
+                    t0 = time.perf_counter()
+                    eng.infer(g, seeds, x)
+                    sec = time.perf_counter() - t0
+                    prof = eng.profile_read()
+                    eng.profile(False)
+                    lin_ms = prof.get("linear", (0.0, 0))[0]
+                    label_macs = 2 * B * 1024 * 1024 * k  # garble + eval passes
+                    line = {"sweep": "linear", "labels": B * 1024, "k": k, "inferences": B,
+                            "label_macs_per_s_kernel": label_macs / (lin_ms / 1e3) if lin_ms else None,
+                            "digit_macs_per_s_kernel": 2 * B * info.linear_macs / (lin_ms / 1e3) if lin_ms else None,
+                            "linear_kernel_ms": lin_ms, "end_to_end_s": sec,
+                            "label_macs_per_s_e2e": label_macs / sec}
+                print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.sweep:
+        run_sweep(args)
+        return
     MODEL_NAME[0] = args.model
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -125,6 +125,19 @@ int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint
 int dashgpu_infer(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
                   const int64_t* inputs, int64_t* outputs, int on_device, dashgpu_timing* t);
 
+/* Streamed inference of a single activation-layer circuit (the label-ops
+ * sweep: {input_shape={N}, layers={relu()}}, reference bench_main.cpp:156-162,
+ * garble_layer/eval_layer layer.hpp:85-97 over element ranges).  Element
+ * chunks of chunk_elems are garbled, encoded, evaluated and decoded in turn
+ * with the reference's gate/wire/ciphertext numbering, so the tables of the
+ * whole layer (1.8 TB at N = 2^26, k = 8) never exist at once.  Host buffers:
+ * seeds [batch][16], inputs [batch][N], outputs [batch][N]; gc_out (optional,
+ * may be NULL) receives every chunk's ciphertexts, [batch][N*uc_cts][16]
+ * bytes = the layer's GarbledCircuit::cts (garble.hpp:46-53). */
+int dashgpu_infer_stream(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
+                         const int64_t* inputs, int64_t* outputs, uint64_t chunk_elems,
+                         uint8_t* gc_out, dashgpu_timing* t);
+
 /* ---- per-kernel CUDA-event timing on the launching stream ---- */
 int dashgpu_profile(int enable);
 /* kinds: 0 act-garble 1 act-eval 2 linear 3 priv-garble 4 priv-eval 5 setup 6 encode 7 decode 8 misc */

@@ -172,6 +172,7 @@ struct SetupParams {
     uint32_t* mult;            // [B][nslot][128][NWMAX]
     uint64_t mult_stride;
     uint32_t n_in;
+    uint64_t e0;               // first input element of this launch (streamed layers)
     uint32_t* base_planes[MAXK]; // [B][nw][n_in] input base labels (encoding info)
     uint32_t* zero;            // [B][k][LABW] byte-digit words
     uint32_t* Rb;              // [B][k][LABW] offsets of the primes, byte-digit words
@@ -204,7 +205,7 @@ DASH_HD void setup_labels_thread(const SetupParams& S, uint32_t b, uint32_t e, i
     const LB L{buf, 1};
     const uint32_t* rk = S.rk + (uint64_t)b * 44;
     if (e < S.n_in) {
-        lb_prf(L, (uint64_t)S.k + (uint64_t)e * S.k + (uint64_t)i, 0, M, rk, t);
+        lb_prf(L, (uint64_t)S.k + (S.e0 + e) * S.k + (uint64_t)i, 0, M, rk, t);
         lb_store_rows(L, S.base_planes[i] + ((uint64_t)b * M.nw) * S.n_in + e, S.n_in, M);
     } else {
         lb_prf(L, (uint64_t)i, 0, M, rk, t);

@@ -1389,6 +1389,27 @@ static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
                  (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_out * 4, g_stream);
 }
 
+// crt_reconstruct + decode_signed (crt.cpp:63-101) of `count` residue tuples
+static void crt_decode(const dashgpu_circuit& c, const uint8_t* res, uint64_t count, int64_t* dst) {
+    const int k = c.k;
+    const u128 half_up = (c.base.P + 1) / 2;
+    for (uint64_t e = 0; e < count; ++e) {
+        u128 acc = 0;
+        for (int i = 0; i < k; ++i) acc += c.base.coeffs[i] % c.base.P * res[e * k + i] % c.base.P;
+        acc %= c.base.P;
+        int64_t v;
+        if (acc < half_up) {
+            if (acc > (u128)INT64_MAX) throw DataError("decode_signed: value exceeds 64-bit signed range");
+            v = (int64_t)acc;
+        } else {
+            const u128 mag = c.base.P - acc;
+            if (mag > (u128)INT64_MAX) throw DataError("decode_signed: value exceeds 64-bit signed range");
+            v = -(int64_t)mag;
+        }
+        dst[e] = v;
+    }
+}
+
 // decode_outputs (garble.cpp:314-343); CRT reconstruction on the host
 static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool values_on_device) {
     dashgpu_circuit& c = *n.c;
@@ -1419,23 +1440,196 @@ static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool va
         host.resize((size_t)n.B * c.n_out);
         dst = host.data();
     }
-    for (uint64_t e = 0; e < (uint64_t)n.B * c.n_out; ++e) {
-        u128 acc = 0;
-        for (int i = 0; i < k; ++i) acc += c.base.coeffs[i] % c.base.P * res[e * k + i] % c.base.P;
-        acc %= c.base.P;
-        const u128 half_up = (c.base.P + 1) / 2;
-        int64_t v;
-        if (acc < half_up) {
-            if (acc > (u128)INT64_MAX) throw DataError("decode_signed: value exceeds 64-bit signed range");
-            v = (int64_t)acc;
-        } else {
-            const u128 mag = c.base.P - acc;
-            if (mag > (u128)INT64_MAX) throw DataError("decode_signed: value exceeds 64-bit signed range");
-            v = -(int64_t)mag;
-        }
-        dst[e] = v;
-    }
+    crt_decode(c, res.data(), (uint64_t)n.B * c.n_out, dst);
     if (values_on_device) dev::h2d(values, host.data(), host.size() * 8, g_stream);
+}
+
+// ============================================================ streamed layers
+//
+// The label-ops sweep of SURVEY.md section 8(d) is one activation layer over N
+// elements ({input_shape={N}, layers={relu()}}, bench_main.cpp:156-162); at
+// N = 2^26, k = 8 its garbled tables are 1.8 TB, so they never exist at once.
+// Element chunks [u0, u0 + C) are garbled, encoded, evaluated and decoded in
+// turn with the reference's numbering: input wire k + e*k + i
+// (garble.cpp:170), gate gate_base + u*uc.gates, wire wire_base + u*uc.wires,
+// ciphertext u*uc.cts inside the layer (layer.cpp:531-541).  Every chunk
+// buffer is C elements wide; only the id bases move.
+struct StreamWS {
+    DevBuf rk, seeds, mult, zero, Rb, commit, blob, slots, dec, vals, resid, err, actp;
+    Lanes base, in, gout, eout;
+    uint64_t C = 0;
+};
+
+static bool streamable(const dashgpu_circuit& c) {
+    return c.layers.size() == 1 && c.layers[0].tape != nullptr;
+}
+
+static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batch, const int64_t* inputs,
+                         int64_t* outputs, uint64_t chunk, uint8_t* gc_out, dashgpu_timing& tm) {
+    if (!streamable(c)) throw DataError("streamed inference needs a single activation-layer circuit");
+    upload_circuit(c);
+    const int k = c.k;
+    const HLayer& l = c.layers[0];
+    const Tape& T = *l.tape;
+    const uint64_t N = l.E_out;
+    const uint64_t C = std::max<uint64_t>(1, std::min<uint64_t>(chunk, N));
+    StreamWS w;
+    w.C = C;
+    const uint64_t mult_stride = (uint64_t)(MAXMOD - 1) * 128 * NWMAX;
+    uint32_t sum_p = 0;
+    for (int p : c.base.primes) sum_p += (uint32_t)p;
+    w.rk.ensure(44 * 4);
+    w.seeds.ensure(16);
+    w.mult.ensure(mult_stride * 4);
+    w.zero.ensure((size_t)k * LABW * 4);
+    w.Rb.ensure((size_t)k * LABW * 4);
+    w.commit.ensure(16);
+    w.blob.ensure((size_t)C * T.cts * 16);
+    w.slots.ensure(std::max<size_t>((size_t)T.nslots * C, 1) * 16);
+    w.dec.ensure((size_t)C * sum_p * 16);
+    w.vals.ensure((size_t)C * 8);
+    w.resid.ensure((size_t)C * k);
+    w.err.ensure(16);
+    w.actp.ensure(sizeof(ActParams));
+    w.base.ensure(c.base, 1, C);
+    w.in.ensure(c.base, 1, C);
+    w.gout.ensure(c.base, 1, C);
+    w.eout.ensure(c.base, 1, C);
+    std::vector<uint8_t> res(C * k);
+    using clk = std::chrono::steady_clock;
+    for (uint32_t b = 0; b < batch; ++b) {
+        uint32_t rk[44];
+        aes_expand_host(seeds + 16 * (size_t)b, rk);
+        dev::h2d(w.rk.p, rk, sizeof rk, g_stream);
+        dev::h2d(w.seeds.p, seeds + 16 * (size_t)b, 16, g_stream);
+        for (uint64_t u0 = 0; u0 < N; u0 += C) {
+            const uint32_t n = (uint32_t)std::min<uint64_t>(C, N - u0);
+            const auto t0 = clk::now();
+            // offsets, zero wires and this chunk's input base labels
+            SetupParams S;
+            std::memset(&S, 0, sizeof S);
+            S.B = 1;
+            S.k = k;
+            fill_primes(c.base, S.primes);
+            for (int m : c.moduli) S.slot_mod[S.nslot++] = (uint16_t)m;
+            S.rk = w.rk.as<uint32_t>();
+            S.seeds = w.seeds.as<uint8_t>();
+            S.mult = w.mult.as<uint32_t>();
+            S.mult_stride = mult_stride;
+            S.n_in = n;
+            S.e0 = u0;
+            for (int i = 0; i < k; ++i) S.base_planes[i] = w.base.lane[i]->as<uint32_t>();
+            S.zero = w.zero.as<uint32_t>();
+            S.Rb = w.Rb.as<uint32_t>();
+            S.commit = w.commit.as<U4>();
+            launch_setup(S, g_stream);
+            // garble the chunk: outputs (PRF functions) first, then the tapes
+            ActParams P;
+            std::memset(&P, 0, sizeof P);
+            P.tape = l.tape_d->as<TapeOp>();
+            P.n_ops = (int)T.ops.size();
+            P.phi = l.phi_d->as<uint8_t>();
+            P.k = k;
+            P.E = n;
+            P.B = 1;
+            P.gate_base = l.gate_base + u0 * T.gates;
+            P.wire_base = l.wire_base + u0 * T.wires;
+            P.uc_cts = T.cts;
+            P.uc_gates = T.gates;
+            P.uc_wires = T.wires;
+            P.blob = w.blob.as<U4>();
+            P.blob_stride = (uint64_t)n * T.cts;
+            for (int i = 0; i < k; ++i) {
+                P.in[i] = w.base.lane[i]->as<uint32_t>();
+                P.out[i] = w.gout.lane[i]->as<uint32_t>();
+                P.out_kind[i] = T.out_kind[i];
+                P.out_wire[i] = T.out_wire[i];
+            }
+            P.rk = w.rk.as<uint32_t>();
+            P.mult = w.mult.as<uint32_t>();
+            P.mult_stride = mult_stride;
+            P.slots = w.slots.as<U4>();
+            uint16_t primes[MAXK];
+            fill_primes(c.base, primes);
+            launch_act_outputs(P, primes, g_stream);
+            dev::h2d(w.actp.p, &P, sizeof P, g_stream);
+            launch_act_multi(w.actp.as<ActParams>(), &P, 1, true, g_stream);
+            DecodeParams D;
+            std::memset(&D, 0, sizeof D);
+            D.B = 1;
+            D.n_out = n;
+            D.k = k;
+            fill_primes(c.base, D.primes);
+            for (int i = 0; i < k; ++i) D.poff[i + 1] = (uint16_t)(D.poff[i] + c.base.primes[i]);
+            make_lane_ptrs(w.gout, k, D.lanes);
+            D.table = w.dec.as<U4>();
+            D.mult = w.mult.as<uint32_t>();
+            D.mult_stride = mult_stride;
+            launch_dectable(D, g_stream);
+            if (gc_out)
+                dev::d2h(gc_out + ((uint64_t)b * N * T.cts + u0 * T.cts) * 16, w.blob.p, (size_t)n * T.cts * 16,
+                         g_stream);
+            dev::sync(g_stream);
+            const auto t1 = clk::now();
+            // garble_inputs of the chunk (garble.cpp:242-263)
+            dev::h2d(w.vals.p, inputs + (uint64_t)b * N + u0, (size_t)n * 8, g_stream);
+            dev::memset0(w.err.p, 4, g_stream);
+            EncodeParams E;
+            std::memset(&E, 0, sizeof E);
+            E.B = 1;
+            E.n_in = n;
+            E.k = k;
+            fill_primes(c.base, E.primes);
+            E.values = w.vals.as<int64_t>();
+            for (int i = 0; i < k; ++i) {
+                E.base[i] = w.base.lane[i]->as<uint32_t>();
+                E.out[i] = w.in.lane[i]->as<uint32_t>();
+            }
+            E.mult = w.mult.as<uint32_t>();
+            E.mult_stride = mult_stride;
+            const u128 half_up = (c.base.P + 1) / 2, half_dn = c.base.P / 2;
+            E.half_up_lo = (uint64_t)half_up;
+            E.half_up_hi = (uint64_t)(half_up >> 64);
+            E.half_dn_lo = (uint64_t)half_dn;
+            E.half_dn_hi = (uint64_t)(half_dn >> 64);
+            E.err = w.err.as<int>();
+            launch_encode(E, g_stream);
+            int err_enc = 0;
+            dev::d2h(&err_enc, w.err.p, 4, g_stream);
+            const auto t2 = clk::now();
+            // evaluate the chunk on the active labels
+            for (int i = 0; i < k; ++i) {
+                P.in[i] = w.in.lane[i]->as<uint32_t>();
+                P.out[i] = w.eout.lane[i]->as<uint32_t>();
+            }
+            dev::h2d(w.actp.p, &P, sizeof P, g_stream);
+            launch_act_multi(w.actp.as<ActParams>(), &P, 1, false, g_stream);
+            dev::sync(g_stream);
+            const auto t3 = clk::now();
+            // decode_outputs of the chunk
+            make_lane_ptrs(w.eout, k, D.lanes);
+            D.residues = w.resid.as<uint8_t>();
+            D.err = w.err.as<int>();
+            dev::sync(g_stream);
+            if (err_enc) throw DataError("encode_signed: value outside the representable range");
+            dev::memset0(w.err.p, 4, g_stream);
+            launch_decode(D, g_stream);
+            int err = 0;
+            dev::d2h(res.data(), w.resid.p, (size_t)n * k, g_stream);
+            dev::d2h(&err, w.err.p, 4, g_stream);
+            dev::sync(g_stream);
+            if (err) throw AuthError("output label not present in the decoding table");
+            crt_decode(c, res.data(), n, outputs + (uint64_t)b * N + u0);
+            const auto t4 = clk::now();
+            tm.ms_garble += std::chrono::duration<double, std::milli>(t1 - t0).count();
+            tm.ms_encode += std::chrono::duration<double, std::milli>(t2 - t1).count();
+            tm.ms_evaluate += std::chrono::duration<double, std::milli>(t3 - t2).count();
+            tm.ms_decode += std::chrono::duration<double, std::milli>(t4 - t3).count();
+            tm.sub_batches += 1;
+        }
+    }
+    tm.h2d_bytes = (uint64_t)batch * (N * 8 + 16 + 44 * 4);
+    tm.d2h_bytes = (uint64_t)batch * N * k;
 }
 
 // ============================================================ exports
@@ -2105,6 +2299,20 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
             tm.d2h_bytes = (uint64_t)batch * c->n_out * c->k;
         }
         tm.ms_total = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+        if (t) *t = tm;
+    });
+}
+
+int dashgpu_infer_stream(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batch, const int64_t* inputs,
+                         int64_t* outputs, uint64_t chunk_elems, uint8_t* gc_out, dashgpu_timing* t) {
+    return guarded([&] {
+        auto* c = const_cast<dashgpu_circuit*>(cc);
+        std::lock_guard<std::mutex> lk(c->mu);
+        dashgpu_timing tm;
+        std::memset(&tm, 0, sizeof tm);
+        const auto t0 = std::chrono::steady_clock::now();
+        infer_stream(*c, seeds, batch, inputs, outputs, chunk_elems, gc_out, tm);
+        tm.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         if (t) *t = tm;
     });
 }

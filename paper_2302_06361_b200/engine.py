@@ -114,6 +114,7 @@ def _declare(L):
     L.dashgpu_import_bundle.argtypes = [vp, u8p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(vp)]
     L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
     L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
+    L.dashgpu_infer_stream.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
     L.dashgpu_profile.argtypes = [ctypes.c_int]
     L.dashgpu_profile_read.argtypes = [f64p, u64p, ctypes.c_int]
     L.dashgpu_prim.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u64p, u64p, u16p, u8p,
@@ -198,6 +199,23 @@ class Dash:
         self._check(self.lib.dashgpu_infer(c.h, ctypes.cast(sbuf, vp), batch, vp(x.ctypes.data),
                                            vp(out.ctypes.data), 0, ctypes.byref(t)))
         return out, t
+
+    def infer_stream(self, c: "GpuCircuit", seeds: bytes, inputs, chunk: int, want_gc: bool = False):
+        """Streamed garble + garble_inputs + evaluate + decode_outputs of a
+        single activation-layer circuit in element chunks (the label-ops
+        sweep).  Returns (outputs, timing, gc) with gc the per-inference
+        ciphertext blobs when want_gc."""
+        t = Timing()
+        batch = len(seeds) // 16
+        sbuf = (ctypes.c_uint8 * len(seeds)).from_buffer_copy(seeds)
+        x = np.ascontiguousarray(inputs, np.int64).reshape(batch, c.info.n_in)
+        out = np.zeros((batch, c.info.n_out), np.int64)
+        gc = np.zeros(batch * c.info.cts * 16, np.uint8) if want_gc else None
+        self._check(self.lib.dashgpu_infer_stream(c.h, ctypes.cast(sbuf, vp), batch, vp(x.ctypes.data),
+                                                  vp(out.ctypes.data), chunk,
+                                                  vp(gc.ctypes.data) if want_gc else None, ctypes.byref(t)))
+        gcs = [gc[b * c.info.cts * 16:(b + 1) * c.info.cts * 16].tobytes() for b in range(batch)] if want_gc else None
+        return out, t, gcs
 
     # ---- profiling ----
     def profile(self, enable: bool):

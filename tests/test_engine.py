@@ -10,7 +10,7 @@ inputs/outputs and decoded values must equal the reference byte for byte
 import numpy as np
 import pytest
 
-from helpers import golden_circuit, golden_input, pairs_u128, seed_hex, sha, u128_pairs
+from helpers import PRIMES, golden_circuit, golden_input, pairs_u128, seed_hex, sha, u128_pairs
 
 BACKENDS = [pytest.param("emu", id="emu"), pytest.param("cuda", id="cuda", marks=pytest.mark.gpu)]
 
@@ -318,3 +318,27 @@ def test_tensor_core_linear_vs_oracle(eng, oracle, kind):
         assert bo.payload(i) == ob.payload(), (kind, i)
         assert out[i].tolist() == oracle.decode(onet, ob).tolist()
         assert out[i].tolist() == g.plain_forward(x[i]).tolist()
+
+
+# ------------------------------------------------------- streamed sweep layers
+
+@pytest.mark.parametrize("name,k,chunk", [("relu3000", 4, 1024), ("sign777", 5, 100), ("relu300", 8, 300)])
+def test_streamed_layer_vs_oracle(eng, oracle, name, k, chunk):
+    # chunks of a single activation layer keep the reference's numbering:
+    # the concatenated chunk tables are the layer's GarbledCircuit::cts
+    from helpers import models
+
+    c = models.build(name, 0, k)
+    g = eng.circuit(c)
+    seeds = seed_hex(0x5A0 + k) + seed_hex(0x5B0 + k)
+    P = int(np.prod(PRIMES[:k]))
+    x = np.random.default_rng(k).integers(-(P // 2), (P + 1) // 2, size=(2, c.n_in))
+    x[:, :3] = [0, 1, -1]
+    out, t, gcs = eng.infer_stream(g, seeds, x, chunk, want_gc=True)
+    assert t.sub_batches == 2 * ((c.n_in + chunk - 1) // chunk)
+    want = np.maximum(x, 0) if name.startswith("relu") else np.where(x > 0, 1, -1)
+    assert (out == want).all()
+    onet = oracle.garble(c, seed_hex(0x5B0 + k))
+    assert gcs[1] == onet.cts().tobytes()
+    ref, _ = eng.infer(g, seeds, x)
+    assert (ref == out).all()
