@@ -248,7 +248,11 @@ def run_sweep(args):
                     info = g.info
                     B = max(1, N // 1024)
                     seeds = b"".join(int(0x5EED0000 + b).to_bytes(16, "big") for b in range(B))
-                    x = np.random.default_rng(k).integers(-7, 8, size=(B, 1024))
+                    P = 1
+                    for p in [2, 3, 5, 7, 11, 13, 17, 19][:k]:
+                        P *= p
+                    lim = min(7, P // 2 - 1)  # encodable inputs (outputs may wrap mod P: throughput only)
+                    x = np.random.default_rng(k).integers(-lim, lim + 1, size=(B, 1024))
                     eng.infer(g, seeds[:16 * min(B, 4)], x[: min(B, 4)])
                     eng.profile(True)
                     t0 = time.perf_counter()

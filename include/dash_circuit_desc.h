@@ -7,8 +7,21 @@
  * k primes, weights row-major [out][in] (Dense) or [out_ch][in_ch][f][f]
  * (Conv2d, square filters, no padding).
  *
- * Extensions beyond the reference (documented in DESIGN.md, oracle-pinned
- * only by the restatement): none in round 1.
+ * Extensions beyond the reference (parity is pinned
+ * by the C restatement only, the reference has no such layers -- SURVEY.md
+ * section 8(d) "ResNet-20 extension notes"):
+ *   DASH_LAYER_PAD2D  zero padding of a [C][H][W] tensor by `pad` cells on
+ *                     every side; pad cells hold the zero-wire label
+ *                     (garble.cpp:157: zero wire i = prf.label(i, p_i)), so
+ *                     an unmodified Conv2d after it is a padded convolution.
+ *   DASH_LAYER_ADD    lane-wise label sum of two equal-shape tensors (the
+ *                     residual add; free, like the reference's free_add,
+ *                     gadgets.hpp:108-118).
+ *   src / src2        DAG inputs: 0 = previous layer's output (the
+ *                     reference's chain), j + 1 = output of layer j, -1 = the
+ *                     circuit input.  src2 is the second operand of ADD.
+ * Layers without extensions keep src = src2 = pad = 0 and serialize exactly
+ * as the reference does.
  */
 #ifndef DASH_CIRCUIT_DESC_H
 #define DASH_CIRCUIT_DESC_H
@@ -25,7 +38,9 @@ enum {
     DASH_LAYER_CONV2D = 2,
     DASH_LAYER_RELU = 3,
     DASH_LAYER_SIGNACT = 4,
-    DASH_LAYER_FLATTEN = 5
+    DASH_LAYER_FLATTEN = 5,
+    DASH_LAYER_PAD2D = 6, /* extension */
+    DASH_LAYER_ADD = 7    /* extension */
 };
 
 typedef struct dash_layer_desc {
@@ -37,6 +52,8 @@ typedef struct dash_layer_desc {
     uint64_t n_weights;
     const int64_t* q_biases;  /* bias_count() entries, or NULL (= all zero) */
     uint64_t n_biases;
+    int32_t src, src2;        /* extension: DAG inputs (see above) */
+    uint32_t pad;             /* extension: PAD2D cells per side */
 } dash_layer_desc;
 
 typedef struct dash_circuit_desc {

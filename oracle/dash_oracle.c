@@ -974,6 +974,8 @@ static void g_act_element(octx* c, int kind, const olabel* in, olabel* out, cons
 typedef struct {
     int kind, priv;
     uint32_t in_dim, out_dim, in_ch, out_ch, filter, stride;
+    int src, src2; /* extension: DAG inputs (dash_circuit_desc.h) */
+    uint32_t pad;  /* extension: PAD2D */
     int64_t* w;
     uint64_t nw;
     int64_t* bias;
@@ -987,10 +989,17 @@ struct orc_circuit {
     double sign_target, alpha;
     int nl;
     olayer* layers;
-    /* derived */
+    /* derived: shapes[0] = input, shapes[j + 1] = output of layer j;
+     * ishapes[j] = input of layer j (from its DAG source) */
     uint32_t shapes[65][8];
     int ranks[65];
+    uint32_t ishapes[64][8];
+    int iranks[64];
 };
+
+/* index into shapes[] / the per-layer value list of a layer's DAG source:
+ * src 0 = previous layer (the reference's chain), j + 1 = layer j, -1 = input */
+static int src_index(int li, int src) { return src == 0 ? li : (src < 0 ? 0 : src); }
 
 typedef struct {
     int n; /* elements */
@@ -1031,8 +1040,16 @@ static int out_shape(const olayer* l, const uint32_t* in, int rin, uint32_t* out
         }
         case DASH_LAYER_RELU:
         case DASH_LAYER_SIGNACT:
+        case DASH_LAYER_ADD:
             memcpy(out, in, sizeof(uint32_t) * (size_t)rin);
             *rout = rin;
+            return 0;
+        case DASH_LAYER_PAD2D:
+            if (rin != 3) return fail(ORC_DATA, "pad layer needs a [C][H][W] input");
+            out[0] = in[0];
+            out[1] = in[1] + 2 * l->pad;
+            out[2] = in[2] + 2 * l->pad;
+            *rout = 3;
             return 0;
         case DASH_LAYER_FLATTEN:
             out[0] = (uint32_t)shape_size(in, rin);
@@ -1083,6 +1100,14 @@ int orc_circuit_new(const dash_circuit_desc* d, orc_circuit** out) {
         l->out_ch = s->out_ch;
         l->filter = s->filter;
         l->stride = s->stride;
+        l->src = s->src;
+        l->src2 = s->src2;
+        l->pad = s->pad;
+        if (l->src > i || l->src < -1 || l->src2 > i || l->src2 < -1 ||
+            (l->kind == DASH_LAYER_ADD && l->src2 == 0)) {
+            orc_circuit_free(c);
+            return fail(ORC_DATA, "layer input refers to a later layer");
+        }
         if (s->q_weights && s->n_weights) {
             l->nw = s->n_weights;
             l->w = (int64_t*)malloc(sizeof(int64_t) * l->nw);
@@ -1093,7 +1118,16 @@ int orc_circuit_new(const dash_circuit_desc* d, orc_circuit** out) {
             l->bias = (int64_t*)malloc(sizeof(int64_t) * l->nb);
             memcpy(l->bias, s->q_biases, sizeof(int64_t) * l->nb);
         }
-        int rc = out_shape(l, c->shapes[i], c->ranks[i], c->shapes[i + 1], &c->ranks[i + 1]);
+        const int si = src_index(i, l->src);
+        memcpy(c->ishapes[i], c->shapes[si], sizeof c->ishapes[i]);
+        c->iranks[i] = c->ranks[si];
+        int rc = out_shape(l, c->ishapes[i], c->iranks[i], c->shapes[i + 1], &c->ranks[i + 1]);
+        if (!rc && l->kind == DASH_LAYER_ADD) {
+            const int s2 = src_index(i, l->src2);
+            if (c->ranks[s2] != c->iranks[i] ||
+                memcmp(c->shapes[s2], c->ishapes[i], sizeof(uint32_t) * (size_t)c->iranks[i]))
+                rc = fail(ORC_DATA, "add operands differ in shape");
+        }
         if (rc) {
             orc_circuit_free(c);
             return rc;
@@ -1129,18 +1163,23 @@ static int circuit_needs_sign(const orc_circuit* c) {
     return 0;
 }
 
-/* plain_forward (layer.cpp:346-376, 56-109) */
+/* plain_forward (layer.cpp:346-376, 56-109), plus the Pad2d / Add / DAG
+ * extensions (pad cells are 0, add is the integer sum) */
 int orc_plain_forward(const orc_circuit* c, const int64_t* in, int64_t* out) {
     const ocrt b = crt_base(c->k);
     const int64_t hi = max_signed(&b), lo = min_signed(&b);
-    uint64_t n = shape_size(c->shapes[0], c->ranks[0]);
-    int64_t* x = (int64_t*)malloc(sizeof(int64_t) * n);
-    memcpy(x, in, sizeof(int64_t) * n);
-    for (int li = 0; li < c->nl; ++li) {
+    int64_t* vals[65] = {0};
+    uint64_t n0 = shape_size(c->shapes[0], c->ranks[0]);
+    vals[0] = (int64_t*)malloc(sizeof(int64_t) * n0);
+    memcpy(vals[0], in, sizeof(int64_t) * n0);
+    int rc = 0;
+    for (int li = 0; li < c->nl && !rc; ++li) {
         const olayer* l = &c->layers[li];
-        const uint32_t* s = c->shapes[li];
+        const uint32_t* s = c->ishapes[li];
+        const int64_t* x = vals[src_index(li, l->src)];
         const uint64_t no = shape_size(c->shapes[li + 1], c->ranks[li + 1]);
         int64_t* y = (int64_t*)malloc(sizeof(int64_t) * (no ? no : 1));
+        vals[li + 1] = y;
         if (l->kind == DASH_LAYER_DENSE || l->kind == DASH_LAYER_CONV2D) {
             for (uint64_t u = 0; u < no; ++u) {
                 __int128 acc;
@@ -1161,9 +1200,26 @@ int orc_plain_forward(const orc_circuit* c, const int64_t* in, int64_t* out) {
                             }
                 }
                 if (acc > INT64_MAX || acc < INT64_MIN || (int64_t)acc > hi || (int64_t)acc < lo) {
-                    free(x);
-                    free(y);
-                    return fail(ORC_OVERFLOW, "intermediate value left the signed range of the base");
+                    rc = fail(ORC_OVERFLOW, "intermediate value left the signed range of the base");
+                    break;
+                }
+                y[u] = (int64_t)acc;
+            }
+        } else if (l->kind == DASH_LAYER_PAD2D) {
+            const uint32_t H = s[1], W = s[2], OH = H + 2 * l->pad, OW = W + 2 * l->pad;
+            for (uint64_t u = 0; u < no; ++u) {
+                const uint64_t ch = u / ((uint64_t)OH * OW);
+                const uint32_t y0 = (uint32_t)((u / OW) % OH), x0 = (uint32_t)(u % OW);
+                const int inside = y0 >= l->pad && y0 < l->pad + H && x0 >= l->pad && x0 < l->pad + W;
+                y[u] = inside ? x[(ch * H + (y0 - l->pad)) * W + (x0 - l->pad)] : 0;
+            }
+        } else if (l->kind == DASH_LAYER_ADD) {
+            const int64_t* x2 = vals[src_index(li, l->src2)];
+            for (uint64_t u = 0; u < no; ++u) {
+                const __int128 acc = (__int128)x[u] + x2[u];
+                if (acc > hi || acc < lo) {
+                    rc = fail(ORC_OVERFLOW, "intermediate value left the signed range of the base");
+                    break;
                 }
                 y[u] = (int64_t)acc;
             }
@@ -1174,13 +1230,10 @@ int orc_plain_forward(const orc_circuit* c, const int64_t* in, int64_t* out) {
                 else y[u] = x[u];
             }
         }
-        free(x);
-        x = y;
-        n = no;
     }
-    memcpy(out, x, sizeof(int64_t) * n);
-    free(x);
-    return 0;
+    if (!rc) memcpy(out, vals[c->nl], sizeof(int64_t) * shape_size(c->shapes[c->nl], c->ranks[c->nl]));
+    for (int i = 0; i <= c->nl; ++i) free(vals[i]);
+    return rc;
 }
 
 /* env shared by the layer runners (layer.hpp:67-75) */
@@ -1220,7 +1273,9 @@ static void count_layer(const orc_circuit* c, int li, const oenv* e, octx* ctx) 
     const olayer* l = &c->layers[li];
     const uint64_t units = shape_size(c->shapes[li + 1], c->ranks[li + 1]);
     switch (l->kind) {
-        case DASH_LAYER_FLATTEN: return;
+        case DASH_LAYER_FLATTEN:
+        case DASH_LAYER_PAD2D:
+        case DASH_LAYER_ADD: return; /* free: no gates, wires or rows */
         case DASH_LAYER_DENSE:
         case DASH_LAYER_CONV2D:
             for (int i = 0; i < e->base.k; ++i) {
@@ -1249,7 +1304,7 @@ static int64_t resid(int64_t w, int p) { return ((w % p) + p) % p; }
 static void linear_lane(const orc_circuit* c, int li, const otensor* in, otensor* out, const olabel* zero,
                         int p, int garbler, const ooffsets* offs) {
     const olayer* l = &c->layers[li];
-    const uint32_t* s = c->shapes[li];
+    const uint32_t* s = c->ishapes[li];
     const int dense = l->kind == DASH_LAYER_DENSE;
     const uint64_t units = (uint64_t)out->n;
     const uint32_t oh = dense ? 0 : c->shapes[li + 1][1], ow = dense ? 0 : c->shapes[li + 1][2];
@@ -1309,19 +1364,35 @@ static void tfree(otensor* t) {
 /* run_layer<Garble> (layer.cpp:419-551).  garble: blob = output position (already
  * sized); eval: blob = this layer's ciphertext span. */
 static int run_layer(const orc_circuit* c, int li, const oenv* e, int garble, uint64_t gate_base,
-                     uint64_t wire_base, u128* blob, uint64_t blob_len, otensor* in /* k lanes, consumed */,
-                     otensor* out /* k lanes */) {
+                     uint64_t wire_base, u128* blob, uint64_t blob_len, const otensor* in /* k lanes */,
+                     const otensor* in2 /* ADD: second operand */, otensor* out /* k lanes */) {
     const olayer* l = &c->layers[li];
     const int k = e->base.k;
     const uint64_t units = shape_size(c->shapes[li + 1], c->ranks[li + 1]);
+    for (int i = 0; i < k; ++i) out[i] = tnew(e->base.primes[i], units);
     if (l->kind == DASH_LAYER_FLATTEN) {
-        for (int i = 0; i < k; ++i) {
-            out[i] = in[i];
-            in[i].l = NULL;
-        }
+        for (int i = 0; i < k; ++i) memcpy(out[i].l, in[i].l, sizeof(olabel) * units);
         return 0;
     }
-    for (int i = 0; i < k; ++i) out[i] = tnew(e->base.primes[i], units);
+    if (l->kind == DASH_LAYER_PAD2D) { /* extension: pad cells = zero-wire label */
+        const uint32_t H = c->ishapes[li][1], W = c->ishapes[li][2], OH = H + 2 * l->pad, OW = W + 2 * l->pad;
+        for (int i = 0; i < k; ++i)
+            for (uint64_t u = 0; u < units; ++u) {
+                const uint64_t ch = u / ((uint64_t)OH * OW);
+                const uint32_t y = (uint32_t)((u / OW) % OH), x = (uint32_t)(u % OW);
+                const int inside = y >= l->pad && y < l->pad + H && x >= l->pad && x < l->pad + W;
+                out[i].l[u] = inside ? in[i].l[(ch * H + (y - l->pad)) * W + (x - l->pad)] : e->zeros[i];
+            }
+        return 0;
+    }
+    if (l->kind == DASH_LAYER_ADD) { /* extension: lane-wise label sum (free_add) */
+        for (int i = 0; i < k; ++i)
+            for (uint64_t u = 0; u < units; ++u) {
+                out[i].l[u] = in[i].l[u];
+                ladd_into(&out[i].l[u], &in2[i].l[u]);
+            }
+        return 0;
+    }
     if (is_linear(l) && !l->priv) {
         for (int i = 0; i < k; ++i)
             linear_lane(c, li, &in[i], &out[i], &e->zeros[i], e->base.primes[i], garble, e->offs);
@@ -1368,7 +1439,7 @@ static int run_layer(const orc_circuit* c, int li, const oenv* e, int garble, ui
                         const uint64_t ic = j / ((uint64_t)l->filter * l->filter);
                         const uint64_t ky = (j / l->filter) % l->filter, kx = j % l->filter;
                         wi = ((oc * l->in_ch + ic) * l->filter + ky) * l->filter + kx;
-                        xi = (ic * c->shapes[li][1] + (oy * l->stride + ky)) * c->shapes[li][2] + (ox * l->stride + kx);
+                        xi = (ic * c->ishapes[li][1] + (oy * l->stride + ky)) * c->ishapes[li][2] + (ox * l->stride + kx);
                     }
                     const uint16_t pm = (uint16_t)p;
                     const ophi wm = {PHI_WMUL, l->nw ? (int)resid(l->w[wi], p) : 0, &pm};
@@ -1508,13 +1579,14 @@ int orc_garble(const orc_circuit* c, const uint8_t* seed16, orc_net** out) {
     env_init(&e, n);
     e.prf = &prf;
     const uint64_t n_in = shape_size(c->shapes[0], c->ranks[0]);
-    otensor wires[MAXK], next[MAXK];
+    /* outs[0] = input base labels, outs[j + 1] = base labels out of layer j */
+    otensor(*outs)[MAXK] = (otensor(*)[MAXK])calloc((size_t)c->nl + 1, sizeof(otensor[MAXK]));
     for (int i = 0; i < k; ++i) {
         n->enc_bases[i] = tnew(n->base.primes[i], n_in);
         for (uint64_t el = 0; el < n_in; ++el)
             n->enc_bases[i].l[el] = prf_label(&prf, (uint64_t)k + el * (uint64_t)k + (uint64_t)i, n->base.primes[i]);
-        wires[i] = tnew(n->base.primes[i], n_in);
-        memcpy(wires[i].l, n->enc_bases[i].l, sizeof(olabel) * n_in);
+        outs[0][i] = tnew(n->base.primes[i], n_in);
+        memcpy(outs[0][i].l, n->enc_bases[i].l, sizeof(olabel) * n_in);
     }
     layout(n, &e, (uint64_t)k * (1 + n_in));
     n->ncts = tot.cts;
@@ -1525,14 +1597,12 @@ int orc_garble(const orc_circuit* c, const uint8_t* seed16, orc_net** out) {
         n->commitment = davies_meyer(v);
     }
     for (int li = 0; li < c->nl; ++li) {
+        const olayer* l = &c->layers[li];
         rc = run_layer(c, li, &e, 1, n->layer_gate[li], n->layer_wire[li], n->cts + n->layer_ct_base[li], 0,
-                       wires, next);
-        for (int i = 0; i < k; ++i) {
-            if (wires[i].l) tfree(&wires[i]);
-            wires[i] = next[i];
-        }
+                       outs[src_index(li, l->src)], outs[src_index(li, l->src2)], outs[li + 1]);
         if (rc) break;
     }
+    otensor* wires = outs[c->nl];
     if (!rc) {
         /* decoding tables (garble.cpp:208-231) */
         n->n_out = shape_size(c->shapes[c->nl], c->ranks[c->nl]);
@@ -1556,7 +1626,9 @@ int orc_garble(const orc_circuit* c, const uint8_t* seed16, orc_net** out) {
         n->stats[1] = tot.gates;
         n->stats[2] = tot.wires + (uint64_t)k * (1 + n_in);
     }
-    for (int i = 0; i < k; ++i) tfree(&wires[i]);
+    for (int li = 0; li <= c->nl; ++li)
+        for (int i = 0; i < k; ++i) tfree(&outs[li][i]);
+    free(outs);
     if (rc) {
         orc_net_free(n);
         return rc;
@@ -1648,6 +1720,11 @@ size_t orc_net_gc_bytes(const orc_net* n, uint8_t* buf, size_t cap) {
             w_le(&w, l->nw, 8);
             for (uint64_t i = 0; i < l->nw; ++i) w_le(&w, (uint64_t)l->w[i], 8);
         }
+        if (l->kind > DASH_LAYER_FLATTEN || l->src || l->src2 || l->pad) { /* extension record */
+            w_le(&w, (uint64_t)(uint32_t)l->src, 4);
+            w_le(&w, (uint64_t)(uint32_t)l->src2, 4);
+            w_le(&w, l->pad, 4);
+        }
     }
     for (int i = 0; i < c->k; ++i) w_u128(&w, compress(&n->zeros[i]));
     w_le(&w, (uint64_t)c->nl + 1, 8);
@@ -1713,27 +1790,35 @@ int orc_evaluate(const orc_net* n, const orc_bundle* in, orc_bundle** out) {
     oenv e;
     env_init(&e, n);
     e.offs = NULL;
-    otensor wires[MAXK], next[MAXK];
+    const int nl = n->c->nl;
+    otensor(*outs)[MAXK] = (otensor(*)[MAXK])calloc((size_t)nl + 1, sizeof(otensor[MAXK]));
     for (int i = 0; i < k; ++i) {
-        wires[i] = tnew(in->lanes[i].m, (uint64_t)in->lanes[i].n);
-        memcpy(wires[i].l, in->lanes[i].l, sizeof(olabel) * (size_t)in->lanes[i].n);
+        outs[0][i] = tnew(in->lanes[i].m, (uint64_t)in->lanes[i].n);
+        memcpy(outs[0][i].l, in->lanes[i].l, sizeof(olabel) * (size_t)in->lanes[i].n);
     }
     int rc = 0;
-    for (int li = 0; li < n->c->nl && !rc; ++li) {
+    int done = 0;
+    for (int li = 0; li < nl && !rc; ++li) {
+        const olayer* l = &n->c->layers[li];
         const uint64_t b0 = n->layer_ct_base[li], b1 = n->layer_ct_base[li + 1];
-        rc = run_layer(n->c, li, &e, 0, n->layer_gate[li], 0, n->cts + b0, b1 - b0, wires, next);
+        rc = run_layer(n->c, li, &e, 0, n->layer_gate[li], 0, n->cts + b0, b1 - b0, outs[src_index(li, l->src)],
+                       outs[src_index(li, l->src2)], outs[li + 1]);
+        done = li + 1;
+    }
+    orc_bundle* b = NULL;
+    if (!rc) {
+        b = (orc_bundle*)calloc(1, sizeof *b);
+        b->k = k;
         for (int i = 0; i < k; ++i) {
-            if (wires[i].l) tfree(&wires[i]);
-            wires[i] = next[i];
+            b->lanes[i] = outs[nl][i];
+            outs[nl][i].l = NULL;
         }
     }
-    if (rc) {
-        for (int i = 0; i < k; ++i) tfree(&wires[i]);
-        return rc;
-    }
-    orc_bundle* b = (orc_bundle*)calloc(1, sizeof *b);
-    b->k = k;
-    for (int i = 0; i < k; ++i) b->lanes[i] = wires[i];
+    for (int li = 0; li <= done; ++li)
+        for (int i = 0; i < k; ++i)
+            if (outs[li][i].l) tfree(&outs[li][i]);
+    free(outs);
+    if (rc) return rc;
     *out = b;
     return 0;
 }

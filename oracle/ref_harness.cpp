@@ -101,6 +101,12 @@ void* ref_circuit_from_desc(const dash_circuit_desc* d) {
     h->c.quant.alpha = d->alpha;
     for (uint32_t i = 0; i < d->n_layers; ++i) {
         const dash_layer_desc& s = d->layers[i];
+        if (s.kind > DASH_LAYER_FLATTEN || s.src || s.src2 || s.pad) {
+            // Pad2d / Add / DAG inputs are extensions of this repo (dash_circuit_desc.h)
+            delete h;
+            g_err = "circuit uses layer extensions the reference does not have";
+            return nullptr;
+        }
         Layer l;
         l.kind = static_cast<LayerKind>(s.kind);
         l.private_weights = s.private_weights != 0;

@@ -16,8 +16,9 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-DENSE, CONV2D, RELU, SIGNACT, FLATTEN = 1, 2, 3, 4, 5
-KIND_NAMES = {DENSE: "Dense", CONV2D: "Conv2d", RELU: "ReLU", SIGNACT: "SignAct", FLATTEN: "Flatten"}
+DENSE, CONV2D, RELU, SIGNACT, FLATTEN, PAD2D, ADD = 1, 2, 3, 4, 5, 6, 7
+KIND_NAMES = {DENSE: "Dense", CONV2D: "Conv2d", RELU: "ReLU", SIGNACT: "SignAct", FLATTEN: "Flatten",
+              PAD2D: "Pad2d", ADD: "Add"}
 PRIMES = [2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53]
 
 
@@ -35,6 +36,9 @@ class LayerDesc(ctypes.Structure):
         ("n_weights", ctypes.c_uint64),
         ("q_biases", ctypes.POINTER(ctypes.c_int64)),
         ("n_biases", ctypes.c_uint64),
+        ("src", ctypes.c_int32),
+        ("src2", ctypes.c_int32),
+        ("pad", ctypes.c_uint32),
     ]
 
 
@@ -62,6 +66,10 @@ class Layer:
     stride: int = 0
     q_weights: Optional[np.ndarray] = None
     q_biases: Optional[np.ndarray] = None
+    # extensions (include/dash_circuit_desc.h): DAG inputs and padding
+    src: int = 0    # 0 = previous layer, j + 1 = output of layer j, -1 = circuit input
+    src2: int = 0   # second operand of Add
+    pad: int = 0    # Pad2d cells per side
 
     def linear(self) -> bool:
         return self.kind in (DENSE, CONV2D)
@@ -87,8 +95,12 @@ class Layer:
                     raise ValueError("convolution filter does not fit the input")
                 return (n - self.filter) // self.stride + 1
             return [self.out_ch, ext(shape[1]), ext(shape[2])]
-        if self.kind in (RELU, SIGNACT):
+        if self.kind in (RELU, SIGNACT, ADD):
             return list(shape)
+        if self.kind == PAD2D:
+            if len(shape) != 3:
+                raise ValueError("pad layer needs a [C][H][W] input")
+            return [shape[0], shape[1] + 2 * self.pad, shape[2] + 2 * self.pad]
         return [int(np.prod(shape))]
 
 
@@ -101,9 +113,11 @@ class Circuit:
     alpha: float = 1.0
 
     def shapes(self) -> List[List[int]]:
+        """s[0] = input, s[j + 1] = output of layer j (inputs follow src)."""
         s = [list(self.input_shape)]
-        for l in self.layers:
-            s.append(l.out_shape(s[-1]))
+        for i, l in enumerate(self.layers):
+            src = i if l.src == 0 else (0 if l.src < 0 else l.src)
+            s.append(l.out_shape(s[src]))
         return s
 
     @property
@@ -124,6 +138,7 @@ class Circuit:
             d.private_weights = 1 if l.private_weights else 0
             d.in_dim, d.out_dim = l.in_dim, l.out_dim
             d.in_ch, d.out_ch, d.filter, d.stride = l.in_ch, l.out_ch, l.filter, l.stride
+            d.src, d.src2, d.pad = l.src, l.src2, l.pad
             if l.q_weights is not None:
                 w = np.ascontiguousarray(l.q_weights, dtype=np.int64)
                 keep.append(w)
@@ -154,22 +169,32 @@ class Circuit:
             w = np.ctypeslib.as_array(s.q_weights, shape=(s.n_weights,)).copy() if s.n_weights else None
             b = np.ctypeslib.as_array(s.q_biases, shape=(s.n_biases,)).copy() if s.n_biases else None
             layers.append(Layer(s.kind, bool(s.private_weights), s.in_dim, s.out_dim, s.in_ch,
-                                s.out_ch, s.filter, s.stride, w, b))
+                                s.out_ch, s.filter, s.stride, w, b, s.src, s.src2, s.pad))
         return Circuit([d.input_shape[i] for i in range(d.rank)], d.k, layers, d.sign_target, d.alpha)
 
 
-def dense(i, o, w, b, priv=False):
+def dense(i, o, w, b, priv=False, src=0):
     return Layer(DENSE, priv, in_dim=i, out_dim=o, q_weights=np.asarray(w, np.int64),
-                 q_biases=np.asarray(b, np.int64))
+                 q_biases=np.asarray(b, np.int64), src=src)
 
 
-def conv2d(ic, oc, f, s, w, b, priv=False):
+def conv2d(ic, oc, f, s, w, b, priv=False, src=0):
     return Layer(CONV2D, priv, in_ch=ic, out_ch=oc, filter=f, stride=s,
-                 q_weights=np.asarray(w, np.int64), q_biases=np.asarray(b, np.int64))
+                 q_weights=np.asarray(w, np.int64), q_biases=np.asarray(b, np.int64), src=src)
 
 
-def relu():
-    return Layer(RELU)
+def relu(src=0):
+    return Layer(RELU, src=src)
+
+
+def pad2d(p, src=0):
+    """Extension: zero padding (pad cells = zero-wire label)."""
+    return Layer(PAD2D, pad=p, src=src)
+
+
+def add(src2, src=0):
+    """Extension: residual add of the previous (or src) output and layer src2 - 1's output."""
+    return Layer(ADD, src=src, src2=src2)
 
 
 def sign_act():

@@ -325,6 +325,42 @@ DASH_HD void decode_thread(const DecodeParams& P, uint32_t b, uint32_t e) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Extension layers (include/dash_circuit_desc.h): Pad2d writes the zero-wire
+// label (garble.cpp:157) into the pad cells of a [C][H][W] plane; Add is the
+// lane-wise label sum (free, like free_add, gadgets.hpp:108-118).  Garbler
+// and evaluator run the same code (the zero wire's active label is its base
+// label).  One thread = one digit word of one element of one inference.
+struct PadAddParams {
+    int add;                   // 0: Pad2d, 1: Add
+    uint32_t B, E_out;
+    uint32_t C, H, W, pad, OH, OW;
+    int k;
+    uint16_t primes[MAXK];
+    uint32_t wbase[MAXK + 1];  // prefix sums of nw over the lanes
+    const uint32_t* in[MAXK];  // [B][nw][E_in]
+    const uint32_t* in2[MAXK]; // Add: second operand [B][nw][E_out]
+    uint32_t* out[MAXK];       // [B][nw][E_out]
+    const uint32_t* zero;      // [B][k][LABW]
+};
+
+DASH_HD void pad_add_thread(const PadAddParams& P, uint32_t b, uint32_t wi, uint32_t u) {
+    int i = 0;
+    while (i + 1 < P.k && wi >= P.wbase[i + 1]) ++i;
+    const uint32_t nw = P.wbase[i + 1] - P.wbase[i], w = wi - P.wbase[i];
+    uint32_t* o = P.out[i] + ((uint64_t)b * nw + w) * P.E_out + u;
+    if (P.add) {
+        const uint64_t at = ((uint64_t)b * nw + w) * P.E_out + u;
+        *o = swar_add(P.in[i][at], P.in2[i][at], c_mod[P.primes[i]]);
+        return;
+    }
+    const uint32_t ch = u / (P.OH * P.OW), y = (u / P.OW) % P.OH, x = u % P.OW;
+    const bool inside = y >= P.pad && y < P.pad + P.H && x >= P.pad && x < P.pad + P.W;
+    *o = inside ? P.in[i][((uint64_t)b * nw + w) * ((uint64_t)P.C * P.H * P.W) +
+                          ((uint64_t)ch * P.H + (y - P.pad)) * P.W + (x - P.pad)]
+                : P.zero[((uint64_t)b * P.k + i) * LABW + w];
+}
+
 // compress every label of a lane plane: out[b][e] (bundle payload / tensor_write)
 struct CompressParams {
     uint32_t B, n;

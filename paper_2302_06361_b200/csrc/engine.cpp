@@ -766,6 +766,8 @@ struct HLayer {
     int kind = 0;
     bool priv = false;
     uint32_t in_dim = 0, out_dim = 0, in_ch = 0, out_ch = 0, filter = 0, stride = 0;
+    int src = 0, src2 = 0;  // extension: DAG inputs (dash_circuit_desc.h)
+    uint32_t pad = 0;       // extension: PAD2D
     std::vector<int64_t> w, bias;
     std::vector<uint32_t> in_shape, out_shape;
     uint64_t E_in = 0, E_out = 0;
@@ -847,12 +849,20 @@ static std::vector<uint32_t> out_shape_of(const HLayer& l, const std::vector<uin
             return {l.out_ch, conv_extent(in[1], l.filter, l.stride), conv_extent(in[2], l.filter, l.stride)};
         case DASH_LAYER_RELU:
         case DASH_LAYER_SIGNACT:
+        case DASH_LAYER_ADD:
             return in;
         case DASH_LAYER_FLATTEN:
             return {(uint32_t)shape_size(in)};
+        case DASH_LAYER_PAD2D:
+            if (in.size() != 3) throw DataError("pad layer needs a [C][H][W] input");
+            return {in[0], in[1] + 2 * l.pad, in[2] + 2 * l.pad};
     }
     throw DataError("unknown layer kind");
 }
+
+// index of a layer's DAG source in the per-layer value list (0 = circuit
+// input, j + 1 = output of layer j); src 0 = previous layer (reference chain)
+static size_t src_index(size_t li, int src) { return src == 0 ? li : (src < 0 ? 0 : (size_t)src); }
 
 static std::shared_ptr<DevBuf> upload(const void* data, size_t bytes) {
     auto b = std::make_shared<DevBuf>();
@@ -908,12 +918,17 @@ static void prepare_circuit(dashgpu_circuit& c) {
     if (c.input_shape.empty() || c.input_shape.size() > 8 || shape_size(c.input_shape) == 0)
         throw DataError("circuit has an empty input shape");
     c.n_in = shape_size(c.input_shape);
-    std::vector<uint32_t> shape = c.input_shape;
+    std::vector<std::vector<uint32_t>> shapes{c.input_shape};
     c.needs_sign = false;
-    for (auto& l : c.layers) {
-        if (l.kind < 1 || l.kind > 5) throw DataError("bad layer kind");
-        l.in_shape = shape;
-        l.out_shape = out_shape_of(l, shape);
+    for (size_t li = 0; li < c.layers.size(); ++li) {
+        auto& l = c.layers[li];
+        if (l.kind < 1 || l.kind > 7) throw DataError("bad layer kind");
+        if (l.src > (int)li || l.src < -1 || l.src2 > (int)li || l.src2 < -1 || (l.kind == DASH_LAYER_ADD && !l.src2))
+            throw DataError("layer input refers to a later layer");
+        l.in_shape = shapes[src_index(li, l.src)];
+        l.out_shape = out_shape_of(l, l.in_shape);
+        if (l.kind == DASH_LAYER_ADD && shapes[src_index(li, l.src2)] != l.in_shape)
+            throw DataError("add operands differ in shape");
         l.E_in = shape_size(l.in_shape);
         l.E_out = shape_size(l.out_shape);
         if (l.linear()) {
@@ -921,9 +936,9 @@ static void prepare_circuit(dashgpu_circuit& c) {
             if (!l.bias.empty() && l.bias.size() != l.bias_count()) throw DataError("quantized bias count mismatch");
         }
         if (l.kind == DASH_LAYER_RELU || l.kind == DASH_LAYER_SIGNACT) c.needs_sign = true;
-        shape = l.out_shape;
+        shapes.push_back(l.out_shape);
     }
-    c.n_out = shape_size(shape);
+    c.n_out = shape_size(shapes.back());
     if (c.n_in > (1u << 26) || c.n_out > (1u << 26)) throw DataError("tensor too large");
     if (c.needs_sign) {
         c.sign = make_sign(c.base, choose_spec(c.base, c.sign_target));
@@ -1063,11 +1078,14 @@ struct Network {
     std::vector<uint8_t> seeds;
     DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err, slots;
     Lanes base;  // encoding info: input base labels
-    Lanes ping, pong;    // garbling planes
-    Lanes eping, epong;  // evaluation planes
+    // per-layer output planes (garbler: base labels, evaluator: active labels);
+    // at[j + 1] = output of layer j, at[0] = the input; Flatten aliases its input
+    struct Outs {
+        std::vector<std::unique_ptr<Lanes>> own;
+        std::vector<const Lanes*> at;
+    } gouts, eouts;
     std::unique_ptr<struct Bundle> bin, bout;  // dashgpu_infer's cached bundles
     // garbling of every activation layer is one launch over these
-    std::vector<std::unique_ptr<Lanes>> act_in;
     std::vector<ActParams> act_host;
     DevBuf act_dev;        // [act_cap] ActParams (last entry: evaluation scratch)
     size_t act_cap = 0;
@@ -1092,15 +1110,37 @@ static void fill_primes(const Crt& b, uint16_t* out) {
 }
 
 // Runs one layer over B inferences.  garbler: base labels; else active.
-static void run_layer(Network& n, const HLayer& l, bool garbler, Lanes& in, Lanes& out) {
+// in2: second operand of the Add extension.
+static void run_layer(Network& n, const HLayer& l, bool garbler, const Lanes& in, const Lanes* in2, Lanes& out) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
-    if (l.kind == DASH_LAYER_FLATTEN) {
-        std::swap(in, out);  // metadata-only reshape: the planes are already flat
-        out.E = l.E_out;
+    out.ensure(c.base, n.B, l.E_out);
+    if (l.kind == DASH_LAYER_PAD2D || l.kind == DASH_LAYER_ADD) {
+        PadAddParams P;
+        std::memset(&P, 0, sizeof P);
+        P.add = l.kind == DASH_LAYER_ADD;
+        P.B = n.B;
+        P.E_out = (uint32_t)l.E_out;
+        if (!P.add) {
+            P.C = l.in_shape[0];
+            P.H = l.in_shape[1];
+            P.W = l.in_shape[2];
+            P.pad = l.pad;
+            P.OH = l.out_shape[1];
+            P.OW = l.out_shape[2];
+        }
+        P.k = k;
+        fill_primes(c.base, P.primes);
+        for (int i = 0; i < k; ++i) {
+            P.wbase[i + 1] = P.wbase[i] + (uint32_t)(n_digits_host(c.base.primes[i]) + 3) / 4;
+            P.in[i] = in.lane[i]->as<uint32_t>();
+            P.in2[i] = in2 ? in2->lane[i]->as<uint32_t>() : nullptr;
+            P.out[i] = out.lane[i]->as<uint32_t>();
+        }
+        P.zero = n.zero.as<uint32_t>();
+        launch_pad_add(P, g_stream);
         return;
     }
-    out.ensure(c.base, n.B, l.E_out);
     if (l.linear() && !l.priv) {
         LinParams Ls[MAXK];
         for (int i = 0; i < k; ++i) {
@@ -1197,17 +1237,10 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, Lanes& in, Lane
     P.mult_stride = n.mult_stride;
     const size_t slot_words = (size_t)l.tape->nslots * n.B * l.E_out;
     if (garbler) {
-        // Inputs stay resident until the combined tape launch; the outputs
-        // (pure PRF functions) are written now so the next layer can proceed.
-        const size_t j = n.act_host.size();
-        if (n.act_in.size() <= j) n.act_in.emplace_back(std::make_unique<Lanes>());
-        Lanes& keep = *n.act_in[j];
-        keep.ensure(c.base, n.B, l.E_out);
-        for (int i = 0; i < k; ++i) {
-            dev::d2d(keep.lane[i]->p, in.lane[i]->p,
-                     (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * l.E_out * 4, g_stream);
-            P.in[i] = keep.lane[i]->as<uint32_t>();
-        }
+        // Inputs (per-layer planes) stay resident until the combined tape
+        // launch; the outputs (pure PRF functions) are written now so the
+        // next layer can proceed.
+        for (int i = 0; i < k; ++i) P.in[i] = in.lane[i]->as<uint32_t>();
         P.slots = n.slots.as<U4>() + n.slot_used;
         n.slot_used += slot_words;
         uint16_t primes[MAXK];
@@ -1257,6 +1290,30 @@ static void network_reserve(Network& n, uint32_t B) {
     n.act_dev.ensure(n.act_cap * sizeof(ActParams));
 }
 
+// All layers of the circuit in order (DAG inputs per layer, see
+// dash_circuit_desc.h); returns the final output planes.
+static const Lanes* run_layers(Network& n, bool garbler, const Lanes& input) {
+    dashgpu_circuit& c = *n.c;
+    Network::Outs& O = garbler ? n.gouts : n.eouts;
+    const size_t L = c.layers.size();
+    O.own.resize(L + 1);
+    O.at.assign(L + 1, nullptr);
+    O.at[0] = &input;
+    for (size_t li = 0; li < L; ++li) {
+        const HLayer& l = c.layers[li];
+        const Lanes* src = O.at[src_index(li, l.src)];
+        if (l.kind == DASH_LAYER_FLATTEN) {  // metadata-only reshape: planes are already flat
+            O.at[li + 1] = src;
+            continue;
+        }
+        if (!O.own[li + 1]) O.own[li + 1] = std::make_unique<Lanes>();
+        const Lanes* src2 = l.kind == DASH_LAYER_ADD ? O.at[src_index(li, l.src2)] : nullptr;
+        run_layer(n, l, garbler, *src, src2, *O.own[li + 1]);
+        O.at[li + 1] = O.own[li + 1].get();
+    }
+    return O.at[L];
+}
+
 // garble (garble.cpp:134-240), batched: inference b uses seeds[b]
 static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
     dashgpu_circuit& c = *n.c;
@@ -1293,19 +1350,10 @@ static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds
     S.Rb = n.Rb.as<uint32_t>();
     S.commit = n.commit.as<U4>();
     launch_setup(S, g_stream);
-    // copy the input base planes into the working planes and run the layers
-    n.ping.ensure(c.base, B, c.n_in);
-    for (int i = 0; i < k; ++i)
-        dev::d2d(n.ping.lane[i]->p, n.base.lane[i]->p,
-                 (size_t)B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_in * 4, g_stream);
-    Lanes* cur = &n.ping;
-    Lanes* nxt = &n.pong;
+    // run the layers on the input base planes
     n.act_host.clear();
     n.slot_used = 0;
-    for (const auto& l : c.layers) {
-        run_layer(n, l, true, *cur, *nxt);
-        std::swap(cur, nxt);
-    }
+    const Lanes* cur = run_layers(n, true, n.base);
     if (!n.act_host.empty()) {
         dev::h2d(n.act_dev.p, n.act_host.data(), n.act_host.size() * sizeof(ActParams), g_stream);
         launch_act_multi(n.act_dev.as<ActParams>(), n.act_host.data(), (int)n.act_host.size(), true, g_stream);
@@ -1370,16 +1418,7 @@ static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
     if (in.B != n.B || in.output) throw DataError("garbled input bundle does not match the network");
-    n.eping.ensure(c.base, n.B, c.n_in);
-    for (int i = 0; i < k; ++i)
-        dev::d2d(n.eping.lane[i]->p, in.lanes.lane[i]->p,
-                 (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_in * 4, g_stream);
-    Lanes* cur = &n.eping;
-    Lanes* nxt = &n.epong;
-    for (const auto& l : c.layers) {
-        run_layer(n, l, false, *cur, *nxt);
-        std::swap(cur, nxt);
-    }
+    const Lanes* cur = run_layers(n, false, in.lanes);
     out.net = &n;
     out.B = n.B;
     out.output = true;
@@ -1708,6 +1747,11 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
             w.le(l.w.size(), 8);
             for (int64_t v : l.w) w.le((uint64_t)v, 8);
         }
+        if (l.kind > DASH_LAYER_FLATTEN || l.src || l.src2 || l.pad) {  // extension record
+            w.le((uint32_t)l.src, 4);
+            w.le((uint32_t)l.src2, 4);
+            w.le(l.pad, 4);
+        }
     }
     std::vector<uint32_t> zero((size_t)c.k * LABW);
     dev::d2h(zero.data(), n.zero.as<uint32_t>() + (uint64_t)b * c.k * LABW, zero.size() * 4, g_stream);
@@ -1896,6 +1940,57 @@ static void build(dashgpu_circuit& c, const std::string& name, uint32_t seed, in
         }
         c.layers.push_back(F);
         c.layers.push_back(dense(128, 10, g, priv));
+    } else if (name == "resnet20" || name == "resnet20s" || name == "resnet_tiny") {
+        // ResNet-20 (CIFAR variant) in reference ops + the Pad2d / Add / DAG
+        // extensions (include/dash_circuit_desc.h, SURVEY.md 8(d) "ResNet-20
+        // extension notes"): 3x3 pad-1 convs with 16/32/64 channels, three
+        // basic blocks per stage, 1x1 stride-2 projection shortcuts, residual
+        // add, ReLU (resnet20s: SignAct after every add), global sum pool as
+        // an identity-channel conv over the final map, FC 64 -> 10.
+        // resnet_tiny: the same graph with 4/8/16 channels on 3x8x8, one
+        // block per stage (parity tests).
+        const bool tiny = name == "resnet_tiny";
+        const uint32_t C0 = tiny ? 4 : 16, S = tiny ? 8 : 32;
+        const int blocks = tiny ? 1 : 3;
+        const HLayer post = name == "resnet20s" ? SA : R;
+        c.input_shape = {3, S, S};
+        // ids: 0 = circuit input, j + 1 = output of layer j
+        auto add_layer = [&](HLayer l, int src_id) {
+            const int li = (int)c.layers.size();
+            l.src = src_id == li ? 0 : (src_id == 0 ? -1 : src_id);
+            c.layers.push_back(std::move(l));
+            return li + 1;
+        };
+        auto padded_conv = [&](int x, uint32_t ci, uint32_t co, uint32_t stride) {
+            HLayer pd = simple(DASH_LAYER_PAD2D);
+            pd.pad = 1;
+            const int p = add_layer(pd, x);
+            return add_layer(conv2d(ci, co, 3, stride, g, priv), p);
+        };
+        int x = add_layer(R, padded_conv(0, 3, C0, 1));
+        uint32_t cin = C0;
+        for (int st = 0; st < 3; ++st) {
+            const uint32_t cout = C0 << st;
+            for (int bk = 0; bk < blocks; ++bk) {
+                const uint32_t stride = (st > 0 && bk == 0) ? 2 : 1;
+                const int r1 = add_layer(R, padded_conv(x, cin, cout, stride));
+                const int c2 = padded_conv(r1, cout, cout, 1);
+                const int sc = (stride != 1 || cin != cout) ? add_layer(conv2d(cin, cout, 1, stride, g, priv), x) : x;
+                HLayer ad = simple(DASH_LAYER_ADD);
+                ad.src2 = c2;
+                x = add_layer(post, add_layer(ad, sc));
+                cin = cout;
+            }
+        }
+        const uint32_t Cf = C0 << 2, Sf = S >> 2;
+        HLayer pool = conv2d(Cf, Cf, Sf, 1, g, false);  // global sum pool: w[oc][ic] = [oc == ic]
+        for (uint32_t oc = 0; oc < Cf; ++oc)
+            for (uint32_t ic = 0; ic < Cf; ++ic)
+                for (uint32_t t = 0; t < Sf * Sf; ++t) pool.w[((uint64_t)oc * Cf + ic) * Sf * Sf + t] = oc == ic;
+        std::fill(pool.bias.begin(), pool.bias.end(), 0);
+        x = add_layer(pool, x);
+        x = add_layer(F, x);
+        add_layer(dense(Cf, 10, g, priv), x);
     } else if (name.rfind("relu", 0) == 0 || name.rfind("sign", 0) == 0) {
         const long n = std::stol(name.substr(4));
         if (n <= 0) throw DataError("bad sweep size");
@@ -1936,10 +2031,15 @@ static void init_device(int device) {
     g_constants = true;
 }
 
-// plain_forward (layer.cpp:346-376, 56-109) with OverflowError range checks
-static std::vector<int64_t> plain_forward(const dashgpu_circuit& c, std::vector<int64_t> x) {
+// plain_forward (layer.cpp:346-376, 56-109) with OverflowError range checks,
+// plus the Pad2d / Add / DAG extensions (pad cells 0, add = integer sum)
+static std::vector<int64_t> plain_forward(const dashgpu_circuit& c, std::vector<int64_t> x0) {
     const int64_t hi = max_signed(c.base), lo = min_signed(c.base);
-    for (const auto& l : c.layers) {
+    std::vector<std::vector<int64_t>> vals;
+    vals.push_back(std::move(x0));
+    for (size_t li = 0; li < c.layers.size(); ++li) {
+        const auto& l = c.layers[li];
+        const std::vector<int64_t>& x = vals[src_index(li, l.src)];
         std::vector<int64_t> y(l.E_out);
         if (l.linear()) {
             for (uint64_t u = 0; u < l.E_out; ++u) {
@@ -1961,6 +2061,21 @@ static std::vector<int64_t> plain_forward(const dashgpu_circuit& c, std::vector<
                 if (acc > hi || acc < lo) throw OverflowErr("intermediate value left the signed range of the base");
                 y[u] = (int64_t)acc;
             }
+        } else if (l.kind == DASH_LAYER_PAD2D) {
+            const uint32_t H = l.in_shape[1], W = l.in_shape[2], OH = l.out_shape[1], OW = l.out_shape[2];
+            for (uint64_t u = 0; u < l.E_out; ++u) {
+                const uint64_t ch = u / ((uint64_t)OH * OW);
+                const uint32_t yy = (uint32_t)((u / OW) % OH), xx = (uint32_t)(u % OW);
+                const bool inside = yy >= l.pad && yy < l.pad + H && xx >= l.pad && xx < l.pad + W;
+                y[u] = inside ? x[(ch * H + (yy - l.pad)) * W + (xx - l.pad)] : 0;
+            }
+        } else if (l.kind == DASH_LAYER_ADD) {
+            const std::vector<int64_t>& x2 = vals[src_index(li, l.src2)];
+            for (uint64_t u = 0; u < l.E_out; ++u) {
+                const __int128 acc = (__int128)x[u] + x2[u];
+                if (acc > hi || acc < lo) throw OverflowErr("intermediate value left the signed range of the base");
+                y[u] = (int64_t)acc;
+            }
         } else {
             for (uint64_t u = 0; u < l.E_out; ++u) {
                 if (l.kind == DASH_LAYER_RELU) y[u] = x[u] > 0 ? x[u] : 0;
@@ -1968,9 +2083,9 @@ static std::vector<int64_t> plain_forward(const dashgpu_circuit& c, std::vector<
                 else y[u] = x[u];
             }
         }
-        x = std::move(y);
+        vals.push_back(std::move(y));
     }
-    return x;
+    return vals.back();
 }
 
 }  // namespace dashgpu
@@ -2045,6 +2160,9 @@ int dashgpu_circuit_create(const dash_circuit_desc* d, dashgpu_circuit** out) {
             l.out_ch = s.out_ch;
             l.filter = s.filter;
             l.stride = s.stride;
+            l.src = s.src;
+            l.src2 = s.src2;
+            l.pad = s.pad;
             if (s.q_weights) l.w.assign(s.q_weights, s.q_weights + s.n_weights);
             if (s.q_biases) l.bias.assign(s.q_biases, s.q_biases + s.n_biases);
             c->layers.push_back(std::move(l));
@@ -2102,6 +2220,9 @@ int dashgpu_circuit_desc_view(const dashgpu_circuit* cc, dash_circuit_desc* out)
             s.out_ch = l.out_ch;
             s.filter = l.filter;
             s.stride = l.stride;
+            s.src = l.src;
+            s.src2 = l.src2;
+            s.pad = l.pad;
             s.q_weights = l.w.empty() ? nullptr : l.w.data();
             s.n_weights = l.w.size();
             s.q_biases = l.bias.empty() ? nullptr : l.bias.data();
@@ -2250,13 +2371,18 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
         using clk = std::chrono::steady_clock;
         const auto t0 = clk::now();
         // per-inference device bytes: ciphertexts + multiples + decode table + planes
+        // per-layer output planes of garbler and evaluator + input planes
         uint64_t planes = 0;
         {
-            uint64_t maxE = c->n_in;
-            for (const auto& l : c->layers) maxE = std::max(maxE, l.E_out);
-            for (int p : c->base.primes) planes += (uint64_t)((n_digits_host(p) + 3) / 4) * maxE * 4;
+            uint64_t sumE = 3 * c->n_in + 2 * c->n_out;
+            for (const auto& l : c->layers)
+                if (l.kind != DASH_LAYER_FLATTEN) sumE += 2 * l.E_out;
+            for (int p : c->base.primes) planes += (uint64_t)((n_digits_host(p) + 3) / 4) * sumE * 4;
         }
-        const uint64_t per = c->total_cts * 16 + (uint64_t)(MAXMOD - 1) * 128 * NWMAX * 4 + planes * 5 +
+        uint64_t slots = 0;
+        for (const auto& l : c->layers)
+            if (l.tape) slots += (uint64_t)l.tape->nslots * l.E_out * 16;
+        const uint64_t per = c->total_cts * 16 + (uint64_t)(MAXMOD - 1) * 128 * NWMAX * 4 + planes + slots +
                              c->n_out * 600 * 16 + 4096;
         if (!c->workspace) {
             c->workspace = std::make_unique<Network>();

@@ -48,6 +48,12 @@ __global__ void __launch_bounds__(128) private_kernel(PrivParams P) {
     private_thread(P, blockIdx.y, u, make_tab(nullptr, threadIdx.x & 31u));
 }
 
+__global__ void __launch_bounds__(128) pad_add_kernel(const __grid_constant__ PadAddParams P) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= P.E_out) return;
+    pad_add_thread(P, blockIdx.z, blockIdx.y, u);
+}
+
 __global__ void __launch_bounds__(128) setup_offsets_kernel(SetupParams Sp) {
     fill_T(g_T0);
     const uint32_t si = blockIdx.x * blockDim.x + threadIdx.x;
@@ -250,6 +256,13 @@ void launch_private(const PrivParams& P, void* st) {
     ProfScope ps(P.garbler ? K_PRIV_GARBLE : K_PRIV_EVAL, S(st));
     ck(cudaFuncSetAttribute(private_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
     private_kernel<<<dim3(cdiv(P.M, 128), P.B), 128, kTabBytes, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_pad_add(const PadAddParams& P, void* st) {
+    if (P.B == 0 || P.E_out == 0) return;
+    ProfScope ps(K_MISC, S(st));
+    pad_add_kernel<<<dim3(cdiv(P.E_out, 128), P.wbase[P.k], P.B), 128, 0, S(st)>>>(P);
     dev::check();
 }
 

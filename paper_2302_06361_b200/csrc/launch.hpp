@@ -66,6 +66,7 @@ void make_weight_map(TcLinear& t);  // encodes t.tmap for t.wexp
 // all lanes of a public linear layer in one launch
 void launch_linear(const LinParams* Ls, int n, const TcLinear& tc, void* stream);
 void launch_private(const PrivParams& P, void* stream);
+void launch_pad_add(const PadAddParams& P, void* stream);  // extension layers
 void launch_setup(const SetupParams& S, void* stream);
 void launch_encode(const EncodeParams& P, void* stream);
 void launch_dectable(const DecodeParams& P, void* stream);

@@ -106,6 +106,13 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear&, void*) {
     }
 }
 
+void launch_pad_add(const PadAddParams& P, void*) {
+#pragma omp parallel for collapse(2)
+    for (int64_t b = 0; b < (int64_t)P.B; ++b)
+        for (int64_t wi = 0; wi < (int64_t)P.wbase[P.k]; ++wi)
+            for (uint32_t u = 0; u < P.E_out; ++u) pad_add_thread(P, (uint32_t)b, (uint32_t)wi, u);
+}
+
 void launch_private(const PrivParams& P, void*) {
 #pragma omp parallel for collapse(2)
     for (int64_t b = 0; b < (int64_t)P.B; ++b)

@@ -342,3 +342,64 @@ def test_streamed_layer_vs_oracle(eng, oracle, name, k, chunk):
     assert gcs[1] == onet.cts().tobytes()
     ref, _ = eng.infer(g, seeds, x)
     assert (ref == out).all()
+
+
+# ------------------------------------- extensions: Pad2d / Add / DAG (ResNet)
+
+def _small_dag():
+    """pad -> conv -> relu -> pad -> conv, + 1x1 shortcut of the input, add,
+    relu, flatten, dense: a residual block whose values stay in range."""
+    from paper_2302_06361_b200.circuit import Circuit, add, conv2d, dense, flatten, pad2d, relu
+
+    r = np.random.default_rng(31)
+    w = lambda *s: r.integers(-1, 2, size=s)  # noqa: E731
+    b = lambda n: r.integers(-3, 4, size=n)  # noqa: E731
+    L = [pad2d(1), conv2d(2, 3, 3, 1, w(3, 2, 3, 3), b(3)), relu(), pad2d(1), conv2d(3, 3, 3, 2, w(3, 3, 3, 3), b(3)),
+         conv2d(2, 3, 1, 2, w(3, 2, 1, 1), b(3), src=-1), add(5), relu(), flatten(), dense(27, 4, w(4, 27), b(4))]
+    return Circuit([2, 5, 5], 8, L)
+
+
+def test_extension_layers_semantics(eng, oracle):
+    # decode(eval(garble)) == plain_forward for the extension layers too, in
+    # the oracle (pinned by restatement) and in the engine
+    c = _small_dag()
+    assert c.shapes()[5] == [3, 3, 3] and c.shapes()[7] == [3, 3, 3]
+    x = np.random.default_rng(2).integers(-7, 8, size=(3, c.n_in))
+    want = np.stack([oracle.plain_forward(c, xi) for xi in x])
+    for i in range(3):
+        onet = oracle.garble(c, seed_hex(0xD0 + i))
+        assert oracle.decode(onet, oracle.evaluate(onet, oracle.garble_inputs(onet, x[i]))).tolist() == want[i].tolist()
+    g = eng.circuit(c)
+    assert (np.stack([g.plain_forward(xi) for xi in x]) == want).all()
+    out, _ = eng.infer(g, b"".join(seed_hex(0xD0 + i) for i in range(3)), x)
+    assert (out == want).all()
+
+
+@pytest.mark.parametrize("name", ["dag", "resnet_tiny"])
+def test_extension_networks_vs_oracle(eng, oracle, name):
+    from helpers import models
+
+    c = _small_dag() if name == "dag" else models.build("resnet_tiny", 2001, 8)
+    g = eng.circuit(c)
+    B = 2
+    seeds = b"".join(seed_hex(0xE0 + i) for i in range(B))
+    x = np.random.default_rng(5).integers(-7, 8, size=(B, c.n_in))
+    net = eng.garble(g, seeds)
+    bo = eng.evaluate(net, eng.garble_inputs(net, x))
+    out = eng.decode_outputs(net, bo)
+    onet = oracle.garble(c, seed_hex(0xE1))
+    assert net.export_gc(1) == onet.gc_bytes()
+    assert net.export_decoding(1) == onet.dec_bytes()
+    ob = oracle.evaluate(onet, oracle.garble_inputs(onet, x[1]))
+    assert bo.payload(1) == ob.payload()
+    assert out[1].tolist() == oracle.decode(onet, ob).tolist()
+
+
+def test_resnet20_shape_and_cost():
+    from helpers import models
+
+    c = models.build("resnet20", 2001, 8)
+    s = c.shapes()
+    assert s[0] == [3, 32, 32] and s[-1] == [10]
+    relu = sum(int(np.prod(s[j + 1])) for j, l in enumerate(c.layers) if l.kind == 3)
+    assert relu == 188_416  # SURVEY.md 8(d): 188,416 ReLU per inference
