@@ -971,6 +971,8 @@ static void g_act_element(octx* c, int kind, const olabel* in, olabel* out, cons
 
 /* ===================== layers (layer.cpp) ===================== */
 
+#define ORC_MAXL 256 /* layers per circuit (ResNet-20 with extensions: 71) */
+
 typedef struct {
     int kind, priv;
     uint32_t in_dim, out_dim, in_ch, out_ch, filter, stride;
@@ -991,10 +993,10 @@ struct orc_circuit {
     olayer* layers;
     /* derived: shapes[0] = input, shapes[j + 1] = output of layer j;
      * ishapes[j] = input of layer j (from its DAG source) */
-    uint32_t shapes[65][8];
-    int ranks[65];
-    uint32_t ishapes[64][8];
-    int iranks[64];
+    uint32_t shapes[ORC_MAXL + 1][8];
+    int ranks[ORC_MAXL + 1];
+    uint32_t ishapes[ORC_MAXL][8];
+    int iranks[ORC_MAXL];
 };
 
 /* index into shapes[] / the per-layer value list of a layer's DAG source:
@@ -1074,7 +1076,7 @@ static int is_linear(const olayer* l) { return l->kind == DASH_LAYER_DENSE || l-
 int orc_circuit_new(const dash_circuit_desc* d, orc_circuit** out) {
     mi_init();
     if (d->k < 1 || d->k > MAXK) return fail(ORC_DATA, "CRT base size out of range");
-    if (d->rank < 1 || d->rank > 8 || d->n_layers > 64) return fail(ORC_DATA, "bad circuit shape");
+    if (d->rank < 1 || d->rank > 8 || d->n_layers > ORC_MAXL) return fail(ORC_DATA, "bad circuit shape");
     orc_circuit* c = (orc_circuit*)calloc(1, sizeof *c);
     c->k = d->k;
     c->rank = (int)d->rank;
@@ -1168,7 +1170,7 @@ static int circuit_needs_sign(const orc_circuit* c) {
 int orc_plain_forward(const orc_circuit* c, const int64_t* in, int64_t* out) {
     const ocrt b = crt_base(c->k);
     const int64_t hi = max_signed(&b), lo = min_signed(&b);
-    int64_t* vals[65] = {0};
+    int64_t* vals[ORC_MAXL + 1] = {0};
     uint64_t n0 = shape_size(c->shapes[0], c->ranks[0]);
     vals[0] = (int64_t*)malloc(sizeof(int64_t) * n0);
     memcpy(vals[0], in, sizeof(int64_t) * n0);
@@ -1495,8 +1497,8 @@ struct orc_net {
     otensor enc_bases[MAXK]; /* input lanes */
     u128* cts;
     uint64_t ncts;
-    uint64_t layer_ct_base[66];
-    uint64_t layer_gate[66], layer_wire[66];
+    uint64_t layer_ct_base[ORC_MAXL + 2];
+    uint64_t layer_gate[ORC_MAXL + 2], layer_wire[ORC_MAXL + 2];
     u128 commitment;
     u128* dec; /* [elem*k + lane][p] flattened with row offsets */
     uint64_t* dec_off;

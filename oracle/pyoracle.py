@@ -218,7 +218,7 @@ class Net:
         return out
 
     def layer_ct_base(self) -> List[int]:
-        out = (ctypes.c_uint64 * 80)()
+        out = (ctypes.c_uint64 * 260)()
         fn = self.lib.f("net_layer_ct_base")
         fn.argtypes = [vp, u64p]
         n = fn(self.h, out)

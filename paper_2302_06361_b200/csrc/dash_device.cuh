@@ -691,10 +691,11 @@ struct ActParams {
 
 // Work map of a multi-layer launch: layer li owns items [base[li], base[li+1]),
 // item -> (b, 32-element block) with wpi[li] blocks per inference.
+constexpr int MAXACT = 64;  // activation layers garbled in one launch (circuits have <= 64 layers)
 struct ItemMap {
     uint32_t n;
-    uint32_t base[MAXK + 1];
-    uint32_t wpi[MAXK];
+    uint32_t base[MAXACT + 1];
+    uint32_t wpi[MAXACT];
 };
 
 // Working buffers of one element: X (first operand / running key), K (the

@@ -105,6 +105,7 @@ static int sm_count() {
 }
 
 void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* st) {
+    if (n > MAXACT) throw std::runtime_error("too many activation layers for one launch");
     ItemMap map;
     std::memset(&map, 0, sizeof map);
     map.n = (uint32_t)n;
