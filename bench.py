@@ -144,6 +144,8 @@ WORKLOADS = {
     "lenet5": "LeNet-5 restated in reference ops, 1x28x28",
     "model_a": "784-128-128-10 ReLU MLP, testsupport::model_a",
     "minionn": "paper Model F, MiniONN-style 7-conv CIFAR CNN, 3x32x32, ReLU",
+    "resnet20": "ResNet-20 CIFAR, 3x32x32, Pad2d/Add/DAG extensions, ReLU",
+    "resnet20s": "ResNet-20 CIFAR, SignAct after every residual add",
     "model_c": "testsupport::model_c", "model_d": "testsupport::model_d",
 }
 
