@@ -665,9 +665,13 @@ DASH_HD void lb_prf(LB L, uint64_t wire, uint32_t stream, const ModC& M, const u
 }
 
 // ------------------------------------------------------------ element tape
+constexpr int MAXCHUNK = 8;  // tape chunks per element in the garbling launch
 struct ActParams {
     const TapeOp* tape;
     int n_ops;
+    // op boundaries of the tape chunks (garbling launch: chunk c of every
+    // element is a separate work item, run after chunk c-1 of that element)
+    uint16_t chunk_op[MAXCHUNK + 1];
     const uint8_t* phi;        // phi pool (values already reduced mod q)
     int k;
     uint32_t E;                // elements per inference in this layer
@@ -977,7 +981,7 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
 }
 
 template <bool GARBLE>
-DASH_HD void act_element(const ActParams& P, Elt& e) {
+DASH_HD void act_element(const ActParams& P, Elt& e, int op0, int op1) {
     e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
     e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
     e.rows = P.blob + (uint64_t)e.b * P.blob_stride + (uint64_t)e.u * P.uc_cts;
@@ -987,7 +991,7 @@ DASH_HD void act_element(const ActParams& P, Elt& e) {
         e.rk = P.rk + (uint64_t)e.b * 44;
         e.mult = P.mult + (uint64_t)e.b * P.mult_stride;
     }
-    for (int i = 0; i < P.n_ops; ++i) {
+    for (int i = op0; i < op1; ++i) {
         const TapeOp op = P.tape[i];
         if (GARBLE) garble_op(P, e, op);
         else eval_op(P, e, op);

@@ -1109,6 +1109,37 @@ static void fill_primes(const Crt& b, uint16_t* out) {
     for (int i = 0; i < b.k; ++i) out[i] = (uint16_t)b.primes[i];
 }
 
+// Splits an element's tape into K op ranges of similar garbling cost (rows +
+// PRF blocks); the garbling launch runs chunk c of every element as its own
+// work item (kernels_act.cu), which keeps the launch's last wave short.
+static void fill_chunks(ActParams& P, const Tape& T, int K) {
+    const size_t n = T.ops.size();
+    std::vector<double> cum(n + 1, 0.0);
+    for (size_t i = 0; i < n; ++i) {
+        const TapeOp& o = T.ops[i];
+        const double pb = (n_digits_host(o.pm) + 3) / 4, qb = (n_digits_host(o.qm ? o.qm : 2) + 3) / 4;
+        double c = 0.05;
+        switch (o.kind) {
+            case OP_PROJ: c = o.pm + qb; break;
+            case OP_GRR: c = o.pm; break;
+            case OP_HALF: c = 2.0 * o.pm + 2 * pb; break;
+            case OP_MMHALF: c = o.pm + 2.0 * o.qm + 2 * pb; break;
+            default: break;
+        }
+        cum[i + 1] = cum[i] + c;
+    }
+    K = std::max(1, std::min<int>(K, MAXCHUNK));
+    P.chunk_op[0] = 0;
+    size_t at = 0;
+    for (int c = 1; c < K; ++c) {
+        const double target = cum[n] * c / K;
+        while (at < n && cum[at] < target) ++at;
+        P.chunk_op[c] = (uint16_t)std::max<size_t>(at, P.chunk_op[c - 1]);
+    }
+    for (int c = K; c <= MAXCHUNK; ++c) P.chunk_op[c] = (uint16_t)n;
+}
+static constexpr int kTapeChunks = 4;
+
 // Runs one layer over B inferences.  garbler: base labels; else active.
 // in2: second operand of the Add extension.
 static void run_layer(Network& n, const HLayer& l, bool garbler, const Lanes& in, const Lanes* in2, Lanes& out) {
@@ -1216,6 +1247,7 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, const Lanes& in
     std::memset(&P, 0, sizeof P);
     P.tape = l.tape_d->as<TapeOp>();
     P.n_ops = (int)l.tape->ops.size();
+    fill_chunks(P, *l.tape, kTapeChunks);
     P.phi = l.phi_d->as<uint8_t>();
     P.k = k;
     P.E = (uint32_t)l.E_out;
@@ -1567,6 +1599,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             std::memset(&P, 0, sizeof P);
             P.tape = l.tape_d->as<TapeOp>();
             P.n_ops = (int)T.ops.size();
+            fill_chunks(P, T, kTapeChunks);
             P.phi = l.phi_d->as<uint8_t>();
             P.k = k;
             P.E = n;

@@ -28,13 +28,20 @@ namespace {
 constexpr int kLaneWords = 2 * NWMAX + 4;
 constexpr int kBufWords = kLaneWords * 32;
 
+// Work item = (tape chunk c, layer, inference, 32-element block), chunk-major:
+// every element's tape is split into nchunks op ranges of similar cost, so the
+// last wave of the persistent launch holds short items (the tail of a launch
+// with whole-tape items idles ~10 % of the warp slots).  Chunks of one
+// element communicate through the global label slots; chunk c waits for the
+// done flag of chunk c-1 (dequeued earlier, so it is running or finished).
 template <bool G>
 __global__ void __launch_bounds__(kActWarps * 32, 1)
-    act_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
+    act_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter, uint32_t* flags,
+               uint32_t nchunks) {
     uint32_t* L = s_dyn + kTabWords;
     fill_T(g_T0);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t total = map.base[map.n];
+    const uint32_t per_chunk = map.base[map.n], total = per_chunk * nchunks;
     uint32_t* lb = L + (uint64_t)warp * kBufWords + lane;
     Elt e;
     e.X = LB{lb, 32};
@@ -47,18 +54,37 @@ __global__ void __launch_bounds__(kActWarps * 32, 1)
     const uint32_t first = kActWarps * gridDim.x;
     for (;;) {
         if (item >= total) break;
+        const uint32_t c = item / per_chunk, it = item - c * per_chunk;
         uint32_t li = 0;
-        while (li + 1 < map.n && item >= map.base[li + 1]) ++li;
-        const uint32_t local = item - map.base[li];
+        while (li + 1 < map.n && it >= map.base[li + 1]) ++li;
+        const uint32_t local = it - map.base[li];
         const ActParams& P = layers[li];
         e.b = local / map.wpi[li];
         e.u = (local % map.wpi[li]) * 32 + lane;
         e.rk = nullptr;
         e.mult = nullptr;
-        if (e.u < P.E) act_element<G>(P, e);
+        if (c > 0) {
+            if (lane == 0) {
+                uint32_t v;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + it) : "memory");
+                    if (v >= c) break;
+                    __nanosleep(2000);
+                }
+            }
+            __syncwarp();
+        }
+        const int op0 = nchunks > 1 ? P.chunk_op[c] : 0, op1 = nchunks > 1 ? P.chunk_op[c + 1] : P.n_ops;
+        if (e.u < P.E) act_element<G>(P, e, op0, op1);
         __syncwarp();
         uint32_t next = 0;
-        if (lane == 0) next = first + atomicAdd(counter, 1u);
+        if (lane == 0) {
+            if (nchunks > 1) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + it), "r"(c + 1) : "memory");
+            }
+            next = first + atomicAdd(counter, 1u);
+        }
         item = __shfl_sync(0xffffffffu, next, 0);
     }
 }
@@ -94,6 +120,17 @@ static uint32_t* act_counter() {
     return counter;
 }
 
+static uint32_t* act_flags(size_t n) {
+    static uint32_t* flags = nullptr;
+    static size_t cap = 0;
+    if (n > cap) {
+        if (flags) cudaFree(flags);
+        cap = std::max<size_t>(n, 1 << 16);
+        ck(cudaMalloc(&flags, cap * sizeof(uint32_t)), "flags");
+    }
+    return flags;
+}
+
 static int sm_count() {
     static int sms = 0;
     if (!sms) {
@@ -121,12 +158,24 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kActWarps * kBufWords;
     uint32_t* counter = act_counter();
     ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
+    // garbling: chunked tapes (host_layers[].chunk_op); evaluation: whole tapes
+    uint32_t nchunks = 1;
+    if (garble) {
+        for (int i = 0; i < n; ++i)
+            for (int c = 1; c <= MAXCHUNK; ++c)
+                if (host_layers[i].chunk_op[c] == host_layers[i].n_ops) {
+                    nchunks = std::max<uint32_t>(nchunks, (uint32_t)c);
+                    break;
+                }
+    }
+    uint32_t* flags = act_flags(map.base[n]);
+    if (nchunks > 1) ck(cudaMemsetAsync(flags, 0, sizeof(uint32_t) * map.base[n], S(st)), "flags reset");
     if (garble) {
         ck(cudaFuncSetAttribute(act_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_kernel<true><<<grid, kActWarps * 32, smem, S(st)>>>(dev_layers, map, counter);
+        act_kernel<true><<<grid, kActWarps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, nchunks);
     } else {
         ck(cudaFuncSetAttribute(act_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_kernel<false><<<grid, kActWarps * 32, smem, S(st)>>>(dev_layers, map, counter);
+        act_kernel<false><<<grid, kActWarps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, 1);
     }
     ck(cudaGetLastError(), "act launch");
 }

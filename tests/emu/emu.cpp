@@ -72,8 +72,8 @@ static void act_layer(const ActParams& P, bool garble) {
             e.t = tab();
             e.rk = nullptr;
             e.mult = nullptr;
-            if (garble) act_element<true>(P, e);
-            else act_element<false>(P, e);
+            if (garble) act_element<true>(P, e, 0, P.n_ops);
+            else act_element<false>(P, e, 0, P.n_ops);
         }
 }
 
