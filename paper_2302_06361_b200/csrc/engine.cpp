@@ -18,6 +18,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -1138,7 +1139,14 @@ static void fill_chunks(ActParams& P, const Tape& T, int K) {
     }
     for (int c = K; c <= MAXCHUNK; ++c) P.chunk_op[c] = (uint16_t)n;
 }
-static constexpr int kTapeChunks = 4;
+// chunks per element tape in the garbling launch (DASH_TAPE_CHUNKS overrides, for tuning)
+static int tape_chunks() {
+    static int k = [] {
+        const char* v = std::getenv("DASH_TAPE_CHUNKS");
+        return v ? std::max(1, std::min(MAXCHUNK, std::atoi(v))) : 8;
+    }();
+    return k;
+}
 
 // Runs one layer over B inferences.  garbler: base labels; else active.
 // in2: second operand of the Add extension.
@@ -1247,7 +1255,7 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, const Lanes& in
     std::memset(&P, 0, sizeof P);
     P.tape = l.tape_d->as<TapeOp>();
     P.n_ops = (int)l.tape->ops.size();
-    fill_chunks(P, *l.tape, kTapeChunks);
+    fill_chunks(P, *l.tape, tape_chunks());
     P.phi = l.phi_d->as<uint8_t>();
     P.k = k;
     P.E = (uint32_t)l.E_out;
@@ -1599,7 +1607,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             std::memset(&P, 0, sizeof P);
             P.tape = l.tape_d->as<TapeOp>();
             P.n_ops = (int)T.ops.size();
-            fill_chunks(P, T, kTapeChunks);
+            fill_chunks(P, T, tape_chunks());
             P.phi = l.phi_d->as<uint8_t>();
             P.k = k;
             P.E = n;

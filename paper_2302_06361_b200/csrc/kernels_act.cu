@@ -35,7 +35,7 @@ constexpr int kBufWords = kLaneWords * 32;
 // element communicate through the global label slots; chunk c waits for the
 // done flag of chunk c-1 (dequeued earlier, so it is running or finished).
 template <bool G>
-__global__ void __launch_bounds__(kActWarps * 32, 1)
+__global__ void __launch_bounds__((G ? kActWarpsGarble : kActWarpsEval) * 32, 1)
     act_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter, uint32_t* flags,
                uint32_t nchunks) {
     uint32_t* L = s_dyn + kTabWords;
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kActWarps * 32, 1)
     // first round: item = warp * grid + cta spreads small launches over all
     // SMs; afterwards warps pull items from the counter (balanced tail)
     uint32_t item = warp * gridDim.x + blockIdx.x;
-    const uint32_t first = kActWarps * gridDim.x;
+    const uint32_t first = (G ? kActWarpsGarble : kActWarpsEval) * gridDim.x;
     for (;;) {
         if (item >= total) break;
         const uint32_t c = item / per_chunk, it = item - c * per_chunk;
@@ -155,7 +155,8 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     // one CTA per SM (the first round strides items across SMs), never fewer
     // CTAs than needed to give every item its own SM when items < #SMs
     const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), map.base[n]);
-    const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kActWarps * kBufWords;
+    const int warps = garble ? kActWarpsGarble : kActWarpsEval;
+    const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)warps * kBufWords;
     uint32_t* counter = act_counter();
     ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
     // garbling: chunked tapes (host_layers[].chunk_op); evaluation: whole tapes
@@ -172,10 +173,10 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     if (nchunks > 1) ck(cudaMemsetAsync(flags, 0, sizeof(uint32_t) * map.base[n], S(st)), "flags reset");
     if (garble) {
         ck(cudaFuncSetAttribute(act_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_kernel<true><<<grid, kActWarps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, nchunks);
+        act_kernel<true><<<grid, warps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, nchunks);
     } else {
         ck(cudaFuncSetAttribute(act_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_kernel<false><<<grid, kActWarps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, 1);
+        act_kernel<false><<<grid, warps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, 1);
     }
     ck(cudaGetLastError(), "act launch");
 }

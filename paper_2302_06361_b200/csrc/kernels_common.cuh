@@ -13,7 +13,13 @@
 
 namespace dashgpu {
 
-constexpr int kActWarps = 24;  // warps per CTA of the activation kernels (one CTA per SM)
+// Warps per CTA of the activation kernels (one CTA per SM).  Garbling is
+// latency-bound and gains from every extra warp up to the shared-memory cap
+// (64 KB AES tables + 28 x 5.5 KB label buffers = 218 KB); evaluation is
+// fastest at 24 (measured on B200: garble 59.1 -> 55.9 ms from 24 to 28
+// warps, eval 13.7 -> 15.2 ms).
+constexpr int kActWarpsGarble = 28;
+constexpr int kActWarpsEval = 24;
 constexpr int kTWords = 256 * 32;
 
 inline void ck(cudaError_t e, const char* what) {
