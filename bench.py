@@ -377,9 +377,14 @@ def main():
     elems_per_launch = (info.relu_elements * B) / max(1, act_n / max(1, args.steps)) if act_n else 0
     achieved = (bytes_per_elem * elems_per_launch) / ((act_ms / act_n) / 1e3) / 1e9 if act_n else 0.0
     traffic = None
+    issue = {}
     tp = os.path.join(ROOT, "profiles", "act_garble_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        tj = json.load(open(tp))
+        traffic = tj.get("dram_bytes_per_launch")
+        # the kernel is integer-issue bound (SURVEY 8(d) honest note): ncu's
+        # issue-active and ALU-pipe fractions are its real roofline
+        issue = {k: tj[k] for k in ("issue_active_frac", "alu_pipe_frac", "warps_active_per_sm") if k in tj}
     launches = sum(v[1] for v in prof.values())
     # public linear lanes on the tensor cores (tcgen05 kind::i8): algorithmic
     # digit-MACs (K * units * sum n_p per pass, garble + eval) vs the nominal
@@ -426,7 +431,8 @@ def main():
                      "kernel": "act_kernel<garble> (ReLU gadget tape)", "peak_source": peak_src,
                      "bytes_per_element": bytes_per_elem,
                      "kernel_ms_per_step": act_ms / args.steps,
-                     "kernel_share_of_step": (act_ms / args.steps) / (ms / args.steps)},
+                     "kernel_share_of_step": (act_ms / args.steps) / (ms / args.steps),
+                     "issue_roofline_ncu": issue or None},
         "roofline_linear": roof_lin,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "inferences/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
