@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--model", default=MODEL)
     ap.add_argument("--k", type=int, default=K)
+    ap.add_argument("--private", action="store_true", help="private-weight linear layers (projection per weight, "
+                                                           "the JSON model default, model_io.cpp:56)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="inferences in the CPU-baseline sample")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (config sweeps)")
     ap.add_argument("--sweep", default="", help="label-ops sweep (BASELINE configs[4]): 'proj' and/or 'linear', "
@@ -296,7 +298,7 @@ def main():
     stream = torch.cuda.current_stream()
     eng = Dash(local)
     eng.set_stream(stream.cuda_stream)
-    g = eng.model(args.model, SEED, args.k)
+    g = eng.model(args.model, SEED, args.k, private=args.private)
     info = g.info
     B = args.batch
     n_in, n_out = info.n_in, info.n_out
@@ -421,7 +423,8 @@ def main():
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": f"{args.model} ({WORKLOADS.get(args.model, 'single-layer sweep')}) k={args.k}, "
+        "config": {"workload": f"{args.model}{' (private weights)' if args.private else ''} "
+                               f"({WORKLOADS.get(args.model, 'single-layer sweep')}) k={args.k}, "
                                f"synthetic inputs U[-7,7], batch {B} per GPU, fresh seed per inference per step",
                    "global_batch": world * B, "inferences_per_gpu": B, "parallelism": f"inference-sharded x{world}",
                    "l2": "per-step garbled tables (%.1f GB) exceed L2; no flush needed" % (info.cts * 16 * B / 1e9),

@@ -13,6 +13,8 @@ __device__ uint32_t g_T0[256];
 #define DASH_CONST_DEFINED 1
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 #include "dash_prim.cuh"
 #include "kernels_common.cuh"
 #include "tc_linear.cuh"
@@ -41,11 +43,114 @@ void prof_drain() {
     prof().pending.clear();
 }
 
-__global__ void __launch_bounds__(128) private_kernel(PrivParams P) {
+// Private-weight linear lane (layer.cpp:195-212, 456-507), warp-cooperative:
+// one warp = one (inference, output unit); lane t takes window weights
+// j = t, t+32, ...: its projection gate x_j -> w_j x_j (p rows, fresh output
+// label) is garbled / evaluated independently, then the 32 term labels are
+// summed with a shuffle butterfly (free add, digit-wise mod p) and the
+// garbler subtracts b R_p (add_public_constant).  Every branch is
+// warp-uniform (one lane modulus per launch); labels live in lane-interleaved
+// shared memory next to the AES tables; persistent CTAs pull units from a
+// counter.  Ciphertext rows keep the reference's order (unit-major, weight,
+// row), so the blob is byte-identical to garble_layer's.
+constexpr int kPrivWarps = 20;
+constexpr int kPrivLaneWords = 3 * NWMAX;
+
+DASH_HD void warp_sum_label(LB A, LB T, bool active, const ModC& M) {
+#if defined(__CUDA_ARCH__)
+    if (M.pow2) {
+        U4 v = lb_u4(T);
+        if (!active) v.x[0] = v.x[1] = v.x[2] = v.x[3] = 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] = __shfl_xor_sync(0xffffffffu, v.x[i], off);
+            p2_add(v.x, o, M);
+        }
+        U4 a = lb_u4(A);
+        p2_add(a.x, v.x, M);
+        lb_set_u4(A, a);
+        return;
+    }
+    for (int w = 0; w < M.nw; ++w) {
+        uint32_t v = active ? T[w] : 0u;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = swar_add(v, __shfl_xor_sync(0xffffffffu, v, off), M);
+        A[w] = swar_add(A[w], v, M);
+    }
+#endif
+}
+
+template <bool G>
+__global__ void __launch_bounds__(kPrivWarps * 32, 1) private_kernel(const __grid_constant__ PrivParams P,
+                                                                      uint32_t* counter) {
     fill_T(g_T0);
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= P.M) return;
-    private_thread(P, blockIdx.y, u, make_tab(nullptr, threadIdx.x & 31u));
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* lb = s_dyn + kTabWords + warp * kPrivLaneWords * 32 + lane;
+    const LB X{lb, 32}, T{lb + NWMAX * 32, 32}, A{lb + 2 * NWMAX * 32, 32};
+    const AesTab t = make_tab(nullptr, lane);
+    const ModC& M = c_mod[P.p];
+    const uint32_t p = P.p, total = P.B * P.M;
+    const uint32_t* Rp = G ? P.mult + ((uint64_t)c_modslot[p] * 128u + 1) * NWMAX : nullptr;
+    uint32_t item = warp * gridDim.x + blockIdx.x;
+    const uint32_t first = kPrivWarps * gridDim.x;
+    while (item < total) {
+        const uint32_t b = item / P.M, u = item - b * P.M;
+        const uint32_t* rk = P.rk + (uint64_t)b * 44;
+        const uint32_t* mult = P.mult + (uint64_t)b * P.mult_stride;
+        const uint32_t* Rb = G ? mult + ((uint64_t)c_modslot[p] * 128u + 1) * NWMAX : nullptr;
+        (void)Rp;
+        uint32_t oc = 0, oy = 0, ox = 0;
+        if (P.conv) {
+            oc = u / (P.OH * P.OW);
+            oy = (u / P.OW) % P.OH;
+            ox = u % P.OW;
+        }
+        const uint8_t* wr = P.wres + (uint64_t)(P.conv ? oc : u) * P.win;
+        for (int w = 0; w < lb_words(M); ++w) A[w] = 0;
+        for (uint32_t j0 = 0; j0 < P.win; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const bool active = j < P.win;
+            if (active) {
+                uint64_t xi;
+                if (!P.conv) {
+                    xi = j;
+                } else {
+                    const uint32_t ic = j / (P.f * P.f), ky = (j / P.f) % P.f, kx = j % P.f;
+                    xi = ((uint64_t)ic * P.H + (oy * P.stride + ky)) * P.W + (ox * P.stride + kx);
+                }
+                lb_load_rows(X, P.in + ((uint64_t)b * M.nw) * P.E_in + xi, P.E_in, M);
+                const uint64_t g = P.gate_base + (uint64_t)u * P.win + j;
+                U4* R = P.blob + (uint64_t)b * P.blob_stride + ((uint64_t)u * P.win + j) * p;
+                const uint32_t c = lb_color(X, M);
+                if (G) {
+                    lb_prf(T, P.wire_base + (uint64_t)u * P.win + j, 0, M, rk, t);
+                    const uint32_t wv = wr[j];
+                    for (uint32_t a = 0; a < p; ++a) {
+                        uint32_t row = c + a;
+                        row = row >= p ? row - p : row;
+                        const U4 H = hash_tw(lb_key_step(X, Rb, M), g, row, 0, t);
+                        R[row] = lb_enc(H, T, mult + ((uint64_t)c_modslot[p] * 128u + (wv * a) % p) * NWMAX, nullptr,
+                                        0, M);
+                    }
+                } else {
+                    lb_dec(T, R[c], hash_tw(lb_compress(X, M), g, c, 0, t), M);
+                }
+            }
+            __syncwarp();
+            warp_sum_label(A, T, active, M);
+        }
+        if (G) {
+            const uint32_t bb = P.bres[P.conv ? oc : u];
+            if (bb) lb_sub_g(A, mult + ((uint64_t)c_modslot[p] * 128u + bb) * NWMAX, M);
+        }
+        if (lane == 0) lb_store_rows(A, P.out + ((uint64_t)b * M.nw) * P.M + u, P.M, M);
+        __syncwarp();
+        uint32_t next = 0;
+        if (lane == 0) next = first + atomicAdd(counter, 1u);
+        item = __shfl_sync(0xffffffffu, next, 0);
+    }
 }
 
 __global__ void __launch_bounds__(128) pad_add_kernel(const __grid_constant__ PadAddParams P) {
@@ -254,8 +359,21 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
 void launch_private(const PrivParams& P, void* st) {
     if (P.B == 0 || P.M == 0) return;
     ProfScope ps(P.garbler ? K_PRIV_GARBLE : K_PRIV_EVAL, S(st));
-    ck(cudaFuncSetAttribute(private_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
-    private_kernel<<<dim3(cdiv(P.M, 128), P.B), 128, kTabBytes, S(st)>>>(P);
+    static uint32_t* counter = nullptr;
+    if (!counter) ck(cudaMalloc(&counter, sizeof(uint32_t)), "counter");
+    ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
+    int sms = 0, dev = 0;
+    ck(cudaGetDevice(&dev), "dev");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+    const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kPrivWarps * kPrivLaneWords * 32;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sms, cdiv((uint64_t)P.B * P.M, 1));
+    if (P.garbler) {
+        ck(cudaFuncSetAttribute(private_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        private_kernel<true><<<grid, kPrivWarps * 32, smem, S(st)>>>(P, counter);
+    } else {
+        ck(cudaFuncSetAttribute(private_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        private_kernel<false><<<grid, kPrivWarps * 32, smem, S(st)>>>(P, counter);
+    }
     dev::check();
 }
 
