@@ -53,8 +53,9 @@ void prof_drain() {
 // shared memory next to the AES tables; persistent CTAs pull units from a
 // counter.  Ciphertext rows keep the reference's order (unit-major, weight,
 // row), so the blob is byte-identical to garble_layer's.
-constexpr int kPrivWarps = 20;
-constexpr int kPrivLaneWords = 3 * NWMAX;
+constexpr int kPrivWarps = 24;
+constexpr int kPrivLaneWords = 2 * NWMAX;  // X, T per lane (lane-interleaved) + one warp-shared sum
+constexpr int kPrivWarpWords = kPrivLaneWords * 32 + NWMAX;
 
 DASH_HD void warp_sum_label(LB A, LB T, bool active, const ModC& M) {
 #if defined(__CUDA_ARCH__)
@@ -70,14 +71,19 @@ DASH_HD void warp_sum_label(LB A, LB T, bool active, const ModC& M) {
         }
         U4 a = lb_u4(A);
         p2_add(a.x, v.x, M);
-        lb_set_u4(A, a);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) lb_set_u4(A, a);
+        __syncwarp();
         return;
     }
     for (int w = 0; w < M.nw; ++w) {
         uint32_t v = active ? T[w] : 0u;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v = swar_add(v, __shfl_xor_sync(0xffffffffu, v, off), M);
-        A[w] = swar_add(A[w], v, M);
+        const uint32_t s = swar_add(A[w], v, M);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) A[w] = s;
+        __syncwarp();
     }
 #endif
 }
@@ -87,8 +93,9 @@ __global__ void __launch_bounds__(kPrivWarps * 32, 1) private_kernel(const __gri
                                                                       uint32_t* counter) {
     fill_T(g_T0);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* lb = s_dyn + kTabWords + warp * kPrivLaneWords * 32 + lane;
-    const LB X{lb, 32}, T{lb + NWMAX * 32, 32}, A{lb + 2 * NWMAX * 32, 32};
+    uint32_t* wb = s_dyn + kTabWords + warp * kPrivWarpWords;
+    // the running sum is identical in every lane (butterfly): one warp copy
+    const LB X{wb + lane, 32}, T{wb + NWMAX * 32 + lane, 32}, A{wb + kPrivLaneWords * 32, 1};
     const AesTab t = make_tab(nullptr, lane);
     const ModC& M = c_mod[P.p];
     const uint32_t p = P.p, total = P.B * P.M;
@@ -108,7 +115,9 @@ __global__ void __launch_bounds__(kPrivWarps * 32, 1) private_kernel(const __gri
             ox = u % P.OW;
         }
         const uint8_t* wr = P.wres + (uint64_t)(P.conv ? oc : u) * P.win;
-        for (int w = 0; w < lb_words(M); ++w) A[w] = 0;
+        if (lane == 0)
+            for (int w = 0; w < lb_words(M); ++w) A[w] = 0;
+        __syncwarp();
         for (uint32_t j0 = 0; j0 < P.win; j0 += 32) {
             const uint32_t j = j0 + lane;
             const bool active = j < P.win;
@@ -127,12 +136,14 @@ __global__ void __launch_bounds__(kPrivWarps * 32, 1) private_kernel(const __gri
                 if (G) {
                     lb_prf(T, P.wire_base + (uint64_t)u * P.win + j, 0, M, rk, t);
                     const uint32_t wv = wr[j];
+                    const uint32_t* mrow = mult + (uint64_t)c_modslot[p] * 128u * NWMAX;
+                    uint32_t row = c, v = 0;  // row (c + a) mod p carries payload (w a mod p) R_p
                     for (uint32_t a = 0; a < p; ++a) {
-                        uint32_t row = c + a;
-                        row = row >= p ? row - p : row;
                         const U4 H = hash_tw(lb_key_step(X, Rb, M), g, row, 0, t);
-                        R[row] = lb_enc(H, T, mult + ((uint64_t)c_modslot[p] * 128u + (wv * a) % p) * NWMAX, nullptr,
-                                        0, M);
+                        R[row] = lb_enc(H, T, mrow + (uint64_t)v * NWMAX, nullptr, 0, M);
+                        row = row + 1 == p ? 0 : row + 1;
+                        v += wv;
+                        v = v >= p ? v - p : v;
                     }
                 } else {
                     lb_dec(T, R[c], hash_tw(lb_compress(X, M), g, c, 0, t), M);
@@ -141,11 +152,13 @@ __global__ void __launch_bounds__(kPrivWarps * 32, 1) private_kernel(const __gri
             __syncwarp();
             warp_sum_label(A, T, active, M);
         }
-        if (G) {
-            const uint32_t bb = P.bres[P.conv ? oc : u];
-            if (bb) lb_sub_g(A, mult + ((uint64_t)c_modslot[p] * 128u + bb) * NWMAX, M);
+        if (lane == 0) {  // A is one warp-shared copy: lane 0 finishes the unit
+            if (G) {
+                const uint32_t bb = P.bres[P.conv ? oc : u];
+                if (bb) lb_sub_g(A, mult + ((uint64_t)c_modslot[p] * 128u + bb) * NWMAX, M);
+            }
+            lb_store_rows(A, P.out + ((uint64_t)b * M.nw) * P.M + u, P.M, M);
         }
-        if (lane == 0) lb_store_rows(A, P.out + ((uint64_t)b * M.nw) * P.M + u, P.M, M);
         __syncwarp();
         uint32_t next = 0;
         if (lane == 0) next = first + atomicAdd(counter, 1u);
@@ -365,7 +378,7 @@ void launch_private(const PrivParams& P, void* st) {
     int sms = 0, dev = 0;
     ck(cudaGetDevice(&dev), "dev");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
-    const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kPrivWarps * kPrivLaneWords * 32;
+    const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kPrivWarps * kPrivWarpWords;
     const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sms, cdiv((uint64_t)P.B * P.M, 1));
     if (P.garbler) {
         ck(cudaFuncSetAttribute(private_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
