@@ -761,6 +761,26 @@ struct DevBuf {
     }
 };
 
+// pinned host memory (asynchronous uploads of launch parameters)
+struct HostBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() { dev::host_release(p); }
+    void ensure(size_t bytes) {
+        if (bytes <= n && p) return;
+        dev::host_release(p);
+        p = dev::host_alloc(bytes);
+        n = bytes;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
 static void* g_stream = nullptr;
 
 struct HLayer {
@@ -1088,8 +1108,21 @@ struct Network {
     std::unique_ptr<struct Bundle> bin, bout;  // dashgpu_infer's cached bundles
     // garbling of every activation layer is one launch over these
     std::vector<ActParams> act_host;
-    DevBuf act_dev;        // [act_cap] ActParams (last entry: evaluation scratch)
-    size_t act_cap = 0;
+    // launch parameters: [0, nact) the garbling launch, [nact + li) the
+    // evaluation launch of layer li; staged through pinned memory so that
+    // enqueueing never blocks the host on the stream
+    DevBuf act_dev;
+    HostBuf act_pin, rk_pin, res_pin, err_pin;
+    size_t act_cap = 0, nact = 0;
+    // work-queue state of this network's persistent kernels
+    DevBuf qctr, qflags;
+    Sched sched() const {
+        Sched q;
+        q.counter = qctr.as<uint32_t>();
+        q.flags = qflags.as<uint32_t>();
+        q.flags_cap = qflags.n / 4;
+        return q;
+    }
     size_t slot_used = 0;  // U4 entries of `slots` handed out to garbled layers
     uint64_t mult_stride = 0;
     uint32_t sum_p = 0;
@@ -1150,7 +1183,8 @@ static int tape_chunks() {
 
 // Runs one layer over B inferences.  garbler: base labels; else active.
 // in2: second operand of the Add extension.
-static void run_layer(Network& n, const HLayer& l, bool garbler, const Lanes& in, const Lanes* in2, Lanes& out) {
+static void run_layer(Network& n, size_t li, const HLayer& l, bool garbler, const Lanes& in, const Lanes* in2,
+                      Lanes& out) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
     out.ensure(c.base, n.B, l.E_out);
@@ -1247,7 +1281,7 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, const Lanes& in
             P.mult = n.mult.as<uint32_t>();
             P.mult_stride = n.mult_stride;
             P.garbler = garbler;
-            launch_private(P, g_stream);
+            launch_private(P, g_stream, n.sched());
         }
         return;
     }
@@ -1291,8 +1325,11 @@ static void run_layer(Network& n, const HLayer& l, bool garbler, const Lanes& in
     }
     for (int i = 0; i < k; ++i) P.in[i] = in.lane[i]->as<uint32_t>();
     P.slots = n.slots.as<U4>();
-    dev::h2d(n.act_dev.as<ActParams>() + n.act_cap - 1, &P, sizeof P, g_stream);
-    launch_act_multi(n.act_dev.as<ActParams>() + n.act_cap - 1, &P, 1, false, g_stream);
+    ActParams* pin = n.act_pin.as<ActParams>() + n.nact + li;
+    ActParams* dp = n.act_dev.as<ActParams>() + n.nact + li;
+    *pin = P;
+    dev::h2d(dp, pin, sizeof P, g_stream);
+    launch_act_multi(dp, pin, 1, false, g_stream, n.sched());
 }
 
 static void network_reserve(Network& n, uint32_t B) {
@@ -1326,8 +1363,18 @@ static void network_reserve(Network& n, uint32_t B) {
             ++nact;
         }
     n.slots.ensure(std::max<size_t>(slot_total, 1) * 16);
-    n.act_cap = nact + 1;
+    n.nact = nact;
+    n.act_cap = nact + c.layers.size();
     n.act_dev.ensure(n.act_cap * sizeof(ActParams));
+    n.act_pin.ensure(n.act_cap * sizeof(ActParams));
+    n.rk_pin.ensure((size_t)B * (44 * 4 + 16));
+    n.res_pin.ensure((size_t)B * c.n_out * k + 16);
+    n.err_pin.ensure(64);
+    size_t items = 0;  // work items per tape chunk of the garbling launch
+    for (const auto& l : c.layers)
+        if (l.tape) items += (size_t)B * ((l.E_out + 31) / 32);
+    n.qctr.ensure(64);
+    n.qflags.ensure(std::max<size_t>(items, 1) * 4);
 }
 
 // All layers of the circuit in order (DAG inputs per layer, see
@@ -1348,7 +1395,7 @@ static const Lanes* run_layers(Network& n, bool garbler, const Lanes& input) {
         }
         if (!O.own[li + 1]) O.own[li + 1] = std::make_unique<Lanes>();
         const Lanes* src2 = l.kind == DASH_LAYER_ADD ? O.at[src_index(li, l.src2)] : nullptr;
-        run_layer(n, l, garbler, *src, src2, *O.own[li + 1]);
+        run_layer(n, li, l, garbler, *src, src2, *O.own[li + 1]);
         O.at[li + 1] = O.own[li + 1].get();
     }
     return O.at[L];
@@ -1369,8 +1416,11 @@ static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds
         std::memcpy(n.seeds.data(), seeds, 16 * (size_t)B);
     }
     for (uint32_t b = 0; b < B; ++b) aes_expand_host(n.seeds.data() + 16 * (size_t)b, rk.data() + 44 * (size_t)b);
-    dev::h2d(n.rk.p, rk.data(), rk.size() * 4, g_stream);
-    dev::h2d(n.seeds_d.p, n.seeds.data(), n.seeds.size(), g_stream);
+    std::memcpy(n.rk_pin.p, rk.data(), rk.size() * 4);
+    dev::h2d(n.rk.p, n.rk_pin.p, rk.size() * 4, g_stream);
+    uint8_t* seeds_pin = n.rk_pin.as<uint8_t>() + (size_t)B * 44 * 4;
+    std::memcpy(seeds_pin, n.seeds.data(), n.seeds.size());
+    dev::h2d(n.seeds_d.p, seeds_pin, n.seeds.size(), g_stream);
     // zero / Rb rows are addressed per lane with stride LABW between inferences
     // in linear_thread; store them lane-major: [k][B][LABW]
     SetupParams S;
@@ -1395,8 +1445,10 @@ static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds
     n.slot_used = 0;
     const Lanes* cur = run_layers(n, true, n.base);
     if (!n.act_host.empty()) {
-        dev::h2d(n.act_dev.p, n.act_host.data(), n.act_host.size() * sizeof(ActParams), g_stream);
-        launch_act_multi(n.act_dev.as<ActParams>(), n.act_host.data(), (int)n.act_host.size(), true, g_stream);
+        std::memcpy(n.act_pin.p, n.act_host.data(), n.act_host.size() * sizeof(ActParams));
+        dev::h2d(n.act_dev.p, n.act_pin.p, n.act_host.size() * sizeof(ActParams), g_stream);
+        launch_act_multi(n.act_dev.as<ActParams>(), n.act_host.data(), (int)n.act_host.size(), true, g_stream,
+                         n.sched());
     }
     // decoding tables from the final base labels
     DecodeParams D;
@@ -1414,7 +1466,9 @@ static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds
     launch_dectable(D, g_stream);
 }
 
-static void encode_into(Network& n, const int64_t* values, bool on_device, Bundle& out) {
+// garble_inputs, enqueued on the network's stream; the range check result
+// lands in err_pin[0] (encode_finish reads it after the stream is synced)
+static void encode_enqueue(Network& n, const int64_t* values, bool on_device, Bundle& out) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
     const int64_t* vd = values;
@@ -1447,10 +1501,17 @@ static void encode_into(Network& n, const int64_t* values, bool on_device, Bundl
     P.half_dn_hi = (uint64_t)(half_dn >> 64);
     P.err = n.err.as<int>();
     launch_encode(P, g_stream);
-    int err = 0;
-    dev::d2h(&err, n.err.p, 4, g_stream);
+    dev::d2h(n.err_pin.as<int>(), n.err.p, 4, g_stream);
+}
+
+static void encode_finish(Network& n) {
+    if (n.err_pin.as<int>()[0]) throw DataError("encode_signed: value outside the representable range");
+}
+
+static void encode_into(Network& n, const int64_t* values, bool on_device, Bundle& out) {
+    encode_enqueue(n, values, on_device, out);
     dev::sync(g_stream);
-    if (err) throw DataError("encode_signed: value outside the representable range");
+    encode_finish(n);
 }
 
 // evaluate (garble.cpp:265-312)
@@ -1489,8 +1550,9 @@ static void crt_decode(const dashgpu_circuit& c, const uint8_t* res, uint64_t co
     }
 }
 
-// decode_outputs (garble.cpp:314-343); CRT reconstruction on the host
-static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool values_on_device) {
+// decode_outputs (garble.cpp:314-343): table lookup on the device (enqueued,
+// residues + miss flag land in pinned memory), CRT reconstruction on the host
+static void decode_enqueue(Network& n, const Bundle& outb) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
     if (!outb.output || outb.B != n.B) throw DataError("output lane count mismatch");
@@ -1507,20 +1569,30 @@ static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool va
     D.err = n.err.as<int>();
     dev::memset0(n.err.p, 4, g_stream);
     launch_decode(D, g_stream);
-    std::vector<uint8_t> res((size_t)n.B * c.n_out * k);
-    int err = 0;
-    dev::d2h(res.data(), n.resid.p, res.size(), g_stream);
-    dev::d2h(&err, n.err.p, 4, g_stream);
-    dev::sync(g_stream);
-    if (err) throw AuthError("output label not present in the decoding table");
+    dev::d2h(n.res_pin.p, n.resid.p, (size_t)n.B * c.n_out * k, g_stream);
+    dev::d2h(n.err_pin.as<int>() + 1, n.err.p, 4, g_stream);
+}
+
+static void decode_finish(Network& n, int64_t* values, bool values_on_device) {
+    dashgpu_circuit& c = *n.c;
+    if (n.err_pin.as<int>()[1]) throw AuthError("output label not present in the decoding table");
     std::vector<int64_t> host;
     int64_t* dst = values;
     if (values_on_device) {
         host.resize((size_t)n.B * c.n_out);
         dst = host.data();
     }
-    crt_decode(c, res.data(), (uint64_t)n.B * c.n_out, dst);
-    if (values_on_device) dev::h2d(values, host.data(), host.size() * 8, g_stream);
+    crt_decode(c, n.res_pin.as<uint8_t>(), (uint64_t)n.B * c.n_out, dst);
+    if (values_on_device) {
+        dev::h2d(values, host.data(), host.size() * 8, g_stream);
+        dev::sync(g_stream);
+    }
+}
+
+static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool values_on_device) {
+    decode_enqueue(n, outb);
+    dev::sync(g_stream);
+    decode_finish(n, values, values_on_device);
 }
 
 // ============================================================ streamed layers
@@ -1534,7 +1606,7 @@ static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool va
 // ciphertext u*uc.cts inside the layer (layer.cpp:531-541).  Every chunk
 // buffer is C elements wide; only the id bases move.
 struct StreamWS {
-    DevBuf rk, seeds, mult, zero, Rb, commit, blob, slots, dec, vals, resid, err, actp;
+    DevBuf rk, seeds, mult, zero, Rb, commit, blob, slots, dec, vals, resid, err, actp, qctr, qflags;
     Lanes base, in, gout, eout;
     uint64_t C = 0;
 };
@@ -1570,6 +1642,12 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
     w.resid.ensure((size_t)C * k);
     w.err.ensure(16);
     w.actp.ensure(sizeof(ActParams));
+    w.qctr.ensure(64);
+    w.qflags.ensure(((C + 31) / 32 + 1) * 4);
+    Sched q;
+    q.counter = w.qctr.as<uint32_t>();
+    q.flags = w.qflags.as<uint32_t>();
+    q.flags_cap = w.qflags.n / 4;
     w.base.ensure(c.base, 1, C);
     w.in.ensure(c.base, 1, C);
     w.gout.ensure(c.base, 1, C);
@@ -1633,7 +1711,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             fill_primes(c.base, primes);
             launch_act_outputs(P, primes, g_stream);
             dev::h2d(w.actp.p, &P, sizeof P, g_stream);
-            launch_act_multi(w.actp.as<ActParams>(), &P, 1, true, g_stream);
+            launch_act_multi(w.actp.as<ActParams>(), &P, 1, true, g_stream, q);
             DecodeParams D;
             std::memset(&D, 0, sizeof D);
             D.B = 1;
@@ -1683,7 +1761,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
                 P.out[i] = w.eout.lane[i]->as<uint32_t>();
             }
             dev::h2d(w.actp.p, &P, sizeof P, g_stream);
-            launch_act_multi(w.actp.as<ActParams>(), &P, 1, false, g_stream);
+            launch_act_multi(w.actp.as<ActParams>(), &P, 1, false, g_stream, q);
             dev::sync(g_stream);
             const auto t3 = clk::now();
             // decode_outputs of the chunk
@@ -2425,20 +2503,27 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
             if (l.tape) slots += (uint64_t)l.tape->nslots * l.E_out * 16;
         const uint64_t per = c->total_cts * 16 + (uint64_t)(MAXMOD - 1) * 128 * NWMAX * 4 + planes + slots +
                              c->n_out * 600 * 16 + 4096;
-        if (!c->workspace) {
-            c->workspace = std::make_unique<Network>();
-            c->workspace->c = c;
-            c->workspace->bin = std::make_unique<Bundle>();
-            c->workspace->bout = std::make_unique<Bundle>();
-        }
-        Network& n = *c->workspace;
+        auto make_ws = [&](std::unique_ptr<Network>& ws) {
+            if (!ws) {
+                ws = std::make_unique<Network>();
+                ws->c = c;
+                ws->bin = std::make_unique<Bundle>();
+                ws->bout = std::make_unique<Bundle>();
+            }
+            return ws.get();
+        };
+        dashgpu_timing tm;
+        std::memset(&tm, 0, sizeof tm);
+        // One network, sub-batched to free HBM.  (Running two half-batches on
+        // two streams was measured slower: the persistent garbling / eval
+        // CTAs hold 196-218 KB of shared memory, so the other stream's
+        // kernels cannot co-reside and the halves serialize.)
+        Network& n = *make_ws(c->workspace);
         uint32_t chunk = batch;
         if (n.cap < batch) {
             const uint64_t budget = (uint64_t)(dev::free_bytes() * 0.85) + (uint64_t)n.cap * per;
             chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(batch, budget / per));
         }
-        dashgpu_timing tm;
-        std::memset(&tm, 0, sizeof tm);
         Bundle& in = *n.bin;
         Bundle& out = *n.bout;
         for (uint32_t b0 = 0; b0 < batch; b0 += chunk) {

@@ -30,8 +30,15 @@ ProfData& prof() {
 
 namespace {
 
-void prof_drain() {
+// all = false: only the events that already completed (a stream sync must
+// not wait on another stream's work: pipelined inference runs two streams)
+void prof_drain(bool all = true) {
+    std::vector<ProfData::Pending> keep;
     for (auto& p : prof().pending) {
+        if (!all && cudaEventQuery(p.b) != cudaSuccess) {
+            keep.push_back(p);
+            continue;
+        }
         cudaEventSynchronize(p.b);
         float ms = 0;
         cudaEventElapsedTime(&ms, p.a, p.b);
@@ -40,7 +47,7 @@ void prof_drain() {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
     }
-    prof().pending.clear();
+    prof().pending.swap(keep);
 }
 
 // Private-weight linear lane (layer.cpp:195-212, 456-507), warp-cooperative:
@@ -259,7 +266,7 @@ void memset0(void* p, size_t n, void* st) {
 }
 void sync(void* st) {
     ck(cudaStreamSynchronize(S(st)), "sync");
-    if (prof().on) prof_drain();
+    if (prof().on) prof_drain(false);
 }
 void check() { ck(cudaGetLastError(), "launch"); }
 size_t free_bytes() {
@@ -273,6 +280,26 @@ void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* m
     ck(cudaMemcpyToSymbol(c_modslot, modslot, sizeof(uint16_t) * (MAXMOD + 1)), "c_modslot");
     ck(cudaMemcpyToSymbol(g_T0, T0, sizeof(uint32_t) * 256), "g_T0");
     upload_act(mods, pi_rk, modslot, T0);
+}
+void* stream_create() {
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+    return s;
+}
+void stream_destroy(void* s) {
+    if (s) cudaStreamDestroy(S(s));
+}
+void* event_create() {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+    return e;
+}
+void event_destroy(void* e) {
+    if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+}
+void event_record(void* e, void* st) { ck(cudaEventRecord(static_cast<cudaEvent_t>(e), S(st)), "event record"); }
+void stream_wait(void* st, void* e) {
+    ck(cudaStreamWaitEvent(S(st), static_cast<cudaEvent_t>(e), 0), "stream wait");
 }
 void prof_enable(int on) { prof().on = on; }
 void prof_reset() {
@@ -369,11 +396,10 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     dev::check();
 }
 
-void launch_private(const PrivParams& P, void* st) {
+void launch_private(const PrivParams& P, void* st, const Sched& q) {
     if (P.B == 0 || P.M == 0) return;
     ProfScope ps(P.garbler ? K_PRIV_GARBLE : K_PRIV_EVAL, S(st));
-    static uint32_t* counter = nullptr;
-    if (!counter) ck(cudaMalloc(&counter, sizeof(uint32_t)), "counter");
+    uint32_t* counter = q.counter + 1;
     ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
     int sms = 0, dev = 0;
     ck(cudaGetDevice(&dev), "dev");

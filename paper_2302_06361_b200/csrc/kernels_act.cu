@@ -114,23 +114,6 @@ void upload_act(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot
     ck(cudaMemcpyToSymbol(g_T0, T0, sizeof(uint32_t) * 256), "g_T0(act)");
 }
 
-static uint32_t* act_counter() {
-    static uint32_t* counter = nullptr;
-    if (!counter) ck(cudaMalloc(&counter, 64 * sizeof(uint32_t)), "counter");
-    return counter;
-}
-
-static uint32_t* act_flags(size_t n) {
-    static uint32_t* flags = nullptr;
-    static size_t cap = 0;
-    if (n > cap) {
-        if (flags) cudaFree(flags);
-        cap = std::max<size_t>(n, 1 << 16);
-        ck(cudaMalloc(&flags, cap * sizeof(uint32_t)), "flags");
-    }
-    return flags;
-}
-
 static int sm_count() {
     static int sms = 0;
     if (!sms) {
@@ -141,7 +124,8 @@ static int sm_count() {
     return sms;
 }
 
-void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* st) {
+void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* st,
+                      const Sched& q) {
     if (n > MAXACT) throw std::runtime_error("too many activation layers for one launch");
     ItemMap map;
     std::memset(&map, 0, sizeof map);
@@ -157,7 +141,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), map.base[n]);
     const int warps = garble ? kActWarpsGarble : kActWarpsEval;
     const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)warps * kBufWords;
-    uint32_t* counter = act_counter();
+    uint32_t* counter = q.counter;
     ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
     // garbling: chunked tapes (host_layers[].chunk_op); evaluation: whole tapes
     uint32_t nchunks = 1;
@@ -169,8 +153,11 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
                     break;
                 }
     }
-    uint32_t* flags = act_flags(map.base[n]);
-    if (nchunks > 1) ck(cudaMemsetAsync(flags, 0, sizeof(uint32_t) * map.base[n], S(st)), "flags reset");
+    uint32_t* flags = q.flags;
+    if (nchunks > 1) {
+        if (q.flags_cap < map.base[n]) throw std::runtime_error("work-queue flags too small");
+        ck(cudaMemsetAsync(flags, 0, sizeof(uint32_t) * map.base[n], S(st)), "flags reset");
+    }
     if (garble) {
         ck(cudaFuncSetAttribute(act_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
         act_kernel<true><<<grid, warps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, nchunks);

@@ -26,6 +26,13 @@ void sync(void* stream);
 void check();  // raise on a pending device error
 size_t free_bytes();
 void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot, const uint32_t* T0);
+// streams / events (pipelined inference runs two networks on two streams)
+void* stream_create();
+void stream_destroy(void* s);
+void* event_create();
+void event_destroy(void* e);
+void event_record(void* e, void* stream);
+void stream_wait(void* stream, void* e);
 
 // per-kernel-kind event timing on the launching stream (bench roofline)
 void prof_enable(int on);
@@ -47,9 +54,18 @@ enum KernelKind {
     K_NKINDS = 9
 };
 
+// Work-queue state of the persistent kernels (one per stream that launches
+// them concurrently): item counter + per-item chunk flags.
+struct Sched {
+    uint32_t* counter = nullptr;  // >= 2 words: [0] activation, [1] private kernel
+    uint32_t* flags = nullptr;
+    size_t flags_cap = 0;         // words
+};
+
 // Activation tapes of n layers in one persistent launch (dev_layers: the same
 // ActParams array in device memory).
-void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* stream);
+void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* stream,
+                      const Sched& q);
 // Garbler-side output labels of an activation layer (pure PRF functions).
 void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* stream);
 // Tensor-core form of one public linear layer (tc_linear.cuh): the expanded
@@ -65,7 +81,7 @@ struct TcLinear {
 void make_weight_map(TcLinear& t);  // encodes t.tmap for t.wexp
 // all lanes of a public linear layer in one launch
 void launch_linear(const LinParams* Ls, int n, const TcLinear& tc, void* stream);
-void launch_private(const PrivParams& P, void* stream);
+void launch_private(const PrivParams& P, void* stream, const Sched& q);
 void launch_pad_add(const PadAddParams& P, void* stream);  // extension layers
 void launch_setup(const SetupParams& S, void* stream);
 void launch_encode(const EncodeParams& P, void* stream);

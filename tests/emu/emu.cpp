@@ -53,6 +53,12 @@ void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* m
         g_T[i] = (i & 32) ? ((v << 16) | (v >> 16)) : v;
     }
 }
+void* stream_create() { return nullptr; }
+void stream_destroy(void*) {}
+void* event_create() { return nullptr; }
+void event_destroy(void*) {}
+void event_record(void*, void*) {}
+void stream_wait(void*, void*) {}
 void prof_enable(int) {}
 void prof_reset() {}
 int prof_read(double*, uint64_t*, int) { return 0; }
@@ -77,7 +83,8 @@ static void act_layer(const ActParams& P, bool garble) {
         }
 }
 
-void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void*) {
+void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void*,
+                      const Sched&) {
     (void)host_layers;
     for (int i = 0; i < n; ++i) act_layer(dev_layers[i], garble);
 }
@@ -113,7 +120,7 @@ void launch_pad_add(const PadAddParams& P, void*) {
             for (uint32_t u = 0; u < P.E_out; ++u) pad_add_thread(P, (uint32_t)b, (uint32_t)wi, u);
 }
 
-void launch_private(const PrivParams& P, void*) {
+void launch_private(const PrivParams& P, void*, const Sched&) {
 #pragma omp parallel for collapse(2)
     for (int64_t b = 0; b < (int64_t)P.B; ++b)
         for (int64_t u = 0; u < (int64_t)P.M; ++u) private_thread(P, (uint32_t)b, (uint32_t)u, tab());

@@ -403,3 +403,17 @@ def test_resnet20_shape_and_cost():
     assert s[0] == [3, 32, 32] and s[-1] == [10]
     relu = sum(int(np.prod(s[j + 1])) for j, l in enumerate(c.layers) if l.kind == 3)
     assert relu == 188_416  # 188,416 ReLU per inference
+
+
+def test_infer_batch19_matches_stepwise(eng):
+    # a larger batch through the fused call (decode finished from pinned residues)
+    g = eng.model("model_tiny", 1000, 8)
+    B = 19
+    seeds = b"".join(seed_hex(0x7A000 + b) for b in range(B))
+    x = np.stack([g.random_input(500 + b) for b in range(B)])
+    out, t = eng.infer(g, seeds, x)
+    assert t.sub_batches >= 1
+    net = eng.garble(g, seeds)
+    ref = eng.decode_outputs(net, eng.evaluate(net, eng.garble_inputs(net, x)))
+    assert (out == ref).all()
+    assert all(out[b].tolist() == g.plain_forward(x[b]).tolist() for b in range(B))
