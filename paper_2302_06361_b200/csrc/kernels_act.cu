@@ -16,6 +16,7 @@ __device__ uint32_t g_T0[256];
 #include <cstring>
 
 #include "kernels_common.cuh"
+#include "wpe.cuh"
 
 namespace dashgpu {
 
@@ -89,6 +90,50 @@ __global__ void __launch_bounds__((G ? kActWarpsGarble : kActWarpsEval) * 32, 1)
     }
 }
 
+// Small garbling launches (few elements in total): one warp per element
+// (wpe.cuh), every activation layer in one persistent launch.
+constexpr int kWpeWarps = 16;
+constexpr uint64_t kWpeMaxElements = 8192;
+
+__global__ void __launch_bounds__(kWpeWarps * 32, 1)
+    act_wpe_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
+    fill_T(g_T0);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* wb = s_dyn + kTabWords + warp * kWpeWords;
+    WpeBufs w;
+    w.X = LB{wb, 1};
+    w.A = LB{wb + NWMAX, 1};
+    w.K = LB{wb + 2 * NWMAX, 1};
+    w.KEY = LB{wb + kWpeShared + lane, 32};
+    Elt e;
+    e.X = w.X;
+    e.K = w.K;
+    e.A = w.A;
+    e.t = make_tab(nullptr, lane);
+    const uint32_t total = map.base[map.n];
+    uint32_t item = warp * gridDim.x + blockIdx.x;
+    const uint32_t first = kWpeWarps * gridDim.x;
+    while (item < total) {
+        uint32_t li = 0;
+        while (li + 1 < map.n && item >= map.base[li + 1]) ++li;
+        const ActParams& P = layers[li];
+        const uint32_t local = item - map.base[li];
+        e.b = local / P.E;
+        e.u = local - e.b * P.E;
+        e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
+        e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
+        e.rows = P.blob + (uint64_t)e.b * P.blob_stride + (uint64_t)e.u * P.uc_cts;
+        e.sstride = (uint64_t)P.B * P.E;
+        e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
+        e.rk = P.rk + (uint64_t)e.b * 44;
+        e.mult = P.mult + (uint64_t)e.b * P.mult_stride;
+        for (int i = 0; i < P.n_ops; ++i) garble_op_w(P, e, P.tape[i], w, lane);
+        uint32_t next = 0;
+        if (lane == 0) next = first + atomicAdd(counter, 1u);
+        item = __shfl_sync(0xffffffffu, next, 0);
+    }
+}
+
 // All k lanes of one layer in one launch: thread (lane i, element u) of
 // inference blockIdx.y; elements are padded to whole warps per lane so the
 // modulus is warp-uniform.
@@ -136,6 +181,24 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     }
     if (map.base[n] == 0) return;
     ProfScope ps(garble ? K_ACT_GARBLE : K_ACT_EVAL, S(st));
+    uint64_t elements = 0;
+    for (int i = 0; i < n; ++i) elements += (uint64_t)host_layers[i].B * host_layers[i].E;
+    if (garble && elements <= kWpeMaxElements) {
+        ItemMap wm;
+        std::memset(&wm, 0, sizeof wm);
+        wm.n = (uint32_t)n;
+        for (int i = 0; i < n; ++i) {
+            wm.wpi[i] = host_layers[i].E;
+            wm.base[i + 1] = wm.base[i] + host_layers[i].B * host_layers[i].E;
+        }
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), cdiv(elements, kWpeWarps));
+        const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeWarps * kWpeWords;
+        ck(cudaMemsetAsync(q.counter, 0, sizeof(uint32_t), S(st)), "counter reset");
+        ck(cudaFuncSetAttribute(act_wpe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        act_wpe_kernel<<<grid, kWpeWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter);
+        ck(cudaGetLastError(), "act wpe launch");
+        return;
+    }
     // one CTA per SM (the first round strides items across SMs), never fewer
     // CTAs than needed to give every item its own SM when items < #SMs
     const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), map.base[n]);
