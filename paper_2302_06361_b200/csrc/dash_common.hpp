@@ -70,8 +70,8 @@ enum OpKind : uint8_t {
     OP_OUTPUT = 7,   // element result for lane `cst`
 };
 
-// Operand encoding: < 64 -> slot index; >= 64 -> input lane (v - 64).
-constexpr uint8_t IN_LANE = 64;
+// Operand encoding: < 240 -> slot index; >= 240 -> input lane (v - 240).
+constexpr uint8_t IN_LANE = 240;
 
 struct TapeOp {
     uint8_t kind;

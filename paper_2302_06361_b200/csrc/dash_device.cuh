@@ -669,6 +669,12 @@ constexpr int MAXCHUNK = 8;  // tape chunks per element in the garbling launch
 struct ActParams {
     const TapeOp* tape;
     int n_ops;
+    // level-scheduled evaluation tape (warp-per-element evaluation of small
+    // launches): ops of level L are lv_tape[lv_start[L] .. lv_start[L+1]),
+    // mutually independent, slots never reused inside a level
+    const TapeOp* lv_tape;
+    const uint16_t* lv_start;
+    int n_levels;
     // op boundaries of the tape chunks (garbling launch: chunk c of every
     // element is a separate work item, run after chunk c-1 of that element)
     uint16_t chunk_op[MAXCHUNK + 1];

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <tuple>
 #include <functional>
 #include <map>
 #include <memory>
@@ -433,6 +434,10 @@ struct Tape {
     std::set<int> moduli;
     uint8_t out_kind[MAXK] = {};   // gadget producing output lane i (OP_MMHALF / OP_PROJ)
     uint32_t out_wire[MAXK] = {};  // its first fresh wire offset
+    // level-scheduled copy for warp-per-element evaluation (see ActParams)
+    std::vector<TapeOp> lv_ops;
+    std::vector<uint16_t> lv_start;
+    int nslots_lv = 0;
 };
 
 // Records the gadget DAG in reference order (CountCtx semantics,
@@ -722,6 +727,70 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
     }
     if (nslots > MAXSLOTS) throw DataError("activation gadget needs too many label slots");
     tp.nslots = nslots;
+    {
+        // Level schedule of the same DAG for warp-per-element evaluation:
+        // level(op) = 1 + max level of its operands' producers; ops of a level
+        // are independent and run on different lanes.  Slots are allocated per
+        // level and freed only after the level of a value's last reader, so
+        // no op of a level overwrites a slot another op of that level reads.
+        std::vector<int> lvl(nops, 0), vlevel(r.vmod.size(), -1), lastlv(r.vmod.size(), -1);
+        int nl = 0;
+        for (int t : order) {
+            const auto& o = r.ops[t];
+            int L = 0;
+            for (int v : {o.a, o.b})
+                if (v >= b.k) L = std::max(L, vlevel[v] + 1);
+            lvl[t] = L;
+            if (o.out >= 0) vlevel[o.out] = L;
+            nl = std::max(nl, L + 1);
+        }
+        for (int t : order)
+            for (int v : {r.ops[t].a, r.ops[t].b})
+                if (v >= b.k) lastlv[v] = std::max(lastlv[v], lvl[t]);
+        std::vector<std::vector<int>> bylv(nl);
+        for (int t : order) bylv[lvl[t]].push_back(t);
+        std::vector<int> lslot(r.vmod.size(), -1), lfree;
+        int lns = 0;
+        for (int L = 0; L < nl; ++L) {
+            auto& ops = bylv[L];
+            std::stable_sort(ops.begin(), ops.end(), [&](int x, int y) {  // similar gadgets on adjacent lanes
+                const auto &ox = r.ops[x], &oy = r.ops[y];
+                return std::make_tuple(ox.kind, ox.pm, ox.qm) < std::make_tuple(oy.kind, oy.pm, oy.qm);
+            });
+            tp.lv_start.push_back((uint16_t)tp.lv_ops.size());
+            for (int t : ops) {
+                const auto& o = r.ops[t];
+                TapeOp d = tp.ops[std::find(order.begin(), order.end(), t) - order.begin()];
+                auto enc = [&](int v) -> uint8_t {
+                    if (v < 0) return 0;
+                    if (v < b.k) return (uint8_t)(IN_LANE + v);
+                    return (uint8_t)lslot[v];
+                };
+                d.a = enc(o.a);
+                d.b = enc(o.b);
+                if (o.out >= 0) {
+                    int sidx;
+                    if (!lfree.empty()) {
+                        sidx = lfree.back();
+                        lfree.pop_back();
+                    } else {
+                        sidx = lns++;
+                    }
+                    lslot[o.out] = sidx;
+                    d.out = (uint8_t)sidx;
+                }
+                tp.lv_ops.push_back(d);
+            }
+            for (size_t v = b.k; v < r.vmod.size(); ++v)  // free values whose readers are all done
+                if (lslot[v] >= 0 && lastlv[v] <= L && vlevel[v] <= L) {
+                    lfree.push_back(lslot[v]);
+                    lslot[v] = -1;
+                }
+        }
+        tp.lv_start.push_back((uint16_t)tp.lv_ops.size());
+        if (lns >= IN_LANE) throw DataError("level schedule needs too many label slots");
+        tp.nslots_lv = lns;
+    }
     tp.phi = r.phi;
     if (tp.phi.empty()) tp.phi.push_back(0);
     for (const auto& o : r.ops)
@@ -782,6 +851,8 @@ struct HostBuf {
 };
 
 static void* g_stream = nullptr;
+// launches with at most this many elements run warp-per-element (kernels_act.cu)
+constexpr uint64_t kWpeMaxElementsHost = 8192;
 
 struct HLayer {
     int kind = 0;
@@ -806,7 +877,7 @@ struct HLayer {
     uint32_t K = 0;  // window
     // activation
     std::shared_ptr<Tape> tape;
-    std::shared_ptr<DevBuf> tape_d, phi_d;
+    std::shared_ptr<DevBuf> tape_d, phi_d, lv_tape_d, lv_start_d;
     bool linear() const { return kind == DASH_LAYER_DENSE || kind == DASH_LAYER_CONV2D; }
     uint64_t weight_count() const {
         if (kind == DASH_LAYER_DENSE) return (uint64_t)in_dim * out_dim;
@@ -1071,6 +1142,8 @@ static void upload_circuit(dashgpu_circuit& c) {
         if (l.tape) {
             l.tape_d = upload(l.tape->ops.data(), l.tape->ops.size() * sizeof(TapeOp));
             l.phi_d = upload(l.tape->phi.data(), l.tape->phi.size());
+            l.lv_tape_d = upload(l.tape->lv_ops.data(), l.tape->lv_ops.size() * sizeof(TapeOp));
+            l.lv_start_d = upload(l.tape->lv_start.data(), l.tape->lv_start.size() * sizeof(uint16_t));
         }
     }
     dev::sync(g_stream);
@@ -1289,6 +1362,9 @@ static void run_layer(Network& n, size_t li, const HLayer& l, bool garbler, cons
     std::memset(&P, 0, sizeof P);
     P.tape = l.tape_d->as<TapeOp>();
     P.n_ops = (int)l.tape->ops.size();
+    P.lv_tape = l.lv_tape_d->as<TapeOp>();
+    P.lv_start = l.lv_start_d->as<uint16_t>();
+    P.n_levels = (int)l.tape->lv_start.size() - 1;
     fill_chunks(P, *l.tape, tape_chunks());
     P.phi = l.phi_d->as<uint8_t>();
     P.k = k;
@@ -1356,13 +1432,16 @@ static void network_reserve(Network& n, uint32_t B) {
     n.resid.ensure((size_t)B * c.n_out * k);
     n.err.ensure(16);
     n.base.ensure(c.base, B, c.n_in);
-    size_t slot_total = 0, nact = 0;
+    size_t slot_total = 0, nact = 0, slot_eval = 0;
     for (const auto& l : c.layers)
         if (l.tape) {
             slot_total += (size_t)l.tape->nslots * B * l.E_out;
+            // warp-per-element evaluation of a small layer uses the level tape's slots
+            if ((uint64_t)B * l.E_out <= kWpeMaxElementsHost)
+                slot_eval = std::max(slot_eval, (size_t)l.tape->nslots_lv * B * l.E_out);
             ++nact;
         }
-    n.slots.ensure(std::max<size_t>(slot_total, 1) * 16);
+    n.slots.ensure(std::max<size_t>(std::max(slot_total, slot_eval), 1) * 16);
     n.nact = nact;
     n.act_cap = nact + c.layers.size();
     n.act_dev.ensure(n.act_cap * sizeof(ActParams));
@@ -1636,7 +1715,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
     w.Rb.ensure((size_t)k * LABW * 4);
     w.commit.ensure(16);
     w.blob.ensure((size_t)C * T.cts * 16);
-    w.slots.ensure(std::max<size_t>((size_t)T.nslots * C, 1) * 16);
+    w.slots.ensure(std::max<size_t>((size_t)std::max(T.nslots, T.nslots_lv) * C, 1) * 16);
     w.dec.ensure((size_t)C * sum_p * 16);
     w.vals.ensure((size_t)C * 8);
     w.resid.ensure((size_t)C * k);
@@ -1685,6 +1764,9 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             std::memset(&P, 0, sizeof P);
             P.tape = l.tape_d->as<TapeOp>();
             P.n_ops = (int)T.ops.size();
+            P.lv_tape = l.lv_tape_d->as<TapeOp>();
+            P.lv_start = l.lv_start_d->as<uint16_t>();
+            P.n_levels = (int)T.lv_start.size() - 1;
             fill_chunks(P, T, tape_chunks());
             P.phi = l.phi_d->as<uint8_t>();
             P.k = k;

@@ -134,6 +134,50 @@ __global__ void __launch_bounds__(kWpeWarps * 32, 1)
     }
 }
 
+// Small evaluation launches: one warp per element, the level-scheduled tape
+// (ActParams::lv_tape), lane t takes ops t, t+32, ... of every level.  Each
+// lane keeps its own X / K / A buffers (lane-interleaved, as act_kernel).
+constexpr int kWpeEvalWarps = 16;
+constexpr int kLaneWordsEval = 2 * NWMAX + 4;
+
+__global__ void __launch_bounds__(kWpeEvalWarps * 32, 1)
+    act_wpe_eval_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
+    fill_T(g_T0);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* lb = s_dyn + kTabWords + warp * kLaneWordsEval * 32 + lane;
+    Elt e;
+    e.X = LB{lb, 32};
+    e.K = LB{lb + NWMAX * 32, 32};
+    e.A = LB{lb + (NWMAX + 4) * 32, 32};
+    e.t = make_tab(nullptr, lane);
+    e.rk = nullptr;
+    e.mult = nullptr;
+    const uint32_t total = map.base[map.n];
+    uint32_t item = warp * gridDim.x + blockIdx.x;
+    const uint32_t first = kWpeEvalWarps * gridDim.x;
+    while (item < total) {
+        uint32_t li = 0;
+        while (li + 1 < map.n && item >= map.base[li + 1]) ++li;
+        const ActParams& P = layers[li];
+        const uint32_t local = item - map.base[li];
+        e.b = local / P.E;
+        e.u = local - e.b * P.E;
+        e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
+        e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
+        e.rows = P.blob + (uint64_t)e.b * P.blob_stride + (uint64_t)e.u * P.uc_cts;
+        e.sstride = (uint64_t)P.B * P.E;
+        e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
+        for (int L = 0; L < P.n_levels; ++L) {
+            const int end = P.lv_start[L + 1];
+            for (int i = P.lv_start[L] + (int)lane; i < end; i += 32) eval_op(P, e, P.lv_tape[i]);
+            __syncwarp();
+        }
+        uint32_t next = 0;
+        if (lane == 0) next = first + atomicAdd(counter, 1u);
+        item = __shfl_sync(0xffffffffu, next, 0);
+    }
+}
+
 // All k lanes of one layer in one launch: thread (lane i, element u) of
 // inference blockIdx.y; elements are padded to whole warps per lane so the
 // modulus is warp-uniform.
@@ -183,6 +227,23 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     ProfScope ps(garble ? K_ACT_GARBLE : K_ACT_EVAL, S(st));
     uint64_t elements = 0;
     for (int i = 0; i < n; ++i) elements += (uint64_t)host_layers[i].B * host_layers[i].E;
+    if (!garble && elements <= kWpeMaxElements) {
+        ItemMap wm;
+        std::memset(&wm, 0, sizeof wm);
+        wm.n = (uint32_t)n;
+        for (int i = 0; i < n; ++i) {
+            wm.wpi[i] = host_layers[i].E;
+            wm.base[i + 1] = wm.base[i] + host_layers[i].B * host_layers[i].E;
+        }
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), cdiv(elements, kWpeEvalWarps));
+        const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeEvalWarps * kLaneWordsEval * 32;
+        ck(cudaMemsetAsync(q.counter, 0, sizeof(uint32_t), S(st)), "counter reset");
+        ck(cudaFuncSetAttribute(act_wpe_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+           "attr");
+        act_wpe_eval_kernel<<<grid, kWpeEvalWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter);
+        ck(cudaGetLastError(), "act wpe eval launch");
+        return;
+    }
     if (garble && elements <= kWpeMaxElements) {
         ItemMap wm;
         std::memset(&wm, 0, sizeof wm);

@@ -78,8 +78,22 @@ static void act_layer(const ActParams& P, bool garble) {
             e.t = tab();
             e.rk = nullptr;
             e.mult = nullptr;
-            if (garble) act_element<true>(P, e, 0, P.n_ops);
-            else act_element<false>(P, e, 0, P.n_ops);
+            if (garble) {
+                act_element<true>(P, e, 0, P.n_ops);
+            } else if ((uint64_t)P.B * P.E <= 8192 && P.n_levels > 0) {
+                // small launches: the level-scheduled tape, as the CUDA
+                // warp-per-element evaluation runs it (levels in order;
+                // the ops of a level are independent)
+                e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
+                e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
+                e.rows = P.blob + (uint64_t)e.b * P.blob_stride + (uint64_t)e.u * P.uc_cts;
+                e.sstride = (uint64_t)P.B * P.E;
+                e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
+                for (int L = 0; L < P.n_levels; ++L)
+                    for (int i = P.lv_start[L + 1] - 1; i >= P.lv_start[L]; --i) eval_op(P, e, P.lv_tape[i]);
+            } else {
+                act_element<false>(P, e, 0, P.n_ops);
+            }
         }
 }
 
