@@ -235,7 +235,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
             wm.wpi[i] = host_layers[i].E;
             wm.base[i + 1] = wm.base[i] + host_layers[i].B * host_layers[i].E;
         }
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), cdiv(elements, kWpeEvalWarps));
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), elements);  // spread: latency-bound
         const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeEvalWarps * kLaneWordsEval * 32;
         ck(cudaMemsetAsync(q.counter, 0, sizeof(uint32_t), S(st)), "counter reset");
         ck(cudaFuncSetAttribute(act_wpe_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
@@ -252,7 +252,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
             wm.wpi[i] = host_layers[i].E;
             wm.base[i + 1] = wm.base[i] + host_layers[i].B * host_layers[i].E;
         }
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), cdiv(elements, kWpeWarps));
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), elements);  // spread: latency-bound
         const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeWarps * kWpeWords;
         ck(cudaMemsetAsync(q.counter, 0, sizeof(uint32_t), S(st)), "counter reset");
         ck(cudaFuncSetAttribute(act_wpe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
