@@ -179,8 +179,11 @@ struct SetupParams {
     U4* commit;                // [B]
 };
 
-DASH_HD void setup_offsets_thread(const SetupParams& S, uint32_t b, uint32_t si, const AesTab& t) {
+// One thread per (modulus slot, multiple x): R_m is drawn by every thread of
+// the slot (a few AES blocks), so the m multiples are written in parallel.
+DASH_HD void setup_offsets_thread(const SetupParams& S, uint32_t b, uint32_t si, uint32_t x, const AesTab& t) {
     const uint32_t m = S.slot_mod[si];
+    if (x >= m) return;
     const ModC& M = c_mod[m];
     uint32_t buf[2][NWMAX] = {};
     const LB R{buf[0], 1}, v{buf[1], 1};
@@ -189,12 +192,11 @@ DASH_HD void setup_offsets_thread(const SetupParams& S, uint32_t b, uint32_t si,
     if (M.pow2) R[0] = (R[0] & ~(M.m - 1u)) | 1u;
     else R[0] = (R[0] & ~0xffu) | 1u;
     uint32_t* base = S.mult + (uint64_t)b * S.mult_stride + (uint64_t)c_modslot[m] * 128 * NWMAX;
-    for (uint32_t x = 0; x < m; ++x) {
-        lb_scale(v, R, x, M);
-        for (int w = 0; w < NWMAX; ++w) base[(uint64_t)x * NWMAX + w] = v[w];
-    }
-    for (int i = 0; i < S.k; ++i)
-        if (S.primes[i] == m) lb_store_rows(R, S.Rb + ((uint64_t)b * S.k + i) * LABW, 1, M);
+    lb_scale(v, R, x, M);
+    for (int w = 0; w < NWMAX; ++w) base[(uint64_t)x * NWMAX + w] = v[w];
+    if (x == 1)
+        for (int i = 0; i < S.k; ++i)
+            if (S.primes[i] == m) lb_store_rows(R, S.Rb + ((uint64_t)b * S.k + i) * LABW, 1, M);
 }
 
 DASH_HD void setup_labels_thread(const SetupParams& S, uint32_t b, uint32_t e, int i, const AesTab& t) {

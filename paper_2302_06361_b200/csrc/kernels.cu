@@ -181,9 +181,8 @@ __global__ void __launch_bounds__(128) pad_add_kernel(const __grid_constant__ Pa
 
 __global__ void __launch_bounds__(128) setup_offsets_kernel(SetupParams Sp) {
     fill_T(g_T0);
-    const uint32_t si = blockIdx.x * blockDim.x + threadIdx.x;
-    if (si >= Sp.nslot) return;
-    setup_offsets_thread(Sp, blockIdx.y, si, make_tab(nullptr, threadIdx.x & 31u));
+    const uint32_t si = blockIdx.x;  // modulus slot; thread = multiple x < 128
+    setup_offsets_thread(Sp, blockIdx.y, si, threadIdx.x, make_tab(nullptr, threadIdx.x & 31u));
 }
 
 __global__ void __launch_bounds__(128) setup_labels_kernel(SetupParams Sp) {
@@ -426,7 +425,7 @@ void launch_pad_add(const PadAddParams& P, void* st) {
 void launch_setup(const SetupParams& Sp, void* st) {
     ProfScope ps(K_SETUP, S(st));
     ck(cudaFuncSetAttribute(setup_offsets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
-    setup_offsets_kernel<<<dim3(cdiv(Sp.nslot, 128), Sp.B), 128, kTabBytes, S(st)>>>(Sp);
+    setup_offsets_kernel<<<dim3(Sp.nslot, Sp.B), 128, kTabBytes, S(st)>>>(Sp);
     dev::check();
     ck(cudaFuncSetAttribute(setup_labels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
     setup_labels_kernel<<<dim3(cdiv(Sp.n_in + 1, 128), Sp.k, Sp.B), 128, kTabBytes, S(st)>>>(Sp);

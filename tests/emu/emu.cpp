@@ -142,7 +142,8 @@ void launch_private(const PrivParams& P, void*, const Sched&) {
 
 void launch_setup(const SetupParams& S, void*) {
     for (uint32_t b = 0; b < S.B; ++b)
-        for (uint32_t si = 0; si < S.nslot; ++si) setup_offsets_thread(S, b, si, tab());
+        for (uint32_t si = 0; si < S.nslot; ++si)
+            for (uint32_t x = 0; x < 128; ++x) setup_offsets_thread(S, b, si, x, tab());
 #pragma omp parallel for collapse(2)
     for (int64_t b = 0; b < (int64_t)S.B; ++b)
         for (int64_t e = 0; e <= (int64_t)S.n_in; ++e)
