@@ -107,6 +107,48 @@ int dashgpu_evaluate(dashgpu_network* n, const dashgpu_bundle* in, dashgpu_bundl
 int dashgpu_decode_outputs(dashgpu_network* n, const dashgpu_bundle* out, int64_t* values);
 void dashgpu_bundle_destroy(dashgpu_bundle* b);
 
+/* ---- layer level (reference layer.hpp:79-97) ----
+ * dashgpu_network_setup: the garbling environment of garble() without any
+ * layer (offsets R_m and their multiples, zero-wire and input base labels,
+ * seed commitment; garble.cpp:134-204).  dashgpu_input_base: the input base
+ * labels (EncodingInfo::input_labels).  dashgpu_layer_garble = garble_layer
+ * (layer.hpp:85-90): base labels of layer li's input (in2: second operand of
+ * the Add extension, else NULL) -> base labels of its output; the layer's
+ * rows land at layer_ct_base[li] of every inference's GC.
+ * dashgpu_layer_eval = eval_layer (layer.hpp:93-97) on active labels.
+ * dashgpu_network_finish: decoding tables from the final base labels, after
+ * which the network equals the one dashgpu_garble builds.
+ * dashgpu_layer_count = count_layer (layer.hpp:79-80): cts, gates, wires. */
+int dashgpu_network_setup(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
+                          dashgpu_network** out);
+int dashgpu_input_base(dashgpu_network* n, dashgpu_bundle** out);
+int dashgpu_layer_garble(dashgpu_network* n, uint32_t layer, const dashgpu_bundle* in,
+                         const dashgpu_bundle* in2, dashgpu_bundle** out);
+int dashgpu_layer_eval(dashgpu_network* n, uint32_t layer, const dashgpu_bundle* in,
+                       const dashgpu_bundle* in2, dashgpu_bundle** out);
+int dashgpu_network_finish(dashgpu_network* n, const dashgpu_bundle* final_base);
+int dashgpu_layer_count(const dashgpu_circuit* c, uint32_t layer, uint64_t* cts_gates_wires3);
+
+/* ---- t_proj primitive (gadgets.hpp:146-176) over n independent gates ----
+ * garble: seed = the PRF seed (offsets R_p, R_q and the fresh out0 labels,
+ * prf.cpp:11-32); in: n compressed base labels mod p (u128 as 2 x u64 LE);
+ * phi: p table values mod q; gates / wires: gate ids and fresh wire ids;
+ * rows: [n][p] u128 (row (color + a) mod p = Enc_{in + aR_p}(out0 + phi(a) R_q));
+ * out0: [n] compressed fresh labels mod q; offsets (may be NULL): R_p, R_q.
+ * eval: active labels in + rows -> active out labels (compressed). */
+int dashgpu_proj_garble(const uint8_t* seed16, uint32_t n, int p, int q, const uint8_t* phi,
+                        const uint64_t* in, const uint64_t* gates, const uint64_t* wires,
+                        uint64_t* rows, uint64_t* out0, uint64_t* offsets);
+int dashgpu_proj_eval(uint32_t n, int p, int q, const uint64_t* in, const uint64_t* gates,
+                      const uint64_t* rows, uint64_t* out);
+
+/* ---- LabelTensor images (label_tensor.hpp:14-42: per lane, label-major
+ * u16 digits [batch][elements][n_p]) <-> device bundles (u8 SoA planes) ---- */
+int dashgpu_bundle_info(const dashgpu_bundle* b, uint32_t* batch, uint64_t* elements);
+int dashgpu_bundle_from_labels(dashgpu_network* n, uint64_t elements, const uint16_t* const* lanes,
+                               int output, dashgpu_bundle** out);
+int dashgpu_bundle_labels(const dashgpu_bundle* b, int lane, uint16_t* out);
+
 /* ---- reference wire formats (byte-identical to the reference) ---- */
 int dashgpu_export_gc(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len);
 int dashgpu_export_encoding(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len);

@@ -363,6 +363,39 @@ DASH_HD void pad_add_thread(const PadAddParams& P, uint32_t b, uint32_t wi, uint
                 : P.zero[((uint64_t)b * P.k + i) * LABW + w];
 }
 
+// ---------------------------------------------------------------------------
+// t_proj primitive (gadgets.hpp:146-176) over n independent gates, one thread
+// per gate: garbler rows [n][p] + fresh out0, or evaluator output labels.
+struct ProjParams {
+    uint32_t n, p, q;
+    const uint8_t* phi;      // [p] values mod q
+    const U4* in;            // [n] compressed labels mod p (garbler: base, evaluator: active)
+    const uint64_t* gates;   // [n] gate ids (tweak g)
+    const uint64_t* wires;   // [n] fresh output wire ids (garbler)
+    U4* rows;                // [n][p]
+    U4* out;                 // [n] compressed labels mod q (garbler: out0, evaluator: active)
+    const uint32_t* rk;      // [44] PRF key schedule
+    const uint32_t* mult;    // multiples table of the PRF's offsets
+    int garbler;
+};
+
+DASH_HD void proj_thread(const ProjParams& P, uint32_t i, const AesTab& t) {
+    const ModC& Mp = c_mod[P.p];
+    const ModC& Mq = c_mod[P.q];
+    uint32_t buf[2][NWMAX] = {};
+    const LB X{buf[0], 1}, A{buf[1], 1};
+    lb_decompress(X, P.in[i], Mp);
+    const uint32_t c = lb_color(X, Mp);
+    U4* R = P.rows + (uint64_t)i * P.p;
+    if (P.garbler) {
+        lb_prf(A, P.wires[i], 0, Mq, P.rk, t);
+        garble_rows_n(X, A, t, P.mult, P.p, P.q, c, P.gates[i], P.phi, 0, R, 0);
+    } else {
+        lb_dec(A, R[c], hash_tw(lb_compress(X, Mp), P.gates[i], c, 0, t), Mq);
+    }
+    P.out[i] = lb_compress(A, Mq);
+}
+
 // compress every label of a lane plane: out[b][e] (bundle payload / tensor_write)
 struct CompressParams {
     uint32_t B, n;

@@ -1480,8 +1480,10 @@ static const Lanes* run_layers(Network& n, bool garbler, const Lanes& input) {
     return O.at[L];
 }
 
-// garble (garble.cpp:134-240), batched: inference b uses seeds[b]
-static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
+// garble (garble.cpp:134-240), batched: inference b uses seeds[b].
+// garble_setup: offsets, multiples, zero-wire / input base labels, seed
+// commitment (garble.cpp:134-204 before the layer loop).
+static void garble_setup(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
     upload_circuit(c);
@@ -1519,34 +1521,47 @@ static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds
     S.Rb = n.Rb.as<uint32_t>();
     S.commit = n.commit.as<U4>();
     launch_setup(S, g_stream);
-    // run the layers on the input base planes
     n.act_host.clear();
     n.slot_used = 0;
-    const Lanes* cur = run_layers(n, true, n.base);
-    if (!n.act_host.empty()) {
-        std::memcpy(n.act_pin.p, n.act_host.data(), n.act_host.size() * sizeof(ActParams));
-        dev::h2d(n.act_dev.p, n.act_pin.p, n.act_host.size() * sizeof(ActParams), g_stream);
-        launch_act_multi(n.act_dev.as<ActParams>(), n.act_host.data(), (int)n.act_host.size(), true, g_stream,
-                         n.sched());
-    }
-    // decoding tables from the final base labels
+}
+
+// decoding tables (garble.cpp:208-231) from the final output base labels
+static void garble_dectables(Network& n, const Lanes& fin) {
+    dashgpu_circuit& c = *n.c;
+    const int k = c.k;
     DecodeParams D;
     std::memset(&D, 0, sizeof D);
-    D.B = B;
+    D.B = n.B;
     D.n_out = (uint32_t)c.n_out;
     D.k = k;
     fill_primes(c.base, D.primes);
     D.poff[0] = 0;
     for (int i = 0; i < k; ++i) D.poff[i + 1] = (uint16_t)(D.poff[i] + c.base.primes[i]);
-    make_lane_ptrs(*cur, k, D.lanes);
+    make_lane_ptrs(fin, k, D.lanes);
     D.table = n.dec.as<U4>();
     D.mult = n.mult.as<uint32_t>();
     D.mult_stride = n.mult_stride;
     launch_dectable(D, g_stream);
 }
 
-// garble_inputs, enqueued on the network's stream; the range check result
-// lands in err_pin[0] (encode_finish reads it after the stream is synced)
+// the deferred combined garbling launch of the activation layers recorded in act_host
+static void garble_act_flush(Network& n) {
+    if (n.act_host.empty()) return;
+    std::memcpy(n.act_pin.p, n.act_host.data(), n.act_host.size() * sizeof(ActParams));
+    dev::h2d(n.act_dev.p, n.act_pin.p, n.act_host.size() * sizeof(ActParams), g_stream);
+    launch_act_multi(n.act_dev.as<ActParams>(), n.act_host.data(), (int)n.act_host.size(), true, g_stream, n.sched());
+    n.act_host.clear();
+    n.slot_used = 0;
+}
+
+static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
+    garble_setup(n, seeds, B, seeds_on_device);
+    // run the layers on the input base planes
+    const Lanes* cur = run_layers(n, true, n.base);
+    garble_act_flush(n);
+    garble_dectables(n, *cur);
+}
+
 static void encode_enqueue(Network& n, const int64_t* values, bool on_device, Bundle& out) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
@@ -2470,6 +2485,143 @@ int dashgpu_garble(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batc
 
 void dashgpu_network_destroy(dashgpu_network* n) { delete n; }
 
+// ---- layer level (layer.hpp:79-97) ----
+int dashgpu_network_setup(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch, dashgpu_network** out) {
+    return guarded([&] {
+        if (batch == 0) throw DataError("empty batch");
+        auto n = std::make_unique<dashgpu_network>();
+        n->net = std::make_unique<Network>();
+        n->net->c = const_cast<dashgpu_circuit*>(c);
+        garble_setup(*n->net, seeds, batch, false);
+        dev::sync(g_stream);
+        *out = n.release();
+    });
+}
+
+static std::unique_ptr<dashgpu_bundle> new_bundle(Network& N, uint64_t E, bool output) {
+    auto bd = std::make_unique<dashgpu_bundle>();
+    bd->b = std::make_unique<Bundle>();
+    bd->b->net = &N;
+    bd->b->B = N.B;
+    bd->b->output = output;
+    bd->b->lanes.ensure(N.c->base, N.B, E);
+    return bd;
+}
+
+static void copy_lanes(const Network& N, const Lanes& from, Lanes& to, uint64_t E) {
+    for (int i = 0; i < N.c->k; ++i)
+        dev::d2d(to.lane[i]->p, from.lane[i]->p,
+                 (size_t)N.B * ((n_digits_host(N.c->base.primes[i]) + 3) / 4) * E * 4, g_stream);
+}
+
+int dashgpu_input_base(dashgpu_network* n, dashgpu_bundle** out) {
+    return guarded([&] {
+        Network& N = *n->net;
+        auto bd = new_bundle(N, N.c->n_in, false);
+        copy_lanes(N, N.base, bd->b->lanes, N.c->n_in);
+        dev::sync(g_stream);
+        *out = bd.release();
+    });
+}
+
+static void layer_pass(dashgpu_network* n, uint32_t li, const dashgpu_bundle* in, const dashgpu_bundle* in2,
+                       dashgpu_bundle** out, bool garbler) {
+    Network& N = *n->net;
+    dashgpu_circuit& c = *N.c;
+    if (li >= c.layers.size()) throw DataError("layer index out of range");
+    const HLayer& l = c.layers[li];
+    if (!in || in->b->B != N.B || in->b->lanes.E != l.E_in) throw DataError("layer input shape mismatch");
+    if (l.kind == DASH_LAYER_ADD && (!in2 || in2->b->B != N.B || in2->b->lanes.E != l.E_out))
+        throw DataError("add layer needs a second operand of the output shape");
+    auto bd = new_bundle(N, l.E_out, li + 1 == c.layers.size());
+    if (l.kind == DASH_LAYER_FLATTEN) {
+        copy_lanes(N, in->b->lanes, bd->b->lanes, l.E_out);
+    } else {
+        run_layer(N, li, l, garbler, in->b->lanes, in2 ? &in2->b->lanes : nullptr, bd->b->lanes);
+        if (garbler) garble_act_flush(N);
+    }
+    dev::sync(g_stream);
+    *out = bd.release();
+}
+
+int dashgpu_layer_garble(dashgpu_network* n, uint32_t li, const dashgpu_bundle* in, const dashgpu_bundle* in2,
+                         dashgpu_bundle** out) {
+    return guarded([&] { layer_pass(n, li, in, in2, out, true); });
+}
+
+int dashgpu_layer_eval(dashgpu_network* n, uint32_t li, const dashgpu_bundle* in, const dashgpu_bundle* in2,
+                       dashgpu_bundle** out) {
+    return guarded([&] { layer_pass(n, li, in, in2, out, false); });
+}
+
+int dashgpu_network_finish(dashgpu_network* n, const dashgpu_bundle* fin) {
+    return guarded([&] {
+        Network& N = *n->net;
+        if (!fin || fin->b->B != N.B || fin->b->lanes.E != N.c->n_out) throw DataError("output shape mismatch");
+        garble_dectables(N, fin->b->lanes);
+        dev::sync(g_stream);
+    });
+}
+
+int dashgpu_layer_count(const dashgpu_circuit* c, uint32_t li, uint64_t* cts_gates_wires) {
+    return guarded([&] {
+        if (li >= c->layers.size()) throw DataError("layer index out of range");
+        const HLayer& l = c->layers[li];
+        cts_gates_wires[0] = l.cts;
+        cts_gates_wires[1] = l.gates;
+        cts_gates_wires[2] = l.wires;
+    });
+}
+
+// ---- LabelTensor upload / download (label_tensor.hpp:14-42: label-major u16 digits) ----
+int dashgpu_bundle_info(const dashgpu_bundle* b, uint32_t* batch, uint64_t* elements) {
+    return guarded([&] {
+        *batch = b->b->B;
+        *elements = b->b->lanes.E;
+    });
+}
+
+int dashgpu_bundle_from_labels(dashgpu_network* n, uint64_t elements, const uint16_t* const* lanes, int output,
+                               dashgpu_bundle** out) {
+    return guarded([&] {
+        Network& N = *n->net;
+        const dashgpu_circuit& c = *N.c;
+        auto bd = new_bundle(N, elements, output != 0);
+        for (int i = 0; i < c.k; ++i) {
+            const int p = c.base.primes[i], nd = n_digits_host(p), nw = (nd + 3) / 4;
+            std::vector<uint32_t> w((size_t)N.B * nw * elements, 0);
+            for (uint32_t b = 0; b < N.B; ++b)
+                for (uint64_t e = 0; e < elements; ++e)
+                    for (int d = 0; d < nd; ++d) {
+                        const uint16_t v = lanes[i][((uint64_t)b * elements + e) * nd + d];
+                        if (v >= p) throw DataError("label digit out of range");
+                        w[((uint64_t)b * nw + d / 4) * elements + e] |= (uint32_t)v << (8 * (d % 4));
+                    }
+            dev::h2d(bd->b->lanes.lane[i]->p, w.data(), w.size() * 4, g_stream);
+            dev::sync(g_stream);
+        }
+        *out = bd.release();
+    });
+}
+
+int dashgpu_bundle_labels(const dashgpu_bundle* bd, int lane, uint16_t* out) {
+    return guarded([&] {
+        const Bundle& B = *bd->b;
+        const dashgpu_circuit& c = *B.net->c;
+        if (lane < 0 || lane >= c.k) throw DataError("lane out of range");
+        const int p = c.base.primes[lane], nd = n_digits_host(p), nw = (nd + 3) / 4;
+        const uint64_t E = B.lanes.E;
+        std::vector<uint32_t> w((size_t)B.B * nw * E);
+        dev::d2h(w.data(), B.lanes.lane[lane]->p, w.size() * 4, g_stream);
+        dev::sync(g_stream);
+        for (uint32_t b = 0; b < B.B; ++b)
+            for (uint64_t e = 0; e < E; ++e)
+                for (int d = 0; d < nd; ++d)
+                    out[((uint64_t)b * E + e) * nd + d] =
+                        (uint16_t)((w[((uint64_t)b * nw + d / 4) * E + e] >> (8 * (d % 4))) & 0xffu);
+    });
+}
+
 int dashgpu_garble_inputs(dashgpu_network* n, const int64_t* values, dashgpu_bundle** out) {
     return guarded([&] {
         auto b = std::make_unique<dashgpu_bundle>();
@@ -2704,6 +2856,124 @@ int dashgpu_prim(int op, uint32_t n, int m, int q, const uint64_t* in, uint64_t*
         dev::sync(g_stream);
         if (digits)
             for (size_t i = 0; i < (size_t)n * 128; ++i) digits[i] = (uint16_t)((dg[i / 4] >> (8 * (i % 4))) & 0xff);
+    });
+}
+
+// ---- t_proj primitive (gadgets.hpp:146-176) ----
+static void proj_setup(const uint8_t* seed16, int p, int q, DevBuf& rk, DevBuf& mult, DevBuf& scratch) {
+    uint32_t k44[44];
+    aes_expand_host(seed16, k44);
+    rk.ensure(sizeof k44);
+    dev::h2d(rk.p, k44, sizeof k44, g_stream);
+    const uint64_t mult_stride = (uint64_t)(MAXMOD - 1) * 128 * NWMAX;
+    mult.ensure(mult_stride * 4);
+    scratch.ensure(4096);
+    SetupParams S;
+    std::memset(&S, 0, sizeof S);
+    S.B = 1;
+    S.k = 1;
+    S.primes[0] = (uint16_t)p;
+    S.slot_mod[S.nslot++] = (uint16_t)p;
+    if (q != p) S.slot_mod[S.nslot++] = (uint16_t)q;
+    S.rk = rk.as<uint32_t>();
+    S.seeds = scratch.as<uint8_t>();
+    S.mult = mult.as<uint32_t>();
+    S.mult_stride = mult_stride;
+    S.n_in = 0;
+    S.base_planes[0] = scratch.as<uint32_t>();
+    S.zero = scratch.as<uint32_t>() + 256;
+    S.Rb = scratch.as<uint32_t>() + 512;
+    S.commit = scratch.as<U4>() + 64;
+    launch_setup(S, g_stream);
+}
+
+int dashgpu_proj_garble(const uint8_t* seed16, uint32_t n, int p, int q, const uint8_t* phi, const uint64_t* in,
+                        const uint64_t* gates, const uint64_t* wires, uint64_t* rows, uint64_t* out0,
+                        uint64_t* offsets) {
+    return guarded([&] {
+        check_constants();
+        if (p < 2 || p > MAXMOD || q < 2 || q > MAXMOD) throw DataError("modulus out of range");
+        for (int a = 0; a < p; ++a)
+            if (phi[a] >= q) throw DataError("projection table value out of range");
+        DevBuf rk, mult, scratch, dphi, din, dg, dw, drows, dout;
+        proj_setup(seed16, p, q, rk, mult, scratch);
+        dphi.ensure(p);
+        dev::h2d(dphi.p, phi, p, g_stream);
+        din.ensure((size_t)n * 16);
+        dg.ensure((size_t)n * 8);
+        dw.ensure((size_t)n * 8);
+        drows.ensure((size_t)n * p * 16);
+        dout.ensure((size_t)n * 16);
+        if (n) {
+            dev::h2d(din.p, in, (size_t)n * 16, g_stream);
+            dev::h2d(dg.p, gates, (size_t)n * 8, g_stream);
+            dev::h2d(dw.p, wires, (size_t)n * 8, g_stream);
+        }
+        ProjParams P;
+        std::memset(&P, 0, sizeof P);
+        P.n = n;
+        P.p = (uint32_t)p;
+        P.q = (uint32_t)q;
+        P.phi = dphi.as<uint8_t>();
+        P.in = din.as<U4>();
+        P.gates = dg.as<uint64_t>();
+        P.wires = dw.as<uint64_t>();
+        P.rows = drows.as<U4>();
+        P.out = dout.as<U4>();
+        P.rk = rk.as<uint32_t>();
+        P.mult = mult.as<uint32_t>();
+        P.garbler = 1;
+        launch_proj(P, g_stream);
+        if (n) {
+            dev::d2h(rows, drows.p, (size_t)n * p * 16, g_stream);
+            dev::d2h(out0, dout.p, (size_t)n * 16, g_stream);
+        }
+        std::vector<uint32_t> R(2 * NWMAX);
+        dev::d2h(R.data(), mult.as<uint32_t>() + ((uint64_t)(p - 2) * 128 + 1) * NWMAX, NWMAX * 4, g_stream);
+        dev::d2h(R.data() + NWMAX, mult.as<uint32_t>() + ((uint64_t)(q - 2) * 128 + 1) * NWMAX, NWMAX * 4, g_stream);
+        dev::sync(g_stream);
+        if (offsets) {
+            // multiples-table rows: byte digits, or the packed-bit (= compressed) form for powers of two
+            auto comp = [](const uint32_t* w, int m) {
+                if ((m & (m - 1)) == 0) return ((u128)w[3] << 96) | ((u128)w[2] << 64) | ((u128)w[1] << 32) | w[0];
+                return host_compress(w, m);
+            };
+            const u128 rp = comp(R.data(), p), rq = comp(R.data() + NWMAX, q);
+            offsets[0] = (uint64_t)rp;
+            offsets[1] = (uint64_t)(rp >> 64);
+            offsets[2] = (uint64_t)rq;
+            offsets[3] = (uint64_t)(rq >> 64);
+        }
+    });
+}
+
+int dashgpu_proj_eval(uint32_t n, int p, int q, const uint64_t* in, const uint64_t* gates, const uint64_t* rows,
+                      uint64_t* out) {
+    return guarded([&] {
+        check_constants();
+        if (p < 2 || p > MAXMOD || q < 2 || q > MAXMOD) throw DataError("modulus out of range");
+        DevBuf din, dg, drows, dout;
+        din.ensure((size_t)n * 16);
+        dg.ensure((size_t)n * 8);
+        drows.ensure((size_t)n * p * 16);
+        dout.ensure((size_t)n * 16);
+        if (n) {
+            dev::h2d(din.p, in, (size_t)n * 16, g_stream);
+            dev::h2d(dg.p, gates, (size_t)n * 8, g_stream);
+            dev::h2d(drows.p, rows, (size_t)n * p * 16, g_stream);
+        }
+        ProjParams P;
+        std::memset(&P, 0, sizeof P);
+        P.n = n;
+        P.p = (uint32_t)p;
+        P.q = (uint32_t)q;
+        P.in = din.as<U4>();
+        P.gates = dg.as<uint64_t>();
+        P.rows = drows.as<U4>();
+        P.out = dout.as<U4>();
+        launch_proj(P, g_stream);
+        if (n) dev::d2h(out, dout.p, (size_t)n * 16, g_stream);
+        dev::sync(g_stream);
     });
 }
 

@@ -179,6 +179,13 @@ __global__ void __launch_bounds__(128) pad_add_kernel(const __grid_constant__ Pa
     pad_add_thread(P, blockIdx.z, blockIdx.y, u);
 }
 
+__global__ void __launch_bounds__(128) proj_kernel(const __grid_constant__ ProjParams P) {
+    fill_T(g_T0);
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    proj_thread(P, i, make_tab(nullptr, threadIdx.x & 31u));
+}
+
 __global__ void __launch_bounds__(128) setup_offsets_kernel(SetupParams Sp) {
     fill_T(g_T0);
     const uint32_t si = blockIdx.x;  // modulus slot; thread = multiple x < 128
@@ -419,6 +426,14 @@ void launch_pad_add(const PadAddParams& P, void* st) {
     if (P.B == 0 || P.E_out == 0) return;
     ProfScope ps(K_MISC, S(st));
     pad_add_kernel<<<dim3(cdiv(P.E_out, 128), P.wbase[P.k], P.B), 128, 0, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_proj(const ProjParams& P, void* st) {
+    if (P.n == 0) return;
+    ProfScope ps(K_MISC, S(st));
+    ck(cudaFuncSetAttribute(proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    proj_kernel<<<cdiv(P.n, 128), 128, kTabBytes, S(st)>>>(P);
     dev::check();
 }
 

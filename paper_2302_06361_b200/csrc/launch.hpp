@@ -83,6 +83,7 @@ void make_weight_map(TcLinear& t);  // encodes t.tmap for t.wexp
 void launch_linear(const LinParams* Ls, int n, const TcLinear& tc, void* stream);
 void launch_private(const PrivParams& P, void* stream, const Sched& q);
 void launch_pad_add(const PadAddParams& P, void* stream);  // extension layers
+void launch_proj(const ProjParams& P, void* stream);        // t_proj primitive
 void launch_setup(const SetupParams& S, void* stream);
 void launch_encode(const EncodeParams& P, void* stream);
 void launch_dectable(const DecodeParams& P, void* stream);

@@ -20,7 +20,7 @@ from typing import Optional
 
 import numpy as np
 
-from .circuit import Circuit, CircuitDesc
+from .circuit import PRIMES, Circuit, CircuitDesc
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdashgpu.so")
@@ -28,6 +28,15 @@ LIB_PATH = os.path.join(HERE, "libdashgpu.so")
 vp = ctypes.c_void_p
 u8p = ctypes.POINTER(ctypes.c_uint8)
 u16p = ctypes.POINTER(ctypes.c_uint16)
+
+
+def _n_digits(m: int) -> int:
+    """Digits of a label mod m (reference label.cpp:15-29): largest n with m^n <= 2^128."""
+    n, v = 0, 1
+    while v * m <= (1 << 128):
+        v *= m
+        n += 1
+    return n
 u64p = ctypes.POINTER(ctypes.c_uint64)
 i64p = ctypes.POINTER(ctypes.c_int64)
 f64p = ctypes.POINTER(ctypes.c_double)
@@ -115,6 +124,19 @@ def _declare(L):
     L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
     L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
     L.dashgpu_infer_stream.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
+    L.dashgpu_network_setup.argtypes = [vp, u8p, ctypes.c_uint32, ctypes.POINTER(vp)]
+    L.dashgpu_input_base.argtypes = [vp, ctypes.POINTER(vp)]
+    L.dashgpu_layer_garble.argtypes = [vp, ctypes.c_uint32, vp, vp, ctypes.POINTER(vp)]
+    L.dashgpu_layer_eval.argtypes = [vp, ctypes.c_uint32, vp, vp, ctypes.POINTER(vp)]
+    L.dashgpu_network_finish.argtypes = [vp, vp]
+    L.dashgpu_layer_count.argtypes = [vp, ctypes.c_uint32, u64p]
+    L.dashgpu_bundle_info.argtypes = [vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64)]
+    L.dashgpu_bundle_from_labels.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(u16p), ctypes.c_int,
+                                             ctypes.POINTER(vp)]
+    L.dashgpu_bundle_labels.argtypes = [vp, ctypes.c_int, u16p]
+    L.dashgpu_proj_garble.argtypes = [u8p, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u8p, u64p, u64p, u64p,
+                                      u64p, u64p, u64p]
+    L.dashgpu_proj_eval.argtypes = [ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u64p, u64p, u64p, u64p]
     L.dashgpu_profile.argtypes = [ctypes.c_int]
     L.dashgpu_profile_read.argtypes = [f64p, u64p, ctypes.c_int]
     L.dashgpu_prim.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u64p, u64p, u16p, u8p,
@@ -176,6 +198,48 @@ class Dash:
         self._check(self.lib.dashgpu_decode_outputs(net.h, outputs.h, out.ctypes.data_as(i64p)))
         return out
 
+    # ---- layer level (layer.hpp:79-97) ----
+    def network_setup(self, c: "GpuCircuit", seeds: bytes) -> "GarbledNetwork":
+        """garble()'s environment without any layer: offsets, multiples, zero / input base labels."""
+        h = vp()
+        buf = (ctypes.c_uint8 * len(seeds)).from_buffer_copy(seeds)
+        self._check(self.lib.dashgpu_network_setup(c.h, buf, len(seeds) // 16, ctypes.byref(h)))
+        return GarbledNetwork(self, h, c, len(seeds) // 16)
+
+    def input_base(self, net: "GarbledNetwork") -> "Bundle":
+        h = vp()
+        self._check(self.lib.dashgpu_input_base(net.h, ctypes.byref(h)))
+        return Bundle(self, h, net, False)
+
+    def layer_garble(self, net: "GarbledNetwork", layer: int, inp: "Bundle", inp2: "Bundle" = None) -> "Bundle":
+        """garble_layer: base labels in -> base labels out; rows into the network's GC."""
+        h = vp()
+        self._check(self.lib.dashgpu_layer_garble(net.h, layer, inp.h, inp2.h if inp2 else None, ctypes.byref(h)))
+        return Bundle(self, h, net, False)
+
+    def layer_eval(self, net: "GarbledNetwork", layer: int, inp: "Bundle", inp2: "Bundle" = None) -> "Bundle":
+        """eval_layer: active labels in -> active labels out."""
+        h = vp()
+        self._check(self.lib.dashgpu_layer_eval(net.h, layer, inp.h, inp2.h if inp2 else None, ctypes.byref(h)))
+        return Bundle(self, h, net, True)
+
+    def network_finish(self, net: "GarbledNetwork", final_base: "Bundle"):
+        self._check(self.lib.dashgpu_network_finish(net.h, final_base.h))
+
+    def layer_count(self, c: "GpuCircuit", layer: int):
+        out = (ctypes.c_uint64 * 3)()
+        self._check(self.lib.dashgpu_layer_count(c.h, layer, out))
+        return tuple(int(v) for v in out)
+
+    def bundle_from_labels(self, net: "GarbledNetwork", lanes, output: bool = False) -> "Bundle":
+        """LabelTensor images (per lane [batch][elements][n_p] u16 digits) -> device bundle."""
+        arrs = [np.ascontiguousarray(a, np.uint16) for a in lanes]
+        ptrs = (u16p * len(arrs))(*[a.ctypes.data_as(u16p) for a in arrs])
+        h = vp()
+        self._check(self.lib.dashgpu_bundle_from_labels(net.h, arrs[0].shape[1], ptrs, 1 if output else 0,
+                                                        ctypes.byref(h)))
+        return Bundle(self, h, net, output)
+
     def import_bundle(self, net: "GarbledNetwork", payload: bytes, output: bool) -> "Bundle":
         h = vp()
         buf = (ctypes.c_uint8 * len(payload)).from_buffer_copy(payload)
@@ -226,6 +290,35 @@ class Dash:
         n = (ctypes.c_uint64 * 16)()
         k = self.lib.dashgpu_profile_read(ms, n, 16)
         return {KERNEL_KINDS[i]: (ms[i], int(n[i])) for i in range(max(k, 0))}
+
+    # ---- t_proj primitive (gadgets.hpp:146-176) ----
+    def proj_garble(self, seed: bytes, p: int, q: int, phi, labels, gates, wires):
+        """n projection gates: labels = compressed base labels mod p (list of ints).
+        Returns (rows [n][p] ints, out0 [n] ints, (R_p, R_q))."""
+        n = len(labels)
+        ia = np.array([[v & (2**64 - 1), v >> 64] for v in labels], np.uint64).reshape(n, 2)
+        ph = np.ascontiguousarray(phi, np.uint8)
+        g = np.ascontiguousarray(gates, np.uint64)
+        w = np.ascontiguousarray(wires, np.uint64)
+        rows = np.zeros((n, p, 2), np.uint64)
+        out0 = np.zeros((n, 2), np.uint64)
+        offs = np.zeros(4, np.uint64)
+        self._check(self.lib.dashgpu_proj_garble((ctypes.c_uint8 * 16)(*seed), n, p, q, ph.ctypes.data_as(u8p),
+                                                 ia.ctypes.data_as(u64p), g.ctypes.data_as(u64p),
+                                                 w.ctypes.data_as(u64p), rows.ctypes.data_as(u64p),
+                                                 out0.ctypes.data_as(u64p), offs.ctypes.data_as(u64p)))
+        j = lambda a: int(a[0]) | (int(a[1]) << 64)  # noqa: E731
+        return ([[j(r) for r in rr] for rr in rows], [j(o) for o in out0], (j(offs[:2]), j(offs[2:])))
+
+    def proj_eval(self, p: int, q: int, labels, gates, rows):
+        n = len(labels)
+        ia = np.array([[v & (2**64 - 1), v >> 64] for v in labels], np.uint64).reshape(n, 2)
+        g = np.ascontiguousarray(gates, np.uint64)
+        ra = np.array([[[v & (2**64 - 1), v >> 64] for v in rr] for rr in rows], np.uint64).reshape(n, p, 2)
+        out = np.zeros((n, 2), np.uint64)
+        self._check(self.lib.dashgpu_proj_eval(n, p, q, ia.ctypes.data_as(u64p), g.ctypes.data_as(u64p),
+                                               ra.ctypes.data_as(u64p), out.ctypes.data_as(u64p)))
+        return [int(o[0]) | (int(o[1]) << 64) for o in out]
 
     # ---- primitives (parity tests) ----
     def prim(self, op: int, m: int, q: int = 0, inp=None, out=None, key: bytes = None, wires=None, gate: int = 0,
@@ -315,6 +408,16 @@ class Bundle:
             self.eng.lib.dashgpu_bundle_destroy(self.h)
         except Exception:
             pass
+
+    def labels(self, lane: int) -> np.ndarray:
+        """LabelTensor image of CRT lane `lane`: [batch][elements][n_p] u16 digits."""
+        B, E = ctypes.c_uint32(), ctypes.c_uint64()
+        self.eng._check(self.eng.lib.dashgpu_bundle_info(self.h, ctypes.byref(B), ctypes.byref(E)))
+        p = PRIMES[lane]
+        nd = _n_digits(p)
+        out = np.zeros((B.value, E.value, nd), np.uint16)
+        self.eng._check(self.eng.lib.dashgpu_bundle_labels(self.h, lane, out.ctypes.data_as(u16p)))
+        return out
 
     def payload(self, b: int = 0) -> bytes:
         """bundle_payload (garble.cpp:465-472) of inference b."""

@@ -134,6 +134,11 @@ void launch_pad_add(const PadAddParams& P, void*) {
             for (uint32_t u = 0; u < P.E_out; ++u) pad_add_thread(P, (uint32_t)b, (uint32_t)wi, u);
 }
 
+void launch_proj(const ProjParams& P, void*) {
+#pragma omp parallel for
+    for (int64_t i = 0; i < (int64_t)P.n; ++i) proj_thread(P, (uint32_t)i, tab());
+}
+
 void launch_private(const PrivParams& P, void*, const Sched&) {
 #pragma omp parallel for collapse(2)
     for (int64_t b = 0; b < (int64_t)P.B; ++b)

@@ -417,3 +417,88 @@ def test_infer_batch19_matches_stepwise(eng):
     ref = eng.decode_outputs(net, eng.evaluate(net, eng.garble_inputs(net, x)))
     assert (out == ref).all()
     assert all(out[b].tolist() == g.plain_forward(x[b]).tolist() for b in range(B))
+
+
+# ------------------------------------------------ layer level (layer.hpp:79-97)
+
+def _layer_by_layer(eng, g, c, seeds, x):
+    net = eng.network_setup(g, seeds)
+    outs = [eng.input_base(net)]
+    for li, l in enumerate(c.layers):
+        src = li if l.src == 0 else (0 if l.src < 0 else l.src)
+        src2 = None if l.kind != 7 else outs[li if l.src2 == 0 else (0 if l.src2 < 0 else l.src2)]
+        outs.append(eng.layer_garble(net, li, outs[src], src2))
+    eng.network_finish(net, outs[-1])
+    act = [eng.garble_inputs(net, x)]
+    for li, l in enumerate(c.layers):
+        src = li if l.src == 0 else (0 if l.src < 0 else l.src)
+        src2 = None if l.kind != 7 else act[li if l.src2 == 0 else (0 if l.src2 < 0 else l.src2)]
+        act.append(eng.layer_eval(net, li, act[src], src2))
+    return net, outs, act
+
+
+@pytest.mark.parametrize("name", ["model_tiny_priv", "model_tiny", "dag"])
+def test_layer_level_api_matches_whole_network(eng, name):
+    from helpers import models
+
+    c = _small_dag() if name == "dag" else models.build("model_tiny", 1000, 8, name.endswith("priv"))
+    g = eng.circuit(c)
+    seeds = seed_hex(0x1A1) + seed_hex(0x1A2)
+    x = np.random.default_rng(9).integers(-7, 8, size=(2, c.n_in))
+    net, outs, act = _layer_by_layer(eng, g, c, seeds, x)
+    whole = eng.garble(g, seeds)
+    for b in range(2):
+        assert net.export_gc(b) == whole.export_gc(b)
+        assert net.export_decoding(b) == whole.export_decoding(b)
+        assert net.export_encoding(b) == whole.export_encoding(b)
+    ref = eng.evaluate(whole, eng.garble_inputs(whole, x))
+    assert act[-1].payload(1) == ref.payload(1)
+    assert (eng.decode_outputs(net, act[-1]) == eng.decode_outputs(whole, ref)).all()
+    assert sum(eng.layer_count(g, li)[0] for li in range(len(c.layers))) == g.info.cts
+
+
+def test_label_tensor_images_roundtrip(eng):
+    g = eng.model("model_tiny", 1000, 8)
+    net = eng.garble(g, seed_hex(0x1B0))
+    bi = eng.garble_inputs(net, g.random_input(3)[None, :])
+    lanes = [bi.labels(i) for i in range(8)]
+    assert lanes[0].shape == (1, g.info.n_in, 128) and lanes[1].shape == (1, g.info.n_in, 80)
+    assert all((l < p).all() for l, p in zip(lanes, [2, 3, 5, 7, 11, 13, 17, 19]))
+    back = eng.bundle_from_labels(net, lanes)
+    assert back.payload(0) == bi.payload(0)
+    out = eng.decode_outputs(net, eng.evaluate(net, back))
+    assert out[0].tolist() == g.plain_forward(g.random_input(3)).tolist()
+
+
+@pytest.mark.parametrize("p,q", [(3, 110), (7, 2), (2, 8), (19, 5), (110, 2)])
+def test_projection_gate_primitive_vs_oracle(eng, oracle, p, q):
+    # t_proj (gadgets.hpp:146-176): every garbled row equals the oracle's
+    # encrypt_label of (in + aR_p) over (out0 + phi(a) R_q); evaluation of any
+    # active input recovers out0 + phi(v) R_q
+    seed = seed_hex(0xC0DE + p)
+    rnd = np.random.default_rng(p * 1000 + q)
+    n = 24
+    phi = rnd.integers(0, q, size=p).tolist()
+    base = [oracle.compress(p, oracle.prf_label(seed_hex(0x77), 300 + i, p)) for i in range(n)]
+    gates = rnd.integers(0, 2**40, size=n).tolist()
+    wires = (10_000 + np.arange(n)).tolist()
+    rows, out0, (Rp, Rq) = eng.proj_garble(seed, p, q, phi, base, gates, wires)
+    rp = np.array(oracle.decompress_mod(Rp, p))
+    rq = np.array(oracle.decompress_mod(Rq, q))
+    assert rp[0] == 1 and rq[0] == 1  # offsets have colour digit 1 (prf.hpp:28-32)
+    vs = rnd.integers(0, p, size=n)
+    active = []
+    for i in range(n):
+        x = np.array(oracle.decompress_mod(base[i], p))
+        o0 = np.array(oracle.decompress_mod(out0[i], q))
+        assert o0.tolist() == oracle.prf_label(seed, wires[i], q)
+        c = int(x[0])
+        for a in range(p):
+            key = ((x + a * rp) % p).tolist()
+            msg = ((o0 + phi[a] * rq) % q).tolist()
+            assert rows[i][(c + a) % p] == oracle.encrypt_label(p, key, gates[i], (c + a) % p, 0, q, msg), (i, a)
+        active.append(oracle.compress(p, ((x + int(vs[i]) * rp) % p).tolist()))
+    got = eng.proj_eval(p, q, active, gates, rows)
+    for i in range(n):
+        o0 = np.array(oracle.decompress_mod(out0[i], q))
+        assert got[i] == oracle.compress(q, ((o0 + phi[vs[i]] * rq) % q).tolist())
