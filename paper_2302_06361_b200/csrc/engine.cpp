@@ -851,8 +851,9 @@ struct HostBuf {
 };
 
 static void* g_stream = nullptr;
-// launches with at most this many elements run warp-per-element (kernels_act.cu)
-constexpr uint64_t kWpeMaxElementsHost = 8192;
+// evaluation launches with at most this many elements run warp-per-element on
+// the level tape (kernels_act.cu kWpeMaxEval)
+constexpr uint64_t kWpeMaxElementsHost = 12000;
 
 struct HLayer {
     int kind = 0;

@@ -93,7 +93,12 @@ __global__ void __launch_bounds__((G ? kActWarpsGarble : kActWarpsEval) * 32, 1)
 // Small garbling launches (few elements in total): one warp per element
 // (wpe.cuh), every activation layer in one persistent launch.
 constexpr int kWpeWarps = 16;
-constexpr uint64_t kWpeMaxElements = 8192;
+// Warp per element wins while the per-thread launch would be latency-bound
+// and the warps fit about one wave: garbling splits rows over the lanes (much
+// lower latency, ~5x lower throughput per SM: Model A b64 = 16k elements is
+// 23.5 ms warp-per-element vs 13.8 ms per-thread), evaluation up to ~12k.
+constexpr uint64_t kWpeMaxGarble = 8192;
+constexpr uint64_t kWpeMaxEval = 12000;  // engine.cpp sizes the slots for it (kWpeMaxElementsHost)
 
 __global__ void __launch_bounds__(kWpeWarps * 32, 1)
     act_wpe_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
@@ -227,7 +232,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     ProfScope ps(garble ? K_ACT_GARBLE : K_ACT_EVAL, S(st));
     uint64_t elements = 0;
     for (int i = 0; i < n; ++i) elements += (uint64_t)host_layers[i].B * host_layers[i].E;
-    if (!garble && elements <= kWpeMaxElements) {
+    if (!garble && elements <= kWpeMaxEval) {
         ItemMap wm;
         std::memset(&wm, 0, sizeof wm);
         wm.n = (uint32_t)n;
@@ -244,7 +249,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         ck(cudaGetLastError(), "act wpe eval launch");
         return;
     }
-    if (garble && elements <= kWpeMaxElements) {
+    if (garble && elements <= kWpeMaxGarble) {
         ItemMap wm;
         std::memset(&wm, 0, sizeof wm);
         wm.n = (uint32_t)n;
@@ -269,7 +274,10 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     ck(cudaMemsetAsync(counter, 0, sizeof(uint32_t), S(st)), "counter reset");
     // garbling: chunked tapes (host_layers[].chunk_op); evaluation: whole tapes
     uint32_t nchunks = 1;
-    if (garble) {
+    // chunked tapes only pay when the launch has more warp items than warp
+    // slots (the last wave); below that every chunk would just wait in turn
+    const uint64_t slots = (uint64_t)sm_count() * kActWarpsGarble;
+    if (garble && map.base[n] > slots) {
         for (int i = 0; i < n; ++i)
             for (int c = 1; c <= MAXCHUNK; ++c)
                 if (host_layers[i].chunk_op[c] == host_layers[i].n_ops) {
