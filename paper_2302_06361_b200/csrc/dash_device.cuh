@@ -910,6 +910,33 @@ DASH_HD void act_output_thread(const ActParams& P, uint32_t b, uint32_t u, int i
 }
 
 // ---- evaluation of one op ----
+// c mod m of a compressed label (its colour digit) without unpacking digits
+DASH_HD uint32_t colour_c(const U4& c, const ModC& M) {
+    if (M.pow2) return c.x[0] & (M.m - 1u);
+    uint64_t r = c.x[3] - (uint32_t)umulhi64((uint64_t)c.x[3], M.mag64) * M.m;
+    for (int i = 2; i >= 0; --i) {
+        const uint64_t x = (r << 32) | c.x[i];  // < m * 2^32: the magic quotient is exact
+        r = x - umulhi64(x, M.mag64) * M.m;
+    }
+    return (uint32_t)r;
+}
+
+// Compressed operand (a slot already holds compress(label) < m^n, so a
+// slot operand is used as is; an input lane is loaded and compressed) and
+// its colour.  digits: also unpack the digits into L (needed by half gates).
+DASH_HD U4 operand_c(LB L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M, uint32_t& colour,
+                     bool digits) {
+    if (v < IN_LANE) {
+        const U4 c = e.slot0[(uint64_t)v * e.sstride];
+        colour = colour_c(c, M);
+        if (digits) load_operand(L, P, e, v, M);
+        return c;
+    }
+    load_operand(L, P, e, v, M);
+    colour = lb_color(L, M);
+    return lb_compress(L, M);
+}
+
 DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
     switch (op.kind) {
         case OP_PROJ:
@@ -918,8 +945,8 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const ModC& Mq = c_mod[op.qm];
             const uint64_t g = e.gate0 + op.gate_off;
             const U4* R = e.rows + op.ct_off;
-            load_operand(e.X, P, e, op.a, Mp);
-            const uint32_t row = lb_color(e.X, Mp);
+            uint32_t row;
+            const U4 Xc = operand_c(e.X, P, e, op.a, Mp, row, false);
             U4 ct;
             if (op.kind == OP_PROJ) {
                 ct = R[row];
@@ -928,7 +955,7 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             } else {
                 ct = R[row - 1];
             }
-            const U4 H = hash_tw(lb_compress(e.X, Mp), g, row, 0, e.t);
+            const U4 H = hash_tw(Xc, g, row, 0, e.t);
             lb_dec(e.A, ct, H, Mq);
             store_slot(e, op.out, e.A, Mq);
             break;
@@ -941,12 +968,11 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const uint32_t p = op.pm, q = mm ? op.qm : op.pm;
             const uint64_t g = e.gate0 + op.gate_off;
             const U4* R = e.rows + op.ct_off;
-            load_operand(e.X, P, e, op.a, Mp);
-            load_operand(e.K, P, e, op.b, Mq);
-            const uint32_t cx = lb_color(e.X, Mp), cy = lb_color(e.K, Mq);
+            uint32_t cx, cy;
+            const U4 Xc = operand_c(e.X, P, e, op.a, Mp, cx, true);
+            const U4 Ky = operand_c(e.K, P, e, op.b, Mq, cy, false);
             // u = Dec(x, {g,cx,0}); out = Dec(y, {g,cy,1}) (+ s x) - u, all streamed
-            const U4 Hx = hash_tw(lb_compress(e.X, Mp), g, cx, 0, e.t);
-            const U4 Ky = lb_compress(e.K, Mq);
+            const U4 Hx = hash_tw(Xc, g, cx, 0, e.t);
             lb_dec(e.A, R[p + cy], hash_tw(Ky, g, cy, 1, e.t), Mp);
             uint32_t s = cy;
             if (mm) {  // decrypt_short (cipher.cpp:62-69)
