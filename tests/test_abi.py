@@ -83,3 +83,26 @@ def test_bad_circuits_raise_data_error():
     bad = Circuit([4], 17, [relu()])  # k out of range
     desc = bad.to_desc()
     assert lib.dashgpu_circuit_create(ctypes.byref(desc), ctypes.byref(h)) == 3
+
+
+def test_bad_extension_circuits_raise_data_error(oracle):
+    # Pad2d / Add / DAG inputs (include/dash_circuit_desc.h) are validated by
+    # the engine and the oracle alike
+    from paper_2302_06361_b200.circuit import Circuit, add, dense, pad2d, relu
+    from paper_2302_06361_b200.engine import _declare
+    from pyoracle import CheckerError
+
+    lib = ctypes.CDLL(CUDA_LIB)
+    _declare(lib)
+    cases = [
+        Circuit([4], 8, [pad2d(1)]),                                     # pad needs [C][H][W]
+        Circuit([4], 8, [relu(), add(3)]),                               # add operand from a later layer
+        Circuit([4], 8, [dense(4, 3, np.zeros(12), np.zeros(3)), add(-1)]),  # add shapes differ (3 vs 4)
+        Circuit([4], 8, [relu(src=2)]),                                  # input from a later layer
+    ]
+    for bad in cases:
+        h = ctypes.c_void_p()
+        desc = bad.to_desc()
+        assert lib.dashgpu_circuit_create(ctypes.byref(desc), ctypes.byref(h)) == 3, bad
+        with pytest.raises(CheckerError):
+            oracle.circuit(bad)
