@@ -154,14 +154,19 @@ static inline U4 aes_pi(U4 s, AesTab t) { return aes_core(s, RkConst{}, t); }
 static inline U4 aes_key(U4 s, const uint32_t* rk, AesTab t) { return aes_core(s, RkPtr{rk}, t); }
 #endif
 
-// Davies-Meyer of K = Kc ^ tweak(g, row, slot)   (cipher.cpp:8-12, cipher.hpp:23-26)
+// Davies-Meyer of K = Kc ^ tweak(g, row, slot)   (cipher.cpp:8-12, cipher.hpp:23-26).
+// INLINE: the AES rounds are inlined at the call site (the garbling row loop,
+// one copy) instead of calling aes_pi: a call spills the caller's live
+// registers to local memory, which misses the small L1 left next to 218 KB
+// of shared memory.
+template <bool INLINE = false>
 DASH_HD U4 hash_tw(const U4& Kc, uint64_t g, uint32_t row, uint32_t slot, const AesTab& t) {
     U4 K;
     K.x[0] = Kc.x[0] ^ (uint32_t)g;
     K.x[1] = Kc.x[1] ^ (uint32_t)(g >> 32);
     K.x[2] = Kc.x[2] ^ row;
     K.x[3] = Kc.x[3] ^ slot;
-    U4 H = aes_pi(K, t);
+    U4 H = INLINE ? aes_core(K, RkConst{}, t) : aes_pi(K, t);
     H.x[0] ^= K.x[0];
     H.x[1] ^= K.x[1];
     H.x[2] ^= K.x[2];
@@ -787,7 +792,7 @@ DASH_NI void garble_rows_n(LB X, LB base, AesTab t, const uint32_t* mult, uint32
     for (uint32_t a = 0; a < p; ++a) {
         uint32_t row = cin + a;
         row = row >= p ? row - p : row;
-        const U4 H = hash_tw(lb_key_step(X, Rp, Mp), g, row, 0, t);
+        const U4 H = hash_tw<true>(lb_key_step(X, Rp, Mp), g, row, 0, t);
         const uint32_t v = phi ? phi[a] : (a * r) % p;
         const U4 ct = lb_enc(H, base, Mrow + (uint64_t)v * NWMAX, nullptr, 0, Mq);
         if (!grr) R[row] = ct;
