@@ -68,7 +68,11 @@ enum OpKind : uint8_t {
     OP_ADD = 5,      // free_add (binary step)
     OP_ADDCONST = 6, // add_public_constant
     OP_OUTPUT = 7,   // element result for lane `cst`
+    OP_ADDACC = 8,   // running sum of a fused free-add chain: A += b (OP_ADD / OP_ADDACC with
+                     // cst & kKeep leave the sum in A instead of storing it)
 };
+
+constexpr uint16_t kKeep = 0x8000;  // fused add chain: result stays in the A buffer
 
 // Operand encoding: < 240 -> slot index; >= 240 -> input lane (v - 240).
 constexpr uint8_t IN_LANE = 240;

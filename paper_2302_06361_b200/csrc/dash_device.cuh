@@ -875,11 +875,12 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             store_slot(e, op.out, e.A, Mp);
             break;
         }
-        case OP_ADD: {
+        case OP_ADD:
+        case OP_ADDACC: {  // free_add; fused chains keep the running sum in A
             const ModC& M = c_mod[op.qm];
-            load_operand(e.A, P, e, op.a, M);
+            if (op.kind == OP_ADD) load_operand(e.A, P, e, op.a, M);
             add_operand(e.A, P, e, op.b, M);
-            store_slot(e, op.out, e.A, M);
+            if (!(op.cst & kKeep)) store_slot(e, op.out, e.A, M);
             break;
         }
         case OP_ADDCONST: {  // add_public_constant (gadgets.hpp:127-139)
@@ -993,11 +994,12 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             store_slot(e, op.out, e.A, Mp);
             break;
         }
-        case OP_ADD: {
+        case OP_ADD:
+        case OP_ADDACC: {
             const ModC& M = c_mod[op.qm];
-            load_operand(e.A, P, e, op.a, M);
+            if (op.kind == OP_ADD) load_operand(e.A, P, e, op.a, M);
             add_operand(e.A, P, e, op.b, M);
-            store_slot(e, op.out, e.A, M);
+            if (!(op.cst & kKeep)) store_slot(e, op.out, e.A, M);
             break;
         }
         case OP_ADDCONST: {

@@ -652,12 +652,21 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
     const int nops = (int)r.ops.size();
     std::vector<int> order;
     std::vector<char> done(nops, 0);
+    // depth-first, deeper operand first (keeps the live label set small once
+    // add chains are fused below: a chain's running-sum terms are produced
+    // after the long carry dependency they are added to)
+    std::vector<int> depth(r.vmod.size(), 0);
+    for (const auto& o : r.ops)
+        if (o.out >= 0)
+            depth[o.out] = 1 + std::max(o.a >= b.k ? depth[o.a] : 0, o.b >= b.k ? depth[o.b] : 0);
     std::function<void(int)> dfs = [&](int v) {
         if (v < 0 || v < b.k) return;
         const int op = r.producer[v];
         if (done[op]) return;
-        dfs(r.ops[op].a);
-        dfs(r.ops[op].b);
+        int x = r.ops[op].a, y = r.ops[op].b;
+        if (y >= b.k && (x < b.k || depth[y] > depth[x])) std::swap(x, y);
+        dfs(x);
+        dfs(y);
         done[op] = 1;
         order.push_back(op);
     };
@@ -669,18 +678,67 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
         }
     for (int i = 0; i < nops; ++i)
         if (!done[i]) throw std::logic_error("tape: unreachable gadget");
+    // Fuse chains of free adds (the mixed-radix sums, the zero-test count):
+    // an ADD whose result only feeds the next ADD's running operand is not
+    // stored; the chain runs as OP_ADD(keep) + OP_ADDACC... at the position of
+    // its last ADD (all terms are computed before it in DFS order), so the
+    // running sum never round-trips through a compressed slot.  Execution
+    // order does not change any output: gate / wire / row ids are per op.
+    std::vector<int> uses(r.vmod.size(), 0);
+    for (const auto& o : r.ops) {
+        if (o.a >= 0) ++uses[o.a];
+        if (o.b >= 0) ++uses[o.b];
+    }
+    std::vector<char> inter(nops, 0);  // ADD whose result is the running operand of the next ADD only
+    for (int i = 0; i < nops; ++i) {
+        const auto& o = r.ops[i];
+        if (o.kind != OP_ADD || o.a < b.k) continue;
+        const int pa = r.producer[o.a];
+        if (r.ops[pa].kind == OP_ADD && uses[o.a] == 1) inter[pa] = 1;
+    }
+    struct Emit {
+        int op, kind, a, b, out;
+        bool keep;
+    };
+    std::vector<Emit> emits;
+    for (int t : order) {
+        const auto& o = r.ops[t];
+        if (o.kind == OP_ADD && inter[t]) continue;  // emitted with its chain
+        if (o.kind != OP_ADD || o.a < b.k || !inter[r.producer[o.a]]) {
+            emits.push_back({t, o.kind, o.a, o.b, o.out, false});
+            continue;
+        }
+        std::vector<int> chain{t};  // walk back to the chain's first ADD
+        while (chain.back() >= 0) {
+            const auto& c = r.ops[chain.back()];
+            if (c.a < b.k || !inter[r.producer[c.a]]) break;
+            chain.push_back(r.producer[c.a]);
+        }
+        std::reverse(chain.begin(), chain.end());
+        const auto& f = r.ops[chain[0]];
+        emits.push_back({chain[0], OP_ADD, f.a, f.b, -1, true});
+        for (size_t j = 1; j < chain.size(); ++j) {
+            const auto& c = r.ops[chain[j]];
+            const bool last_add = j + 1 == chain.size();
+            emits.push_back({chain[j], OP_ADDACC, -1, c.b, last_add ? c.out : -1, !last_add});
+        }
+    }
     std::vector<int> last(r.vmod.size(), -1);
-    for (int t = 0; t < (int)order.size(); ++t) {
-        const auto& o = r.ops[order[t]];
-        if (o.a >= 0) last[o.a] = t;
-        if (o.b >= 0) last[o.b] = t;
+    for (int t = 0; t < (int)emits.size(); ++t) {
+        if (emits[t].a >= 0) last[emits[t].a] = t;
+        if (emits[t].b >= 0) last[emits[t].b] = t;
     }
     std::vector<int> slot(r.vmod.size(), -1);
     std::vector<int> freelist;
     int nslots = 0;
     Tape tp;
-    for (int t = 0; t < (int)order.size(); ++t) {
-        const auto& o = r.ops[order[t]];
+    for (int t = 0; t < (int)emits.size(); ++t) {
+        const Emit& em = emits[t];
+        Recorder::ROp o = r.ops[em.op];
+        o.kind = em.kind;
+        o.a = em.a;
+        o.b = em.b;
+        o.out = em.out;
         TapeOp d;
         std::memset(&d, 0, sizeof d);
         d.kind = (uint8_t)o.kind;
@@ -694,7 +752,7 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
         d.b = enc(o.b);
         d.pm = (uint16_t)o.pm;
         d.qm = (uint16_t)o.qm;
-        d.cst = (uint16_t)o.cst;
+        d.cst = (uint16_t)(o.cst | (em.keep ? kKeep : 0));
         d.gate_off = (uint32_t)o.gate;
         d.wire_off = (uint32_t)o.wire;
         d.ct_off = (uint32_t)o.ct;
@@ -760,7 +818,16 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
             tp.lv_start.push_back((uint16_t)tp.lv_ops.size());
             for (int t : ops) {
                 const auto& o = r.ops[t];
-                TapeOp d = tp.ops[std::find(order.begin(), order.end(), t) - order.begin()];
+                TapeOp d;
+                std::memset(&d, 0, sizeof d);
+                d.kind = (uint8_t)o.kind;
+                d.pm = (uint16_t)o.pm;
+                d.qm = (uint16_t)o.qm;
+                d.cst = (uint16_t)o.cst;
+                d.gate_off = (uint32_t)o.gate;
+                d.wire_off = (uint32_t)o.wire;
+                d.ct_off = (uint32_t)o.ct;
+                d.phi_off = o.phi;
                 auto enc = [&](int v) -> uint8_t {
                     if (v < 0) return 0;
                     if (v < b.k) return (uint8_t)(IN_LANE + v);
@@ -1242,6 +1309,7 @@ static void fill_chunks(ActParams& P, const Tape& T, int K) {
     for (int c = 1; c < K; ++c) {
         const double target = cum[n] * c / K;
         while (at < n && cum[at] < target) ++at;
+        while (at < n && T.ops[at].kind == OP_ADDACC) ++at;  // never split a fused add chain
         P.chunk_op[c] = (uint16_t)std::max<size_t>(at, P.chunk_op[c - 1]);
     }
     for (int c = K; c <= MAXCHUNK; ++c) P.chunk_op[c] = (uint16_t)n;

@@ -174,6 +174,7 @@ __device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const 
             break;
         }
         case OP_ADD:
+        case OP_ADDACC:
         case OP_ADDCONST:
             if (lane == 0) garble_op(P, e, op);
             __syncwarp();
