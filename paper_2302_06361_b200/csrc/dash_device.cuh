@@ -43,7 +43,7 @@ extern DASH_CONST uint16_t c_modslot[MAXMOD + 1];  // modulus -> mult-table slot
 #endif
 
 
-struct U4 {
+struct alignas(16) U4 {  // 16-byte aligned: one 128-bit load / store per garbled row
     uint32_t x[4];
 };
 
