@@ -718,7 +718,8 @@ struct ItemMap {
 struct Elt {
     uint32_t b, u;
     uint64_t gate0, wire0;
-    U4* rows;
+    U4* rows;           // row j of this element at rows[j * rs] (act_rows)
+    uint32_t rs;
     const uint32_t* rk;
     const uint32_t* mult;
     U4* slot0;          // slot s at slot0[s * sstride]
@@ -726,6 +727,31 @@ struct Elt {
     LB X, K, A;
     AesTab t;
 };
+
+// Garbled rows of an activation layer in HBM: blocks of 32 consecutive
+// elements, row-major inside a block (row j of the block's element l at
+// block + j*w + l, w = block width, 32 except a ragged last block), so the 32
+// lanes of a warp write one contiguous 512-byte run per row instead of 32
+// scattered half-sectors.  dashgpu_export_gc restores the reference order
+// (element-major, layer.cpp:537-541).
+DASH_HD U4* act_rows(U4* layer_blob, uint32_t E, uint64_t uc_cts, uint32_t u, uint32_t& rs) {
+    const uint32_t blk = u >> 5, left = E - (blk << 5);
+    rs = left < 32 ? left : 32;
+    return layer_blob + (uint64_t)blk * 32 * uc_cts + (u & 31);
+}
+
+// Garbled rows are written once and read much later (evaluation): streaming
+// stores keep them from evicting the kernels' L2 working set (label slots,
+// multiples tables, register spills).
+DASH_HD void store_row(U4* p, const U4& v) {
+#if defined(__CUDA_ARCH__)
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x[0]), "r"(v.x[1]), "r"(v.x[2]),
+                 "r"(v.x[3])
+                 : "memory");
+#else
+    *p = v;
+#endif
+}
 
 DASH_HD const uint32_t* mult_row(const Elt& e, uint32_t m, uint32_t v) {
     return e.mult + ((uint64_t)c_modslot[m] * 128u + v) * NWMAX;
@@ -784,7 +810,7 @@ DASH_NI void store_n(U4* slot, LB L, uint32_t m) { *slot = lb_compress(L, c_mod[
 // base + phi(a) R_q (phi table) or base + (a r mod p) R_p (phi == nullptr);
 // GRR stores row j at R[j-1] and drops row 0 (gadgets.hpp:156-175, 195-219, 244-252).
 DASH_NI void garble_rows_n(LB X, LB base, AesTab t, const uint32_t* mult, uint32_t p, uint32_t q, uint32_t cin,
-                           uint64_t g, const uint8_t* phi, uint32_t r, U4* R, int grr) {
+                           uint64_t g, const uint8_t* phi, uint32_t r, U4* R, int grr, uint32_t rs) {
     const ModC& Mp = c_mod[p];
     const ModC& Mq = c_mod[q];
     const uint32_t* Rp = mult + ((uint64_t)c_modslot[p] * 128u + 1) * NWMAX;
@@ -795,8 +821,8 @@ DASH_NI void garble_rows_n(LB X, LB base, AesTab t, const uint32_t* mult, uint32
         const U4 H = hash_tw<true>(lb_key_step(X, Rp, Mp), g, row, 0, t);
         const uint32_t v = phi ? phi[a] : (a * r) % p;
         const U4 ct = lb_enc(H, base, Mrow + (uint64_t)v * NWMAX, nullptr, 0, Mq);
-        if (!grr) R[row] = ct;
-        else if (row != 0) R[row - 1] = ct;
+        if (!grr) store_row(R + (uint64_t)row * rs, ct);
+        else if (row != 0) store_row(R + (uint64_t)(row - 1) * rs, ct);
     }
 }
 
@@ -810,7 +836,7 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const uint32_t p = op.pm;
             const uint64_t g = e.gate0 + op.gate_off;
             const uint8_t* phi = P.phi + op.phi_off;
-            U4* R = e.rows + op.ct_off;
+            U4* R = e.rows + (uint64_t)op.ct_off * e.rs;
             load_operand(e.X, P, e, op.a, Mp);
             const uint32_t cin = lb_color(e.X, Mp);
             if (op.kind == OP_PROJ) {
@@ -825,7 +851,7 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
                 lb_neg(e.A, Mq);
                 lb_sub_g(e.A, mult_row(e, op.qm, phi[a0]), Mq);
             }
-            garble_rows_n(e.X, e.A, e.t, e.mult, p, op.qm, cin, g, phi, 0, R, op.kind == OP_GRR);
+            garble_rows_n(e.X, e.A, e.t, e.mult, p, op.qm, cin, g, phi, 0, R, op.kind == OP_GRR, e.rs);
             store_slot(e, op.out, e.A, Mq);
             break;
         }
@@ -836,7 +862,7 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const ModC& Mq = c_mod[mm ? op.qm : op.pm];
             const uint32_t p = op.pm, q = mm ? op.qm : op.pm;
             const uint64_t g = e.gate0 + op.gate_off;
-            U4* R = e.rows + op.ct_off;
+            U4* R = e.rows + (uint64_t)op.ct_off * e.rs;
             load_operand(e.K, P, e, op.b, Mq);
             const uint32_t cy = lb_color(e.K, Mq);
             load_operand(e.X, P, e, op.a, Mp);
@@ -846,7 +872,7 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             prf_n(e.A, e.wire0 + op.wire_off, 0, op.pm, e.rk, e.t);
             const U4 u0c = lb_compress(e.A, Mp);
             // X is the running key here (K only holds the Z_2-sized y operand)
-            garble_rows_n(e.X, e.A, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0);
+            garble_rows_n(e.X, e.A, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0, e.rs);
             // evaluator rows: key y + bR_q, payload v0 - s x, slot 1
             load_operand(e.X, P, e, op.a, Mp);
             prf_n(e.A, e.wire0 + op.wire_off + 1, 0, op.pm, e.rk, e.t);
@@ -864,13 +890,13 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
                 const U4 Kc = lb_key_step(e.K, Rq, Mq);
                 const U4 H = hash_tw(Kc, g, row, 1, e.t);
                 LB X = e.X;
-                R[p + row] = lb_enc(H, e.A, nullptr, &X, mm ? s : row, Mp);
+                store_row(R + (uint64_t)(p + row) * e.rs, lb_enc(H, e.A, nullptr, &X, mm ? s : row, Mp));
                 if (mm) {  // encrypt_short field of this row (cipher.cpp:45-60)
                     const U4 Hs = hash_tw(Kc, g, 0, 2, e.t);
                     u4_or_shl(sb, (s ^ (Hs.x[0] & fmask)) & fmask, fw * row);
                 }
             }
-            if (mm) R[p + q] = sb;
+            if (mm) store_row(R + (uint64_t)(p + q) * e.rs, sb);
             lb_sub_c(e.A, u0c, Mp);  // out = v0 - u0
             store_slot(e, op.out, e.A, Mp);
             break;
@@ -950,16 +976,16 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const ModC& Mp = c_mod[op.pm];
             const ModC& Mq = c_mod[op.qm];
             const uint64_t g = e.gate0 + op.gate_off;
-            const U4* R = e.rows + op.ct_off;
+            const U4* R = e.rows + (uint64_t)op.ct_off * e.rs;
             uint32_t row;
             const U4 Xc = operand_c(e.X, P, e, op.a, Mp, row, false);
             U4 ct;
             if (op.kind == OP_PROJ) {
-                ct = R[row];
+                ct = R[(uint64_t)row * e.rs];
             } else if (row == 0) {
                 ct.x[0] = ct.x[1] = ct.x[2] = ct.x[3] = 0;
             } else {
-                ct = R[row - 1];
+                ct = R[(uint64_t)(row - 1) * e.rs];
             }
             const U4 H = hash_tw(Xc, g, row, 0, e.t);
             lb_dec(e.A, ct, H, Mq);
@@ -973,23 +999,23 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const ModC& Mq = c_mod[mm ? op.qm : op.pm];
             const uint32_t p = op.pm, q = mm ? op.qm : op.pm;
             const uint64_t g = e.gate0 + op.gate_off;
-            const U4* R = e.rows + op.ct_off;
+            const U4* R = e.rows + (uint64_t)op.ct_off * e.rs;
             uint32_t cx, cy;
             const U4 Xc = operand_c(e.X, P, e, op.a, Mp, cx, true);
             const U4 Ky = operand_c(e.K, P, e, op.b, Mq, cy, false);
             // u = Dec(x, {g,cx,0}); out = Dec(y, {g,cy,1}) (+ s x) - u, all streamed
             const U4 Hx = hash_tw(Xc, g, cx, 0, e.t);
-            lb_dec(e.A, R[p + cy], hash_tw(Ky, g, cy, 1, e.t), Mp);
+            lb_dec(e.A, R[(uint64_t)(p + cy) * e.rs], hash_tw(Ky, g, cy, 1, e.t), Mp);
             uint32_t s = cy;
             if (mm) {  // decrypt_short (cipher.cpp:62-69)
                 const uint32_t fw = field_width(p);
                 const uint32_t fmask = (1u << fw) - 1u;
                 const U4 Hs = hash_tw(Ky, g, 0, 2, e.t);
-                const uint32_t field = u4_shr_low(R[p + q], fw * cy) & fmask;
+                const uint32_t field = u4_shr_low(R[(uint64_t)(p + q) * e.rs], fw * cy) & fmask;
                 s = ((field ^ (Hs.x[0] & fmask)) & fmask) % p;
             }
             lb_add_scaled(e.A, e.X, s, Mp);
-            lb_sub_c(e.A, R[cx], Mp);  // - u = - (decompress(ct_x) - pad_x)
+            lb_sub_c(e.A, R[(uint64_t)cx * e.rs], Mp);  // - u = - (decompress(ct_x) - pad_x)
             lb_add_c(e.A, Hx, Mp);
             store_slot(e, op.out, e.A, Mp);
             break;
@@ -1023,7 +1049,7 @@ template <bool GARBLE>
 DASH_HD void act_element(const ActParams& P, Elt& e, int op0, int op1) {
     e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
     e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
-    e.rows = P.blob + (uint64_t)e.b * P.blob_stride + (uint64_t)e.u * P.uc_cts;
+    e.rows = act_rows(P.blob + (uint64_t)e.b * P.blob_stride, P.E, P.uc_cts, e.u, e.rs);
     e.sstride = (uint64_t)P.B * P.E;
     e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
     if (GARBLE) {

@@ -389,7 +389,7 @@ DASH_HD void proj_thread(const ProjParams& P, uint32_t i, const AesTab& t) {
     U4* R = P.rows + (uint64_t)i * P.p;
     if (P.garbler) {
         lb_prf(A, P.wires[i], 0, Mq, P.rk, t);
-        garble_rows_n(X, A, t, P.mult, P.p, P.q, c, P.gates[i], P.phi, 0, R, 0);
+        garble_rows_n(X, A, t, P.mult, P.p, P.q, c, P.gates[i], P.phi, 0, R, 0, 1);
     } else {
         lb_dec(A, R[c], hash_tw(lb_compress(X, Mp), P.gates[i], c, 0, t), Mq);
     }

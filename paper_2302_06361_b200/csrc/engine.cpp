@@ -1758,6 +1758,13 @@ static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool va
     decode_finish(n, values, values_on_device);
 }
 
+// Position in HBM of row j of element u of an activation layer, relative to
+// the layer's first row (act_rows: 32-element blocks, row-major per block).
+static uint64_t act_row_pos(uint64_t E, uint64_t uc, uint64_t u, uint64_t j) {
+    const uint64_t blk = u >> 5, w = std::min<uint64_t>(32, E - (blk << 5));
+    return blk * 32 * uc + j * w + (u & 31);
+}
+
 // ============================================================ streamed layers
 //
 // The label-ops sweep of SURVEY.md section 8(d) is one activation layer over N
@@ -1890,9 +1897,14 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             D.mult = w.mult.as<uint32_t>();
             D.mult_stride = mult_stride;
             launch_dectable(D, g_stream);
-            if (gc_out)
-                dev::d2h(gc_out + ((uint64_t)b * N * T.cts + u0 * T.cts) * 16, w.blob.p, (size_t)n * T.cts * 16,
-                         g_stream);
+            if (gc_out) {  // chunk rows -> reference order (act_rows layout with E = n)
+                std::vector<U4> rows((size_t)n * T.cts);
+                dev::d2h(rows.data(), w.blob.p, rows.size() * 16, g_stream);
+                dev::sync(g_stream);
+                U4* dst = reinterpret_cast<U4*>(gc_out) + (uint64_t)b * N * T.cts + u0 * T.cts;
+                for (uint64_t u = 0; u < n; ++u)
+                    for (uint64_t j = 0; j < T.cts; ++j) dst[u * T.cts + j] = rows[act_row_pos(n, T.cts, u, j)];
+            }
             dev::sync(g_stream);
             const auto t1 = clk::now();
             // garble_inputs of the chunk (garble.cpp:242-263)
@@ -2000,6 +2012,28 @@ static u128 u4_to_u128(const U4& v) {
     return ((u128)v.x[3] << 96) | ((u128)v.x[2] << 64) | ((u128)v.x[1] << 32) | v.x[0];
 }
 
+// device row index of reference ciphertext index idx (one inference's GC)
+static uint64_t device_ct_index(const dashgpu_circuit& c, uint64_t idx) {
+    for (const auto& l : c.layers)
+        if (l.tape && idx >= l.ct_base && idx < l.ct_base + l.cts) {
+            const uint64_t r = idx - l.ct_base, uc = l.tape->cts;
+            return l.ct_base + act_row_pos(l.E_out, uc, r / uc, r % uc);
+        }
+    return idx;
+}
+
+// device rows of one inference -> the reference's GarbledCircuit::cts order
+static void act_rows_to_reference(const dashgpu_circuit& c, std::vector<U4>& cts) {
+    std::vector<U4> tmp;
+    for (const auto& l : c.layers) {
+        if (!l.tape || !l.cts) continue;
+        const uint64_t uc = l.tape->cts;
+        tmp.assign(cts.begin() + l.ct_base, cts.begin() + l.ct_base + l.cts);
+        for (uint64_t u = 0; u < l.E_out; ++u)
+            for (uint64_t j = 0; j < uc; ++j) cts[l.ct_base + u * uc + j] = tmp[act_row_pos(l.E_out, uc, u, j)];
+    }
+}
+
 static size_t out_bytes(const std::vector<uint8_t>& v, uint8_t* buf, size_t cap, size_t* len) {
     if (len) *len = v.size();
     if (buf && cap >= v.size()) std::memcpy(buf, v.data(), v.size());
@@ -2045,6 +2079,7 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
     U4 commit;
     dev::d2h(&commit, n.commit.as<U4>() + b, 16, g_stream);
     dev::sync(g_stream);
+    act_rows_to_reference(c, cts);
     for (int i = 0; i < c.k; ++i) w.u128v(host_compress(zero.data() + (size_t)i * LABW, c.base.primes[i]));
     w.le(c.layers.size() + 1, 8);
     for (const auto& l : c.layers) w.le(l.ct_base, 8);
@@ -2775,7 +2810,7 @@ int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint
         Network& N = *n->net;
         if (b >= N.B || index >= N.c->total_cts) throw DataError("ciphertext index out of range");
         U4 v;
-        U4* p = N.blob.as<U4>() + (uint64_t)b * N.c->total_cts + index;
+        U4* p = N.blob.as<U4>() + (uint64_t)b * N.c->total_cts + device_ct_index(*N.c, index);
         dev::d2h(&v, p, 16, g_stream);
         dev::sync(g_stream);
         uint8_t* vb = reinterpret_cast<uint8_t*>(&v);

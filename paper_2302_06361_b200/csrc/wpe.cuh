@@ -65,7 +65,7 @@ __device__ void prf_coop(LB L, uint64_t wire, uint32_t stream, uint32_t m, const
 // (cin + a) mod p with key X + a R_p and payload base + v(a) R_q.
 __device__ void garble_rows_w(LB X, LB base, LB KEY, const AesTab& t, const uint32_t* mult, uint32_t p, uint32_t q,
                               uint32_t cin, uint64_t g, const uint8_t* phi, uint32_t r, U4* R, int grr,
-                              uint32_t lane) {
+                              uint32_t rs, uint32_t lane) {
     const ModC& Mp = c_mod[p];
     const ModC& Mq = c_mod[q];
     const uint32_t* Mp0 = mult + (uint64_t)c_modslot[p] * 128u * NWMAX;
@@ -78,8 +78,8 @@ __device__ void garble_rows_w(LB X, LB base, LB KEY, const AesTab& t, const uint
         const U4 H = hash_tw(lb_compress(KEY, Mp), g, row, 0, t);
         const uint32_t v = phi ? phi[a] : (a * r) % p;
         const U4 ct = lb_enc(H, base, Mq0 + (uint64_t)v * NWMAX, nullptr, 0, Mq);
-        if (!grr) R[row] = ct;
-        else if (row != 0) R[row - 1] = ct;
+        if (!grr) R[(uint64_t)row * rs] = ct;
+        else if (row != 0) R[(uint64_t)(row - 1) * rs] = ct;
     }
     __syncwarp();
 }
@@ -114,8 +114,8 @@ __device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const 
                 }
                 __syncwarp();
             }
-            garble_rows_w(w.X, w.A, w.KEY, e.t, e.mult, p, op.qm, cin, g, phi, 0, e.rows + op.ct_off,
-                          op.kind == OP_GRR, lane);
+            garble_rows_w(w.X, w.A, w.KEY, e.t, e.mult, p, op.qm, cin, g, phi, 0,
+                          e.rows + (uint64_t)op.ct_off * e.rs, op.kind == OP_GRR, e.rs, lane);
             if (lane == 0) store_slot(e, op.out, w.A, Mq);
             __syncwarp();
             break;
@@ -127,7 +127,7 @@ __device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const 
             const ModC& Mq = c_mod[mm ? op.qm : op.pm];
             const uint32_t p = op.pm, q = mm ? op.qm : op.pm;
             const uint64_t g = e.gate0 + op.gate_off;
-            U4* R = e.rows + op.ct_off;
+            U4* R = e.rows + (uint64_t)op.ct_off * e.rs;
             if (lane == 0) {
                 load_operand(w.K, P, e, op.b, Mq);
                 load_operand(w.X, P, e, op.a, Mp);
@@ -138,7 +138,7 @@ __device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const 
             // garbler rows: key x + aR_p, payload u0 + (a r mod p) R_p
             prf_coop(w.A, e.wire0 + op.wire_off, 0, op.pm, e.rk, e.t, lane);
             const U4 u0c = lb_compress(w.A, Mp);
-            garble_rows_w(w.X, w.A, w.KEY, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0, lane);
+            garble_rows_w(w.X, w.A, w.KEY, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0, e.rs, lane);
             // evaluator rows: key y + bR_q, payload v0 - s x
             prf_coop(w.A, e.wire0 + op.wire_off + 1, 0, op.pm, e.rk, e.t, lane);
             const uint32_t fw = field_width(p);
@@ -154,7 +154,7 @@ __device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const 
                 lb_add_g(w.KEY, mult_row(e, q, b), Mq);
                 const U4 Kc = lb_compress(w.KEY, Mq);
                 LB X = w.X;
-                R[p + row] = lb_enc(hash_tw(Kc, g, row, 1, e.t), w.A, nullptr, &X, mm ? s : row, Mp);
+                R[(uint64_t)(p + row) * e.rs] = lb_enc(hash_tw(Kc, g, row, 1, e.t), w.A, nullptr, &X, mm ? s : row, Mp);
                 if (mm) {  // encrypt_short field of this row (cipher.cpp:45-60)
                     const U4 Hs = hash_tw(Kc, g, 0, 2, e.t);
                     u4_or_shl(sb, (s ^ (Hs.x[0] & fmask)) & fmask, fw * row);
@@ -163,7 +163,7 @@ __device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const 
             if (mm) {
                 for (int i = 0; i < 4; ++i)
                     for (int off = 16; off > 0; off >>= 1) sb.x[i] |= __shfl_xor_sync(0xffffffffu, sb.x[i], off);
-                if (lane == 0) R[p + q] = sb;
+                if (lane == 0) R[(uint64_t)(p + q) * e.rs] = sb;
             }
             __syncwarp();
             if (lane == 0) {

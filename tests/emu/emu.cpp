@@ -86,7 +86,7 @@ static void act_layer(const ActParams& P, bool garble) {
                 // the ops of a level are independent)
                 e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
                 e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
-                e.rows = P.blob + (uint64_t)e.b * P.blob_stride + (uint64_t)e.u * P.uc_cts;
+                e.rows = act_rows(P.blob + (uint64_t)e.b * P.blob_stride, P.E, P.uc_cts, e.u, e.rs);
                 e.sstride = (uint64_t)P.B * P.E;
                 e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
                 for (int L = 0; L < P.n_levels; ++L)
