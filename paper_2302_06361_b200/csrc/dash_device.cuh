@@ -702,6 +702,10 @@ struct ActParams {
     // projection; act_output_thread writes them before the tape runs.
     uint8_t out_kind[MAXK];    // OP_MMHALF or OP_PROJ
     uint32_t out_wire[MAXK];   // wire offset of that gadget within the element
+    // compressed u0, v0 of the output mm half gates ([B][E][k][2], garbling):
+    // act_output_thread draws them once, the tape's MMHALF (cst = lane + 1)
+    // reads them instead of drawing the same PRF labels again
+    U4* mmlab;
 };
 
 // Work map of a multi-layer launch: layer li owns items [base[li], base[li+1]),
@@ -869,13 +873,22 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const uint32_t cx = lb_color(e.X, Mp);
             const uint32_t r = mm ? cx : cy;
             // garbler rows: key x + aR_p, payload u0 + (a r mod p) R_p, slot 0
-            prf_n(e.A, e.wire0 + op.wire_off, 0, op.pm, e.rk, e.t);
-            const U4 u0c = lb_compress(e.A, Mp);
+            const U4* ml = (op.cst && P.mmlab) ? P.mmlab + (((uint64_t)e.b * P.E + e.u) * P.k + (op.cst - 1)) * 2
+                                               : nullptr;
+            U4 u0c;
+            if (ml) {
+                u0c = ml[0];
+                lb_decompress(e.A, u0c, Mp);
+            } else {
+                prf_n(e.A, e.wire0 + op.wire_off, 0, op.pm, e.rk, e.t);
+                u0c = lb_compress(e.A, Mp);
+            }
             // X is the running key here (K only holds the Z_2-sized y operand)
             garble_rows_n(e.X, e.A, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0, e.rs);
             // evaluator rows: key y + bR_q, payload v0 - s x, slot 1
             load_operand(e.X, P, e, op.a, Mp);
-            prf_n(e.A, e.wire0 + op.wire_off + 1, 0, op.pm, e.rk, e.t);
+            if (ml) lb_decompress(e.A, ml[1], Mp);
+            else prf_n(e.A, e.wire0 + op.wire_off + 1, 0, op.pm, e.rk, e.t);
             load_operand(e.K, P, e, op.b, Mq);
             const uint32_t* Rq = mult_row(e, q, 1);
             const uint32_t fw = field_width(p);
@@ -934,6 +947,11 @@ DASH_HD void act_output_thread(const ActParams& P, uint32_t b, uint32_t u, int i
     lb_prf(A, w, 0, M, rk, t);
     if (P.out_kind[i] == OP_MMHALF) {  // out = v0 - u0, v0 drawn at the next wire id
         lb_prf(T, w + 1, 0, M, rk, t);
+        if (P.mmlab) {
+            U4* ml = P.mmlab + (((uint64_t)b * P.E + u) * P.k + i) * 2;
+            ml[0] = lb_compress(A, M);
+            ml[1] = lb_compress(T, M);
+        }
         lb_sub(T, A, M);
         lb_store_rows(T, P.out[i] + ((uint64_t)b * M.nw) * P.E + u, P.E, M);
     } else {

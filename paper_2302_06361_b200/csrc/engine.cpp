@@ -867,6 +867,15 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
             tp.out_kind[o.cst] = (uint8_t)prod.kind;
             tp.out_wire[o.cst] = (uint32_t)prod.wire;
         }
+    // output mm half gates carry their lane (cst = lane + 1): the garbling tape
+    // reads their u0 / v0 from act_output_thread instead of drawing them again
+    for (const auto& o : r.ops)
+        if (o.kind == OP_OUTPUT && r.ops[r.producer[o.a]].kind == OP_MMHALF) {
+            const auto& prod = r.ops[r.producer[o.a]];
+            for (auto* ops : {&tp.ops, &tp.lv_ops})
+                for (auto& d : *ops)
+                    if (d.kind == OP_MMHALF && d.wire_off == (uint32_t)prod.wire) d.cst = (uint16_t)(o.cst + 1);
+        }
     tp.cts = r.cts;
     for (const auto& o : r.ops)
         tp.eval_rows += o.kind == OP_PROJ || o.kind == OP_GRR ? 1 : o.kind == OP_HALF ? 2 : o.kind == OP_MMHALF ? 3 : 0;
@@ -1238,7 +1247,7 @@ struct Network {
     dashgpu_circuit* c = nullptr;
     uint32_t B = 0, cap = 0;
     std::vector<uint8_t> seeds;
-    DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err, slots;
+    DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err, slots, mmlab;
     Lanes base;  // encoding info: input base labels
     // per-layer output planes (garbler: base labels, evaluator: active labels);
     // at[j + 1] = output of layer j, at[0] = the input; Flatten aliases its input
@@ -1265,6 +1274,7 @@ struct Network {
         return q;
     }
     size_t slot_used = 0;  // U4 entries of `slots` handed out to garbled layers
+    size_t mm_used = 0;    // U4 entries of `mmlab` handed out to garbled layers
     uint64_t mult_stride = 0;
     uint32_t sum_p = 0;
 };
@@ -1462,6 +1472,8 @@ static void run_layer(Network& n, size_t li, const HLayer& l, bool garbler, cons
         for (int i = 0; i < k; ++i) P.in[i] = in.lane[i]->as<uint32_t>();
         P.slots = n.slots.as<U4>() + n.slot_used;
         n.slot_used += slot_words;
+        P.mmlab = n.mmlab.as<U4>() + n.mm_used;
+        n.mm_used += (size_t)n.B * l.E_out * k * 2;
         uint16_t primes[MAXK];
         fill_primes(c.base, primes);
         launch_act_outputs(P, primes, g_stream);
@@ -1511,6 +1523,10 @@ static void network_reserve(Network& n, uint32_t B) {
             ++nact;
         }
     n.slots.ensure(std::max<size_t>(std::max(slot_total, slot_eval), 1) * 16);
+    size_t mm_total = 0;
+    for (const auto& l : c.layers)
+        if (l.tape) mm_total += (size_t)B * l.E_out * k * 2;
+    n.mmlab.ensure(std::max<size_t>(mm_total, 1) * 16);
     n.nact = nact;
     n.act_cap = nact + c.layers.size();
     n.act_dev.ensure(n.act_cap * sizeof(ActParams));
@@ -1592,6 +1608,7 @@ static void garble_setup(Network& n, const uint8_t* seeds, uint32_t B, bool seed
     launch_setup(S, g_stream);
     n.act_host.clear();
     n.slot_used = 0;
+    n.mm_used = 0;
 }
 
 // decoding tables (garble.cpp:208-231) from the final output base labels
@@ -1621,6 +1638,7 @@ static void garble_act_flush(Network& n) {
     launch_act_multi(n.act_dev.as<ActParams>(), n.act_host.data(), (int)n.act_host.size(), true, g_stream, n.sched());
     n.act_host.clear();
     n.slot_used = 0;
+    n.mm_used = 0;
 }
 
 static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
@@ -1776,7 +1794,7 @@ static uint64_t act_row_pos(uint64_t E, uint64_t uc, uint64_t u, uint64_t j) {
 // ciphertext u*uc.cts inside the layer (layer.cpp:531-541).  Every chunk
 // buffer is C elements wide; only the id bases move.
 struct StreamWS {
-    DevBuf rk, seeds, mult, zero, Rb, commit, blob, slots, dec, vals, resid, err, actp, qctr, qflags;
+    DevBuf rk, seeds, mult, zero, Rb, commit, blob, slots, dec, vals, resid, err, actp, qctr, qflags, mmlab;
     Lanes base, in, gout, eout;
     uint64_t C = 0;
 };
@@ -1812,6 +1830,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
     w.resid.ensure((size_t)C * k);
     w.err.ensure(16);
     w.actp.ensure(sizeof(ActParams));
+    w.mmlab.ensure((size_t)C * k * 2 * 16);
     w.qctr.ensure(64);
     w.qflags.ensure(((C + 31) / 32 + 1) * 4);
     Sched q;
@@ -1880,6 +1899,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             P.mult = w.mult.as<uint32_t>();
             P.mult_stride = mult_stride;
             P.slots = w.slots.as<U4>();
+            P.mmlab = w.mmlab.as<U4>();
             uint16_t primes[MAXK];
             fill_primes(c.base, primes);
             launch_act_outputs(P, primes, g_stream);

@@ -136,11 +136,23 @@ __device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const 
             const uint32_t cy = lb_color(w.K, Mq), cx = lb_color(w.X, Mp);
             const uint32_t r = mm ? cx : cy;
             // garbler rows: key x + aR_p, payload u0 + (a r mod p) R_p
-            prf_coop(w.A, e.wire0 + op.wire_off, 0, op.pm, e.rk, e.t, lane);
+            const U4* ml = (op.cst && P.mmlab) ? P.mmlab + (((uint64_t)e.b * P.E + e.u) * P.k + (op.cst - 1)) * 2
+                                               : nullptr;
+            if (ml) {
+                if (lane == 0) lb_decompress(w.A, ml[0], Mp);
+                __syncwarp();
+            } else {
+                prf_coop(w.A, e.wire0 + op.wire_off, 0, op.pm, e.rk, e.t, lane);
+            }
             const U4 u0c = lb_compress(w.A, Mp);
             garble_rows_w(w.X, w.A, w.KEY, e.t, e.mult, p, p, cx, g, nullptr, r, R, 0, e.rs, lane);
             // evaluator rows: key y + bR_q, payload v0 - s x
-            prf_coop(w.A, e.wire0 + op.wire_off + 1, 0, op.pm, e.rk, e.t, lane);
+            if (ml) {
+                if (lane == 0) lb_decompress(w.A, ml[1], Mp);
+                __syncwarp();
+            } else {
+                prf_coop(w.A, e.wire0 + op.wire_off + 1, 0, op.pm, e.rk, e.t, lane);
+            }
             const uint32_t fw = field_width(p);
             const uint32_t fmask = (1u << fw) - 1u;
             U4 sb;
