@@ -9,9 +9,9 @@
 //   hash / cipher    src/cipher.cpp:8-69, include/dash/cipher.hpp:13-26,62-66
 //   gadgets          include/dash/gadgets.hpp:127-358
 //
-// Design: labels of non-power-of-two moduli live in registers
-// as packed u8 digits (four per u32 word); power-of-two moduli use the packed
-// bit form, which *is* their compressed value.  Compression works word by
+// Design: labels of non-power-of-two moduli live in per-lane
+// shared-memory buffers as packed u8 digits (four per u32 word); power-of-two
+// moduli use the packed bit form, which *is* their compressed value.  Compression works word by
 // word (Horner in base m^4); decompression divides the 128-bit value by
 // D = m^(4W) <= 2^31 with a precomputed 64-bit reciprocal, then splits each
 // chunk into digits with 32-bit magic multiplies.  Every modulus-dependent

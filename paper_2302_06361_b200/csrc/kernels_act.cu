@@ -1,8 +1,12 @@
 // Activation-layer kernels (ReLU / SignAct gadget tapes), garble and eval.
-// One thread = one (inference, element); a warp = 32 consecutive elements of
-// one inference, so every tape branch, modulus and offset load is warp-uniform.
-// CTA = 8 warps; shared memory = replicated AES T-table (32 KB) + per-lane
-// compressed label slots.
+// act_kernel: one thread = one (inference, element); a warp = 32 consecutive
+// elements of one inference, so every tape branch, modulus and offset load is
+// warp-uniform.  One persistent CTA per SM (28 warps garbling, 24 evaluating);
+// shared memory = the replicated AES T-tables (64 KB) + per-lane label
+// buffers.  Garbling work items are (tape chunk, layer, inference, block).
+// act_wpe_kernel / act_wpe_eval_kernel: one warp per element for small
+// launches (wpe.cuh, level-scheduled evaluation tape).  act_out_kernel: the
+// garbler's output labels of a layer (pure PRF functions).
 #include "dash_common.hpp"
 
 namespace dashgpu {
