@@ -64,6 +64,9 @@ typedef struct dashgpu_circuit_info {
     uint32_t max_slots;
 } dashgpu_circuit_info;
 
+/* dashgpu_infer enqueues a whole sub-batch without host syncs, so it reports
+ * the sub-batch wall time in ms_garble (the other phase fields stay 0);
+ * dashgpu_infer_stream fills every phase. */
 typedef struct dashgpu_timing {
     double ms_garble, ms_encode, ms_evaluate, ms_decode, ms_total;
     uint64_t h2d_bytes, d2h_bytes;

@@ -226,6 +226,25 @@ DASH_HD void setup_labels_thread(const SetupParams& S, uint32_t b, uint32_t e, i
     }
 }
 
+// AES-128 key schedule of a 16-byte seed (aes.cpp:32-46) on the device, so a
+// batch whose seeds are already in HBM needs no host round trip.  S-box =
+// byte 1 of T0 (T0[x] = (2S, S, S, 3S) little-endian).
+DASH_HD void expand_thread(const uint8_t* key, uint32_t* rk, const uint32_t* T0) {
+    const uint8_t rcon[10] = {1, 2, 4, 8, 16, 32, 64, 128, 0x1b, 0x36};
+    for (int i = 0; i < 4; ++i)
+        rk[i] = (uint32_t)key[4 * i] | ((uint32_t)key[4 * i + 1] << 8) | ((uint32_t)key[4 * i + 2] << 16) |
+                ((uint32_t)key[4 * i + 3] << 24);
+    for (int i = 4; i < 44; ++i) {
+        uint32_t t = rk[i - 1];
+        if (i % 4 == 0) {
+            auto sb = [&](uint32_t x) { return (T0[x & 0xffu] >> 8) & 0xffu; };
+            // RotWord + SubWord + Rcon on the little-endian word
+            t = (sb(t >> 8) ^ rcon[i / 4 - 1]) | (sb(t >> 16) << 8) | (sb(t >> 24) << 16) | (sb(t) << 24);
+        }
+        rk[i] = rk[i - 4] ^ t;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // garble_inputs (garble.cpp:242-263): label = base + (enc(v) mod p) R_p
 struct EncodeParams {

@@ -1246,7 +1246,6 @@ struct Lanes {
 struct Network {
     dashgpu_circuit* c = nullptr;
     uint32_t B = 0, cap = 0;
-    std::vector<uint8_t> seeds;
     DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err, slots, mmlab;
     Lanes base;  // encoding info: input base labels
     // per-layer output planes (garbler: base labels, evaluator: active labels);
@@ -1573,20 +1572,15 @@ static void garble_setup(Network& n, const uint8_t* seeds, uint32_t B, bool seed
     const int k = c.k;
     upload_circuit(c);
     network_reserve(n, B);
-    n.seeds.assign(16 * (size_t)B, 0);
-    std::vector<uint32_t> rk((size_t)B * 44);
+    // seeds -> device, AES key schedules expanded on the device (no host
+    // round trip when the seeds are already in HBM)
     if (seeds_on_device) {
-        dev::d2h(n.seeds.data(), seeds, 16 * (size_t)B, g_stream);
-        dev::sync(g_stream);
+        dev::d2d(n.seeds_d.p, seeds, 16 * (size_t)B, g_stream);
     } else {
-        std::memcpy(n.seeds.data(), seeds, 16 * (size_t)B);
+        std::memcpy(n.rk_pin.p, seeds, 16 * (size_t)B);
+        dev::h2d(n.seeds_d.p, n.rk_pin.p, 16 * (size_t)B, g_stream);
     }
-    for (uint32_t b = 0; b < B; ++b) aes_expand_host(n.seeds.data() + 16 * (size_t)b, rk.data() + 44 * (size_t)b);
-    std::memcpy(n.rk_pin.p, rk.data(), rk.size() * 4);
-    dev::h2d(n.rk.p, n.rk_pin.p, rk.size() * 4, g_stream);
-    uint8_t* seeds_pin = n.rk_pin.as<uint8_t>() + (size_t)B * 44 * 4;
-    std::memcpy(seeds_pin, n.seeds.data(), n.seeds.size());
-    dev::h2d(n.seeds_d.p, seeds_pin, n.seeds.size(), g_stream);
+    launch_expand(n.seeds_d.as<uint8_t>(), n.rk.as<uint32_t>(), B, g_stream);
     // zero / Rb rows are addressed per lane with stride LABW between inferences
     // in linear_thread; store them lane-major: [k][B][LABW]
     SetupParams S;
@@ -2885,23 +2879,19 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
         Bundle& in = *n.bin;
         Bundle& out = *n.bout;
         for (uint32_t b0 = 0; b0 < batch; b0 += chunk) {
+            // one host sync per sub-batch: everything up to the decoded
+            // residues is enqueued back to back (range / authenticity flags
+            // are checked after the sync)
             const uint32_t B = std::min(chunk, batch - b0);
             const auto a = clk::now();
             garble_into(n, seeds + (size_t)16 * b0, B, on_device != 0);
-            dev::sync(g_stream);
-            const auto b = clk::now();
-            encode_into(n, inputs + (size_t)b0 * c->n_in, on_device != 0, in);
-            const auto d = clk::now();
+            encode_enqueue(n, inputs + (size_t)b0 * c->n_in, on_device != 0, in);
             evaluate_into(n, in, out);
+            decode_enqueue(n, out);
             dev::sync(g_stream);
-            const auto e = clk::now();
-            decode_into(n, out, outputs + (size_t)b0 * c->n_out, on_device != 0);
-            dev::sync(g_stream);
-            const auto f = clk::now();
-            tm.ms_garble += std::chrono::duration<double, std::milli>(b - a).count();
-            tm.ms_encode += std::chrono::duration<double, std::milli>(d - b).count();
-            tm.ms_evaluate += std::chrono::duration<double, std::milli>(e - d).count();
-            tm.ms_decode += std::chrono::duration<double, std::milli>(f - e).count();
+            encode_finish(n);
+            decode_finish(n, outputs + (size_t)b0 * c->n_out, on_device != 0);
+            tm.ms_garble += std::chrono::duration<double, std::milli>(clk::now() - a).count();
             tm.sub_batches += 1;
         }
         if (!on_device) {

@@ -186,6 +186,11 @@ __global__ void __launch_bounds__(128) proj_kernel(const __grid_constant__ ProjP
     proj_thread(P, i, make_tab(nullptr, threadIdx.x & 31u));
 }
 
+__global__ void __launch_bounds__(128) expand_kernel(const uint8_t* seeds, uint32_t* rk, uint32_t B) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) expand_thread(seeds + (uint64_t)b * 16, rk + (uint64_t)b * 44, g_T0);
+}
+
 __global__ void __launch_bounds__(128) setup_offsets_kernel(SetupParams Sp) {
     fill_T(g_T0);
     const uint32_t si = blockIdx.x;  // modulus slot; thread = multiple x < 128
@@ -434,6 +439,13 @@ void launch_proj(const ProjParams& P, void* st) {
     ProfScope ps(K_MISC, S(st));
     ck(cudaFuncSetAttribute(proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
     proj_kernel<<<cdiv(P.n, 128), 128, kTabBytes, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_expand(const uint8_t* seeds, uint32_t* rk, uint32_t B, void* st) {
+    if (!B) return;
+    ProfScope ps(K_SETUP, S(st));
+    expand_kernel<<<cdiv(B, 128), 128, 0, S(st)>>>(seeds, rk, B);
     dev::check();
 }
 

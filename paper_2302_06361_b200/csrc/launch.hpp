@@ -85,6 +85,7 @@ void launch_private(const PrivParams& P, void* stream, const Sched& q);
 void launch_pad_add(const PadAddParams& P, void* stream);  // extension layers
 void launch_proj(const ProjParams& P, void* stream);        // t_proj primitive
 void launch_setup(const SetupParams& S, void* stream);
+void launch_expand(const uint8_t* seeds, uint32_t* rk, uint32_t B, void* stream);  // device AES key schedules
 void launch_encode(const EncodeParams& P, void* stream);
 void launch_dectable(const DecodeParams& P, void* stream);
 void launch_decode(const DecodeParams& P, void* stream);

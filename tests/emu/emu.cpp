@@ -23,6 +23,7 @@ uint16_t c_modslot[MAXMOD + 1];
 namespace dashgpu {
 
 static uint32_t g_T[256 * 64];
+static uint32_t g_T0plain[256];
 
 static AesTab tab() { return make_tab(g_T, 0); }
 
@@ -48,6 +49,7 @@ void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* m
     std::memcpy(c_mod, mods, sizeof(ModC) * (MAXMOD + 1));
     std::memcpy(c_pi_rk, pi_rk, sizeof(uint32_t) * 44);
     std::memcpy(c_modslot, modslot, sizeof(uint16_t) * (MAXMOD + 1));
+    std::memcpy(g_T0plain, T0, sizeof g_T0plain);
     for (int i = 0; i < 256 * 64; ++i) {
         const uint32_t v = T0[i >> 6];
         g_T[i] = (i & 32) ? ((v << 16) | (v >> 16)) : v;
@@ -132,6 +134,10 @@ void launch_pad_add(const PadAddParams& P, void*) {
     for (int64_t b = 0; b < (int64_t)P.B; ++b)
         for (int64_t wi = 0; wi < (int64_t)P.wbase[P.k]; ++wi)
             for (uint32_t u = 0; u < P.E_out; ++u) pad_add_thread(P, (uint32_t)b, (uint32_t)wi, u);
+}
+
+void launch_expand(const uint8_t* seeds, uint32_t* rk, uint32_t B, void*) {
+    for (uint32_t b = 0; b < B; ++b) expand_thread(seeds + (uint64_t)b * 16, rk + (uint64_t)b * 44, g_T0plain);
 }
 
 void launch_proj(const ProjParams& P, void*) {
