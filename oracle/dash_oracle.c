@@ -2004,10 +2004,14 @@ double orc_bench_infer(const orc_circuit* c, int n, const uint8_t* seeds, const 
     struct timespec t0, t1;
     clock_gettime(CLOCK_MONOTONIC, &t0);
     int err = 0;
+    /* fewer inferences than threads: one at a time, OpenMP inside the layers
+     * (the reference's own intra-layer mode); else one inference per thread */
+    const int outer = n >= threads ? threads : 1;
 #ifdef _OPENMP
     omp_set_max_active_levels(1);
+    if (outer == 1) omp_set_num_threads(threads);
 #endif
-#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(outer)
     for (int b = 0; b < n; ++b) {
         orc_net* net = NULL;
         orc_bundle *in = NULL, *out = NULL;
