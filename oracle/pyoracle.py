@@ -399,6 +399,8 @@ class RefLib(_Base):
     def circuit(self, c):
         desc = c.to_desc()
         h = self.lib.ref_circuit_from_desc(ctypes.byref(desc))
+        if not h:  # e.g. Pad2d / Add extensions the reference does not have
+            raise CheckerError(3, self.err())
         return _CircuitHandle(self, vp(h), c)
 
     def model(self, name: str, seed: int, k: int, priv: bool = False):

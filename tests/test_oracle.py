@@ -165,3 +165,15 @@ def test_oracle_matches_reference_randomized(oracle):
         msg = ref.prf_label(seed, w + 1, q)
         g, row, slot = rnd.getrandbits(48), rnd.randrange(1 << 16), rnd.randrange(3)
         assert oracle.encrypt_label(m, d, g, row, slot, q, msg) == ref.encrypt_label(m, d, g, row, slot, q, msg)
+
+
+def test_reference_harness_rejects_extension_circuits():
+    # Pad2d / Add / DAG inputs exist only in this repo (dash_circuit_desc.h):
+    # the compiled reference must refuse them, not misread them
+    import pyoracle
+    from helpers import models
+
+    if not pyoracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    with pytest.raises(pyoracle.CheckerError):
+        pyoracle.RefLib().circuit(models.build("resnet_tiny", 2001, 8))
