@@ -332,7 +332,9 @@ int prof_read(double* ms, uint64_t* n, int maxk) {
 
 }  // namespace dev
 
-void make_weight_map(TcLinear& T) {
+// 2-D u8 tensor map, K-major rows, 128-byte swizzle (tc_linear.cuh operands)
+static void encode_u8_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t rows, uint64_t stride,
+                         uint32_t box_inner, uint32_t box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -340,15 +342,19 @@ void make_weight_map(TcLinear& T) {
            "cuTensorMapEncodeTiled entry point");
         if (q != cudaDriverEntryPointSuccess || !encode) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
     }
-    CUtensorMap m;
-    const cuuint64_t dims[2] = {T.Kpad, (cuuint64_t)T.k * T.Npad};
-    const cuuint64_t strides[1] = {T.Kpad};
-    const cuuint32_t box[2] = {(cuuint32_t)tc::BKB, T.BN};
+    const cuuint64_t dims[2] = {inner, rows};
+    const cuuint64_t strides[1] = {stride};
+    const cuuint32_t box[2] = {box_inner, box_rows};
     const cuuint32_t es[2] = {1, 1};
-    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)T.wexp, dims, strides, box, es,
+    const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+void make_weight_map(TcLinear& T) {
+    CUtensorMap m;
+    encode_u8_2d(&m, T.wexp, T.Kpad, (uint64_t)T.k * T.Npad, T.Kpad, (uint32_t)tc::BKB, T.BN);
     static_assert(sizeof(CUtensorMap) == sizeof(T.tmap), "tensor map size");
     memcpy(T.tmap, &m, sizeof m);
 }
@@ -399,11 +405,20 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
         l.wrow = (uint32_t)i * T.Npad;
         tiles += cdiv(l.rows, tc::BM) * P.tiles_n;
     }
+    // dense layer over 16-byte-aligned planes: the A tiles are plain 2-D boxes
+    // of the [B*nw][4*E_in] digit-byte matrix, loaded by TMA instead of gathered
+    tc::TcAMaps amaps;
+    memset(&amaps, 0, sizeof amaps);
+    P.a_tma = !L0.conv && (L0.E_in % 4) == 0;
+    if (P.a_tma)
+        for (int i = 0; i < n; ++i)
+            encode_u8_2d(&amaps.m[i], Ls[i].in, (uint64_t)4 * L0.E_in, (uint64_t)Ls[i].B * Ls[i].nw,
+                         (uint64_t)4 * L0.E_in, (uint32_t)tc::BKB, (uint32_t)tc::BM);
     const size_t smem = tc::smem_bytes(T.BN);
     ck(cudaFuncSetAttribute(tc::tc_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
     CUtensorMap map;
     memcpy(&map, T.tmap, sizeof map);
-    tc::tc_linear_kernel<<<tiles, tc::kThreads, smem, S(st)>>>(map, P);
+    tc::tc_linear_kernel<<<tiles, tc::kThreads, smem, S(st)>>>(map, P, amaps);
     dev::check();
 }
 

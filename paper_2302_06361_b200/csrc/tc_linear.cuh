@@ -59,7 +59,14 @@ struct TcParams {
     uint32_t kblocks;     // K stages (KWS window elements each)
     uint32_t P, OW, s, W, E_in, M, nout, tiles_n, BN, stages, zstride;
     int garbler;
+    int a_tma;            // dense layer whose planes are TMA-able: A tiles by TMA, no gather
     const int32_t* koff;  // [kblocks * KWS] element offset of window index i, -1 = padding
+};
+
+// A operand maps of a dense layer (one per CRT lane: the digit plane viewed
+// as a [rows = B*nw][4*E_in] byte matrix, K-major, 128-byte swizzle)
+struct TcAMaps {
+    CUtensorMap m[MAXK];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -128,7 +135,8 @@ __device__ __forceinline__ uint32_t modp(uint32_t x, uint32_t p, uint32_t mag, u
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_linear_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ TcParams P) {
+    tc_linear_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ TcParams P,
+                     const __grid_constant__ TcAMaps amaps) {
     extern __shared__ uint8_t tc_smem_raw[];
     uint8_t* base = (uint8_t*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -150,12 +158,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (tid == 0) {
         for (uint32_t s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, 129);
+            mbar_init(full0 + 8 * s, P.a_tma ? 1 : 129);
             mbar_init(empty0 + 8 * s, 1);
         }
         mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+        if (P.a_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&amaps.m[li]) : "memory");
     }
     if (warp == 4) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -168,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tslot;
 
     if (warp < 4) {
+      if (!P.a_tma) {
         // ---------------- producer: im2col gather of A into swizzled smem
         const uint32_t q = lane & 3, rsub = lane >> 2;
         uint64_t rb[4];
@@ -204,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(full0 + 8 * s);
         }
+      }
 
         // ---------------- epilogue: TMEM -> mod p -> packed digit words
         mbar_wait(done, 0);
@@ -240,11 +251,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (lane == 0) {
         // ---------------- weights by TMA + MMA issue (one thread)
         const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-        const uint32_t wrow = L.wrow + nt * BN, tx = BN * BKB;
+        const uint32_t wrow = L.wrow + nt * BN, tx = BN * BKB + (P.a_tma ? kAStage : 0u);
+        const CUtensorMap* amap = &amaps.m[li];
         const uint32_t pre = P.kblocks < S ? P.kblocks : S;
         for (uint32_t kb = 0; kb < pre; ++kb) {
             mbar_expect_tx(full0 + 8 * kb, tx);
             tma_load_2d(sB + kb * BN * BKB, &wmap, full0 + 8 * kb, (int)(kb * BKB), (int)wrow);
+            if (P.a_tma) tma_load_2d(sA + kb * kAStage, amap, full0 + 8 * kb, (int)(kb * BKB), (int)(mt * BM));
         }
         for (uint32_t kb = 0; kb < P.kblocks; ++kb) {
             const uint32_t s = kb % S, round = kb / S;
@@ -259,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(empty0 + 8 * s, round & 1);
                 mbar_expect_tx(full0 + 8 * s, tx);
                 tma_load_2d(bsm, &wmap, full0 + 8 * s, (int)((kb + S) * BKB), (int)wrow);
+                if (P.a_tma) tma_load_2d(a, amap, full0 + 8 * s, (int)((kb + S) * BKB), (int)(mt * BM));
             }
         }
         mma_commit(done);
