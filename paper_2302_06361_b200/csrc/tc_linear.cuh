@@ -228,15 +228,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t rw = P.garbler ? L.R[(uint64_t)b * P.zstride + w] : 0u;
         const uint32_t mask = (4 * w + 4 > L.n) ? (0xffffffffu >> (8 * (4 * w + 4 - L.n))) : 0xffffffffu;
         uint32_t* orow = L.out + (uint64_t)bw * P.M + pos;
+        // dense rows: the 4 output words of a column chunk are adjacent
+        const bool vec = P.P == 1 && (P.M & 3) == 0;
         for (uint32_t cc = 0; cc < BN / 16; ++cc) {
             uint32_t v[16];
             tmem_ld16(tmem + ((warp * 32) << 16) + cc * 16, v);
+            uint32_t o4[4];
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
                 const uint32_t oc = nt * (BN / 4) + cc * 4 + g;
-                if (!valid || oc >= P.nout) continue;
-                const uint32_t z = L.zt[oc];
-                const uint32_t bb = P.garbler ? L.bres[oc] : 0u;
+                const uint32_t oci = oc < P.nout ? oc : 0;
+                const uint32_t z = L.zt[oci];
+                const uint32_t bb = P.garbler ? L.bres[oci] : 0u;
                 const uint32_t nb = bb ? L.p - bb : 0u;
                 uint32_t o = 0;
 #pragma unroll
@@ -245,7 +248,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t t1 = s0 + z * ((zw >> (8 * j)) & 0xffu) + nb * ((rw >> (8 * j)) & 0xffu);
                     o |= modp(t1, L.p, L.mag, L.sh) << (8 * j);
                 }
-                orow[(uint64_t)oc * P.P] = o & mask;
+                o4[g] = o & mask;
+            }
+            if (!valid) continue;
+            const uint32_t oc0 = nt * (BN / 4) + cc * 4;
+            if (vec && oc0 + 4 <= P.nout) {
+                asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(orow + oc0), "r"(o4[0]), "r"(o4[1]),
+                             "r"(o4[2]), "r"(o4[3])
+                             : "memory");
+            } else {
+#pragma unroll
+                for (int g = 0; g < 4; ++g)
+                    if (oc0 + g < P.nout) orow[(uint64_t)(oc0 + g) * P.P] = o4[g];
             }
         }
     } else if (lane == 0) {
