@@ -305,7 +305,12 @@ struct DecodeParams {
     uint64_t mult_stride;
     uint8_t* residues;         // [B][n_out][k]
     int* err;
-};
+    // crt_reconstruct + decode_signed on the device (crt.cpp:63-101):
+    // values[b][e] = signed(sum_i coeff_i r_i mod P); coeff_i = (P/p_i) * inv
+    int64_t* values;           // [B][n_out] (nullptr: residues only)
+    uint64_t coeff_lo[MAXK], coeff_hi[MAXK];  // coeff_i mod P
+    uint64_t P_lo, P_hi;
+}; 
 
 DASH_HD void dectable_thread(const DecodeParams& P, uint32_t b, uint32_t e, int i) {
     const uint32_t p = P.primes[i];
@@ -323,7 +328,17 @@ DASH_HD void dectable_thread(const DecodeParams& P, uint32_t b, uint32_t e, int 
     }
 }
 
+// error flag, the most severe code wins (AuthenticityError over DataError)
+DASH_HD void flag_err(int* err, int code) {
+#if defined(__CUDA_ARCH__)
+    atomicMax(err, code);
+#else
+    if (*err < code) *err = code;
+#endif
+}
+
 DASH_HD void decode_thread(const DecodeParams& P, uint32_t b, uint32_t e) {
+    uint8_t res[MAXK];
     uint32_t buf[NWMAX];
     const LB L{buf, 1};
     for (int i = 0; i < P.k; ++i) {
@@ -339,11 +354,37 @@ DASH_HD void decode_thread(const DecodeParams& P, uint32_t b, uint32_t e) {
                 found = (int)v;
         }
         if (found < 0) {
-            *P.err = ST_AUTH;
+            flag_err(P.err, ST_AUTH);
             found = 0;
         }
         P.residues[((uint64_t)b * P.n_out + e) * P.k + i] = (uint8_t)found;
+        res[i] = (uint8_t)found;
     }
+    if (!P.values) return;
+    const u128 Pm = ((u128)P.P_hi << 64) | P.P_lo;
+    u128 acc = 0;
+    for (int i = 0; i < P.k; ++i) {
+        const u128 c = ((u128)P.coeff_hi[i] << 64) | P.coeff_lo[i];  // < P
+        acc += c * res[i] % Pm;  // c * r < 2^128 for the CRT bases (P < 2^66, r < 64)
+        if (acc >= Pm) acc -= Pm;
+    }
+    const u128 half_up = (Pm + 1) / 2;
+    int64_t v;
+    if (acc < half_up) {
+        if (acc > (u128)INT64_MAX) {
+            flag_err(P.err, ST_DATA);
+            return;
+        }
+        v = (int64_t)acc;
+    } else {
+        const u128 mag = Pm - acc;
+        if (mag > (u128)INT64_MAX) {
+            flag_err(P.err, ST_DATA);
+            return;
+        }
+        v = -(int64_t)mag;
+    }
+    P.values[(uint64_t)b * P.n_out + e] = v;
 }
 
 // ---------------------------------------------------------------------------

@@ -1246,7 +1246,7 @@ struct Lanes {
 struct Network {
     dashgpu_circuit* c = nullptr;
     uint32_t B = 0, cap = 0;
-    DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err, slots, mmlab;
+    DevBuf seeds_d, rk, mult, zero, Rb, commit, blob, dec, vals, resid, err, slots, mmlab, outv;
     Lanes base;  // encoding info: input base labels
     // per-layer output planes (garbler: base labels, evaluator: active labels);
     // at[j + 1] = output of layer j, at[0] = the input; Flatten aliases its input
@@ -1531,7 +1531,8 @@ static void network_reserve(Network& n, uint32_t B) {
     n.act_dev.ensure(n.act_cap * sizeof(ActParams));
     n.act_pin.ensure(n.act_cap * sizeof(ActParams));
     n.rk_pin.ensure((size_t)B * (44 * 4 + 16));
-    n.res_pin.ensure((size_t)B * c.n_out * k + 16);
+    n.res_pin.ensure((size_t)B * c.n_out * 8 + 16);
+    n.outv.ensure((size_t)B * c.n_out * 8 + 16);
     n.err_pin.ensure(64);
     size_t items = 0;  // work items per tape chunk of the garbling launch
     for (const auto& l : c.layers)
@@ -1704,30 +1705,24 @@ static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
                  (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_out * 4, g_stream);
 }
 
-// crt_reconstruct + decode_signed (crt.cpp:63-101) of `count` residue tuples
-static void crt_decode(const dashgpu_circuit& c, const uint8_t* res, uint64_t count, int64_t* dst) {
-    const int k = c.k;
-    const u128 half_up = (c.base.P + 1) / 2;
-    for (uint64_t e = 0; e < count; ++e) {
-        u128 acc = 0;
-        for (int i = 0; i < k; ++i) acc += c.base.coeffs[i] % c.base.P * res[e * k + i] % c.base.P;
-        acc %= c.base.P;
-        int64_t v;
-        if (acc < half_up) {
-            if (acc > (u128)INT64_MAX) throw DataError("decode_signed: value exceeds 64-bit signed range");
-            v = (int64_t)acc;
-        } else {
-            const u128 mag = c.base.P - acc;
-            if (mag > (u128)INT64_MAX) throw DataError("decode_signed: value exceeds 64-bit signed range");
-            v = -(int64_t)mag;
-        }
-        dst[e] = v;
-    }
-}
 
 // decode_outputs (garble.cpp:314-343): table lookup on the device (enqueued,
 // residues + miss flag land in pinned memory), CRT reconstruction on the host
-static void decode_enqueue(Network& n, const Bundle& outb) {
+// CRT coefficients of the base, reduced mod P, as the device decode wants them
+static void fill_crt(const Crt& base, DecodeParams& D) {
+    for (int i = 0; i < base.k; ++i) {
+        const u128 cf = base.coeffs[i] % base.P;
+        D.coeff_lo[i] = (uint64_t)cf;
+        D.coeff_hi[i] = (uint64_t)(cf >> 64);
+    }
+    D.P_lo = (uint64_t)base.P;
+    D.P_hi = (uint64_t)(base.P >> 64);
+}
+
+// decode_outputs (garble.cpp:314-343) with crt_reconstruct / decode_signed
+// (crt.cpp:63-101) on the device: values go straight to dev_values (device
+// outputs) or to the network's buffer and a pinned host copy.
+static void decode_enqueue(Network& n, const Bundle& outb, int64_t* dev_values = nullptr) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
     if (!outb.output || outb.B != n.B) throw DataError("output lane count mismatch");
@@ -1742,30 +1737,24 @@ static void decode_enqueue(Network& n, const Bundle& outb) {
     D.table = n.dec.as<U4>();
     D.residues = n.resid.as<uint8_t>();
     D.err = n.err.as<int>();
+    D.values = dev_values ? dev_values : n.outv.as<int64_t>();
+    fill_crt(c.base, D);
     dev::memset0(n.err.p, 4, g_stream);
     launch_decode(D, g_stream);
-    dev::d2h(n.res_pin.p, n.resid.p, (size_t)n.B * c.n_out * k, g_stream);
+    if (!dev_values) dev::d2h(n.res_pin.p, n.outv.p, (size_t)n.B * c.n_out * 8, g_stream);
     dev::d2h(n.err_pin.as<int>() + 1, n.err.p, 4, g_stream);
 }
 
 static void decode_finish(Network& n, int64_t* values, bool values_on_device) {
     dashgpu_circuit& c = *n.c;
-    if (n.err_pin.as<int>()[1]) throw AuthError("output label not present in the decoding table");
-    std::vector<int64_t> host;
-    int64_t* dst = values;
-    if (values_on_device) {
-        host.resize((size_t)n.B * c.n_out);
-        dst = host.data();
-    }
-    crt_decode(c, n.res_pin.as<uint8_t>(), (uint64_t)n.B * c.n_out, dst);
-    if (values_on_device) {
-        dev::h2d(values, host.data(), host.size() * 8, g_stream);
-        dev::sync(g_stream);
-    }
+    const int err = n.err_pin.as<int>()[1];
+    if (err == ST_AUTH) throw AuthError("output label not present in the decoding table");
+    if (err) throw DataError("decode_signed: value exceeds 64-bit signed range");
+    if (!values_on_device) std::memcpy(values, n.res_pin.p, (size_t)n.B * c.n_out * 8);
 }
 
 static void decode_into(Network& n, const Bundle& outb, int64_t* values, bool values_on_device) {
-    decode_enqueue(n, outb);
+    decode_enqueue(n, outb, values_on_device ? values : nullptr);
     dev::sync(g_stream);
     decode_finish(n, values, values_on_device);
 }
@@ -1788,7 +1777,7 @@ static uint64_t act_row_pos(uint64_t E, uint64_t uc, uint64_t u, uint64_t j) {
 // ciphertext u*uc.cts inside the layer (layer.cpp:531-541).  Every chunk
 // buffer is C elements wide; only the id bases move.
 struct StreamWS {
-    DevBuf rk, seeds, mult, zero, Rb, commit, blob, slots, dec, vals, resid, err, actp, qctr, qflags, mmlab;
+    DevBuf rk, seeds, mult, zero, Rb, commit, blob, slots, dec, vals, resid, err, actp, qctr, qflags, mmlab, outv;
     Lanes base, in, gout, eout;
     uint64_t C = 0;
 };
@@ -1822,6 +1811,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
     w.dec.ensure((size_t)C * sum_p * 16);
     w.vals.ensure((size_t)C * 8);
     w.resid.ensure((size_t)C * k);
+    w.outv.ensure((size_t)C * 8);
     w.err.ensure(16);
     w.actp.ensure(sizeof(ActParams));
     w.mmlab.ensure((size_t)C * k * 2 * 16);
@@ -1835,7 +1825,6 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
     w.in.ensure(c.base, 1, C);
     w.gout.ensure(c.base, 1, C);
     w.eout.ensure(c.base, 1, C);
-    std::vector<uint8_t> res(C * k);
     using clk = std::chrono::steady_clock;
     for (uint32_t b = 0; b < batch; ++b) {
         uint32_t rk[44];
@@ -1960,16 +1949,18 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             make_lane_ptrs(w.eout, k, D.lanes);
             D.residues = w.resid.as<uint8_t>();
             D.err = w.err.as<int>();
+            D.values = w.outv.as<int64_t>();
+            fill_crt(c.base, D);
             dev::sync(g_stream);
             if (err_enc) throw DataError("encode_signed: value outside the representable range");
             dev::memset0(w.err.p, 4, g_stream);
             launch_decode(D, g_stream);
             int err = 0;
-            dev::d2h(res.data(), w.resid.p, (size_t)n * k, g_stream);
+            dev::d2h(outputs + (uint64_t)b * N + u0, w.outv.p, (size_t)n * 8, g_stream);
             dev::d2h(&err, w.err.p, 4, g_stream);
             dev::sync(g_stream);
-            if (err) throw AuthError("output label not present in the decoding table");
-            crt_decode(c, res.data(), n, outputs + (uint64_t)b * N + u0);
+            if (err == ST_AUTH) throw AuthError("output label not present in the decoding table");
+            if (err) throw DataError("decode_signed: value exceeds 64-bit signed range");
             const auto t4 = clk::now();
             tm.ms_garble += std::chrono::duration<double, std::milli>(t1 - t0).count();
             tm.ms_encode += std::chrono::duration<double, std::milli>(t2 - t1).count();
@@ -2887,7 +2878,7 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
             garble_into(n, seeds + (size_t)16 * b0, B, on_device != 0);
             encode_enqueue(n, inputs + (size_t)b0 * c->n_in, on_device != 0, in);
             evaluate_into(n, in, out);
-            decode_enqueue(n, out);
+            decode_enqueue(n, out, on_device ? outputs + (size_t)b0 * c->n_out : nullptr);
             dev::sync(g_stream);
             encode_finish(n);
             decode_finish(n, outputs + (size_t)b0 * c->n_out, on_device != 0);
