@@ -929,7 +929,7 @@ struct HostBuf {
 static void* g_stream = nullptr;
 // evaluation launches with at most this many elements run warp-per-element on
 // the level tape (kernels_act.cu kWpeMaxEval)
-constexpr uint64_t kWpeMaxElementsHost = 12000;
+constexpr uint64_t kWpeMaxElementsHost = 148 * 16 * 32 / 2;
 
 struct HLayer {
     int kind = 0;

@@ -102,7 +102,9 @@ constexpr int kWpeWarps = 16;
 // lower latency, ~5x lower throughput per SM: Model A b64 = 16k elements is
 // 23.5 ms warp-per-element vs 13.8 ms per-thread), evaluation up to ~12k.
 constexpr uint64_t kWpeMaxGarble = 8192;
-constexpr uint64_t kWpeMaxEval = 12000;  // engine.cpp sizes the slots for it (kWpeMaxElementsHost)
+// evaluation: lane groups of G >= 2 while elements * G fits one wave of
+// 16-warp CTAs (<= 148 * 512 / 2 = 37,888 elements; engine.cpp sizes the
+// level-tape slots for it: kWpeMaxElementsHost)
 
 __global__ void __launch_bounds__(kWpeWarps * 32, 1)
     act_wpe_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
@@ -149,8 +151,11 @@ __global__ void __launch_bounds__(kWpeWarps * 32, 1)
 constexpr int kWpeEvalWarps = 16;
 constexpr int kLaneWordsEval = 2 * NWMAX + 4;
 
+// Lanes form groups of G (a power of two): a warp evaluates 32/G elements, the
+// G lanes of a group take ops j, j+G, ... of every level of their element;
+// lane j of every group runs the same tape op (SIMT-uniform across groups).
 __global__ void __launch_bounds__(kWpeEvalWarps * 32, 1)
-    act_wpe_eval_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
+    act_wpe_eval_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter, uint32_t G) {
     fill_T(g_T0);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* lb = s_dyn + kTabWords + warp * kLaneWordsEval * 32 + lane;
@@ -164,13 +169,16 @@ __global__ void __launch_bounds__(kWpeEvalWarps * 32, 1)
     const uint32_t total = map.base[map.n];
     uint32_t item = warp * gridDim.x + blockIdx.x;
     const uint32_t first = kWpeEvalWarps * gridDim.x;
+    const uint32_t per = 32 / G, grp = lane / G, j = lane & (G - 1);
     while (item < total) {
         uint32_t li = 0;
         while (li + 1 < map.n && item >= map.base[li + 1]) ++li;
         const ActParams& P = layers[li];
         const uint32_t local = item - map.base[li];
-        e.b = local / P.E;
-        e.u = local - e.b * P.E;
+        e.b = local / map.wpi[li];
+        e.u = (local - e.b * map.wpi[li]) * per + grp;
+        const bool active = e.u < P.E;
+        if (!active) e.u = P.E - 1;  // idle group: stays in step with the warp's level syncs
         e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
         e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
         e.rows = act_rows(P.blob + (uint64_t)e.b * P.blob_stride, P.E, P.uc_cts, e.u, e.rs);
@@ -178,7 +186,8 @@ __global__ void __launch_bounds__(kWpeEvalWarps * 32, 1)
         e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
         for (int L = 0; L < P.n_levels; ++L) {
             const int end = P.lv_start[L + 1];
-            for (int i = P.lv_start[L] + (int)lane; i < end; i += 32) eval_op(P, e, P.lv_tape[i]);
+            if (active)
+                for (int i = P.lv_start[L] + (int)j; i < end; i += (int)G) eval_op(P, e, P.lv_tape[i]);
             __syncwarp();
         }
         uint32_t next = 0;
@@ -236,20 +245,25 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     ProfScope ps(garble ? K_ACT_GARBLE : K_ACT_EVAL, S(st));
     uint64_t elements = 0;
     for (int i = 0; i < n; ++i) elements += (uint64_t)host_layers[i].B * host_layers[i].E;
-    if (!garble && elements <= kWpeMaxEval) {
+    // evaluation lane groups: the largest G whose warps still fit one wave
+    uint32_t G = 32;
+    const uint64_t wave = (uint64_t)sm_count() * kWpeEvalWarps * 32;
+    while (G > 1 && elements * G > wave) G >>= 1;
+    if (!garble && G >= 2) {
         ItemMap wm;
         std::memset(&wm, 0, sizeof wm);
         wm.n = (uint32_t)n;
+        const uint32_t per = 32 / G;
         for (int i = 0; i < n; ++i) {
-            wm.wpi[i] = host_layers[i].E;
-            wm.base[i + 1] = wm.base[i] + host_layers[i].B * host_layers[i].E;
+            wm.wpi[i] = (host_layers[i].E + per - 1) / per;
+            wm.base[i + 1] = wm.base[i] + host_layers[i].B * wm.wpi[i];
         }
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), elements);  // spread: latency-bound
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), wm.base[n]);  // spread: latency-bound
         const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeEvalWarps * kLaneWordsEval * 32;
         ck(cudaMemsetAsync(q.counter, 0, sizeof(uint32_t), S(st)), "counter reset");
         ck(cudaFuncSetAttribute(act_wpe_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
            "attr");
-        act_wpe_eval_kernel<<<grid, kWpeEvalWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter);
+        act_wpe_eval_kernel<<<grid, kWpeEvalWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter, G);
         ck(cudaGetLastError(), "act wpe eval launch");
         return;
     }

@@ -82,7 +82,7 @@ static void act_layer(const ActParams& P, bool garble) {
             e.mult = nullptr;
             if (garble) {
                 act_element<true>(P, e, 0, P.n_ops);
-            } else if ((uint64_t)P.B * P.E <= 12000 && P.n_levels > 0) {
+            } else if ((uint64_t)P.B * P.E <= 148 * 16 * 32 / 2 && P.n_levels > 0) {
                 // small launches: the level-scheduled tape, as the CUDA
                 // warp-per-element evaluation runs it (levels in order;
                 // the ops of a level are independent)
