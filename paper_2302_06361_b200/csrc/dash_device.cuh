@@ -22,6 +22,16 @@
 
 namespace dashgpu {
 
+// loop unrolling knobs (tuning builds: -DDASH_AES_UNROLL=n / -DDASH_CODEC_UNROLL=n)
+#ifndef DASH_AES_UNROLL
+#define DASH_AES_UNROLL 1
+#endif
+#ifndef DASH_CODEC_UNROLL
+#define DASH_CODEC_UNROLL 1
+#endif
+constexpr int kAesUnroll = DASH_AES_UNROLL;
+constexpr int kCodecUnroll = DASH_CODEC_UNROLL;
+
 // ---------------------------------------------------------------- intrinsics
 #if defined(__CUDA_ARCH__)
 DASH_HD uint32_t umulhi32(uint32_t a, uint32_t b) { return __umulhi(a, b); }
@@ -106,7 +116,7 @@ DASH_HD U4 aes_core(U4 s, const RK& rk, const AesTab& t) {
     (tlo(t, P0(a, 0)) ^ tlo(t, P2(c, 2)) ^ rotl32(tlo(t, P0(b, 1)) ^ tlo(t, P2(d, 3)), 8) ^ (k))
     uint32_t s0 = s.x[0] ^ rk(0), s1 = s.x[1] ^ rk(1), s2 = s.x[2] ^ rk(2), s3 = s.x[3] ^ rk(3);
 #if defined(__CUDA_ARCH__)
-#pragma unroll 1
+#pragma unroll kAesUnroll
 #endif
     for (int r = 1; r < 10; ++r) {
         const uint32_t t0 = COL(s0, s1, s2, s3, rk(4 * r));
@@ -462,6 +472,9 @@ DASH_HD U4 lb_key_step(LB key, const uint32_t* R, const ModC& M) {
         return r;
     }
     uint32_t c[4] = {0, 0, 0, 0};
+#if defined(__CUDA_ARCH__)
+#pragma unroll kCodecUnroll
+#endif
     for (int w = M.nw - 1; w >= 0; --w) {
         const uint32_t x = key[w];
         const uint32_t cv = (x & 0xff) + M.m * (((x >> 8) & 0xff) + M.m * (((x >> 16) & 0xff) + M.m * (x >> 24)));
@@ -485,6 +498,9 @@ DASH_HD void digits_stream(const U4& cin, const ModC& M, F&& f) {
     int w = 0;
     for (int j = 0; j < M.nchunks; ++j) {
         uint32_t chunk = divmod_D(c, M, M.limbs[j]);
+#if defined(__CUDA_ARCH__)
+#pragma unroll kCodecUnroll
+#endif
         for (int ww = 0; ww < M.W && w < M.nw; ++ww, ++w) {
             const uint32_t q = fdiv(chunk, M.mag_m4, M.sh_m4);
             uint32_t v = split4(chunk - q * M.m4, M);
