@@ -225,9 +225,30 @@ def run_sweep(args):
     One JSON line per grid point, all on one GPU (the sweep shards by element
     range / CRT lane with no exchange)."""
     import torch
+    import torch.distributed as dist
     from paper_2302_06361_b200.engine import Dash
+    from paper_2302_06361_b200.shard import shard_range
 
-    eng = Dash(0)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:  # proj: element-range shards of the layer; linear: inference shards (SURVEY 8(e))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def max_over_ranks(sec):
+        if world == 1:
+            return sec
+        t = torch.tensor([sec], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    eng = Dash(local)
     eng.set_stream(torch.cuda.current_stream().cuda_stream)
     kinds = [s for s in args.sweep.split(",") if s]
     for kind in kinds:
@@ -245,13 +266,14 @@ def run_sweep(args):
                     gw = eng.model("relu16384", 0, k)  # warm-up: same kernels, small layer
                     eng.infer_stream(gw, (0x5EED).to_bytes(16, "big"), x[:, :16384] if N >= 16384 else
                                      np.zeros((1, 16384), np.int64), 1 << 14)
-                    torch.cuda.synchronize()
+                    a, b = shard_range(N, world, rank)
+                    barrier()
                     t0 = time.perf_counter()
-                    out, tm, _ = eng.infer_stream(g, (0x5EED0001).to_bytes(16, "big"), x, chunk)
-                    sec = time.perf_counter() - t0
-                    assert (out[0] == np.maximum(x[0], 0)).all(), "ReLU sweep mismatch"
+                    out, tm, _ = eng.infer_stream(g, (0x5EED0001).to_bytes(16, "big"), x, chunk, u_range=(a, b))
+                    sec = max_over_ranks(time.perf_counter() - t0)
+                    assert (out[0, a:b] == np.maximum(x[0, a:b], 0)).all(), "ReLU sweep mismatch"
                     rows = N * (info.act_uc_cts + info.act_eval_rows)
-                    line = {"sweep": "proj", "labels": N, "k": k, "label_ops_per_s": rows / sec,
+                    line = {"sweep": "proj", "labels": N, "k": k, "n_gpus": world, "label_ops_per_s": rows / sec,
                             "elements_per_s": N / sec, "seconds": sec, "garbled_rows": N * info.act_uc_cts,
                             "eval_rows": N * info.act_eval_rows, "table_bytes": 16 * N * info.act_uc_cts,
                             "table_GBps": 16 * N * info.act_uc_cts / sec / 1e9, "chunk_elements": chunk,
@@ -260,7 +282,9 @@ def run_sweep(args):
                     g = eng.model("dense1024", 0, k)
                     info = g.info
                     B = max(1, N // 1024)
-                    seeds = b"".join(int(0x5EED0000 + b).to_bytes(16, "big") for b in range(B))
+                    a, b = shard_range(B, world, rank)
+                    B = max(1, b - a)
+                    seeds = b"".join(int(0x5EED0000 + a + i).to_bytes(16, "big") for i in range(B))
                     P = 1
                     for p in [2, 3, 5, 7, 11, 13, 17, 19][:k]:
                         P *= p
@@ -268,19 +292,25 @@ def run_sweep(args):
                     x = np.random.default_rng(k).integers(-lim, lim + 1, size=(B, 1024))
                     eng.infer(g, seeds[:16 * min(B, 4)], x[: min(B, 4)])
                     eng.profile(True)
+                    barrier()
                     t0 = time.perf_counter()
                     eng.infer(g, seeds, x)
-                    sec = time.perf_counter() - t0
+                    sec = max_over_ranks(time.perf_counter() - t0)
                     prof = eng.profile_read()
                     eng.profile(False)
-                    lin_ms = prof.get("linear", (0.0, 0))[0]
+                    lin_ms = max_over_ranks(prof.get("linear", (0.0, 0))[0])
+                    B = B * world  # whole-job inferences (equal shards)
                     label_macs = 2 * B * 1024 * 1024 * k  # garble + eval passes
-                    line = {"sweep": "linear", "labels": B * 1024, "k": k, "inferences": B,
+                    line = {"sweep": "linear", "labels": B * 1024, "k": k, "n_gpus": world, "inferences": B,
                             "label_macs_per_s_kernel": label_macs / (lin_ms / 1e3) if lin_ms else None,
                             "digit_macs_per_s_kernel": 2 * B * info.linear_macs / (lin_ms / 1e3) if lin_ms else None,
                             "linear_kernel_ms": lin_ms, "end_to_end_s": sec,
                             "label_macs_per_s_e2e": label_macs / sec}
-                print(json.dumps(line), flush=True)
+                if rank == 0:
+                    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def main():

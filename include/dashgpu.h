@@ -182,6 +182,13 @@ int dashgpu_infer(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch
 int dashgpu_infer_stream(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
                          const int64_t* inputs, int64_t* outputs, uint64_t chunk_elems,
                          uint8_t* gc_out, dashgpu_timing* t);
+/* The same over elements [u_begin, u_end) only (a layer shards
+ * by element range across GPUs with no exchange -- gate / wire / row ids are
+ * affine in the element index).  inputs / outputs / gc_out keep the full-layer
+ * indexing; only the range is read / written. */
+int dashgpu_infer_stream_range(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
+                               const int64_t* inputs, int64_t* outputs, uint64_t chunk_elems,
+                               uint64_t u_begin, uint64_t u_end, uint8_t* gc_out, dashgpu_timing* t);
 
 /* ---- per-kernel CUDA-event timing on the launching stream ---- */
 int dashgpu_profile(int enable);

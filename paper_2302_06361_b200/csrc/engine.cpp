@@ -1787,14 +1787,17 @@ static bool streamable(const dashgpu_circuit& c) {
 }
 
 static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batch, const int64_t* inputs,
-                         int64_t* outputs, uint64_t chunk, uint8_t* gc_out, dashgpu_timing& tm) {
+                         int64_t* outputs, uint64_t chunk, uint8_t* gc_out, dashgpu_timing& tm, uint64_t u_begin,
+                         uint64_t u_end) {
     if (!streamable(c)) throw DataError("streamed inference needs a single activation-layer circuit");
     upload_circuit(c);
     const int k = c.k;
     const HLayer& l = c.layers[0];
     const Tape& T = *l.tape;
     const uint64_t N = l.E_out;
-    const uint64_t C = std::max<uint64_t>(1, std::min<uint64_t>(chunk, N));
+    u_end = std::min<uint64_t>(u_end, N);
+    if (u_begin > u_end) throw DataError("element range out of order");
+    const uint64_t C = std::max<uint64_t>(1, std::min<uint64_t>(chunk, std::max<uint64_t>(u_end - u_begin, 1)));
     StreamWS w;
     w.C = C;
     const uint64_t mult_stride = (uint64_t)(MAXMOD - 1) * 128 * NWMAX;
@@ -1831,8 +1834,8 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
         aes_expand_host(seeds + 16 * (size_t)b, rk);
         dev::h2d(w.rk.p, rk, sizeof rk, g_stream);
         dev::h2d(w.seeds.p, seeds + 16 * (size_t)b, 16, g_stream);
-        for (uint64_t u0 = 0; u0 < N; u0 += C) {
-            const uint32_t n = (uint32_t)std::min<uint64_t>(C, N - u0);
+        for (uint64_t u0 = u_begin; u0 < u_end; u0 += C) {
+            const uint32_t n = (uint32_t)std::min<uint64_t>(C, u_end - u0);
             const auto t0 = clk::now();
             // offsets, zero wires and this chunk's input base labels
             SetupParams S;
@@ -1969,8 +1972,8 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             tm.sub_batches += 1;
         }
     }
-    tm.h2d_bytes = (uint64_t)batch * (N * 8 + 16 + 44 * 4);
-    tm.d2h_bytes = (uint64_t)batch * N * k;
+    tm.h2d_bytes = (uint64_t)batch * ((u_end - u_begin) * 8 + 16 + 44 * 4);
+    tm.d2h_bytes = (uint64_t)batch * (u_end - u_begin) * 8;
 }
 
 // ============================================================ exports
@@ -2896,13 +2899,19 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
 
 int dashgpu_infer_stream(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batch, const int64_t* inputs,
                          int64_t* outputs, uint64_t chunk_elems, uint8_t* gc_out, dashgpu_timing* t) {
+    return dashgpu_infer_stream_range(cc, seeds, batch, inputs, outputs, chunk_elems, 0, ~0ull, gc_out, t);
+}
+
+int dashgpu_infer_stream_range(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batch,
+                               const int64_t* inputs, int64_t* outputs, uint64_t chunk_elems, uint64_t u_begin,
+                               uint64_t u_end, uint8_t* gc_out, dashgpu_timing* t) {
     return guarded([&] {
         auto* c = const_cast<dashgpu_circuit*>(cc);
         std::lock_guard<std::mutex> lk(c->mu);
         dashgpu_timing tm;
         std::memset(&tm, 0, sizeof tm);
         const auto t0 = std::chrono::steady_clock::now();
-        infer_stream(*c, seeds, batch, inputs, outputs, chunk_elems, gc_out, tm);
+        infer_stream(*c, seeds, batch, inputs, outputs, chunk_elems, gc_out, tm, u_begin, u_end);
         tm.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         if (t) *t = tm;
     });

@@ -124,6 +124,8 @@ def _declare(L):
     L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
     L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
     L.dashgpu_infer_stream.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
+    L.dashgpu_infer_stream_range.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, ctypes.c_uint64,
+                                             ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
     L.dashgpu_network_setup.argtypes = [vp, u8p, ctypes.c_uint32, ctypes.POINTER(vp)]
     L.dashgpu_input_base.argtypes = [vp, ctypes.POINTER(vp)]
     L.dashgpu_layer_garble.argtypes = [vp, ctypes.c_uint32, vp, vp, ctypes.POINTER(vp)]
@@ -264,20 +266,24 @@ class Dash:
                                            vp(out.ctypes.data), 0, ctypes.byref(t)))
         return out, t
 
-    def infer_stream(self, c: "GpuCircuit", seeds: bytes, inputs, chunk: int, want_gc: bool = False):
+    def infer_stream(self, c: "GpuCircuit", seeds: bytes, inputs, chunk: int, want_gc: bool = False,
+                     u_range=None):
         """Streamed garble + garble_inputs + evaluate + decode_outputs of a
         single activation-layer circuit in element chunks (the label-ops
-        sweep).  Returns (outputs, timing, gc) with gc the per-inference
-        ciphertext blobs when want_gc."""
+        sweep).  u_range = (begin, end): only those elements (a rank's shard,
+        SURVEY 8(e)); outputs / gc keep full-layer indexing.  Returns
+        (outputs, timing, gc) with gc the per-inference ciphertext blobs when
+        want_gc."""
         t = Timing()
         batch = len(seeds) // 16
         sbuf = (ctypes.c_uint8 * len(seeds)).from_buffer_copy(seeds)
         x = np.ascontiguousarray(inputs, np.int64).reshape(batch, c.info.n_in)
         out = np.zeros((batch, c.info.n_out), np.int64)
         gc = np.zeros(batch * c.info.cts * 16, np.uint8) if want_gc else None
-        self._check(self.lib.dashgpu_infer_stream(c.h, ctypes.cast(sbuf, vp), batch, vp(x.ctypes.data),
-                                                  vp(out.ctypes.data), chunk,
-                                                  vp(gc.ctypes.data) if want_gc else None, ctypes.byref(t)))
+        u0, u1 = u_range if u_range is not None else (0, c.info.n_in)
+        self._check(self.lib.dashgpu_infer_stream_range(c.h, ctypes.cast(sbuf, vp), batch, vp(x.ctypes.data),
+                                                        vp(out.ctypes.data), chunk, u0, u1,
+                                                        vp(gc.ctypes.data) if want_gc else None, ctypes.byref(t)))
         gcs = [gc[b * c.info.cts * 16:(b + 1) * c.info.cts * 16].tobytes() for b in range(batch)] if want_gc else None
         return out, t, gcs
 

@@ -502,3 +502,23 @@ def test_projection_gate_primitive_vs_oracle(eng, oracle, p, q):
     for i in range(n):
         o0 = np.array(oracle.decompress_mod(out0[i], q))
         assert got[i] == oracle.compress(q, ((o0 + phi[vs[i]] * rq) % q).tolist())
+
+
+def test_streamed_layer_element_ranges_compose(eng):
+    # element-range shards of one layer reproduce the whole layer
+    from helpers import models
+
+    c = models.build("relu3000", 0, 4)
+    g = eng.circuit(c)
+    seed = seed_hex(0x5C0)
+    x = np.random.default_rng(1).integers(-100, 100, size=(1, c.n_in))
+    full, _, gcf = eng.infer_stream(g, seed, x, 512, want_gc=True)
+    uc = g.info.cts // c.n_in
+    parts_out = np.zeros_like(full)
+    gc = bytearray(len(gcf[0]))
+    for a, b in [(0, 1100), (1100, 1101), (1101, 3000)]:
+        o, t, gp = eng.infer_stream(g, seed, x, 512, want_gc=True, u_range=(a, b))
+        parts_out[:, a:b] = o[:, a:b]
+        gc[a * uc * 16:b * uc * 16] = gp[0][a * uc * 16:b * uc * 16]
+    assert (parts_out == full).all()
+    assert bytes(gc) == gcf[0]

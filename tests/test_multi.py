@@ -63,3 +63,42 @@ def test_two_rank_gloo_gather_equals_single_process(tmp_path, emu):
     single, _ = emu.infer(g, b"".join(step_seeds(0, B)), x)
     assert gathered.shape == single.shape
     assert (gathered == single).all()
+
+
+def _stream_worker(rank, world, port, out_path):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_06361_b200.engine import Dash
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    eng = Dash(lib_path=EMU_LIB)
+    g = eng.model("relu1000", 0, 3)
+    x = np.random.default_rng(2).integers(-14, 15, size=(1, 1000))
+    a, b = shard_range(1000, world, rank)
+    out, _, _ = eng.infer_stream(g, int(7).to_bytes(16, "big"), x, 256, u_range=(a, b))
+    mine = torch.zeros(1000, dtype=torch.int64)
+    mine[a:b] = torch.from_numpy(out[0, a:b])
+    dist.all_reduce(mine)  # disjoint shards: the sum is the concatenation
+    if rank == 0:
+        np.save(out_path, mine.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not os.path.exists(EMU_LIB), reason="emulation library not built")
+def test_two_rank_element_sharded_layer_equals_single_process(tmp_path, emu):
+    # an activation layer shards by element range with no exchange
+    out_path = str(tmp_path / "layer.npy")
+    mp.spawn(_stream_worker, args=(2, _free_port(), out_path), nprocs=2, join=True)
+    got = np.load(out_path)
+    g = emu.model("relu1000", 0, 3)
+    x = np.random.default_rng(2).integers(-14, 15, size=(1, 1000))
+    single, _, _ = emu.infer_stream(g, int(7).to_bytes(16, "big"), x, 256)
+    assert (got == single[0]).all()
+    assert (single[0] == np.maximum(x[0], 0)).all()
