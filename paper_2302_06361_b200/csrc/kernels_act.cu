@@ -97,25 +97,31 @@ __global__ void __launch_bounds__((G ? kActWarpsGarble : kActWarpsEval) * 32, 1)
 // Small garbling launches (few elements in total): one warp per element
 // (wpe.cuh), every activation layer in one persistent launch.
 constexpr int kWpeWarps = 16;
-// Warp per element wins while the per-thread launch would be latency-bound
-// and the warps fit about one wave: garbling splits rows over the lanes (much
-// lower latency, ~5x lower throughput per SM: Model A b64 = 16k elements is
-// 23.5 ms warp-per-element vs 13.8 ms per-thread), evaluation up to ~12k.
-constexpr uint64_t kWpeMaxGarble = 8192;
+// Lane groups win while the per-thread launch would be latency-bound: G
+// lanes per element cut an element's latency ~G-fold but idle lanes on small
+// gates cost throughput (whole-warp groups for Model A b64 = 16k elements
+// were 23.5 ms vs 13.8 ms per-thread); G is chosen so the warps fit
+// kWpeGarbleWaves waves.
+#ifndef DASH_WPE_GARBLE_WAVES
+#define DASH_WPE_GARBLE_WAVES 1
+#endif
+constexpr uint64_t kWpeGarbleWaves = DASH_WPE_GARBLE_WAVES;
 // evaluation: lane groups of G >= 2 while elements * G fits one wave of
 // 16-warp CTAs (<= 148 * 512 / 2 = 37,888 elements; engine.cpp sizes the
 // level-tape slots for it: kWpeMaxElementsHost)
 
 __global__ void __launch_bounds__(kWpeWarps * 32, 1)
-    act_wpe_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter) {
+    act_wpe_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter, uint32_t G) {
     fill_T(g_T0);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t per = 32 / G, grp = lane / G, j = lane & (G - 1);
     uint32_t* wb = s_dyn + kTabWords + warp * kWpeWords;
+    uint32_t* gb = wb + NWMAX * 32 + grp * kWpeShared;  // this group's shared labels
     WpeBufs w;
-    w.X = LB{wb, 1};
-    w.A = LB{wb + NWMAX, 1};
-    w.K = LB{wb + 2 * NWMAX, 1};
-    w.KEY = LB{wb + kWpeShared + lane, 32};
+    w.X = LB{gb, 1};
+    w.A = LB{gb + NWMAX, 1};
+    w.K = LB{gb + 2 * NWMAX, 1};
+    w.KEY = LB{wb + lane, 32};
     Elt e;
     e.X = w.X;
     e.K = w.K;
@@ -129,8 +135,11 @@ __global__ void __launch_bounds__(kWpeWarps * 32, 1)
         while (li + 1 < map.n && item >= map.base[li + 1]) ++li;
         const ActParams& P = layers[li];
         const uint32_t local = item - map.base[li];
-        e.b = local / P.E;
-        e.u = local - e.b * P.E;
+        e.b = local / map.wpi[li];
+        e.u = (local - e.b * map.wpi[li]) * per + grp;
+        // a group past the layer's last element repeats that element (same
+        // values written twice) so every group stays in step with the syncs
+        if (e.u >= P.E) e.u = P.E - 1;
         e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
         e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
         e.rows = act_rows(P.blob + (uint64_t)e.b * P.blob_stride, P.E, P.uc_cts, e.u, e.rs);
@@ -138,7 +147,7 @@ __global__ void __launch_bounds__(kWpeWarps * 32, 1)
         e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
         e.rk = P.rk + (uint64_t)e.b * 44;
         e.mult = P.mult + (uint64_t)e.b * P.mult_stride;
-        for (int i = 0; i < P.n_ops; ++i) garble_op_w(P, e, P.tape[i], w, lane);
+        for (int i = 0; i < P.n_ops; ++i) garble_op_w(P, e, P.tape[i], w, j, G);
         uint32_t next = 0;
         if (lane == 0) next = first + atomicAdd(counter, 1u);
         item = __shfl_sync(0xffffffffu, next, 0);
@@ -267,19 +276,24 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         ck(cudaGetLastError(), "act wpe eval launch");
         return;
     }
-    if (garble && elements <= kWpeMaxGarble) {
+    // garbling lane groups: the largest G whose warps fit one wave of 16-warp
+    // CTAs; G = 1 is the per-thread kernel below
+    uint32_t Gg = 32;
+    while (Gg > 1 && elements * Gg > (uint64_t)sm_count() * kWpeWarps * 32 * kWpeGarbleWaves) Gg >>= 1;
+    if (garble && Gg >= 2) {
         ItemMap wm;
         std::memset(&wm, 0, sizeof wm);
         wm.n = (uint32_t)n;
+        const uint32_t per = 32 / Gg;
         for (int i = 0; i < n; ++i) {
-            wm.wpi[i] = host_layers[i].E;
-            wm.base[i + 1] = wm.base[i] + host_layers[i].B * host_layers[i].E;
+            wm.wpi[i] = (host_layers[i].E + per - 1) / per;
+            wm.base[i + 1] = wm.base[i] + host_layers[i].B * wm.wpi[i];
         }
-        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), elements);  // spread: latency-bound
+        const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), wm.base[n]);  // spread: latency-bound
         const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeWarps * kWpeWords;
         ck(cudaMemsetAsync(q.counter, 0, sizeof(uint32_t), S(st)), "counter reset");
         ck(cudaFuncSetAttribute(act_wpe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
-        act_wpe_kernel<<<grid, kWpeWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter);
+        act_wpe_kernel<<<grid, kWpeWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter, Gg);
         ck(cudaGetLastError(), "act wpe launch");
         return;
     }
