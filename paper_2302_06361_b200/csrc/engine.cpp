@@ -927,9 +927,6 @@ struct HostBuf {
 };
 
 static void* g_stream = nullptr;
-// evaluation launches with at most this many elements run warp-per-element on
-// the level tape (kernels_act.cu kWpeMaxEval)
-constexpr uint64_t kWpeMaxElementsHost = 148 * 16 * 32 / 2;
 
 struct HLayer {
     int kind = 0;
@@ -1517,7 +1514,7 @@ static void network_reserve(Network& n, uint32_t B) {
         if (l.tape) {
             slot_total += (size_t)l.tape->nslots * B * l.E_out;
             // warp-per-element evaluation of a small layer uses the level tape's slots
-            if ((uint64_t)B * l.E_out <= kWpeMaxElementsHost)
+            if ((uint64_t)B * l.E_out <= dev::lane_group_eval_max())
                 slot_eval = std::max(slot_eval, (size_t)l.tape->nslots_lv * B * l.E_out);
             ++nact;
         }

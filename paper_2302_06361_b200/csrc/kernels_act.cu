@@ -108,7 +108,7 @@ constexpr int kWpeWarps = 16;
 constexpr uint64_t kWpeGarbleWaves = DASH_WPE_GARBLE_WAVES;
 // evaluation: lane groups of G >= 2 while elements * G fits one wave of
 // 16-warp CTAs (<= 148 * 512 / 2 = 37,888 elements; engine.cpp sizes the
-// level-tape slots for it: kWpeMaxElementsHost)
+// level-tape slots for it: dev::lane_group_eval_max())
 
 __global__ void __launch_bounds__(kWpeWarps * 32, 1)
     act_wpe_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t* counter, uint32_t G) {
@@ -239,6 +239,10 @@ static int sm_count() {
     }
     return sms;
 }
+
+namespace dev {
+uint64_t lane_group_eval_max() { return (uint64_t)sm_count() * kWpeEvalWarps * 32 / 2; }
+}  // namespace dev
 
 void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* st,
                       const Sched& q) {

@@ -26,7 +26,10 @@ void sync(void* stream);
 void check();  // raise on a pending device error
 size_t free_bytes();
 void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot, const uint32_t* T0);
-// streams / events (pipelined inference runs two networks on two streams)
+// elements up to which an evaluation launch runs in lane groups on the level
+// tape (kernels_act.cu; the engine sizes the level tape's slots for it)
+uint64_t lane_group_eval_max();
+// streams / events
 void* stream_create();
 void stream_destroy(void* s);
 void* event_create();

@@ -55,6 +55,7 @@ void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* m
         g_T[i] = (i & 32) ? ((v << 16) | (v >> 16)) : v;
     }
 }
+uint64_t lane_group_eval_max() { return 148 * 16 * 32 / 2; }
 void* stream_create() { return nullptr; }
 void stream_destroy(void*) {}
 void* event_create() { return nullptr; }
@@ -82,7 +83,7 @@ static void act_layer(const ActParams& P, bool garble) {
             e.mult = nullptr;
             if (garble) {
                 act_element<true>(P, e, 0, P.n_ops);
-            } else if ((uint64_t)P.B * P.E <= 148 * 16 * 32 / 2 && P.n_levels > 0) {
+            } else if ((uint64_t)P.B * P.E <= dev::lane_group_eval_max() && P.n_levels > 0) {
                 // small launches: the level-scheduled tape, as the CUDA
                 // warp-per-element evaluation runs it (levels in order;
                 // the ops of a level are independent)
