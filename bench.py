@@ -474,7 +474,10 @@ def main():
                      "bytes_per_element": bytes_per_elem,
                      "kernel_ms_per_step": act_ms / args.steps,
                      "kernel_share_of_step": (act_ms / args.steps) / (ms / args.steps),
-                     "issue_roofline_ncu": issue or None},
+                     "issue_roofline_ncu": issue or None,
+                     "note": "integer-issue / latency bound (AES T-tables + base-m label codec, SURVEY 8(d) honest "
+                             "note): the HBM fraction is small by construction; issue_roofline_ncu is its real "
+                             "roofline (ncu issue-active and ALU-pipe utilisation of this kernel)"},
         "roofline_linear": roof_lin,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "inferences/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
