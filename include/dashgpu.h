@@ -14,6 +14,7 @@
  *   dashgpu_export_decoding <- dash::serialize_decoding         garble.hpp:122
  *   dashgpu_export_bundle   <- dash::bundle_payload             garble.hpp:131
  *   dashgpu_import_bundle   <- dash::bundle_from_payload        garble.hpp:132-134
+ *   dashgpu_import_gc       <- dash::parse_garbled_circuit      garble.hpp:117 (garble.cpp:368-403)
  *   dashgpu_circuit_create  <- dash::validate_circuit + circuit_layout   circuit.hpp:26, garble.hpp:86-88
  *   dashgpu_circuit_info    <- dash::count_circuit / GarbleStats         circuit.hpp:61-62, garble.hpp:36-41
  *
@@ -160,6 +161,13 @@ int dashgpu_export_bundle(const dashgpu_bundle* bd, uint32_t b, uint8_t* buf, si
 /* payload of every inference concatenated ([batch][k][n][16] bytes) */
 int dashgpu_import_bundle(dashgpu_network* n, const uint8_t* data, size_t len, int output,
                           dashgpu_bundle** out);
+/* evaluator side (EvaluatorService GC_TRANSFER, protocol.cpp:309-316):
+ * batch serialized GCs (export_gc format) of one circuit -> a network that
+ * evaluates them as inferences 0..batch-1 (garbling it returns
+ * DASHGPU_ERR_DATA: private weights are not in a GC).  Owns its circuit. */
+int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t batch, dashgpu_network** out);
+/* the circuit a network garbles / evaluates (borrowed: lives as long as the network) */
+int dashgpu_network_circuit(const dashgpu_network* n, const dashgpu_circuit** out);
 /* fault injection for tests: XOR `mask` (16 bytes) into ciphertext `index` of inference b */
 int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint8_t* mask16);
 

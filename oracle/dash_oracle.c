@@ -1709,7 +1709,9 @@ size_t orc_net_gc_bytes(const orc_net* n, uint8_t* buf, size_t cap) {
     for (int li = 0; li < c->nl; ++li) {
         const olayer* l = &c->layers[li];
         w_le(&w, (uint64_t)l->kind, 1);
-        w_le(&w, l->priv ? 1 : 0, 1);
+        /* bit 1 of the private byte flags the extension record (dash_circuit_desc.h) */
+        const int ext = l->kind > DASH_LAYER_FLATTEN || l->src || l->src2 || l->pad;
+        w_le(&w, (uint64_t)(l->priv ? 1 : 0) | (ext ? 2u : 0u), 1);
         w_le(&w, l->in_dim, 4);
         w_le(&w, l->out_dim, 4);
         w_le(&w, l->in_ch, 4);
@@ -1722,7 +1724,7 @@ size_t orc_net_gc_bytes(const orc_net* n, uint8_t* buf, size_t cap) {
             w_le(&w, l->nw, 8);
             for (uint64_t i = 0; i < l->nw; ++i) w_le(&w, (uint64_t)l->w[i], 8);
         }
-        if (l->kind > DASH_LAYER_FLATTEN || l->src || l->src2 || l->pad) { /* extension record */
+        if (ext) { /* extension record */
             w_le(&w, (uint64_t)(uint32_t)l->src, 4);
             w_le(&w, (uint64_t)(uint32_t)l->src2, 4);
             w_le(&w, l->pad, 4);

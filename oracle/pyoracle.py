@@ -439,6 +439,15 @@ class RefLib(_Base):
             raise CheckerError(3, self.err())
         return Bundle(self, vp(h))
 
+    def eval_gc_bytes(self, gc: bytes, b: Bundle, threads: int = 0) -> Bundle:
+        """parse_garbled_circuit + evaluate (EvaluatorService, protocol.cpp:309-331)."""
+        out = vp()
+        buf = (ctypes.c_uint8 * len(gc)).from_buffer_copy(gc)
+        rc = self.lib.ref_eval_gc_bytes(buf, len(gc), b.h, threads, ctypes.byref(out))
+        if rc:
+            raise CheckerError(rc, self.err())
+        return Bundle(self, out)
+
     def decode(self, net: Net, b: Bundle) -> np.ndarray:
         out = np.zeros(net.circuit.c.n_out, np.int64)
         rc = self.lib.ref_decode(net.h, b.h, out.ctypes.data_as(i64p))

@@ -985,6 +985,10 @@ struct dashgpu_circuit {
     std::vector<dash_layer_desc> desc_layers;  // for dashgpu_circuit_desc_view
     std::unique_ptr<dashgpu::Network> workspace;  // dashgpu_infer cache
     bool uploaded = false;  // per-layer device buffers created (upload_circuit)
+    // evaluator copy parsed from a GC (dashgpu_import_gc): private weights
+    // withheld, so it can evaluate but not garble; sign spec taken from the GC
+    bool eval_only = false;
+    dashgpu::Spec gc_spec;
     std::mutex mu;
     ~dashgpu_circuit();
 };
@@ -1098,6 +1102,7 @@ static void prepare_circuit(dashgpu_circuit& c) {
         l.E_in = shape_size(l.in_shape);
         l.E_out = shape_size(l.out_shape);
         if (l.linear()) {
+            if (c.eval_only && l.priv && l.w.empty()) l.w.assign(l.weight_count(), 0);  // never read by evaluation
             if (l.w.size() != l.weight_count()) throw DataError("circuit must be quantized before garbling");
             if (!l.bias.empty() && l.bias.size() != l.bias_count()) throw DataError("quantized bias count mismatch");
         }
@@ -1107,7 +1112,8 @@ static void prepare_circuit(dashgpu_circuit& c) {
     c.n_out = shape_size(shapes.back());
     if (c.n_in > (1u << 26) || c.n_out > (1u << 26)) throw DataError("tensor too large");
     if (c.needs_sign) {
-        c.sign = make_sign(c.base, choose_spec(c.base, c.sign_target));
+        if (c.eval_only && c.gc_spec.empty()) throw DataError("garbled circuit lacks a sign spec");
+        c.sign = make_sign(c.base, c.gc_spec.empty() ? choose_spec(c.base, c.sign_target) : c.gc_spec);
         c.relu_tape = std::make_shared<Tape>(build_tape(DASH_LAYER_RELU, c.base, c.sign));
         c.sign_tape = std::make_shared<Tape>(build_tape(DASH_LAYER_SIGNACT, c.base, c.sign));
     }
@@ -1568,6 +1574,7 @@ static const Lanes* run_layers(Network& n, bool garbler, const Lanes& input) {
 static void garble_setup(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
+    if (c.eval_only) throw DataError("circuit is an evaluator copy (private weights withheld): it cannot garble");
     upload_circuit(c);
     network_reserve(n, B);
     // seeds -> device, AES key schedules expanded on the device (no host
@@ -2016,6 +2023,11 @@ static u128 host_compress(const uint32_t* words, int m) {
 static u128 u4_to_u128(const U4& v) {
     return ((u128)v.x[3] << 96) | ((u128)v.x[2] << 64) | ((u128)v.x[1] << 32) | v.x[0];
 }
+static U4 u128_to_u4(u128 v) {
+    U4 r;
+    for (int i = 0; i < 4; ++i) r.x[i] = (uint32_t)(v >> (32 * i));
+    return r;
+}
 
 // device row index of reference ciphertext index idx (one inference's GC)
 static uint64_t device_ct_index(const dashgpu_circuit& c, uint64_t idx) {
@@ -2036,6 +2048,18 @@ static void act_rows_to_reference(const dashgpu_circuit& c, std::vector<U4>& cts
         tmp.assign(cts.begin() + l.ct_base, cts.begin() + l.ct_base + l.cts);
         for (uint64_t u = 0; u < l.E_out; ++u)
             for (uint64_t j = 0; j < uc; ++j) cts[l.ct_base + u * uc + j] = tmp[act_row_pos(l.E_out, uc, u, j)];
+    }
+}
+
+// inverse of act_rows_to_reference (an imported GC -> device rows)
+static void reference_to_act_rows(const dashgpu_circuit& c, std::vector<U4>& cts) {
+    std::vector<U4> tmp;
+    for (const auto& l : c.layers) {
+        if (!l.tape || !l.cts) continue;
+        const uint64_t uc = l.tape->cts;
+        tmp.assign(cts.begin() + l.ct_base, cts.begin() + l.ct_base + l.cts);
+        for (uint64_t u = 0; u < l.E_out; ++u)
+            for (uint64_t j = 0; j < uc; ++j) cts[l.ct_base + act_row_pos(l.E_out, uc, u, j)] = tmp[u * uc + j];
     }
 }
 
@@ -2063,7 +2087,10 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
     w.le(c.layers.size(), 2);
     for (const auto& l : c.layers) {
         w.le((uint64_t)l.kind, 1);
-        w.le(l.priv ? 1 : 0, 1);
+        // bit 1 of the private byte flags the extension record, so a reader
+        // knows it follows (reference circuits never set it)
+        const bool ext = l.kind > DASH_LAYER_FLATTEN || l.src || l.src2 || l.pad;
+        w.le((l.priv ? 1 : 0) | (ext ? 2 : 0), 1);
         for (uint32_t v : {l.in_dim, l.out_dim, l.in_ch, l.out_ch, l.filter, l.stride}) w.le(v, 4);
         const bool ww = l.linear() && !l.priv;
         w.le(ww ? 1 : 0, 1);
@@ -2071,7 +2098,7 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
             w.le(l.w.size(), 8);
             for (int64_t v : l.w) w.le((uint64_t)v, 8);
         }
-        if (l.kind > DASH_LAYER_FLATTEN || l.src || l.src2 || l.pad) {  // extension record
+        if (ext) {  // extension record
             w.le((uint32_t)l.src, 4);
             w.le((uint32_t)l.src2, 4);
             w.le(l.pad, 4);
@@ -2114,6 +2141,127 @@ static std::vector<U4> compress_lanes(const Lanes& L, const Crt& base, uint32_t 
         dev::sync(g_stream);
     }
     return out;
+}
+
+// ---- GC import (evaluator side) ----
+struct Reader {
+    const uint8_t* p;
+    size_t n, at = 0;
+    uint64_t le(int w) {
+        if (n - at < (size_t)w) throw DataError("truncated garbled circuit");
+        uint64_t v = 0;
+        for (int i = 0; i < w; ++i) v |= (uint64_t)p[at + i] << (8 * i);
+        at += w;
+        return v;
+    }
+    u128 u128v() {
+        const uint64_t lo = le(8);
+        return ((u128)le(8) << 64) | lo;
+    }
+};
+
+// decompress_mod (label.cpp:228-232) into byte-digit words
+static void host_decompress(u128 v, int m, uint32_t* words) {
+    const int n = n_digits_host(m);
+    const bool pow2 = (m & (m - 1)) == 0;
+    if (!pow2) {
+        u128 mn = 1;
+        for (int i = 0; i < n; ++i) mn *= (u128)m;
+        v %= mn;
+    }
+    int e = 0;
+    while ((1 << e) < m) ++e;
+    for (int w = 0; w < LABW; ++w) words[w] = 0;
+    for (int i = 0; i < n; ++i) {
+        const uint32_t d = pow2 ? (uint32_t)(v & (u128)(m - 1)) : (uint32_t)(v % (u128)m);
+        v = pow2 ? v >> e : v / (u128)m;
+        words[i / 4] |= d << (8 * (i % 4));
+    }
+}
+
+struct ParsedGc {
+    size_t circuit_bytes = 0;  // prefix holding the circuit description
+    std::vector<u128> zero;
+    std::vector<uint64_t> bases;
+    std::vector<u128> cts;
+    u128 commit = 0;
+};
+
+// parse_garbled_circuit (garble.cpp:368-403) + read_layer (garble.cpp:89-107);
+// the circuit is built into c when c is non-null
+static ParsedGc parse_gc(const uint8_t* data, size_t len, dashgpu_circuit* c) {
+    Reader r{data, len};
+    if (len < 4 || std::memcmp(data, "DASH", 4) != 0) throw DataError("bad file magic");
+    r.at = 4;
+    if (r.le(2) != 1) throw DataError("unsupported format version");
+    if (r.le(1) != 1) throw DataError("wrong file kind");
+    const int k = (int)r.le(1);
+    if (k < 1 || k > MAXK) throw DataError("bad base size");
+    const int rank = (int)r.le(1);
+    if (rank == 0 || rank > 8) throw DataError("bad tensor rank");
+    std::vector<uint32_t> shape(rank);
+    uint64_t total = 1;
+    for (auto& d : shape) {
+        d = (uint32_t)r.le(4);
+        if (d == 0) throw DataError("zero tensor dimension");
+        total *= d;
+        if (total > (1ull << 26)) throw DataError("tensor too large");
+    }
+    const uint64_t alpha = r.le(8), target = r.le(8);
+    const int t = (int)r.le(1);
+    Spec spec(t);
+    for (auto& m : spec) m = (int)r.le(2);
+    const uint32_t nl = (uint32_t)r.le(2);
+    std::vector<HLayer> layers(nl);
+    for (auto& l : layers) {
+        l.kind = (int)r.le(1);
+        if (l.kind < 1 || l.kind > 7) throw DataError("bad layer kind");
+        const uint32_t flags = (uint32_t)r.le(1);
+        l.priv = (flags & 1) != 0;
+        l.in_dim = (uint32_t)r.le(4);
+        l.out_dim = (uint32_t)r.le(4);
+        l.in_ch = (uint32_t)r.le(4);
+        l.out_ch = (uint32_t)r.le(4);
+        l.filter = (uint32_t)r.le(4);
+        l.stride = (uint32_t)r.le(4);
+        if (r.le(1) != 0) {
+            const uint64_t n = r.le(8);
+            if (n != l.weight_count()) throw DataError("bad weight count");
+            if (n > (len - r.at) / 8) throw DataError("truncated garbled circuit");
+            l.w.resize(n);
+            for (auto& v : l.w) v = (int64_t)r.le(8);
+        }
+        if (flags & 2) {  // extension record (export_gc)
+            l.src = (int32_t)(uint32_t)r.le(4);
+            l.src2 = (int32_t)(uint32_t)r.le(4);
+            l.pad = (uint32_t)r.le(4);
+        }
+    }
+    ParsedGc g;
+    g.circuit_bytes = r.at;
+    if (c) {
+        c->k = k;
+        c->input_shape = shape;
+        std::memcpy(&c->alpha, &alpha, 8);
+        std::memcpy(&c->sign_target, &target, 8);
+        c->layers = std::move(layers);
+        c->eval_only = true;
+        c->gc_spec = spec;
+        prepare_circuit(*c);  // validate_circuit + layout + tapes
+    }
+    for (int i = 0; i < k; ++i) g.zero.push_back(r.u128v());
+    const uint64_t nb = r.le(8);
+    if (nb != (uint64_t)nl + 1) throw DataError("bad ciphertext index length");
+    g.bases.resize(nb);
+    for (auto& b : g.bases) b = r.le(8);
+    const uint64_t ncts = r.le(8);
+    if (ncts > (1ull << 32)) throw DataError("ciphertext blob too large");
+    if (ncts > (len - r.at) / 16) throw DataError("truncated garbled circuit");
+    g.cts.resize(ncts);
+    for (auto& v : g.cts) v = r.u128v();
+    g.commit = r.u128v();
+    if (r.at != len) throw DataError("trailing bytes in garbled circuit file");
+    return g;
 }
 
 static std::vector<uint8_t> export_encoding(const Network& n, uint32_t b) {
@@ -2418,6 +2566,7 @@ static std::vector<int64_t> plain_forward(const dashgpu_circuit& c, std::vector<
 dashgpu_circuit::~dashgpu_circuit() = default;
 
 struct dashgpu_network {
+    std::unique_ptr<dashgpu_circuit> own_c;  // evaluator copy of an imported GC
     std::unique_ptr<dashgpu::Network> net;
 };
 struct dashgpu_bundle {
@@ -2807,6 +2956,66 @@ int dashgpu_import_bundle(dashgpu_network* n, const uint8_t* data, size_t len, i
             dev::sync(g_stream);
         }
         *out = bd.release();
+    });
+}
+
+// EvaluatorService GC_TRANSFER (protocol.cpp:309-316): garbled circuits ->
+// an evaluator network, one inference per GC; all GCs of a batch must carry
+// the same circuit.  The consistency checks of evaluate (garble.cpp:262-303)
+// run here, once.
+int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t batch, dashgpu_network** out) {
+    return guarded([&] {
+        if (!gcs || !lens || !out) throw DataError("null argument");
+        if (batch == 0) throw DataError("empty batch");
+        auto n = std::make_unique<dashgpu_network>();
+        n->own_c = std::make_unique<dashgpu_circuit>();
+        dashgpu_circuit& c = *n->own_c;
+        std::vector<ParsedGc> gs;
+        gs.push_back(parse_gc(gcs[0], lens[0], &c));
+        for (uint32_t b = 1; b < batch; ++b) {
+            gs.push_back(parse_gc(gcs[b], lens[b], nullptr));
+            if (gs[b].circuit_bytes != gs[0].circuit_bytes ||
+                std::memcmp(gcs[b], gcs[0], gs[0].circuit_bytes) != 0)
+                throw DataError("garbled circuits of a batch differ in their circuit");
+        }
+        for (const auto& g : gs) {
+            if (g.cts.size() != c.total_cts) throw DataError("ciphertext blob does not match the circuit");
+            for (size_t li = 0; li < c.layers.size(); ++li)
+                if (g.bases[li] != c.layers[li].ct_base) throw DataError("ciphertext blob does not match the circuit");
+            if (g.bases.back() != c.total_cts) throw DataError("ciphertext blob does not match the circuit");
+        }
+        n->net = std::make_unique<Network>();
+        Network& N = *n->net;
+        N.c = &c;
+        upload_circuit(c);
+        network_reserve(N, batch);
+        std::vector<uint32_t> zero((size_t)batch * c.k * LABW);
+        std::vector<U4> cts;
+        std::vector<U4> commit(batch);
+        for (uint32_t b = 0; b < batch; ++b) {
+            for (int i = 0; i < c.k; ++i)
+                host_decompress(gs[b].zero[i], c.base.primes[i], zero.data() + ((size_t)b * c.k + i) * LABW);
+            cts.resize(c.total_cts);
+            for (uint64_t j = 0; j < c.total_cts; ++j) cts[j] = u128_to_u4(gs[b].cts[j]);
+            reference_to_act_rows(c, cts);
+            dev::h2d(N.blob.as<U4>() + (uint64_t)b * c.total_cts, cts.data(), cts.size() * 16, g_stream);
+            commit[b] = u128_to_u4(gs[b].commit);
+            dev::sync(g_stream);  // cts is reused for the next inference
+        }
+        dev::h2d(N.zero.p, zero.data(), zero.size() * 4, g_stream);
+        dev::h2d(N.commit.p, commit.data(), commit.size() * 16, g_stream);
+        // garbler-only state stays zero on an evaluator network
+        dev::memset0(N.Rb.p, N.Rb.n, g_stream);
+        dev::memset0(N.rk.p, N.rk.n, g_stream);
+        dev::sync(g_stream);
+        *out = n.release();
+    });
+}
+
+int dashgpu_network_circuit(const dashgpu_network* n, const dashgpu_circuit** out) {
+    return guarded([&] {
+        if (!n || !out) throw DataError("null argument");
+        *out = n->net->c;
     });
 }
 

@@ -121,6 +121,9 @@ def _declare(L):
     for n in ("dashgpu_export_gc", "dashgpu_export_encoding", "dashgpu_export_decoding", "dashgpu_export_bundle"):
         getattr(L, n).argtypes = [vp, ctypes.c_uint32, u8p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     L.dashgpu_import_bundle.argtypes = [vp, u8p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(vp)]
+    L.dashgpu_import_gc.argtypes = [ctypes.POINTER(u8p), ctypes.POINTER(ctypes.c_size_t), ctypes.c_uint32,
+                                    ctypes.POINTER(vp)]
+    L.dashgpu_network_circuit.argtypes = [vp, ctypes.POINTER(vp)]
     L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
     L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
     L.dashgpu_infer_stream.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
@@ -248,6 +251,22 @@ class Dash:
         self._check(self.lib.dashgpu_import_bundle(net.h, buf, len(payload), 1 if output else 0, ctypes.byref(h)))
         return Bundle(self, h, net, output)
 
+    def import_gc(self, gcs) -> "GarbledNetwork":
+        """parse_garbled_circuit (garble.cpp:368-403) on the evaluator side:
+        serialized GCs of one circuit -> an evaluator network, inference b
+        evaluating gcs[b] (EvaluatorService GC_TRANSFER, protocol.cpp:309)."""
+        if isinstance(gcs, (bytes, bytearray)):
+            gcs = [gcs]
+        bufs = [(ctypes.c_uint8 * len(g)).from_buffer_copy(g) for g in gcs]
+        ptrs = (u8p * len(bufs))(*[ctypes.cast(b, u8p) for b in bufs])
+        lens = (ctypes.c_size_t * len(bufs))(*[len(g) for g in gcs])
+        h = vp()
+        self._check(self.lib.dashgpu_import_gc(ptrs, lens, len(bufs), ctypes.byref(h)))
+        ch = vp()
+        self._check(self.lib.dashgpu_network_circuit(h, ctypes.byref(ch)))
+        net = GarbledNetwork(self, h, GpuCircuit(self, ch, owned=False), len(bufs))
+        return net
+
     def infer(self, c: "GpuCircuit", seeds, inputs, outputs=None, on_device: bool = False):
         """garble + garble_inputs + evaluate + decode_outputs for every inference.
 
@@ -342,14 +361,15 @@ class Dash:
 
 
 class GpuCircuit:
-    def __init__(self, eng: Dash, h):
-        self.eng, self.h = eng, h
+    def __init__(self, eng: Dash, h, owned: bool = True):
+        self.eng, self.h, self.owned = eng, h, owned
         self.info = CircuitInfo()
         eng._check(eng.lib.dashgpu_circuit_info_get(h, ctypes.byref(self.info)))
 
     def __del__(self):
         try:
-            self.eng.lib.dashgpu_circuit_destroy(self.h)
+            if self.owned:
+                self.eng.lib.dashgpu_circuit_destroy(self.h)
         except Exception:
             pass
 

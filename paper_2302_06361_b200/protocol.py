@@ -1,0 +1,547 @@
+"""Garbler / evaluator session services over the B200 engine.
+
+The reference's protocol layer (proj/core/include/dash/protocol.hpp,
+src/protocol.cpp) is the caller of the hot path: the garbler garbles a
+circuit per session and ships gNN, turns plain inputs into garbled inputs
+and decodes the garbled output; the evaluator holds gNN and evaluates.  This
+module keeps its frame format, payload codecs and session state machines
+byte-compatible and runs every garble / garble_inputs / evaluate /
+decode_outputs on the device through the C ABI:
+
+* GarblerService keeps each session's garbled network resident in HBM
+  (encoding and decoding tables never leave the device; the reference keeps
+  EncodingInfo / DecodingInfo in host memory),
+* EvaluatorService turns GC_TRANSFER bytes into a device network with
+  ``dashgpu_import_gc`` and answers GARBLED_INPUT with one device evaluation.
+
+Transport: frames are plain bytes (``encode_frame`` / ``FrameDecoder``); the
+in-process loopback ``run_local_protocol`` drives both services as the
+reference's does (protocol.cpp:355-435).  The TCP servers of the reference
+(protocol.cpp:437-614) are out of scope: any
+byte stream can carry these frames.
+"""
+from __future__ import annotations
+
+import os
+import struct
+import threading
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from .circuit import ADD, FLATTEN, Circuit, Layer
+from .engine import AuthenticityError, Dash, DataError, Error, GarbledNetwork
+
+MAX_FRAME_PAYLOAD = 1 << 30  # kMaxFramePayload (protocol.hpp:40)
+_MAGIC, _VERSION, _KIND_MODEL = b"DASH", 1, 6  # garble.hpp:21-28 (FileKind::QuantizedModel)
+
+
+class ProtocolError(Error):
+    """dash::ProtocolError"""
+
+
+class FrameType(IntEnum):  # protocol.hpp:24-32
+    MODEL_UPLOAD = 1
+    GC_TRANSFER = 2
+    INPUT_UPLOAD = 3
+    GARBLED_INPUT = 4
+    GARBLED_OUTPUT = 5
+    RESULT = 6
+    ERROR = 7
+
+
+class ErrorCode(IntEnum):  # protocol.hpp:57-61
+    PROTOCOL = 1
+    DATA = 2
+    AUTHENTICITY = 3
+
+
+class Edge(IntEnum):  # protocol.hpp:108-113
+    CLIENT_TO_GARBLER = 1
+    GARBLER_TO_CLIENT = 2
+    GARBLER_TO_EVALUATOR = 3
+    EVALUATOR_TO_GARBLER = 4
+
+
+class Destination(IntEnum):  # protocol.hpp:131
+    REPLY = 1
+    EVALUATOR = 2
+
+
+@dataclass
+class Frame:
+    type: FrameType
+    session: int
+    payload: bytes = b""
+
+
+@dataclass
+class Outbound:
+    dest: Destination
+    frame: Frame
+
+
+@dataclass
+class TraceEntry:
+    edge: Edge
+    type: FrameType
+    payload_bytes: int
+
+
+# ---------------------------------------------------------------- framing
+
+def encode_frame(f: Frame) -> bytes:
+    """length u32 | type u8 | session u128 | payload (protocol.cpp:21-30)."""
+    if len(f.payload) > MAX_FRAME_PAYLOAD:
+        raise ProtocolError("frame payload too large")
+    s = f.session
+    return struct.pack("<IBQQ", 17 + len(f.payload), int(f.type), s & (2**64 - 1), s >> 64) + bytes(f.payload)
+
+
+class FrameDecoder:
+    """Incremental frame parser for byte streams (protocol.cpp:32-60)."""
+
+    def __init__(self):
+        self._buf = bytearray()
+        self._pos = 0
+
+    def feed(self, data: bytes):
+        self._buf += data
+
+    def next(self) -> Optional[Frame]:
+        if len(self._buf) - self._pos < 4:
+            return None
+        (length,) = struct.unpack_from("<I", self._buf, self._pos)
+        if length < 17:
+            raise ProtocolError("frame shorter than its header")
+        if length > 17 + MAX_FRAME_PAYLOAD:
+            raise ProtocolError("frame too large")
+        if len(self._buf) - self._pos < 4 + length:
+            return None
+        t, lo, hi = struct.unpack_from("<BQQ", self._buf, self._pos + 4)
+        if t < 1 or t > 7:
+            raise ProtocolError("unknown frame type")
+        start = self._pos + 4 + 17
+        f = Frame(FrameType(t), (hi << 64) | lo, bytes(self._buf[start:self._pos + 4 + length]))
+        self._pos += 4 + length
+        if self._pos == len(self._buf):
+            self._buf.clear()
+            self._pos = 0
+        elif self._pos > (1 << 20):
+            del self._buf[:self._pos]
+            self._pos = 0
+        return f
+
+
+# ---------------------------------------------------------------- payload codecs
+
+class _Reader:
+    def __init__(self, b: bytes):
+        self.b, self.at = b, 0
+
+    def take(self, fmt: str):
+        n = struct.calcsize(fmt)
+        if len(self.b) - self.at < n:
+            raise DataError("truncated data")
+        v = struct.unpack_from(fmt, self.b, self.at)
+        self.at += n
+        return v if len(v) > 1 else v[0]
+
+    def remaining(self) -> int:
+        return len(self.b) - self.at
+
+
+def encode_error(code: ErrorCode, message: str) -> bytes:
+    m = message.encode()
+    return struct.pack("<BI", int(code), len(m)) + m
+
+
+def decode_error(payload: bytes):
+    r = _Reader(payload)
+    code = r.take("<B")
+    if code < 1 or code > 3:
+        raise ProtocolError("bad error code")
+    n = r.take("<I")
+    if r.remaining() < n:
+        raise DataError("truncated data")
+    return ErrorCode(code), payload[r.at:r.at + n].decode(errors="replace")
+
+
+def serialize_circuit(c: Circuit) -> bytes:
+    """Quantized-circuit container (model_io.cpp:215-239).  Extension layers
+    (Pad2d / Add / DAG inputs) flag bit 1 of the private byte and append
+    src | src2 | pad, as the GC format does."""
+    out = bytearray(_MAGIC + struct.pack("<HB", _VERSION, _KIND_MODEL))
+    out += struct.pack("<BB", c.k, len(c.input_shape))
+    out += struct.pack(f"<{len(c.input_shape)}I", *c.input_shape)
+    out += struct.pack("<ddH", c.alpha, c.sign_target, len(c.layers))
+    for l in c.layers:
+        ext = l.kind > FLATTEN or l.src or l.src2 or l.pad
+        out += struct.pack("<BB6I", l.kind, (1 if l.private_weights else 0) | (2 if ext else 0), l.in_dim,
+                           l.out_dim, l.in_ch, l.out_ch, l.filter, l.stride)
+        for a in (l.q_weights, l.q_biases):
+            v = np.zeros(0, np.int64) if a is None else np.ascontiguousarray(a, np.int64).ravel()
+            out += struct.pack("<Q", v.size) + v.astype("<i8").tobytes()
+        if ext:
+            out += struct.pack("<iiI", l.src, l.src2, l.pad)
+    return bytes(out)
+
+
+def parse_circuit(data: bytes) -> Circuit:
+    """parse_circuit (model_io.cpp:241-280); validate_circuit is the engine's
+    (dashgpu_circuit_create) when the garbler builds the circuit."""
+    r = _Reader(data)
+    if r.take("<4s") != _MAGIC:
+        raise DataError("bad file magic")
+    if r.take("<H") != _VERSION:
+        raise DataError("unsupported format version")
+    if r.take("<B") != _KIND_MODEL:
+        raise DataError("wrong file kind")
+    k = r.take("<B")
+    if k < 1 or k > 16:
+        raise DataError("bad base size")
+    rank = r.take("<B")
+    if rank == 0 or rank > 8:
+        raise DataError("bad input rank")
+    shape = [r.take("<I") for _ in range(rank)]
+    alpha, target, n_layers = r.take("<ddH")
+    layers = []
+    for _ in range(n_layers):
+        kind, flags, *dims = r.take("<BB6I")
+        if kind < 1 or kind > ADD:
+            raise DataError("bad layer kind")
+        l = Layer(kind, bool(flags & 1), *dims)
+        for name, count in (("q_weights", l.weight_count()), ("q_biases", _bias_count(l))):
+            n = r.take("<Q")
+            if n != 0 and n != count:
+                raise DataError("bad weight count" if name == "q_weights" else "bad bias count")
+            if r.remaining() < 8 * n:
+                raise DataError("truncated data")
+            v = np.frombuffer(data, "<i8", n, r.at).astype(np.int64) if n else None
+            r.at += 8 * n
+            setattr(l, name, v)
+        if flags & 2:
+            l.src, l.src2, l.pad = r.take("<iiI")
+        layers.append(l)
+    if r.remaining():
+        raise DataError("trailing bytes in quantized model")
+    return Circuit(shape, k, layers, target, alpha)
+
+
+def _bias_count(l: Layer) -> int:
+    return l.out_dim if l.kind == 1 else (l.out_ch if l.kind == 2 else 0)
+
+
+def encode_model_upload(c: Circuit, owners: int) -> bytes:
+    return struct.pack("<H", owners) + serialize_circuit(c)
+
+
+def decode_model_upload(payload: bytes):
+    if len(payload) < 2:
+        raise DataError("truncated data")
+    return parse_circuit(payload[2:]), struct.unpack_from("<H", payload)[0]
+
+
+def encode_input_upload(owner: int, offset: int, values: Sequence[int]) -> bytes:
+    """owner u16 | offset u32 | count u32 | i16 per element (protocol.cpp:98-110)."""
+    v = np.asarray(values, np.int64)
+    if v.size and (v.min() < -32768 or v.max() > 32767):
+        raise DataError("plain input does not fit the 16-bit wire type")
+    return struct.pack("<HII", owner, offset, v.size) + v.astype("<i2").tobytes()
+
+
+def decode_input_upload(payload: bytes):
+    r = _Reader(payload)
+    owner, offset, count = r.take("<HII")
+    if count * 2 != r.remaining():
+        raise ProtocolError("input upload length mismatch")
+    return owner, offset, np.frombuffer(payload, "<i2", count, r.at).astype(np.int64)
+
+
+def encode_result(values) -> bytes:
+    return np.asarray(values, np.int64).astype("<i8").tobytes()
+
+
+def decode_result(payload: bytes) -> np.ndarray:
+    if len(payload) % 8:
+        raise ProtocolError("result payload length not a multiple of 8")
+    return np.frombuffer(payload, "<i8").astype(np.int64)
+
+
+@dataclass
+class CommVolume:  # protocol.hpp:88-103
+    garbled_in: int
+    garbled_out: int
+    plain_in: int
+    plain_out: int
+
+    def online_bytes(self) -> int:
+        return self.garbled_in + self.garbled_out + self.plain_in + self.plain_out
+
+    def with_overhead(self) -> int:
+        return 2 * self.online_bytes()
+
+
+def comm_volume(k: int, in_size: int, out_size: int) -> CommVolume:
+    return CommVolume(16 * k * in_size, 16 * k * out_size, 2 * in_size, 8 * out_size)
+
+
+def _code_for(e: Exception) -> ErrorCode:
+    if isinstance(e, AuthenticityError):
+        return ErrorCode.AUTHENTICITY
+    if isinstance(e, DataError):
+        return ErrorCode.DATA
+    return ErrorCode.PROTOCOL
+
+
+def _error_frame(session: int, e: Exception) -> Frame:
+    return Frame(FrameType.ERROR, session, encode_error(_code_for(e), str(e)))
+
+
+# ---------------------------------------------------------------- services
+
+@dataclass
+class GarblerConfig:  # protocol.hpp:136-140
+    seed: Optional[bytes] = None  # fixed seed (tests / DASH_SEED); None = fresh per session
+
+
+@dataclass
+class _GarblerSession:
+    net: GarbledNetwork
+    owners: int
+    inputs: np.ndarray
+    filled: np.ndarray
+    phase: str = "inputs"  # inputs -> awaiting -> done | failed
+    filled_count: int = 0
+    result: Optional[np.ndarray] = None
+    error: str = ""
+    error_code: ErrorCode = ErrorCode.PROTOCOL
+
+
+class GarblerService:
+    """The trusted garbling device (protocol.cpp:167-298): garbles on the GPU,
+    keeps the session's encoding / decoding tables in HBM, never ships them."""
+
+    def __init__(self, eng: Dash, cfg: GarblerConfig = None):
+        self.eng, self.cfg = eng, cfg or GarblerConfig()
+        self._mu = threading.Lock()
+        self._sessions: Dict[int, _GarblerSession] = {}
+
+    def handle(self, f: Frame) -> List[Outbound]:
+        try:
+            if f.type == FrameType.MODEL_UPLOAD:
+                return [self._on_model_upload(f)]
+            if f.type == FrameType.INPUT_UPLOAD:
+                out = self._on_input_upload(f)
+                return [out] if out else []
+            if f.type == FrameType.GARBLED_OUTPUT:
+                self._on_garbled_output(f)
+                return []
+            if f.type == FrameType.RESULT:
+                return [self._on_result_request(f)]
+            if f.type == FrameType.ERROR:
+                code, msg = decode_error(f.payload)
+                with self._mu:
+                    s = self._sessions.get(f.session)
+                    if s:
+                        s.phase, s.error, s.error_code = "failed", msg, code
+                return []
+            raise ProtocolError("unexpected frame type for garbler")
+        except Error as e:
+            return [Outbound(Destination.REPLY, _error_frame(f.session, e))]
+
+    def _on_model_upload(self, f: Frame) -> Outbound:
+        circuit, owners = decode_model_upload(f.payload)
+        if owners == 0:
+            raise ProtocolError("at least one input owner required")
+        n_in = circuit.n_in
+        if owners > n_in:
+            raise ProtocolError("more input owners than input elements")
+        seed = self.cfg.seed if self.cfg.seed is not None else os.urandom(16)
+        net = self.eng.garble(self.eng.circuit(circuit), seed)
+        gc = net.export_gc(0)
+        with self._mu:
+            if f.session in self._sessions:
+                raise ProtocolError("session already exists")
+            self._sessions[f.session] = _GarblerSession(net, owners, np.zeros(n_in, np.int64),
+                                                        np.zeros(n_in, bool))
+        return Outbound(Destination.EVALUATOR, Frame(FrameType.GC_TRANSFER, f.session, gc))
+
+    def _on_input_upload(self, f: Frame) -> Optional[Outbound]:
+        owner, offset, values = decode_input_upload(f.payload)
+        with self._mu:
+            s = self._sessions.get(f.session)
+            if s is None:
+                raise ProtocolError("unknown session")
+            if s.phase != "inputs":
+                raise ProtocolError("inputs already complete for this session")
+            if owner >= s.owners:
+                raise ProtocolError("input owner out of range")
+            end = offset + values.size
+            if end > s.inputs.size:
+                raise ProtocolError("input range out of bounds")
+            for i in range(values.size):  # per element, as the reference (partial fills stay)
+                if s.filled[offset + i]:
+                    raise ProtocolError("input element uploaded twice")
+                s.filled[offset + i] = True
+                s.inputs[offset + i] = values[i]
+            s.filled_count += values.size
+            if s.filled_count < s.inputs.size:
+                return None
+            gin = self.eng.garble_inputs(s.net, s.inputs[None, :])
+            s.phase = "awaiting"
+            return Outbound(Destination.EVALUATOR, Frame(FrameType.GARBLED_INPUT, f.session, gin.payload(0)))
+
+    def _on_garbled_output(self, f: Frame):
+        with self._mu:
+            s = self._sessions.get(f.session)
+            if s is None:
+                raise ProtocolError("unknown session")
+            if s.phase != "awaiting":
+                raise ProtocolError("no garbled output expected for this session")
+            try:
+                out = self.eng.import_bundle(s.net, f.payload, True)
+                s.result = self.eng.decode_outputs(s.net, out)[0]
+                s.phase = "done"
+            except Error as e:
+                s.phase, s.error, s.error_code = "failed", str(e), _code_for(e)
+
+    def _on_result_request(self, f: Frame) -> Outbound:
+        if f.payload:
+            raise ProtocolError("result frames to the garbler must be empty")
+        with self._mu:
+            s = self._sessions.get(f.session)
+            if s is None:
+                raise ProtocolError("unknown session")
+            if s.phase == "done":
+                return Outbound(Destination.REPLY, Frame(FrameType.RESULT, f.session, encode_result(s.result)))
+            if s.phase == "failed":
+                return Outbound(Destination.REPLY, Frame(FrameType.ERROR, f.session,
+                                                         encode_error(s.error_code, s.error)))
+            raise ProtocolError("result not ready")
+
+    def session_done(self, session: int) -> bool:
+        with self._mu:
+            s = self._sessions.get(session)
+            return s is not None and s.phase in ("done", "failed")
+
+
+@dataclass
+class _EvaluatorSession:
+    net: GarbledNetwork
+    memory: int
+    used: bool = False
+
+
+class EvaluatorService:
+    """The untrusted inference device (protocol.cpp:303-350): holds gNN in
+    HBM only; each garbled circuit is single-use."""
+
+    def __init__(self, eng: Dash):
+        self.eng = eng
+        self._mu = threading.Lock()
+        self._sessions: Dict[int, _EvaluatorSession] = {}
+
+    def handle(self, f: Frame) -> Optional[Frame]:
+        try:
+            if f.type == FrameType.GC_TRANSFER:
+                net = self.eng.import_gc([f.payload])
+                info = net.circuit.info
+                mem = info.cts * 16 + info.k * 16 + 16 * info.k * info.n_in  # protocol.cpp:347-350
+                with self._mu:
+                    if f.session in self._sessions:
+                        raise ProtocolError("session already has a circuit")
+                    self._sessions[f.session] = _EvaluatorSession(net, mem)
+                return None  # same-connection ordering is the ack
+            if f.type == FrameType.GARBLED_INPUT:
+                with self._mu:
+                    s = self._sessions.get(f.session)
+                    if s is None:
+                        raise ProtocolError("unknown session")
+                    if s.used:
+                        raise ProtocolError("garbled circuit already used (single-use)")
+                    s.used = True
+                gin = self.eng.import_bundle(s.net, f.payload, False)
+                gout = self.eng.evaluate(s.net, gin)
+                return Frame(FrameType.GARBLED_OUTPUT, f.session, gout.payload(0))
+            raise ProtocolError("unexpected frame type for evaluator")
+        except Error as e:
+            return _error_frame(f.session, e)
+
+    def session_memory(self, session: int) -> int:
+        with self._mu:
+            s = self._sessions.get(session)
+            return s.memory if s else 0
+
+
+# ---------------------------------------------------------------- loopback
+
+@dataclass
+class LocalRunResult:
+    outputs: np.ndarray = None
+    trace: List[TraceEntry] = field(default_factory=list)
+
+
+LOOPBACK_SESSION = (0x44415348 << 64) | 1  # make_u128(0x44415348, 1) (protocol.cpp:362)
+
+
+def run_local_protocol(eng: Dash, quantized: Circuit, inputs, owners: int = 1,
+                       cfg: GarblerConfig = None) -> LocalRunResult:
+    """Both services in one process (protocol.cpp:355-435): model upload ->
+    gNN transfer -> per-owner input uploads -> garbled input -> evaluation ->
+    garbled output -> decode -> result request."""
+    x = np.asarray(inputs, np.int64).ravel()
+    if x.size != quantized.n_in:
+        raise DataError("input size does not match the model")
+    if owners == 0:
+        raise DataError("at least one input owner required")
+    garbler, evaluator = GarblerService(eng, cfg), EvaluatorService(eng)
+    session = LOOPBACK_SESSION
+    res = LocalRunResult()
+
+    def to_evaluator(frame: Frame):
+        res.trace.append(TraceEntry(Edge.GARBLER_TO_EVALUATOR, frame.type, len(frame.payload)))
+        reply = evaluator.handle(frame)
+        while reply is not None:
+            res.trace.append(TraceEntry(Edge.EVALUATOR_TO_GARBLER, reply.type, len(reply.payload)))
+            outs = garbler.handle(reply)
+            reply = None
+            for o in outs:
+                if o.dest == Destination.EVALUATOR:
+                    reply = o.frame
+
+    def to_garbler(frame: Frame) -> List[Frame]:
+        res.trace.append(TraceEntry(Edge.CLIENT_TO_GARBLER, frame.type, len(frame.payload)))
+        replies = []
+        for o in garbler.handle(frame):
+            if o.dest == Destination.EVALUATOR:
+                to_evaluator(o.frame)
+            else:
+                replies.append(o.frame)
+        return replies
+
+    def fail_on_error(replies):
+        for r in replies:
+            if r.type == FrameType.ERROR:
+                raise ProtocolError(decode_error(r.payload)[1])
+
+    fail_on_error(to_garbler(Frame(FrameType.MODEL_UPLOAD, session, encode_model_upload(quantized, owners))))
+    n = x.size
+    chunk, extra = divmod(n, owners)
+    offset = 0
+    for o in range(owners):
+        count = chunk + (1 if o < extra else 0)
+        fail_on_error(to_garbler(Frame(FrameType.INPUT_UPLOAD, session,
+                                       encode_input_upload(o, offset, x[offset:offset + count]))))
+        offset += count
+    replies = to_garbler(Frame(FrameType.RESULT, session, b""))
+    if len(replies) != 1:
+        raise ProtocolError("no result reply")
+    res.trace.append(TraceEntry(Edge.GARBLER_TO_CLIENT, replies[0].type, len(replies[0].payload)))
+    if replies[0].type == FrameType.ERROR:
+        code, msg = decode_error(replies[0].payload)
+        raise {ErrorCode.AUTHENTICITY: AuthenticityError, ErrorCode.DATA: DataError}.get(code, ProtocolError)(msg)
+    res.outputs = decode_result(replies[0].payload)
+    return res

@@ -522,3 +522,108 @@ def test_streamed_layer_element_ranges_compose(eng):
         gc[a * uc * 16:b * uc * 16] = gp[0][a * uc * 16:b * uc * 16]
     assert (parts_out == full).all()
     assert bytes(gc) == gcf[0]
+
+
+# ------------------------------------------- evaluator side: GC import (protocol)
+
+def _evaluator_session(eng, oracle, c, seeds, x):
+    """EvaluatorService flow (protocol.cpp:309-331) with the GCs made by the
+    oracle: GC bytes -> import -> evaluate the oracle's garbled inputs; the
+    returned payload must be the oracle evaluator's, byte for byte."""
+    onets = [oracle.garble(c, s) for s in seeds]
+    gcs = [o.gc_bytes() for o in onets]
+    ev = eng.import_gc(gcs)
+    assert ev.batch == len(seeds)
+    for b, g in enumerate(gcs):  # parse -> serialize is the identity
+        assert ev.export_gc(b) == g
+    obi = [oracle.garble_inputs(o, xi) for o, xi in zip(onets, x)]
+    bi = eng.import_bundle(ev, b"".join(o.payload() for o in obi), False)
+    bo = eng.evaluate(ev, bi)
+    for b, o in enumerate(onets):
+        ob = oracle.evaluate(o, obi[b])
+        assert bo.payload(b) == ob.payload(), b
+        # the garbler decodes the returned GARBLED_OUTPUT (GarblerService)
+        assert oracle.decode(o, oracle.bundle_from_payload(o, bo.payload(b), True)).tolist() == \
+            oracle.decode(o, ob).tolist()
+    return ev
+
+
+@pytest.mark.parametrize("private", [False, True])
+def test_import_gc_evaluates_oracle_gcs(eng, oracle, private):
+    from helpers import models
+
+    c = models.build("model_tiny", 1000, 8, private=private)
+    seeds = [seed_hex(0x1E0), seed_hex(0x1E1)]
+    x = np.random.default_rng(11).integers(-7, 8, size=(2, c.n_in))
+    _evaluator_session(eng, oracle, c, seeds, x)
+
+
+def test_import_gc_extension_circuit(eng, oracle):
+    # the extension record is flagged in the private byte, so a DAG circuit parses back
+    c = _small_dag()
+    x = np.random.default_rng(12).integers(-7, 8, size=(1, c.n_in))
+    _evaluator_session(eng, oracle, c, [seed_hex(0x1E5)], x)
+
+
+def test_import_gc_from_engine_garbler(eng):
+    # garbler and evaluator both on the engine: GC bytes travel, labels do not
+    from paper_2302_06361_b200.engine import DataError
+
+    g = eng.model("model_tiny", 1000, 8, private=True)
+    seeds = seed_hex(0x1F0) + seed_hex(0x1F1) + seed_hex(0x1F2)
+    net = eng.garble(g, seeds)
+    x = np.stack([g.random_input(30 + b) for b in range(3)])
+    bi = eng.garble_inputs(net, x)
+    ev = eng.import_gc([net.export_gc(b) for b in range(3)])
+    bo = eng.evaluate(ev, eng.import_bundle(ev, b"".join(bi.payload(b) for b in range(3)), False))
+    back = eng.import_bundle(net, b"".join(bo.payload(b) for b in range(3)), True)
+    assert eng.decode_outputs(net, back).tolist() == [g.plain_forward(xi).tolist() for xi in x]
+    with pytest.raises(DataError):  # the evaluator copy has no private weights
+        eng.garble(ev.circuit, seed_hex(1))
+
+
+def test_import_gc_rejects_bad_files(eng):
+    from paper_2302_06361_b200.engine import DataError
+
+    g = eng.model("relu4", 0, 2)
+    gc = eng.garble(g, seed_hex(2)).export_gc(0)
+    other = eng.garble(eng.model("relu16", 0, 2), seed_hex(2)).export_gc(0)
+    bad = [gc[:-1], gc + b"\0", b"XASH" + gc[4:], gc[:6] + b"\x02" + gc[7:]]
+    cut = 7 + 1 + 1 + 4 + 16 + 1  # header, k, shape, alpha/target, t
+    bad.append(gc[:cut] + b"\x7f" + gc[cut + 1:])  # mixed-radix m_1 odd / out of range
+    for b in bad:
+        with pytest.raises(DataError):
+            eng.import_gc([b])
+    with pytest.raises(DataError):  # a batch must share its circuit
+        eng.import_gc([gc, other])
+
+
+@pytest.mark.parametrize("private", [False, True])
+def test_import_gc_agrees_with_reference_parser(eng, private):
+    # the compiled reference's parse_garbled_circuit + evaluate on the same
+    # bytes: identical GARBLED_OUTPUT, and the same accept / reject verdicts
+    import pyoracle
+    from helpers import models
+    from paper_2302_06361_b200.engine import DataError
+
+    if not pyoracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    ref = pyoracle.RefLib()
+    c = models.build("model_tiny", 1000, 8, private=private)
+    seed = seed_hex(0x1A0)
+    x = np.random.default_rng(13).integers(-7, 8, size=c.n_in)
+    rnet = ref.garble(c, seed)
+    rbi = ref.garble_inputs(rnet, x)
+    gc = rnet.gc_bytes()
+    ev = eng.import_gc([gc])
+    bo = eng.evaluate(ev, eng.import_bundle(ev, rbi.payload(), False))
+    assert bo.payload(0) == ref.eval_gc_bytes(gc, rbi).payload()
+    cut = 7 + 1 + 1 + 4 * gc[8] + 16 + 1  # header, k, shape, alpha / target, t
+    n_layers_at = cut + 2 * gc[cut - 1]
+    for bad in (gc[:-16], gc + b"\0", gc[:4] + b"\x02\x00" + gc[6:], gc[:cut] + b"\x07" + gc[cut + 1:],
+                gc[:n_layers_at + 2] + b"\x09" + gc[n_layers_at + 3:]):
+        with pytest.raises(pyoracle.CheckerError) as e:
+            ref.eval_gc_bytes(bad, rbi)
+        assert e.value.code == 3
+        with pytest.raises(DataError):
+            eng.import_gc([bad])

@@ -1,0 +1,276 @@
+"""Garbler / evaluator services over the engine (paper_2302_06361_b200/protocol.py).
+
+Ports the reference's own protocol tests (proj/tests/unit/test_protocol.cpp)
+case by case; the frame / codec cases need no device, the service cases run
+on the CPU emulation (``emu``) and on the B200 (``cuda``, ``-m gpu``).
+"""
+import numpy as np
+import pytest
+
+from helpers import models, seed_hex
+from paper_2302_06361_b200 import protocol as P
+
+BACKENDS = [pytest.param("emu", id="emu"), pytest.param("cuda", id="cuda", marks=pytest.mark.gpu)]
+
+
+@pytest.fixture(params=BACKENDS)
+def eng(request):
+    return request.getfixturevalue("emu" if request.param == "emu" else "gpu")
+
+
+def tiny():
+    return models.build("model_tiny", 1000, 8)
+
+
+def count_type(trace, t):
+    return sum(1 for e in trace if e.type == t)
+
+
+# ---------------------------------------------------------------- framing (test_protocol.cpp:34-118)
+
+def test_frames_survive_a_byte_by_byte_stream():
+    frames = [P.Frame(P.FrameType.MODEL_UPLOAD, 1, b"abc"), P.Frame(P.FrameType.RESULT, (1 << 127) | 5, b""),
+              P.Frame(P.FrameType.GARBLED_INPUT, 2**64 + 3, bytes(range(256)) * 3)]
+    stream = b""
+    for f in frames:
+        b = P.encode_frame(f)
+        assert len(b) == 4 + 17 + len(f.payload)
+        stream += b
+    dec, got = P.FrameDecoder(), []
+    for i in range(len(stream)):
+        dec.feed(stream[i:i + 1])
+        f = dec.next()
+        if f:
+            got.append(f)
+    assert [(f.type, f.session, f.payload) for f in got] == [(f.type, f.session, f.payload) for f in frames]
+    assert dec.next() is None
+    # wire layout: length | type | session (lo u64, hi u64, little-endian) | payload
+    assert P.encode_frame(P.Frame(P.FrameType.ERROR, 0x0102, b"z")) == \
+        bytes([18, 0, 0, 0, 7, 2, 1]) + bytes(14) + b"z"
+
+
+def test_frame_length_field_is_bounded():
+    dec = P.FrameDecoder()
+    dec.feed(bytes([5, 0, 0, 0]))
+    with pytest.raises(P.ProtocolError):
+        dec.next()
+    big = 17 + (1 << 30) + 1
+    dec2 = P.FrameDecoder()
+    dec2.feed(big.to_bytes(4, "little"))
+    with pytest.raises(P.ProtocolError):
+        dec2.next()
+    dec3 = P.FrameDecoder()
+    dec3.feed(bytes([17, 0, 0, 0, 9]) + bytes(16))
+    with pytest.raises(P.ProtocolError):
+        dec3.next()
+
+
+def test_payload_codecs_roundtrip():
+    code, msg = P.decode_error(P.encode_error(P.ErrorCode.AUTHENTICITY, "bad label"))
+    assert code == P.ErrorCode.AUTHENTICITY and msg == "bad label"
+    c = tiny()
+    mu = P.encode_model_upload(c, 3)
+    c2, owners = P.decode_model_upload(mu)
+    assert owners == 3
+    assert P.serialize_circuit(c2) == P.serialize_circuit(c)
+    assert len(mu) == 2 + len(P.serialize_circuit(c))
+    vals = [-32768, -1, 0, 1, 32767, 5]
+    iu = P.encode_input_upload(4, 19, vals)
+    assert len(iu) == 10 + 2 * len(vals)
+    owner, offset, v = P.decode_input_upload(iu)
+    assert (owner, offset, v.tolist()) == (4, 19, vals)
+    with pytest.raises(P.DataError):
+        P.encode_input_upload(0, 0, [32768])
+    with pytest.raises(P.ProtocolError):
+        P.decode_input_upload(iu[:-1])
+    res = [1, -2, 2**40, -(2**62)]
+    assert P.decode_result(P.encode_result(res)).tolist() == res
+    assert len(P.encode_result(res)) == 8 * len(res)
+    assert P.decode_result(P.encode_result([])).size == 0
+
+
+def test_quantized_model_container_matches_reference_layout():
+    # model_io.cpp:215-239 field by field, and the extension record round trip
+    c = tiny()
+    b = P.serialize_circuit(c)
+    assert b[:7] == b"DASH\x01\x00\x06" and b[7] == 8 and b[8] == 3
+    from test_engine import _small_dag  # noqa: E402
+
+    d = _small_dag()
+    d2 = P.parse_circuit(P.serialize_circuit(d))
+    assert [(l.kind, l.src, l.src2, l.pad) for l in d2.layers] == [(l.kind, l.src, l.src2, l.pad) for l in d.layers]
+    for bad in (b[:-1], b + b"\0", b[:6] + b"\x01" + b[7:]):
+        with pytest.raises(P.DataError):
+            P.parse_circuit(bad)
+
+
+def test_communication_volume_matches_model_dimensions():
+    a = P.comm_volume(8, 784, 10)  # Model A (test_protocol.cpp:120-136)
+    assert (a.garbled_in, a.garbled_out, a.plain_in, a.plain_out) == (100352, 1280, 1568, 80)
+    assert a.online_bytes() == 100352 + 1280 + 1568 + 80 and a.with_overhead() == 2 * a.online_bytes()
+    f = P.comm_volume(9, 3072, 10)
+    assert (f.garbled_in, f.garbled_out, f.plain_in, f.plain_out) == (16 * 9 * 3072, 16 * 9 * 10, 6144, 80)
+
+
+# ---------------------------------------------------------------- services
+
+def _cfg(oracle, s):
+    return P.GarblerConfig(seed=oracle.seed_from_string(s))
+
+
+def test_loopback_computes_plain_result_in_one_round(eng, oracle):
+    c = tiny()
+    x = np.random.default_rng(900).integers(-7, 8, size=c.n_in)
+    run = P.run_local_protocol(eng, c, x, 2, _cfg(oracle, "90a1"))
+    assert run.outputs.tolist() == oracle.plain_forward(c, x).tolist()
+    T = P.FrameType
+    assert count_type(run.trace, T.GARBLED_INPUT) == 1 and count_type(run.trace, T.GARBLED_OUTPUT) == 1
+    assert count_type(run.trace, T.GC_TRANSFER) == 1 and count_type(run.trace, T.INPUT_UPLOAD) == 2
+    assert count_type(run.trace, T.ERROR) == 0
+    assert [e.type for e in run.trace] == [T.MODEL_UPLOAD, T.GC_TRANSFER, T.INPUT_UPLOAD, T.INPUT_UPLOAD,
+                                           T.GARBLED_INPUT, T.GARBLED_OUTPUT, T.RESULT, T.RESULT]
+    n_in = c.n_in
+    assert run.trace[4].payload_bytes == 16 * c.k * n_in
+    assert run.trace[5].payload_bytes == 16 * c.k * 3
+    assert run.trace[6].payload_bytes == 0 and run.trace[7].payload_bytes == 8 * 3
+    assert run.trace[2].payload_bytes == 10 + 2 * (n_in // 2)
+
+
+def test_gc_transfer_is_the_reference_gc(eng, oracle):
+    # what the GPU garbler ships is serialize_garbled_circuit of the reference
+    c = tiny()
+    svc = P.GarblerService(eng, _cfg(oracle, "90a9"))
+    outs = svc.handle(P.Frame(P.FrameType.MODEL_UPLOAD, 3, P.encode_model_upload(c, 1)))
+    assert outs[0].dest == P.Destination.EVALUATOR and outs[0].frame.type == P.FrameType.GC_TRANSFER
+    assert outs[0].frame.payload == oracle.garble(c, oracle.seed_from_string("90a9")).gc_bytes()
+
+
+def test_input_partitioning_does_not_change_garbled_input(eng, oracle):
+    c = tiny()
+    x = np.random.default_rng(901).integers(-7, 8, size=c.n_in)
+
+    def upload(svc, session, owners):
+        outs = svc.handle(P.Frame(P.FrameType.MODEL_UPLOAD, session, P.encode_model_upload(c, owners)))
+        assert len(outs) == 1 and outs[0].frame.type == P.FrameType.GC_TRANSFER
+        gc, gin = outs[0].frame.payload, b""
+        chunk = x.size // owners
+        for o in range(owners):
+            off = o * chunk
+            count = x.size - off if o + 1 == owners else chunk
+            for out in svc.handle(P.Frame(P.FrameType.INPUT_UPLOAD, session,
+                                          P.encode_input_upload(o, off, x[off:off + count]))):
+                assert out.frame.type == P.FrameType.GARBLED_INPUT
+                gin = out.frame.payload
+        return gc, gin
+
+    gc1, gin1 = upload(P.GarblerService(eng, _cfg(oracle, "90a2")), 7, 1)
+    gc3, gin3 = upload(P.GarblerService(eng, _cfg(oracle, "90a2")), 7, 3)
+    assert gc1 == gc3 and gin1 and gin1 == gin3
+
+
+def test_garbled_circuits_are_single_use(eng, oracle):
+    c = tiny()
+    onet = oracle.garble(c, oracle.seed_from_string("90a3"))
+    gin = oracle.garble_inputs(onet, np.random.default_rng(903).integers(-7, 8, size=c.n_in))
+    ev = P.EvaluatorService(eng)
+    assert ev.handle(P.Frame(P.FrameType.GC_TRANSFER, 11, onet.gc_bytes())) is None
+    f = P.Frame(P.FrameType.GARBLED_INPUT, 11, gin.payload())
+    first = ev.handle(f)
+    assert first.type == P.FrameType.GARBLED_OUTPUT and len(first.payload) == 16 * c.k * 3
+    assert first.payload == oracle.evaluate(onet, gin).payload()
+    second = ev.handle(f)
+    assert second.type == P.FrameType.ERROR and P.decode_error(second.payload)[0] == P.ErrorCode.PROTOCOL
+
+
+def test_evaluator_rejects_foreign_sessions_and_bad_bundles(eng, oracle):
+    ev = P.EvaluatorService(eng)
+    orphan = ev.handle(P.Frame(P.FrameType.GARBLED_INPUT, 99, b""))
+    assert orphan.type == P.FrameType.ERROR and P.decode_error(orphan.payload)[0] == P.ErrorCode.PROTOCOL
+    gc = oracle.garble(tiny(), oracle.seed_from_string("90a4")).gc_bytes()
+    ev.handle(P.Frame(P.FrameType.GC_TRANSFER, 12, gc))
+    bad = ev.handle(P.Frame(P.FrameType.GARBLED_INPUT, 12, bytes([1, 2, 3])))
+    assert bad.type == P.FrameType.ERROR and P.decode_error(bad.payload)[0] == P.ErrorCode.DATA
+    dup = ev.handle(P.Frame(P.FrameType.GC_TRANSFER, 12, gc))
+    assert dup is not None and dup.type == P.FrameType.ERROR
+    broken = ev.handle(P.Frame(P.FrameType.GC_TRANSFER, 13, gc[:-3]))
+    assert broken.type == P.FrameType.ERROR and P.decode_error(broken.payload)[0] == P.ErrorCode.DATA
+
+
+def test_evaluator_session_memory(eng, oracle):
+    c = tiny()
+    onet = oracle.garble(c, oracle.seed_from_string("90a5"))
+    ev = P.EvaluatorService(eng)
+    assert ev.session_memory(13) == 0
+    ev.handle(P.Frame(P.FrameType.GC_TRANSFER, 13, onet.gc_bytes()))
+    assert ev.session_memory(13) == onet.cts().size // 2 * 16 + c.k * 16 + 16 * c.k * c.n_in
+
+
+def test_garbler_rejects_bad_uploads(eng, oracle):
+    c = tiny()
+    svc = P.GarblerService(eng, _cfg(oracle, "90a6"))
+    T, s = P.FrameType, 21
+
+    def one(frame):
+        outs = svc.handle(frame)
+        assert len(outs) == 1
+        return outs[0].frame
+
+    f = one(P.Frame(T.MODEL_UPLOAD, s, P.encode_model_upload(c, 0)))
+    assert f.type == T.ERROR and P.decode_error(f.payload)[0] == P.ErrorCode.PROTOCOL
+    assert one(P.Frame(T.MODEL_UPLOAD, s, P.encode_model_upload(c, 1))).type == T.GC_TRANSFER
+    assert one(P.Frame(T.MODEL_UPLOAD, s, P.encode_model_upload(c, 1))).type == T.ERROR
+    f = one(P.Frame(T.RESULT, s, b""))
+    assert f.type == T.ERROR and P.decode_error(f.payload)[0] == P.ErrorCode.PROTOCOL
+    assert one(P.Frame(T.RESULT, s, b"\x01")).type == T.ERROR
+    half = [1] * 36
+    assert svc.handle(P.Frame(T.INPUT_UPLOAD, s, P.encode_input_upload(0, 0, half))) == []
+    f = one(P.Frame(T.INPUT_UPLOAD, s, P.encode_input_upload(0, 0, half)))
+    assert f.type == T.ERROR and P.decode_error(f.payload)[0] == P.ErrorCode.PROTOCOL
+    assert one(P.Frame(T.INPUT_UPLOAD, s, P.encode_input_upload(5, 36, half))).type == T.ERROR
+    assert one(P.Frame(T.INPUT_UPLOAD, s, P.encode_input_upload(0, 60, half))).type == T.ERROR
+    # a model the engine cannot garble is a DATA error
+    bad = tiny()
+    bad.layers[0].q_weights = bad.layers[0].q_weights[:-1]
+    f = one(P.Frame(T.MODEL_UPLOAD, 22, P.encode_model_upload(bad, 1)))
+    assert f.type == T.ERROR and P.decode_error(f.payload)[0] == P.ErrorCode.DATA
+
+
+def test_tampered_garbled_output_fails_with_authenticity(eng, oracle):
+    c = tiny()
+    svc, ev = P.GarblerService(eng, _cfg(oracle, "90a7")), P.EvaluatorService(eng)
+    x = np.random.default_rng(907).integers(-7, 8, size=c.n_in)
+    outs = svc.handle(P.Frame(P.FrameType.MODEL_UPLOAD, 31, P.encode_model_upload(c, 1)))
+    assert ev.handle(outs[0].frame) is None
+    outs = svc.handle(P.Frame(P.FrameType.INPUT_UPLOAD, 31, P.encode_input_upload(0, 0, x)))
+    assert len(outs) == 1 and outs[0].frame.type == P.FrameType.GARBLED_INPUT
+    reply = ev.handle(outs[0].frame)
+    assert reply.type == P.FrameType.GARBLED_OUTPUT
+    payload = bytearray(reply.payload)
+    payload[5] ^= 0x10
+    assert svc.handle(P.Frame(reply.type, 31, bytes(payload))) == []
+    assert svc.session_done(31)
+    outs = svc.handle(P.Frame(P.FrameType.RESULT, 31, b""))
+    assert outs[0].frame.type == P.FrameType.ERROR
+    assert P.decode_error(outs[0].frame.payload)[0] == P.ErrorCode.AUTHENTICITY
+
+
+def test_loopback_honors_owner_count(eng, oracle):
+    c = tiny()
+    x = np.random.default_rng(908).integers(-7, 8, size=c.n_in)
+    want = oracle.plain_forward(c, x).tolist()
+    for owners in (1, 3, 5):
+        run = P.run_local_protocol(eng, c, x, owners, _cfg(oracle, "90a8"))
+        assert run.outputs.tolist() == want
+        assert count_type(run.trace, P.FrameType.INPUT_UPLOAD) == owners
+        assert count_type(run.trace, P.FrameType.GARBLED_INPUT) == 1
+
+
+def test_loopback_private_weights_and_extension_model(eng, oracle):
+    # private-weight layers travel without weights; DAG circuits carry their
+    # extension records through MODEL_UPLOAD and GC_TRANSFER
+    from test_engine import _small_dag
+
+    for c in (models.build("model_tiny", 1000, 8, private=True), _small_dag()):
+        x = np.random.default_rng(909).integers(-7, 8, size=c.n_in)
+        run = P.run_local_protocol(eng, c, x, 2, _cfg(oracle, "90aa"))
+        assert run.outputs.tolist() == oracle.plain_forward(c, x).tolist()
