@@ -825,24 +825,33 @@ DASH_NI void operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, u
 }
 DASH_NI void store_n(U4* slot, LB L, uint32_t m) { *slot = lb_compress(L, c_mod[m]); }
 
-// The garbling row loop of every projection / half gate (one copy):
-// row(a) = (cin + a) mod p, key X + aR_p (X advances), payload
-// base + phi(a) R_q (phi table) or base + (a r mod p) R_p (phi == nullptr);
-// GRR stores row j at R[j-1] and drops row 0 (gadgets.hpp:156-175, 195-219, 244-252).
+// The garbling row loop of every projection / half gate (one copy).  Row
+// r = (cin + a) mod p holds key X + aR_p and payload base + phi(a) R_q (phi
+// table) or base + (a r mod p) R_p (phi == nullptr); GRR stores row j at
+// R[j-1] and has no row 0 (gadgets.hpp:156-175, 195-219, 244-252).  The loop
+// runs in ROW order (a = (r - cin) mod p, the key starts at X + a(r0) R_p and
+// steps by R_p, wrapping since p R_p = 0): every lane of a warp writes the
+// same row of its element, so a warp's stores fill whole 512-byte lines of
+// the interleaved table, and GRR's row 0 is never computed.  X advances.
 DASH_NI void garble_rows_n(LB X, LB base, AesTab t, const uint32_t* mult, uint32_t p, uint32_t q, uint32_t cin,
                            uint64_t g, const uint8_t* phi, uint32_t r, U4* R, int grr, uint32_t rs) {
     const ModC& Mp = c_mod[p];
     const ModC& Mq = c_mod[q];
-    const uint32_t* Rp = mult + ((uint64_t)c_modslot[p] * 128u + 1) * NWMAX;
+    const uint32_t* Mp0 = mult + (uint64_t)c_modslot[p] * 128u * NWMAX;
+    const uint32_t* Rp = Mp0 + NWMAX;
     const uint32_t* Mrow = mult + (uint64_t)c_modslot[q] * 128u * NWMAX;
-    for (uint32_t a = 0; a < p; ++a) {
-        uint32_t row = cin + a;
-        row = row >= p ? row - p : row;
+    const uint32_t r0 = grr ? 1u : 0u;
+    uint32_t a = r0 + p - cin;
+    a = a >= p ? a - p : a;
+    if (a) lb_add_g(X, Mp0 + (uint64_t)a * NWMAX, Mp);
+    U4* out = R;  // row r0 goes to R[0] (GRR: row j at R[j-1])
+    for (uint32_t row = r0; row < p; ++row) {
         const U4 H = hash_tw<true>(lb_key_step(X, Rp, Mp), g, row, 0, t);
         const uint32_t v = phi ? phi[a] : (a * r) % p;
         const U4 ct = lb_enc(H, base, Mrow + (uint64_t)v * NWMAX, nullptr, 0, Mq);
-        if (!grr) store_row(R + (uint64_t)row * rs, ct);
-        else if (row != 0) store_row(R + (uint64_t)(row - 1) * rs, ct);
+        store_row(out, ct);
+        out += rs;
+        a = a + 1 == p ? 0 : a + 1;
     }
 }
 
@@ -911,9 +920,10 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const uint32_t fmask = (1u << fw) - 1u;
             U4 sb;
             sb.x[0] = sb.x[1] = sb.x[2] = sb.x[3] = 0;
-            for (uint32_t b = 0; b < q; ++b) {
-                uint32_t row = cy + b;
-                row = row >= q ? row - q : row;
+            // row order as in garble_rows_n: b = (row - cy) mod q, key y + bR_q
+            uint32_t b = cy ? q - cy : 0;
+            if (b) lb_add_g(e.K, mult_row(e, q, b), Mq);
+            for (uint32_t row = 0; row < q; ++row, b = b + 1 == q ? 0 : b + 1) {
                 uint32_t s = r + b;
                 s = s >= p ? s - p : s;
                 const U4 Kc = lb_key_step(e.K, Rq, Mq);
