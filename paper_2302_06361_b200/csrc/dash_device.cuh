@@ -114,27 +114,34 @@ DASH_HD U4 aes_core(U4 s, const RK& rk, const AesTab& t) {
 #define P2(v, r) bperm((v), L2, 0x5504u | ((r) << 4))
 #define COL(a, b, c, d, k) \
     (tlo(t, P0(a, 0)) ^ tlo(t, P2(c, 2)) ^ rotl32(tlo(t, P0(b, 1)) ^ tlo(t, P2(d, 3)), 8) ^ (k))
-    uint32_t s0 = s.x[0] ^ rk(0), s1 = s.x[1] ^ rk(1), s2 = s.x[2] ^ rk(2), s3 = s.x[3] ^ rk(3);
+    const U4 k0 = rk.round(0);
+    uint32_t s0 = s.x[0] ^ k0.x[0], s1 = s.x[1] ^ k0.x[1], s2 = s.x[2] ^ k0.x[2], s3 = s.x[3] ^ k0.x[3];
 #if defined(__CUDA_ARCH__)
 #pragma unroll kAesUnroll
 #endif
     for (int r = 1; r < 10; ++r) {
-        const uint32_t t0 = COL(s0, s1, s2, s3, rk(4 * r));
-        const uint32_t t1 = COL(s1, s2, s3, s0, rk(4 * r + 1));
-        const uint32_t t2 = COL(s2, s3, s0, s1, rk(4 * r + 2));
-        const uint32_t t3 = COL(s3, s0, s1, s2, rk(4 * r + 3));
+        const U4 k = rk.round(r);  // one 128-bit load per round for keyed AES
+        const uint32_t t0 = COL(s0, s1, s2, s3, k.x[0]);
+        const uint32_t t1 = COL(s1, s2, s3, s0, k.x[1]);
+        const uint32_t t2 = COL(s2, s3, s0, s1, k.x[2]);
+        const uint32_t t3 = COL(s3, s0, s1, s2, k.x[3]);
         s0 = t0;
         s1 = t1;
         s2 = t2;
         s3 = t3;
     }
-    // last round: S-box = byte 1 of T0 (no MixColumns)
-#define SB(v, r) ((tlo(t, P0(v, r)) >> 8) & 0xffu)
+    // last round: S-box = byte 1 of T0 (no MixColumns); three PRMTs gather
+    // the four S-box bytes of a column
+#define SB(v, r) tlo(t, P0(v, r))
+#define GATHER(a, b, c, d) \
+    bperm(bperm(SB(a, 0), SB(b, 1), 0x0051u), bperm(SB(c, 2), SB(d, 3), 0x5100u), 0x7610u)
+    const U4 k10 = rk.round(10);
     U4 o;
-    o.x[0] = (SB(s0, 0) | (SB(s1, 1) << 8) | (SB(s2, 2) << 16) | (SB(s3, 3) << 24)) ^ rk(40);
-    o.x[1] = (SB(s1, 0) | (SB(s2, 1) << 8) | (SB(s3, 2) << 16) | (SB(s0, 3) << 24)) ^ rk(41);
-    o.x[2] = (SB(s2, 0) | (SB(s3, 1) << 8) | (SB(s0, 2) << 16) | (SB(s1, 3) << 24)) ^ rk(42);
-    o.x[3] = (SB(s3, 0) | (SB(s0, 1) << 8) | (SB(s1, 2) << 16) | (SB(s2, 3) << 24)) ^ rk(43);
+    o.x[0] = GATHER(s0, s1, s2, s3) ^ k10.x[0];
+    o.x[1] = GATHER(s1, s2, s3, s0) ^ k10.x[1];
+    o.x[2] = GATHER(s2, s3, s0, s1) ^ k10.x[2];
+    o.x[3] = GATHER(s3, s0, s1, s2) ^ k10.x[3];
+#undef GATHER
 #undef SB
 #undef COL
 #undef P2
@@ -143,16 +150,26 @@ DASH_HD U4 aes_core(U4 s, const RK& rk, const AesTab& t) {
 }
 
 struct RkConst {
-    DASH_HD uint32_t operator()(int i) const { return c_pi_rk[i]; }
+    DASH_HD U4 round(int r) const {
+        U4 k;
+        for (int i = 0; i < 4; ++i) k.x[i] = c_pi_rk[4 * r + i];
+        return k;
+    }
 };
-struct RkPtr {
+struct RkPtr {  // 16-byte aligned schedule (44 words per inference)
     const uint32_t* p;
-    DASH_HD uint32_t operator()(int i) const {
+    DASH_HD U4 round(int r) const {
+        U4 k;
 #if defined(__CUDA_ARCH__)
-        return __ldg(p + i);
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + r);
+        k.x[0] = v.x;
+        k.x[1] = v.y;
+        k.x[2] = v.z;
+        k.x[3] = v.w;
 #else
-        return p[i];
+        for (int i = 0; i < 4; ++i) k.x[i] = p[4 * r + i];
 #endif
+        return k;
     }
 };
 
