@@ -633,15 +633,38 @@ DASH_HD void lb_dec(LB out, const U4& ct, const U4& H, const ModC& M) {
 }
 
 // ---- global label rows: u8 digits, four per word, word stride `stride` ----
+// Words are fetched kRowBatch at a time into registers before any of them is
+// used: L is a generic pointer (shared memory), so a load / store per word
+// would serialise one global-memory latency per word (the compiler cannot
+// prove p and L do not alias).
+constexpr int kRowBatch = 4;
+// (The garbling tape keeps batch 1: it is issue-bound and at its register
+// cap, and its operand loads are a small share of its time.)
+template <int NB = kRowBatch, class F>
+DASH_HD void rows_batched(const uint32_t* p, uint64_t stride, int nw, F&& f) {
+    for (int w0 = 0; w0 < nw; w0 += NB) {
+        uint32_t v[NB];
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+        for (int j = 0; j < NB; ++j) v[j] = w0 + j < nw ? p[(uint64_t)(w0 + j) * stride] : 0u;
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
+        for (int j = 0; j < NB; ++j)
+            if (w0 + j < nw) f(w0 + j, v[j]);
+    }
+}
+
+template <int NB = kRowBatch>
 DASH_HD void lb_load_rows(LB L, const uint32_t* p, uint64_t stride, const ModC& M) {
     if (!M.pow2) {
-        for (int w = 0; w < M.nw; ++w) L[w] = p[(uint64_t)w * stride];
+        rows_batched<NB>(p, stride, M.nw, [&](int w, uint32_t x) { L[w] = x; });
         return;
     }
     U4 acc;
     acc.x[0] = acc.x[1] = acc.x[2] = acc.x[3] = 0;
-    for (int w = 0; w < M.nw; ++w) {
-        const uint32_t x = p[(uint64_t)w * stride];
+    rows_batched<NB>(p, stride, M.nw, [&](int w, uint32_t x) {
         for (int j = 0; j < 4; ++j) {
             const int i = 4 * w + j;
             if (i < M.n) {
@@ -649,7 +672,7 @@ DASH_HD void lb_load_rows(LB L, const uint32_t* p, uint64_t stride, const ModC& 
                 u4_or_shl(acc, d, (uint32_t)(M.e * i));
             }
         }
-    }
+    });
     lb_set_u4(L, acc);
 }
 
@@ -799,12 +822,15 @@ DASH_HD const uint32_t* mult_row(const Elt& e, uint32_t m, uint32_t v) {
 #else
 #define DASH_NI static inline
 #endif
+template <int NB>
 DASH_NI void operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m);
 DASH_NI void store_n(U4* slot, LB L, uint32_t m);
 
+// NB: words of an input-lane operand fetched per batch (rows_batched)
+template <int NB = 1>
 DASH_HD void load_operand(LB L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M) {
-    if (v >= IN_LANE) operand_n(L, P.in[v - IN_LANE] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, nullptr, M.m);
-    else operand_n(L, nullptr, 0, e.slot0 + (uint64_t)v * e.sstride, M.m);
+    if (v >= IN_LANE) operand_n<NB>(L, P.in[v - IN_LANE] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, nullptr, M.m);
+    else operand_n<NB>(L, nullptr, 0, e.slot0 + (uint64_t)v * e.sstride, M.m);
 }
 
 DASH_HD void store_slot(const Elt& e, uint8_t s, LB L, const ModC& M) {
@@ -812,22 +838,24 @@ DASH_HD void store_slot(const Elt& e, uint8_t s, LB L, const ModC& M) {
 }
 
 // L += operand v (streamed, no scratch label)
+template <int NB>
 DASH_NI void add_operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m) {
     const ModC& M = c_mod[m];
     if (!rows) {
         lb_add_c(L, *slot, M);
     } else if (!M.pow2) {
-        for (int w = 0; w < M.nw; ++w) L[w] = swar_add(L[w], rows[(uint64_t)w * E], M);
+        rows_batched<NB>(rows, E, M.nw, [&](int w, uint32_t x) { L[w] = swar_add(L[w], x, M); });
     } else {
         uint32_t tmp[4];
         const LB T{tmp, 1};
-        lb_load_rows(T, rows, E, M);
+        lb_load_rows<NB>(T, rows, E, M);
         lb_add(L, T, M);
     }
 }
+template <int NB = 1>
 DASH_HD void add_operand(LB L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M) {
-    if (v >= IN_LANE) add_operand_n(L, P.in[v - IN_LANE] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, nullptr, M.m);
-    else add_operand_n(L, nullptr, 0, e.slot0 + (uint64_t)v * e.sstride, M.m);
+    if (v >= IN_LANE) add_operand_n<NB>(L, P.in[v - IN_LANE] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, nullptr, M.m);
+    else add_operand_n<NB>(L, nullptr, 0, e.slot0 + (uint64_t)v * e.sstride, M.m);
 }
 
 // Single-copy helpers (called once per gadget, not per row): keeps the
@@ -836,8 +864,9 @@ DASH_NI void prf_n(LB L, uint64_t wire, uint32_t stream, uint32_t m, const uint3
     lb_prf(L, wire, stream, c_mod[m], rk, t);
 }
 // operand from an input lane (row pointer of this element) or from a slot
+template <int NB>
 DASH_NI void operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m) {
-    if (rows) lb_load_rows(L, rows, E, c_mod[m]);
+    if (rows) lb_load_rows<NB>(L, rows, E, c_mod[m]);
     else lb_decompress(L, *slot, c_mod[m]);
 }
 DASH_NI void store_n(U4* slot, LB L, uint32_t m) { *slot = lb_compress(L, c_mod[m]); }
@@ -1022,10 +1051,10 @@ DASH_HD U4 operand_c(LB L, const ActParams& P, const Elt& e, uint8_t v, const Mo
     if (v < IN_LANE) {
         const U4 c = e.slot0[(uint64_t)v * e.sstride];
         colour = colour_c(c, M);
-        if (digits) load_operand(L, P, e, v, M);
+        if (digits) load_operand<kRowBatch>(L, P, e, v, M);
         return c;
     }
-    load_operand(L, P, e, v, M);
+    load_operand<kRowBatch>(L, P, e, v, M);
     colour = lb_color(L, M);
     return lb_compress(L, M);
 }
@@ -1084,22 +1113,22 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
         case OP_ADD:
         case OP_ADDACC: {
             const ModC& M = c_mod[op.qm];
-            if (op.kind == OP_ADD) load_operand(e.A, P, e, op.a, M);
-            add_operand(e.A, P, e, op.b, M);
+            if (op.kind == OP_ADD) load_operand<kRowBatch>(e.A, P, e, op.a, M);
+            add_operand<kRowBatch>(e.A, P, e, op.b, M);
             if (!(op.cst & kKeep)) store_slot(e, op.out, e.A, M);
             break;
         }
         case OP_ADDCONST: {
             if (op.a != op.out) {
                 const ModC& M = c_mod[op.qm];
-                load_operand(e.A, P, e, op.a, M);
+                load_operand<kRowBatch>(e.A, P, e, op.a, M);
                 store_slot(e, op.out, e.A, M);
             }
             break;
         }
         case OP_OUTPUT: {
             const ModC& M = c_mod[op.qm];
-            load_operand(e.A, P, e, op.a, M);
+            load_operand<kRowBatch>(e.A, P, e, op.a, M);
             lb_store_rows(e.A, P.out[op.cst] + ((uint64_t)e.b * M.nw) * P.E + e.u, P.E, M);
             break;
         }
