@@ -152,7 +152,7 @@ class Dash:
     """Handle to the device engine (one CUDA device)."""
 
     def __init__(self, device: int = 0, lib_path: Optional[str] = None):
-        path = lib_path or LIB_PATH
+        path = lib_path or os.environ.get("DASHGPU_LIB") or LIB_PATH  # override: A/B of library builds
         if not os.path.exists(path):
             raise CudaError(f"{path} is not built; run __graft_entry__.build()")
         self.lib = ctypes.CDLL(path)

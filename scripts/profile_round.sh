@@ -11,5 +11,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:act_
   -o gpurun_out/act_garble_b64 python scripts/ncu_target.py 64 > gpurun_out/ncu_act.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_linear -s 0 -c 8 \
   -o gpurun_out/tc_linear_b64 python scripts/ncu_target.py 64 > gpurun_out/ncu_tc.log 2>&1
-tail -2 gpurun_out/ncu_act.log gpurun_out/ncu_tc.log
+tail -n 2 gpurun_out/ncu_act.log gpurun_out/ncu_tc.log
 cat gpurun_out/bench_launch_list.txt
