@@ -762,6 +762,9 @@ struct ActParams {
     // act_output_thread draws them once, the tape's MMHALF (cst = lane + 1)
     // reads them instead of drawing the same PRF labels again
     U4* mmlab;
+    // garbling: `slots` holds max(nslots, nslots_lv) per element, so a small
+    // launch may run the level tape with several warps per element
+    int lv_ok;
 };
 
 // Work map of a multi-layer launch: layer li owns items [base[li], base[li+1]),

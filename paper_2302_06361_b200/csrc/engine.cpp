@@ -856,6 +856,18 @@ static Tape build_tape(int kind, const Crt& b, const SignCtx& s) {
         }
         tp.lv_start.push_back((uint16_t)tp.lv_ops.size());
         if (lns >= IN_LANE) throw DataError("level schedule needs too many label slots");
+        if (std::getenv("DASH_DEBUG_LEVELS")) {
+            for (size_t L = 0; L + 1 < tp.lv_start.size(); ++L) {
+                double cost = 0, mx = 0;
+                for (int i = tp.lv_start[L]; i < tp.lv_start[L + 1]; ++i) {
+                    const auto& o = tp.lv_ops[i];
+                    double c = o.kind == OP_PROJ ? o.pm + (n_digits_host(o.qm) + 3) / 4 : o.kind == OP_GRR ? o.pm : o.kind == OP_HALF ? 2 * o.pm : o.kind == OP_MMHALF ? o.pm + 2 * o.qm : 0;
+                    cost += c;
+                    mx = std::max(mx, c);
+                }
+                fprintf(stderr, "level %zu ops %d cost %.0f max %.0f\n", L, tp.lv_start[L + 1] - tp.lv_start[L], cost, mx);
+            }
+        }
         tp.nslots_lv = lns;
     }
     tp.phi = r.phi;
@@ -1337,6 +1349,10 @@ static int tape_chunks() {
 
 // Runs one layer over B inferences.  garbler: base labels; else active.
 // in2: second operand of the Add extension.
+// level-parallel garbling of an activation layer of `elements` (B x E)
+static bool act_lv_ok(const Tape&, uint64_t elements) { return dev::garble_lv_warps(elements) >= 2; }
+static int act_slots(const Tape& T, bool lv) { return lv ? std::max(T.nslots, T.nslots_lv) : T.nslots; }
+
 static void run_layer(Network& n, size_t li, const HLayer& l, bool garbler, const Lanes& in, const Lanes* in2,
                       Lanes& out) {
     dashgpu_circuit& c = *n.c;
@@ -1466,8 +1482,12 @@ static void run_layer(Network& n, size_t li, const HLayer& l, bool garbler, cons
     P.rk = n.rk.as<uint32_t>();
     P.mult = n.mult.as<uint32_t>();
     P.mult_stride = n.mult_stride;
-    const size_t slot_words = (size_t)l.tape->nslots * n.B * l.E_out;
     if (garbler) {
+        // a layer small enough for level-parallel garbling gets room for the
+        // level tape's slots too (kernels_act.cu act_lv_garble_kernel)
+        const bool lv = act_lv_ok(*l.tape, (uint64_t)n.B * l.E_out);
+        const size_t slot_words = (size_t)act_slots(*l.tape, lv) * n.B * l.E_out;
+        P.lv_ok = lv;
         // Inputs (per-layer planes) stay resident until the combined tape
         // launch; the outputs (pure PRF functions) are written now so the
         // next layer can proceed.
@@ -1518,7 +1538,7 @@ static void network_reserve(Network& n, uint32_t B) {
     size_t slot_total = 0, nact = 0, slot_eval = 0;
     for (const auto& l : c.layers)
         if (l.tape) {
-            slot_total += (size_t)l.tape->nslots * B * l.E_out;
+            slot_total += (size_t)act_slots(*l.tape, act_lv_ok(*l.tape, (uint64_t)B * l.E_out)) * B * l.E_out;
             // warp-per-element evaluation of a small layer uses the level tape's slots
             if ((uint64_t)B * l.E_out <= dev::lane_group_eval_max())
                 slot_eval = std::max(slot_eval, (size_t)l.tape->nslots_lv * B * l.E_out);
@@ -1888,7 +1908,8 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             P.rk = w.rk.as<uint32_t>();
             P.mult = w.mult.as<uint32_t>();
             P.mult_stride = mult_stride;
-            P.slots = w.slots.as<U4>();
+            P.slots = w.slots.as<U4>();  // max(nslots, nslots_lv) per element
+            P.lv_ok = 1;
             P.mmlab = w.mmlab.as<U4>();
             uint16_t primes[MAXK];
             fill_primes(c.base, primes);

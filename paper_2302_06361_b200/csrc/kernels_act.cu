@@ -154,6 +154,54 @@ __global__ void __launch_bounds__(kWpeWarps * 32, 1)
     }
 }
 
+// Small garbling launches (batch-1 latency): W warps per element run the
+// level-scheduled tape (ActParams::lv_tape).  Warp w of an element takes ops
+// w, w+W, ... of every level, each op row-parallel over its 32 lanes
+// (garble_op_w with G = 32), and the element's warps meet at a named barrier
+// between levels.  The wide first levels (an element's k x t projections)
+// then run W ops at a time instead of one.
+constexpr int kLvWords = kWpeShared + NWMAX * 32;  // one lane group (G = 32) per warp
+__global__ void __launch_bounds__(kWpeWarps * 32, 1)
+    act_lv_garble_kernel(const ActParams* __restrict__ layers, ItemMap map, uint32_t W) {
+    fill_T(g_T0);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t grp = warp / W, wi = warp - grp * W, epc = kWpeWarps / W;
+    uint32_t* wb = s_dyn + kTabWords + warp * kLvWords;
+    uint32_t* gb = wb + NWMAX * 32;
+    WpeBufs w;
+    w.X = LB{gb, 1};
+    w.A = LB{gb + NWMAX, 1};
+    w.K = LB{gb + 2 * NWMAX, 1};
+    w.KEY = LB{wb + lane, 32};
+    Elt e;
+    e.X = w.X;
+    e.K = w.K;
+    e.A = w.A;
+    e.t = make_tab(nullptr, lane);
+    const uint32_t item = blockIdx.x * epc + grp;
+    if (item >= map.base[map.n]) return;  // the whole element group leaves together
+    uint32_t li = 0;
+    while (li + 1 < map.n && item >= map.base[li + 1]) ++li;
+    const ActParams& P = layers[li];
+    const uint32_t local = item - map.base[li];
+    e.b = local / P.E;
+    e.u = local - e.b * P.E;
+    e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
+    e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
+    e.rows = act_rows(P.blob + (uint64_t)e.b * P.blob_stride, P.E, P.uc_cts, e.u, e.rs);
+    e.sstride = (uint64_t)P.B * P.E;
+    e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
+    e.rk = P.rk + (uint64_t)e.b * 44;
+    e.mult = P.mult + (uint64_t)e.b * P.mult_stride;
+    for (int L = 0; L < P.n_levels; ++L) {
+        for (int i = P.lv_start[L] + (int)wi; i < P.lv_start[L + 1]; i += (int)W)
+            garble_op_w(P, e, P.lv_tape[i], w, lane, 32);
+        // slots written by this level are read by the next one (bar.sync
+        // orders the element's global-memory accesses among its warps)
+        asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(W * 32) : "memory");
+    }
+}
+
 // Small evaluation launches: one warp per element, the level-scheduled tape
 // (ActParams::lv_tape), lane t takes ops t, t+32, ... of every level.  Each
 // lane keeps its own X / K / A buffers (lane-interleaved, as act_kernel).
@@ -242,6 +290,13 @@ static int sm_count() {
 
 namespace dev {
 uint64_t lane_group_eval_max() { return (uint64_t)sm_count() * kWpeEvalWarps * 32 / 2; }
+// warps per element of the level-parallel garbling launch (0: not used): the
+// largest power of two <= 8 whose warps still fit one wave of 16-warp CTAs
+uint32_t garble_lv_warps(uint64_t elements) {
+    uint32_t W = 8;
+    while (W >= 2 && elements * W > (uint64_t)sm_count() * kWpeWarps) W >>= 1;
+    return W >= 2 ? W : 0;
+}
 }  // namespace dev
 
 void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void* st,
@@ -279,6 +334,30 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         act_wpe_eval_kernel<<<grid, kWpeEvalWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter, G);
         ck(cudaGetLastError(), "act wpe eval launch");
         return;
+    }
+    // level-parallel garbling: W warps per element when the launch is small
+    // enough and every layer's slot region holds the level tape's slots
+    if (garble) {
+        bool lv_ok = true;
+        for (int i = 0; i < n; ++i) lv_ok = lv_ok && host_layers[i].lv_ok;
+        const uint32_t W = lv_ok ? dev::garble_lv_warps(elements) : 0;
+        if (W >= 2) {
+            ItemMap lm;
+            std::memset(&lm, 0, sizeof lm);
+            lm.n = (uint32_t)n;
+            for (int i = 0; i < n; ++i) {
+                lm.wpi[i] = host_layers[i].E;
+                lm.base[i + 1] = lm.base[i] + host_layers[i].B * host_layers[i].E;
+            }
+            const uint32_t epc = kWpeWarps / W;
+            const uint32_t grid = (uint32_t)((lm.base[n] + epc - 1) / epc);
+            const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeWarps * kLvWords;
+            ck(cudaFuncSetAttribute(act_lv_garble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "attr");
+            act_lv_garble_kernel<<<grid, kWpeWarps * 32, smem, S(st)>>>(dev_layers, lm, W);
+            ck(cudaGetLastError(), "act lv garble launch");
+            return;
+        }
     }
     // garbling lane groups: the largest G whose warps fit one wave of 16-warp
     // CTAs; G = 1 is the per-thread kernel below

@@ -29,6 +29,7 @@ void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* m
 // elements up to which an evaluation launch runs in lane groups on the level
 // tape (kernels_act.cu; the engine sizes the level tape's slots for it)
 uint64_t lane_group_eval_max();
+uint32_t garble_lv_warps(uint64_t elements);  // level-parallel garbling (0 = not used)
 // streams / events
 void* stream_create();
 void stream_destroy(void* s);

@@ -56,6 +56,11 @@ void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* m
     }
 }
 uint64_t lane_group_eval_max() { return 148 * 16 * 32 / 2; }
+uint32_t garble_lv_warps(uint64_t elements) {  // kernels_act.cu, 148 SMs x 16 warps
+    uint32_t W = 8;
+    while (W >= 2 && elements * W > 148ull * 16) W >>= 1;
+    return W >= 2 ? W : 0;
+}
 void* stream_create() { return nullptr; }
 void stream_destroy(void*) {}
 void* event_create() { return nullptr; }
@@ -67,7 +72,7 @@ void prof_reset() {}
 int prof_read(double*, uint64_t*, int) { return 0; }
 }  // namespace dev
 
-static void act_layer(const ActParams& P, bool garble) {
+static void act_layer(const ActParams& P, bool garble, bool lv_garble) {
 #pragma omp parallel for collapse(2) schedule(dynamic, 16)
     for (int64_t b = 0; b < (int64_t)P.B; ++b)
         for (int64_t u = 0; u < (int64_t)P.E; ++u) {
@@ -81,7 +86,19 @@ static void act_layer(const ActParams& P, bool garble) {
             e.t = tab();
             e.rk = nullptr;
             e.mult = nullptr;
-            if (garble) {
+            if (garble && lv_garble) {
+                // level-parallel garbling (act_lv_garble_kernel): the level
+                // tape, ops of a level in reverse order (they are independent)
+                e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
+                e.wire0 = P.wire_base + (uint64_t)e.u * P.uc_wires;
+                e.rows = act_rows(P.blob + (uint64_t)e.b * P.blob_stride, P.E, P.uc_cts, e.u, e.rs);
+                e.sstride = (uint64_t)P.B * P.E;
+                e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
+                e.rk = P.rk + (uint64_t)e.b * 44;
+                e.mult = P.mult + (uint64_t)e.b * P.mult_stride;
+                for (int L = 0; L < P.n_levels; ++L)
+                    for (int i = P.lv_start[L + 1] - 1; i >= P.lv_start[L]; --i) garble_op(P, e, P.lv_tape[i]);
+            } else if (garble) {
                 act_element<true>(P, e, 0, P.n_ops);
             } else if ((uint64_t)P.B * P.E <= dev::lane_group_eval_max() && P.n_levels > 0) {
                 // small launches: the level-scheduled tape, as the CUDA
@@ -102,8 +119,14 @@ static void act_layer(const ActParams& P, bool garble) {
 
 void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void*,
                       const Sched&) {
-    (void)host_layers;
-    for (int i = 0; i < n; ++i) act_layer(dev_layers[i], garble);
+    uint64_t elements = 0;
+    bool lv_ok = true;
+    for (int i = 0; i < n; ++i) {
+        elements += (uint64_t)host_layers[i].B * host_layers[i].E;
+        lv_ok = lv_ok && host_layers[i].lv_ok;
+    }
+    const bool lv = garble && lv_ok && dev::garble_lv_warps(elements) >= 2;
+    for (int i = 0; i < n; ++i) act_layer(dev_layers[i], garble, lv);
 }
 
 void launch_act_outputs(const ActParams& P, const uint16_t* primes, void*) {
