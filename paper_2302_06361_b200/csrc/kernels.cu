@@ -18,6 +18,7 @@ __device__ uint32_t g_T0[256];
 #include "dash_prim.cuh"
 #include "kernels_common.cuh"
 #include "tc_linear.cuh"
+#include "wpe.cuh"
 
 namespace dashgpu {
 
@@ -202,6 +203,38 @@ __global__ void __launch_bounds__(128) setup_labels_kernel(SetupParams Sp) {
     const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e > Sp.n_in) return;
     setup_labels_thread(Sp, blockIdx.z, e, (int)blockIdx.y, make_tab(nullptr, threadIdx.x & 31u));
+}
+
+// Small launches: one warp per label (PRF counter blocks over the lanes,
+// prf_coop); same values as setup_labels_thread.
+constexpr int kLabWarps = 8;
+__global__ void __launch_bounds__(kLabWarps * 32) setup_labels_warp_kernel(SetupParams Sp) {
+    fill_T(g_T0);
+    const uint32_t lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const uint32_t idx = blockIdx.x * kLabWarps + wl, b = blockIdx.y;
+    const uint32_t i = idx % (uint32_t)Sp.k, e = idx / (uint32_t)Sp.k;
+    if (e > Sp.n_in) return;  // whole warp
+    const LB L{s_dyn + kTabWords + wl * NWMAX, 1};
+    const AesTab t = make_tab(nullptr, lane);
+    const uint32_t p = Sp.primes[i];
+    const ModC& M = c_mod[p];
+    const uint32_t* rk = Sp.rk + (uint64_t)b * 44;
+    // e < n_in: input base of element e, lane i (wire k + e*k + i); e == n_in: zero wire i
+    const uint64_t wire = e < Sp.n_in ? (uint64_t)Sp.k + (Sp.e0 + e) * Sp.k + (uint64_t)i : (uint64_t)i;
+    prf_coop(L, wire, 0, p, rk, t, lane, 32);
+    if (lane != 0) return;
+    if (e < Sp.n_in) lb_store_rows(L, Sp.base_planes[i] + ((uint64_t)b * M.nw) * Sp.n_in + e, Sp.n_in, M);
+    else lb_store_rows(L, Sp.zero + ((uint64_t)b * Sp.k + i) * LABW, 1, M);
+    if (e == Sp.n_in && i == 0) {  // seed commitment = davies_meyer(seed bytes read little-endian)
+        const uint8_t* sd = Sp.seeds + (uint64_t)b * 16;
+        U4 v;
+        for (int j = 0; j < 4; ++j)
+            v.x[j] = (uint32_t)sd[4 * j] | ((uint32_t)sd[4 * j + 1] << 8) | ((uint32_t)sd[4 * j + 2] << 16) |
+                     ((uint32_t)sd[4 * j + 3] << 24);
+        U4 h = aes_pi(v, t);
+        for (int j = 0; j < 4; ++j) h.x[j] ^= v.x[j];
+        Sp.commit[b] = h;
+    }
 }
 
 __global__ void __launch_bounds__(128) encode_kernel(EncodeParams P) {
@@ -469,8 +502,21 @@ void launch_setup(const SetupParams& Sp, void* st) {
     ck(cudaFuncSetAttribute(setup_offsets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
     setup_offsets_kernel<<<dim3(Sp.nslot, Sp.B), 128, kTabBytes, S(st)>>>(Sp);
     dev::check();
-    ck(cudaFuncSetAttribute(setup_labels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
-    setup_labels_kernel<<<dim3(cdiv(Sp.n_in + 1, 128), Sp.k, Sp.B), 128, kTabBytes, S(st)>>>(Sp);
+    const uint64_t labels = (uint64_t)(Sp.n_in + 1) * Sp.k * Sp.B;
+    int sms = 0, devi = 0;
+    ck(cudaGetDevice(&devi), "dev");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, devi), "sms");
+    if (labels <= (uint64_t)sms * 24 * 2) {  // <= two waves of warps: one warp per label
+        const size_t smem = kTabBytes + sizeof(uint32_t) * kLabWarps * NWMAX;
+        ck(cudaFuncSetAttribute(setup_labels_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+           "attr");
+        setup_labels_warp_kernel<<<dim3(cdiv((uint64_t)(Sp.n_in + 1) * Sp.k, kLabWarps), Sp.B), kLabWarps * 32, smem,
+                                   S(st)>>>(Sp);
+    } else {
+        ck(cudaFuncSetAttribute(setup_labels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes),
+           "attr");
+        setup_labels_kernel<<<dim3(cdiv(Sp.n_in + 1, 128), Sp.k, Sp.B), 128, kTabBytes, S(st)>>>(Sp);
+    }
     dev::check();
 }
 

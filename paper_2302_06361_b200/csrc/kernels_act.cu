@@ -269,6 +269,40 @@ __global__ void __launch_bounds__(256) act_out_kernel(ActParams P, Primes pr, ui
                       make_tab(nullptr, threadIdx.x & 31u));
 }
 
+// Small launches: one warp per (inference, element, lane) output label, the
+// PRF counter blocks split over the 32 lanes (prf_coop); lane 0 finishes the
+// label.  Same values as act_output_thread.
+constexpr int kOutWarps = 8;
+__global__ void __launch_bounds__(kOutWarps * 32) act_out_warp_kernel(ActParams P, Primes pr) {
+    fill_T(g_T0);
+    const uint32_t lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const uint32_t idx = blockIdx.x * kOutWarps + wl;
+    const uint32_t i = idx % (uint32_t)P.k, u = idx / (uint32_t)P.k, b = blockIdx.y;
+    if (u >= P.E) return;  // whole warp
+    LB A{s_dyn + kTabWords + wl * 2 * NWMAX, 1}, T{s_dyn + kTabWords + wl * 2 * NWMAX + NWMAX, 1};
+    const AesTab t = make_tab(nullptr, lane);
+    const uint32_t p = pr.p[i];
+    const ModC& M = c_mod[p];
+    const uint32_t* rk = P.rk + (uint64_t)b * 44;
+    const uint64_t w = P.wire_base + (uint64_t)u * P.uc_wires + P.out_wire[i];
+    prf_coop(A, w, 0, p, rk, t, lane, 32);
+    const bool mm = P.out_kind[i] == OP_MMHALF;
+    if (mm) prf_coop(T, w + 1, 0, p, rk, t, lane, 32);
+    if (lane == 0) {
+        if (mm) {  // out = v0 - u0 (gadgets.hpp:354)
+            if (P.mmlab) {
+                U4* ml = P.mmlab + (((uint64_t)b * P.E + u) * P.k + i) * 2;
+                ml[0] = lb_compress(A, M);
+                ml[1] = lb_compress(T, M);
+            }
+            lb_sub(T, A, M);
+            lb_store_rows(T, P.out[i] + ((uint64_t)b * M.nw) * P.E + u, P.E, M);
+        } else {
+            lb_store_rows(A, P.out[i] + ((uint64_t)b * M.nw) * P.E + u, P.E, M);
+        }
+    }
+}
+
 }  // namespace
 
 void upload_act(const ModC* mods, const uint32_t* pi_rk, const uint16_t* modslot, const uint32_t* T0) {
@@ -420,6 +454,15 @@ void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* st) {
     ProfScope ps(K_SETUP, S(st));
     Primes pr;
     for (int i = 0; i < MAXK; ++i) pr.p[i] = i < P.k ? primes[i] : 0;
+    const uint64_t labels = (uint64_t)P.B * P.E * P.k;
+    if (labels <= (uint64_t)sm_count() * 24 * 2) {  // <= two waves of warps: one warp per label
+        const size_t smem = kTabBytes + sizeof(uint32_t) * kOutWarps * 2 * NWMAX;
+        ck(cudaFuncSetAttribute(act_out_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+           "attr");
+        act_out_warp_kernel<<<dim3(cdiv((uint64_t)P.E * P.k, kOutWarps), P.B), kOutWarps * 32, smem, S(st)>>>(P, pr);
+        ck(cudaGetLastError(), "act outputs launch");
+        return;
+    }
     const uint32_t epad = (P.E + 31) / 32 * 32;
     ck(cudaFuncSetAttribute(act_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
     act_out_kernel<<<dim3(cdiv((uint64_t)epad * P.k, 256), P.B), 256, kTabBytes, S(st)>>>(P, pr, epad);

@@ -27,7 +27,7 @@ struct WpeBufs {
 };
 
 // LabelPrf::draw (prf.cpp:11-27) with the counter blocks split over the lanes
-__device__ void prf_coop(LB L, uint64_t wire, uint32_t stream, uint32_t m, const uint32_t* rk, const AesTab& t,
+static __device__ void prf_coop(LB L, uint64_t wire, uint32_t stream, uint32_t m, const uint32_t* rk, const AesTab& t,
                          uint32_t j, uint32_t G) {
     const ModC& M = c_mod[m];
     const int nb = (M.n + 3) / 4;
@@ -65,7 +65,7 @@ __device__ void prf_coop(LB L, uint64_t wire, uint32_t stream, uint32_t m, const
 
 // The rows of a projection / half gate (garble_rows_n), lane a mod 32 takes row
 // (cin + a) mod p with key X + a R_p and payload base + v(a) R_q.
-__device__ void garble_rows_w(LB X, LB base, LB KEY, const AesTab& t, const uint32_t* mult, uint32_t p, uint32_t q,
+static __device__ void garble_rows_w(LB X, LB base, LB KEY, const AesTab& t, const uint32_t* mult, uint32_t p, uint32_t q,
                               uint32_t cin, uint64_t g, const uint8_t* phi, uint32_t r, U4* R, int grr,
                               uint32_t rs, uint32_t j, uint32_t G) {
     const ModC& Mp = c_mod[p];
@@ -86,12 +86,12 @@ __device__ void garble_rows_w(LB X, LB base, LB KEY, const AesTab& t, const uint
     __syncwarp();
 }
 
-__device__ void load_w(LB L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M, uint32_t j) {
+static __device__ void load_w(LB L, const ActParams& P, const Elt& e, uint8_t v, const ModC& M, uint32_t j) {
     if (j == 0) load_operand(L, P, e, v, M);
     __syncwarp();
 }
 
-__device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const WpeBufs& w, uint32_t j,
+static __device__ void garble_op_w(const ActParams& P, Elt& e, const TapeOp& op, const WpeBufs& w, uint32_t j,
                             uint32_t G) {
     switch (op.kind) {
         case OP_PROJ:
