@@ -448,7 +448,7 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
             encode_u8_2d(&amaps.m[i], Ls[i].in, (uint64_t)4 * L0.E_in, (uint64_t)Ls[i].B * Ls[i].nw,
                          (uint64_t)4 * L0.E_in, (uint32_t)tc::BKB, (uint32_t)tc::BM);
     const size_t smem = tc::smem_bytes(T.BN);
-    ck(cudaFuncSetAttribute(tc::tc_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+    smem_attr((const void*)tc::tc_linear_kernel, smem);
     CUtensorMap map;
     memcpy(&map, T.tmap, sizeof map);
     tc::tc_linear_kernel<<<tiles, tc::kThreads, smem, S(st)>>>(map, P, amaps);
@@ -466,10 +466,10 @@ void launch_private(const PrivParams& P, void* st, const Sched& q) {
     const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kPrivWarps * kPrivWarpWords;
     const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sms, cdiv((uint64_t)P.B * P.M, 1));
     if (P.garbler) {
-        ck(cudaFuncSetAttribute(private_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        smem_attr((const void*)private_kernel<true>, smem);
         private_kernel<true><<<grid, kPrivWarps * 32, smem, S(st)>>>(P, counter);
     } else {
-        ck(cudaFuncSetAttribute(private_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        smem_attr((const void*)private_kernel<false>, smem);
         private_kernel<false><<<grid, kPrivWarps * 32, smem, S(st)>>>(P, counter);
     }
     dev::check();
@@ -485,7 +485,7 @@ void launch_pad_add(const PadAddParams& P, void* st) {
 void launch_proj(const ProjParams& P, void* st) {
     if (P.n == 0) return;
     ProfScope ps(K_MISC, S(st));
-    ck(cudaFuncSetAttribute(proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    smem_attr((const void*)proj_kernel, kTabBytes);
     proj_kernel<<<cdiv(P.n, 128), 128, kTabBytes, S(st)>>>(P);
     dev::check();
 }
@@ -499,22 +499,23 @@ void launch_expand(const uint8_t* seeds, uint32_t* rk, uint32_t B, void* st) {
 
 void launch_setup(const SetupParams& Sp, void* st) {
     ProfScope ps(K_SETUP, S(st));
-    ck(cudaFuncSetAttribute(setup_offsets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    smem_attr((const void*)setup_offsets_kernel, kTabBytes);
     setup_offsets_kernel<<<dim3(Sp.nslot, Sp.B), 128, kTabBytes, S(st)>>>(Sp);
     dev::check();
     const uint64_t labels = (uint64_t)(Sp.n_in + 1) * Sp.k * Sp.B;
-    int sms = 0, devi = 0;
-    ck(cudaGetDevice(&devi), "dev");
-    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, devi), "sms");
+    static int sms = 0;
+    if (!sms) {
+        int devi = 0;
+        ck(cudaGetDevice(&devi), "dev");
+        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, devi), "sms");
+    }
     if (labels <= (uint64_t)sms * 24 * 2) {  // <= two waves of warps: one warp per label
         const size_t smem = kTabBytes + sizeof(uint32_t) * kLabWarps * NWMAX;
-        ck(cudaFuncSetAttribute(setup_labels_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-           "attr");
+        smem_attr((const void*)setup_labels_warp_kernel, smem);
         setup_labels_warp_kernel<<<dim3(cdiv((uint64_t)(Sp.n_in + 1) * Sp.k, kLabWarps), Sp.B), kLabWarps * 32, smem,
                                    S(st)>>>(Sp);
     } else {
-        ck(cudaFuncSetAttribute(setup_labels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes),
-           "attr");
+        smem_attr((const void*)setup_labels_kernel, kTabBytes);
         setup_labels_kernel<<<dim3(cdiv(Sp.n_in + 1, 128), Sp.k, Sp.B), 128, kTabBytes, S(st)>>>(Sp);
     }
     dev::check();
@@ -551,7 +552,7 @@ void launch_decompress(const CompressParams& P, uint32_t* lane_out, void* st) {
 }
 
 void launch_prim(const PrimParams& P, void* st) {
-    ck(cudaFuncSetAttribute(prim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    smem_attr((const void*)prim_kernel, kTabBytes);
     prim_kernel<<<cdiv(P.n, 128), 128, kTabBytes, S(st)>>>(P);
     dev::check();
 }

@@ -363,8 +363,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), wm.base[n]);  // spread: latency-bound
         const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeEvalWarps * kLaneWordsEval * 32;
         ck(cudaMemsetAsync(q.counter, 0, sizeof(uint32_t), S(st)), "counter reset");
-        ck(cudaFuncSetAttribute(act_wpe_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-           "attr");
+        smem_attr((const void*)act_wpe_eval_kernel, smem);
         act_wpe_eval_kernel<<<grid, kWpeEvalWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter, G);
         ck(cudaGetLastError(), "act wpe eval launch");
         return;
@@ -386,8 +385,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
             const uint32_t epc = kWpeWarps / W;
             const uint32_t grid = (uint32_t)((lm.base[n] + epc - 1) / epc);
             const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeWarps * kLvWords;
-            ck(cudaFuncSetAttribute(act_lv_garble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "attr");
+            smem_attr((const void*)act_lv_garble_kernel, smem);
             act_lv_garble_kernel<<<grid, kWpeWarps * 32, smem, S(st)>>>(dev_layers, lm, W);
             ck(cudaGetLastError(), "act lv garble launch");
             return;
@@ -409,7 +407,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)sm_count(), wm.base[n]);  // spread: latency-bound
         const size_t smem = kTabBytes + sizeof(uint32_t) * (size_t)kWpeWarps * kWpeWords;
         ck(cudaMemsetAsync(q.counter, 0, sizeof(uint32_t), S(st)), "counter reset");
-        ck(cudaFuncSetAttribute(act_wpe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        smem_attr((const void*)act_wpe_kernel, smem);
         act_wpe_kernel<<<grid, kWpeWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter, Gg);
         ck(cudaGetLastError(), "act wpe launch");
         return;
@@ -440,10 +438,10 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         ck(cudaMemsetAsync(flags, 0, sizeof(uint32_t) * map.base[n], S(st)), "flags reset");
     }
     if (garble) {
-        ck(cudaFuncSetAttribute(act_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        smem_attr((const void*)act_kernel<true>, smem);
         act_kernel<true><<<grid, warps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, nchunks);
     } else {
-        ck(cudaFuncSetAttribute(act_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "attr");
+        smem_attr((const void*)act_kernel<false>, smem);
         act_kernel<false><<<grid, warps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, 1);
     }
     ck(cudaGetLastError(), "act launch");
@@ -457,14 +455,13 @@ void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* st) {
     const uint64_t labels = (uint64_t)P.B * P.E * P.k;
     if (labels <= (uint64_t)sm_count() * 24 * 2) {  // <= two waves of warps: one warp per label
         const size_t smem = kTabBytes + sizeof(uint32_t) * kOutWarps * 2 * NWMAX;
-        ck(cudaFuncSetAttribute(act_out_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-           "attr");
+        smem_attr((const void*)act_out_warp_kernel, smem);
         act_out_warp_kernel<<<dim3(cdiv((uint64_t)P.E * P.k, kOutWarps), P.B), kOutWarps * 32, smem, S(st)>>>(P, pr);
         ck(cudaGetLastError(), "act outputs launch");
         return;
     }
     const uint32_t epad = (P.E + 31) / 32 * 32;
-    ck(cudaFuncSetAttribute(act_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTabBytes), "attr");
+    smem_attr((const void*)act_out_kernel, kTabBytes);
     act_out_kernel<<<dim3(cdiv((uint64_t)epad * P.k, 256), P.B), 256, kTabBytes, S(st)>>>(P, pr, epad);
     ck(cudaGetLastError(), "act outputs launch");
 }

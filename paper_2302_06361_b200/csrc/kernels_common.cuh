@@ -2,6 +2,8 @@
 // Each TU defines its own copy of the constant tables (no relocatable device
 // code) before including this header; dev::upload_constants() fills both.
 #pragma once
+#include <mutex>
+#include <unordered_map>
 
 #include <cuda_runtime.h>
 
@@ -27,6 +29,17 @@ inline void ck(cudaError_t e, const char* what) {
 }
 inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 inline uint32_t cdiv(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size:
+// the call costs microseconds, and small launches are latency-bound
+inline void smem_attr(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& v = done[fn];
+    if (v >= bytes) return;
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), "attr");
+    v = bytes;
+}
 
 // ---- per-kind CUDA-event timing on the launching stream (kernels.cu owns it)
 struct ProfData {
