@@ -627,3 +627,25 @@ def test_import_gc_agrees_with_reference_parser(eng, private):
         assert e.value.code == 3
         with pytest.raises(DataError):
             eng.import_gc([bad])
+
+
+@pytest.mark.gpu
+def test_launch_shapes_agree(gpu):
+    # Model A: batch 1 takes the level-parallel garbling and warp-per-label
+    # PRF kernels, batch 8 the lane-group kernels, batch 160 the per-thread
+    # persistent kernels; inference 0 (same seed, same input) must produce
+    # the same garbled circuit, decoding tables and garbled output bytes
+    g = gpu.model("model_a", 1001, 8)
+    x0 = g.random_input(77)
+    ref = None
+    for B in (1, 8, 160):
+        seeds = b"".join(seed_hex(0xAB00 + b) for b in range(B))
+        x = np.stack([x0] + [g.random_input(78 + b) for b in range(1, B)])
+        net = gpu.garble(g, seeds)
+        bo = gpu.evaluate(net, gpu.garble_inputs(net, x))
+        got = (sha(net.export_gc(0)), sha(net.export_decoding(0)), bo.payload(0),
+               gpu.decode_outputs(net, bo)[0].tolist())
+        if ref is None:
+            ref = got
+            assert got[3] == g.plain_forward(x0).tolist()
+        assert got == ref, B
