@@ -528,6 +528,33 @@ DASH_HD void digits_stream(const U4& cin, const ModC& M, F&& f) {
     }
 }
 
+// digits_stream of two values in one loop: two independent division chains
+// interleave (evaluation decrypts ct - pad; its latency is this chain)
+template <class F>
+DASH_HD void digits_stream2(const U4& x, const U4& y, const ModC& M, F&& f) {
+    uint32_t a[4] = {x.x[0], x.x[1], x.x[2], x.x[3]}, b[4] = {y.x[0], y.x[1], y.x[2], y.x[3]};
+    const uint32_t keep = top_keep(M);
+    int w = 0;
+    for (int j = 0; j < M.nchunks; ++j) {
+        uint32_t ca = divmod_D(a, M, M.limbs[j]);
+        uint32_t cb = divmod_D(b, M, M.limbs[j]);
+#if defined(__CUDA_ARCH__)
+#pragma unroll kCodecUnroll
+#endif
+        for (int ww = 0; ww < M.W && w < M.nw; ++ww, ++w) {
+            const uint32_t qa = fdiv(ca, M.mag_m4, M.sh_m4), qb = fdiv(cb, M.mag_m4, M.sh_m4);
+            uint32_t va = split4(ca - qa * M.m4, M), vb = split4(cb - qb * M.m4, M);
+            ca = qa;
+            cb = qb;
+            if (w == M.nw - 1) {
+                va &= keep;
+                vb &= keep;
+            }
+            f(w, va, vb);
+        }
+    }
+}
+
 DASH_HD void lb_decompress(LB out, const U4& c, const ModC& M) {
     if (M.pow2) {
         U4 v;
@@ -628,8 +655,7 @@ DASH_HD void lb_dec(LB out, const U4& ct, const U4& H, const ModC& M) {
         lb_set_u4(out, p2_sub(a, b, M));
         return;
     }
-    lb_decompress(out, ct, M);
-    digits_stream(H, M, [&](int w, uint32_t v) { out[w] = swar_add(out[w], M.spread - v, M); });
+    digits_stream2(ct, H, M, [&](int w, uint32_t a, uint32_t h) { out[w] = swar_add(a, M.spread - h, M); });
 }
 
 // ---- global label rows: u8 digits, four per word, word stride `stride` ----
@@ -1098,7 +1124,8 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
             const U4 Ky = operand_c(e.K, P, e, op.b, Mq, cy, false);
             // u = Dec(x, {g,cx,0}); out = Dec(y, {g,cy,1}) (+ s x) - u, all streamed
             const U4 Hx = hash_tw(Xc, g, cx, 0, e.t);
-            lb_dec(e.A, R[(uint64_t)(p + cy) * e.rs], hash_tw(Ky, g, cy, 1, e.t), Mp);
+            const U4 Hy = hash_tw(Ky, g, cy, 1, e.t);
+            const U4 cty = R[(uint64_t)(p + cy) * e.rs], ctx = R[(uint64_t)cx * e.rs];
             uint32_t s = cy;
             if (mm) {  // decrypt_short (cipher.cpp:62-69)
                 const uint32_t fw = field_width(p);
@@ -1107,9 +1134,19 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
                 const uint32_t field = u4_shr_low(R[(uint64_t)(p + q) * e.rs], fw * cy) & fmask;
                 s = ((field ^ (Hs.x[0] & fmask)) & fmask) % p;
             }
-            lb_add_scaled(e.A, e.X, s, Mp);
-            lb_sub_c(e.A, R[(uint64_t)cx * e.rs], Mp);  // - u = - (decompress(ct_x) - pad_x)
-            lb_add_c(e.A, Hx, Mp);
+            if (Mp.pow2) {
+                lb_dec(e.A, cty, Hy, Mp);
+                lb_add_scaled(e.A, e.X, s, Mp);
+                lb_sub_c(e.A, ctx, Mp);  // - u = - (decompress(ct_x) - pad_x)
+                lb_add_c(e.A, Hx, Mp);
+            } else {  // the same sums, two decryptions per loop (digits_stream2)
+                digits_stream2(cty, Hy, Mp, [&](int w, uint32_t a, uint32_t h) {
+                    e.A[w] = swar_add(swar_add(a, Mp.spread - h, Mp), scale_word(e.X[w], s, Mp), Mp);
+                });
+                digits_stream2(ctx, Hx, Mp, [&](int w, uint32_t c, uint32_t h) {
+                    e.A[w] = swar_add(e.A[w], swar_add(h, Mp.spread - c, Mp), Mp);
+                });
+            }
             store_slot(e, op.out, e.A, Mp);
             break;
         }
