@@ -658,6 +658,33 @@ DASH_HD void lb_dec(LB out, const U4& ct, const U4& H, const ModC& M) {
     digits_stream2(ct, H, M, [&](int w, uint32_t a, uint32_t h) { out[w] = swar_add(a, M.spread - h, M); });
 }
 
+// compress(decompress_mod(ct) - decompress_mod(H)): the decrypted label
+// straight into its compressed slot form, accumulated low word first in the
+// decryption loop (no digit buffer, no second Horner pass)
+DASH_HD U4 lb_dec_c(const U4& ct, const U4& H, const ModC& M) {
+    if (M.pow2) {
+        U4 a, b;
+        for (int i = 0; i < 4; ++i) {
+            a.x[i] = ct.x[i] & M.bits[i];
+            b.x[i] = H.x[i] & M.bits[i];
+        }
+        return p2_sub(a, b, M);
+    }
+    uint32_t c[4] = {0, 0, 0, 0}, pw[4] = {1, 0, 0, 0};
+    digits_stream2(ct, H, M, [&](int, uint32_t a, uint32_t h) {
+        const uint32_t t = swar_add(a, M.spread - h, M);
+        const uint32_t cv = (t & 0xff) + M.m * (((t >> 8) & 0xff) + M.m * (((t >> 16) & 0xff) + M.m * (t >> 24)));
+        mac_128(c, pw, cv);
+        mul_add_128(pw, M.m4, 0);
+    });
+    U4 o;
+    o.x[0] = c[0];
+    o.x[1] = c[1];
+    o.x[2] = c[2];
+    o.x[3] = c[3];
+    return o;
+}
+
 // ---- global label rows: u8 digits, four per word, word stride `stride` ----
 // Words are fetched kRowBatch at a time into registers before any of them is
 // used: L is a generic pointer (shared memory), so a load / store per word
@@ -1107,8 +1134,7 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
                 ct = R[(uint64_t)(row - 1) * e.rs];
             }
             const U4 H = hash_tw(Xc, g, row, 0, e.t);
-            lb_dec(e.A, ct, H, Mq);
-            store_slot(e, op.out, e.A, Mq);
+            e.slot0[(uint64_t)op.out * e.sstride] = lb_dec_c(ct, H, Mq);  // compressed, no digit buffer
             break;
         }
         case OP_HALF:
