@@ -1115,6 +1115,10 @@ DASH_HD U4 operand_c(LB L, const ActParams& P, const Elt& e, uint8_t v, const Mo
     return lb_compress(L, M);
 }
 
+// LAT: latency-bound small launches (act_wpe_eval_kernel) also decompress
+// both slot operands of an add in one loop; the throughput-bound per-thread
+// kernel keeps the smaller code
+template <bool LAT = false>
 DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
     switch (op.kind) {
         case OP_PROJ:
@@ -1179,6 +1183,13 @@ DASH_HD void eval_op(const ActParams& P, const Elt& e, const TapeOp& op) {
         case OP_ADD:
         case OP_ADDACC: {
             const ModC& M = c_mod[op.qm];
+            if (LAT && op.kind == OP_ADD && op.a < IN_LANE && op.b < IN_LANE && !M.pow2) {
+                // two slot operands: both decompressed in one loop
+                const U4 ca = e.slot0[(uint64_t)op.a * e.sstride], cb = e.slot0[(uint64_t)op.b * e.sstride];
+                digits_stream2(ca, cb, M, [&](int w, uint32_t a, uint32_t b) { e.A[w] = swar_add(a, b, M); });
+                if (!(op.cst & kKeep)) store_slot(e, op.out, e.A, M);
+                break;
+            }
             if (op.kind == OP_ADD) load_operand<kRowBatch>(e.A, P, e, op.a, M);
             add_operand<kRowBatch>(e.A, P, e, op.b, M);
             if (!(op.cst & kKeep)) store_slot(e, op.out, e.A, M);

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kWpeEvalWarps * 32, 1)
         for (int L = 0; L < P.n_levels; ++L) {
             const int end = P.lv_start[L + 1];
             if (active)
-                for (int i = P.lv_start[L] + (int)j; i < end; i += (int)G) eval_op(P, e, P.lv_tape[i]);
+                for (int i = P.lv_start[L] + (int)j; i < end; i += (int)G) eval_op<true>(P, e, P.lv_tape[i]);
             __syncwarp();
         }
         uint32_t next = 0;

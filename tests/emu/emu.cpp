@@ -110,7 +110,7 @@ static void act_layer(const ActParams& P, bool garble, bool lv_garble) {
                 e.sstride = (uint64_t)P.B * P.E;
                 e.slot0 = P.slots + (uint64_t)e.b * P.E + e.u;
                 for (int L = 0; L < P.n_levels; ++L)
-                    for (int i = P.lv_start[L + 1] - 1; i >= P.lv_start[L]; --i) eval_op(P, e, P.lv_tape[i]);
+                    for (int i = P.lv_start[L + 1] - 1; i >= P.lv_start[L]; --i) eval_op<true>(P, e, P.lv_tape[i]);
             } else {
                 act_element<false>(P, e, 0, P.n_ops);
             }
