@@ -12,6 +12,9 @@ encodes, evaluates and decodes the whole batch; the per-step garbled tables
   e2e     the same metric through the C-ABI call dashgpu_infer with HOST
           buffers: H2D of seeds + inputs and D2H of the decoded outputs inside
           the timed region.
+  kernels the library's per-launch CUDA events (kernels_ms_per_step, the
+          roofline's kernel duration) come from a second, untimed pass of
+          the same steps, so their host cost does not enter `value`.
   --impl reference: the reference's own CPU implementation (oracle/_ref, the
           unmodified dash_core sources) on the host cores, rank 0 only.
 
@@ -363,7 +366,6 @@ def main():
     for i in range(args.warmup):
         step_device(i)
     barrier()
-    eng.profile(True)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -373,6 +375,13 @@ def main():
         end.record(stream)
         barrier()
     ms = start.elapsed_time(end)
+    # per-kernel CUDA events (kernels_ms_per_step, roofline) from a second
+    # pass of the same steps: the event records cost host time per launch,
+    # which a latency-bound small step would otherwise count in `value`
+    eng.profile(True)
+    for i in range(args.steps):
+        step_device(args.warmup + i)
+    barrier()
     prof = eng.profile_read()
     eng.profile(False)
     t = torch.tensor([ms], device="cuda")
