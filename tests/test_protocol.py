@@ -274,3 +274,39 @@ def test_loopback_private_weights_and_extension_model(eng, oracle):
         x = np.random.default_rng(909).integers(-7, 8, size=c.n_in)
         run = P.run_local_protocol(eng, c, x, 2, _cfg(oracle, "90aa"))
         assert run.outputs.tolist() == oracle.plain_forward(c, x).tolist()
+
+
+def test_frame_decoder_compacts_and_rejects_bad_payload_codecs():
+    dec = P.FrameDecoder()
+    big = P.Frame(P.FrameType.GC_TRANSFER, 9, bytes(1 << 20))
+    small = P.Frame(P.FrameType.RESULT, 9, b"")
+    dec.feed(P.encode_frame(big) + P.encode_frame(small) + P.encode_frame(small)[:5])
+    assert dec.next().payload == big.payload
+    assert dec.next().type == P.FrameType.RESULT
+    assert dec.next() is None  # partial frame stays buffered
+    dec.feed(P.encode_frame(small)[5:])
+    assert dec.next().session == 9
+    with pytest.raises(P.ProtocolError):
+        P.decode_error(bytes([9]) + P.encode_error(P.ErrorCode.DATA, "x")[1:])
+    with pytest.raises(P.DataError):
+        P.decode_error(P.encode_error(P.ErrorCode.DATA, "hello")[:-2])
+    with pytest.raises(P.ProtocolError):
+        P.decode_result(b"\0" * 7)
+    with pytest.raises(P.ProtocolError):
+        P.encode_frame(P.Frame(P.FrameType.ERROR, 0, bytes((1 << 30) + 1)))
+
+
+def test_evaluator_rejects_unexpected_frames(eng):
+    ev = P.EvaluatorService(eng)
+    f = ev.handle(P.Frame(P.FrameType.MODEL_UPLOAD, 5, b""))
+    assert f.type == P.FrameType.ERROR and P.decode_error(f.payload)[0] == P.ErrorCode.PROTOCOL
+    svc = P.GarblerService(eng)
+    out = svc.handle(P.Frame(P.FrameType.GC_TRANSFER, 5, b""))
+    assert out[0].frame.type == P.FrameType.ERROR and out[0].dest == P.Destination.REPLY
+    # an ERROR frame from the evaluator fails the garbler's session
+    c = tiny()
+    svc.handle(P.Frame(P.FrameType.MODEL_UPLOAD, 6, P.encode_model_upload(c, 1)))
+    assert svc.handle(P.Frame(P.FrameType.ERROR, 6, P.encode_error(P.ErrorCode.DATA, "bad bundle"))) == []
+    assert svc.session_done(6)
+    res = svc.handle(P.Frame(P.FrameType.RESULT, 6, b""))[0].frame
+    assert res.type == P.FrameType.ERROR and P.decode_error(res.payload) == (P.ErrorCode.DATA, "bad bundle")
