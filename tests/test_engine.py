@@ -649,3 +649,23 @@ def test_launch_shapes_agree(gpu):
             ref = got
             assert got[3] == g.plain_forward(x0).tolist()
         assert got == ref, B
+
+
+@pytest.mark.gpu
+def test_import_gc_lenet_batch(gpu):
+    # a full LeNet-5 GC (7.8 M rows, four activation layers in the device row
+    # layout) exported, imported as a batch of 2 and evaluated: the imported
+    # network's garbled outputs equal the garbling network's own evaluation
+    g = gpu.model("lenet5", 2001, 8)
+    seeds = seed_hex(0x1E70) + seed_hex(0x1E71)
+    x = np.stack([g.random_input(5), g.random_input(6)])
+    net = gpu.garble(g, seeds)
+    bi = gpu.garble_inputs(net, x)
+    bo = gpu.evaluate(net, bi)
+    gcs = [net.export_gc(0), net.export_gc(1)]
+    ev = gpu.import_gc(gcs)
+    assert ev.export_gc(1) == gcs[1]
+    bo2 = gpu.evaluate(ev, gpu.import_bundle(ev, bi.payload(0) + bi.payload(1), False))
+    assert bo2.payload(0) == bo.payload(0) and bo2.payload(1) == bo.payload(1)
+    out = gpu.decode_outputs(net, gpu.import_bundle(net, bo2.payload(0) + bo2.payload(1), True))
+    assert out.tolist() == [g.plain_forward(xi).tolist() for xi in x]
