@@ -2061,28 +2061,31 @@ static uint64_t device_ct_index(const dashgpu_circuit& c, uint64_t idx) {
 }
 
 // device rows of one inference -> the reference's GarbledCircuit::cts order
-static void act_rows_to_reference(const dashgpu_circuit& c, std::vector<U4>& cts) {
+// Device rows of an activation layer <-> the reference order: block by block
+// of 32 elements (act_row_pos), so both sides stay within a cache-sized
+// window (32 elements x uc rows).  to_ref: device -> reference order.
+static void act_rows_permute(const dashgpu_circuit& c, std::vector<U4>& cts, bool to_ref) {
     std::vector<U4> tmp;
     for (const auto& l : c.layers) {
         if (!l.tape || !l.cts) continue;
-        const uint64_t uc = l.tape->cts;
+        const uint64_t uc = l.tape->cts, E = l.E_out;
         tmp.assign(cts.begin() + l.ct_base, cts.begin() + l.ct_base + l.cts);
-        for (uint64_t u = 0; u < l.E_out; ++u)
-            for (uint64_t j = 0; j < uc; ++j) cts[l.ct_base + u * uc + j] = tmp[act_row_pos(l.E_out, uc, u, j)];
+        for (uint64_t b0 = 0; b0 < E; b0 += 32) {
+            const uint64_t w = std::min<uint64_t>(32, E - b0);
+            U4* dev = (to_ref ? tmp.data() : cts.data() + l.ct_base) + b0 * uc;        // [j][l]
+            U4* ref = (to_ref ? cts.data() + l.ct_base : tmp.data()) + b0 * uc;        // [l][j]
+            for (uint64_t j = 0; j < uc; ++j)
+                for (uint64_t e = 0; e < w; ++e) {
+                    if (to_ref) ref[e * uc + j] = dev[j * w + e];
+                    else dev[j * w + e] = ref[e * uc + j];
+                }
+        }
     }
 }
-
-// inverse of act_rows_to_reference (an imported GC -> device rows)
-static void reference_to_act_rows(const dashgpu_circuit& c, std::vector<U4>& cts) {
-    std::vector<U4> tmp;
-    for (const auto& l : c.layers) {
-        if (!l.tape || !l.cts) continue;
-        const uint64_t uc = l.tape->cts;
-        tmp.assign(cts.begin() + l.ct_base, cts.begin() + l.ct_base + l.cts);
-        for (uint64_t u = 0; u < l.E_out; ++u)
-            for (uint64_t j = 0; j < uc; ++j) cts[l.ct_base + act_row_pos(l.E_out, uc, u, j)] = tmp[u * uc + j];
-    }
-}
+// device rows of one inference -> the reference's GarbledCircuit::cts order
+static void act_rows_to_reference(const dashgpu_circuit& c, std::vector<U4>& cts) { act_rows_permute(c, cts, true); }
+// inverse (an imported GC -> device rows)
+static void reference_to_act_rows(const dashgpu_circuit& c, std::vector<U4>& cts) { act_rows_permute(c, cts, false); }
 
 static size_t out_bytes(const std::vector<uint8_t>& v, uint8_t* buf, size_t cap, size_t* len) {
     if (len) *len = v.size();
@@ -2204,7 +2207,8 @@ struct ParsedGc {
     size_t circuit_bytes = 0;  // prefix holding the circuit description
     std::vector<u128> zero;
     std::vector<uint64_t> bases;
-    std::vector<u128> cts;
+    const uint8_t* cts = nullptr;  // n_cts little-endian u128 rows inside the input
+    uint64_t n_cts = 0;
     u128 commit = 0;
 };
 
@@ -2278,8 +2282,9 @@ static ParsedGc parse_gc(const uint8_t* data, size_t len, dashgpu_circuit* c) {
     const uint64_t ncts = r.le(8);
     if (ncts > (1ull << 32)) throw DataError("ciphertext blob too large");
     if (ncts > (len - r.at) / 16) throw DataError("truncated garbled circuit");
-    g.cts.resize(ncts);
-    for (auto& v : g.cts) v = r.u128v();
+    g.cts = data + r.at;  // little-endian u128 rows == the U4 layout
+    g.n_cts = ncts;
+    r.at += 16 * ncts;
     g.commit = r.u128v();
     if (r.at != len) throw DataError("trailing bytes in garbled circuit file");
     return g;
@@ -3000,7 +3005,7 @@ int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t ba
                 throw DataError("garbled circuits of a batch differ in their circuit");
         }
         for (const auto& g : gs) {
-            if (g.cts.size() != c.total_cts) throw DataError("ciphertext blob does not match the circuit");
+            if (g.n_cts != c.total_cts) throw DataError("ciphertext blob does not match the circuit");
             for (size_t li = 0; li < c.layers.size(); ++li)
                 if (g.bases[li] != c.layers[li].ct_base) throw DataError("ciphertext blob does not match the circuit");
             if (g.bases.back() != c.total_cts) throw DataError("ciphertext blob does not match the circuit");
@@ -3017,7 +3022,7 @@ int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t ba
             for (int i = 0; i < c.k; ++i)
                 host_decompress(gs[b].zero[i], c.base.primes[i], zero.data() + ((size_t)b * c.k + i) * LABW);
             cts.resize(c.total_cts);
-            for (uint64_t j = 0; j < c.total_cts; ++j) cts[j] = u128_to_u4(gs[b].cts[j]);
+            std::memcpy(cts.data(), gs[b].cts, c.total_cts * 16);
             reference_to_act_rows(c, cts);
             dev::h2d(N.blob.as<U4>() + (uint64_t)b * c.total_cts, cts.data(), cts.size() * 16, g_stream);
             commit[b] = u128_to_u4(gs[b].commit);

@@ -257,14 +257,14 @@ class Dash:
         evaluating gcs[b] (EvaluatorService GC_TRANSFER, protocol.cpp:309)."""
         if isinstance(gcs, (bytes, bytearray)):
             gcs = [gcs]
-        bufs = [(ctypes.c_uint8 * len(g)).from_buffer_copy(g) for g in gcs]
-        ptrs = (u8p * len(bufs))(*[ctypes.cast(b, u8p) for b in bufs])
-        lens = (ctypes.c_size_t * len(bufs))(*[len(g) for g in gcs])
+        gcs = [bytes(g) for g in gcs]  # no copy for bytes; pointers into them (kept alive below)
+        ptrs = (u8p * len(gcs))(*[ctypes.cast(ctypes.c_char_p(g), u8p) for g in gcs])
+        lens = (ctypes.c_size_t * len(gcs))(*[len(g) for g in gcs])
         h = vp()
-        self._check(self.lib.dashgpu_import_gc(ptrs, lens, len(bufs), ctypes.byref(h)))
+        self._check(self.lib.dashgpu_import_gc(ptrs, lens, len(gcs), ctypes.byref(h)))
         ch = vp()
         self._check(self.lib.dashgpu_network_circuit(h, ctypes.byref(ch)))
-        net = GarbledNetwork(self, h, GpuCircuit(self, ch, owned=False), len(bufs))
+        net = GarbledNetwork(self, h, GpuCircuit(self, ch, owned=False), len(gcs))
         return net
 
     def infer(self, c: "GpuCircuit", seeds, inputs, outputs=None, on_device: bool = False):

@@ -429,10 +429,23 @@ class GarblerService:
 
 
 @dataclass
+class _EvalGroup:
+    """Sessions whose GCs were imported together into one batched device
+    network (EvaluatorService.handle_batch): evaluated in one launch once
+    every member's garbled input is in."""
+    net: GarbledNetwork
+    sessions: List[int]
+    inputs: Dict[int, bytes] = field(default_factory=dict)  # member index -> payload
+    failed: set = field(default_factory=set)                # members answered with an error
+
+
+@dataclass
 class _EvaluatorSession:
     net: GarbledNetwork
     memory: int
     used: bool = False
+    group: Optional[_EvalGroup] = None
+    index: int = 0
 
 
 class EvaluatorService:
@@ -443,8 +456,17 @@ class EvaluatorService:
         self.eng = eng
         self._mu = threading.Lock()
         self._sessions: Dict[int, _EvaluatorSession] = {}
+        self._ready: List[Frame] = []  # replies of batched sessions not yet handed out
 
     def handle(self, f: Frame) -> Optional[Frame]:
+        with self._mu:
+            s = self._sessions.get(f.session) if f.type == FrameType.GARBLED_INPUT else None
+        if s is not None and s.group is not None:  # member of a batched network
+            replies = self.handle_batch([f])
+            mine = [r for r in replies if r.session == f.session]
+            with self._mu:
+                self._ready.extend(r for r in replies if r.session != f.session)
+            return mine[0] if mine else None
         try:
             if f.type == FrameType.GC_TRANSFER:
                 net = self.eng.import_gc([f.payload])
@@ -474,6 +496,87 @@ class EvaluatorService:
         with self._mu:
             s = self._sessions.get(session)
             return s.memory if s else 0
+
+    # ---- batched sessions (B200 serving: one launch for many sessions) ----
+    def handle_batch(self, frames: Sequence[Frame]) -> List[Frame]:
+        """Frames of many sessions at once.  GC_TRANSFER frames of one batch
+        that carry the same circuit are imported into ONE device network
+        (dashgpu_import_gc with B GCs); their GARBLED_INPUT frames are held
+        until every member's input is in and then evaluated in one launch.
+        Same rules and error frames as handle(): single use, unknown or
+        duplicate sessions, malformed bundles (a failed member is answered
+        with its ERROR frame; the others still get their outputs).  Returns
+        every reply that became ready, in no particular session order."""
+        replies: List[Frame] = []
+        gcs = [f for f in frames if f.type == FrameType.GC_TRANSFER]
+        rest = [f for f in frames if f.type != FrameType.GC_TRANSFER]
+        if len(gcs) >= 2:
+            replies += self._import_group(gcs)
+        elif gcs:
+            r = self.handle(gcs[0])
+            if r is not None:
+                replies.append(r)
+        for f in rest:
+            with self._mu:
+                s = self._sessions.get(f.session) if f.type == FrameType.GARBLED_INPUT else None
+            if s is None or s.group is None:
+                r = self.handle(f)
+                if r is not None:
+                    replies.append(r)
+                continue
+            replies += self._group_input(f, s)
+        with self._mu:
+            replies += self._ready
+            self._ready = []
+        return replies
+
+    def _import_group(self, gcs: Sequence[Frame]) -> List[Frame]:
+        replies, fresh, seen = [], [], set()
+        with self._mu:
+            for f in gcs:
+                if f.session in self._sessions or f.session in seen:
+                    replies.append(_error_frame(f.session, ProtocolError("session already has a circuit")))
+                else:
+                    seen.add(f.session)
+                    fresh.append(f)
+        if len(fresh) < 2:
+            return replies + [r for r in (self.handle(f) for f in fresh) if r is not None]
+        try:
+            net = self.eng.import_gc([f.payload for f in fresh])
+        except Error:  # bad file or mixed circuits: per-session imports attribute the errors
+            return replies + [r for r in (self.handle(f) for f in fresh) if r is not None]
+        info = net.circuit.info
+        mem = info.cts * 16 + info.k * 16 + 16 * info.k * info.n_in
+        grp = _EvalGroup(net, [f.session for f in fresh])
+        with self._mu:
+            for i, f in enumerate(fresh):
+                self._sessions[f.session] = _EvaluatorSession(net, mem, group=grp, index=i)
+        return replies
+
+    def _group_input(self, f: Frame, s: _EvaluatorSession) -> List[Frame]:
+        grp = s.group
+        info = grp.net.circuit.info
+        want = 16 * info.k * info.n_in
+        with self._mu:
+            if s.used:
+                return [_error_frame(f.session, ProtocolError("garbled circuit already used (single-use)"))]
+            s.used = True
+            if len(f.payload) != want:  # bundle_from_payload's size check
+                grp.failed.add(s.index)
+                grp.inputs[s.index] = bytes(want)
+                out = [_error_frame(f.session, DataError("wire payload size mismatch"))]
+            else:
+                grp.inputs[s.index] = bytes(f.payload)
+                out = []
+            if len(grp.inputs) < len(grp.sessions):
+                return out
+            payload = b"".join(grp.inputs[i] for i in range(len(grp.sessions)))
+        try:
+            gout = self.eng.evaluate(grp.net, self.eng.import_bundle(grp.net, payload, False))
+        except Error as e:
+            return out + [_error_frame(sid, e) for i, sid in enumerate(grp.sessions) if i not in grp.failed]
+        return out + [Frame(FrameType.GARBLED_OUTPUT, sid, gout.payload(i))
+                      for i, sid in enumerate(grp.sessions) if i not in grp.failed]
 
 
 # ---------------------------------------------------------------- loopback

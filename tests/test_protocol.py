@@ -310,3 +310,61 @@ def test_evaluator_rejects_unexpected_frames(eng):
     assert svc.session_done(6)
     res = svc.handle(P.Frame(P.FrameType.RESULT, 6, b""))[0].frame
     assert res.type == P.FrameType.ERROR and P.decode_error(res.payload) == (P.ErrorCode.DATA, "bad bundle")
+
+
+# ---------------------------------------------------------------- batched evaluator sessions
+
+def _oracle_sessions(oracle, c, n, tag):
+    nets = [oracle.garble(c, oracle.seed_from_string(f"{tag}{i}")) for i in range(n)]
+    rng = np.random.default_rng(len(tag) + n)
+    gins = [oracle.garble_inputs(o, rng.integers(-7, 8, size=c.n_in)) for o in nets]
+    return nets, gins
+
+
+def test_batched_sessions_evaluate_in_one_network(eng, oracle):
+    c = tiny()
+    nets, gins = _oracle_sessions(oracle, c, 4, "b0")
+    ev = P.EvaluatorService(eng)
+    T = P.FrameType
+    assert ev.handle_batch([P.Frame(T.GC_TRANSFER, 100 + i, o.gc_bytes()) for i, o in enumerate(nets)]) == []
+    assert ev.session_memory(101) == ev.session_memory(100) > 0
+    # half of the inputs: nothing can be evaluated yet
+    assert ev.handle_batch([P.Frame(T.GARBLED_INPUT, 100 + i, gins[i].payload()) for i in (2, 0)]) == []
+    out = ev.handle_batch([P.Frame(T.GARBLED_INPUT, 100 + i, gins[i].payload()) for i in (1, 3)])
+    assert sorted(f.session for f in out) == [100, 101, 102, 103]
+    for f in out:
+        i = f.session - 100
+        assert f.type == T.GARBLED_OUTPUT
+        assert f.payload == oracle.evaluate(nets[i], gins[i]).payload()
+    again = ev.handle(P.Frame(T.GARBLED_INPUT, 101, gins[1].payload()))
+    assert again.type == T.ERROR and P.decode_error(again.payload)[0] == P.ErrorCode.PROTOCOL
+
+
+def test_batched_sessions_isolate_a_bad_member(eng, oracle):
+    c = tiny()
+    nets, gins = _oracle_sessions(oracle, c, 3, "b1")
+    ev = P.EvaluatorService(eng)
+    T = P.FrameType
+    ev.handle_batch([P.Frame(T.GC_TRANSFER, 200 + i, o.gc_bytes()) for i, o in enumerate(nets)])
+    # through handle(): member 1's malformed bundle is answered at once,
+    # member 2's output arrives with the last input, member 0's stays queued
+    assert ev.handle(P.Frame(T.GARBLED_INPUT, 200, gins[0].payload())) is None
+    bad = ev.handle(P.Frame(T.GARBLED_INPUT, 201, b"\1\2\3"))
+    assert bad.type == T.ERROR and P.decode_error(bad.payload)[0] == P.ErrorCode.DATA
+    last = ev.handle(P.Frame(T.GARBLED_INPUT, 202, gins[2].payload()))
+    assert last.type == T.GARBLED_OUTPUT and last.payload == oracle.evaluate(nets[2], gins[2]).payload()
+    queued = ev.handle_batch([])
+    assert [(f.session, f.payload) for f in queued] == [(200, oracle.evaluate(nets[0], gins[0]).payload())]
+
+
+def test_batched_gc_transfer_of_mixed_circuits_falls_back(eng, oracle):
+    a, b = tiny(), models.build("relu16", 0, 5)
+    na, nb = oracle.garble(a, seed_hex(0xB2)), oracle.garble(b, seed_hex(0xB3))
+    ev = P.EvaluatorService(eng)
+    T = P.FrameType
+    out = ev.handle_batch([P.Frame(T.GC_TRANSFER, 1, na.gc_bytes()), P.Frame(T.GC_TRANSFER, 2, nb.gc_bytes()),
+                           P.Frame(T.GC_TRANSFER, 2, nb.gc_bytes())])
+    assert [f.type for f in out] == [T.ERROR]  # the duplicate session
+    gb = oracle.garble_inputs(nb, np.arange(16) - 8)
+    r = ev.handle(P.Frame(T.GARBLED_INPUT, 2, gb.payload()))
+    assert r.type == T.GARBLED_OUTPUT and r.payload == oracle.evaluate(nb, gb).payload()
