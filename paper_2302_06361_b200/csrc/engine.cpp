@@ -2097,6 +2097,7 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
     const dashgpu_circuit& c = *n.c;
     if (b >= n.B) throw DataError("inference index out of range");
     Writer w;
+    w.b.reserve(c.total_cts * 16 + 4096);
     w.header(1);
     w.le((uint64_t)c.k, 1);
     w.shape(c.input_shape);
@@ -2141,7 +2142,7 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
     for (const auto& l : c.layers) w.le(l.ct_base, 8);
     w.le(c.total_cts, 8);
     w.le(c.total_cts, 8);
-    for (const auto& v : cts) w.u128v(u4_to_u128(v));
+    w.bytes(cts.data(), cts.size() * 16);  // little-endian u128 rows == the U4 layout
     w.u128v(u4_to_u128(commit));
     return w.b;
 }
@@ -2625,6 +2626,31 @@ static int guarded(F&& f) {
     }
 }
 
+// The size query (buf == nullptr) and the copy call of one export come in
+// pairs; the query keeps its result for the copy that follows on this thread
+// (a GC is ~125 MB for LeNet-5: built once, not twice).
+template <class F>
+static void export_cached(const dashgpu_network* n, uint32_t b, int kind, uint8_t* buf, size_t cap, size_t* len,
+                          F&& make) {
+    static thread_local struct {
+        const dashgpu_network* n = nullptr;
+        uint32_t b = 0;
+        int kind = -1;
+        std::vector<uint8_t> v;
+    } cache;
+    const bool hit = cache.n == n && cache.b == b && cache.kind == kind;
+    std::vector<uint8_t> v = hit ? std::move(cache.v) : make();
+    cache.n = nullptr;
+    cache.kind = -1;
+    cache.v.clear();
+    out_bytes(v, buf, cap, len);
+    if (!buf) {
+        cache.n = n;
+        cache.b = b;
+        cache.kind = kind;
+        cache.v = std::move(v);
+    }
+}
 extern "C" {
 
 const char* dashgpu_last_error(void) { return g_err.c_str(); }
@@ -2932,13 +2958,13 @@ int dashgpu_decode_outputs(dashgpu_network* n, const dashgpu_bundle* out, int64_
 void dashgpu_bundle_destroy(dashgpu_bundle* b) { delete b; }
 
 int dashgpu_export_gc(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
-    return guarded([&] { out_bytes(export_gc(*n->net, b), buf, cap, len); });
+    return guarded([&] { export_cached(n, b, 1, buf, cap, len, [&] { return export_gc(*n->net, b); }); });
 }
 int dashgpu_export_encoding(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
-    return guarded([&] { out_bytes(export_encoding(*n->net, b), buf, cap, len); });
+    return guarded([&] { export_cached(n, b, 2, buf, cap, len, [&] { return export_encoding(*n->net, b); }); });
 }
 int dashgpu_export_decoding(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
-    return guarded([&] { out_bytes(export_decoding(*n->net, b), buf, cap, len); });
+    return guarded([&] { export_cached(n, b, 3, buf, cap, len, [&] { return export_decoding(*n->net, b); }); });
 }
 int dashgpu_export_bundle(const dashgpu_bundle* bd, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
     return guarded([&] {
