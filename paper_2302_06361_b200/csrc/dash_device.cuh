@@ -878,6 +878,14 @@ DASH_HD const uint32_t* mult_row(const Elt& e, uint32_t m, uint32_t v) {
 #else
 #define DASH_NI static inline
 #endif
+// The out-of-line tape helpers only ever see label buffers in shared memory
+// (act / wpe / lv kernels): telling the compiler so turns their generic
+// LD/ST into LDS/STS (the provenance is lost at the call boundary).
+#if defined(__CUDA_ARCH__)
+#define DASH_SHARED(lb) __builtin_assume(__isShared((lb).p))
+#else
+#define DASH_SHARED(lb) ((void)0)
+#endif
 template <int NB>
 DASH_NI void operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m);
 DASH_NI void store_n(U4* slot, LB L, uint32_t m);
@@ -896,6 +904,7 @@ DASH_HD void store_slot(const Elt& e, uint8_t s, LB L, const ModC& M) {
 // L += operand v (streamed, no scratch label)
 template <int NB>
 DASH_NI void add_operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m) {
+    DASH_SHARED(L);
     const ModC& M = c_mod[m];
     if (!rows) {
         lb_add_c(L, *slot, M);
@@ -917,15 +926,20 @@ DASH_HD void add_operand(LB L, const ActParams& P, const Elt& e, uint8_t v, cons
 // Single-copy helpers (called once per gadget, not per row): keeps the
 // instruction working set of 24 co-resident warps inside the I-cache.
 DASH_NI void prf_n(LB L, uint64_t wire, uint32_t stream, uint32_t m, const uint32_t* rk, AesTab t) {
+    DASH_SHARED(L);
     lb_prf(L, wire, stream, c_mod[m], rk, t);
 }
 // operand from an input lane (row pointer of this element) or from a slot
 template <int NB>
 DASH_NI void operand_n(LB L, const uint32_t* rows, uint32_t E, const U4* slot, uint32_t m) {
+    DASH_SHARED(L);
     if (rows) lb_load_rows<NB>(L, rows, E, c_mod[m]);
     else lb_decompress(L, *slot, c_mod[m]);
 }
-DASH_NI void store_n(U4* slot, LB L, uint32_t m) { *slot = lb_compress(L, c_mod[m]); }
+DASH_NI void store_n(U4* slot, LB L, uint32_t m) {
+    DASH_SHARED(L);
+    *slot = lb_compress(L, c_mod[m]);
+}
 
 // The garbling row loop of every projection / half gate (one copy).  Row
 // r = (cin + a) mod p holds key X + aR_p and payload base + phi(a) R_q (phi
@@ -937,6 +951,8 @@ DASH_NI void store_n(U4* slot, LB L, uint32_t m) { *slot = lb_compress(L, c_mod[
 // the interleaved table, and GRR's row 0 is never computed.  X advances.
 DASH_NI void garble_rows_n(LB X, LB base, AesTab t, const uint32_t* mult, uint32_t p, uint32_t q, uint32_t cin,
                            uint64_t g, const uint8_t* phi, uint32_t r, U4* R, int grr, uint32_t rs) {
+    DASH_SHARED(X);
+    DASH_SHARED(base);
     const ModC& Mp = c_mod[p];
     const ModC& Mq = c_mod[q];
     const uint32_t* Mp0 = mult + (uint64_t)c_modslot[p] * 128u * NWMAX;

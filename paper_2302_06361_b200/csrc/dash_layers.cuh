@@ -439,11 +439,10 @@ struct ProjParams {
     int garbler;
 };
 
-DASH_HD void proj_thread(const ProjParams& P, uint32_t i, const AesTab& t) {
+// X, A: label buffers (shared memory on the device: garble_rows_n assumes it)
+DASH_HD void proj_thread(const ProjParams& P, uint32_t i, const AesTab& t, LB X, LB A) {
     const ModC& Mp = c_mod[P.p];
     const ModC& Mq = c_mod[P.q];
-    uint32_t buf[2][NWMAX] = {};
-    const LB X{buf[0], 1}, A{buf[1], 1};
     lb_decompress(X, P.in[i], Mp);
     const uint32_t c = lb_color(X, Mp);
     U4* R = P.rows + (uint64_t)i * P.p;

@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(128) proj_kernel(const __grid_constant__ ProjP
     fill_T(g_T0);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.n) return;
-    proj_thread(P, i, make_tab(nullptr, threadIdx.x & 31u));
+    // per-thread label buffers in shared memory, lane-interleaved (stride 32)
+    uint32_t* lb = s_dyn + kTabWords + (threadIdx.x >> 5) * (2 * NWMAX * 32) + (threadIdx.x & 31u);
+    proj_thread(P, i, make_tab(nullptr, threadIdx.x & 31u), LB{lb, 32}, LB{lb + NWMAX * 32, 32});
 }
 
 __global__ void __launch_bounds__(128) expand_kernel(const uint8_t* seeds, uint32_t* rk, uint32_t B) {
@@ -485,8 +487,9 @@ void launch_pad_add(const PadAddParams& P, void* st) {
 void launch_proj(const ProjParams& P, void* st) {
     if (P.n == 0) return;
     ProfScope ps(K_MISC, S(st));
-    smem_attr((const void*)proj_kernel, kTabBytes);
-    proj_kernel<<<cdiv(P.n, 128), 128, kTabBytes, S(st)>>>(P);
+    const size_t smem = kTabBytes + sizeof(uint32_t) * 4 * 2 * NWMAX * 32;  // 4 warps x (X, A)
+    smem_attr((const void*)proj_kernel, smem);
+    proj_kernel<<<cdiv(P.n, 128), 128, smem, S(st)>>>(P);
     dev::check();
 }
 

@@ -166,7 +166,10 @@ void launch_expand(const uint8_t* seeds, uint32_t* rk, uint32_t B, void*) {
 
 void launch_proj(const ProjParams& P, void*) {
 #pragma omp parallel for
-    for (int64_t i = 0; i < (int64_t)P.n; ++i) proj_thread(P, (uint32_t)i, tab());
+    for (int64_t i = 0; i < (int64_t)P.n; ++i) {
+        uint32_t buf[2][NWMAX] = {};
+        proj_thread(P, (uint32_t)i, tab(), LB{buf[0], 1}, LB{buf[1], 1});
+    }
 }
 
 void launch_private(const PrivParams& P, void*, const Sched&) {
