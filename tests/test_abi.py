@@ -22,7 +22,7 @@ def test_header_declares_the_reference_api():
     syms = declared_symbols()
     for s in ["dashgpu_garble", "dashgpu_garble_inputs", "dashgpu_evaluate", "dashgpu_decode_outputs",
               "dashgpu_export_gc", "dashgpu_export_encoding", "dashgpu_export_decoding", "dashgpu_export_bundle",
-              "dashgpu_import_bundle", "dashgpu_infer", "dashgpu_circuit_create"]:
+              "dashgpu_import_bundle", "dashgpu_import_gc", "dashgpu_infer", "dashgpu_circuit_create"]:
         assert s in syms
 
 
@@ -106,3 +106,19 @@ def test_bad_extension_circuits_raise_data_error(oracle):
         assert lib.dashgpu_circuit_create(ctypes.byref(desc), ctypes.byref(h)) == 3, bad
         with pytest.raises(CheckerError):
             oracle.circuit(bad)
+
+
+def test_import_gc_rejects_bad_arguments_without_a_device():
+    # argument and file checks come before any device work (host-only path)
+    lib = ctypes.CDLL(CUDA_LIB)
+    vp = ctypes.c_void_p
+    out = vp()
+    assert lib.dashgpu_import_gc(None, None, 1, ctypes.byref(out)) == 3  # DASHGPU_ERR_DATA
+    data = ctypes.c_char_p(b"DASH\x01\x00\x02" + bytes(64))          # wrong file kind
+    ptrs = (ctypes.c_char_p * 1)(data)
+    lens = (ctypes.c_size_t * 1)(71)
+    assert lib.dashgpu_import_gc(ptrs, lens, 0, ctypes.byref(out)) == 3  # empty batch
+    assert lib.dashgpu_import_gc(ptrs, lens, 1, ctypes.byref(out)) == 3
+    lib.dashgpu_last_error.restype = ctypes.c_char_p
+    assert b"kind" in lib.dashgpu_last_error()
+    assert lib.dashgpu_network_circuit(None, ctypes.byref(out)) == 3
