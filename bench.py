@@ -55,6 +55,7 @@ def parse():
                                                 "comma separated; --sweep-log2 / --sweep-k select the grid")
     ap.add_argument("--sweep-log2", default="16,18,20,22,24,26")
     ap.add_argument("--sweep-k", default="2,4,6,8")
+    ap.add_argument("--emulate", action="store_true", help=argparse.SUPPRESS)  # tests: CPU emulation + gloo
     return ap.parse_args()
 
 
@@ -138,7 +139,7 @@ def cpu_baseline(circuit_desc_c, n_in, n_out, sample):
             v = sample / sec
             if best is None or v > best[0]:
                 best = (v, mode, sec)
-        return {"value": best[0], "unit": "inferences/s", "cores": cores, "kind": kind,
+        return {"value": best[0], "unit": "inferences/s", "cores": cores, "kind": kind, "cpu": host_cpu(),
                 "sample": f"{sample} {MODEL_NAME[0]} inferences (garble+garble_inputs+evaluate+decode_outputs), "
                           f"{'inference-parallel' if best[1] == 1 else 'OpenMP intra-layer'} on {cores} threads, "
                           f"{best[2]:.1f} s"}
@@ -148,7 +149,7 @@ def cpu_baseline(circuit_desc_c, n_in, n_out, sample):
     x = np.random.default_rng(7).integers(-7, 8, size=(sample, n_in)).astype(np.int64)
     sec, _ = O.bench_infer(ch, seeds, x, cores)
     mode = "inference-parallel" if sample >= cores else "OpenMP intra-layer"
-    return {"value": sample / sec, "unit": "inferences/s", "cores": cores, "kind": "port",
+    return {"value": sample / sec, "unit": "inferences/s", "cores": cores, "kind": "port", "cpu": host_cpu(),
             "sample": f"{sample} {MODEL_NAME[0]} inferences, C oracle port (the reference has no Pad2d/Add layers), "
                       f"{mode} on {cores} threads, {sec:.1f} s"}
 
@@ -164,53 +165,103 @@ WORKLOADS = {
 }
 
 
+def host_cpu():
+    """lscpu-style model string of the host (state the CPU)."""
+    name, fam, model = "unknown", "?", "?"
+    try:
+        for line in open("/proc/cpuinfo"):
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "model name":
+                name = v
+            elif k == "cpu family":
+                fam = v
+            elif k == "model":
+                model = v
+            if name != "unknown" and fam != "?" and model != "?":
+                break
+    except OSError:
+        pass
+    return f"{name} (family {fam} model {model}), {os.cpu_count()} logical CPUs"
+
+
+def reference_circuit(model, k):
+    """The benchmark circuit as a plain weight file (oracle/models/*.npz,
+    written by oracle/models/export_models.py): the reference arm hands it to
+    the unmodified reference without loading the product library."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+
+    path = os.path.join(ROOT, "oracle", "models", f"{model}_s{SEED}_k{k}.npz")
+    if not os.path.exists(path):
+        raise SystemExit(f"no weight file {path}; run oracle/models/export_models.py")
+    return pyoracle.load_circuit(path)
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU implementation, rank 0 only."""
+    """--impl reference: the reference's CPU implementation, rank 0 only.
+
+    Same workload as the GPU arm: each timed step garbles, encodes, evaluates
+    and decodes args.batch fresh inferences (64 for the headline) on the
+    unmodified reference (oracle/_ref: proj/core/src/*.cpp, -O2
+    -march=native) with one inference per core (inference-parallel; the
+    reference has no batching, so this is its best mode for a batch).  The
+    untimed warm-up steps run one inference per core."""
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
-    from paper_2302_06361_b200.circuit import Circuit
-    from paper_2302_06361_b200 import models
 
-    c = models.build(args.model, SEED, args.k)
+    c = reference_circuit(args.model, args.k)
+    for l in c.layers:  # --private: projection per weight (model_io.cpp:56 default)
+        l.private_weights = bool(args.private and l.linear())
     cores = os.cpu_count() or 1
     n_in = c.n_in
-    per_step = max(1, min(args.batch, cores))
     if pyoracle.have_ref():
-        R = pyoracle.RefLib()
-        ch = R.circuit(c)
-        kind = "reference"
-
-        def step(i):
-            seeds = b"".join(int(0x5EED0000 + i * per_step + b).to_bytes(16, "big") for b in range(per_step))
-            x = np.random.default_rng(i).integers(-7, 8, size=(per_step, n_in)).astype(np.int64)
-            return R.bench_infer(ch, seeds, x, 1, cores)[0]
+        try:
+            R = pyoracle.RefLib()
+            ch = R.circuit(c)
+            kind = "reference"
+        except pyoracle.CheckerError:  # Pad2d / Add extensions (ResNet-20): the reference cannot run them
+            R = None
     else:
+        R = None
+    if R is None:
         O = pyoracle.Oracle()
         ch = O.circuit(c)
         kind = "port"
 
-        def step(i):
-            seeds = b"".join(int(0x5EED0000 + i * per_step + b).to_bytes(16, "big") for b in range(per_step))
-            x = np.random.default_rng(i).integers(-7, 8, size=(per_step, n_in)).astype(np.int64)
-            return O.bench_infer(ch, seeds, x, cores)[0]
+    def step(i, n):
+        seeds = b"".join(int(0x5EED0000 + i * n + b).to_bytes(16, "big") for b in range(n))
+        x = np.random.default_rng(i).integers(-7, 8, size=(n, n_in)).astype(np.int64)
+        if R is not None:
+            return R.bench_infer(ch, seeds, x, 1, cores)[0]
+        return O.bench_infer(ch, seeds, x, cores)[0]
+
     for i in range(args.warmup):
-        step(i)
+        step(i, min(args.batch, cores))
     total = 0.0
     for i in range(args.steps):
-        total += step(args.warmup + i)
-    value = per_step * args.steps / total
+        total += step(args.warmup + i, args.batch)
+    value = args.batch * args.steps / total
     line = {"metric": "garbled inferences/sec (garble+eval)", "value": value, "unit": "inferences/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.model} k={args.k}, reference CPU path, {per_step} inferences per step "
-                                   f"(one per core, inference-parallel)", "global_batch": per_step,
-                       "inferences_per_gpu": per_step},
+            "config": {"workload": f"{args.model}{' (private weights)' if args.private else ''} "
+                                   f"({WORKLOADS.get(args.model, 'single-layer sweep')}) k={args.k}, "
+                                   f"synthetic inputs U[-7,7], batch {args.batch} per step, fresh seed per "
+                                   f"inference per step",
+                       "global_batch": args.batch, "inferences_per_gpu": args.batch,
+                       "parallelism": f"reference CPU path, inference-parallel on {cores} cores"},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "inferences/s", "cores": cores, "kind": kind,
-                             "sample": f"{per_step} inferences per step x {args.steps} steps"},
+                             "cpu": host_cpu(),
+                             "sample": f"{args.batch} inferences per step x {args.steps} timed steps "
+                                       f"(garble+garble_inputs+evaluate+decode_outputs, one inference per core); "
+                                       f"warm-up steps {min(args.batch, cores)} inferences",
+                             "build": "oracle/_ref: unmodified proj/core/src/*.cpp, g++ -O2 -march=native -fopenmp"
+                             if kind == "reference" else "oracle/liboracle.so (C restatement)"},
             "e2e": {"value": value, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -316,147 +367,239 @@ def run_sweep(args):
         dist.destroy_process_group()
 
 
-def main():
-    args = parse()
-    if args.sweep:
-        run_sweep(args)
-        return
-    MODEL_NAME[0] = args.model
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        return
+SUM_N = [128, 80, 55, 45, 37, 34, 31, 30, 28, 26, 25, 24, 23, 23, 23, 22]  # digits per label, primes 2..53
 
+
+def measured_peaks():
+    """HBM GB/s (driver-measured, MEASURED_PEAKS.json) and the int8
+    tensor-core peak measured by scripts/int8_peak.py (profiles/int8_peak.json)."""
+    hbm, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        hbm, hbm_src = float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    i8, i8_src = 4500.0, "nominal B200 dense int8 (no measured int8 peak)"
+    p = os.path.join(ROOT, "profiles", "int8_peak.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        i8, i8_src = float(j["tops"]), f"measured: {j.get('how', 'scripts/int8_peak.py')}"
+    return hbm, hbm_src, i8, i8_src
+
+
+def roofline_fields(args, info, B, ms, prof):
+    """Roofline of the dominant kernel + every kernel kind of the step.
+
+    Algorithmic bytes per activation element: garbling writes
+    16 B per garbled row (uc_cts rows) and reads + writes the element's u8
+    label bundle (2 * sum n_p); evaluation reads 16 B per decrypted row
+    (eval_rows) plus the same label I/O.  Linear lanes: 2 ops per digit-MAC,
+    K * units * sum n_p per pass (linear_macs), garble + eval passes."""
+    hbm, hbm_src, i8, i8_src = measured_peaks()
+    sum_n = sum(SUM_N[: args.k])
+    steps = args.steps
+    elems = info.relu_elements * B  # activation elements per step
+    out = {}
+
+    def per_launch(kind):
+        t, n = prof.get(kind, (0.0, 0))
+        return (t / n if n else 0.0), (n / steps if n else 0.0)
+
+    for kind, rows in (("act_garble", info.act_uc_cts), ("act_eval", info.act_eval_rows)):
+        t_launch, launches = per_launch(kind)
+        if not launches:
+            continue
+        bpe = 16 * rows + 2 * sum_n
+        byts = bpe * elems / launches
+        ach = byts / (t_launch / 1e3) / 1e9
+        out[kind] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                     "bytes_per_element": bpe, "elements_per_launch": elems / launches,
+                     "kernel_ms_per_step": prof[kind][0] / steps,
+                     "share_of_step": prof[kind][0] / steps / (ms / steps)}
+    t_launch, launches = per_launch("linear")
+    if launches and info.linear_macs:
+        ops = 2 * 2 * info.linear_macs * B  # garble + eval passes, 2 ops per digit-MAC
+        tops = ops / (prof["linear"][0] / steps / 1e3) / 1e12
+        out["linear"] = {"bound": "tensor", "achieved": tops, "peak": i8, "unit": "TOPS (int8)", "frac": tops / i8,
+                         "peak_source": i8_src, "digit_macs_per_inference_pass": int(info.linear_macs),
+                         "kernel_ms_per_step": prof["linear"][0] / steps,
+                         "share_of_step": prof["linear"][0] / steps / (ms / steps)}
+    for kind in ("setup", "priv_garble", "priv_eval", "encode", "decode", "misc"):
+        t, n = prof.get(kind, (0.0, 0))
+        if n:
+            out[kind] = {"kernel_ms_per_step": t / steps, "share_of_step": t / steps / (ms / steps),
+                         "launches_per_step": n / steps}
+    head = dict(out.get("act_garble", {}))
+    traffic, issue = None, {}
+    tp = os.path.join(ROOT, "profiles", "act_garble_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        traffic = tj.get("dram_bytes_per_launch")
+        issue = {k: tj[k] for k in ("issue_active_frac", "alu_pipe_frac", "warps_active_per_sm",
+                                    "warp_instructions_per_launch", "instructions_per_garbled_row") if k in tj}
+    roof = {"bound": "hbm", "achieved": head.get("achieved", 0.0), "peak": hbm, "unit": "GB/s",
+            "frac": head.get("frac"), "traffic": traffic, "kernel": "act_kernel<garble> (ReLU gadget tape)",
+            "peak_source": hbm_src, "bytes_per_element": head.get("bytes_per_element"),
+            "kernel_ms_per_step": head.get("kernel_ms_per_step"), "kernel_share_of_step": head.get("share_of_step"),
+            "issue_roofline_ncu": issue or None,
+            "note": "integer-issue bound (AES T-tables + base-m label codec, SURVEY 8(d) honest note): the HBM "
+                    "fraction is small by construction; issue_roofline_ncu (ncu issue-active, ALU pipe, "
+                    "instructions per garbled row) is its real roofline"}
+    return {"roofline": roof, "rooflines": out}
+
+
+def launch_ranks(args):
+    """--gpus N without a launcher: run this script under torchrun, one rank
+    per GPU on 127.0.0.1 (the driver's own launch line), and relay rank 0's
+    JSON line.  NCCL's INIT log (communicator + nranks) goes to stderr."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    if not args.emulate:
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def output_checksum(out: np.ndarray) -> int:
+    """Order-sensitive digest of decoded outputs (verifies the all-gather)."""
+    v = np.ascontiguousarray(out, np.int64).view(np.uint64).astype(object)
+    h = 0
+    for x in v.ravel().tolist():
+        h = (h * 1000003 + x) % ((1 << 61) - 1)
+    return h
+
+
+def run_ours(args, rank, world, local):
+    """The product path on this rank's GPU: garble + garble_inputs + evaluate
+    + decode_outputs of args.batch fresh inferences per step through
+    dashgpu_infer; decoded outputs all-gathered over NCCL once per step.
+    --emulate (tests only): the CPU emulation of the device code, gloo and
+    wall-clock timing, so the multi-rank launcher is testable without a GPU."""
     import torch
     import torch.distributed as dist
 
     from paper_2302_06361_b200.engine import Dash
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    stream = torch.cuda.current_stream()
-    eng = Dash(local)
-    eng.set_stream(stream.cuda_stream)
+    emu = args.emulate
+    if emu:
+        dev = torch.device("cpu")
+        if world > 1:
+            dist.init_process_group("gloo")
+        eng = Dash(lib_path=os.path.join(ROOT, "tests", "emu", "libdashemu.so"), emulation=True)
+        stream = None
+    else:
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+        stream = torch.cuda.current_stream()
+        eng = Dash(local)
+        eng.set_stream(stream.cuda_stream)
     g = eng.model(args.model, SEED, args.k, private=args.private)
     info = g.info
     B = args.batch
     n_in, n_out = info.n_in, info.n_out
     rng = np.random.default_rng(1234 + rank)
     host_x = rng.integers(-7, 8, size=(B, n_in)).astype(np.int64)
-    dev_x = torch.from_numpy(host_x).cuda()
-    dev_out = torch.zeros((B, n_out), dtype=torch.int64, device="cuda")
+    dev_x = torch.from_numpy(host_x).to(dev)
+    dev_out = torch.zeros((B, n_out), dtype=torch.int64, device=dev)
     steps_seeds = [seeds_for(s, rank, world, B) for s in range(args.warmup + args.steps)]
-    dev_seeds = [torch.frombuffer(bytearray(s), dtype=torch.uint8).cuda() for s in steps_seeds]
-    gathered = torch.zeros((world * B, n_out), dtype=torch.int64, device="cuda")
+    dev_seeds = [torch.frombuffer(bytearray(s), dtype=torch.uint8).to(dev) for s in steps_seeds]
+    gathered = torch.zeros((world * B, n_out), dtype=torch.int64, device=dev)
+
+    def sync():
+        if not emu:
+            torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
             dist.barrier()
-        torch.cuda.synchronize()
+        sync()
+
+    class Timer:
+        def __enter__(self):
+            barrier()
+            if emu:
+                self.t0 = time.perf_counter()
+            else:
+                self.a, self.b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                self.a.record(stream)
+            return self
+
+        def __exit__(self, *exc):
+            if emu:
+                barrier()
+                self.ms = 1e3 * (time.perf_counter() - self.t0)
+            else:
+                self.b.record(stream)
+                barrier()
+                self.ms = self.a.elapsed_time(self.b)
+            t = torch.tensor([self.ms], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
+            self.ms = float(t.item())
 
     def step_device(i):
-        eng.infer(g, dev_seeds[i].data_ptr(), dev_x.data_ptr(), (dev_out.data_ptr(), B), on_device=True)
+        if emu:
+            out, _ = eng.infer(g, steps_seeds[i], host_x)
+            dev_out.copy_(torch.from_numpy(out))
+        else:
+            eng.infer(g, dev_seeds[i].data_ptr(), dev_x.data_ptr(), (dev_out.data_ptr(), B), on_device=True)
         if world > 1:
             dist.all_gather_into_tensor(gathered, dev_out)
 
     # ---- value: HBM-resident inputs ----
     for i in range(args.warmup):
         step_device(i)
-    barrier()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        start.record(stream)
-        for i in range(args.steps):
-            step_device(args.warmup + i)
-        end.record(stream)
-        barrier()
-    ms = start.elapsed_time(end)
+    with ClockSampler(local) if not emu else _Null() as clk:
+        with Timer() as tv:
+            for i in range(args.steps):
+                step_device(args.warmup + i)
+    ms = tv.ms
+    value = world * B * args.steps / (ms / 1e3)
+    # the all-gather of the last step must hold every rank's own decode
+    local_sum = torch.tensor([output_checksum(dev_out.cpu().numpy())], dtype=torch.int64, device=dev)
+    sums = [torch.zeros_like(local_sum) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(sums, local_sum)
+    else:
+        sums = [local_sum]
+        gathered.copy_(dev_out)
+    gat = gathered.cpu().numpy()
+    gather_ok = all(output_checksum(gat[r * B:(r + 1) * B]) == int(sums[r].item()) for r in range(world))
+    gather_ok = gather_ok and (gat[rank * B:(rank + 1) * B] == dev_out.cpu().numpy()).all()
     # per-kernel CUDA events (kernels_ms_per_step, roofline) from a second
     # pass of the same steps: the event records cost host time per launch,
     # which a latency-bound small step would otherwise count in `value`
-    eng.profile(True)
-    for i in range(args.steps):
-        step_device(args.warmup + i)
-    barrier()
-    prof = eng.profile_read()
-    eng.profile(False)
-    t = torch.tensor([ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    value = world * B * args.steps / (ms / 1e3)
+    prof = {}
+    if not emu:
+        eng.profile(True)
+        for i in range(args.steps):
+            step_device(args.warmup + i)
+        barrier()
+        prof = eng.profile_read()
+        eng.profile(False)
 
     # ---- e2e: host buffers through the C ABI (dashgpu_infer) ----
-    out_host = None
     h2d = d2h = 0
-    barrier()
-    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_start.record(stream)
-    for i in range(args.steps):
-        out_host, tm = eng.infer(g, steps_seeds[args.warmup + i], host_x)
-        h2d, d2h = tm.h2d_bytes, tm.d2h_bytes
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, torch.from_numpy(out_host).cuda())
-    e_end.record(stream)
-    barrier()
-    ems = e_start.elapsed_time(e_end)
-    t = torch.tensor([ems], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ems = float(t.item())
-    e2e = world * B * args.steps / (ems / 1e3)
+    with Timer() as te:
+        for i in range(args.steps):
+            out_host, tm = eng.infer(g, steps_seeds[args.warmup + i], host_x)
+            h2d, d2h = tm.h2d_bytes, tm.d2h_bytes
+            if world > 1:
+                dist.all_gather_into_tensor(gathered, torch.from_numpy(out_host).to(dev))
+    e2e = world * B * args.steps / (te.ms / 1e3)
 
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
-
-    # ---- roofline of the dominant kernel (activation garbling) ----
-    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    peak, peak_src = 6650.0, "fallback"
-    if os.path.exists(peaks_path):
-        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured"
-    sum_n = sum(n for n in [128, 80, 55, 45, 37, 34, 31, 30, 28, 26, 25, 24, 23, 23, 23, 22][: args.k])
-    act_ms, act_n = prof.get("act_garble", (0.0, 0))
-    bytes_per_elem = 16 * info.act_uc_cts + 2 * sum_n  # table writes + label bundle read/write (u8)
-    elems_per_launch = (info.relu_elements * B) / max(1, act_n / max(1, args.steps)) if act_n else 0
-    achieved = (bytes_per_elem * elems_per_launch) / ((act_ms / act_n) / 1e3) / 1e9 if act_n else 0.0
-    traffic = None
-    issue = {}
-    tp = os.path.join(ROOT, "profiles", "act_garble_traffic.json")
-    if os.path.exists(tp):
-        tj = json.load(open(tp))
-        traffic = tj.get("dram_bytes_per_launch")
-        # the kernel is integer-issue bound (SURVEY 8(d) honest note): ncu's
-        # issue-active and ALU-pipe fractions are its real roofline
-        issue = {k: tj[k] for k in ("issue_active_frac", "alu_pipe_frac", "warps_active_per_sm") if k in tj}
-    launches = sum(v[1] for v in prof.values())
-    # public linear lanes on the tensor cores (tcgen05 kind::i8): algorithmic
-    # digit-MACs (K * units * sum n_p per pass, garble + eval) vs the nominal
-    # dense int8 peak; the kernel executes 4x these MACs (digit-word expansion,
-    # tc_linear.cuh) and its ncu tensor-pipe share is in profiles/.
-    lin_ms, lin_n = prof.get("linear", (0.0, 0))
-    roof_lin = None
-    if lin_n and info.linear_macs:
-        tops = 2 * 2 * info.linear_macs * B * args.steps / (lin_ms / 1e3) / 1e12
-        roof_lin = {"bound": "tensor", "achieved": tops, "peak": 4500.0, "unit": "TOPS (int8)", "frac": tops / 4500.0,
-                    "peak_source": "nominal B200 dense int8 (no measured int8 peak in MEASURED_PEAKS.json)",
-                    "kernel": "tc_linear_kernel (tcgen05.mma kind::i8, TMA weights)",
-                    "digit_macs_per_inference_pass": int(info.linear_macs),
-                    "kernel_ms_per_step": lin_ms / args.steps}
-
-    cpu = None
-    sample = args.cpu_sample or min(B, max(8, os.cpu_count() or 8))
-    try:
-        cpu = None if args.no_cpu else cpu_baseline(g.to_circuit(), n_in, n_out, sample)
-    except Exception as e:  # the CPU baseline must not hide the GPU line
-        cpu = {"value": None, "unit": "inferences/s", "cores": os.cpu_count(), "kind": "unavailable",
-               "sample": str(e)[:200]}
 
     line = {
         "metric": "garbled inferences/sec (garble+eval)",
@@ -477,27 +620,54 @@ def main():
                    "global_batch": world * B, "inferences_per_gpu": B, "parallelism": f"inference-sharded x{world}",
                    "l2": "per-step garbled tables (%.1f GB) exceed L2; no flush needed" % (info.cts * 16 * B / 1e9),
                    "ciphertexts_per_inference": info.cts, "relu_elements_per_inference": info.relu_elements},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "kernel": "act_kernel<garble> (ReLU gadget tape)", "peak_source": peak_src,
-                     "bytes_per_element": bytes_per_elem,
-                     "kernel_ms_per_step": act_ms / args.steps,
-                     "kernel_share_of_step": (act_ms / args.steps) / (ms / args.steps),
-                     "issue_roofline_ncu": issue or None,
-                     "note": "integer-issue / latency bound (AES T-tables + base-m label codec, SURVEY 8(d) honest "
-                             "note): the HBM fraction is small by construction; issue_roofline_ncu is its real "
-                             "roofline (ncu issue-active and ALU-pipe utilisation of this kernel)"},
-        "roofline_linear": roof_lin,
-        "cpu_baseline": cpu,
+        "gather": {"collective": "all_gather of decoded outputs (int64) once per step",
+                   "bytes_per_step": world * B * n_out * 8, "verified": bool(gather_ok)},
         "e2e": {"value": e2e, "unit": "inferences/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "clocks": clk.summary(),
-        "gpu_launches": int(launches),
-        "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
     }
+    if emu:
+        line["emulated"] = "CPU emulation of the device code (tests only): not a measurement"
+    else:
+        line.update(roofline_fields(args, info, B, ms, prof))
+        cpu = None
+        sample = args.cpu_sample or min(B, max(8, os.cpu_count() or 8))
+        try:
+            cpu = None if args.no_cpu else cpu_baseline(reference_circuit(args.model, args.k), n_in, n_out, sample)
+        except (Exception, SystemExit) as e:  # the CPU baseline must not hide the GPU line
+            cpu = {"value": None, "unit": "inferences/s", "cores": os.cpu_count(), "kind": "unavailable",
+                   "sample": str(e)[:200]}
+        line["cpu_baseline"] = cpu
+        line["clocks"] = clk.summary()
+        line["gpu_launches"] = int(sum(v[1] for v in prof.values()))
+        line["kernels_ms_per_step"] = {k: v[0] / args.steps for k, v in prof.items() if v[1]}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(launch_ranks(args))
+    if args.sweep:
+        run_sweep(args)
+        return
+    MODEL_NAME[0] = args.model
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
 
 
 if __name__ == "__main__":

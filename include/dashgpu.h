@@ -77,6 +77,8 @@ typedef struct dashgpu_timing {
 const char* dashgpu_last_error(void);
 int dashgpu_version(void);
 /* Selects the CUDA device and uploads the constant tables. */
+/* 1 = the CUDA engine (this library); anything else is a test build. */
+int dashgpu_backend(void);
 int dashgpu_init(int device);
 /* Stream all work is enqueued on (a cudaStream_t; NULL = legacy default). */
 int dashgpu_set_stream(void* stream);
@@ -202,6 +204,13 @@ int dashgpu_infer_stream_range(const dashgpu_circuit* c, const uint8_t* seeds, u
 int dashgpu_profile(int enable);
 /* kinds: 0 act-garble 1 act-eval 2 linear 3 priv-garble 4 priv-eval 5 setup 6 encode 7 decode 8 misc */
 int dashgpu_profile_read(double* ms, uint64_t* launches, int max_kinds);
+/* Shape of the most recent activation-layer launch (garble = 1: the combined
+ * garbling launch; 0: the last evaluation launch): out[0] variant (0 none,
+ * 1 lane-group evaluation, 2 level-parallel garbling, 3 lane-group garbling,
+ * 4 one element per thread), out[1] tape chunks per element, out[2] grid,
+ * out[3] work items, out[4] lanes per element.  Lets parity tests pin the
+ * launch configuration a benchmark times. */
+int dashgpu_last_act_launch(int garble, uint32_t out[5]);
 
 /* ---- primitive kernels (parity tests) ----
  * op 0: decompress_mod(in[i], m) -> digits (u16), then compress -> out[i]

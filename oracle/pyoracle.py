@@ -476,6 +476,45 @@ class RefLib(_Base):
         return sec, out
 
 
+_LAYER_FIELDS = ("kind", "private_weights", "in_dim", "out_dim", "in_ch", "out_ch", "filter", "stride", "src", "src2",
+                 "pad")
+
+
+def save_circuit(c, path: str):
+    """Circuit -> plain npz (layer scalars + int8 weights / int64 biases)."""
+    arrs = {"input_shape": np.asarray(c.input_shape, np.int64), "k": np.int64(c.k),
+            "sign_target": np.float64(c.sign_target), "alpha": np.float64(c.alpha),
+            "layers": np.asarray([[int(getattr(l, f)) for f in _LAYER_FIELDS] for l in c.layers], np.int64)}
+    for i, l in enumerate(c.layers):
+        if l.q_weights is not None:
+            w = np.asarray(l.q_weights, np.int64)
+            assert np.abs(w).max(initial=0) < 128
+            arrs[f"w{i}"] = w.astype(np.int8)
+        if l.q_biases is not None:
+            arrs[f"b{i}"] = np.asarray(l.q_biases, np.int64)
+    np.savez_compressed(path, **arrs)
+
+
+def load_circuit(path: str):
+    """npz written by save_circuit -> Circuit (the pure-Python circuit types;
+    no native library is loaded)."""
+    from paper_2302_06361_b200.circuit import Circuit, Layer
+
+    z = np.load(path)
+    layers = []
+    for i, row in enumerate(z["layers"]):
+        kw = dict(zip(_LAYER_FIELDS, (int(v) for v in row)))
+        kw["private_weights"] = bool(kw["private_weights"])
+        l = Layer(**kw)
+        if f"w{i}" in z:
+            l.q_weights = z[f"w{i}"].astype(np.int64)
+        if f"b{i}" in z:
+            l.q_biases = z[f"b{i}"].astype(np.int64)
+        layers.append(l)
+    return Circuit([int(v) for v in z["input_shape"]], int(z["k"]), layers, float(z["sign_target"]),
+                   float(z["alpha"]))
+
+
 def have_ref() -> bool:
     return os.path.exists(REF_SO)
 

@@ -481,4 +481,23 @@ DASH_HD void decompress_thread(const CompressParams& P, uint32_t b, uint32_t e, 
     lb_store_rows(L, lane_out + ((uint64_t)b * M.nw) * P.n + e, P.n, M);
 }
 
+// Activation-layer rows between the device layout (act_rows: blocks of 32
+// elements, row-major inside a block) and the reference's element-major
+// GarbledCircuit::cts order (layer.cpp:537-541), for GC export / import.
+// Thread r handles reference row r = e * uc + j of the layer.
+struct RowsPermuteParams {
+    const U4* src;
+    U4* dst;
+    uint64_t E, uc;
+    int to_ref;  // 1: device -> reference order, 0: reference -> device
+};
+
+DASH_HD void rows_permute_thread(const RowsPermuteParams& P, uint64_t r) {
+    const uint64_t e = r / P.uc, j = r - e * P.uc;
+    const uint64_t blk = e >> 5, left = P.E - (blk << 5), w = left < 32 ? left : 32;
+    const uint64_t d = blk * 32 * P.uc + j * w + (e & 31);
+    if (P.to_ref) P.dst[r] = P.src[d];
+    else P.dst[d] = P.src[r];
+}
+
 }  // namespace dashgpu

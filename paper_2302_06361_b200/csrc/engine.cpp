@@ -1718,7 +1718,10 @@ static void encode_into(Network& n, const int64_t* values, bool on_device, Bundl
 static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
-    if (in.B != n.B || in.output) throw DataError("garbled input bundle does not match the network");
+    // evaluate's input checks (garble.cpp:265-280): a bundle of another
+    // network or element count would make the kernels read out of bounds
+    if (in.net != &n || in.B != n.B || in.output) throw DataError("garbled input bundle does not match the network");
+    if (in.lanes.E != c.n_in || in.lanes.lane.size() != (size_t)k) throw DataError("garbled input shape mismatch");
     const Lanes* cur = run_layers(n, false, in.lanes);
     out.net = &n;
     out.B = n.B;
@@ -1749,7 +1752,9 @@ static void fill_crt(const Crt& base, DecodeParams& D) {
 static void decode_enqueue(Network& n, const Bundle& outb, int64_t* dev_values = nullptr) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
-    if (!outb.output || outb.B != n.B) throw DataError("output lane count mismatch");
+    if (outb.net != &n || !outb.output || outb.B != n.B) throw DataError("output lane count mismatch");
+    if (outb.lanes.E != c.n_out || outb.lanes.lane.size() != (size_t)k)
+        throw DataError("output element count mismatch");  // decode_outputs, garble.cpp:318-322
     DecodeParams D;
     std::memset(&D, 0, sizeof D);
     D.B = n.B;
@@ -2060,32 +2065,26 @@ static uint64_t device_ct_index(const dashgpu_circuit& c, uint64_t idx) {
     return idx;
 }
 
-// device rows of one inference -> the reference's GarbledCircuit::cts order
-// Device rows of an activation layer <-> the reference order: block by block
-// of 32 elements (act_row_pos), so both sides stay within a cache-sized
-// window (32 elements x uc rows).  to_ref: device -> reference order.
-static void act_rows_permute(const dashgpu_circuit& c, std::vector<U4>& cts, bool to_ref) {
-    std::vector<U4> tmp;
+// One inference's ciphertexts between the device row layout and the
+// reference's GarbledCircuit::cts order, on the device (rows_permute_thread):
+// activation layers are permuted block by block, everything else copied.
+// to_ref: device (src) -> reference (dst); else reference -> device.
+static void blob_permute(const dashgpu_circuit& c, const U4* src, U4* dst, bool to_ref) {
+    uint64_t at = 0;
     for (const auto& l : c.layers) {
         if (!l.tape || !l.cts) continue;
-        const uint64_t uc = l.tape->cts, E = l.E_out;
-        tmp.assign(cts.begin() + l.ct_base, cts.begin() + l.ct_base + l.cts);
-        for (uint64_t b0 = 0; b0 < E; b0 += 32) {
-            const uint64_t w = std::min<uint64_t>(32, E - b0);
-            U4* dev = (to_ref ? tmp.data() : cts.data() + l.ct_base) + b0 * uc;        // [j][l]
-            U4* ref = (to_ref ? cts.data() + l.ct_base : tmp.data()) + b0 * uc;        // [l][j]
-            for (uint64_t j = 0; j < uc; ++j)
-                for (uint64_t e = 0; e < w; ++e) {
-                    if (to_ref) ref[e * uc + j] = dev[j * w + e];
-                    else dev[j * w + e] = ref[e * uc + j];
-                }
-        }
+        if (l.ct_base > at) dev::d2d(dst + at, src + at, (l.ct_base - at) * 16, g_stream);
+        RowsPermuteParams P;
+        P.src = src + l.ct_base;
+        P.dst = dst + l.ct_base;
+        P.E = l.E_out;
+        P.uc = l.tape->cts;
+        P.to_ref = to_ref ? 1 : 0;
+        launch_rows_permute(P, g_stream);
+        at = l.ct_base + l.cts;
     }
+    if (c.total_cts > at) dev::d2d(dst + at, src + at, (c.total_cts - at) * 16, g_stream);
 }
-// device rows of one inference -> the reference's GarbledCircuit::cts order
-static void act_rows_to_reference(const dashgpu_circuit& c, std::vector<U4>& cts) { act_rows_permute(c, cts, true); }
-// inverse (an imported GC -> device rows)
-static void reference_to_act_rows(const dashgpu_circuit& c, std::vector<U4>& cts) { act_rows_permute(c, cts, false); }
 
 static size_t out_bytes(const std::vector<uint8_t>& v, uint8_t* buf, size_t cap, size_t* len) {
     if (len) *len = v.size();
@@ -2131,18 +2130,23 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
     }
     std::vector<uint32_t> zero((size_t)c.k * LABW);
     dev::d2h(zero.data(), n.zero.as<uint32_t>() + (uint64_t)b * c.k * LABW, zero.size() * 4, g_stream);
-    std::vector<U4> cts(c.total_cts);
-    dev::d2h(cts.data(), n.blob.as<U4>() + (uint64_t)b * c.total_cts, cts.size() * 16, g_stream);
+    // rows -> reference order on the device, then one D2H straight into the
+    // writer's buffer (little-endian u128 rows == the U4 layout)
+    DevBuf ref;
+    ref.ensure(std::max<uint64_t>(c.total_cts, 1) * 16);
+    blob_permute(c, n.blob.as<U4>() + (uint64_t)b * c.total_cts, ref.as<U4>(), true);
     U4 commit;
     dev::d2h(&commit, n.commit.as<U4>() + b, 16, g_stream);
     dev::sync(g_stream);
-    act_rows_to_reference(c, cts);
     for (int i = 0; i < c.k; ++i) w.u128v(host_compress(zero.data() + (size_t)i * LABW, c.base.primes[i]));
     w.le(c.layers.size() + 1, 8);
     for (const auto& l : c.layers) w.le(l.ct_base, 8);
     w.le(c.total_cts, 8);
     w.le(c.total_cts, 8);
-    w.bytes(cts.data(), cts.size() * 16);  // little-endian u128 rows == the U4 layout
+    const size_t at = w.b.size();
+    w.b.resize(at + c.total_cts * 16);
+    dev::d2h(w.b.data() + at, ref.p, c.total_cts * 16, g_stream);
+    dev::sync(g_stream);
     w.u128v(u4_to_u128(commit));
     return w.b;
 }
@@ -2655,6 +2659,7 @@ extern "C" {
 
 const char* dashgpu_last_error(void) { return g_err.c_str(); }
 int dashgpu_version(void) { return 1; }
+int dashgpu_backend(void) { return dev::backend(); }
 
 int dashgpu_init(int device) {
     return guarded([&] { init_device(device); });
@@ -3042,17 +3047,15 @@ int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t ba
         upload_circuit(c);
         network_reserve(N, batch);
         std::vector<uint32_t> zero((size_t)batch * c.k * LABW);
-        std::vector<U4> cts;
         std::vector<U4> commit(batch);
+        DevBuf ref;  // one inference's rows in the reference order, then permuted on the device
+        ref.ensure(std::max<uint64_t>(c.total_cts, 1) * 16);
         for (uint32_t b = 0; b < batch; ++b) {
             for (int i = 0; i < c.k; ++i)
                 host_decompress(gs[b].zero[i], c.base.primes[i], zero.data() + ((size_t)b * c.k + i) * LABW);
-            cts.resize(c.total_cts);
-            std::memcpy(cts.data(), gs[b].cts, c.total_cts * 16);
-            reference_to_act_rows(c, cts);
-            dev::h2d(N.blob.as<U4>() + (uint64_t)b * c.total_cts, cts.data(), cts.size() * 16, g_stream);
+            dev::h2d(ref.p, gs[b].cts, c.total_cts * 16, g_stream);
+            blob_permute(c, ref.as<U4>(), N.blob.as<U4>() + (uint64_t)b * c.total_cts, false);
             commit[b] = u128_to_u4(gs[b].commit);
-            dev::sync(g_stream);  // cts is reused for the next inference
         }
         dev::h2d(N.zero.p, zero.data(), zero.size() * 4, g_stream);
         dev::h2d(N.commit.p, commit.data(), commit.size() * 16, g_stream);
@@ -3186,6 +3189,17 @@ int dashgpu_profile_read(double* ms, uint64_t* launches, int max_kinds) {
     int k = 0;
     int rc = guarded([&] { k = dev::prof_read(ms, launches, max_kinds); });
     return rc ? -rc : k;
+}
+
+int dashgpu_last_act_launch(int garble, uint32_t out[5]) {
+    return guarded([&] {
+        const dev::ActShape s = dev::last_act_shape(garble != 0);
+        out[0] = s.variant;
+        out[1] = s.nchunks;
+        out[2] = s.grid;
+        out[3] = s.items;
+        out[4] = s.group;
+    });
 }
 
 int dashgpu_prim(int op, uint32_t n, int m, int q, const uint64_t* in, uint64_t* out, uint16_t* digits,

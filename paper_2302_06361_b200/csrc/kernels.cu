@@ -269,6 +269,12 @@ __global__ void __launch_bounds__(128) decompress_kernel(CompressParams P, uint3
     decompress_thread(P, blockIdx.y, e, lane_out);
 }
 
+__global__ void __launch_bounds__(256) rows_permute_kernel(RowsPermuteParams P) {
+    const uint64_t n = P.E * P.uc;
+    for (uint64_t r = (uint64_t)blockIdx.x * 256 + threadIdx.x; r < n; r += (uint64_t)gridDim.x * 256)
+        rows_permute_thread(P, r);
+}
+
 __global__ void __launch_bounds__(128) prim_kernel(PrimParams P) {
     fill_T(g_T0);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -551,6 +557,14 @@ void launch_compress(const CompressParams& P, void* st) {
 void launch_decompress(const CompressParams& P, uint32_t* lane_out, void* st) {
     ProfScope ps(K_MISC, S(st));
     decompress_kernel<<<dim3(cdiv(P.n, 128), P.B), 128, 0, S(st)>>>(P, lane_out);
+    dev::check();
+}
+
+void launch_rows_permute(const RowsPermuteParams& P, void* st) {
+    const uint64_t n = P.E * P.uc;
+    if (!n) return;
+    ProfScope ps(K_MISC, S(st));
+    rows_permute_kernel<<<(uint32_t)std::min<uint64_t>(cdiv(n, 256), 148ull * 16), 256, 0, S(st)>>>(P);
     dev::check();
 }
 

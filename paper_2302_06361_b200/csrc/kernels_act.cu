@@ -17,6 +17,7 @@ __device__ uint32_t g_T0[256];
 }  // namespace dashgpu
 #define DASH_CONST_DEFINED 1
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels_common.cuh"
@@ -322,7 +323,22 @@ static int sm_count() {
     return sms;
 }
 
+static dev::ActShape g_shape[2];
+
+static void note_shape(bool garble, uint32_t variant, uint32_t nchunks, uint32_t grid, uint64_t items, uint32_t group) {
+    g_shape[garble ? 1 : 0] = dev::ActShape{variant, nchunks, grid, (uint32_t)items, group};
+}
+
 namespace dev {
+ActShape last_act_shape(bool garble) { return g_shape[garble ? 1 : 0]; }
+uint64_t chunk_min_items() {
+    const char* e = std::getenv("DASH_CHUNK_MIN_ITEMS");
+    return e ? (uint64_t)std::atol(e) : (uint64_t)sm_count() * kActWarpsGarble;
+}
+bool force_thread_shape() {
+    const char* e = std::getenv("DASH_ACT_SHAPE");
+    return e && std::strcmp(e, "thread") == 0;
+}
 uint64_t lane_group_eval_max() { return (uint64_t)sm_count() * kWpeEvalWarps * 32 / 2; }
 // warps per element of the level-parallel garbling launch (0: not used): the
 // largest power of two <= 8 whose warps still fit one wave of 16-warp CTAs
@@ -351,7 +367,8 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     uint32_t G = 32;
     const uint64_t wave = (uint64_t)sm_count() * kWpeEvalWarps * 32;
     while (G > 1 && elements * G > wave) G >>= 1;
-    if (!garble && G >= 2) {
+    const bool thread_only = dev::force_thread_shape();
+    if (!garble && G >= 2 && !thread_only) {
         ItemMap wm;
         std::memset(&wm, 0, sizeof wm);
         wm.n = (uint32_t)n;
@@ -366,11 +383,12 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         smem_attr((const void*)act_wpe_eval_kernel, smem);
         act_wpe_eval_kernel<<<grid, kWpeEvalWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter, G);
         ck(cudaGetLastError(), "act wpe eval launch");
+        note_shape(false, dev::ACT_SHAPE_WPE_EVAL, 1, grid, wm.base[n], G);
         return;
     }
     // level-parallel garbling: W warps per element when the launch is small
     // enough and every layer's slot region holds the level tape's slots
-    if (garble) {
+    if (garble && !thread_only) {
         bool lv_ok = true;
         for (int i = 0; i < n; ++i) lv_ok = lv_ok && host_layers[i].lv_ok;
         const uint32_t W = lv_ok ? dev::garble_lv_warps(elements) : 0;
@@ -388,6 +406,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
             smem_attr((const void*)act_lv_garble_kernel, smem);
             act_lv_garble_kernel<<<grid, kWpeWarps * 32, smem, S(st)>>>(dev_layers, lm, W);
             ck(cudaGetLastError(), "act lv garble launch");
+            note_shape(true, dev::ACT_SHAPE_LV_GARBLE, 1, grid, lm.base[n], 32 * W);
             return;
         }
     }
@@ -395,7 +414,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     // CTAs; G = 1 is the per-thread kernel below
     uint32_t Gg = 32;
     while (Gg > 1 && elements * Gg > (uint64_t)sm_count() * kWpeWarps * 32 * kWpeGarbleWaves) Gg >>= 1;
-    if (garble && Gg >= 2) {
+    if (garble && Gg >= 2 && !thread_only) {
         ItemMap wm;
         std::memset(&wm, 0, sizeof wm);
         wm.n = (uint32_t)n;
@@ -410,6 +429,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         smem_attr((const void*)act_wpe_kernel, smem);
         act_wpe_kernel<<<grid, kWpeWarps * 32, smem, S(st)>>>(dev_layers, wm, q.counter, Gg);
         ck(cudaGetLastError(), "act wpe launch");
+        note_shape(true, dev::ACT_SHAPE_WPE_GARBLE, 1, grid, wm.base[n], Gg);
         return;
     }
     // one CTA per SM (the first round strides items across SMs), never fewer
@@ -423,8 +443,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
     uint32_t nchunks = 1;
     // chunked tapes only pay when the launch has more warp items than warp
     // slots (the last wave); below that every chunk would just wait in turn
-    const uint64_t slots = (uint64_t)sm_count() * kActWarpsGarble;
-    if (garble && map.base[n] > slots) {
+    if (garble && map.base[n] > dev::chunk_min_items()) {
         for (int i = 0; i < n; ++i)
             for (int c = 1; c <= MAXCHUNK; ++c)
                 if (host_layers[i].chunk_op[c] == host_layers[i].n_ops) {
@@ -445,6 +464,7 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
         act_kernel<false><<<grid, warps * 32, smem, S(st)>>>(dev_layers, map, counter, flags, 1);
     }
     ck(cudaGetLastError(), "act launch");
+    note_shape(garble, dev::ACT_SHAPE_THREAD, nchunks, grid, map.base[n], 1);
 }
 
 void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* st) {

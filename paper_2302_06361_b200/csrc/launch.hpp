@@ -30,6 +30,20 @@ void upload_constants(const ModC* mods, const uint32_t* pi_rk, const uint16_t* m
 // tape (kernels_act.cu; the engine sizes the level tape's slots for it)
 uint64_t lane_group_eval_max();
 uint32_t garble_lv_warps(uint64_t elements);  // level-parallel garbling (0 = not used)
+// Launch shape of the most recent activation launch (garble / eval), so tests
+// can pin the configuration a benchmark times: variant (ACT_SHAPE_*), tape
+// chunks per element, grid, work items (warps or lane groups), lanes per element.
+enum { ACT_SHAPE_NONE = 0, ACT_SHAPE_WPE_EVAL = 1, ACT_SHAPE_LV_GARBLE = 2, ACT_SHAPE_WPE_GARBLE = 3, ACT_SHAPE_THREAD = 4 };
+struct ActShape {
+    uint32_t variant, nchunks, grid, items, group;
+};
+ActShape last_act_shape(bool garble);
+// warp items above which the per-thread garbling launch splits element tapes
+// into chunks (default: one wave of garbling warps; DASH_CHUNK_MIN_ITEMS overrides)
+uint64_t chunk_min_items();
+// DASH_ACT_SHAPE=thread: activation launches always take the per-thread
+// kernels (tests pin the chunked garbling path on small circuits)
+bool force_thread_shape();
 // streams / events
 void* stream_create();
 void stream_destroy(void* s);
@@ -95,6 +109,7 @@ void launch_dectable(const DecodeParams& P, void* stream);
 void launch_decode(const DecodeParams& P, void* stream);
 void launch_compress(const CompressParams& P, void* stream);
 void launch_decompress(const CompressParams& P, uint32_t* lane_out, void* stream);
+void launch_rows_permute(const RowsPermuteParams& P, void* stream);  // GC export / import row order
 
 // primitive kernels for parity tests: op 0 decompress+compress, 1 aes_pi,
 // 2 aes with key, 3 prf label, 4 encrypt_label, 5 decrypt_label

@@ -102,6 +102,7 @@ KERNEL_KINDS = ["act_garble", "act_eval", "linear", "priv_garble", "priv_eval", 
 
 def _declare(L):
     L.dashgpu_last_error.restype = ctypes.c_char_p
+    L.dashgpu_backend.restype = ctypes.c_int
     L.dashgpu_init.argtypes = [ctypes.c_int]
     L.dashgpu_set_stream.argtypes = [vp]
     L.dashgpu_circuit_create.argtypes = [vp, ctypes.POINTER(vp)]
@@ -144,6 +145,7 @@ def _declare(L):
     L.dashgpu_proj_eval.argtypes = [ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u64p, u64p, u64p, u64p]
     L.dashgpu_profile.argtypes = [ctypes.c_int]
     L.dashgpu_profile_read.argtypes = [f64p, u64p, ctypes.c_int]
+    L.dashgpu_last_act_launch.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
     L.dashgpu_prim.argtypes = [ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u64p, u64p, u16p, u8p,
                                u64p, ctypes.c_uint64]
 
@@ -151,12 +153,19 @@ def _declare(L):
 class Dash:
     """Handle to the device engine (one CUDA device)."""
 
-    def __init__(self, device: int = 0, lib_path: Optional[str] = None):
-        path = lib_path or os.environ.get("DASHGPU_LIB") or LIB_PATH  # override: A/B of library builds
+    def __init__(self, device: int = 0, lib_path: Optional[str] = None, emulation: bool = False):
+        """lib_path / DASHGPU_LIB: another build of libdashgpu.so (A/B of kernel
+        variants).  Whatever is loaded must be the CUDA engine
+        (dashgpu_backend() == 1); only the tests pass emulation=True to load
+        their CPU emulation of the device code (tests/emu)."""
+        path = lib_path or os.environ.get("DASHGPU_LIB") or LIB_PATH
         if not os.path.exists(path):
             raise CudaError(f"{path} is not built; run __graft_entry__.build()")
         self.lib = ctypes.CDLL(path)
         _declare(self.lib)
+        if self.lib.dashgpu_backend() != 1 and not emulation:
+            raise CudaError(f"{path} is not the CUDA engine (backend {self.lib.dashgpu_backend()}); "
+                            "there is no CPU fallback")
         self._check(self.lib.dashgpu_init(device))
 
     def _check(self, rc: int):
@@ -239,6 +248,8 @@ class Dash:
     def bundle_from_labels(self, net: "GarbledNetwork", lanes, output: bool = False) -> "Bundle":
         """LabelTensor images (per lane [batch][elements][n_p] u16 digits) -> device bundle."""
         arrs = [np.ascontiguousarray(a, np.uint16) for a in lanes]
+        if len(arrs) != net.circuit.info.k:
+            raise DataError("one label image per CRT lane expected")
         ptrs = (u16p * len(arrs))(*[a.ctypes.data_as(u16p) for a in arrs])
         h = vp()
         self._check(self.lib.dashgpu_bundle_from_labels(net.h, arrs[0].shape[1], ptrs, 1 if output else 0,
@@ -315,6 +326,16 @@ class Dash:
         n = (ctypes.c_uint64 * 16)()
         k = self.lib.dashgpu_profile_read(ms, n, 16)
         return {KERNEL_KINDS[i]: (ms[i], int(n[i])) for i in range(max(k, 0))}
+
+    ACT_SHAPES = {0: "none", 1: "lane-group eval", 2: "level-parallel garble", 3: "lane-group garble",
+                  4: "per-thread"}
+
+    def last_act_launch(self, garble: bool = True) -> dict:
+        """Launch shape of the most recent activation launch (kernels_act.cu)."""
+        o = (ctypes.c_uint32 * 5)()
+        self._check(self.lib.dashgpu_last_act_launch(1 if garble else 0, o))
+        return {"variant": self.ACT_SHAPES.get(o[0], str(o[0])), "nchunks": o[1], "grid": o[2], "items": o[3],
+                "group": o[4]}
 
     # ---- t_proj primitive (gadgets.hpp:146-176) ----
     def proj_garble(self, seed: bytes, p: int, q: int, phi, labels, gates, wires):

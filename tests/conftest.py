@@ -37,7 +37,7 @@ def emu():
         pytest.skip("tests/emu/libdashemu.so not built")
     from paper_2302_06361_b200.engine import Dash
 
-    return Dash(lib_path=EMU_LIB)
+    return Dash(lib_path=EMU_LIB, emulation=True)
 
 
 @pytest.fixture(scope="session")

@@ -6,6 +6,7 @@
 // machine without a GPU.  Linked with engine.cpp into tests/emu/libdashemu.so.
 // The product package never loads this library; on a GPU box the tests run
 // the real CUDA library (paper_2302_06361_b200/libdashgpu.so).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -72,11 +73,34 @@ void prof_reset() {}
 int prof_read(double*, uint64_t*, int) { return 0; }
 }  // namespace dev
 
-static void act_layer(const ActParams& P, bool garble, bool lv_garble) {
+namespace dev {
+static ActShape g_shape[2];
+ActShape last_act_shape(bool garble) { return g_shape[garble ? 1 : 0]; }
+uint64_t chunk_min_items() {  // kernels_act.cu: one wave of 28-warp garbling CTAs on 148 SMs
+    const char* e = std::getenv("DASH_CHUNK_MIN_ITEMS");
+    return e ? (uint64_t)std::atol(e) : 148ull * 28;
+}
+bool force_thread_shape() {
+    const char* e = std::getenv("DASH_ACT_SHAPE");
+    return e && std::strcmp(e, "thread") == 0;
+}
+}  // namespace dev
+
+static const uint32_t kPoison = 0xA5C3E1F7u;
+
+// Runs ops [op0, op1) of every element's tape.  chunk > 0 emulates a chunked
+// work item of the persistent garbling kernel (kernels_act.cu act_kernel): it
+// runs on whatever warp dequeues it, so its shared-memory label buffers hold
+// garbage from other work -- they are poisoned here, and every value a chunk
+// needs must come from the global label slots.
+static void act_layer(const ActParams& P, bool garble, bool lv_garble, int chunk = -1, bool thread_eval = false) {
 #pragma omp parallel for collapse(2) schedule(dynamic, 16)
     for (int64_t b = 0; b < (int64_t)P.B; ++b)
         for (int64_t u = 0; u < (int64_t)P.E; ++u) {
             uint32_t buf[3][NWMAX];
+            if (chunk >= 0)
+                for (int j = 0; j < 3; ++j)
+                    for (int w = 0; w < NWMAX; ++w) buf[j][w] = kPoison ^ (uint32_t)(u * 131 + w * 7 + j);
             Elt e;
             e.b = (uint32_t)b;
             e.u = (uint32_t)u;
@@ -86,7 +110,9 @@ static void act_layer(const ActParams& P, bool garble, bool lv_garble) {
             e.t = tab();
             e.rk = nullptr;
             e.mult = nullptr;
-            if (garble && lv_garble) {
+            if (chunk >= 0) {
+                act_element<true>(P, e, P.chunk_op[chunk], P.chunk_op[chunk + 1]);
+            } else if (garble && lv_garble) {
                 // level-parallel garbling (act_lv_garble_kernel): the level
                 // tape, ops of a level in reverse order (they are independent)
                 e.gate0 = P.gate_base + (uint64_t)e.u * P.uc_gates;
@@ -100,7 +126,7 @@ static void act_layer(const ActParams& P, bool garble, bool lv_garble) {
                     for (int i = P.lv_start[L + 1] - 1; i >= P.lv_start[L]; --i) garble_op(P, e, P.lv_tape[i]);
             } else if (garble) {
                 act_element<true>(P, e, 0, P.n_ops);
-            } else if ((uint64_t)P.B * P.E <= dev::lane_group_eval_max() && P.n_levels > 0) {
+            } else if (!thread_eval && (uint64_t)P.B * P.E <= dev::lane_group_eval_max() && P.n_levels > 0) {
                 // small launches: the level-scheduled tape, as the CUDA
                 // warp-per-element evaluation runs it (levels in order;
                 // the ops of a level are independent)
@@ -117,16 +143,56 @@ static void act_layer(const ActParams& P, bool garble, bool lv_garble) {
         }
 }
 
+// Mirrors the launch-shape choice of kernels_act.cu launch_act_multi (148 SMs).
 void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers, int n, bool garble, void*,
                       const Sched&) {
-    uint64_t elements = 0;
+    uint64_t elements = 0, items = 0;
     bool lv_ok = true;
     for (int i = 0; i < n; ++i) {
         elements += (uint64_t)host_layers[i].B * host_layers[i].E;
+        items += (uint64_t)host_layers[i].B * ((host_layers[i].E + 31) / 32);
         lv_ok = lv_ok && host_layers[i].lv_ok;
     }
-    const bool lv = garble && lv_ok && dev::garble_lv_warps(elements) >= 2;
-    for (int i = 0; i < n; ++i) act_layer(dev_layers[i], garble, lv);
+    const bool thread_only = dev::force_thread_shape();
+    if (!garble) {
+        uint32_t G = 32;
+        while (G > 1 && elements * G > 148ull * 16 * 32) G >>= 1;
+        if (thread_only) G = 1;
+        dev::g_shape[0] = G >= 2 ? dev::ActShape{dev::ACT_SHAPE_WPE_EVAL, 1, 148, (uint32_t)elements, G}
+                                 : dev::ActShape{dev::ACT_SHAPE_THREAD, 1, 148, (uint32_t)items, 1};
+        for (int i = 0; i < n; ++i) act_layer(dev_layers[i], false, false, -1, thread_only);
+        return;
+    }
+    const bool lv = !thread_only && lv_ok && dev::garble_lv_warps(elements) >= 2;
+    if (lv) {
+        dev::g_shape[1] = dev::ActShape{dev::ACT_SHAPE_LV_GARBLE, 1, 0, (uint32_t)elements,
+                                        32 * dev::garble_lv_warps(elements)};
+        for (int i = 0; i < n; ++i) act_layer(dev_layers[i], true, true);
+        return;
+    }
+    uint32_t Gg = 32;
+    while (Gg > 1 && elements * Gg > 148ull * 16 * 32) Gg >>= 1;
+    if (Gg >= 2 && !thread_only) {
+        dev::g_shape[1] = dev::ActShape{dev::ACT_SHAPE_WPE_GARBLE, 1, 148, (uint32_t)elements, Gg};
+        for (int i = 0; i < n; ++i) act_layer(dev_layers[i], true, false);
+        return;
+    }
+    uint32_t nchunks = 1;
+    if (items > dev::chunk_min_items())
+        for (int i = 0; i < n; ++i)
+            for (int c = 1; c <= MAXCHUNK; ++c)
+                if (host_layers[i].chunk_op[c] == host_layers[i].n_ops) {
+                    nchunks = std::max<uint32_t>(nchunks, (uint32_t)c);
+                    break;
+                }
+    dev::g_shape[1] = dev::ActShape{dev::ACT_SHAPE_THREAD, nchunks, 148, (uint32_t)items, 1};
+    if (nchunks == 1) {
+        for (int i = 0; i < n; ++i) act_layer(dev_layers[i], true, false);
+        return;
+    }
+    // chunk-major, as the persistent kernel dequeues its items
+    for (uint32_t c = 0; c < nchunks; ++c)
+        for (int i = 0; i < n; ++i) act_layer(dev_layers[i], true, false, (int)c);
 }
 
 void launch_act_outputs(const ActParams& P, const uint16_t* primes, void*) {
@@ -213,6 +279,11 @@ void launch_compress(const CompressParams& P, void*) {
 void launch_decompress(const CompressParams& P, uint32_t* lane_out, void*) {
     for (uint32_t b = 0; b < P.B; ++b)
         for (uint32_t e = 0; e < P.n; ++e) decompress_thread(P, b, e, lane_out);
+}
+
+void launch_rows_permute(const RowsPermuteParams& P, void*) {
+#pragma omp parallel for
+    for (int64_t r = 0; r < (int64_t)(P.E * P.uc); ++r) rows_permute_thread(P, (uint64_t)r);
 }
 
 void launch_prim(const PrimParams& P, void*) {

@@ -122,3 +122,16 @@ def test_import_gc_rejects_bad_arguments_without_a_device():
     lib.dashgpu_last_error.restype = ctypes.c_char_p
     assert b"kind" in lib.dashgpu_last_error()
     assert lib.dashgpu_network_circuit(None, ctypes.byref(out)) == 3
+
+
+def test_emulation_library_is_refused_by_the_product_api():
+    """Dash() only runs the CUDA engine: the tests' CPU emulation of the
+    device code (tests/emu) loads only with the explicit test flag."""
+    from conftest import EMU_LIB
+    from paper_2302_06361_b200.engine import CudaError, Dash
+
+    if not os.path.exists(EMU_LIB):
+        pytest.skip("emulation library not built")
+    with pytest.raises(CudaError, match="not the CUDA engine"):
+        Dash(lib_path=EMU_LIB)
+    assert Dash(lib_path=EMU_LIB, emulation=True).lib.dashgpu_backend() == 2

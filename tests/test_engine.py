@@ -669,3 +669,28 @@ def test_import_gc_lenet_batch(gpu):
     assert bo2.payload(0) == bo.payload(0) and bo2.payload(1) == bo.payload(1)
     out = gpu.decode_outputs(net, gpu.import_bundle(net, bo2.payload(0) + bo2.payload(1), True))
     assert out.tolist() == gpu.decode_outputs(net, bo).tolist()
+
+
+def test_foreign_or_misshapen_bundles_are_data_errors(eng):
+    # evaluate / decode_outputs input checks (garble.cpp:265-280, 314-322):
+    # a bundle of another network, or of the wrong element count, is refused
+    from paper_2302_06361_b200.engine import DataError
+
+    g = eng.model("model_tiny", 1000, 8)
+    a = eng.garble(g, seed_hex(0x51))
+    b = eng.garble(g, seed_hex(0x52))
+    x = g.random_input(3)[None, :]
+    bi_b = eng.garble_inputs(b, x)
+    with pytest.raises(DataError):
+        eng.evaluate(a, bi_b)
+    bo_b = eng.evaluate(b, bi_b)
+    with pytest.raises(DataError):
+        eng.decode_outputs(a, bo_b)
+    lanes = [bo_b.labels(i) for i in range(g.info.k)]
+    wrong = eng.bundle_from_labels(a, [l[:, :2] for l in lanes], output=True)  # 2 of 3 output elements
+    with pytest.raises(DataError):
+        eng.decode_outputs(a, wrong)
+    with pytest.raises(DataError):
+        eng.evaluate(a, eng.bundle_from_labels(a, [l[:, :2] for l in lanes], output=False))
+    with pytest.raises(DataError):
+        eng.bundle_from_labels(a, lanes[:-1], output=True)

@@ -31,7 +31,7 @@ def _worker(rank, world, port, B, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    eng = Dash(lib_path=EMU_LIB)
+    eng = Dash(lib_path=EMU_LIB, emulation=True)
     g = eng.model("model_tiny", 1000, 8)
     seeds = step_seeds(0, B)
     a, b = shard_range(B, world, rank)
@@ -77,7 +77,7 @@ def _stream_worker(rank, world, port, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    eng = Dash(lib_path=EMU_LIB)
+    eng = Dash(lib_path=EMU_LIB, emulation=True)
     g = eng.model("relu1000", 0, 3)
     x = np.random.default_rng(2).integers(-14, 15, size=(1, 1000))
     a, b = shard_range(1000, world, rank)
@@ -102,3 +102,26 @@ def test_two_rank_element_sharded_layer_equals_single_process(tmp_path, emu):
     single, _, _ = emu.infer_stream(g, int(7).to_bytes(16, "big"), x, 256)
     assert (got == single[0]).all()
     assert (single[0] == np.maximum(x[0], 0)).all()
+
+
+@pytest.mark.skipif(not os.path.exists(EMU_LIB), reason="emulation library not built")
+def test_bench_launches_ranks_itself_and_verifies_the_gather():
+    """bench.py --gpus 2 with no launcher spawns two ranks itself (torchrun on
+    127.0.0.1), shards the batch, all-gathers the decoded outputs and checks
+    the gathered shards against each rank's own decode.  --emulate swaps the
+    GPU for the CPU emulation and NCCL for gloo; the launcher is the same."""
+    import json
+    import subprocess
+    import sys
+
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--emulate", "--model", "model_tiny",
+           "--batch", "3", "--steps", "2", "--warmup", "1", "--no-cpu"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 6
+    assert d["gather"]["verified"] is True
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
