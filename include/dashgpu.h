@@ -211,6 +211,15 @@ int dashgpu_profile_read(double* ms, uint64_t* launches, int max_kinds);
  * out[3] work items, out[4] lanes per element.  Lets parity tests pin the
  * launch configuration a benchmark times. */
 int dashgpu_last_act_launch(int garble, uint32_t out[5]);
+/* The element tape of the circuit's ReLU (kind 3) or SignAct (kind 4)
+ * gadget as recorded from the reference gadget DAG (gadgets.hpp:146-481):
+ * per op its kind (1 proj, 2 grr, 3 half, 4 mm-half, 5 add, 6 add-const,
+ * 7 output, 8 fused add), input / output moduli and gate / wire / ciphertext
+ * offsets inside the element.  ops == NULL: *n = op count only. */
+typedef struct {
+    uint32_t kind, pm, qm, gate_off, wire_off, ct_off;
+} dashgpu_tape_op;
+int dashgpu_activation_tape(const dashgpu_circuit* c, int kind, dashgpu_tape_op* ops, uint32_t cap, uint32_t* n);
 
 /* ---- primitive kernels (parity tests) ----
  * op 0: decompress_mod(in[i], m) -> digits (u16), then compress -> out[i]

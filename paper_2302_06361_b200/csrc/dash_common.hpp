@@ -55,6 +55,17 @@ struct ModC {
     uint32_t bits[4]; // pow2: low e*n bits
     uint32_t hi[4];   // pow2: top bit of every field
     uint32_t lo[4];   // pow2: bottom bit of every field
+    // word values by byte dot products (dash_device.cuh wval):
+    // d0 + m d1 = dp4a(x, wlo), d2 + m d3 = dp4a(x, whi)
+    uint32_t wlo, whi, m2;
+    uint32_t negm, negm4;  // (uint32_t)-m, -m^4: x - q m as one multiply-add
+    // Horner compress (dash_device.cuh horner): hp words per step (2 when
+    // m^8 < 2^32), step multiplier m8 = m^(4 hp), htop words in the top step,
+    // hlim[L-1] steps whose partial value fits L 32-bit limbs
+    uint32_t m8;
+    uint8_t hp, htop, hlim[4];
+    // chunk recombination (lb_enc / lb_dec_c): limbs of D^(j+1) per chunk j
+    uint8_t climbs[21];
 };
 
 // Activation-tape operations (one per gadget call of the reference's

@@ -230,11 +230,11 @@ DASH_HD uint32_t divmod_D(uint32_t c[4], const ModC& M, int limbs) {
 // Four base-m digits of v < m^4 packed as bytes.
 DASH_HD uint32_t split4(uint32_t v, const ModC& M) {
     const uint32_t q1 = fdiv(v, M.mag_m, M.sh_m);
-    const uint32_t d0 = v - q1 * M.m;
+    const uint32_t d0 = q1 * M.negm + v;  // v - q1 m
     const uint32_t q2 = fdiv(q1, M.mag_m, M.sh_m);
-    const uint32_t d1 = q1 - q2 * M.m;
+    const uint32_t d1 = q2 * M.negm + q1;
     const uint32_t q3 = fdiv(q2, M.mag_m, M.sh_m);
-    const uint32_t d2 = q2 - q3 * M.m;
+    const uint32_t d2 = q3 * M.negm + q2;
     return d0 | (d1 << 8) | (d2 << 16) | (q3 << 24);
 }
 
@@ -255,7 +255,7 @@ DASH_HD void mul_add_128(uint32_t c[4], uint32_t m, uint32_t add) {
 DASH_HD uint32_t swar_add(uint32_t a, uint32_t b, const ModC& M) {
     const uint32_t s = a + b;
     const uint32_t ge = ((s + M.addc) >> 7) & 0x01010101u;
-    return s - ge * M.m;
+    return ge * M.negm + s;  // s - ge * m in one IMAD
 }
 
 DASH_HD void p2_add(uint32_t a[4], const uint32_t b[4], const ModC& M) {
@@ -461,21 +461,139 @@ DASH_HD void lb_scale(LB o, LB a, uint32_t s, const ModC& M) {
     for (int w = 0; w < M.nw; ++w) o[w] = scale_word(a[w], s, M);
 }
 
-// compress (label.cpp:208-219): Horner in base m^4, one word per step
-DASH_HD U4 lb_compress(LB a, const ModC& M) {
-    if (M.pow2) return lb_u4(a);
-    uint32_t c[4] = {0, 0, 0, 0};
-    for (int w = M.nw - 1; w >= 0; --w) {
-        const uint32_t x = a[w];
-        const uint32_t cv = (x & 0xff) + M.m * (((x >> 8) & 0xff) + M.m * (((x >> 16) & 0xff) + M.m * (x >> 24)));
-        mul_add_128(c, M.m4, cv);
+// ---- multi-limb helpers of the codec: c = c * mul + v on L limbs (the
+// result is known to fit L limbs; higher limbs stay zero) ----
+DASH_HD void mad_l2(uint32_t& c0, uint32_t& c1, uint32_t mul, uint32_t v) {
+    const uint64_t t = (uint64_t)c0 * mul + v;
+    c0 = (uint32_t)t;
+    c1 = c1 * mul + (uint32_t)(t >> 32);
+}
+DASH_HD void mad_l3(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t mul, uint32_t v) {
+#if defined(__CUDA_ARCH__)
+    uint32_t h0, h1;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(h0) : "r"(c0), "r"(mul));
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(h1) : "r"(c1), "r"(mul));
+    asm("mad.lo.cc.u32 %0, %0, %3, %4;\n\t"
+        "madc.lo.cc.u32 %1, %1, %3, %5;\n\t"
+        "madc.lo.u32 %2, %2, %3, %6;"
+        : "+r"(c0), "+r"(c1), "+r"(c2)
+        : "r"(mul), "r"(v), "r"(h0), "r"(h1));
+#else
+    uint64_t t = (uint64_t)c0 * mul + v;
+    c0 = (uint32_t)t;
+    t = (uint64_t)c1 * mul + (t >> 32);
+    c1 = (uint32_t)t;
+    c2 = c2 * mul + (uint32_t)(t >> 32);
+#endif
+}
+DASH_HD void mad_l4(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t mul, uint32_t v) {
+#if defined(__CUDA_ARCH__)
+    uint32_t h0, h1, h2;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(h0) : "r"(c0), "r"(mul));
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(h1) : "r"(c1), "r"(mul));
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(h2) : "r"(c2), "r"(mul));
+    asm("mad.lo.cc.u32 %0, %0, %4, %5;\n\t"
+        "madc.lo.cc.u32 %1, %1, %4, %6;\n\t"
+        "madc.lo.cc.u32 %2, %2, %4, %7;\n\t"
+        "madc.lo.u32 %3, %3, %4, %8;"
+        : "+r"(c0), "+r"(c1), "+r"(c2), "+r"(c3)
+        : "r"(mul), "r"(v), "r"(h0), "r"(h1), "r"(h2));
+#else
+    uint64_t t = (uint64_t)c0 * mul + v;
+    c0 = (uint32_t)t;
+    t = (uint64_t)c1 * mul + (t >> 32);
+    c1 = (uint32_t)t;
+    t = (uint64_t)c2 * mul + (t >> 32);
+    c2 = (uint32_t)t;
+    c3 = c3 * mul + (uint32_t)(t >> 32);
+#endif
+}
+// c += v * p on L limbs (p = D^j, c + v p fits L limbs)
+DASH_HD void mac_l(uint32_t c[4], const uint32_t p[4], uint32_t v, int L) {
+    uint64_t t = (uint64_t)p[0] * v + c[0];
+    c[0] = (uint32_t)t;
+    if (L < 2) return;
+    t = (uint64_t)p[1] * v + c[1] + (t >> 32);
+    c[1] = (uint32_t)t;
+    if (L < 3) return;
+    t = (uint64_t)p[2] * v + c[2] + (t >> 32);
+    c[2] = (uint32_t)t;
+    if (L < 4) return;
+    c[3] = (uint32_t)((uint64_t)p[3] * v + c[3] + (t >> 32));
+}
+
+DASH_HD uint32_t dp4a_u8(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+    return __dp4a(a, b, c);
+#else
+    for (int i = 0; i < 4; ++i) c += ((a >> (8 * i)) & 0xffu) * ((b >> (8 * i)) & 0xffu);
+    return c;
+#endif
+}
+// value of one word of four base-m digits, d0 + m d1 + m^2 (d2 + m d3) < m^4
+DASH_HD uint32_t wval(uint32_t x, const ModC& M) { return dp4a_u8(x, M.wlo, dp4a_u8(x, M.whi, 0u) * M.m2); }
+
+// compress (label.cpp:208-219) as a Horner over the label's words, top
+// down: word(w) yields word w (called once per word, nw-1 .. 0).  Two words
+// per step when m^8 < 2^32, and each step only touches the 32-bit limbs its
+// partial value can occupy (ModC::hlim, host-computed).
+template <class F>
+DASH_HD U4 horner(const ModC& M, F&& word) {
+    int w = M.nw - 1;
+    uint32_t c0 = wval(word(w), M), c1 = 0, c2 = 0, c3 = 0;
+    --w;
+    if (M.htop == 2) {
+        c0 = c0 * M.m4 + wval(word(w), M);
+        --w;
+    }
+    const uint32_t mul = M.m8, m4 = M.m4;
+    const bool two = M.hp == 2;
+    auto stepv = [&]() {
+        uint32_t v = wval(word(w), M);
+        --w;
+        if (two) {
+            v = v * m4 + wval(word(w), M);
+            --w;
+        }
+        return v;
+    };
+#if defined(__CUDA_ARCH__)
+#pragma unroll 1
+#endif
+    for (int i = M.hlim[0]; i > 0; --i) c0 = c0 * mul + stepv();
+#if defined(__CUDA_ARCH__)
+#pragma unroll 1
+#endif
+    for (int i = M.hlim[1]; i > 0; --i) {
+        const uint32_t v = stepv();
+        mad_l2(c0, c1, mul, v);
+    }
+#if defined(__CUDA_ARCH__)
+#pragma unroll 1
+#endif
+    for (int i = M.hlim[2]; i > 0; --i) {
+        const uint32_t v = stepv();
+        mad_l3(c0, c1, c2, mul, v);
+    }
+#if defined(__CUDA_ARCH__)
+#pragma unroll 1
+#endif
+    for (int i = M.hlim[3]; i > 0; --i) {
+        const uint32_t v = stepv();
+        mad_l4(c0, c1, c2, c3, mul, v);
     }
     U4 o;
-    o.x[0] = c[0];
-    o.x[1] = c[1];
-    o.x[2] = c[2];
-    o.x[3] = c[3];
+    o.x[0] = c0;
+    o.x[1] = c1;
+    o.x[2] = c2;
+    o.x[3] = c3;
     return o;
+}
+
+// compress (label.cpp:208-219)
+DASH_HD U4 lb_compress(LB a, const ModC& M) {
+    if (M.pow2) return lb_u4(a);
+    return horner(M, [&](int w) { return a[w]; });
 }
 
 // Returns compress(key), then key += R (the per-row key step of every
@@ -488,22 +606,11 @@ DASH_HD U4 lb_key_step(LB key, const uint32_t* R, const ModC& M) {
         lb_set_u4(key, k);
         return r;
     }
-    uint32_t c[4] = {0, 0, 0, 0};
-#if defined(__CUDA_ARCH__)
-#pragma unroll kCodecUnroll
-#endif
-    for (int w = M.nw - 1; w >= 0; --w) {
+    return horner(M, [&](int w) {
         const uint32_t x = key[w];
-        const uint32_t cv = (x & 0xff) + M.m * (((x >> 8) & 0xff) + M.m * (((x >> 16) & 0xff) + M.m * (x >> 24)));
-        mul_add_128(c, M.m4, cv);
         key[w] = swar_add(x, R[w], M);
-    }
-    U4 o;
-    o.x[0] = c[0];
-    o.x[1] = c[1];
-    o.x[2] = c[2];
-    o.x[3] = c[3];
-    return o;
+        return x;
+    });
 }
 
 // Streams the base-m words of decompress_mod(cin, m) (label.cpp:228-232)
@@ -520,7 +627,7 @@ DASH_HD void digits_stream(const U4& cin, const ModC& M, F&& f) {
 #endif
         for (int ww = 0; ww < M.W && w < M.nw; ++ww, ++w) {
             const uint32_t q = fdiv(chunk, M.mag_m4, M.sh_m4);
-            uint32_t v = split4(chunk - q * M.m4, M);
+            uint32_t v = split4(q * M.negm4 + chunk, M);
             chunk = q;
             if (w == M.nw - 1) v &= keep;
             f(w, v);
@@ -528,10 +635,67 @@ DASH_HD void digits_stream(const U4& cin, const ModC& M, F&& f) {
     }
 }
 
+// digits_stream with a callback after every chunk of W words (fc(j))
+template <class F, class G>
+DASH_HD void digits_stream_c(const U4& cin, const ModC& M, F&& f, G&& fc) {
+    uint32_t c[4] = {cin.x[0], cin.x[1], cin.x[2], cin.x[3]};
+    const uint32_t keep = top_keep(M);
+    int w = 0;
+    for (int j = 0; j < M.nchunks; ++j) {
+        uint32_t chunk = divmod_D(c, M, M.limbs[j]);
+        for (int ww = 0; ww < M.W && w < M.nw; ++ww, ++w) {
+            const uint32_t q = fdiv(chunk, M.mag_m4, M.sh_m4);
+            uint32_t v = split4(q * M.negm4 + chunk, M);
+            chunk = q;
+            if (w == M.nw - 1) v &= keep;
+            f(w, v);
+        }
+        fc(j);
+    }
+}
+
+// Accumulates a label's compressed value low chunk first: word values are
+// combined inside a chunk in 32 bits (the chunk's value < D < 2^31), and
+// chunk j enters the 128-bit sum as chunk * D^j on the limbs it can reach.
+struct ChunkAcc {
+    uint32_t c[4] = {0, 0, 0, 0}, pd[4] = {1, 0, 0, 0};
+    uint32_t acc = 0, pw = 1;
+    DASH_HD void word(uint32_t t, const ModC& M) {
+        acc += wval(t, M) * pw;
+        pw *= M.m4;
+    }
+    DASH_HD void chunk(int j, const ModC& M) {
+        const int L = M.climbs[j];
+        mac_l(c, pd, acc, L);
+        acc = 0;
+        pw = 1;
+        if (j + 1 < M.nchunks) {  // pd *= D
+            uint64_t t = (uint64_t)pd[0] * M.D;
+            pd[0] = (uint32_t)t;
+            t = (uint64_t)pd[1] * M.D + (t >> 32);
+            pd[1] = (uint32_t)t;
+            t = (uint64_t)pd[2] * M.D + (t >> 32);
+            pd[2] = (uint32_t)t;
+            pd[3] = pd[3] * M.D + (uint32_t)(t >> 32);
+        }
+    }
+    DASH_HD U4 value() const {
+        U4 o;
+        o.x[0] = c[0];
+        o.x[1] = c[1];
+        o.x[2] = c[2];
+        o.x[3] = c[3];
+        return o;
+    }
+};
+
 // digits_stream of two values in one loop: two independent division chains
 // interleave (evaluation decrypts ct - pad; its latency is this chain)
-template <class F>
-DASH_HD void digits_stream2(const U4& x, const U4& y, const ModC& M, F&& f) {
+struct NoChunk {
+    DASH_HD void operator()(int) const {}
+};
+template <class F, class G = NoChunk>
+DASH_HD void digits_stream2(const U4& x, const U4& y, const ModC& M, F&& f, G&& fc = G()) {
     uint32_t a[4] = {x.x[0], x.x[1], x.x[2], x.x[3]}, b[4] = {y.x[0], y.x[1], y.x[2], y.x[3]};
     const uint32_t keep = top_keep(M);
     int w = 0;
@@ -543,7 +707,7 @@ DASH_HD void digits_stream2(const U4& x, const U4& y, const ModC& M, F&& f) {
 #endif
         for (int ww = 0; ww < M.W && w < M.nw; ++ww, ++w) {
             const uint32_t qa = fdiv(ca, M.mag_m4, M.sh_m4), qb = fdiv(cb, M.mag_m4, M.sh_m4);
-            uint32_t va = split4(ca - qa * M.m4, M), vb = split4(cb - qb * M.m4, M);
+            uint32_t va = split4(qa * M.negm4 + ca, M), vb = split4(qb * M.negm4 + cb, M);
             ca = qa;
             cb = qb;
             if (w == M.nw - 1) {
@@ -552,6 +716,7 @@ DASH_HD void digits_stream2(const U4& x, const U4& y, const ModC& M, F&& f) {
             }
             f(w, va, vb);
         }
+        fc(j);
     }
 }
 
@@ -565,49 +730,40 @@ DASH_HD void lb_decompress(LB out, const U4& c, const ModC& M) {
     digits_stream(c, M, [&](int w, uint32_t v) { out[w] = v; });
 }
 
-// c += v * pw (4-limb accumulator, v < 2^28)
-DASH_HD void mac_128(uint32_t c[4], const uint32_t pw[4], uint32_t v) {
-    uint64_t t = (uint64_t)pw[0] * v + c[0];
-    c[0] = (uint32_t)t;
-    t = (uint64_t)pw[1] * v + c[1] + (t >> 32);
-    c[1] = (uint32_t)t;
-    t = (uint64_t)pw[2] * v + c[2] + (t >> 32);
-    c[2] = (uint32_t)t;
-    c[3] = (uint32_t)((uint64_t)pw[3] * v + c[3] + (t >> 32));
-}
-
 // Row encryption (cipher.cpp:27-29 with the payload of gadgets.hpp):
 //   ct = compress(decompress_mod(H, q) + base [+ g] [- s*sub])
 // The pad digits stream out low word first; the ciphertext is accumulated
-// low-first as sum_w value(word_w) * (m^4)^w, so no scratch label is needed.
-DASH_HD U4 lb_enc(const U4& H, LB base, const uint32_t* g, LB* sub, uint32_t s, const ModC& M) {
+// low chunk first (ChunkAcc), so no scratch label is needed.
+// G: payload adds the global label g; SUB: payload subtracts s * sub
+template <bool G, bool SUB>
+DASH_HD U4 lb_enc_t(const U4& H, LB base, const uint32_t* g, LB sub, uint32_t s, const ModC& M) {
     if (M.pow2) {
         U4 t;
         for (int i = 0; i < 4; ++i) t.x[i] = H.x[i] & M.bits[i];
         U4 b = lb_u4(base);
         p2_add(t.x, b.x, M);
-        if (g) {
+        if (G) {
             uint32_t y[4] = {g[0], g[1], g[2], g[3]};
             p2_add(t.x, y, M);
         }
-        if (sub) t = p2_sub(t, p2_scale(lb_u4(*sub), s, M), M);
+        if (SUB) t = p2_sub(t, p2_scale(lb_u4(sub), s, M), M);
         return t;
     }
-    uint32_t c[4] = {0, 0, 0, 0}, pw[4] = {1, 0, 0, 0};
-    digits_stream(H, M, [&](int w, uint32_t v) {
-        uint32_t t = swar_add(v, base[w], M);
-        if (g) t = swar_add(t, g[w], M);
-        if (sub) t = swar_add(t, M.spread - scale_word((*sub)[w], s, M), M);
-        const uint32_t cv = (t & 0xff) + M.m * (((t >> 8) & 0xff) + M.m * (((t >> 16) & 0xff) + M.m * (t >> 24)));
-        mac_128(c, pw, cv);
-        mul_add_128(pw, M.m4, 0);
-    });
-    U4 o;
-    o.x[0] = c[0];
-    o.x[1] = c[1];
-    o.x[2] = c[2];
-    o.x[3] = c[3];
-    return o;
+    ChunkAcc A;
+    digits_stream_c(
+        H, M,
+        [&](int w, uint32_t v) {
+            uint32_t t = swar_add(v, base[w], M);
+            if (G) t = swar_add(t, g[w], M);
+            if (SUB) t = swar_add(t, M.spread - scale_word(sub[w], s, M), M);
+            A.word(t, M);
+        },
+        [&](int j) { A.chunk(j, M); });
+    return A.value();
+}
+DASH_HD U4 lb_enc(const U4& H, LB base, const uint32_t* g, LB* sub, uint32_t s, const ModC& M) {
+    if (sub) return g ? lb_enc_t<true, true>(H, base, g, *sub, s, M) : lb_enc_t<false, true>(H, base, g, *sub, s, M);
+    return g ? lb_enc_t<true, false>(H, base, g, base, s, M) : lb_enc_t<false, false>(H, base, g, base, s, M);
 }
 
 // out += digits(c)  (componentwise, streamed: no scratch label)
@@ -670,19 +826,11 @@ DASH_HD U4 lb_dec_c(const U4& ct, const U4& H, const ModC& M) {
         }
         return p2_sub(a, b, M);
     }
-    uint32_t c[4] = {0, 0, 0, 0}, pw[4] = {1, 0, 0, 0};
-    digits_stream2(ct, H, M, [&](int, uint32_t a, uint32_t h) {
-        const uint32_t t = swar_add(a, M.spread - h, M);
-        const uint32_t cv = (t & 0xff) + M.m * (((t >> 8) & 0xff) + M.m * (((t >> 16) & 0xff) + M.m * (t >> 24)));
-        mac_128(c, pw, cv);
-        mul_add_128(pw, M.m4, 0);
-    });
-    U4 o;
-    o.x[0] = c[0];
-    o.x[1] = c[1];
-    o.x[2] = c[2];
-    o.x[3] = c[3];
-    return o;
+    ChunkAcc A;
+    digits_stream2(
+        ct, H, M, [&](int, uint32_t a, uint32_t h) { A.word(swar_add(a, M.spread - h, M), M); },
+        [&](int j) { A.chunk(j, M); });
+    return A.value();
 }
 
 // ---- global label rows: u8 digits, four per word, word stride `stride` ----
@@ -966,7 +1114,7 @@ DASH_NI void garble_rows_n(LB X, LB base, AesTab t, const uint32_t* mult, uint32
     for (uint32_t row = r0; row < p; ++row) {
         const U4 H = hash_tw<true>(lb_key_step(X, Rp, Mp), g, row, 0, t);
         const uint32_t v = phi ? phi[a] : (a * r) % p;
-        const U4 ct = lb_enc(H, base, Mrow + (uint64_t)v * NWMAX, nullptr, 0, Mq);
+        const U4 ct = lb_enc_t<true, false>(H, base, Mrow + (uint64_t)v * NWMAX, base, 0, Mq);
         store_row(out, ct);
         out += rs;
         a = a + 1 == p ? 0 : a + 1;
@@ -1047,7 +1195,7 @@ DASH_HD void garble_op(const ActParams& P, const Elt& e, const TapeOp& op) {
                 const U4 Kc = lb_key_step(e.K, Rq, Mq);
                 const U4 H = hash_tw(Kc, g, row, 1, e.t);
                 LB X = e.X;
-                store_row(R + (uint64_t)(p + row) * e.rs, lb_enc(H, e.A, nullptr, &X, mm ? s : row, Mp));
+                store_row(R + (uint64_t)(p + row) * e.rs, lb_enc_t<false, true>(H, e.A, nullptr, X, mm ? s : row, Mp));
                 if (mm) {  // encrypt_short field of this row (cipher.cpp:45-60)
                     const U4 Hs = hash_tw(Kc, g, 0, 2, e.t);
                     u4_or_shl(sb, (s ^ (Hs.x[0] & fmask)) & fmask, fw * row);

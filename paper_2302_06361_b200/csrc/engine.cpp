@@ -108,6 +108,8 @@ static ModC make_modc(int m) {
     magic31((uint64_t)m, c.mag_m, c.sh_m);
     c.mag64 = (uint64_t)(~0ull / (uint64_t)m) + 1;
     c.spread = (uint32_t)m * 0x01010101u;
+    c.negm = 0u - (uint32_t)m;
+    c.negm4 = 0u - (uint32_t)m * m * m * m;
     c.addc = (uint32_t)(128 - (m < 128 ? m : 127)) * 0x01010101u;
     if (c.pow2) {
         u128 bits = 0, hi = 0, lo = 0;
@@ -146,6 +148,27 @@ static ModC make_modc(int m) {
     }
     magic31(c.m4, c.mag_m4, c.sh_m4);
     c.invD = ~0ull / (uint64_t)c.D;
+    // byte dot-product word values and the paired / limb-bounded Horner
+    c.wlo = 1u | ((uint32_t)m << 8);
+    c.whi = (1u << 16) | ((uint32_t)m << 24);
+    c.m2 = (uint32_t)m * m;
+    const u128 m8 = (u128)c.m4 * c.m4;
+    c.hp = m8 < ((u128)1 << 32) ? 2 : 1;
+    c.m8 = c.hp == 2 ? (uint32_t)m8 : c.m4;
+    c.htop = (c.hp == 2 && c.nw % 2 == 0) ? 2 : 1;
+    auto limbs_of_digits = [&](int digits) {  // limbs of m^digits - 1
+        u128 v = 1;
+        for (int i = 0; i < digits; ++i) v *= (u128)m;
+        const int b = bitlen(v - 1);
+        return std::max(1, (b + 31) / 32);
+    };
+    for (int wlo = c.nw - c.htop - c.hp; wlo >= 0; wlo -= c.hp) {
+        const int L = limbs_of_digits(std::min<int>(c.n, c.n - 4 * wlo));
+        ++c.hlim[L - 1];
+    }
+    if (limbs_of_digits(std::min<int>(c.n, 4 * c.htop)) != 1) throw std::logic_error("horner top step overflow");
+    for (int j = 0; j < c.nchunks && j < 21; ++j)
+        c.climbs[j] = (uint8_t)limbs_of_digits(std::min<int>(c.n, 4 * c.W * (j + 1)));
     return c;
 }
 
@@ -3189,6 +3212,20 @@ int dashgpu_profile_read(double* ms, uint64_t* launches, int max_kinds) {
     int k = 0;
     int rc = guarded([&] { k = dev::prof_read(ms, launches, max_kinds); });
     return rc ? -rc : k;
+}
+
+int dashgpu_activation_tape(const dashgpu_circuit* c, int kind, dashgpu_tape_op* ops, uint32_t cap, uint32_t* n) {
+    return guarded([&] {
+        if (!c || !n) throw DataError("null argument");
+        const auto& t = kind == DASH_LAYER_SIGNACT ? c->sign_tape : c->relu_tape;
+        if (!t) throw DataError("circuit has no activation layer");
+        *n = (uint32_t)t->ops.size();
+        if (!ops) return;
+        for (uint32_t i = 0; i < *n && i < cap; ++i) {
+            const TapeOp& o = t->ops[i];
+            ops[i] = dashgpu_tape_op{o.kind, o.pm, o.qm, o.gate_off, o.wire_off, o.ct_off};
+        }
+    });
 }
 
 int dashgpu_last_act_launch(int garble, uint32_t out[5]) {
