@@ -80,8 +80,15 @@ int dashgpu_version(void);
 /* 1 = the CUDA engine (this library); anything else is a test build. */
 int dashgpu_backend(void);
 int dashgpu_init(int device);
-/* Stream all work is enqueued on (a cudaStream_t; NULL = legacy default). */
+/* Stream all work of the calling host thread is enqueued on (a cudaStream_t;
+ * NULL = legacy default).  Thread-local: each host thread drives its own. */
 int dashgpu_set_stream(void* stream);
+/* Per-call device and stream: selects `device` for the calling
+ * host thread (uploading the constant tables on first use of that device)
+ * and sets the thread's stream.  Circuits and networks are bound to the
+ * device they were first used on; dashgpu_infer keeps one workspace per
+ * stream, so threads on different streams run one circuit concurrently. */
+int dashgpu_use(int device, void* stream);
 
 /* ---- circuits (host) ---- */
 int dashgpu_circuit_create(const dash_circuit_desc* desc, dashgpu_circuit** out);
@@ -106,6 +113,13 @@ int dashgpu_plain_forward(const dashgpu_circuit* c, const int64_t* in, int64_t* 
 int dashgpu_garble(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
                    dashgpu_network** out);
 void dashgpu_network_destroy(dashgpu_network* n);
+/* Garbler side, once the GCs have been exported (serialize_garbled_circuit
+ * handed them to the evaluator): frees the ciphertexts, gadget slots and
+ * per-layer planes, keeping only what garble_inputs and decode_outputs need
+ * (offsets and their multiples, input base labels, decoding tables) -- the
+ * reference garbler likewise keeps only EncodingInfo / DecodingInfo.  Later
+ * export_gc / evaluate / layer calls on n fail with DASHGPU_ERR_DATA. */
+int dashgpu_network_release_gc(dashgpu_network* n);
 /* values: host [batch][n_in] signed quantized inputs */
 int dashgpu_garble_inputs(dashgpu_network* n, const int64_t* values, dashgpu_bundle** out);
 int dashgpu_evaluate(dashgpu_network* n, const dashgpu_bundle* in, dashgpu_bundle** out);

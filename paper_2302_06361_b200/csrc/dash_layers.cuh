@@ -68,9 +68,13 @@ DASH_HD void linear_thread(const LinParams& L, uint32_t b, uint32_t w, uint32_t 
     const uint32_t zw = L.zero[(uint64_t)b * L.zstride + w];
     const uint32_t rw = L.garbler ? L.R[(uint64_t)b * L.zstride + w] : 0u;
     uint32_t accs[4] = {acc0, acc1, acc2, acc3};
+    const uint32_t c31 = 0x7fffffffu - fdiv(0x7fffffffu, M.mag_m, M.sh_m) * L.p + 1u;  // == 2^31 mod p (up to one p)
     uint32_t o = 0;
     for (int j = 0; j < 4; ++j) {
-        const uint32_t s = accs[j] - fdiv(accs[j], M.mag_m, M.sh_m) * L.p;
+        // u32 wrap-around as the reference's accumulator (layer.cpp:116-118);
+        // the 31-bit-exact magic sees the low 31 bits plus 2^31 mod p
+        const uint32_t lo = accs[j] & 0x7fffffffu;
+        const uint32_t s = lo - fdiv(lo, M.mag_m, M.sh_m) * L.p + (accs[j] >> 31) * c31;
         const uint32_t t = s + z * ((zw >> (8 * j)) & 0xffu) + nb * ((rw >> (8 * j)) & 0xffu);
         const uint32_t d = t - fdiv(t, M.mag_m, M.sh_m) * L.p;
         o |= d << (8 * j);

@@ -16,6 +16,7 @@
 //  * reference wire formats (garble.cpp:347-526) and the C ABI (dashgpu.h).
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -929,6 +930,11 @@ struct DevBuf {
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { dev::release(p); }
+    void reset() {
+        dev::release(p);
+        p = nullptr;
+        n = 0;
+    }
     void ensure(size_t bytes) {
         if (bytes <= n && p) return;
         dev::release(p);
@@ -961,7 +967,10 @@ struct HostBuf {
     }
 };
 
-static void* g_stream = nullptr;
+// Device and stream of this host thread's calls (dashgpu_use /
+// dashgpu_set_stream): every entry point enqueues on the calling thread's
+// stream, so several host threads can drive several streams (and devices).
+static thread_local void* g_stream = nullptr;
 
 struct HLayer {
     int kind = 0;
@@ -1018,8 +1027,15 @@ struct dashgpu_circuit {
     std::set<int> moduli;
     uint64_t relu_elements = 0, linear_macs = 0;
     std::vector<dash_layer_desc> desc_layers;  // for dashgpu_circuit_desc_view
-    std::unique_ptr<dashgpu::Network> workspace;  // dashgpu_infer cache
+    // dashgpu_infer caches: one workspace per stream, so concurrent streams
+    // (host threads) run the same circuit without serializing on it
+    struct Workspace {
+        std::unique_ptr<dashgpu::Network> net;
+        std::mutex mu;
+    };
+    std::map<void*, std::unique_ptr<Workspace>> workspaces;
     bool uploaded = false;  // per-layer device buffers created (upload_circuit)
+    int device = -1;        // device the per-layer buffers live on
     // evaluator copy parsed from a GC (dashgpu_import_gc): private weights
     // withheld, so it can evaluate but not garble; sign spec taken from the GC
     bool eval_only = false;
@@ -1239,7 +1255,12 @@ static void prepare_circuit(dashgpu_circuit& c) {
 
 static void upload_circuit(dashgpu_circuit& c) {
     check_constants();
-    if (c.uploaded) return;
+    if (c.uploaded) {
+        if (c.device != dev::get_device())
+            throw DataError("circuit parameters live on device " + std::to_string(c.device) +
+                            "; build one circuit per device");
+        return;
+    }
     for (auto& l : c.layers) {
         l.wres.clear();
         l.zt.clear();
@@ -1262,6 +1283,7 @@ static void upload_circuit(dashgpu_circuit& c) {
         }
     }
     dev::sync(g_stream);
+    c.device = dev::get_device();
     c.uploaded = true;
 }
 
@@ -1309,6 +1331,12 @@ struct Network {
         q.flags = qflags.as<uint32_t>();
         q.flags_cap = qflags.n / 4;
         return q;
+    }
+    // dashgpu_network_release_gc: ciphertexts, gadget slots and layer planes
+    // freed once the GC has been exported; encoding and decoding remain
+    bool gc_released = false;
+    void require_gc() const {
+        if (gc_released) throw DataError("garbled circuit already released (dashgpu_network_release_gc)");
     }
     size_t slot_used = 0;  // U4 entries of `slots` handed out to garbled layers
     size_t mm_used = 0;    // U4 entries of `mmlab` handed out to garbled layers
@@ -1685,6 +1713,7 @@ static void garble_act_flush(Network& n) {
 
 static void garble_into(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
     garble_setup(n, seeds, B, seeds_on_device);
+    n.gc_released = false;
     // run the layers on the input base planes
     const Lanes* cur = run_layers(n, true, n.base);
     garble_act_flush(n);
@@ -1745,6 +1774,7 @@ static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
     // network or element count would make the kernels read out of bounds
     if (in.net != &n || in.B != n.B || in.output) throw DataError("garbled input bundle does not match the network");
     if (in.lanes.E != c.n_in || in.lanes.lane.size() != (size_t)k) throw DataError("garbled input shape mismatch");
+    n.require_gc();
     const Lanes* cur = run_layers(n, false, in.lanes);
     out.net = &n;
     out.B = n.B;
@@ -2118,6 +2148,7 @@ static size_t out_bytes(const std::vector<uint8_t>& v, uint8_t* buf, size_t cap,
 static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
     const dashgpu_circuit& c = *n.c;
     if (b >= n.B) throw DataError("inference index out of range");
+    n.require_gc();
     Writer w;
     w.b.reserve(c.total_cts * 16 + 4096);
     w.header(1);
@@ -2535,16 +2566,21 @@ static void build(dashgpu_circuit& c, const std::string& name, uint32_t seed, in
 
 // ============================================================ constants
 
-static bool g_constants = false;
+static std::atomic<uint64_t> g_constants{0};  // devices whose constant tables are uploaded
 static std::mutex g_init_mu;
 
 static void check_constants() {
-    if (!g_constants) throw std::runtime_error("dashgpu_init() has not been called");
+    const int d = dev::get_device();
+    if (d < 0 || d >= 64 || !((g_constants.load() >> d) & 1))
+        throw std::runtime_error("dashgpu_init() / dashgpu_use() has not been called for device " +
+                                 std::to_string(d));
 }
 
 static void init_device(int device) {
     std::lock_guard<std::mutex> lk(g_init_mu);
+    if (device < 0 || device >= 64) throw DataError("device index out of range");
     dev::set_device(device);
+    if ((g_constants.load() >> device) & 1) return;
     static std::vector<ModC> mods(MAXMOD + 1);
     for (int m = 2; m <= MAXMOD; ++m) mods[m] = make_modc(m);
     uint32_t pi_rk[44];
@@ -2555,7 +2591,7 @@ static void init_device(int device) {
     uint32_t T0[256];
     t0_table(T0);
     dev::upload_constants(mods.data(), pi_rk, modslot, T0);
-    g_constants = true;
+    g_constants |= 1ull << device;
 }
 
 // plain_forward (layer.cpp:346-376, 56-109) with OverflowError range checks,
@@ -2691,6 +2727,13 @@ int dashgpu_init(int device) {
 int dashgpu_set_stream(void* stream) {
     g_stream = stream;
     return DASHGPU_OK;
+}
+
+int dashgpu_use(int device, void* stream) {
+    return guarded([&] {
+        init_device(device);  // selects the device for this thread; constants once per device
+        g_stream = stream;
+    });
 }
 
 int dashgpu_circuit_create(const dash_circuit_desc* d, dashgpu_circuit** out) {
@@ -2867,6 +2910,7 @@ static void layer_pass(dashgpu_network* n, uint32_t li, const dashgpu_bundle* in
     Network& N = *n->net;
     dashgpu_circuit& c = *N.c;
     if (li >= c.layers.size()) throw DataError("layer index out of range");
+    N.require_gc();
     const HLayer& l = c.layers[li];
     if (!in || in->b->B != N.B || in->b->lanes.E != l.E_in) throw DataError("layer input shape mismatch");
     if (l.kind == DASH_LAYER_ADD && (!in2 || in2->b->B != N.B || in2->b->lanes.E != l.E_out))
@@ -2890,6 +2934,21 @@ int dashgpu_layer_garble(dashgpu_network* n, uint32_t li, const dashgpu_bundle* 
 int dashgpu_layer_eval(dashgpu_network* n, uint32_t li, const dashgpu_bundle* in, const dashgpu_bundle* in2,
                        dashgpu_bundle** out) {
     return guarded([&] { layer_pass(n, li, in, in2, out, false); });
+}
+
+int dashgpu_network_release_gc(dashgpu_network* n) {
+    return guarded([&] {
+        if (!n) throw DataError("null network");
+        Network& N = *n->net;
+        dev::sync(g_stream);  // nothing in flight may still read them
+        for (DevBuf* b : {&N.blob, &N.slots, &N.mmlab, &N.act_dev, &N.qflags}) b->reset();
+        N.gouts.own.clear();
+        N.gouts.at.clear();
+        N.eouts.own.clear();
+        N.eouts.at.clear();
+        N.slot_used = N.mm_used = 0;
+        N.gc_released = true;
+    });
 }
 
 int dashgpu_network_finish(dashgpu_network* n, const dashgpu_bundle* fin) {
@@ -3101,6 +3160,7 @@ int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint
     return guarded([&] {
         Network& N = *n->net;
         if (b >= N.B || index >= N.c->total_cts) throw DataError("ciphertext index out of range");
+        N.require_gc();
         U4 v;
         U4* p = N.blob.as<U4>() + (uint64_t)b * N.c->total_cts + device_ct_index(*N.c, index);
         dev::d2h(&v, p, 16, g_stream);
@@ -3116,7 +3176,17 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
                   int64_t* outputs, int on_device, dashgpu_timing* t) {
     return guarded([&] {
         auto* c = const_cast<dashgpu_circuit*>(cc);
-        std::lock_guard<std::mutex> lk(c->mu);
+        // one workspace per stream: the circuit lock covers the lookup and
+        // the one-time parameter upload, the workspace lock this stream's work
+        dashgpu_circuit::Workspace* wsp;
+        {
+            std::lock_guard<std::mutex> lk(c->mu);
+            auto& slot = c->workspaces[g_stream];
+            if (!slot) slot = std::make_unique<dashgpu_circuit::Workspace>();
+            wsp = slot.get();
+            upload_circuit(*c);
+        }
+        std::lock_guard<std::mutex> lk(wsp->mu);
         using clk = std::chrono::steady_clock;
         const auto t0 = clk::now();
         // per-inference device bytes: ciphertexts + multiples + decode table + planes
@@ -3148,7 +3218,7 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
         // two streams was measured slower: the persistent garbling / eval
         // CTAs hold 196-218 KB of shared memory, so the other stream's
         // kernels cannot co-reside and the halves serialize.)
-        Network& n = *make_ws(c->workspace);
+        Network& n = *make_ws(wsp->net);
         uint32_t chunk = batch;
         if (n.cap < batch) {
             const uint64_t budget = (uint64_t)(dev::free_bytes() * 0.85) + (uint64_t)n.cap * per;
@@ -3173,8 +3243,11 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
             tm.sub_batches += 1;
         }
         if (!on_device) {
-            tm.h2d_bytes = (uint64_t)batch * (c->n_in * 8 + 16 + 44 * 4);
-            tm.d2h_bytes = (uint64_t)batch * c->n_out * c->k;
+            // seeds + quantized inputs in, decoded outputs out (AES key
+            // schedules are expanded on the device, launch parameters are
+            // staged once per network)
+            tm.h2d_bytes = (uint64_t)batch * (c->n_in * 8 + 16);
+            tm.d2h_bytes = (uint64_t)batch * c->n_out * 8;
         }
         tm.ms_total = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
         if (t) *t = tm;

@@ -287,6 +287,10 @@ __global__ void __launch_bounds__(128) prim_kernel(PrimParams P) {
 namespace dev {
 
 void set_device(int d) { ck(cudaSetDevice(d), "cudaSetDevice"); }
+int get_device() {
+    int d = -1;
+    return cudaGetDevice(&d) == cudaSuccess ? d : -1;
+}
 int backend() { return 1; }
 void* alloc(size_t n) {
     void* p = nullptr;

@@ -13,6 +13,7 @@ namespace dashgpu {
 namespace dev {
 
 void set_device(int device);
+int get_device();  // current device of the calling host thread (-1 = none)
 int backend();  // 1 = CUDA
 void* alloc(size_t bytes);
 void release(void* p);

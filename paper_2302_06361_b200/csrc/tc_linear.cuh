@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t rw = P.garbler ? L.R[(uint64_t)b * P.zstride + w] : 0u;
         const uint32_t mask = (4 * w + 4 > L.n) ? (0xffffffffu >> (8 * (4 * w + 4 - L.n))) : 0xffffffffu;
         uint32_t* orow = L.out + (uint64_t)bw * P.M + pos;
+        const uint32_t c31 = modp(0x7fffffffu, L.p, L.mag, L.sh) + 1u;  // == 2^31 mod p (up to one p)
         // dense rows: the 4 output words of a column chunk are adjacent
         const bool vec = P.P == 1 && (P.M & 3) == 0;
         for (uint32_t cc = 0; cc < BN / 16; ++cc) {
@@ -244,7 +245,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t o = 0;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const uint32_t s0 = modp(v[g * 4 + j], L.p, L.mag, L.sh);
+                    // the reference accumulates in u32 with wrap-around
+                    // (layer.cpp:116-118); the s32 MMA accumulator wraps the
+                    // same way, and the 31-bit-exact magic sees its low 31
+                    // bits plus bit 31's residue (2^31 mod p, in [1, p])
+                    const uint32_t s0 = modp(v[g * 4 + j] & 0x7fffffffu, L.p, L.mag, L.sh) + (v[g * 4 + j] >> 31) * c31;
                     const uint32_t t1 = s0 + z * ((zw >> (8 * j)) & 0xffu) + nb * ((rw >> (8 * j)) & 0xffu);
                     o |= modp(t1, L.p, L.mag, L.sh) << (8 * j);
                 }

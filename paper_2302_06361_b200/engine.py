@@ -105,6 +105,8 @@ def _declare(L):
     L.dashgpu_backend.restype = ctypes.c_int
     L.dashgpu_init.argtypes = [ctypes.c_int]
     L.dashgpu_set_stream.argtypes = [vp]
+    L.dashgpu_use.argtypes = [ctypes.c_int, vp]
+    L.dashgpu_network_release_gc.argtypes = [vp]
     L.dashgpu_circuit_create.argtypes = [vp, ctypes.POINTER(vp)]
     L.dashgpu_circuit_destroy.argtypes = [vp]
     L.dashgpu_circuit_info_get.argtypes = [vp, ctypes.POINTER(CircuitInfo)]
@@ -173,7 +175,12 @@ class Dash:
             raise _CODES.get(rc, Error)(self.lib.dashgpu_last_error().decode())
 
     def set_stream(self, stream_ptr: int):
+        """Stream of the calling host thread (thread-local in the library)."""
         self.lib.dashgpu_set_stream(vp(stream_ptr))
+
+    def use(self, device: int, stream_ptr: int = 0):
+        """Per-call device and stream for the calling host thread (dashgpu_use)."""
+        self._check(self.lib.dashgpu_use(device, vp(stream_ptr)))
 
     # ---- circuits ----
     def circuit(self, c: Circuit) -> "GpuCircuit":
@@ -441,6 +448,11 @@ class GarbledNetwork:
 
     def export_decoding(self, b: int = 0) -> bytes:
         return self._export(self.eng.lib.dashgpu_export_decoding, b)
+
+    def release_gc(self):
+        """Garbler side after export_gc: free ciphertexts / slots / layer planes
+        (dashgpu_network_release_gc); garble_inputs and decode_outputs still work."""
+        self.eng._check(self.eng.lib.dashgpu_network_release_gc(self.h))
 
     def tamper(self, b: int, index: int, mask: bytes):
         self.eng._check(self.eng.lib.dashgpu_tamper_ct(self.h, b, index, (ctypes.c_uint8 * 16)(*mask)))

@@ -25,6 +25,7 @@ from __future__ import annotations
 import os
 import struct
 import threading
+import time
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import Dict, List, Optional, Sequence
@@ -347,6 +348,7 @@ class GarblerService:
                     s = self._sessions.get(f.session)
                     if s:
                         s.phase, s.error, s.error_code = "failed", msg, code
+                        s.net = None
                 return []
             raise ProtocolError("unexpected frame type for garbler")
         except Error as e:
@@ -362,6 +364,9 @@ class GarblerService:
         seed = self.cfg.seed if self.cfg.seed is not None else os.urandom(16)
         net = self.eng.garble(self.eng.circuit(circuit), seed)
         gc = net.export_gc(0)
+        # the GC has left: keep only encoding + decoding material in HBM, as the
+        # reference garbler keeps only EncodingInfo / DecodingInfo (protocol.cpp:211-226)
+        net.release_gc()
         with self._mu:
             if f.session in self._sessions:
                 raise ProtocolError("session already exists")
@@ -407,6 +412,11 @@ class GarblerService:
                 s.phase = "done"
             except Error as e:
                 s.phase, s.error, s.error_code = "failed", str(e), _code_for(e)
+            finally:
+                # single use: the session's device memory goes as soon as the
+                # outcome is known; only the host-side result / error stays
+                if s.phase in ("done", "failed"):
+                    s.net = None
 
     def _on_result_request(self, f: Frame) -> Outbound:
         if f.payload:
@@ -437,6 +447,9 @@ class _EvalGroup:
     sessions: List[int]
     inputs: Dict[int, bytes] = field(default_factory=dict)  # member index -> payload
     failed: set = field(default_factory=set)                # members answered with an error
+    want: int = 0                                           # GARBLED_INPUT payload bytes per member
+    deadline: float = float("inf")                          # time.monotonic() after which flush_expired runs it
+    done: bool = False
 
 
 @dataclass
@@ -450,10 +463,16 @@ class _EvaluatorSession:
 
 class EvaluatorService:
     """The untrusted inference device (protocol.cpp:303-350): holds gNN in
-    HBM only; each garbled circuit is single-use."""
+    HBM only; each garbled circuit is single-use.
 
-    def __init__(self, eng: Dash):
+    batch_timeout: seconds a batched group (handle_batch) waits for its
+    members' GARBLED_INPUT frames; flush_expired() then evaluates the group
+    with placeholder inputs for the missing members and answers those with
+    ERROR frames, so one stalled client cannot starve the others."""
+
+    def __init__(self, eng: Dash, batch_timeout: float = 30.0):
         self.eng = eng
+        self.batch_timeout = batch_timeout
         self._mu = threading.Lock()
         self._sessions: Dict[int, _EvaluatorSession] = {}
         self._ready: List[Frame] = []  # replies of batched sessions not yet handed out
@@ -464,7 +483,7 @@ class EvaluatorService:
         if s is not None and s.group is not None:  # member of a batched network
             replies = self.handle_batch([f])
             mine = [r for r in replies if r.session == f.session]
-            with self._mu:
+            with self._mu:  # the other members' replies: take_ready() / handle_all()
                 self._ready.extend(r for r in replies if r.session != f.session)
             return mine[0] if mine else None
         try:
@@ -485,12 +504,40 @@ class EvaluatorService:
                     if s.used:
                         raise ProtocolError("garbled circuit already used (single-use)")
                     s.used = True
-                gin = self.eng.import_bundle(s.net, f.payload, False)
-                gout = self.eng.evaluate(s.net, gin)
-                return Frame(FrameType.GARBLED_OUTPUT, f.session, gout.payload(0))
+                try:
+                    gin = self.eng.import_bundle(s.net, f.payload, False)
+                    gout = self.eng.evaluate(s.net, gin)
+                    return Frame(FrameType.GARBLED_OUTPUT, f.session, gout.payload(0))
+                finally:
+                    s.net = None  # single use: free the GC's HBM now
             raise ProtocolError("unexpected frame type for evaluator")
         except Error as e:
             return _error_frame(f.session, e)
+
+    def handle_all(self, f: Frame) -> List[Frame]:
+        """handle() plus every reply that became ready because of f (other
+        members of a batched group), none parked."""
+        r = self.handle(f)
+        return ([r] if r is not None else []) + self.take_ready()
+
+    def take_ready(self) -> List[Frame]:
+        """Replies of batched sessions completed by earlier frames."""
+        with self._mu:
+            out, self._ready = self._ready, []
+        return out
+
+    def flush_expired(self, now: Optional[float] = None) -> List[Frame]:
+        """Evaluate every batched group whose deadline passed: present members
+        get their GARBLED_OUTPUT, missing ones an ERROR frame (their circuits
+        are consumed: single use)."""
+        now = time.monotonic() if now is None else now
+        with self._mu:
+            groups = {id(s.group): s.group for s in self._sessions.values()
+                      if s.group is not None and not s.group.done and s.group.deadline <= now}
+        replies: List[Frame] = []
+        for grp in groups.values():
+            replies += self._run_group(grp, expired=True)
+        return replies + self.take_ready()
 
     def session_memory(self, session: int) -> int:
         with self._mu:
@@ -547,7 +594,8 @@ class EvaluatorService:
             return replies + [r for r in (self.handle(f) for f in fresh) if r is not None]
         info = net.circuit.info
         mem = info.cts * 16 + info.k * 16 + 16 * info.k * info.n_in
-        grp = _EvalGroup(net, [f.session for f in fresh])
+        grp = _EvalGroup(net, [f.session for f in fresh], want=16 * info.k * info.n_in,
+                         deadline=time.monotonic() + self.batch_timeout)
         with self._mu:
             for i, f in enumerate(fresh):
                 self._sessions[f.session] = _EvaluatorSession(net, mem, group=grp, index=i)
@@ -555,8 +603,7 @@ class EvaluatorService:
 
     def _group_input(self, f: Frame, s: _EvaluatorSession) -> List[Frame]:
         grp = s.group
-        info = grp.net.circuit.info
-        want = 16 * info.k * info.n_in
+        want = grp.want
         with self._mu:
             if s.used:
                 return [_error_frame(f.session, ProtocolError("garbled circuit already used (single-use)"))]
@@ -570,13 +617,38 @@ class EvaluatorService:
                 out = []
             if len(grp.inputs) < len(grp.sessions):
                 return out
+        return out + self._run_group(grp, expired=False)
+
+    def _run_group(self, grp: _EvalGroup, expired: bool) -> List[Frame]:
+        want = grp.want
+        out: List[Frame] = []
+        with self._mu:
+            if grp.done:
+                return []
+            grp.done = True
+            for i, sid in enumerate(grp.sessions):
+                if i not in grp.inputs:  # expired: placeholder input, member consumed
+                    grp.inputs[i] = bytes(want)
+                    grp.failed.add(i)
+                    s = self._sessions.get(sid)
+                    if s is not None:
+                        s.used = True
+                    out.append(_error_frame(sid, ProtocolError("garbled input not received before the batch deadline")))
             payload = b"".join(grp.inputs[i] for i in range(len(grp.sessions)))
         try:
             gout = self.eng.evaluate(grp.net, self.eng.import_bundle(grp.net, payload, False))
+            out += [Frame(FrameType.GARBLED_OUTPUT, sid, gout.payload(i))
+                    for i, sid in enumerate(grp.sessions) if i not in grp.failed]
         except Error as e:
-            return out + [_error_frame(sid, e) for i, sid in enumerate(grp.sessions) if i not in grp.failed]
-        return out + [Frame(FrameType.GARBLED_OUTPUT, sid, gout.payload(i))
-                      for i, sid in enumerate(grp.sessions) if i not in grp.failed]
+            out += [_error_frame(sid, e) for i, sid in enumerate(grp.sessions) if i not in grp.failed]
+        finally:
+            with self._mu:  # every member is single-use: the group's GCs leave HBM
+                grp.net = None
+                for sid in grp.sessions:
+                    s = self._sessions.get(sid)
+                    if s is not None:
+                        s.net = None
+        return out
 
 
 # ---------------------------------------------------------------- loopback

@@ -368,3 +368,67 @@ def test_batched_gc_transfer_of_mixed_circuits_falls_back(eng, oracle):
     gb = oracle.garble_inputs(nb, np.arange(16) - 8)
     r = ev.handle(P.Frame(T.GARBLED_INPUT, 2, gb.payload()))
     assert r.type == T.GARBLED_OUTPUT and r.payload == oracle.evaluate(nb, gb).payload()
+
+
+def test_batched_group_deadline_flushes_a_stalled_member(eng, oracle):
+    """a member whose GARBLED_INPUT never arrives must not starve
+    the group: after the deadline the present members get their outputs and
+    the missing one an ERROR frame (its circuit is consumed)."""
+    c = tiny()
+    nets, gins = _oracle_sessions(oracle, c, 3, "b4")
+    ev = P.EvaluatorService(eng, batch_timeout=5.0)
+    T = P.FrameType
+    ev.handle_batch([P.Frame(T.GC_TRANSFER, 300 + i, o.gc_bytes()) for i, o in enumerate(nets)])
+    assert ev.handle_all(P.Frame(T.GARBLED_INPUT, 300, gins[0].payload())) == []
+    assert ev.handle_all(P.Frame(T.GARBLED_INPUT, 302, gins[2].payload())) == []
+    import time
+    assert ev.flush_expired(time.monotonic()) == []  # not expired yet
+    out = ev.flush_expired(time.monotonic() + 10.0)
+    got = {f.session: f for f in out}
+    assert sorted(got) == [300, 301, 302]
+    assert got[301].type == T.ERROR and P.decode_error(got[301].payload)[0] == P.ErrorCode.PROTOCOL
+    for i in (0, 2):
+        assert got[300 + i].type == T.GARBLED_OUTPUT
+        assert got[300 + i].payload == oracle.evaluate(nets[i], gins[i]).payload()
+    late = ev.handle(P.Frame(T.GARBLED_INPUT, 301, gins[1].payload()))
+    assert late.type == T.ERROR  # single use
+    assert ev.flush_expired(time.monotonic() + 20.0) == []
+
+
+def test_handle_all_returns_every_completed_reply(eng, oracle):
+    c = tiny()
+    nets, gins = _oracle_sessions(oracle, c, 2, "b5")
+    ev = P.EvaluatorService(eng)
+    T = P.FrameType
+    ev.handle_batch([P.Frame(T.GC_TRANSFER, 400 + i, o.gc_bytes()) for i, o in enumerate(nets)])
+    assert ev.handle_all(P.Frame(T.GARBLED_INPUT, 400, gins[0].payload())) == []
+    out = ev.handle_all(P.Frame(T.GARBLED_INPUT, 401, gins[1].payload()))
+    assert sorted(f.session for f in out) == [400, 401]
+    assert ev.take_ready() == []
+
+
+def test_garbler_releases_the_gc_after_transfer(eng, oracle):
+    """the garbler keeps only encoding / decoding material once the
+    GC has been sent (dashgpu_network_release_gc); the session still encodes
+    inputs and decodes the result, and its device network is dropped once
+    the result is known."""
+    c = tiny()
+    g = P.GarblerService(eng, P.GarblerConfig(seed=seed_hex(0x77)))
+    T = P.FrameType
+    out = g.handle(P.Frame(T.MODEL_UPLOAD, 9, P.encode_model_upload(c, 1)))
+    gc = out[0].frame.payload
+    net = g._sessions[9].net
+    with pytest.raises(P.DataError):
+        net.export_gc(0)
+    x = np.random.default_rng(5).integers(-7, 8, size=c.n_in)
+    gin = g.handle(P.Frame(T.INPUT_UPLOAD, 9, P.encode_input_upload(0, 0, x)))[0].frame.payload
+    on = oracle.garble(c, seed_hex(0x77))
+    assert gc == on.gc_bytes()
+    og = oracle.garble_inputs(on, x)
+    assert gin == og.payload()
+    gout = oracle.evaluate(on, og).payload()
+    assert g.handle(P.Frame(T.GARBLED_OUTPUT, 9, gout)) == []
+    assert g._sessions[9].net is None
+    res = g.handle(P.Frame(T.RESULT, 9, b""))[0].frame
+    assert res.type == T.RESULT
+    assert (P.decode_result(res.payload) == oracle.decode(on, oracle.evaluate(on, og))).all()
