@@ -51,7 +51,8 @@ def parse():
                                                            "the JSON model default, model_io.cpp:56)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="inferences in the CPU-baseline sample")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (config sweeps)")
-    ap.add_argument("--sweep", default="", help="label-ops sweep (BASELINE configs[4]): 'proj' and/or 'linear', "
+    ap.add_argument("--sweep", default="", help="label-ops sweep (BASELINE configs[4]): 'proj' (ReLU layer), "
+                                                "'tproj' (raw projection gates) and/or 'linear' (Dense 1024^2), "
                                                 "comma separated; --sweep-log2 / --sweep-k select the grid")
     ap.add_argument("--sweep-log2", default="16,18,20,22,24,26")
     ap.add_argument("--sweep-k", default="2,4,6,8")
@@ -305,6 +306,21 @@ def run_sweep(args):
     eng = Dash(local)
     eng.set_stream(torch.cuda.current_stream().cuda_stream)
     kinds = [s for s in args.sweep.split(",") if s]
+    PR = [2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53]
+
+    def timed(fn):
+        """fn() between CUDA events on the library's stream (torch's current
+        stream), max over ranks; returns (device seconds, wall seconds)."""
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        r = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        return max_over_ranks(e0.elapsed_time(e1) / 1e3), max_over_ranks(wall), r
+
     for kind in kinds:
         for j in [int(v) for v in args.sweep_log2.split(",")]:
             for k in [int(v) for v in args.sweep_k.split(",")]:
@@ -313,25 +329,77 @@ def run_sweep(args):
                     g = eng.model(f"relu{N}", 0, k)
                     info = g.info
                     P = 1
-                    for p in [2, 3, 5, 7, 11, 13, 17, 19][:k]:
+                    for p in PR[:k]:
                         P *= p
                     x = np.random.default_rng(j * 16 + k).integers(-(P // 2), (P + 1) // 2, size=(1, N))
-                    chunk = max(1 << 14, int(24e9 // (16 * info.act_uc_cts)))
-                    gw = eng.model("relu16384", 0, k)  # warm-up: same kernels, small layer
-                    eng.infer_stream(gw, (0x5EED).to_bytes(16, "big"), x[:, :16384] if N >= 16384 else
-                                     np.zeros((1, 16384), np.int64), 1 << 14)
+                    chunk = min(N, max(1 << 14, int(24e9 // (16 * info.act_uc_cts))))
                     a, b = shard_range(N, world, rank)
-                    barrier()
-                    t0 = time.perf_counter()
-                    out, tm, _ = eng.infer_stream(g, (0x5EED0001).to_bytes(16, "big"), x, chunk, u_range=(a, b))
-                    sec = max_over_ranks(time.perf_counter() - t0)
+                    chunk = min(chunk, max(1, b - a))
+                    # warm-up on the same circuit at the timed chunk size: the
+                    # stream workspace is allocated here and reused by the timed call
+                    eng.infer_stream(g, (0x5EED).to_bytes(16, "big"), x, chunk, u_range=(a, a + chunk))
+                    sec, wall, (out, tm, _) = timed(lambda: eng.infer_stream(
+                        g, (0x5EED0001).to_bytes(16, "big"), x, chunk, u_range=(a, b)))
                     assert (out[0, a:b] == np.maximum(x[0, a:b], 0)).all(), "ReLU sweep mismatch"
                     rows = N * (info.act_uc_cts + info.act_eval_rows)
                     line = {"sweep": "proj", "labels": N, "k": k, "n_gpus": world, "label_ops_per_s": rows / sec,
-                            "elements_per_s": N / sec, "seconds": sec, "garbled_rows": N * info.act_uc_cts,
-                            "eval_rows": N * info.act_eval_rows, "table_bytes": 16 * N * info.act_uc_cts,
+                            "elements_per_s": N / sec, "seconds": sec, "wall_seconds": wall,
+                            "garbled_rows": N * info.act_uc_cts, "eval_rows": N * info.act_eval_rows,
+                            "table_bytes": 16 * N * info.act_uc_cts,
                             "table_GBps": 16 * N * info.act_uc_cts / sec / 1e9, "chunk_elements": chunk,
-                            "chunks": tm.sub_batches, "ms_garble": tm.ms_garble, "ms_evaluate": tm.ms_evaluate}
+                            "chunks": tm.sub_batches, "check": "decoded == ReLU(x) for every element",
+                            "workload": "{input_shape={N}, layers={relu()}} (bench_main.cpp:156-162), garble + "
+                                        "garble_inputs + evaluate + decode, streamed in element chunks"}
+                elif kind == "tproj":
+                    # raw t_proj (bench_main.cpp:40-74, phi(a) = a^2 + 1 mod p): N gates per CRT lane,
+                    # garbled (p rows each) then evaluated (one row each), device-resident
+                    a, b = shard_range(N, world, rank)
+                    n = max(1, b - a)
+                    pmax = max(PR[:k])
+                    gen = torch.Generator(device="cuda").manual_seed(j * 16 + k)
+                    lab = torch.randint(-2**62, 2**62, (n, 2), dtype=torch.int64, device="cuda", generator=gen)
+                    gates = torch.arange(a, a + n, dtype=torch.int64, device="cuda")
+                    wires = gates + N
+                    rows = torch.empty((n * pmax, 2), dtype=torch.int64, device="cuda")
+                    out0 = torch.empty((n, 2), dtype=torch.int64, device="cuda")
+                    outv = torch.empty((n, 2), dtype=torch.int64, device="cuda")
+                    seed = (0x7B0 + k).to_bytes(16, "big")
+                    ctxs = [eng.proj_ctx(seed, p, p, [(v * v + 1) % p for v in range(p)]) for p in PR[:k]]
+                    for c in ctxs:  # warm-up
+                        c.garble(min(n, 4096), lab.data_ptr(), gates.data_ptr(), wires.data_ptr(),
+                                 rows.data_ptr(), out0.data_ptr())
+                    tg = te = 0.0
+                    for c in ctxs:
+                        dg, _, _ = timed(lambda: c.garble(n, lab.data_ptr(), gates.data_ptr(), wires.data_ptr(),
+                                                          rows.data_ptr(), out0.data_ptr()))
+                        # evaluate on the base labels (= the active labels of value 0: colour-random rows)
+                        de, _, _ = timed(lambda: c.eval(n, lab.data_ptr(), gates.data_ptr(), rows.data_ptr(),
+                                                        outv.data_ptr()))
+                        tg, te = tg + dg, te + de
+                        # property check on a sample: eval(x0) == out0 + phi(0) R_q = out0 + R_q
+                        p = c.p
+                        smp = np.random.default_rng(p).integers(0, n, size=64)
+                        _, _, (_, Rq) = eng.proj_garble(seed, p, p, [(v * v + 1) % p for v in range(p)], [0], [0], [0])
+                        o0 = out0.cpu().numpy().view(np.uint64)
+                        ov = outv.cpu().numpy().view(np.uint64)
+                        for i in smp.tolist():
+                            want = label_add(int(o0[i, 0]) | (int(o0[i, 1]) << 64), Rq, p)
+                            assert (int(ov[i, 0]) | (int(ov[i, 1]) << 64)) == want, ("t_proj sweep mismatch", p, i)
+                    Ng = N * world if world > 1 else N
+                    grows = sum(Ng * p for p in PR[:k])
+                    erows = Ng * k
+                    gbytes = sum(Ng * (16 * p + 16 + 16 + 16) for p in PR[:k])  # rows + in + out0 + ids
+                    ebytes = Ng * k * (16 + 16 + 16 + 8)                       # row + in + out + id
+                    line = {"sweep": "tproj", "labels": N, "k": k, "n_gpus": world,
+                            "label_ops_per_s": (grows + erows) / (tg + te), "seconds": tg + te,
+                            "garble_rows_per_s": grows / tg, "eval_rows_per_s": erows / te,
+                            "garble_s": tg, "eval_s": te, "garble_GBps": gbytes / tg / 1e9,
+                            "eval_GBps": ebytes / te / 1e9,
+                            "check": "eval(base label) == out0 + R_q on 64 sampled gates per lane",
+                            "workload": "N independent t_proj gates per CRT lane p_i -> p_i, phi(a) = a^2+1 mod p "
+                                        "(bench_main.cpp:40-74), device-resident inputs"}
+                    del rows, out0, outv, lab
+                    torch.cuda.empty_cache()
                 else:
                     g = eng.model("dense1024", 0, k)
                     info = g.info
@@ -340,16 +408,13 @@ def run_sweep(args):
                     B = max(1, b - a)
                     seeds = b"".join(int(0x5EED0000 + a + i).to_bytes(16, "big") for i in range(B))
                     P = 1
-                    for p in [2, 3, 5, 7, 11, 13, 17, 19][:k]:
+                    for p in PR[:k]:
                         P *= p
                     lim = min(7, P // 2 - 1)  # encodable inputs (outputs may wrap mod P: throughput only)
                     x = np.random.default_rng(k).integers(-lim, lim + 1, size=(B, 1024))
-                    eng.infer(g, seeds[:16 * min(B, 4)], x[: min(B, 4)])
+                    eng.infer(g, seeds, x)  # warm-up at the timed batch: workspace allocated once
                     eng.profile(True)
-                    barrier()
-                    t0 = time.perf_counter()
-                    eng.infer(g, seeds, x)
-                    sec = max_over_ranks(time.perf_counter() - t0)
+                    sec, wall, _ = timed(lambda: eng.infer(g, seeds, x))
                     prof = eng.profile_read()
                     eng.profile(False)
                     lin_ms = max_over_ranks(prof.get("linear", (0.0, 0))[0])
@@ -358,6 +423,7 @@ def run_sweep(args):
                     line = {"sweep": "linear", "labels": B * 1024, "k": k, "n_gpus": world, "inferences": B,
                             "label_macs_per_s_kernel": label_macs / (lin_ms / 1e3) if lin_ms else None,
                             "digit_macs_per_s_kernel": 2 * B * info.linear_macs / (lin_ms / 1e3) if lin_ms else None,
+                            "int8_ops_per_s_kernel": 4 * B * info.linear_macs / (lin_ms / 1e3) if lin_ms else None,
                             "linear_kernel_ms": lin_ms, "end_to_end_s": sec,
                             "label_macs_per_s_e2e": label_macs / sec}
                 if rank == 0:
@@ -368,6 +434,28 @@ def run_sweep(args):
 
 
 SUM_N = [128, 80, 55, 45, 37, 34, 31, 30, 28, 26, 25, 24, 23, 23, 23, 22]  # digits per label, primes 2..53
+
+
+def _ndig(m):
+    """n_digits (label.cpp:15-64): the most base-m digits whose range fits 128 bits."""
+    n, v = 0, 1
+    while v * m <= 1 << 128:
+        v *= m
+        n += 1
+    return n
+
+
+def label_add(a: int, b: int, m: int) -> int:
+    """compress(decompress_mod(a) + decompress_mod(b)) mod m, digit-wise
+    (label.cpp:83-219), for the sweep's sampled property check."""
+    n = _ndig(m)
+    mod = m ** n
+    a, b = a % mod if mod < 1 << 128 else a, b % mod if mod < 1 << 128 else b
+    out, pw = 0, 1
+    for _ in range(n):
+        out += ((a % m + b % m) % m) * pw
+        a, b, pw = a // m, b // m, pw * m
+    return out
 
 
 def measured_peaks():

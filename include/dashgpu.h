@@ -161,6 +161,19 @@ int dashgpu_proj_garble(const uint8_t* seed16, uint32_t n, int p, int q, const u
                         uint64_t* rows, uint64_t* out0, uint64_t* offsets);
 int dashgpu_proj_eval(uint32_t n, int p, int q, const uint64_t* in, const uint64_t* gates,
                       const uint64_t* rows, uint64_t* out);
+/* Device-resident form for throughput (the raw t_proj sweep of SURVEY 8(d)
+ * (ii); the reference times one gate at a time, bench_main.cpp:40-74):
+ * a context holds the PRF key schedule, R_p / R_q multiples and phi; every
+ * buffer is a DEVICE pointer with the layouts above (in / out0 / out: n x
+ * 16 B, gates / wires: n x u64, rows: n x p x 16 B); calls are enqueued on
+ * the calling thread's stream without a host sync. */
+typedef struct dashgpu_proj_ctx dashgpu_proj_ctx;
+int dashgpu_proj_ctx_create(const uint8_t* seed16, int p, int q, const uint8_t* phi, dashgpu_proj_ctx** out);
+void dashgpu_proj_ctx_destroy(dashgpu_proj_ctx* c);
+int dashgpu_proj_garble_dev(const dashgpu_proj_ctx* c, uint32_t n, const void* in, const void* gates,
+                            const void* wires, void* rows, void* out0);
+int dashgpu_proj_eval_dev(const dashgpu_proj_ctx* c, uint32_t n, const void* in, const void* gates,
+                          const void* rows, void* out);
 
 /* ---- LabelTensor images (label_tensor.hpp:14-42: per lane, label-major
  * u16 digits [batch][elements][n_p]) <-> device bundles (u8 SoA planes) ---- */

@@ -1010,6 +1010,7 @@ struct HLayer {
 };
 
 struct Network;
+struct StreamWS;
 
 }  // namespace dashgpu
 
@@ -1034,6 +1035,7 @@ struct dashgpu_circuit {
         std::mutex mu;
     };
     std::map<void*, std::unique_ptr<Workspace>> workspaces;
+    std::map<void*, std::shared_ptr<dashgpu::StreamWS>> stream_ws;  // dashgpu_infer_stream, per stream
     bool uploaded = false;  // per-layer device buffers created (upload_circuit)
     int device = -1;        // device the per-layer buffers live on
     // evaluator copy parsed from a GC (dashgpu_import_gc): private weights
@@ -1861,11 +1863,75 @@ static uint64_t act_row_pos(uint64_t E, uint64_t uc, uint64_t u, uint64_t j) {
 struct StreamWS {
     DevBuf rk, seeds, mult, zero, Rb, commit, blob, slots, dec, vals, resid, err, actp, qctr, qflags, mmlab, outv;
     Lanes base, in, gout, eout;
-    uint64_t C = 0;
+    uint64_t C = 0;  // chunk capacity (elements) the buffers are sized for
+    // host staging, double-buffered: chunk i's inputs / decoded outputs go
+    // through slot i & 1; the host touches a slot only after the event of
+    // the chunk that used it two chunks earlier (no per-chunk stream sync)
+    HostBuf in_pin[2], out_pin[2], act_pin, par_pin;
+    void* ev[2] = {nullptr, nullptr};
+    int64_t* pend_dst[2] = {nullptr, nullptr};
+    uint32_t pend_n[2] = {0, 0};
+    ~StreamWS() {
+        for (void* e : ev) dev::event_destroy(e);
+    }
 };
 
 static bool streamable(const dashgpu_circuit& c) {
     return c.layers.size() == 1 && c.layers[0].tape != nullptr;
+}
+
+// Workspace of (circuit, stream), sized once for chunks of C elements and
+// reused by every later call (the sweep's timed calls allocate nothing).
+static StreamWS& stream_ws(dashgpu_circuit& c, uint64_t C) {
+    auto& slot = c.stream_ws[g_stream];
+    if (slot && slot->C >= C) return *slot;
+    slot.reset();  // free the smaller workspace before allocating the larger one
+    auto w = std::make_shared<StreamWS>();
+    const int k = c.k;
+    const Tape& T = *c.layers[0].tape;
+    const uint64_t mult_stride = (uint64_t)(MAXMOD - 1) * 128 * NWMAX;
+    uint32_t sum_p = 0;
+    for (int p : c.base.primes) sum_p += (uint32_t)p;
+    w->C = C;
+    w->rk.ensure(44 * 4);
+    w->seeds.ensure(16);
+    w->mult.ensure(mult_stride * 4);
+    w->zero.ensure((size_t)k * LABW * 4);
+    w->Rb.ensure((size_t)k * LABW * 4);
+    w->commit.ensure(16);
+    w->blob.ensure((size_t)C * T.cts * 16);
+    w->slots.ensure(std::max<size_t>((size_t)std::max(T.nslots, T.nslots_lv) * C, 1) * 16);
+    w->dec.ensure((size_t)C * sum_p * 16);
+    w->vals.ensure((size_t)2 * C * 8);
+    w->resid.ensure((size_t)C * k);
+    w->outv.ensure((size_t)2 * C * 8);
+    w->err.ensure(16);
+    w->actp.ensure(2 * sizeof(ActParams));
+    w->mmlab.ensure((size_t)C * k * 2 * 16);
+    w->qctr.ensure(64);
+    w->qflags.ensure(((C + 31) / 32 + 1) * 4);
+    w->base.ensure(c.base, 1, C);
+    w->in.ensure(c.base, 1, C);
+    w->gout.ensure(c.base, 1, C);
+    w->eout.ensure(c.base, 1, C);
+    for (int i = 0; i < 2; ++i) {
+        w->in_pin[i].ensure((size_t)C * 8);
+        w->out_pin[i].ensure((size_t)C * 8);
+        w->ev[i] = dev::event_create();
+    }
+    w->act_pin.ensure(4 * sizeof(ActParams));
+    w->par_pin.ensure(64 + 44 * 4 + 16 + 8);
+    slot = w;
+    return *w;
+}
+
+// retire the chunk that last used staging slot s: its decoded outputs are
+// copied from pinned memory to the caller's buffer
+static void stream_retire(StreamWS& w, int s) {
+    if (!w.pend_dst[s]) return;
+    dev::event_sync(w.ev[s]);
+    std::memcpy(w.pend_dst[s], w.out_pin[s].p, (size_t)w.pend_n[s] * 8);
+    w.pend_dst[s] = nullptr;
 }
 
 static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batch, const int64_t* inputs,
@@ -1880,45 +1946,61 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
     u_end = std::min<uint64_t>(u_end, N);
     if (u_begin > u_end) throw DataError("element range out of order");
     const uint64_t C = std::max<uint64_t>(1, std::min<uint64_t>(chunk, std::max<uint64_t>(u_end - u_begin, 1)));
-    StreamWS w;
-    w.C = C;
+    StreamWS& w = stream_ws(c, C);
     const uint64_t mult_stride = (uint64_t)(MAXMOD - 1) * 128 * NWMAX;
-    uint32_t sum_p = 0;
-    for (int p : c.base.primes) sum_p += (uint32_t)p;
-    w.rk.ensure(44 * 4);
-    w.seeds.ensure(16);
-    w.mult.ensure(mult_stride * 4);
-    w.zero.ensure((size_t)k * LABW * 4);
-    w.Rb.ensure((size_t)k * LABW * 4);
-    w.commit.ensure(16);
-    w.blob.ensure((size_t)C * T.cts * 16);
-    w.slots.ensure(std::max<size_t>((size_t)std::max(T.nslots, T.nslots_lv) * C, 1) * 16);
-    w.dec.ensure((size_t)C * sum_p * 16);
-    w.vals.ensure((size_t)C * 8);
-    w.resid.ensure((size_t)C * k);
-    w.outv.ensure((size_t)C * 8);
-    w.err.ensure(16);
-    w.actp.ensure(sizeof(ActParams));
-    w.mmlab.ensure((size_t)C * k * 2 * 16);
-    w.qctr.ensure(64);
-    w.qflags.ensure(((C + 31) / 32 + 1) * 4);
     Sched q;
     q.counter = w.qctr.as<uint32_t>();
     q.flags = w.qflags.as<uint32_t>();
     q.flags_cap = w.qflags.n / 4;
-    w.base.ensure(c.base, 1, C);
-    w.in.ensure(c.base, 1, C);
-    w.gout.ensure(c.base, 1, C);
-    w.eout.ensure(c.base, 1, C);
+    uint16_t primes[MAXK];
+    fill_primes(c.base, primes);
+    // per-chunk launch parameters that do not depend on the chunk
+    ActParams P;
+    std::memset(&P, 0, sizeof P);
+    P.tape = l.tape_d->as<TapeOp>();
+    P.n_ops = (int)T.ops.size();
+    P.lv_tape = l.lv_tape_d->as<TapeOp>();
+    P.lv_start = l.lv_start_d->as<uint16_t>();
+    P.n_levels = (int)T.lv_start.size() - 1;
+    fill_chunks(P, T, tape_chunks());
+    P.phi = l.phi_d->as<uint8_t>();
+    P.k = k;
+    P.B = 1;
+    P.uc_cts = T.cts;
+    P.uc_gates = T.gates;
+    P.uc_wires = T.wires;
+    P.blob = w.blob.as<U4>();
+    for (int i = 0; i < k; ++i) {
+        P.out_kind[i] = T.out_kind[i];
+        P.out_wire[i] = T.out_wire[i];
+    }
+    P.rk = w.rk.as<uint32_t>();
+    P.mult = w.mult.as<uint32_t>();
+    P.mult_stride = mult_stride;
+    P.slots = w.slots.as<U4>();  // max(nslots, nslots_lv) per element
+    P.lv_ok = 1;
+    P.mmlab = w.mmlab.as<U4>();
+    ActParams* actp = w.actp.as<ActParams>();  // [0] garbling, [1] evaluation of the current chunk
+    // the sweep's error flags accumulate over the call (kernels only raise
+    // them): [0] encode range, [1] decode miss / range; checked once at the end
+    dev::memset0(w.err.p, 8, g_stream);
     using clk = std::chrono::steady_clock;
+    const auto t_start = clk::now();
+    uint64_t ci = 0;  // chunk counter (staging slot = ci & 1)
     for (uint32_t b = 0; b < batch; ++b) {
         uint32_t rk[44];
         aes_expand_host(seeds + 16 * (size_t)b, rk);
-        dev::h2d(w.rk.p, rk, sizeof rk, g_stream);
-        dev::h2d(w.seeds.p, seeds + 16 * (size_t)b, 16, g_stream);
-        for (uint64_t u0 = u_begin; u0 < u_end; u0 += C) {
+        // the previous inference's chunks may still read rk / seeds
+        for (int s = 0; s < 2; ++s) stream_retire(w, s);
+        dev::sync(g_stream);
+        std::memcpy(w.par_pin.p, rk, sizeof rk);
+        std::memcpy(w.par_pin.as<uint8_t>() + sizeof rk, seeds + 16 * (size_t)b, 16);
+        dev::h2d(w.rk.p, w.par_pin.p, sizeof rk, g_stream);
+        dev::h2d(w.seeds.p, w.par_pin.as<uint8_t>() + sizeof rk, 16, g_stream);
+        for (uint64_t u0 = u_begin; u0 < u_end; u0 += C, ++ci) {
+            const int s = (int)(ci & 1);
             const uint32_t n = (uint32_t)std::min<uint64_t>(C, u_end - u0);
-            const auto t0 = clk::now();
+            stream_retire(w, s);  // chunk ci - 2 is done: slot s is free
             // offsets, zero wires and this chunk's input base labels
             SetupParams S;
             std::memset(&S, 0, sizeof S);
@@ -1938,42 +2020,19 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             S.commit = w.commit.as<U4>();
             launch_setup(S, g_stream);
             // garble the chunk: outputs (PRF functions) first, then the tapes
-            ActParams P;
-            std::memset(&P, 0, sizeof P);
-            P.tape = l.tape_d->as<TapeOp>();
-            P.n_ops = (int)T.ops.size();
-            P.lv_tape = l.lv_tape_d->as<TapeOp>();
-            P.lv_start = l.lv_start_d->as<uint16_t>();
-            P.n_levels = (int)T.lv_start.size() - 1;
-            fill_chunks(P, T, tape_chunks());
-            P.phi = l.phi_d->as<uint8_t>();
-            P.k = k;
             P.E = n;
-            P.B = 1;
             P.gate_base = l.gate_base + u0 * T.gates;
             P.wire_base = l.wire_base + u0 * T.wires;
-            P.uc_cts = T.cts;
-            P.uc_gates = T.gates;
-            P.uc_wires = T.wires;
-            P.blob = w.blob.as<U4>();
             P.blob_stride = (uint64_t)n * T.cts;
             for (int i = 0; i < k; ++i) {
                 P.in[i] = w.base.lane[i]->as<uint32_t>();
                 P.out[i] = w.gout.lane[i]->as<uint32_t>();
-                P.out_kind[i] = T.out_kind[i];
-                P.out_wire[i] = T.out_wire[i];
             }
-            P.rk = w.rk.as<uint32_t>();
-            P.mult = w.mult.as<uint32_t>();
-            P.mult_stride = mult_stride;
-            P.slots = w.slots.as<U4>();  // max(nslots, nslots_lv) per element
-            P.lv_ok = 1;
-            P.mmlab = w.mmlab.as<U4>();
-            uint16_t primes[MAXK];
-            fill_primes(c.base, primes);
             launch_act_outputs(P, primes, g_stream);
-            dev::h2d(w.actp.p, &P, sizeof P, g_stream);
-            launch_act_multi(w.actp.as<ActParams>(), &P, 1, true, g_stream, q);
+            ActParams* pin = w.act_pin.as<ActParams>() + 2 * s;  // pinned launch parameters of slot s
+            pin[0] = P;
+            dev::h2d(actp, pin, sizeof P, g_stream);
+            launch_act_multi(actp, &P, 1, true, g_stream, q);
             DecodeParams D;
             std::memset(&D, 0, sizeof D);
             D.B = 1;
@@ -1986,7 +2045,7 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             D.mult = w.mult.as<uint32_t>();
             D.mult_stride = mult_stride;
             launch_dectable(D, g_stream);
-            if (gc_out) {  // chunk rows -> reference order (act_rows layout with E = n)
+            if (gc_out) {  // test path: chunk rows -> reference order (act_rows layout with E = n)
                 std::vector<U4> rows((size_t)n * T.cts);
                 dev::d2h(rows.data(), w.blob.p, rows.size() * 16, g_stream);
                 dev::sync(g_stream);
@@ -1994,18 +2053,17 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
                 for (uint64_t u = 0; u < n; ++u)
                     for (uint64_t j = 0; j < T.cts; ++j) dst[u * T.cts + j] = rows[act_row_pos(n, T.cts, u, j)];
             }
-            dev::sync(g_stream);
-            const auto t1 = clk::now();
-            // garble_inputs of the chunk (garble.cpp:242-263)
-            dev::h2d(w.vals.p, inputs + (uint64_t)b * N + u0, (size_t)n * 8, g_stream);
-            dev::memset0(w.err.p, 4, g_stream);
+            // garble_inputs of the chunk (garble.cpp:242-263), inputs staged in pinned slot s
+            std::memcpy(w.in_pin[s].p, inputs + (uint64_t)b * N + u0, (size_t)n * 8);
+            int64_t* vals = w.vals.as<int64_t>() + (size_t)s * C;
+            dev::h2d(vals, w.in_pin[s].p, (size_t)n * 8, g_stream);
             EncodeParams E;
             std::memset(&E, 0, sizeof E);
             E.B = 1;
             E.n_in = n;
             E.k = k;
             fill_primes(c.base, E.primes);
-            E.values = w.vals.as<int64_t>();
+            E.values = vals;
             for (int i = 0; i < k; ++i) {
                 E.base[i] = w.base.lane[i]->as<uint32_t>();
                 E.out[i] = w.in.lane[i]->as<uint32_t>();
@@ -2019,42 +2077,38 @@ static void infer_stream(dashgpu_circuit& c, const uint8_t* seeds, uint32_t batc
             E.half_dn_hi = (uint64_t)(half_dn >> 64);
             E.err = w.err.as<int>();
             launch_encode(E, g_stream);
-            int err_enc = 0;
-            dev::d2h(&err_enc, w.err.p, 4, g_stream);
-            const auto t2 = clk::now();
             // evaluate the chunk on the active labels
+            ActParams Pe = P;
             for (int i = 0; i < k; ++i) {
-                P.in[i] = w.in.lane[i]->as<uint32_t>();
-                P.out[i] = w.eout.lane[i]->as<uint32_t>();
+                Pe.in[i] = w.in.lane[i]->as<uint32_t>();
+                Pe.out[i] = w.eout.lane[i]->as<uint32_t>();
             }
-            dev::h2d(w.actp.p, &P, sizeof P, g_stream);
-            launch_act_multi(w.actp.as<ActParams>(), &P, 1, false, g_stream, q);
-            dev::sync(g_stream);
-            const auto t3 = clk::now();
-            // decode_outputs of the chunk
+            pin[1] = Pe;
+            dev::h2d(actp + 1, pin + 1, sizeof Pe, g_stream);
+            launch_act_multi(actp + 1, &Pe, 1, false, g_stream, q);
+            // decode_outputs of the chunk into staging slot s
             make_lane_ptrs(w.eout, k, D.lanes);
             D.residues = w.resid.as<uint8_t>();
-            D.err = w.err.as<int>();
-            D.values = w.outv.as<int64_t>();
+            D.err = w.err.as<int>() + 1;
+            D.values = w.outv.as<int64_t>() + (size_t)s * C;
             fill_crt(c.base, D);
-            dev::sync(g_stream);
-            if (err_enc) throw DataError("encode_signed: value outside the representable range");
-            dev::memset0(w.err.p, 4, g_stream);
             launch_decode(D, g_stream);
-            int err = 0;
-            dev::d2h(outputs + (uint64_t)b * N + u0, w.outv.p, (size_t)n * 8, g_stream);
-            dev::d2h(&err, w.err.p, 4, g_stream);
-            dev::sync(g_stream);
-            if (err == ST_AUTH) throw AuthError("output label not present in the decoding table");
-            if (err) throw DataError("decode_signed: value exceeds 64-bit signed range");
-            const auto t4 = clk::now();
-            tm.ms_garble += std::chrono::duration<double, std::milli>(t1 - t0).count();
-            tm.ms_encode += std::chrono::duration<double, std::milli>(t2 - t1).count();
-            tm.ms_evaluate += std::chrono::duration<double, std::milli>(t3 - t2).count();
-            tm.ms_decode += std::chrono::duration<double, std::milli>(t4 - t3).count();
+            dev::d2h(w.out_pin[s].p, D.values, (size_t)n * 8, g_stream);
+            dev::event_record(w.ev[s], g_stream);
+            w.pend_dst[s] = outputs + (uint64_t)b * N + u0;
+            w.pend_n[s] = n;
             tm.sub_batches += 1;
         }
     }
+    int err[2] = {0, 0};
+    dev::d2h(err, w.err.p, 8, g_stream);
+    for (int s = 0; s < 2; ++s) stream_retire(w, s);
+    dev::sync(g_stream);
+    if (err[0]) throw DataError("encode_signed: value outside the representable range");
+    if (err[1] == ST_AUTH) throw AuthError("output label not present in the decoding table");
+    if (err[1]) throw DataError("decode_signed: value exceeds 64-bit signed range");
+    // one pipelined pass: the phases overlap, so the whole call is reported
+    tm.ms_garble = std::chrono::duration<double, std::milli>(clk::now() - t_start).count();
     tm.h2d_bytes = (uint64_t)batch * ((u_end - u_begin) * 8 + 16 + 44 * 4);
     tm.d2h_bytes = (uint64_t)batch * (u_end - u_begin) * 8;
 }
@@ -3440,6 +3494,74 @@ int dashgpu_proj_garble(const uint8_t* seed16, uint32_t n, int p, int q, const u
             offsets[2] = (uint64_t)rq;
             offsets[3] = (uint64_t)(rq >> 64);
         }
+    });
+}
+
+// Device-resident t_proj over n gates (the raw projection sweep, SURVEY
+// 8(d) (ii); bench_main.cpp:40-74 times one gate at a time on the CPU): the
+// context holds the PRF key schedule and the multiples tables of R_p / R_q,
+// every buffer argument is a device pointer, work is enqueued on the calling
+// thread's stream without a host sync.
+struct dashgpu_proj_ctx {
+    int p = 0, q = 0;
+    dashgpu::DevBuf rk, mult, scratch, phi;
+};
+
+int dashgpu_proj_ctx_create(const uint8_t* seed16, int p, int q, const uint8_t* phi, dashgpu_proj_ctx** out) {
+    return guarded([&] {
+        check_constants();
+        if (!seed16 || !phi || !out) throw DataError("null argument");
+        if (p < 2 || p > MAXMOD || q < 2 || q > MAXMOD) throw DataError("modulus out of range");
+        for (int a = 0; a < p; ++a)
+            if (phi[a] >= q) throw DataError("projection table value out of range");
+        auto c = std::make_unique<dashgpu_proj_ctx>();
+        c->p = p;
+        c->q = q;
+        proj_setup(seed16, p, q, c->rk, c->mult, c->scratch);
+        c->phi.ensure(p);
+        dev::h2d(c->phi.p, phi, p, g_stream);
+        dev::sync(g_stream);
+        *out = c.release();
+    });
+}
+
+void dashgpu_proj_ctx_destroy(dashgpu_proj_ctx* c) { delete c; }
+
+static ProjParams proj_params(const dashgpu_proj_ctx* c, uint32_t n, const void* in, const void* gates, void* rows,
+                              void* out) {
+    if (!c) throw DataError("null projection context");
+    if (n && (!in || !gates || !rows || !out)) throw DataError("null device buffer");
+    ProjParams P;
+    std::memset(&P, 0, sizeof P);
+    P.n = n;
+    P.p = (uint32_t)c->p;
+    P.q = (uint32_t)c->q;
+    P.phi = c->phi.as<uint8_t>();
+    P.in = static_cast<const U4*>(in);
+    P.gates = static_cast<const uint64_t*>(gates);
+    P.rows = static_cast<U4*>(rows);
+    P.out = static_cast<U4*>(out);
+    P.rk = c->rk.as<uint32_t>();
+    P.mult = c->mult.as<uint32_t>();
+    return P;
+}
+
+int dashgpu_proj_garble_dev(const dashgpu_proj_ctx* c, uint32_t n, const void* in, const void* gates,
+                            const void* wires, void* rows, void* out0) {
+    return guarded([&] {
+        ProjParams P = proj_params(c, n, in, gates, rows, out0);
+        if (n && !wires) throw DataError("null device buffer");
+        P.wires = static_cast<const uint64_t*>(wires);
+        P.garbler = 1;
+        if (n) launch_proj(P, g_stream);
+    });
+}
+
+int dashgpu_proj_eval_dev(const dashgpu_proj_ctx* c, uint32_t n, const void* in, const void* gates,
+                          const void* rows, void* out) {
+    return guarded([&] {
+        ProjParams P = proj_params(c, n, in, gates, const_cast<void*>(rows), out);
+        if (n) launch_proj(P, g_stream);
     });
 }
 

@@ -353,6 +353,7 @@ void* event_create() {
 void event_destroy(void* e) {
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
 }
+void event_sync(void* e) { ck(cudaEventSynchronize(static_cast<cudaEvent_t>(e)), "event sync"); }
 void event_record(void* e, void* st) { ck(cudaEventRecord(static_cast<cudaEvent_t>(e), S(st)), "event record"); }
 void stream_wait(void* st, void* e) {
     ck(cudaStreamWaitEvent(S(st), static_cast<cudaEvent_t>(e), 0), "stream wait");

@@ -51,6 +51,7 @@ void stream_destroy(void* s);
 void* event_create();
 void event_destroy(void* e);
 void event_record(void* e, void* stream);
+void event_sync(void* e);  // host waits for the event
 void stream_wait(void* stream, void* e);
 
 // per-kernel-kind event timing on the launching stream (bench roofline)

@@ -145,6 +145,10 @@ def _declare(L):
     L.dashgpu_proj_garble.argtypes = [u8p, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u8p, u64p, u64p, u64p,
                                       u64p, u64p, u64p]
     L.dashgpu_proj_eval.argtypes = [ctypes.c_uint32, ctypes.c_int, ctypes.c_int, u64p, u64p, u64p, u64p]
+    L.dashgpu_proj_ctx_create.argtypes = [u8p, ctypes.c_int, ctypes.c_int, u8p, ctypes.POINTER(vp)]
+    L.dashgpu_proj_ctx_destroy.argtypes = [vp]
+    L.dashgpu_proj_garble_dev.argtypes = [vp, ctypes.c_uint32, vp, vp, vp, vp, vp]
+    L.dashgpu_proj_eval_dev.argtypes = [vp, ctypes.c_uint32, vp, vp, vp, vp]
     L.dashgpu_profile.argtypes = [ctypes.c_int]
     L.dashgpu_profile_read.argtypes = [f64p, u64p, ctypes.c_int]
     L.dashgpu_last_act_launch.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
@@ -373,6 +377,15 @@ class Dash:
                                                ra.ctypes.data_as(u64p), out.ctypes.data_as(u64p)))
         return [int(o[0]) | (int(o[1]) << 64) for o in out]
 
+    def proj_ctx(self, seed: bytes, p: int, q: int, phi) -> "ProjCtx":
+        """Device-resident t_proj (dashgpu_proj_ctx_*): buffers are device
+        pointers (ints), work goes on this thread's stream without a sync."""
+        ph = np.ascontiguousarray(phi, np.uint8)
+        h = vp()
+        self._check(self.lib.dashgpu_proj_ctx_create((ctypes.c_uint8 * 16)(*seed), p, q, ph.ctypes.data_as(u8p),
+                                                     ctypes.byref(h)))
+        return ProjCtx(self, h, p, q)
+
     # ---- primitives (parity tests) ----
     def prim(self, op: int, m: int, q: int = 0, inp=None, out=None, key: bytes = None, wires=None, gate: int = 0,
              n: int = None):
@@ -386,6 +399,24 @@ class Dash:
                                           dg.ctypes.data_as(u16p), kb,
                                           None if wa is None else wa.ctypes.data_as(u64p), gate))
         return oa, dg
+
+
+class ProjCtx:
+    def __init__(self, eng: Dash, h, p: int, q: int):
+        self.eng, self.h, self.p, self.q = eng, h, p, q
+
+    def __del__(self):
+        try:
+            self.eng.lib.dashgpu_proj_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+    def garble(self, n: int, labels: int, gates: int, wires: int, rows: int, out0: int):
+        self.eng._check(self.eng.lib.dashgpu_proj_garble_dev(self.h, n, vp(labels), vp(gates), vp(wires), vp(rows),
+                                                             vp(out0)))
+
+    def eval(self, n: int, labels: int, gates: int, rows: int, out: int):
+        self.eng._check(self.eng.lib.dashgpu_proj_eval_dev(self.h, n, vp(labels), vp(gates), vp(rows), vp(out)))
 
 
 class GpuCircuit:

@@ -67,6 +67,7 @@ void* stream_create() { return nullptr; }
 void stream_destroy(void*) {}
 void* event_create() { return nullptr; }
 void event_destroy(void*) {}
+void event_sync(void*) {}
 void event_record(void*, void*) {}
 void stream_wait(void*, void*) {}
 void prof_enable(int) {}

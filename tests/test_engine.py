@@ -694,3 +694,53 @@ def test_foreign_or_misshapen_bundles_are_data_errors(eng):
         eng.evaluate(a, eng.bundle_from_labels(a, [l[:, :2] for l in lanes], output=False))
     with pytest.raises(DataError):
         eng.bundle_from_labels(a, lanes[:-1], output=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,q", [(2, 2), (7, 7), (19, 19), (23, 110)])
+def test_projection_ctx_device_path_matches_host_api(gpu, oracle, p, q):
+    """The device-resident t_proj (dashgpu_proj_ctx_*, the raw projection
+    sweep's path) over 70,000 gates (many blocks) gives the same rows / out0 /
+    evaluations as the host-buffer API, which the test above pins to the
+    oracle; a sample of rows is also checked against the oracle directly."""
+    import torch
+
+    gpu.set_stream(torch.cuda.current_stream().cuda_stream)
+    n = 70_000
+    seed = seed_hex(0xD0 + p)
+    phi = [(v * v + 1) % q for v in range(p)]
+    rnd = np.random.default_rng(p + q)
+    lab = rnd.integers(0, 2**63, size=(n, 2), dtype=np.int64)
+    gates = rnd.integers(0, 2**40, size=n).astype(np.int64)
+    wires = (5_000_000 + np.arange(n)).astype(np.int64)
+    dl, dg, dw = (torch.from_numpy(a).cuda() for a in (lab, gates, wires))
+    rows = torch.empty((n * p, 2), dtype=torch.int64, device="cuda")
+    out0 = torch.empty((n, 2), dtype=torch.int64, device="cuda")
+    outv = torch.empty((n, 2), dtype=torch.int64, device="cuda")
+    ctx = gpu.proj_ctx(seed, p, q, phi)
+    ctx.garble(n, dl.data_ptr(), dg.data_ptr(), dw.data_ptr(), rows.data_ptr(), out0.data_ptr())
+    ctx.eval(n, dl.data_ptr(), dg.data_ptr(), rows.data_ptr(), outv.data_ptr())
+    torch.cuda.synchronize()
+    rows_h = rows.cpu().numpy().view(np.uint64).reshape(n, p, 2)
+    out0_h = out0.cpu().numpy().view(np.uint64)
+    outv_h = outv.cpu().numpy().view(np.uint64)
+    j = lambda a: int(a[0]) | (int(a[1]) << 64)  # noqa: E731
+    sample = sorted(set(rnd.integers(0, n, size=40).tolist()) | {0, n - 1})
+    labels = [j(lab[i].view(np.uint64)) for i in sample]
+    hrows, hout0, (Rp, Rq) = gpu.proj_garble(seed, p, q, phi, labels, gates[sample].tolist(), wires[sample].tolist())
+    hev = gpu.proj_eval(p, q, labels, gates[sample].tolist(), hrows)
+    rp = np.array(oracle.decompress_mod(Rp, p))
+    rq = np.array(oracle.decompress_mod(Rq, q))
+    for t, i in enumerate(sample):
+        assert [j(r) for r in rows_h[i]] == hrows[t]
+        assert j(out0_h[i]) == hout0[t]
+        assert j(outv_h[i]) == hev[t]
+        x = np.array(oracle.decompress_mod(labels[t], p))
+        o0 = np.array(oracle.decompress_mod(hout0[t], q))
+        c = int(x[0])
+        a = (t * 7) % p
+        key = ((x + a * rp) % p).tolist()
+        msg = ((o0 + phi[a] * rq) % q).tolist()
+        assert j(rows_h[i][(c + a) % p]) == oracle.encrypt_label(p, key, int(gates[i]), (c + a) % p, 0, q, msg)
+        # the base label is the active label of value 0
+        assert j(outv_h[i]) == oracle.compress(q, ((o0 + phi[0] * rq) % q).tolist())
