@@ -518,7 +518,8 @@ def roofline_fields(args, info, B, ms, prof):
     head = dict(out.get("act_garble", {}))
     traffic, issue = None, {}
     tp = os.path.join(ROOT, "profiles", "act_garble_traffic.json")
-    if os.path.exists(tp):
+    # the ncu capture is of the headline launch (LeNet-5, k = 8, batch 64): other configs get no traffic figure
+    if os.path.exists(tp) and (args.model, args.k, args.batch, args.private) == (MODEL, K, 64, False):
         tj = json.load(open(tp))
         traffic = tj.get("dram_bytes_per_launch")
         issue = {k: tj[k] for k in ("issue_active_frac", "alu_pipe_frac", "warps_active_per_sm",

@@ -991,6 +991,7 @@ struct HLayer {
     std::vector<int32_t> koff_h;
     std::shared_ptr<DevBuf> wexp, koff;
     TcLinear tc;
+    std::vector<int> tc_primes;  // CRT primes of the lanes (build_tc_linear)
     std::vector<uint64_t> lane_ct_off, lane_gate_off, lane_wire_off;  // private
     uint32_t K = 0;  // window
     // activation
@@ -1101,28 +1102,55 @@ static int64_t resid(int64_t w, int p) { return ((w % p) + p) % p; }
 // whole 128-byte K stages and N tiles, and the im2col window offsets
 // koff[i] = ic*H*W + ky*W + kx (dense: i).
 static void build_tc_linear(HLayer& l, int k) {
+    // tc_linear.cuh: per lane a plain [Npad][Kpad] u8 K-major weight-residue
+    // matrix (row oc, column = window index i), all lanes stacked
     const bool dense = l.kind == DASH_LAYER_DENSE;
     const uint32_t nout = dense ? l.out_dim : l.out_ch, K = l.K;
     TcLinear& T = l.tc;
     T.k = (uint32_t)k;
     T.nout = nout;
-    T.kblocks = (K + 31) / 32;
+    // zero-wire and bias terms folded into the contraction as two extra
+    // window columns (A: the zero label / R_p digits of the row's inference,
+    // B: z_oc and p - b_oc) when the u32 accumulator provably stays below
+    // 2^31: then sum mod p equals the reference's (acc mod p + z zero - b R)
+    // mod p (layer.cpp:177-188) and the epilogue is one reduction per digit
+    T.fold = 1;
+    for (int i = 0; i < k; ++i) {
+        const uint64_t p = (uint64_t)l.tc_primes[i];
+        if ((uint64_t)(K + 2) * (p - 1) * (p - 1) >= (1ull << 31)) T.fold = 0;
+    }
+    const uint32_t Keff = K + (T.fold ? 2 : 0);
+    T.kblocks = (Keff + 127) / 128;
     T.Kpad = T.kblocks * 128;
-    const uint32_t n4 = 4 * nout;
-    T.BN = n4 <= 32 ? 32 : n4 <= 64 ? 64 : n4 <= 128 ? 128 : 256;
-    T.Npad = (n4 + T.BN - 1) / T.BN * T.BN;
+    static const uint32_t bn_max = [] {  // tuning: DASH_TC_BNMAX=128 caps the column tile
+        const char* e = std::getenv("DASH_TC_BNMAX");
+        return (e && std::atoi(e) == 128) ? 128u : 256u;
+    }();
+    T.BN = nout <= 16 ? 16 : nout <= 32 ? 32 : nout <= 64 ? 64 : nout <= 128 ? 128 : bn_max;
+    T.Npad = (nout + T.BN - 1) / T.BN * T.BN;
+    for (int i = 0; i < k; ++i) {  // the epilogue reads z / bias residues a column tile at a time
+        l.zt_h[i].resize(std::max<size_t>(l.zt_h[i].size(), T.Npad), 0);
+        l.bres_h[i].resize(std::max<size_t>(l.bres_h[i].size(), T.Npad), 0);
+    }
     l.wexp_h.assign((size_t)k * T.Npad * T.Kpad, 0);
     const uint64_t M = l.E_out;
     for (int i = 0; i < k; ++i) {
         const std::vector<uint8_t>& wr = l.wres_h[i];
-        for (uint32_t oc = 0; oc < nout; ++oc)
-            for (uint32_t j = 0; j < 4; ++j) {
-                uint8_t* row = &l.wexp_h[((size_t)i * T.Npad + 4 * oc + j) * T.Kpad];
-                for (uint32_t kw = 0; kw < K; ++kw)
-                    row[4 * kw + j] = dense ? wr[(uint64_t)kw * M + oc] : wr[(uint64_t)oc * K + kw];
+        for (uint32_t oc = 0; oc < nout; ++oc) {
+            uint8_t* row = &l.wexp_h[((size_t)i * T.Npad + oc) * T.Kpad];
+            for (uint32_t kw = 0; kw < K; ++kw) row[kw] = dense ? wr[(uint64_t)kw * M + oc] : wr[(uint64_t)oc * K + kw];
+            if (T.fold) {
+                const uint32_t p = (uint32_t)l.tc_primes[i], b = l.bres_h[i][oc];
+                row[K] = l.zt_h[i][oc];                   // x z_oc the zero-wire label
+                row[K + 1] = (uint8_t)(b ? p - b : 0u);  // x (p - b_oc) R_p (garbler; the evaluator's column is 0)
             }
+        }
     }
-    l.koff_h.assign((size_t)T.kblocks * 32, -1);
+    l.koff_h.assign((size_t)T.kblocks * 128, -1);
+    if (T.fold) {
+        l.koff_h[K] = -2;      // the zero-wire label word of the row's inference
+        l.koff_h[K + 1] = -3;  // R_p word (garbler), 0 (evaluator)
+    }
     for (uint32_t kw = 0; kw < K; ++kw) {
         if (dense) {
             l.koff_h[kw] = (int32_t)kw;
@@ -1213,7 +1241,10 @@ static void prepare_circuit(dashgpu_circuit& c) {
                     l.wres_h.push_back(std::move(wr));
                     l.zt_h.push_back(std::move(zt));
                     l.bres_h.push_back(std::move(br));
-                    if (i == k - 1) build_tc_linear(l, k);
+                    if (i == k - 1) {
+                        l.tc_primes = c.base.primes;
+                        build_tc_linear(l, k);
+                    }
                 } else {
                     std::vector<uint8_t> wr(l.w.size()), br(nrow);
                     for (uint64_t row = 0; row < nrow; ++row) {

@@ -413,6 +413,7 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     const LinParams& L0 = Ls[0];
     P.nl = n;
     P.kblocks = T.kblocks;
+    P.K = L0.K;
     P.BN = T.BN;
     P.tiles_n = T.Npad / T.BN;
     P.nout = T.nout;
@@ -427,10 +428,21 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     }
     P.E_in = L0.E_in;
     P.M = L0.M;
-    P.stages = tc::stages_for(T.BN);
+    P.stages = tc::stages_for(T.BN, T.kblocks);
     P.zstride = L0.zstride;
     P.garbler = L0.garbler;
     P.koff = T.koff;
+    P.dense_vec = !L0.conv && (L0.E_in % 4) == 0;
+    P.fold = T.fold;
+    // small windows: SUB row tiles share one 128-byte K stage (TMEM: SUB * BN <= 256 columns per buffer)
+    P.sub = 1;
+    if (T.kblocks == 1) {
+        const uint32_t keff = L0.K + (T.fold ? 2u : 0u), k32 = (keff + 31) / 32 * 32;
+        uint32_t sub = k32 <= 32 ? 4u : k32 <= 64 ? 2u : 1u;
+        while (sub > 1 && sub * T.BN > 256) sub >>= 1;
+        P.sub = sub;
+    }
+    P.ksub = tc::BKB / P.sub;
     uint32_t tiles = 0;
     for (int i = 0; i < n; ++i) {
         const LinParams& L = Ls[i];
@@ -446,25 +458,22 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
         l.nw = L.nw;
         l.mag = L.mag;
         l.sh = L.sh;
-        l.rows = L.B * L.nw * P.P;
+        l.groups = L.B * L.nw * P.P;
         l.tile_base = tiles;
         l.wrow = (uint32_t)i * T.Npad;
-        tiles += cdiv(l.rows, tc::BM) * P.tiles_n;
+        tiles += cdiv(l.groups, tc::GM * P.sub) * P.tiles_n;
     }
-    // dense layer over 16-byte-aligned planes: the A tiles are plain 2-D boxes
-    // of the [B*nw][4*E_in] digit-byte matrix, loaded by TMA instead of gathered
-    tc::TcAMaps amaps;
-    memset(&amaps, 0, sizeof amaps);
-    P.a_tma = !L0.conv && (L0.E_in % 4) == 0;
-    if (P.a_tma)
-        for (int i = 0; i < n; ++i)
-            encode_u8_2d(&amaps.m[i], Ls[i].in, (uint64_t)4 * L0.E_in, (uint64_t)Ls[i].B * Ls[i].nw,
-                         (uint64_t)4 * L0.E_in, (uint32_t)tc::BKB, (uint32_t)tc::BM);
-    const size_t smem = tc::smem_bytes(T.BN);
+    P.tiles = tiles;
+    P.raw_stages = tc::raw_stages();
+    const size_t smem = tc::smem_bytes(T.BN, P.stages);
     smem_attr((const void*)tc::tc_linear_kernel, smem);
     CUtensorMap map;
     memcpy(&map, T.tmap, sizeof map);
-    tc::tc_linear_kernel<<<tiles, tc::kThreads, smem, S(st)>>>(map, P, amaps);
+    int sms = 0, dev = 0;
+    ck(cudaGetDevice(&dev), "dev");
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+    const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)sms);  // persistent: one CTA per SM
+    tc::tc_linear_kernel<<<grid, tc::kThreads, smem, S(st)>>>(map, P);
     dev::check();
 }
 

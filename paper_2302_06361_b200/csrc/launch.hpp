@@ -88,15 +88,16 @@ void launch_act_multi(const ActParams* dev_layers, const ActParams* host_layers,
                       const Sched& q);
 // Garbler-side output labels of an activation layer (pure PRF functions).
 void launch_act_outputs(const ActParams& P, const uint16_t* primes, void* stream);
-// Tensor-core form of one public linear layer (tc_linear.cuh): the expanded
-// weight residues of all k lanes, [k][Npad][Kpad] u8 K-major (row (oc, j'),
-// column (window index i, byte j), nonzero only for j == j'), the window
-// offset table and the TMA descriptor of the weights.
+// Tensor-core form of one public linear layer (tc_linear.cuh): the weight
+// residues of all k lanes, [k][Npad][Kpad] u8 K-major (row oc, column =
+// window index i), the window offset table and the TMA descriptor of the
+// weights.
 struct TcLinear {
     alignas(64) uint8_t tmap[128];
     const uint8_t* wexp = nullptr;
-    const int32_t* koff = nullptr;  // [kblocks * 32] element offsets, -1 = padding
+    const int32_t* koff = nullptr;  // [kblocks * 128] element offsets, -1 = padding
     uint32_t kblocks = 0, Npad = 0, Kpad = 0, BN = 0, nout = 0, k = 0;
+    int fold = 0;  // zero-wire / bias terms are window columns K, K + 1 (tc_linear.cuh)
 };
 void make_weight_map(TcLinear& t);  // encodes t.tmap for t.wexp
 // all lanes of a public linear layer in one launch

@@ -8,37 +8,47 @@
 // window is < 794k, so the s32 accumulator is exact
 // and one u8 "limb" per digit suffices (digits < 128, residues < p <= 53).
 //
-// GEMM shape per CRT lane (prime p, nw = ceil(n_p/4) digit words):
-//   rows  r  = (b, w, pos)            b inference, w digit word, pos = (oy, ox)
-//   K'       = (window index i, j)    i = (ic, ky, kx), j = byte of the word
-//   cols  n  = (oc, j')
-//   A[r][(i,j)]   = digit 4w+j of input element (ic, oy*s+ky, ox*s+kx)  (im2col gather)
-//   B[(oc,j')][(i,j)] = (w mod p)[oc][i] if j == j' else 0              (expanded weights)
-// so D[r][(oc,j')] is digit 4w+j' of output unit (oc, pos).  The j/j'
-// expansion costs 4x the MACs of the digit contraction but keeps both operands
-// K-major with 4-byte granularity, which lets the im2col gather move whole
-// u32 words (four digits) straight from the wire planes [B][nw][E] and lets
-// the epilogue thread that owns a TMEM row pack four adjacent columns into one
-// output word.  Dense layers are the f = 1, H = W = 1 case with P = 1.
+// GEMM per CRT lane (prime p, nw = ceil(n_p/4) digit words, P output
+// positions; dense layers are the f = 1, H = W = 1, P = 1 case):
+//   row group g = (b, w, pos)        b inference, w digit word, pos = (oy, ox)
+//   MMA rows    (j, g)               j = digit of the word (0..3)
+//   K           i = (ic, ky, kx)     window element, ONE byte per element
+//   cols        oc                   output channel / unit
+//   A[(j,g)][i] = digit 4w+j of input element (ic, oy*s+ky, ox*s+kx)
+//   B[oc][i]    = (w mod p)[oc][i]                     (plain weight residues)
+// so D[(j,g)][oc] is digit 4w+j of output unit (oc, pos): every MAC is an
+// algorithmic digit-MAC (no expansion).  The wire planes hold four digits per
+// u32 word ([B][nw][E]), so the producer warps load whole words (16-byte
+// loads of four consecutive window elements where the window is contiguous)
+// and transpose 4x4 byte blocks in registers (8 PRMT per 16 bytes) into the
+// four K-major rows j of the A tile.  A 128-row tile holds 32 row groups x 4
+// digits, with digit j in TMEM lanes [32j, 32j+32): epilogue warp j reduces
+// digit j of 32 row groups mod p and the four warps meet in shared memory to
+// pack whole output words.
 //
-// CTA (160 threads): warps 0-3 gather A tiles into 128B-swizzled shared
-// memory and later run the epilogue (TMEM -> registers, mod p, + z*zero,
+// CTA (160 threads): warps 0-3 gather + transpose A tiles into 128B-swizzled
+// shared memory and later run the epilogue (TMEM -> registers, mod p, + z*zero,
 // - b*R, pack, store); warp 4 lane 0 streams weight tiles with TMA and issues
 // tcgen05.mma (M = 128, N = BN, K = 32 bytes per instruction).  Stages are
-// tracked with mbarriers (full: 128 gather arrivals + 1 TMA transaction;
-// empty: tcgen05.commit).
+// tracked with mbarriers (full: 128 producer arrivals + 1 TMA transaction;
+// empty: tcgen05.commit).  Two CTAs fit an SM at BN = 256, so one CTA's
+// epilogue overlaps the other's MMAs.
 #pragma once
 
 #include <cuda.h>
 
+#include <cstdlib>
+
 namespace dashgpu {
 namespace tc {
 
-constexpr int BM = 128;        // rows per tile (TMEM lanes)
-constexpr int BKB = 128;       // K bytes per stage: one 128-byte swizzle row
-constexpr int KWS = BKB / 4;   // window elements (u32 words) per stage
-constexpr int kThreads = 160;  // 4 gather/epilogue warps + 1 TMA/MMA warp
+constexpr int BM = 128;        // MMA rows per tile (TMEM lanes) = 4 digits x GM row groups
+constexpr int GM = 32;         // row groups per tile
+constexpr int BKB = 128;       // K bytes (window elements) per stage: one 128-byte swizzle row
+constexpr int kThreads = 320;  // 4 producer warps, 4 epilogue warps, MMA warp, weight-TMA warp
 constexpr uint32_t kAStage = BM * BKB;
+constexpr uint32_t kRawRow = 132;                 // words per raw row (128 + 4: conflict-free 16-byte reads)
+constexpr uint32_t kRawStage = GM * kRawRow * 4;  // bytes of one raw (untransposed) window stage
 
 struct TcLane {
     const uint32_t* in;   // [B][nw][E_in]
@@ -48,25 +58,25 @@ struct TcLane {
     const uint32_t* zero; // zero-wire label words, inference b at zero[b*zstride]
     const uint32_t* R;    // offset R_p words (garbler)
     uint32_t p, n, nw, mag, sh;
-    uint32_t rows;        // B * nw * P
-    uint32_t tile_base;   // first CTA of this lane
+    uint32_t groups;      // B * nw * P row groups
+    uint32_t tile_base;   // first tile of this lane
     uint32_t wrow;        // first row of this lane in the weight tensor
 };
 
 struct TcParams {
     TcLane L[MAXK];
     int nl;
-    uint32_t kblocks;     // K stages (KWS window elements each)
+    uint32_t kblocks;     // K stages (BKB window elements each)
+    uint32_t K;           // window elements
     uint32_t P, OW, s, W, E_in, M, nout, tiles_n, BN, stages, zstride;
+    uint32_t raw_stages;  // depth of the producers' cp.async window ring
+    uint32_t sub;         // row tiles per stage (windows of <= 32 / 64 bytes share the 128-byte K stage)
+    uint32_t ksub;        // K bytes per row tile within a stage (128 / sub)
+    uint32_t tiles;       // all tiles of the launch (persistent CTAs stride over them)
     int garbler;
-    int a_tma;            // dense layer whose planes are TMA-able: A tiles by TMA, no gather
-    const int32_t* koff;  // [kblocks * KWS] element offset of window index i, -1 = padding
-};
-
-// A operand maps of a dense layer (one per CRT lane: the digit plane viewed
-// as a [rows = B*nw][4*E_in] byte matrix, K-major, 128-byte swizzle)
-struct TcAMaps {
-    CUtensorMap m[MAXK];
+    int fold;             // window columns K, K + 1 carry the zero-wire label / R_p (x z_oc, x (p - b_oc))
+    int dense_vec;        // dense layer, E_in % 4 == 0: window words loaded 4 at a time (16 B)
+    const int32_t* koff;  // [kblocks * BKB] element offset of window index i, -1 = padding
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -134,180 +144,375 @@ __device__ __forceinline__ uint32_t modp(uint32_t x, uint32_t p, uint32_t mag, u
     return x - (__umulhi(x, mag) >> sh) * p;
 }
 
+// 4x4 byte transpose: x[c] holds digits (0..3) of window element c; y[j]
+// gets digit j of elements 0..3 (element c in byte c)
+__device__ __forceinline__ void tr4(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t& y0, uint32_t& y1,
+                                    uint32_t& y2, uint32_t& y3) {
+    const uint32_t a = __byte_perm(x0, x1, 0x5140), b = __byte_perm(x2, x3, 0x5140);  // x0b0 x1b0 x0b1 x1b1
+    const uint32_t c = __byte_perm(x0, x1, 0x7362), d = __byte_perm(x2, x3, 0x7362);  // x0b2 x1b2 x0b3 x1b3
+    y0 = __byte_perm(a, b, 0x5410);
+    y1 = __byte_perm(a, b, 0x7632);
+    y2 = __byte_perm(c, d, 0x5410);
+    y3 = __byte_perm(c, d, 0x7632);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// tile t of the launch -> (lane li, row tile mt, column tile nt); column
+// tiles of one row tile are adjacent, so their window words come from L2
+struct TileId {
+    int li;
+    uint32_t mt, nt;
+};
+__device__ __forceinline__ TileId tile_of(const TcParams& P, uint32_t t) {
+    TileId r;
+    r.li = 0;
+    while (r.li + 1 < P.nl && t >= P.L[r.li + 1].tile_base) ++r.li;
+    t -= P.L[r.li].tile_base;
+    r.mt = t / P.tiles_n;
+    r.nt = t - r.mt * P.tiles_n;
+    return r;
+}
+
+// Row group g of lane L: (b, w, pos) -> first word of its window in the plane
+struct Group {
+    const uint32_t* src;
+    uint32_t bw, pos;
+    bool ok;
+};
+__device__ __forceinline__ Group group_of(const TcParams& P, const TcLane& L, uint32_t g) {
+    Group r;
+    r.ok = g < L.groups;
+    const uint32_t gg = r.ok ? g : 0;
+    r.bw = gg / P.P;
+    r.pos = gg - r.bw * P.P;
+    const uint32_t oy = r.pos / P.OW, ox = r.pos - oy * P.OW;
+    r.src = L.in + (uint64_t)r.bw * P.E_in + (uint64_t)(oy * P.s) * P.W + ox * P.s;
+    return r;
+}
+
+// Persistent, warp-specialized: CTA c takes tiles c, c + grid, ...; the
+// producers run ahead across tile boundaries, the MMA warp alternates two
+// TMEM accumulators so the epilogue of one tile overlaps the MMAs of the next.
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_linear_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ TcParams P,
-                     const __grid_constant__ TcAMaps amaps) {
+    tc_linear_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ TcParams P) {
     extern __shared__ uint8_t tc_smem_raw[];
     uint8_t* base = (uint8_t*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t S = P.stages, BN = P.BN;
+    const uint32_t S = P.stages, BN = P.BN, RS = P.raw_stages, SUB = P.sub, KS = P.ksub;
+    // TMEM columns per accumulator: SUB row tiles x BN columns (power of two >= 32)
+    uint32_t tcols = 32;
+    while (tcols < SUB * BN) tcols <<= 1;
 
-    // tile -> (lane, row tile, column tile)
-    uint32_t t = blockIdx.x;
-    int li = 0;
-    while (li + 1 < P.nl && t >= P.L[li + 1].tile_base) ++li;
-    const TcLane& L = P.L[li];
-    t -= L.tile_base;
-    const uint32_t mt = t / P.tiles_n, nt = t - mt * P.tiles_n;
-
-    const uint32_t sA = smem_u32(base);
-    const uint32_t sB = sA + S * kAStage;
-    uint64_t* bars = (uint64_t*)(base + S * (kAStage + BN * BKB));
-    const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * S, done = full0 + 16 * S;
-    uint32_t* tslot = (uint32_t*)(bars + 2 * S + 1);
+    const uint32_t sA = smem_u32(base);                     // S x [128 rows][128 B], swizzled
+    const uint32_t sB = sA + S * kAStage;                   // S x [BN rows][128 B], swizzled (TMA)
+    const uint32_t sRaw = sB + S * BN * BKB;                // RS x [32 rows][132 words]
+    const uint32_t sStg = sRaw + RS * kRawStage;            // epilogue staging [BN][32] words
+    uint64_t* bars = (uint64_t*)(base + (sStg - sA) + BN * 32 * 4);
+    const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * S, tfull0 = full0 + 16 * S,
+                   tempty0 = tfull0 + 16;
+    uint32_t* tslot = (uint32_t*)(bars + 2 * S + 4);
 
     if (tid == 0) {
         for (uint32_t s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, P.a_tma ? 1 : 129);
-            mbar_init(empty0 + 8 * s, 1);
+            mbar_init(full0 + 8 * s, 129);  // 128 producer arrivals + the weight TMA
+            mbar_init(empty0 + 8 * s, 1);   // tcgen05.commit
         }
-        mbar_init(done, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(tfull0 + 8 * i, 1);     // last MMA of a tile committed
+            mbar_init(tempty0 + 8 * i, 128);  // epilogue warps drained the accumulator
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
-        if (P.a_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&amaps.m[li]) : "memory");
     }
-    if (warp == 4) {
+    if (warp == 8) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                     "r"(BN));
+                     "r"(2 * tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    const uint32_t nk = P.kblocks;
 
     if (warp < 4) {
-      if (!P.a_tma) {
-        // ---------------- producer: im2col gather of A into swizzled smem
-        const uint32_t q = lane & 3, rsub = lane >> 2;
-        uint64_t rb[4];
-        bool ok[4];
+        // ---------------- producers: thread (warp q, lane t) owns row group
+        // t of every tile and window elements [32q, 32q + 32) of every stage.
+        // cp.async brings the raw words RS-1 stages ahead into a private ring
+        // (each thread reads back only what it copied), then 4x4 byte
+        // transposes write the rows (j, t) of the swizzled A tile.
+        const uint32_t rawrow = sRaw + lane * kRawRow * 4 + warp * 32 * 4;
+        // this warp's bytes [32 warp, 32 warp + 32) of a stage belong to row
+        // tile st = 32 warp / KS, window offset ko0 = 32 warp mod KS
+        const uint32_t st = (32 * warp) / KS, ko0 = (32 * warp) % KS;
+        uint32_t f_issue = 0, f = 0;  // flat stage counters over (tile, kb)
+        uint32_t it_tile = blockIdx.x, it_kb = 0;  // issue iterator
+        Group ig;
+        bool ig_valid = false;
+        uint32_t ig_g0 = 0, ig_groups = 0, ig_nw = 1, ig_b = 0, ig_w = 0;
+        const uint32_t *ig_in = nullptr, *ig_zero = nullptr, *ig_R = nullptr;
+        auto issue = [&]() {  // cp.async of the next stage (or an empty group)
+            if (it_tile < P.tiles) {
+                if (!ig_valid) {
+                    const TileId ti = tile_of(P, it_tile);
+                    const TcLane L = P.L[ti.li];
+                    ig_g0 = (ti.mt * SUB + st) * GM;
+                    ig = group_of(P, L, ig_g0 + lane);
+                    ig_groups = L.groups;
+                    ig_nw = L.nw;
+                    ig_in = L.in;
+                    ig_zero = L.zero;
+                    ig_R = L.R;
+                    ig_b = ig.bw / L.nw;
+                    ig_w = ig.bw - ig_b * L.nw;
+                    ig_valid = true;
+                }
+                const uint32_t slot = sRaw + (f_issue % RS) * kRawStage;
+                const uint32_t i0 = it_kb * KS + ko0;
+                if (P.dense_vec) {
+                    // coalesced: 8 lanes copy one row group's 128 contiguous
+                    // bytes, 4 row groups per instruction (dense: g = (b, w))
+                    const uint32_t ch = lane & 7, i = i0 + 4 * ch;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            const uint32_t r = mt * BM + warp * 32 + g * 8 + rsub;
-            ok[g] = r < L.rows;
-            const uint32_t rr = ok[g] ? r : 0;
-            const uint32_t bw = rr / P.P, pos = rr - bw * P.P;
-            const uint32_t oy = pos / P.OW, ox = pos - oy * P.OW;
-            rb[g] = (uint64_t)bw * P.E_in + (uint64_t)(oy * P.s) * P.W + ox * P.s;
-        }
-        for (uint32_t kb = 0; kb < P.kblocks; ++kb) {
-            const uint32_t s = kb % S, round = kb / S;
-            uint32_t v[8][4];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int32_t ko = __ldg(P.koff + kb * KWS + c * 4 + q);
-#pragma unroll
-                for (int g = 0; g < 4; ++g) v[c][g] = (ko >= 0 && ok[g]) ? __ldg(L.in + rb[g] + (uint32_t)ko) : 0u;
+                    for (int c = 0; c < 8; ++c) {
+                        const uint32_t r = 4 * c + (lane >> 3), g = ig_g0 + r;
+                        const bool ok = g < ig_groups;
+                        const uint32_t dst = slot + r * kRawRow * 4 + (warp * 32 + 4 * ch) * 4;
+                        if (i < P.K) {
+                            cp_async16(dst, ok ? ig_in + (uint64_t)g * P.E_in + i : P.L[0].in, ok);
+                        } else if (P.fold && i == P.K) {  // {zero word, R word (garbler), 0, 0}
+                            const uint32_t b = g / ig_nw, w = g - b * ig_nw;
+                            cp_async4(dst, ig_zero + (uint64_t)b * P.zstride + w, ok);
+                            cp_async4(dst + 4, ig_R + (uint64_t)b * P.zstride + w, ok && P.garbler);
+                            cp_async4(dst + 8, P.L[0].in, false);
+                            cp_async4(dst + 12, P.L[0].in, false);
+                        } else {
+                            cp_async16(dst, P.L[0].in, false);
+                        }
+                    }
+                } else {
+                    const uint32_t dst = rawrow + (f_issue % RS) * kRawStage;
+#pragma unroll 8
+                    for (int c = 0; c < 32; ++c) {
+                        const int32_t ko = __ldg(P.koff + i0 + c);
+                        const uint32_t* src = ko >= 0 ? ig.src + ko
+                                              : ko == -2 ? ig_zero + (uint64_t)ig_b * P.zstride + ig_w
+                                                         : ig_R + (uint64_t)ig_b * P.zstride + ig_w;
+                        const bool ok = ig.ok && (ko >= 0 || ko == -2 || (ko == -3 && P.garbler));
+                        cp_async4(dst + 4 * c, ok ? src : P.L[0].in, ok);
+                    }
+                }
+                if (++it_kb == nk) {
+                    it_kb = 0;
+                    it_tile += gridDim.x;
+                    ig_valid = false;
+                }
             }
-            if (kb >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
-            const uint32_t a = sA + s * kAStage;
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const uint32_t row = warp * 32 + g * 8 + rsub;
+            cp_commit();
+            ++f_issue;
+        };
+        for (uint32_t d = 0; d + 1 < RS; ++d) issue();
+        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
+            for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+                issue();
+                if (RS == 3) cp_wait<2>();  // the stage issued RS - 1 groups ago has landed
+                else cp_wait<1>();
+                if (P.dense_vec) __syncwarp();  // rows were copied by other lanes of this warp
+                const uint32_t s = f % S, round = f / S;
+                const uint32_t raw = rawrow + (f % RS) * kRawStage;
+                uint32_t x[32];
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a + row * BKB + ((c ^ rsub) << 4) + q * 4),
-                                 "r"(v[c][g])
-                                 : "memory");
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(full0 + 8 * s);
-        }
-      }
-
-        // ---------------- epilogue: TMEM -> mod p -> packed digit words
-        mbar_wait(done, 0);
-        tc_fence_after();
-        const uint32_t r = mt * BM + warp * 32 + lane;
-        const bool valid = r < L.rows;
-        const uint32_t rr = valid ? r : 0;
-        const uint32_t bw = rr / P.P, pos = rr - bw * P.P;
-        const uint32_t b = bw / L.nw, w = bw - b * L.nw;
-        const uint32_t zw = L.zero[(uint64_t)b * P.zstride + w];
-        const uint32_t rw = P.garbler ? L.R[(uint64_t)b * P.zstride + w] : 0u;
-        const uint32_t mask = (4 * w + 4 > L.n) ? (0xffffffffu >> (8 * (4 * w + 4 - L.n))) : 0xffffffffu;
-        uint32_t* orow = L.out + (uint64_t)bw * P.M + pos;
-        const uint32_t c31 = modp(0x7fffffffu, L.p, L.mag, L.sh) + 1u;  // == 2^31 mod p (up to one p)
-        // dense rows: the 4 output words of a column chunk are adjacent
-        const bool vec = P.P == 1 && (P.M & 3) == 0;
-        for (uint32_t cc = 0; cc < BN / 16; ++cc) {
-            uint32_t v[16];
-            tmem_ld16(tmem + ((warp * 32) << 16) + cc * 16, v);
-            uint32_t o4[4];
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(x[4 * c]), "=r"(x[4 * c + 1]), "=r"(x[4 * c + 2]), "=r"(x[4 * c + 3])
+                                 : "r"(raw + 16 * c));
+                if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+                const uint32_t a = sA + s * kAStage;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const uint32_t oc = nt * (BN / 4) + cc * 4 + g;
-                const uint32_t oci = oc < P.nout ? oc : 0;
-                const uint32_t z = L.zt[oci];
-                const uint32_t bb = P.garbler ? L.bres[oci] : 0u;
-                const uint32_t nb = bb ? L.p - bb : 0u;
-                uint32_t o = 0;
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t y[4][4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    // the reference accumulates in u32 with wrap-around
-                    // (layer.cpp:116-118); the s32 MMA accumulator wraps the
-                    // same way, and the 31-bit-exact magic sees its low 31
-                    // bits plus bit 31's residue (2^31 mod p, in [1, p])
-                    const uint32_t s0 = modp(v[g * 4 + j] & 0x7fffffffu, L.p, L.mag, L.sh) + (v[g * 4 + j] >> 31) * c31;
-                    const uint32_t t1 = s0 + z * ((zw >> (8 * j)) & 0xffu) + nb * ((rw >> (8 * j)) & 0xffu);
-                    o |= modp(t1, L.p, L.mag, L.sh) << (8 * j);
+                    for (int cc = 0; cc < 4; ++cc) {
+                        const int c = 16 * h + 4 * cc;
+                        tr4(x[c], x[c + 1], x[c + 2], x[c + 3], y[0][cc], y[1][cc], y[2][cc], y[3][cc]);
+                    }
+                    const uint32_t chunk = ((2 * warp + h) ^ (lane & 7)) << 4;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a + (j * 32 + lane) * BKB + chunk),
+                                     "r"(y[j][0]), "r"(y[j][1]), "r"(y[j][2]), "r"(y[j][3])
+                                     : "memory");
                 }
-                o4[g] = o & mask;
-            }
-            if (!valid) continue;
-            const uint32_t oc0 = nt * (BN / 4) + cc * 4;
-            if (vec && oc0 + 4 <= P.nout) {
-                asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(orow + oc0), "r"(o4[0]), "r"(o4[1]),
-                             "r"(o4[2]), "r"(o4[3])
-                             : "memory");
-            } else {
-#pragma unroll
-                for (int g = 0; g < 4; ++g)
-                    if (oc0 + g < P.nout) orow[(uint64_t)(oc0 + g) * P.P] = o4[g];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(full0 + 8 * s);
             }
         }
-    } else if (lane == 0) {
-        // ---------------- weights by TMA + MMA issue (one thread)
-        const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-        const uint32_t wrow = L.wrow + nt * BN, tx = BN * BKB + (P.a_tma ? kAStage : 0u);
-        const CUtensorMap* amap = &amaps.m[li];
-        const uint32_t pre = P.kblocks < S ? P.kblocks : S;
-        for (uint32_t kb = 0; kb < pre; ++kb) {
-            mbar_expect_tx(full0 + 8 * kb, tx);
-            tma_load_2d(sB + kb * BN * BKB, &wmap, full0 + 8 * kb, (int)(kb * BKB), (int)wrow);
-            if (P.a_tma) tma_load_2d(sA + kb * kAStage, amap, full0 + 8 * kb, (int)(kb * BKB), (int)(mt * BM));
-        }
-        for (uint32_t kb = 0; kb < P.kblocks; ++kb) {
-            const uint32_t s = kb % S, round = kb / S;
-            mbar_wait(full0 + 8 * s, round & 1);
+        cp_wait<0>();
+    } else if (warp < 8) {
+        // ---------------- epilogue: warp 4 + j reads TMEM lanes [32j, 32j + 32) = digit j.
+        // Digits of four adjacent columns are packed into one staging word
+        // (plane j); after the barrier each thread transposes four planes'
+        // words (4x4 bytes) into the output words of four columns.
+        const uint32_t j = warp - 4;
+        uint32_t n = 0;  // tiles done by this CTA
+        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++n) {
+            const TileId ti = tile_of(P, t);
+            const TcLane L = P.L[ti.li];  // by value: registers, not reloaded around the asm below
+            const uint32_t buf = n & 1;
+            mbar_wait(tfull0 + 8 * buf, (n >> 1) & 1);
             tc_fence_after();
-            const uint32_t a = sA + s * kAStage, bsm = sB + s * BN * BKB;
+            for (uint32_t sb = 0; sb < SUB; ++sb) {
+            const Group G = group_of(P, L, (ti.mt * SUB + sb) * GM + lane);
+            const uint32_t b = G.bw / L.nw, w = G.bw - b * L.nw;
+            const uint32_t zj = (__ldg(L.zero + (uint64_t)b * P.zstride + w) >> (8 * j)) & 0xffu;
+            const uint32_t rj = P.garbler ? (__ldg(L.R + (uint64_t)b * P.zstride + w) >> (8 * j)) & 0xffu : 0u;
+            const bool live = 4 * w + j < L.n;  // digits beyond n_p stay zero
+            const uint32_t p = L.p, mag = L.mag, sh = L.sh;
+            const uint32_t c31 = modp(0x7fffffffu, p, mag, sh) + 1u;  // == 2^31 mod p (up to one p)
+            const uint8_t* ztp = L.zt + ti.nt * BN;    // padded to whole column tiles on the host
+            const uint8_t* brp = L.bres + ti.nt * BN;
+            const uint32_t plane = sStg + j * (BN / 4) * 32 * 4;
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free (previous tile stored)
+            for (uint32_t cc = 0; cc < BN / 16; ++cc) {
+                uint32_t v[16];
+                tmem_ld16(tmem + buf * tcols + sb * BN + ((j * 32) << 16) + cc * 16, v);
+                const uint4 zv = __ldg(reinterpret_cast<const uint4*>(ztp + cc * 16));
+                const uint4 bv = P.garbler ? __ldg(reinterpret_cast<const uint4*>(brp + cc * 16)) : make_uint4(0, 0, 0, 0);
+                const uint32_t zw4[4] = {zv.x, zv.y, zv.z, zv.w}, bw4[4] = {bv.x, bv.y, bv.z, bv.w};
+                if (P.fold) {  // zero / bias terms are in the accumulator, which stays below 2^31
 #pragma unroll
-            for (int kk = 0; kk < BKB / 32; ++kk)
-                mma_u8(tmem, sw128_desc(a + kk * 32), sw128_desc(bsm + kk * 32), idesc, (kb | kk) != 0);
-            mma_commit(empty0 + 8 * s);
-            if (kb + S < P.kblocks) {
-                mbar_wait(empty0 + 8 * s, round & 1);
-                mbar_expect_tx(full0 + 8 * s, tx);
-                tma_load_2d(bsm, &wmap, full0 + 8 * s, (int)((kb + S) * BKB), (int)wrow);
-                if (P.a_tma) tma_load_2d(a, amap, full0 + 8 * s, (int)((kb + S) * BKB), (int)(mt * BM));
+                    for (int g4 = 0; g4 < 4; ++g4) {
+                        uint32_t word = 0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) word |= modp(v[4 * g4 + q], p, mag, sh) << (8 * q);
+                        if (!live) word = 0;
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + ((cc * 4 + g4) * 32 + lane) * 4), "r"(word));
+                    }
+                    continue;
+                }
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4) {
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t x = v[4 * g4 + q];
+                        const uint32_t z = (zw4[g4] >> (8 * q)) & 0xffu;
+                        const uint32_t bb = (bw4[g4] >> (8 * q)) & 0xffu;
+                        const uint32_t nb = bb ? p - bb : 0u;
+                        // u32 wrap-around as the reference's accumulator (layer.cpp:116-118);
+                        // the s32 MMA accumulator wraps the same way, the 31-bit-exact
+                        // magic sees the low 31 bits plus bit 31's residue
+                        const uint32_t s0 = modp(x & 0x7fffffffu, p, mag, sh) + (x >> 31) * c31;
+                        word |= modp(s0 + z * zj + nb * rj, p, mag, sh) << (8 * q);
+                    }
+                    if (!live) word = 0;
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + ((cc * 4 + g4) * 32 + lane) * 4), "r"(word));
+                }
+            }
+            if (sb + 1 == SUB) {
+                tc_fence_before();
+                mbar_arrive(tempty0 + 8 * buf);  // accumulator drained: the MMA warp may reuse it
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (G.ok) {
+                uint32_t* orow = L.out + (uint64_t)G.bw * P.M + G.pos;
+                const bool vec = P.P == 1 && (P.M & 3) == 0;
+                for (uint32_t c4 = j; c4 < BN / 4; c4 += 4) {  // columns 4 c4 .. 4 c4 + 3
+                    const uint32_t oc = ti.nt * BN + 4 * c4;
+                    if (oc >= P.nout) break;
+                    uint32_t x0, x1, x2, x3, o0, o1, o2, o3;
+                    const uint32_t a = sStg + (c4 * 32 + lane) * 4, ps = (BN / 4) * 32 * 4;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x0) : "r"(a));
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x1) : "r"(a + ps));
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x2) : "r"(a + 2 * ps));
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x3) : "r"(a + 3 * ps));
+                    tr4(x0, x1, x2, x3, o0, o1, o2, o3);  // o_q = output word of column 4 c4 + q
+                    if (vec && oc + 4 <= P.nout) {
+                        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(orow + oc), "r"(o0), "r"(o1),
+                                     "r"(o2), "r"(o3)
+                                     : "memory");
+                    } else {
+                        orow[(uint64_t)oc * P.P] = o0;
+                        if (oc + 1 < P.nout) orow[(uint64_t)(oc + 1) * P.P] = o1;
+                        if (oc + 2 < P.nout) orow[(uint64_t)(oc + 2) * P.P] = o2;
+                        if (oc + 3 < P.nout) orow[(uint64_t)(oc + 3) * P.P] = o3;
+                    }
+                }
+            }
             }
         }
-        mma_commit(done);
+    } else if (warp == 8 && lane == 0) {
+        // ---------------- MMA issue (one thread), two TMEM accumulators
+        const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+        uint32_t f = 0, n = 0;
+        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++n) {
+            const uint32_t buf = n & 1, d = tmem + buf * tcols;  // row tile sb at columns sb * BN
+            if (n >= 2) mbar_wait(tempty0 + 8 * buf, ((n >> 1) & 1) ^ 1);
+            tc_fence_after();
+            for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+                const uint32_t s = f % S, round = f / S;
+                mbar_wait(full0 + 8 * s, round & 1);
+                tc_fence_after();
+                const uint32_t a = sA + s * kAStage, bsm = sB + s * BN * BKB;
+                for (uint32_t sb = 0; sb < SUB; ++sb)
+                    for (uint32_t kk = 0; kk < KS / 32; ++kk)
+                        mma_u8(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
+                               (kb | kk) != 0);
+                mma_commit(empty0 + 8 * s);
+            }
+            mma_commit(tfull0 + 8 * buf);
+        }
+    } else if (warp == 9 && lane == 0) {
+        // ---------------- weight tiles by TMA, S stages ahead of the MMAs
+        uint32_t f = 0;
+        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
+            const TileId ti = tile_of(P, t);
+            const uint32_t wrow = P.L[ti.li].wrow + ti.nt * BN;
+            for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+                const uint32_t s = f % S, round = f / S;
+                if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+                mbar_expect_tx(full0 + 8 * s, BN * BKB);
+                tma_load_2d(sB + s * BN * BKB, &wmap, full0 + 8 * s, (int)(kb * BKB), (int)wrow);
+            }
+        }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 4) {
+    if (warp == 8) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tcols));
     }
 }
 
-inline uint32_t stages_for(uint32_t BN) { return BN >= 256 ? 2u : (BN >= 128 ? 3u : 4u); }
-inline size_t smem_bytes(uint32_t BN) {
-    const uint32_t S = stages_for(BN);
-    return 1024 + (size_t)S * (kAStage + BN * BKB) + 8 * (2 * S + 2);
+// raw window ring depth (the producers' cp.async prefetch distance is RS - 1): 2 or 3
+inline uint32_t raw_stages() {
+    static const uint32_t rs = [] {
+        const char* e = getenv("DASH_TC_RS");
+        return (e && atoi(e) == 2) ? 2u : 3u;
+    }();
+    return rs;
+}
+inline uint32_t stages_for(uint32_t BN, uint32_t kblocks) {
+    (void)kblocks;
+    const uint32_t fixed = 1024 + raw_stages() * kRawStage + BN * 32 * 4 + 256;
+    const uint32_t per = kAStage + BN * BKB;
+    uint32_t S = (225u * 1024u - fixed) / per;
+    if (S > 8) S = 8;
+    return S < 2 ? 2 : S;
+}
+inline size_t smem_bytes(uint32_t BN, uint32_t S) {
+    return 1024 + (size_t)S * (kAStage + BN * BKB) + raw_stages() * kRawStage + BN * 32 * 4 + 8 * (2 * S + 4) + 16;
 }
 
 }  // namespace tc

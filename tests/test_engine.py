@@ -283,14 +283,21 @@ def _linear_case(kind):
     tiles (4*out_ch > 256), many K stages, strided windows, ragged row tiles."""
     from paper_2302_06361_b200.circuit import Circuit, conv2d, dense, flatten, relu
 
-    r = np.random.default_rng({"wide": 11, "deep": 12, "strided": 13}[kind])
+    r = np.random.default_rng({"wide": 11, "deep": 12, "strided": 13, "ntiles": 14, "ragged": 15}[kind])
     w = lambda *s: r.integers(-2, 3, size=s)  # noqa: E731
     b = lambda n: r.integers(-10, 11, size=n)  # noqa: E731
     if kind == "wide":   # conv N = 512 (2 tiles), dense N = 280 (BN 256, 2 tiles)
         L = [conv2d(3, 128, 3, 1, w(128, 3, 3, 3), b(128)), flatten(), dense(2048, 70, w(70, 2048), b(70)), relu(),
              dense(70, 10, w(10, 70), b(10))]
         return Circuit([3, 6, 6], 9, L)
-    if kind == "deep":   # K = 3000 window elements: 94 K stages, zero-padded tail
+    if kind == "ntiles":  # conv N = 272 and dense N = 300: two BN = 256 column tiles each; K = 4352
+        L = [conv2d(3, 272, 3, 1, w(272, 3, 3, 3), b(272)), flatten(), dense(4352, 300, w(300, 4352), b(300)),
+             relu(), dense(300, 10, w(10, 300), b(10))]
+        return Circuit([3, 6, 6], 8, L)
+    if kind == "ragged":  # E_in % 4 != 0: the dense window goes through the offset table, not 16-byte loads
+        L = [dense(1001, 40, w(40, 1001), b(40)), relu(), dense(40, 3, w(3, 40), b(3))]
+        return Circuit([1001], 6, L)
+    if kind == "deep":   # K = 3000 window elements: 24 K stages, zero-padded tail
         L = [dense(3000, 20, w(20, 3000), b(20)), relu(), dense(20, 3, w(3, 20), b(3))]
         return Circuit([3000], 8, L)
     # strided / non-square windows over ragged planes (E_in = 5*13*11)
@@ -299,7 +306,7 @@ def _linear_case(kind):
     return Circuit([5, 13, 11], 7, L)
 
 
-@pytest.mark.parametrize("kind", ["wide", "deep", "strided"])
+@pytest.mark.parametrize("kind", ["wide", "ntiles", "ragged", "deep", "strided"])
 def test_tensor_core_linear_vs_oracle(eng, oracle, kind):
     gpu = eng
     c = _linear_case(kind)
@@ -744,3 +751,34 @@ def test_projection_ctx_device_path_matches_host_api(gpu, oracle, p, q):
         assert j(rows_h[i][(c + a) % p]) == oracle.encrypt_label(p, key, int(gates[i]), (c + a) % p, 0, q, msg)
         # the base label is the active label of value 0
         assert j(outv_h[i]) == oracle.compress(q, ((o0 + phi[0] * rq) % q).tolist())
+
+
+@pytest.mark.gpu
+def test_linear_accumulator_wraps_like_the_reference(gpu):
+    """The reference accumulates each digit sum in u32 and wraps
+    (layer.cpp:116-118, acc[d] += w * digits[d]); windows with
+    K (p-1)^2 >= 2^31 must still match.  Dense(1.6M -> 1), k = 16, every
+    weight -1 (residue p-1) and every input digit p-1: lane p = 53 sums
+    1.6M * 52^2 = 4.33e9 (wraps past 2^32), p = 47 sums 3.39e9 (bit 31 set)."""
+    from paper_2302_06361_b200.circuit import Circuit, dense
+
+    K = 1_600_000
+    k = 16
+    c = Circuit([K], k, [dense(K, 1, np.full((1, K), -1, np.int64), np.zeros(1, np.int64))])
+    g = gpu.circuit(c)
+    net = gpu.network_setup(g, seed_hex(0xACC))
+    lanes = [np.full((1, K, _ndig(p)), p - 1, np.uint16) for p in PRIMES[:k]]
+    out = gpu.layer_eval(net, 0, gpu.bundle_from_labels(net, lanes))
+    for i, p in enumerate(PRIMES[:k]):
+        acc = (K * (p - 1) * (p - 1)) % (1 << 32)
+        got = out.labels(i)[0, 0]
+        assert (got == acc % p).all(), (p, acc, got[:4])
+    assert K * 52 * 52 >= 1 << 32 and (1 << 31) <= K * 46 * 46 < 1 << 32
+
+
+def _ndig(m):
+    n, v = 0, 1
+    while v * m <= 1 << 128:
+        v *= m
+        n += 1
+    return n
