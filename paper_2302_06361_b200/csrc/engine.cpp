@@ -1101,12 +1101,57 @@ static int64_t resid(int64_t w, int p) { return ((w % p) + p) % p; }
 // weights W'[(lane, oc, j')][(i, j)] = wres[oc][i] if j == j', zero padded to
 // whole 128-byte K stages and N tiles, and the im2col window offsets
 // koff[i] = ic*H*W + ky*W + kx (dense: i).
-static void build_tc_linear(HLayer& l, int k) {
-    // tc_linear.cuh: per lane a plain [Npad][Kpad] u8 K-major weight-residue
-    // matrix (row oc, column = window index i), all lanes stacked
+// tc_linear_exp.cuh: rows (b, w, pos), K' = (window index, digit byte), the
+// weight residues expanded block-diagonally over the four digit bytes
+static void build_tc_linear_exp(HLayer& l, int k) {
     const bool dense = l.kind == DASH_LAYER_DENSE;
     const uint32_t nout = dense ? l.out_dim : l.out_ch, K = l.K;
     TcLinear& T = l.tc;
+    T.mode = TcLinear::EXPANDED;
+    T.fold = 0;
+    T.k = (uint32_t)k;
+    T.nout = nout;
+    T.kblocks = (K + 31) / 32;
+    T.Kpad = T.kblocks * 128;
+    const uint32_t n4 = 4 * nout;
+    T.BN = n4 <= 32 ? 32 : n4 <= 64 ? 64 : n4 <= 128 ? 128 : 256;
+    T.Npad = (n4 + T.BN - 1) / T.BN * T.BN;
+    l.wexp_h.assign((size_t)k * T.Npad * T.Kpad, 0);
+    const uint64_t M = l.E_out;
+    for (int i = 0; i < k; ++i) {
+        const std::vector<uint8_t>& wr = l.wres_h[i];
+        for (uint32_t oc = 0; oc < nout; ++oc)
+            for (uint32_t j = 0; j < 4; ++j) {
+                uint8_t* row = &l.wexp_h[((size_t)i * T.Npad + 4 * oc + j) * T.Kpad];
+                for (uint32_t kw = 0; kw < K; ++kw)
+                    row[4 * kw + j] = dense ? wr[(uint64_t)kw * M + oc] : wr[(uint64_t)oc * K + kw];
+            }
+    }
+    l.koff_h.assign((size_t)T.kblocks * 32, -1);
+    for (uint32_t kw = 0; kw < K; ++kw) {
+        if (dense) {
+            l.koff_h[kw] = (int32_t)kw;
+        } else {
+            const uint32_t f = l.filter, ic = kw / (f * f), ky = (kw / f) % f, kx = kw % f;
+            l.koff_h[kw] = (int32_t)((ic * l.in_shape[1] + ky) * l.in_shape[2] + kx);
+        }
+    }
+}
+
+static void build_tc_linear(HLayer& l, int k) {
+    // convolutions and dense layers over unaligned planes: the expanded-digit
+    // kernel (whole-word window gathers); aligned dense layers: the digit-row
+    // kernel (no expansion)
+    const bool dense = l.kind == DASH_LAYER_DENSE;
+    if (!dense || l.K % 4 != 0) {
+        build_tc_linear_exp(l, k);
+        return;
+    }
+    // tc_linear.cuh: per lane a plain [Npad][Kpad] u8 K-major weight-residue
+    // matrix (row oc, column = window index i), all lanes stacked
+    const uint32_t nout = dense ? l.out_dim : l.out_ch, K = l.K;
+    TcLinear& T = l.tc;
+    T.mode = TcLinear::DIGIT_ROWS;
     T.k = (uint32_t)k;
     T.nout = nout;
     // zero-wire and bias terms folded into the contraction as two extra

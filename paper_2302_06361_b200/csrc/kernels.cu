@@ -18,6 +18,7 @@ __device__ uint32_t g_T0[256];
 #include "dash_prim.cuh"
 #include "kernels_common.cuh"
 #include "tc_linear.cuh"
+#include "tc_linear_exp.cuh"
 #include "wpe.cuh"
 
 namespace dashgpu {
@@ -400,14 +401,80 @@ static void encode_u8_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64
 
 void make_weight_map(TcLinear& T) {
     CUtensorMap m;
-    encode_u8_2d(&m, T.wexp, T.Kpad, (uint64_t)T.k * T.Npad, T.Kpad, (uint32_t)tc::BKB, T.BN);
+    encode_u8_2d(&m, T.wexp, T.Kpad, (uint64_t)T.k * T.Npad, T.Kpad, (uint32_t)tc::BKB, T.BN);  // both kernels: 128-byte K boxes
     static_assert(sizeof(CUtensorMap) == sizeof(T.tmap), "tensor map size");
     memcpy(T.tmap, &m, sizeof m);
+}
+
+// expanded-digit kernel (tc_linear_exp.cuh): convolutions, unaligned dense layers
+static void launch_linear_exp(const LinParams* Ls, int n, const TcLinear& T, void* st) {
+    tcx::TcParams P;
+    memset(&P, 0, sizeof P);
+    const LinParams& L0 = Ls[0];
+    P.nl = n;
+    P.kblocks = T.kblocks;
+    P.BN = T.BN;
+    P.tiles_n = T.Npad / T.BN;
+    P.nout = T.nout;
+    if (L0.conv) {
+        P.P = L0.OH * L0.OW;
+        P.OW = L0.OW;
+        P.s = L0.stride;
+        P.W = L0.W;
+    } else {
+        P.P = 1;
+        P.OW = 1;
+    }
+    P.E_in = L0.E_in;
+    P.M = L0.M;
+    P.stages = tcx::stages_for(T.BN);
+    P.zstride = L0.zstride;
+    P.garbler = L0.garbler;
+    P.koff = T.koff;
+    uint32_t tiles = 0;
+    for (int i = 0; i < n; ++i) {
+        const LinParams& L = Ls[i];
+        tcx::TcLane& l = P.L[i];
+        l.in = L.in;
+        l.out = L.out;
+        l.zt = L.zt;
+        l.bres = L.bres;
+        l.zero = L.zero;
+        l.R = L.R;
+        l.p = L.p;
+        l.n = L.n;
+        l.nw = L.nw;
+        l.mag = L.mag;
+        l.sh = L.sh;
+        l.rows = L.B * L.nw * P.P;
+        l.tile_base = tiles;
+        l.wrow = (uint32_t)i * T.Npad;
+        tiles += cdiv(l.rows, tcx::BM) * P.tiles_n;
+    }
+    // dense layer over 16-byte-aligned planes: the A tiles are plain 2-D boxes
+    // of the [B*nw][4*E_in] digit-byte matrix, loaded by TMA instead of gathered
+    tcx::TcAMaps amaps;
+    memset(&amaps, 0, sizeof amaps);
+    P.a_tma = !L0.conv && (L0.E_in % 4) == 0;
+    if (P.a_tma)
+        for (int i = 0; i < n; ++i)
+            encode_u8_2d(&amaps.m[i], Ls[i].in, (uint64_t)4 * L0.E_in, (uint64_t)Ls[i].B * Ls[i].nw,
+                         (uint64_t)4 * L0.E_in, (uint32_t)tcx::BKB, (uint32_t)tcx::BM);
+    const size_t smem = tcx::smem_bytes(T.BN);
+    smem_attr((const void*)tcx::tc_linear_kernel, smem);
+    CUtensorMap map;
+    memcpy(&map, T.tmap, sizeof map);
+    tcx::tc_linear_kernel<<<tiles, tcx::kThreads, smem, S(st)>>>(map, P, amaps);
+    dev::check();
 }
 
 void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     if (n <= 0 || Ls[0].B == 0 || Ls[0].M == 0) return;
     ProfScope ps(K_LINEAR, S(st));
+    if (T.mode == TcLinear::EXPANDED) {
+        launch_linear_exp(Ls, n, T, st);
+        return;
+    }
     tc::TcParams P;
     memset(&P, 0, sizeof P);
     const LinParams& L0 = Ls[0];
@@ -428,7 +495,10 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     }
     P.E_in = L0.E_in;
     P.M = L0.M;
-    P.stages = tc::stages_for(T.BN, T.kblocks);
+    uint32_t koff_bytes = (!L0.conv && (L0.E_in % 4) == 0) ? 0u : T.kblocks * tc::BKB * 4;
+    if (koff_bytes > 32 * 1024) koff_bytes = 0;  // huge windows read the table from global memory
+    P.koff_smem = koff_bytes != 0;
+    P.stages = tc::stages_for(T.BN, koff_bytes);
     P.zstride = L0.zstride;
     P.garbler = L0.garbler;
     P.koff = T.koff;
@@ -465,7 +535,7 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     }
     P.tiles = tiles;
     P.raw_stages = tc::raw_stages();
-    const size_t smem = tc::smem_bytes(T.BN, P.stages);
+    const size_t smem = tc::smem_bytes(T.BN, P.stages, koff_bytes);
     smem_attr((const void*)tc::tc_linear_kernel, smem);
     CUtensorMap map;
     memcpy(&map, T.tmap, sizeof map);

@@ -20,7 +20,10 @@ namespace dashgpu {
 // (64 KB AES tables + 28 x 5.5 KB label buffers = 218 KB); evaluation is
 // fastest at 24 (measured on B200: garble 59.1 -> 55.9 ms from 24 to 28
 // warps, eval 13.7 -> 15.2 ms).
-constexpr int kActWarpsGarble = 28;
+#ifndef DASH_GARBLE_WARPS
+#define DASH_GARBLE_WARPS 28
+#endif
+constexpr int kActWarpsGarble = DASH_GARBLE_WARPS;
 constexpr int kActWarpsEval = 24;
 constexpr int kTWords = 256 * 32;
 

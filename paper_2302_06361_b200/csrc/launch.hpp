@@ -98,6 +98,8 @@ struct TcLinear {
     const int32_t* koff = nullptr;  // [kblocks * 128] element offsets, -1 = padding
     uint32_t kblocks = 0, Npad = 0, Kpad = 0, BN = 0, nout = 0, k = 0;
     int fold = 0;  // zero-wire / bias terms are window columns K, K + 1 (tc_linear.cuh)
+    enum { DIGIT_ROWS = 0, EXPANDED = 1 };
+    int mode = DIGIT_ROWS;  // DIGIT_ROWS: tc_linear.cuh (aligned dense); EXPANDED: tc_linear_exp.cuh
 };
 void make_weight_map(TcLinear& t);  // encodes t.tmap for t.wexp
 // all lanes of a public linear layer in one launch

@@ -76,6 +76,7 @@ struct TcParams {
     int garbler;
     int fold;             // window columns K, K + 1 carry the zero-wire label / R_p (x z_oc, x (p - b_oc))
     int dense_vec;        // dense layer, E_in % 4 == 0: window words loaded 4 at a time (16 B)
+    int koff_smem;        // the offset table is copied to shared memory (all but huge windows)
     const int32_t* koff;  // [kblocks * BKB] element offset of window index i, -1 = padding
 };
 
@@ -218,7 +219,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sB = sA + S * kAStage;                   // S x [BN rows][128 B], swizzled (TMA)
     const uint32_t sRaw = sB + S * BN * BKB;                // RS x [32 rows][132 words]
     const uint32_t sStg = sRaw + RS * kRawStage;            // epilogue staging [BN][32] words
-    uint64_t* bars = (uint64_t*)(base + (sStg - sA) + BN * 32 * 4);
+    const uint32_t sKoff = sStg + BN * 32 * 4;              // window offset table (conv), kblocks x 128 ints
+    const uint32_t koff_bytes = P.koff_smem ? P.kblocks * BKB * 4 : 0u;
+    uint64_t* bars = (uint64_t*)(base + (sKoff - sA) + koff_bytes);
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * S, tfull0 = full0 + 16 * S,
                    tempty0 = tfull0 + 16;
     uint32_t* tslot = (uint32_t*)(bars + 2 * S + 4);
@@ -240,6 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                      "r"(2 * tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    // the window offsets are read by every producer lane for every element:
+    // shared memory, not L1 (which the streamed 4-byte window copies evict)
+    for (uint32_t i = tid; i < koff_bytes / 4; i += kThreads)
+        asm volatile("st.shared.s32 [%0], %1;" ::"r"(sKoff + 4 * i), "r"(__ldg(P.koff + i)) : "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -303,14 +310,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 } else {
                     const uint32_t dst = rawrow + (f_issue % RS) * kRawStage;
+                    const uint32_t* zsrc = ig_zero + (uint64_t)ig_b * P.zstride + ig_w;
+                    const uint32_t* rsrc = ig_R + (uint64_t)ig_b * P.zstride + ig_w;
+                    const bool garb = P.garbler != 0;
 #pragma unroll 8
                     for (int c = 0; c < 32; ++c) {
-                        const int32_t ko = __ldg(P.koff + i0 + c);
-                        const uint32_t* src = ko >= 0 ? ig.src + ko
-                                              : ko == -2 ? ig_zero + (uint64_t)ig_b * P.zstride + ig_w
-                                                         : ig_R + (uint64_t)ig_b * P.zstride + ig_w;
-                        const bool ok = ig.ok && (ko >= 0 || ko == -2 || (ko == -3 && P.garbler));
-                        cp_async4(dst + 4 * c, ok ? src : P.L[0].in, ok);
+                        int32_t ko;
+                        if (P.koff_smem) asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ko) : "r"(sKoff + 4 * (i0 + c)));
+                        else ko = __ldg(P.koff + i0 + c);
+                        const bool real = ko >= 0;
+                        const uint32_t* src = real ? ig.src + ko : (ko == -2 ? zsrc : rsrc);
+                        const bool ok = ig.ok && (real || ko == -2 || (ko == -3 && garb));
+                        cp_async4(dst + 4 * c, ok ? src : zsrc, ok);
                     }
                 }
                 if (++it_kb == nk) {
@@ -503,16 +514,16 @@ inline uint32_t raw_stages() {
     }();
     return rs;
 }
-inline uint32_t stages_for(uint32_t BN, uint32_t kblocks) {
-    (void)kblocks;
-    const uint32_t fixed = 1024 + raw_stages() * kRawStage + BN * 32 * 4 + 256;
+inline uint32_t stages_for(uint32_t BN, uint32_t koff_bytes) {
+    const uint32_t fixed = 1024 + raw_stages() * kRawStage + BN * 32 * 4 + koff_bytes + 256;
     const uint32_t per = kAStage + BN * BKB;
     uint32_t S = (225u * 1024u - fixed) / per;
     if (S > 8) S = 8;
     return S < 2 ? 2 : S;
 }
-inline size_t smem_bytes(uint32_t BN, uint32_t S) {
-    return 1024 + (size_t)S * (kAStage + BN * BKB) + raw_stages() * kRawStage + BN * 32 * 4 + 8 * (2 * S + 4) + 16;
+inline size_t smem_bytes(uint32_t BN, uint32_t S, uint32_t koff_bytes) {
+    return 1024 + (size_t)S * (kAStage + BN * BKB) + raw_stages() * kRawStage + BN * 32 * 4 + koff_bytes +
+           8 * (2 * S + 4) + 16;
 }
 
 }  // namespace tc
