@@ -16,13 +16,15 @@ decode_outputs on the device through the C ABI:
 
 Transport: frames are plain bytes (``encode_frame`` / ``FrameDecoder``); the
 in-process loopback ``run_local_protocol`` drives both services as the
-reference's does (protocol.cpp:355-435).  The TCP servers of the reference
-(protocol.cpp:437-614) are out of scope: any
-byte stream can carry these frames.
+reference's does (protocol.cpp:355-435), and the TCP plumbing of the
+reference (protocol.cpp:437-614) is ``serve_garbler`` / ``serve_evaluator`` /
+``remote_infer`` (one thread per client connection, one locked
+request/reply link from the garbler to the evaluator).
 """
 from __future__ import annotations
 
 import os
+import socket
 import struct
 import threading
 import time
@@ -720,3 +722,250 @@ def run_local_protocol(eng: Dash, quantized: Circuit, inputs, owners: int = 1,
         raise {ErrorCode.AUTHENTICITY: AuthenticityError, ErrorCode.DATA: DataError}.get(code, ProtocolError)(msg)
     res.outputs = decode_result(replies[0].payload)
     return res
+
+
+# ---------------------------------------------------------------- TCP transport (protocol.cpp:437-614)
+
+_RECV_CHUNK = 16384
+
+
+def _send_frame(sock: socket.socket, f: Frame):
+    try:
+        sock.sendall(encode_frame(f))
+    except OSError as e:
+        raise ProtocolError("connection write failed") from e
+
+
+def _read_frame(sock: socket.socket, dec: FrameDecoder) -> Optional[Frame]:
+    """Blocking read of the next whole frame; None on clean EOF (read_frame_fd)."""
+    while True:
+        f = dec.next()
+        if f is not None:
+            return f
+        try:
+            data = sock.recv(_RECV_CHUNK)
+        except OSError as e:
+            raise ProtocolError("connection read failed") from e
+        if not data:
+            return None
+        dec.feed(data)
+
+
+def _connect(host: str, port: int) -> socket.socket:
+    try:
+        s = socket.create_connection((host, port))
+    except OSError as e:
+        raise ProtocolError(f"cannot connect to {host}:{port}") from e
+    s.setsockopt(socket.IPPROTO_TCP, socket.TCP_NODELAY, 1)
+    return s
+
+
+def _listen(host: str, port: int) -> socket.socket:
+    try:
+        infos = socket.getaddrinfo(host or None, port, socket.AF_UNSPEC, socket.SOCK_STREAM, 0, socket.AI_PASSIVE)
+    except OSError as e:
+        raise ProtocolError(f"cannot resolve bind address {host}") from e
+    for fam, typ, proto, _, addr in infos:
+        s = socket.socket(fam, typ, proto)
+        try:
+            s.setsockopt(socket.SOL_SOCKET, socket.SO_REUSEADDR, 1)
+            s.bind(addr)
+            s.listen(16)
+            return s
+        except OSError:
+            s.close()
+    raise ProtocolError(f"cannot bind {host}:{port}")
+
+
+class _TcpServer:
+    """Accept loop with one thread per connection (the reference detaches a
+    std::thread per accepted client).  ``port`` is the bound port (0 binds an
+    ephemeral one); ``start()`` runs the loop in a daemon thread, ``close()``
+    stops accepting and drops the open connections."""
+
+    def __init__(self, bind_host: str, port: int):
+        self._listener = _listen(bind_host, port)
+        self.port = self._listener.getsockname()[1]
+        self._conns: List[socket.socket] = []
+        self._conns_mu = threading.Lock()
+        self._closed = False
+        self._thread: Optional[threading.Thread] = None
+
+    def _serve_client(self, conn: socket.socket):  # pragma: no cover - overridden
+        raise NotImplementedError
+
+    def _client(self, conn: socket.socket):
+        try:
+            self._serve_client(conn)
+        except Error:
+            pass  # connection torn down; session state remains consistent
+        finally:
+            with self._conns_mu:
+                if conn in self._conns:
+                    self._conns.remove(conn)
+            conn.close()
+
+    def serve_forever(self):
+        while not self._closed:
+            try:
+                conn, _ = self._listener.accept()
+            except OSError:
+                if self._closed:
+                    return
+                continue
+            conn.setsockopt(socket.IPPROTO_TCP, socket.TCP_NODELAY, 1)
+            with self._conns_mu:
+                self._conns.append(conn)
+            threading.Thread(target=self._client, args=(conn,), daemon=True).start()
+
+    def start(self):
+        self._thread = threading.Thread(target=self.serve_forever, daemon=True)
+        self._thread.start()
+        return self
+
+    def close(self):
+        self._closed = True
+        try:
+            self._listener.shutdown(socket.SHUT_RDWR)
+        except OSError:
+            pass
+        self._listener.close()
+        with self._conns_mu:
+            for c in self._conns:
+                try:
+                    c.shutdown(socket.SHUT_RDWR)
+                except OSError:
+                    pass
+        if self._thread is not None:
+            self._thread.join(timeout=5)
+
+    def __enter__(self):
+        return self.start()
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class EvaluatorServer(_TcpServer):
+    """serve_evaluator (protocol.cpp:585-603): answers each frame of a
+    connection with EvaluatorService.handle's reply."""
+
+    def __init__(self, eng: Dash, bind_host: str = "127.0.0.1", port: int = 0):
+        super().__init__(bind_host, port)
+        self.service = EvaluatorService(eng)
+        self._mu = threading.Lock()  # one device evaluation at a time
+
+    def _serve_client(self, conn: socket.socket):
+        dec = FrameDecoder()
+        while True:
+            f = _read_frame(conn, dec)
+            if f is None:
+                return
+            with self._mu:
+                reply = self.service.handle(f)
+            if reply is not None:
+                _send_frame(conn, reply)
+
+
+class GarblerServer(_TcpServer):
+    """serve_garbler (protocol.cpp:537-583): clients speak to the garbler;
+    frames for the evaluator go over one connection, written under a lock,
+    and each GARBLED_INPUT is a strict request/reply pair on it."""
+
+    def __init__(self, eng: Dash, evaluator_host: str, evaluator_port: int, bind_host: str = "127.0.0.1",
+                 port: int = 0, cfg: GarblerConfig = None):
+        self.service = GarblerService(eng, cfg)
+        self._evaluator = _connect(evaluator_host, evaluator_port)
+        self._eval_mu = threading.Lock()
+        self._eval_dec = FrameDecoder()
+        self._mu = threading.Lock()  # one device call at a time
+        super().__init__(bind_host, port)
+
+    def _handle(self, f: Frame) -> List[Outbound]:
+        with self._mu:
+            return self.service.handle(f)
+
+    def _to_evaluator(self, frame: Frame):
+        with self._eval_mu:
+            while True:
+                expects_reply = frame.type == FrameType.GARBLED_INPUT
+                _send_frame(self._evaluator, frame)
+                if not expects_reply:
+                    return
+                reply = _read_frame(self._evaluator, self._eval_dec)
+                if reply is None:
+                    raise ProtocolError("evaluator closed the connection")
+                nxt = None
+                for o in self._handle(reply):
+                    if o.dest == Destination.EVALUATOR:
+                        nxt = o.frame
+                if nxt is None:
+                    return
+                frame = nxt
+
+    def _serve_client(self, conn: socket.socket):
+        dec = FrameDecoder()
+        while True:
+            f = _read_frame(conn, dec)
+            if f is None:
+                return
+            for o in self._handle(f):
+                if o.dest == Destination.EVALUATOR:
+                    self._to_evaluator(o.frame)
+                else:
+                    _send_frame(conn, o.frame)
+
+    def close(self):
+        super().close()
+        self._evaluator.close()
+
+
+def serve_evaluator(eng: Dash, bind_host: str, port: int):
+    """Blocking evaluator server (protocol.hpp:232-233); never returns."""
+    EvaluatorServer(eng, bind_host, port).serve_forever()
+
+
+def serve_garbler(eng: Dash, bind_host: str, port: int, evaluator_host: str, evaluator_port: int,
+                  cfg: GarblerConfig = None):
+    """Blocking garbler server (protocol.hpp:227-230); never returns."""
+    GarblerServer(eng, evaluator_host, evaluator_port, bind_host, port, cfg).serve_forever()
+
+
+def remote_infer(garbler_host: str, port: int, quantized: Circuit, inputs, owners: int = 1,
+                 timeout: float = 120.0) -> np.ndarray:
+    """Client side (protocol.cpp:616-659): upload the model and the owners'
+    input slices to the garbler, then poll RESULT until it is ready."""
+    x = np.asarray(inputs, np.int64).ravel()
+    if x.size != quantized.n_in:
+        raise DataError("input size does not match the model")
+    if owners == 0:
+        raise DataError("at least one input owner required")
+    session = int.from_bytes(os.urandom(16), "little")
+    with _connect(garbler_host, port) as conn:
+        _send_frame(conn, Frame(FrameType.MODEL_UPLOAD, session, encode_model_upload(quantized, owners)))
+        chunk, extra = divmod(x.size, owners)
+        offset = 0
+        for o in range(owners):
+            count = chunk + (1 if o < extra else 0)
+            _send_frame(conn, Frame(FrameType.INPUT_UPLOAD, session,
+                                    encode_input_upload(o, offset, x[offset:offset + count])))
+            offset += count
+        dec = FrameDecoder()
+        deadline = time.monotonic() + timeout
+        while True:
+            _send_frame(conn, Frame(FrameType.RESULT, session, b""))
+            reply = _read_frame(conn, dec)
+            if reply is None:
+                raise ProtocolError("garbler closed the connection")
+            if reply.type == FrameType.RESULT:
+                return decode_result(reply.payload)
+            code, msg = decode_error(reply.payload)
+            if code == ErrorCode.AUTHENTICITY:
+                raise AuthenticityError(msg)
+            if code == ErrorCode.DATA:
+                raise DataError(msg)
+            if msg != "result not ready":
+                raise ProtocolError(msg)
+            if time.monotonic() > deadline:
+                raise ProtocolError("timed out waiting for the result")
+            time.sleep(0.05)

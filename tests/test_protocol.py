@@ -432,3 +432,57 @@ def test_garbler_releases_the_gc_after_transfer(eng, oracle):
     res = g.handle(P.Frame(T.RESULT, 9, b""))[0].frame
     assert res.type == T.RESULT
     assert (P.decode_result(res.payload) == oracle.decode(on, oracle.evaluate(on, og))).all()
+
+
+# ---------------------------------------------------------------- TCP transport (protocol.cpp:437-659)
+
+def test_tcp_remote_infer_matches_plain_forward(eng, oracle):
+    # serve_evaluator + serve_garbler + remote_infer on loopback sockets: the
+    # client gets the plain result, for several owner splits and two
+    # concurrent clients on one garbler
+    import threading
+
+    c = tiny()
+    with P.EvaluatorServer(eng, "127.0.0.1", 0) as ev, \
+            P.GarblerServer(eng, "127.0.0.1", ev.port, "127.0.0.1", 0) as gb:
+        for owners, seed in ((1, 910), (3, 911)):
+            x = np.random.default_rng(seed).integers(-7, 8, size=c.n_in)
+            got = P.remote_infer("127.0.0.1", gb.port, c, x, owners)
+            assert got.tolist() == oracle.plain_forward(c, x).tolist()
+        xs = [np.random.default_rng(920 + i).integers(-7, 8, size=c.n_in) for i in range(2)]
+        res = [None, None]
+
+        def client(i):
+            res[i] = P.remote_infer("127.0.0.1", gb.port, c, xs[i], 2)
+
+        ts = [threading.Thread(target=client, args=(i,)) for i in range(2)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(60)
+        assert [r.tolist() for r in res] == [oracle.plain_forward(c, x).tolist() for x in xs]
+        assert all(gb.service.session_done(s) for s in list(gb.service._sessions))
+
+
+def test_tcp_errors_reach_the_client(eng, oracle):
+    c = tiny()
+    x = np.zeros(c.n_in, np.int64)
+    with pytest.raises(P.DataError):  # client-side checks (protocol.cpp:620-622)
+        P.remote_infer("127.0.0.1", 1, c, x[:-1])
+    with pytest.raises(P.DataError):
+        P.remote_infer("127.0.0.1", 1, c, x, 0)
+    with pytest.raises(P.ProtocolError):  # nothing listens there
+        P.remote_infer("127.0.0.1", 1, c, x)
+    with P.EvaluatorServer(eng, "127.0.0.1", 0) as ev, \
+            P.GarblerServer(eng, "127.0.0.1", ev.port, "127.0.0.1", 0) as gb:
+        # more owners than input elements: the garbler's ERROR reply is what the
+        # client's RESULT poll reads first
+        with pytest.raises(P.ProtocolError, match="more input owners"):
+            P.remote_infer("127.0.0.1", gb.port, c, x, c.n_in + 1)
+        # a raw client asking for an unknown session's result
+        import socket
+
+        with socket.create_connection(("127.0.0.1", gb.port)) as s:
+            s.sendall(P.encode_frame(P.Frame(P.FrameType.RESULT, 77, b"")))
+            f = P._read_frame(s, P.FrameDecoder())
+            assert f.type == P.FrameType.ERROR and "unknown session" in P.decode_error(f.payload)[1]
