@@ -10,6 +10,10 @@ for cfg in "model_a 8 1" "model_a 8 64" "lenet5 8 64 --private" "minionn 9 256" 
   timeout 1200 python bench.py --model $1 --k $2 --batch $3 $4 --steps 3 --warmup 3 --no-cpu \
     > gpurun_out/measure/$tag.json 2> gpurun_out/measure/$tag.err
 done
-timeout 900 python bench.py --sweep proj --sweep-log2 16,20,24,26 --sweep-k 2,4,8 > gpurun_out/measure/sweep_proj.jsonl 2> gpurun_out/measure/sweep_proj.err
-timeout 600 python bench.py --sweep linear --sweep-log2 16,20,24 --sweep-k 2,8 > gpurun_out/measure/sweep_linear.jsonl 2> gpurun_out/measure/sweep_linear.err
+# BASELINE configs[4]: the whole grid, k = 2..8 x N = 2^16..2^26 (even powers)
+G="--sweep-log2 16,18,20,22,24,26 --sweep-k 2,3,4,5,6,7,8"
+timeout 1500 python bench.py --sweep proj $G > gpurun_out/measure/sweep_proj.jsonl 2> gpurun_out/measure/sweep_proj.err
+timeout 900 python bench.py --sweep tproj $G > gpurun_out/measure/sweep_tproj.jsonl 2> gpurun_out/measure/sweep_tproj.err
+timeout 900 python bench.py --sweep linear $G > gpurun_out/measure/sweep_linear.jsonl 2> gpurun_out/measure/sweep_linear.err
+tail -n 3 gpurun_out/measure/sweep_*.err
 for f in gpurun_out/measure/*.json; do echo "$f: $(python -c "import json,sys;d=json.load(open('$f'));print(round(d.get('value',0),2), d.get('unit'))" 2>&1 | tail -1)"; done
