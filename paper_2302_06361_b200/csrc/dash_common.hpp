@@ -45,7 +45,8 @@ struct ModC {
     uint8_t nchunks;  // ceil(nw / W)
     uint8_t limbs[21];// significant 32-bit limbs of the value before chunk j
     uint32_t m4;      // m^4
-    uint32_t D;       // m^(4W) <= 2^31: chunk divisor
+    uint32_t D;       // m^(4W) < 2^30: chunk divisor
+    uint32_t negD;    // (uint32_t)-D
     uint32_t mag_m, sh_m;    // x/m  = umulhi(x, mag_m)  >> sh_m  (x < 2^31)
     uint32_t mag_m4, sh_m4;  // x/m^4 = umulhi(x, mag_m4) >> sh_m4 (x < 2^31)
     uint32_t spread;  // m * 0x01010101 (SWAR)

@@ -206,25 +206,52 @@ DASH_HD uint32_t fdiv(uint32_t x, uint32_t mag, uint32_t sh) { return umulhi32(x
 
 // 128-bit value c (4 limbs, c[0] least significant) divided in place by D,
 // returning c mod D.  `limbs` bounds the nonzero limbs (host-computed).
+// Each limb step divides cur = rem 2^32 + c_i (rem < D < 2^30) by D with the
+// reciprocal invD = ih 2^32 + il = floor((2^64 - 1) / D) using 32-bit
+// multiplies only: q~ = rem ih + hi32(rem il + c_i ih) drops the c_i il
+// partial product and the reciprocal's truncation, so q - 2 <= q~ <= q; the
+// low word r~ = c_i - q~ D is then exact (r~ < 3D < 2^32) and two
+// conditional subtractions finish (no 64 x 64 multiply-high, no branches).
+// One limb step: (rem 2^32 + ci) = q D + r, rem < D
+DASH_HD void dm_step(uint32_t rem, uint32_t ci, uint32_t il, uint32_t ih, uint32_t negD, uint32_t D, uint32_t& q,
+                     uint32_t& r) {
+#if defined(__CUDA_ARCH__)
+    asm("{\n\t.reg .u64 t;\n\t.reg .u32 lo, hi;\n\t.reg .pred p;\n\t"
+        "mul.wide.u32 t, %2, %4;\n\t"
+        "mad.wide.u32 t, %3, %5, t;\n\t"
+        "mov.b64 {lo, hi}, t;\n\t"
+        "mad.lo.u32 %1, %2, %5, hi;\n\t"
+        "mad.lo.u32 %0, %1, %6, %3;\n\t"
+        "setp.ge.u32 p, %0, %7;\n\t@p sub.u32 %0, %0, %7;\n\t@p add.u32 %1, %1, 1;\n\t"
+        "setp.ge.u32 p, %0, %7;\n\t@p sub.u32 %0, %0, %7;\n\t@p add.u32 %1, %1, 1;\n\t}"
+        : "=&r"(r), "=&r"(q)  // early clobber: q is written before ci is read
+        : "r"(rem), "r"(ci), "r"(il), "r"(ih), "r"(negD), "r"(D));
+#else
+    const uint64_t t = (uint64_t)rem * il + (uint64_t)ci * ih;
+    q = rem * ih + (uint32_t)(t >> 32);
+    r = q * negD + ci;
+    for (int k = 0; k < 2; ++k)
+        if (r >= D) {
+            r -= D;
+            ++q;
+        }
+#endif
+}
 DASH_HD uint32_t divmod_D(uint32_t c[4], const ModC& M, int limbs) {
-    uint64_t rem = 0;
+    uint32_t rem = 0;
+    const uint32_t il = (uint32_t)M.invD, ih = (uint32_t)(M.invD >> 32), D = M.D, negD = M.negD;
 #if defined(__CUDA_ARCH__)
 #pragma unroll
 #endif
     for (int i = 3; i >= 0; --i) {
         if (i < limbs) {
-            const uint64_t cur = (rem << 32) | c[i];
-            uint64_t q = umulhi64(cur, M.invD);
-            uint64_t r = cur - q * M.D;
-            if (r >= M.D) {
-                r -= M.D;
-                ++q;
-            }
-            c[i] = (uint32_t)q;
+            uint32_t q, r;
+            dm_step(rem, c[i], il, ih, negD, D, q, r);
+            c[i] = q;
             rem = r;
         }
     }
-    return (uint32_t)rem;
+    return rem;
 }
 
 // Four base-m digits of v < m^4 packed as bytes.

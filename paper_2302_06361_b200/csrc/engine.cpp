@@ -132,13 +132,14 @@ static ModC make_modc(int m) {
     while (true) {
         u128 p = 1;
         for (int i = 0; i < 4 * (W + 1); ++i) p *= (u128)m;
-        if (p > ((u128)1 << 31)) break;
+        if (p >= ((u128)1 << 30)) break;  // D < 2^30: divmod_D's r~ < 3D fits 32 bits
         ++W;
     }
     c.W = (uint8_t)W;
     u128 D = 1;
     for (int i = 0; i < 4 * W; ++i) D *= (u128)m;
     c.D = (uint32_t)D;
+    c.negD = 0u - c.D;
     c.nchunks = (uint8_t)((c.nw + W - 1) / W);
     u128 bound = ~(u128)0;
     for (int j = 0; j < c.nchunks && j < 21; ++j) {
