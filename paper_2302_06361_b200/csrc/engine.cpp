@@ -1160,7 +1160,10 @@ static void build_tc_linear(HLayer& l, int k) {
     // B: z_oc and p - b_oc) when the u32 accumulator provably stays below
     // 2^31: then sum mod p equals the reference's (acc mod p + z zero - b R)
     // mod p (layer.cpp:177-188) and the epilogue is one reduction per digit
-    T.fold = 1;
+    // Folding is kept for small windows (K <= 64, several row tiles per
+    // stage, cp.async window copies); larger windows load their window words
+    // by TMA straight from the plane, where the extra columns cannot come from.
+    T.fold = K <= 64;
     for (int i = 0; i < k; ++i) {
         const uint64_t p = (uint64_t)l.tc_primes[i];
         if ((uint64_t)(K + 2) * (p - 1) * (p - 1) >= (1ull << 31)) T.fold = 0;

@@ -498,12 +498,15 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     uint32_t koff_bytes = (!L0.conv && (L0.E_in % 4) == 0) ? 0u : T.kblocks * tc::BKB * 4;
     if (koff_bytes > 32 * 1024) koff_bytes = 0;  // huge windows read the table from global memory
     P.koff_smem = koff_bytes != 0;
-    P.stages = tc::stages_for(T.BN, koff_bytes);
+
     P.zstride = L0.zstride;
     P.garbler = L0.garbler;
     P.koff = T.koff;
     P.dense_vec = !L0.conv && (L0.E_in % 4) == 0;
     P.fold = T.fold;
+    P.nowrap = 1;
+    for (int i = 0; i < n; ++i)
+        if ((uint64_t)(L0.K + 3) * Ls[i].p * Ls[i].p >= (1ull << 31)) P.nowrap = 0;  // acc + z zero + nb R
     // small windows: SUB row tiles share one 128-byte K stage (TMEM: SUB * BN <= 256 columns per buffer)
     P.sub = 1;
     if (T.kblocks == 1) {
@@ -513,6 +516,10 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
         P.sub = sub;
     }
     P.ksub = tc::BKB / P.sub;
+    // dense window words by TMA: one row tile per stage, no fold columns
+    // (the zero-wire / R_p words come from other arrays)
+    P.a_tma = P.dense_vec && P.sub == 1 && !T.fold && std::getenv("DASH_TC_NOTMA") == nullptr;
+    P.stages = tc::stages_for(T.BN, koff_bytes, P.a_tma);
     uint32_t tiles = 0;
     for (int i = 0; i < n; ++i) {
         const LinParams& L = Ls[i];
@@ -534,16 +541,22 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
         tiles += cdiv(l.groups, tc::GM * P.sub) * P.tiles_n;
     }
     P.tiles = tiles;
-    P.raw_stages = tc::raw_stages();
-    const size_t smem = tc::smem_bytes(T.BN, P.stages, koff_bytes);
+    P.raw_stages = tc::raw_stages(P.a_tma);
+    const size_t smem = tc::smem_bytes(T.BN, P.stages, koff_bytes, P.a_tma);
     smem_attr((const void*)tc::tc_linear_kernel, smem);
     CUtensorMap map;
     memcpy(&map, T.tmap, sizeof map);
+    tc::TcRawMaps rmaps;
+    memset(&rmaps, 0, sizeof rmaps);
+    if (P.a_tma)
+        for (int i = 0; i < n; ++i)  // [B * nw][4 E_in] bytes, boxes of 32 rows x 128 bytes
+            encode_u8_2d(&rmaps.m[i], Ls[i].in, (uint64_t)4 * L0.E_in, (uint64_t)Ls[i].B * Ls[i].nw,
+                         (uint64_t)4 * L0.E_in, 128u, (uint32_t)tc::GM);
     int sms = 0, dev = 0;
     ck(cudaGetDevice(&dev), "dev");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
     const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)sms);  // persistent: one CTA per SM
-    tc::tc_linear_kernel<<<grid, tc::kThreads, smem, S(st)>>>(map, P);
+    tc::tc_linear_kernel<<<grid, tc::kThreads, smem, S(st)>>>(map, P, rmaps);
     dev::check();
 }
 

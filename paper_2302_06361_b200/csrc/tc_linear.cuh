@@ -26,13 +26,13 @@
 // digit j of 32 row groups mod p and the four warps meet in shared memory to
 // pack whole output words.
 //
-// CTA (160 threads): warps 0-3 gather + transpose A tiles into 128B-swizzled
-// shared memory and later run the epilogue (TMEM -> registers, mod p, + z*zero,
-// - b*R, pack, store); warp 4 lane 0 streams weight tiles with TMA and issues
-// tcgen05.mma (M = 128, N = BN, K = 32 bytes per instruction).  Stages are
-// tracked with mbarriers (full: 128 producer arrivals + 1 TMA transaction;
-// empty: tcgen05.commit).  Two CTAs fit an SM at BN = 256, so one CTA's
-// epilogue overlaps the other's MMAs.
+// CTA (kThreads = 32 (kProd + 6)): kProd producer warps gather + transpose
+// A tiles into 128B-swizzled shared memory; four epilogue warps (TMEM ->
+// registers, mod p, + z*zero, - b*R, pack, store); one MMA warp whose lane 0
+// issues tcgen05.mma (M = 128, N = BN, K = 32 bytes per instruction) into two
+// TMEM accumulators; one warp streams weight tiles with TMA.  Stages are
+// tracked with mbarriers (full: 32 kProd producer arrivals + 1 TMA
+// transaction; empty: tcgen05.commit).  One persistent CTA per SM.
 #pragma once
 
 #include <cuda.h>
@@ -45,7 +45,36 @@ namespace tc {
 constexpr int BM = 128;        // MMA rows per tile (TMEM lanes) = 4 digits x GM row groups
 constexpr int GM = 32;         // row groups per tile
 constexpr int BKB = 128;       // K bytes (window elements) per stage: one 128-byte swizzle row
-constexpr int kThreads = 320;  // 4 producer warps, 4 epilogue warps, MMA warp, weight-TMA warp
+// producer warps (tuning build: -DDASH_TC_PROD=4): each owns BKB / kProd
+// window elements of every stage for all 32 row groups of the tile; the
+// producers' load -> transpose -> store chain is the kernel's critical path,
+// so more of them in flight shortens a stage
+#ifndef DASH_TC_PROD
+#define DASH_TC_PROD 8
+#endif
+constexpr int kProd = DASH_TC_PROD;
+// timing experiments only (results are wrong): 1 = no MMAs, 2 = producers
+// skip the window copies and transposes, 4 = no weight TMA, 8 = no epilogue,
+// 16 = no window copies (transposes of stale data)
+#ifndef DASH_TC_DBG
+#define DASH_TC_DBG 0
+#endif
+constexpr int kEW = BKB / kProd;                 // window elements (K bytes) per producer warp and stage
+// epilogue warps: 4 or 8 (-DDASH_TC_EPI=4); warp kEpi0 + e reads TMEM lane
+// quarter e mod 4 (its digit j) and column half e / 4 of the tile
+#ifndef DASH_TC_EPI
+#define DASH_TC_EPI 8
+#endif
+constexpr int kEpiW = DASH_TC_EPI;
+constexpr int kThreads = 32 * (kProd + kEpiW + 3);  // producers, epilogue, MMA, weight TMA, window TMA
+constexpr int kEpi0 = kProd, kMmaWarp = kProd + kEpiW, kTmaWarp = kProd + kEpiW + 1, kRawWarp = kProd + kEpiW + 2;
+constexpr uint32_t kRawStageT = GM * BKB * 4;  // TMA window stage: 4 swizzled [32 rows][128 B] boxes
+
+// per-lane 2-D maps of the wire planes [B * nw][4 E_in] bytes (TMA window path)
+struct TcRawMaps {
+    CUtensorMap m[MAXK];
+};
+static_assert(kProd % 4 == 0, "epilogue warp j must sit on TMEM lane quarter j (warp id mod 4)");
 constexpr uint32_t kAStage = BM * BKB;
 constexpr uint32_t kRawRow = 132;                 // words per raw row (128 + 4: conflict-free 16-byte reads)
 constexpr uint32_t kRawStage = GM * kRawRow * 4;  // bytes of one raw (untransposed) window stage
@@ -69,12 +98,14 @@ struct TcParams {
     uint32_t kblocks;     // K stages (BKB window elements each)
     uint32_t K;           // window elements
     uint32_t P, OW, s, W, E_in, M, nout, tiles_n, BN, stages, zstride;
-    uint32_t raw_stages;  // depth of the producers' cp.async window ring
+    uint32_t raw_stages;  // depth of the window ring (cp.async by the producers, or TMA)
+    int a_tma;            // dense window words by TMA (kRawWarp) instead of the producers' cp.async
     uint32_t sub;         // row tiles per stage (windows of <= 32 / 64 bytes share the 128-byte K stage)
     uint32_t ksub;        // K bytes per row tile within a stage (128 / sub)
     uint32_t tiles;       // all tiles of the launch (persistent CTAs stride over them)
     int garbler;
     int fold;             // window columns K, K + 1 carry the zero-wire label / R_p (x z_oc, x (p - b_oc))
+    int nowrap;           // (K + 3) p^2 < 2^31 for every lane: acc + z zero + (p - b) R is one 31-bit reduction
     int dense_vec;        // dense layer, E_in % 4 == 0: window words loaded 4 at a time (16 B)
     int koff_smem;        // the offset table is copied to shared memory (all but huge windows)
     const int32_t* koff;  // [kblocks * BKB] element offset of window index i, -1 = padding
@@ -139,6 +170,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 32 accumulator columns in one TMEM round trip: two x16 loads and the wait
+// in one asm statement, so no use of v can be scheduled before the wait
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%32];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%33];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr), "r"(taddr + 16)
+        : "memory");
 }
 
 __device__ __forceinline__ uint32_t modp(uint32_t x, uint32_t p, uint32_t mag, uint32_t sh) {
@@ -206,7 +252,8 @@ __device__ __forceinline__ Group group_of(const TcParams& P, const TcLane& L, ui
 // producers run ahead across tile boundaries, the MMA warp alternates two
 // TMEM accumulators so the epilogue of one tile overlaps the MMAs of the next.
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_linear_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ TcParams P) {
+    tc_linear_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ TcParams P,
+                     const __grid_constant__ TcRawMaps rmaps) {
     extern __shared__ uint8_t tc_smem_raw[];
     uint8_t* base = (uint8_t*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -218,27 +265,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sA = smem_u32(base);                     // S x [128 rows][128 B], swizzled
     const uint32_t sB = sA + S * kAStage;                   // S x [BN rows][128 B], swizzled (TMA)
     const uint32_t sRaw = sB + S * BN * BKB;                // RS x [32 rows][132 words]
-    const uint32_t sStg = sRaw + RS * kRawStage;            // epilogue staging [BN][32] words
-    const uint32_t sKoff = sStg + BN * 32 * 4;              // window offset table (conv), kblocks x 128 ints
+    const uint32_t rstage = P.a_tma ? kRawStageT : kRawStage;
+    const uint32_t sStg = sRaw + RS * rstage;               // epilogue staging [BN][32] words
+    const uint32_t sZB = sStg + BN * 32 * 4;                // 2 x [z residues | bias residues] of a column tile
+    const uint32_t sKoff = sZB + 4 * BN;                    // window offset table (conv), kblocks x 128 ints
     const uint32_t koff_bytes = P.koff_smem ? P.kblocks * BKB * 4 : 0u;
     uint64_t* bars = (uint64_t*)(base + (sKoff - sA) + koff_bytes);
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * S, tfull0 = full0 + 16 * S,
-                   tempty0 = tfull0 + 16;
-    uint32_t* tslot = (uint32_t*)(bars + 2 * S + 4);
+                   tempty0 = tfull0 + 16, rfull0 = tempty0 + 16, rempty0 = rfull0 + 8 * RS;
+    uint32_t* tslot = (uint32_t*)(bars + 2 * S + 4 + 2 * RS);
 
     if (tid == 0) {
         for (uint32_t s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, 129);  // 128 producer arrivals + the weight TMA
+            mbar_init(full0 + 8 * s, 32 * kProd + 1);  // producer arrivals + the weight TMA
             mbar_init(empty0 + 8 * s, 1);   // tcgen05.commit
+        }
+        for (uint32_t r = 0; r < RS; ++r) {
+            mbar_init(rfull0 + 8 * r, 1);              // window TMA transaction
+            mbar_init(rempty0 + 8 * r, 32 * kProd);    // producers read the window stage
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(tfull0 + 8 * i, 1);     // last MMA of a tile committed
-            mbar_init(tempty0 + 8 * i, 128);  // epilogue warps drained the accumulator
+            mbar_init(tempty0 + 8 * i, 32 * kEpiW);  // epilogue warps drained the accumulator
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+        if (P.a_tma)
+            for (int i = 0; i < P.nl; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"(&rmaps.m[i]) : "memory");
     }
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                      "r"(2 * tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -253,16 +308,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tslot;
     const uint32_t nk = P.kblocks;
 
-    if (warp < 4) {
+    if (warp < kProd) {
         // ---------------- producers: thread (warp q, lane t) owns row group
-        // t of every tile and window elements [32q, 32q + 32) of every stage.
+        // t of every tile and window elements [kEW q, kEW q + kEW) of every stage.
         // cp.async brings the raw words RS-1 stages ahead into a private ring
         // (each thread reads back only what it copied), then 4x4 byte
         // transposes write the rows (j, t) of the swizzled A tile.
-        const uint32_t rawrow = sRaw + lane * kRawRow * 4 + warp * 32 * 4;
-        // this warp's bytes [32 warp, 32 warp + 32) of a stage belong to row
-        // tile st = 32 warp / KS, window offset ko0 = 32 warp mod KS
-        const uint32_t st = (32 * warp) / KS, ko0 = (32 * warp) % KS;
+        const uint32_t rawrow = sRaw + lane * kRawRow * 4 + warp * kEW * 4;
+        // this warp's bytes [kEW warp, kEW warp + kEW) of a stage belong to row
+        // tile st = kEW warp / KS, window offset ko0 = kEW warp mod KS
+        const uint32_t st = (kEW * warp) / KS, ko0 = (kEW * warp) % KS;
         uint32_t f_issue = 0, f = 0;  // flat stage counters over (tile, kb)
         uint32_t it_tile = blockIdx.x, it_kb = 0;  // issue iterator
         Group ig;
@@ -270,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t ig_g0 = 0, ig_groups = 0, ig_nw = 1, ig_b = 0, ig_w = 0;
         const uint32_t *ig_in = nullptr, *ig_zero = nullptr, *ig_R = nullptr;
         auto issue = [&]() {  // cp.async of the next stage (or an empty group)
-            if (it_tile < P.tiles) {
+            if (!(DASH_TC_DBG & 16) && it_tile < P.tiles) {
                 if (!ig_valid) {
                     const TileId ti = tile_of(P, it_tile);
                     const TcLane L = P.L[ti.li];
@@ -290,12 +345,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (P.dense_vec) {
                     // coalesced: 8 lanes copy one row group's 128 contiguous
                     // bytes, 4 row groups per instruction (dense: g = (b, w))
-                    const uint32_t ch = lane & 7, i = i0 + 4 * ch;
+                    constexpr int LPR = kEW / 4, RPI = 32 / LPR;  // lanes per row group, row groups per copy
+                    const uint32_t ch = lane % LPR, i = i0 + 4 * ch;
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint32_t r = 4 * c + (lane >> 3), g = ig_g0 + r;
+                    for (int c = 0; c < 32 / RPI; ++c) {
+                        const uint32_t r = RPI * c + lane / LPR, g = ig_g0 + r;
                         const bool ok = g < ig_groups;
-                        const uint32_t dst = slot + r * kRawRow * 4 + (warp * 32 + 4 * ch) * 4;
+                        const uint32_t dst = slot + r * kRawRow * 4 + (warp * kEW + 4 * ch) * 4;
                         if (i < P.K) {
                             cp_async16(dst, ok ? ig_in + (uint64_t)g * P.E_in + i : P.L[0].in, ok);
                         } else if (P.fold && i == P.K) {  // {zero word, R word (garbler), 0, 0}
@@ -314,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t* rsrc = ig_R + (uint64_t)ig_b * P.zstride + ig_w;
                     const bool garb = P.garbler != 0;
 #pragma unroll 8
-                    for (int c = 0; c < 32; ++c) {
+                    for (int c = 0; c < kEW; ++c) {
                         int32_t ko;
                         if (P.koff_smem) asm volatile("ld.shared.s32 %0, [%1];" : "=r"(ko) : "r"(sKoff + 4 * (i0 + c)));
                         else ko = __ldg(P.koff + i0 + c);
@@ -333,32 +389,74 @@ __global__ void __launch_bounds__(kThreads, 1)
             cp_commit();
             ++f_issue;
         };
-        for (uint32_t d = 0; d + 1 < RS; ++d) issue();
+        if (!P.a_tma)
+            for (uint32_t d = 0; d + 1 < RS; ++d) issue();
+        // TMA window path: this warp's bytes [4 kEW warp, 4 kEW (warp + 1)) of
+        // each swizzled 512-byte row live in box q at 16-byte chunks c0 + c
+        const uint32_t tb0 = 4 * kEW * warp, tq = tb0 / 128, tc0 = (tb0 % 128) / 16;
         for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
             for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+                if (DASH_TC_DBG & 2) {
+                    const uint32_t s = f % S, round = f / S;
+                    if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+                    mbar_arrive(full0 + 8 * s);
+                    continue;
+                }
+                if (P.a_tma) {
+                    const uint32_t r = f % RS, s = f % S, round = f / S;
+                    mbar_wait(rfull0 + 8 * r, (f / RS) & 1);
+                    const uint32_t box = sRaw + r * kRawStageT + tq * 4096 + lane * 128;
+                    uint32_t x[kEW];
+#pragma unroll
+                    for (int c = 0; c < kEW / 4; ++c)
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(x[4 * c]), "=r"(x[4 * c + 1]), "=r"(x[4 * c + 2]), "=r"(x[4 * c + 3])
+                                     : "r"(box + (((tc0 + c) ^ (lane & 7)) << 4)));
+                    if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+                    const uint32_t a = sA + s * kAStage;
+#pragma unroll
+                    for (int h = 0; h < kEW / 16; ++h) {
+                        uint32_t y[4][4];
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc) {
+                            const int c = 16 * h + 4 * cc;
+                            tr4(x[c], x[c + 1], x[c + 2], x[c + 3], y[0][cc], y[1][cc], y[2][cc], y[3][cc]);
+                        }
+                        const uint32_t chunk = (((kEW / 16) * warp + h) ^ (lane & 7)) << 4;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a + (j * 32 + lane) * BKB + chunk),
+                                         "r"(y[j][0]), "r"(y[j][1]), "r"(y[j][2]), "r"(y[j][3])
+                                         : "memory");
+                    }
+                    mbar_arrive(rempty0 + 8 * r);  // window stage consumed (values are in registers)
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive(full0 + 8 * s);
+                    continue;
+                }
                 issue();
                 if (RS == 3) cp_wait<2>();  // the stage issued RS - 1 groups ago has landed
                 else cp_wait<1>();
                 if (P.dense_vec) __syncwarp();  // rows were copied by other lanes of this warp
                 const uint32_t s = f % S, round = f / S;
                 const uint32_t raw = rawrow + (f % RS) * kRawStage;
-                uint32_t x[32];
+                uint32_t x[kEW];
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < kEW / 4; ++c)
                     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                                  : "=r"(x[4 * c]), "=r"(x[4 * c + 1]), "=r"(x[4 * c + 2]), "=r"(x[4 * c + 3])
                                  : "r"(raw + 16 * c));
                 if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
                 const uint32_t a = sA + s * kAStage;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < kEW / 16; ++h) {
                     uint32_t y[4][4];
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
                         const int c = 16 * h + 4 * cc;
                         tr4(x[c], x[c + 1], x[c + 2], x[c + 3], y[0][cc], y[1][cc], y[2][cc], y[3][cc]);
                     }
-                    const uint32_t chunk = ((2 * warp + h) ^ (lane & 7)) << 4;
+                    const uint32_t chunk = (((kEW / 16) * warp + h) ^ (lane & 7)) << 4;
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a + (j * 32 + lane) * BKB + chunk),
@@ -369,44 +467,108 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(full0 + 8 * s);
             }
         }
-        cp_wait<0>();
-    } else if (warp < 8) {
-        // ---------------- epilogue: warp 4 + j reads TMEM lanes [32j, 32j + 32) = digit j.
+        if (!P.a_tma) cp_wait<0>();
+    } else if (warp < kEpi0 + kEpiW) {
+        // ---------------- epilogue: warp kEpi0 + j reads TMEM lanes [32j, 32j + 32) = digit j.
         // Digits of four adjacent columns are packed into one staging word
         // (plane j); after the barrier each thread transposes four planes'
         // words (4x4 bytes) into the output words of four columns.
-        const uint32_t j = warp - 4;
+        const uint32_t e = warp - kEpi0, j = e & 3, hf = e >> 2;
+        // columns of this warp: all BN (4 warps, or BN = 16), else half of them
+        const uint32_t CW = (kEpiW == 4 || BN < 32) ? BN : BN / 2, cbeg = (kEpiW == 4 || BN < 32) ? 0 : hf * CW;
+        const bool cols = kEpiW == 4 || BN >= 32 || hf == 0;
         uint32_t n = 0;  // tiles done by this CTA
+        // the column tile's z / bias residues are staged in shared memory one
+        // tile ahead (cp.async by the first epilogue warp, double-buffered)
+        auto zb_fetch = [&](uint32_t t, uint32_t slot) {
+            if (e != 0) return;
+            if (t < P.tiles && 16 * lane < (P.garbler ? 2 * BN : BN)) {  // the evaluator has no bias residues
+                const TileId tn = tile_of(P, t);
+                const uint8_t* src = lane * 16 < BN ? P.L[tn.li].zt + tn.nt * BN + 16 * lane
+                                                    : P.L[tn.li].bres + tn.nt * BN + 16 * lane - BN;
+                cp_async16(sZB + slot * 2 * BN + 16 * lane, src, true);
+            }
+            cp_commit();
+        };
+        zb_fetch(blockIdx.x, 0);
         for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++n) {
             const TileId ti = tile_of(P, t);
             const TcLane L = P.L[ti.li];  // by value: registers, not reloaded around the asm below
             const uint32_t buf = n & 1;
+            // this tile's first row tile: zero-wire / R_p words fetched before the accumulator wait
+            const Group G0 = group_of(P, L, ti.mt * SUB * GM + lane);
+            const uint32_t b0 = G0.bw / L.nw, w0 = G0.bw - b0 * L.nw;
+            const uint32_t zpre = __ldg(L.zero + (uint64_t)b0 * P.zstride + w0);
+            const uint32_t rpre = P.garbler ? __ldg(L.R + (uint64_t)b0 * P.zstride + w0) : 0u;
+            if (e == 0) cp_wait<0>();  // this tile's z / bias residues (visible after the bar.sync below)
             mbar_wait(tfull0 + 8 * buf, (n >> 1) & 1);
             tc_fence_after();
+            if (DASH_TC_DBG & 8) {
+                tc_fence_before();
+                mbar_arrive(tempty0 + 8 * buf);
+                continue;
+            }
             for (uint32_t sb = 0; sb < SUB; ++sb) {
             const Group G = group_of(P, L, (ti.mt * SUB + sb) * GM + lane);
             const uint32_t b = G.bw / L.nw, w = G.bw - b * L.nw;
-            const uint32_t zj = (__ldg(L.zero + (uint64_t)b * P.zstride + w) >> (8 * j)) & 0xffu;
-            const uint32_t rj = P.garbler ? (__ldg(L.R + (uint64_t)b * P.zstride + w) >> (8 * j)) & 0xffu : 0u;
+            const uint32_t zword = sb == 0 ? zpre : __ldg(L.zero + (uint64_t)b * P.zstride + w);
+            const uint32_t rword = sb == 0 ? rpre : P.garbler ? __ldg(L.R + (uint64_t)b * P.zstride + w) : 0u;
+            const uint32_t zj = (zword >> (8 * j)) & 0xffu, rj = (rword >> (8 * j)) & 0xffu;
             const bool live = 4 * w + j < L.n;  // digits beyond n_p stay zero
+            const uint32_t zr = zj | (rj << 16);  // dp2a operand (zero_j, R_j)
             const uint32_t p = L.p, mag = L.mag, sh = L.sh;
             const uint32_t c31 = modp(0x7fffffffu, p, mag, sh) + 1u;  // == 2^31 mod p (up to one p)
-            const uint8_t* ztp = L.zt + ti.nt * BN;    // padded to whole column tiles on the host
-            const uint8_t* brp = L.bres + ti.nt * BN;
+            const uint32_t zbs = sZB + buf * 2 * BN;  // [z residues of the BN columns | bias residues]
             const uint32_t plane = sStg + j * (BN / 4) * 32 * 4;
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // staging free (previous tile stored)
-            for (uint32_t cc = 0; cc < BN / 16; ++cc) {
-                uint32_t v[16];
-                tmem_ld16(tmem + buf * tcols + sb * BN + ((j * 32) << 16) + cc * 16, v);
-                const uint4 zv = __ldg(reinterpret_cast<const uint4*>(ztp + cc * 16));
-                const uint4 bv = P.garbler ? __ldg(reinterpret_cast<const uint4*>(brp + cc * 16)) : make_uint4(0, 0, 0, 0);
-                const uint32_t zw4[4] = {zv.x, zv.y, zv.z, zv.w}, bw4[4] = {bv.x, bv.y, bv.z, bv.w};
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiW) : "memory");  // staging free (previous tile stored)
+            if (sb == 0) zb_fetch(t + gridDim.x, buf ^ 1);  // the other buffer's tile is done
+            // 32 accumulator columns per TMEM round trip (two x16 loads, one wait)
+            for (uint32_t c0 = cbeg; cols && c0 < cbeg + CW; c0 += 32) {
+                uint32_t v2[32];
+                const uint32_t taddr = tmem + buf * tcols + sb * BN + ((j * 32) << 16) + c0;
+                const bool two = c0 + 16 < cbeg + CW;
+                if (two) {
+                    tmem_ld32(taddr, v2);
+                } else {
+                    uint32_t v1[16];
+                    tmem_ld16(taddr, v1);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v2[i] = v1[i];
+                }
                 if (P.fold) {  // zero / bias terms are in the accumulator, which stays below 2^31
 #pragma unroll
-                    for (int g4 = 0; g4 < 4; ++g4) {
+                    for (int g4 = 0; g4 < 8; ++g4) {
+                        if (g4 >= 4 && !two) break;
                         uint32_t word = 0;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) word |= modp(v[4 * g4 + q], p, mag, sh) << (8 * q);
+                        for (int q = 0; q < 4; ++q) word |= modp(v2[4 * g4 + q], p, mag, sh) << (8 * q);
+                        if (!live) word = 0;
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + ((c0 / 4 + g4) * 32 + lane) * 4), "r"(word));
+                    }
+                    continue;
+                }
+                for (uint32_t hh = 0; hh < (two ? 2u : 1u); ++hh) {
+                const uint32_t cc = (c0 + 16 * hh) / 16;
+                const uint32_t* v = v2 + 16 * hh;
+                uint4 zv, bv;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(zv.x), "=r"(zv.y), "=r"(zv.z), "=r"(zv.w) : "r"(zbs + cc * 16));
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(bv.x), "=r"(bv.y), "=r"(bv.z), "=r"(bv.w) : "r"(zbs + BN + cc * 16));
+                if (!P.garbler) bv = make_uint4(0, 0, 0, 0);
+                const uint32_t zw4[4] = {zv.x, zv.y, zv.z, zv.w}, bw4[4] = {bv.x, bv.y, bv.z, bv.w};
+                if (P.nowrap) {
+                    // acc + z_oc zero_j + (p - b_oc) R_j < 2^31: one reduction per digit; the
+                    // two column terms are one dp2a against (zero_j, R_j) (b_oc = 0 adds p R_j = 0 mod p)
+                    const uint32_t pp = p * 0x01010101u;
+#pragma unroll
+                    for (int g4 = 0; g4 < 4; ++g4) {
+                        const uint32_t nbw = pp - bw4[g4];
+                        const uint32_t lo = __byte_perm(zw4[g4], nbw, 0x5140), hi = __byte_perm(zw4[g4], nbw, 0x7362);
+                        uint32_t word = modp(__dp2a_lo(zr, lo, v[4 * g4]), p, mag, sh);
+                        word |= modp(__dp2a_hi(zr, lo, v[4 * g4 + 1]), p, mag, sh) << 8;
+                        word |= modp(__dp2a_lo(zr, hi, v[4 * g4 + 2]), p, mag, sh) << 16;
+                        word |= modp(__dp2a_hi(zr, hi, v[4 * g4 + 3]), p, mag, sh) << 24;
                         if (!live) word = 0;
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + ((cc * 4 + g4) * 32 + lane) * 4), "r"(word));
                     }
@@ -430,16 +592,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (!live) word = 0;
                     asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + ((cc * 4 + g4) * 32 + lane) * 4), "r"(word));
                 }
+                }
             }
             if (sb + 1 == SUB) {
                 tc_fence_before();
                 mbar_arrive(tempty0 + 8 * buf);  // accumulator drained: the MMA warp may reuse it
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiW) : "memory");
             if (G.ok) {
                 uint32_t* orow = L.out + (uint64_t)G.bw * P.M + G.pos;
                 const bool vec = P.P == 1 && (P.M & 3) == 0;
-                for (uint32_t c4 = j; c4 < BN / 4; c4 += 4) {  // columns 4 c4 .. 4 c4 + 3
+                for (uint32_t c4 = e; c4 < BN / 4; c4 += kEpiW) {  // columns 4 c4 .. 4 c4 + 3
                     const uint32_t oc = ti.nt * BN + 4 * c4;
                     if (oc >= P.nout) break;
                     uint32_t x0, x1, x2, x3, o0, o1, o2, o3;
@@ -463,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             }
         }
-    } else if (warp == 8 && lane == 0) {
+    } else if (warp == kMmaWarp && lane == 0) {
         // ---------------- MMA issue (one thread), two TMEM accumulators
         const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
         uint32_t f = 0, n = 0;
@@ -478,13 +641,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t a = sA + s * kAStage, bsm = sB + s * BN * BKB;
                 for (uint32_t sb = 0; sb < SUB; ++sb)
                     for (uint32_t kk = 0; kk < KS / 32; ++kk)
-                        mma_u8(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
+                        if (!(DASH_TC_DBG & 1)) mma_u8(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
                                (kb | kk) != 0);
                 mma_commit(empty0 + 8 * s);
             }
             mma_commit(tfull0 + 8 * buf);
         }
-    } else if (warp == 9 && lane == 0) {
+    } else if (warp == kTmaWarp && lane == 0) {
         // ---------------- weight tiles by TMA, S stages ahead of the MMAs
         uint32_t f = 0;
         for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
@@ -493,37 +656,65 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
                 const uint32_t s = f % S, round = f / S;
                 if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+                if (DASH_TC_DBG & 4) {
+                    mbar_arrive(full0 + 8 * s);
+                    continue;
+                }
                 mbar_expect_tx(full0 + 8 * s, BN * BKB);
                 tma_load_2d(sB + s * BN * BKB, &wmap, full0 + 8 * s, (int)(kb * BKB), (int)wrow);
+            }
+        }
+    } else if (warp == kRawWarp && lane == 0 && P.a_tma) {
+        // ---------------- window words by TMA, RS stages ahead of the producers:
+        // row groups [32 mt, 32 mt + 32) x window words [128 kb, 128 kb + 128)
+        // of the lane's plane, four 128-byte swizzled boxes per stage
+        uint32_t f = 0;
+        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
+            const TileId ti = tile_of(P, t);
+            const CUtensorMap* m = &rmaps.m[ti.li];
+            const int g0 = (int)(ti.mt * GM);
+            for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+                const uint32_t r = f % RS, round = f / RS;
+                if (f >= RS) mbar_wait(rempty0 + 8 * r, (round & 1) ^ 1);
+                mbar_expect_tx(rfull0 + 8 * r, kRawStageT);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    tma_load_2d(sRaw + r * kRawStageT + q * 4096, m, rfull0 + 8 * r, (int)(kb * 512 + q * 128), g0);
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tcols));
     }
 }
 
-// raw window ring depth (the producers' cp.async prefetch distance is RS - 1): 2 or 3
-inline uint32_t raw_stages() {
+// window ring depth: cp.async path 2 or 3 (DASH_TC_RS), TMA path 2..4 (DASH_TC_RST)
+inline uint32_t raw_stages(bool tma) {
     static const uint32_t rs = [] {
         const char* e = getenv("DASH_TC_RS");
         return (e && atoi(e) == 2) ? 2u : 3u;
     }();
-    return rs;
+    static const uint32_t rst = [] {
+        const char* e = getenv("DASH_TC_RST");
+        const int v = e ? atoi(e) : 3;
+        return (uint32_t)(v < 2 ? 2 : v > 4 ? 4 : v);
+    }();
+    return tma ? rst : rs;
 }
-inline uint32_t stages_for(uint32_t BN, uint32_t koff_bytes) {
-    const uint32_t fixed = 1024 + raw_stages() * kRawStage + BN * 32 * 4 + koff_bytes + 256;
+inline uint32_t raw_bytes(bool tma) { return raw_stages(tma) * (tma ? kRawStageT : kRawStage); }
+inline uint32_t stages_for(uint32_t BN, uint32_t koff_bytes, bool tma) {
+    const uint32_t fixed = 1024 + raw_bytes(tma) + BN * 32 * 4 + 4 * BN + koff_bytes + 256;
     const uint32_t per = kAStage + BN * BKB;
     uint32_t S = (225u * 1024u - fixed) / per;
     if (S > 8) S = 8;
     return S < 2 ? 2 : S;
 }
-inline size_t smem_bytes(uint32_t BN, uint32_t S, uint32_t koff_bytes) {
-    return 1024 + (size_t)S * (kAStage + BN * BKB) + raw_stages() * kRawStage + BN * 32 * 4 + koff_bytes +
-           8 * (2 * S + 4) + 16;
+inline size_t smem_bytes(uint32_t BN, uint32_t S, uint32_t koff_bytes, bool tma) {
+    return 1024 + (size_t)S * (kAStage + BN * BKB) + raw_bytes(tma) + BN * 32 * 4 + 4 * BN + koff_bytes +
+           8 * (2 * S + 4 + 2 * raw_stages(tma)) + 16;
 }
 
 }  // namespace tc
