@@ -50,7 +50,7 @@ constexpr int BKB = 128;       // K bytes (window elements) per stage: one 128-b
 // producers' load -> transpose -> store chain is the kernel's critical path,
 // so more of them in flight shortens a stage
 #ifndef DASH_TC_PROD
-#define DASH_TC_PROD 8
+#define DASH_TC_PROD 4
 #endif
 constexpr int kProd = DASH_TC_PROD;
 // timing experiments only (results are wrong): 1 = no MMAs, 2 = producers
@@ -215,6 +215,21 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Stage ring position: slot i, phase bit, and whether it wrapped once (the
+// slot then has to be released before reuse); no per-stage divisions
+struct Ring {
+    uint32_t i = 0, ph = 0, n;
+    bool warm = false;
+    __device__ explicit Ring(uint32_t n_) : n(n_) {}
+    __device__ void next() {
+        if (++i == n) {
+            i = 0;
+            ph ^= 1;
+            warm = true;
+        }
+    }
+};
+
 // tile t of the launch -> (lane li, row tile mt, column tile nt); column
 // tiles of one row tile are adjacent, so their window words come from L2
 struct TileId {
@@ -318,7 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // this warp's bytes [kEW warp, kEW warp + kEW) of a stage belong to row
         // tile st = kEW warp / KS, window offset ko0 = kEW warp mod KS
         const uint32_t st = (kEW * warp) / KS, ko0 = (kEW * warp) % KS;
-        uint32_t f_issue = 0, f = 0;  // flat stage counters over (tile, kb)
+        uint32_t f = 0;  // flat stage counter over (tile, kb)
+        Ring ri_(RS), rs_(S), rr_(RS);  // cp.async issue slot, A/B stage, window stage
         uint32_t it_tile = blockIdx.x, it_kb = 0;  // issue iterator
         Group ig;
         bool ig_valid = false;
@@ -340,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ig_w = ig.bw - ig_b * L.nw;
                     ig_valid = true;
                 }
-                const uint32_t slot = sRaw + (f_issue % RS) * kRawStage;
+                const uint32_t slot = sRaw + ri_.i * kRawStage;
                 const uint32_t i0 = it_kb * KS + ko0;
                 if (P.dense_vec) {
                     // coalesced: 8 lanes copy one row group's 128 contiguous
@@ -365,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 } else {
-                    const uint32_t dst = rawrow + (f_issue % RS) * kRawStage;
+                    const uint32_t dst = rawrow + ri_.i * kRawStage;
                     const uint32_t* zsrc = ig_zero + (uint64_t)ig_b * P.zstride + ig_w;
                     const uint32_t* rsrc = ig_R + (uint64_t)ig_b * P.zstride + ig_w;
                     const bool garb = P.garbler != 0;
@@ -387,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             cp_commit();
-            ++f_issue;
+            ri_.next();
         };
         if (!P.a_tma)
             for (uint32_t d = 0; d + 1 < RS; ++d) issue();
@@ -395,16 +411,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // each swizzled 512-byte row live in box q at 16-byte chunks c0 + c
         const uint32_t tb0 = 4 * kEW * warp, tq = tb0 / 128, tc0 = (tb0 % 128) / 16;
         for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
-            for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+            for (uint32_t kb = 0; kb < nk; ++kb, ++f, rs_.next(), rr_.next()) {
                 if (DASH_TC_DBG & 2) {
-                    const uint32_t s = f % S, round = f / S;
-                    if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+                    const uint32_t s = rs_.i;
+                    if (rs_.warm) mbar_wait(empty0 + 8 * s, rs_.ph ^ 1);
                     mbar_arrive(full0 + 8 * s);
                     continue;
                 }
                 if (P.a_tma) {
-                    const uint32_t r = f % RS, s = f % S, round = f / S;
-                    mbar_wait(rfull0 + 8 * r, (f / RS) & 1);
+                    const uint32_t r = rr_.i, s = rs_.i;
+                    mbar_wait(rfull0 + 8 * r, rr_.ph);
                     const uint32_t box = sRaw + r * kRawStageT + tq * 4096 + lane * 128;
                     uint32_t x[kEW];
 #pragma unroll
@@ -412,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                                      : "=r"(x[4 * c]), "=r"(x[4 * c + 1]), "=r"(x[4 * c + 2]), "=r"(x[4 * c + 3])
                                      : "r"(box + (((tc0 + c) ^ (lane & 7)) << 4)));
-                    if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+                    if (rs_.warm) mbar_wait(empty0 + 8 * s, rs_.ph ^ 1);
                     const uint32_t a = sA + s * kAStage;
 #pragma unroll
                     for (int h = 0; h < kEW / 16; ++h) {
@@ -438,15 +454,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (RS == 3) cp_wait<2>();  // the stage issued RS - 1 groups ago has landed
                 else cp_wait<1>();
                 if (P.dense_vec) __syncwarp();  // rows were copied by other lanes of this warp
-                const uint32_t s = f % S, round = f / S;
-                const uint32_t raw = rawrow + (f % RS) * kRawStage;
+                const uint32_t s = rs_.i;
+                const uint32_t raw = rawrow + rr_.i * kRawStage;
                 uint32_t x[kEW];
 #pragma unroll
                 for (int c = 0; c < kEW / 4; ++c)
                     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                                  : "=r"(x[4 * c]), "=r"(x[4 * c + 1]), "=r"(x[4 * c + 2]), "=r"(x[4 * c + 3])
                                  : "r"(raw + 16 * c));
-                if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+                if (rs_.warm) mbar_wait(empty0 + 8 * s, rs_.ph ^ 1);
                 const uint32_t a = sA + s * kAStage;
 #pragma unroll
                 for (int h = 0; h < kEW / 16; ++h) {
@@ -629,14 +645,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == kMmaWarp && lane == 0) {
         // ---------------- MMA issue (one thread), two TMEM accumulators
         const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-        uint32_t f = 0, n = 0;
+        uint32_t n = 0;
+        Ring ms_(S);
         for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++n) {
             const uint32_t buf = n & 1, d = tmem + buf * tcols;  // row tile sb at columns sb * BN
             if (n >= 2) mbar_wait(tempty0 + 8 * buf, ((n >> 1) & 1) ^ 1);
             tc_fence_after();
-            for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
-                const uint32_t s = f % S, round = f / S;
-                mbar_wait(full0 + 8 * s, round & 1);
+            for (uint32_t kb = 0; kb < nk; ++kb, ms_.next()) {
+                const uint32_t s = ms_.i;
+                mbar_wait(full0 + 8 * s, ms_.ph);
                 tc_fence_after();
                 const uint32_t a = sA + s * kAStage, bsm = sB + s * BN * BKB;
                 for (uint32_t sb = 0; sb < SUB; ++sb)
@@ -649,13 +666,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == kTmaWarp && lane == 0) {
         // ---------------- weight tiles by TMA, S stages ahead of the MMAs
-        uint32_t f = 0;
+        Ring ws_(S);
         for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
             const TileId ti = tile_of(P, t);
             const uint32_t wrow = P.L[ti.li].wrow + ti.nt * BN;
-            for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
-                const uint32_t s = f % S, round = f / S;
-                if (f >= S) mbar_wait(empty0 + 8 * s, (round & 1) ^ 1);
+            for (uint32_t kb = 0; kb < nk; ++kb, ws_.next()) {
+                const uint32_t s = ws_.i;
+                if (ws_.warm) mbar_wait(empty0 + 8 * s, ws_.ph ^ 1);
                 if (DASH_TC_DBG & 4) {
                     mbar_arrive(full0 + 8 * s);
                     continue;
@@ -668,14 +685,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- window words by TMA, RS stages ahead of the producers:
         // row groups [32 mt, 32 mt + 32) x window words [128 kb, 128 kb + 128)
         // of the lane's plane, four 128-byte swizzled boxes per stage
-        uint32_t f = 0;
+        Ring q_(RS);
         for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
             const TileId ti = tile_of(P, t);
             const CUtensorMap* m = &rmaps.m[ti.li];
             const int g0 = (int)(ti.mt * GM);
-            for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
-                const uint32_t r = f % RS, round = f / RS;
-                if (f >= RS) mbar_wait(rempty0 + 8 * r, (round & 1) ^ 1);
+            for (uint32_t kb = 0; kb < nk; ++kb, q_.next()) {
+                const uint32_t r = q_.i;
+                if (q_.warm) mbar_wait(rempty0 + 8 * r, q_.ph ^ 1);
                 mbar_expect_tx(rfull0 + 8 * r, kRawStageT);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
