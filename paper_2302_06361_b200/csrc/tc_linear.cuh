@@ -55,7 +55,8 @@ constexpr int BKB = 128;       // K bytes (window elements) per stage: one 128-b
 constexpr int kProd = DASH_TC_PROD;
 // timing experiments only (results are wrong): 1 = no MMAs, 2 = producers
 // skip the window copies and transposes, 4 = no weight TMA, 8 = no epilogue,
-// 16 = no window copies (transposes of stale data)
+// 16 = no window copies (transposes of stale data), 128 = no output stores,
+// 256 = no accumulator reduction
 #ifndef DASH_TC_DBG
 #define DASH_TC_DBG 0
 #endif
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sRaw = sB + S * BN * BKB;                // RS x [32 rows][132 words]
     const uint32_t rstage = P.a_tma ? kRawStageT : kRawStage;
     const uint32_t sStg = sRaw + RS * rstage;               // epilogue staging [BN][32] words
-    const uint32_t sZB = sStg + BN * 32 * 4;                // 2 x [z residues | bias residues] of a column tile
+    const uint32_t sZB = sStg + 4 * 32 * (BN / 4 + 1) * 4;  // 2 x [z residues | bias residues] of a column tile
     const uint32_t sKoff = sZB + 4 * BN;                    // window offset table (conv), kblocks x 128 ints
     const uint32_t koff_bytes = P.koff_smem ? P.kblocks * BKB * 4 : 0u;
     uint64_t* bars = (uint64_t*)(base + (sKoff - sA) + koff_bytes);
@@ -535,11 +536,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t p = L.p, mag = L.mag, sh = L.sh;
             const uint32_t c31 = modp(0x7fffffffu, p, mag, sh) + 1u;  // == 2^31 mod p (up to one p)
             const uint32_t zbs = sZB + buf * 2 * BN;  // [z residues of the BN columns | bias residues]
-            const uint32_t plane = sStg + j * (BN / 4) * 32 * 4;
+            // staging plane j: [32 row groups][BN / 4 + 1] words (odd row pitch: the
+            // reduction's per-row-group stores and the output phase's per-quad
+            // loads are both conflict-free)
+            const uint32_t QP = BN / 4 + 1, plane = sStg + j * 32 * QP * 4;
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiW) : "memory");  // staging free (previous tile stored)
             if (sb == 0) zb_fetch(t + gridDim.x, buf ^ 1);  // the other buffer's tile is done
             // 32 accumulator columns per TMEM round trip (two x16 loads, one wait)
-            for (uint32_t c0 = cbeg; cols && c0 < cbeg + CW; c0 += 32) {
+            for (uint32_t c0 = cbeg; cols && !(DASH_TC_DBG & 256) && c0 < cbeg + CW; c0 += 32) {
                 uint32_t v2[32];
                 const uint32_t taddr = tmem + buf * tcols + sb * BN + ((j * 32) << 16) + c0;
                 const bool two = c0 + 16 < cbeg + CW;
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) word |= modp(v2[4 * g4 + q], p, mag, sh) << (8 * q);
                         if (!live) word = 0;
-                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + ((c0 / 4 + g4) * 32 + lane) * 4), "r"(word));
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + c0 / 4 + g4) * 4), "r"(word));
                     }
                     continue;
                 }
@@ -586,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         word |= modp(__dp2a_lo(zr, hi, v[4 * g4 + 2]), p, mag, sh) << 16;
                         word |= modp(__dp2a_hi(zr, hi, v[4 * g4 + 3]), p, mag, sh) << 24;
                         if (!live) word = 0;
-                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + ((cc * 4 + g4) * 32 + lane) * 4), "r"(word));
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + cc * 4 + g4) * 4), "r"(word));
                     }
                     continue;
                 }
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         word |= modp(s0 + z * zj + nb * rj, p, mag, sh) << (8 * q);
                     }
                     if (!live) word = 0;
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + ((cc * 4 + g4) * 32 + lane) * 4), "r"(word));
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + cc * 4 + g4) * 4), "r"(word));
                 }
                 }
             }
@@ -615,14 +619,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(tempty0 + 8 * buf);  // accumulator drained: the MMA warp may reuse it
             }
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiW) : "memory");
-            if (G.ok) {
-                uint32_t* orow = L.out + (uint64_t)G.bw * P.M + G.pos;
-                const bool vec = P.P == 1 && (P.M & 3) == 0;
-                for (uint32_t c4 = e; c4 < BN / 4; c4 += kEpiW) {  // columns 4 c4 .. 4 c4 + 3
+            // output phase: warp e stores row groups [e R, e R + R), lane = column
+            // quad, so a warp writes 512 contiguous bytes of an output row
+            constexpr uint32_t RPW = 32 / kEpiW;
+            const bool vec = P.P == 1 && (P.M & 3) == 0;
+            for (uint32_t i = 0; i < RPW && !(DASH_TC_DBG & 128); ++i) {
+                const uint32_t r = e * RPW + i;
+                const Group Gr = group_of(P, L, (ti.mt * SUB + sb) * GM + r);
+                if (!Gr.ok) break;  // row groups past the lane's last one are all at the end
+                uint32_t* orow = L.out + (uint64_t)Gr.bw * P.M + Gr.pos;
+                for (uint32_t c4 = lane; c4 < BN / 4; c4 += 32) {  // columns 4 c4 .. 4 c4 + 3
                     const uint32_t oc = ti.nt * BN + 4 * c4;
                     if (oc >= P.nout) break;
                     uint32_t x0, x1, x2, x3, o0, o1, o2, o3;
-                    const uint32_t a = sStg + (c4 * 32 + lane) * 4, ps = (BN / 4) * 32 * 4;
+                    const uint32_t a = sStg + (r * QP + c4) * 4, ps = 32 * QP * 4;
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x0) : "r"(a));
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x1) : "r"(a + ps));
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x2) : "r"(a + 2 * ps));
@@ -721,16 +731,17 @@ inline uint32_t raw_stages(bool tma) {
     }();
     return tma ? rst : rs;
 }
+inline uint32_t stg_bytes(uint32_t BN) { return 4 * 32 * (BN / 4 + 1) * 4; }  // epilogue staging planes
 inline uint32_t raw_bytes(bool tma) { return raw_stages(tma) * (tma ? kRawStageT : kRawStage); }
 inline uint32_t stages_for(uint32_t BN, uint32_t koff_bytes, bool tma) {
-    const uint32_t fixed = 1024 + raw_bytes(tma) + BN * 32 * 4 + 4 * BN + koff_bytes + 256;
+    const uint32_t fixed = 1024 + raw_bytes(tma) + stg_bytes(BN) + 4 * BN + koff_bytes + 256;
     const uint32_t per = kAStage + BN * BKB;
     uint32_t S = (225u * 1024u - fixed) / per;
     if (S > 8) S = 8;
     return S < 2 ? 2 : S;
 }
 inline size_t smem_bytes(uint32_t BN, uint32_t S, uint32_t koff_bytes, bool tma) {
-    return 1024 + (size_t)S * (kAStage + BN * BKB) + raw_bytes(tma) + BN * 32 * 4 + 4 * BN + koff_bytes +
+    return 1024 + (size_t)S * (kAStage + BN * BKB) + raw_bytes(tma) + stg_bytes(BN) + 4 * BN + koff_bytes +
            8 * (2 * S + 4 + 2 * raw_stages(tma)) + 16;
 }
 
