@@ -389,6 +389,11 @@ def run_sweep(args):
                             "table_bytes": 16 * N * info.act_uc_cts,
                             "table_GBps": 16 * N * info.act_uc_cts / sec / 1e9, "chunk_elements": chunk,
                             "chunks": tm.sub_batches, "check": "decoded == ReLU(x) for every element",
+                            "roofline": {"bound": "hbm", "achieved": 16 * N * info.act_uc_cts / sec / 1e9,
+                                         "peak": measured_peaks()[0], "unit": "GB/s",
+                                         "frac": 16 * N * info.act_uc_cts / sec / 1e9 / measured_peaks()[0],
+                                         "note": "garbled-table bytes over the whole streamed layer; the gadget "
+                                                 "tape is integer-issue bound (AES + label codec)"},
                             "workload": "{input_shape={N}, layers={relu()}} (bench_main.cpp:156-162), garble + "
                                         "garble_inputs + evaluate + decode, streamed in element chunks"}
                 elif kind == "tproj":
@@ -467,6 +472,12 @@ def run_sweep(args):
                             "int8_ops_per_s_kernel": 4 * B * info.linear_macs / (lin_ms / 1e3) if lin_ms else None,
                             "linear_kernel_ms": lin_ms, "end_to_end_s": sec,
                             "label_macs_per_s_e2e": label_macs / sec}
+                    if lin_ms:
+                        _, _, i8, i8_src = measured_peaks()
+                        ach = 4 * B * info.linear_macs / (lin_ms / 1e3) / 1e12
+                        line["roofline"] = {"bound": "tensor", "achieved": ach, "peak": i8, "unit": "TOPS (int8)",
+                                            "frac": ach / i8, "peak_source": i8_src,
+                                            "kernel": "tc_linear_kernel (digit rows, tcgen05.mma kind::i8)"}
                 if rank == 0:
                     print(json.dumps(line), flush=True)
     if world > 1:
