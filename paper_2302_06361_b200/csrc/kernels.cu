@@ -519,7 +519,14 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     // dense window words by TMA: one row tile per stage, no fold columns
     // (the zero-wire / R_p words come from other arrays)
     P.a_tma = P.dense_vec && P.sub == 1 && !T.fold && std::getenv("DASH_TC_NOTMA") == nullptr;
-    P.stages = tc::stages_for(T.BN, koff_bytes, P.a_tma);
+    // CTA pairs (tcgen05.mma.cta_group::2, M = 256) on the TMA window path,
+    // opt-in (DASH_TC_CG=2): bit-exact, but measured at half the single-CTA
+    // throughput on the Dense 1024^2 sweep
+    uint64_t mt_total = 0;
+    for (int i = 0; i < n; ++i) mt_total += cdiv((uint64_t)Ls[i].B * Ls[i].nw * P.P, tc::GM);
+    const char* cge = std::getenv("DASH_TC_CG");
+    const uint32_t CG = (P.a_tma && T.BN >= 32 && mt_total >= 2 * (uint64_t)n && cge && std::atoi(cge) == 2) ? 2u : 1u;
+    P.stages = tc::stages_for(T.BN, koff_bytes, P.a_tma, CG);
     uint32_t tiles = 0;
     for (int i = 0; i < n; ++i) {
         const LinParams& L = Ls[i];
@@ -538,14 +545,16 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
         l.groups = L.B * L.nw * P.P;
         l.tile_base = tiles;
         l.wrow = (uint32_t)i * T.Npad;
-        tiles += cdiv(l.groups, tc::GM * P.sub) * P.tiles_n;
+        tiles += cdiv(cdiv(l.groups, tc::GM * P.sub), CG) * P.tiles_n;  // (pairs of) row tiles x column tiles
     }
     P.tiles = tiles;
     P.raw_stages = tc::raw_stages(P.a_tma);
-    const size_t smem = tc::smem_bytes(T.BN, P.stages, koff_bytes, P.a_tma);
-    smem_attr((const void*)tc::tc_linear_kernel, smem);
+    const size_t smem = tc::smem_bytes(T.BN, P.stages, koff_bytes, P.a_tma, CG);
     CUtensorMap map;
-    memcpy(&map, T.tmap, sizeof map);
+    if (CG == 2)  // each CTA of a pair loads half of the BN weight rows
+        encode_u8_2d(&map, T.wexp, T.Kpad, (uint64_t)T.k * T.Npad, T.Kpad, (uint32_t)tc::BKB, T.BN / 2);
+    else
+        memcpy(&map, T.tmap, sizeof map);
     tc::TcRawMaps rmaps;
     memset(&rmaps, 0, sizeof rmaps);
     if (P.a_tma)
@@ -555,8 +564,51 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     int sms = 0, dev = 0;
     ck(cudaGetDevice(&dev), "dev");
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
-    const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)sms);  // persistent: one CTA per SM
-    tc::tc_linear_kernel<<<grid, tc::kThreads, smem, S(st)>>>(map, P, rmaps);
+    if (CG == 2) {
+        // persistent CTA pairs: clusters of two, one CTA per SM
+        smem_attr((const void*)tc::tc_linear_kernel<2>, smem);
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof cfg);
+        // persistent: as many pairs as can be resident at once (a GPC with an
+        // odd SM count leaves one SM without a partner)
+        static int max_pairs = 0;
+        if (max_pairs == 0) {
+            cudaLaunchConfig_t q;
+            memset(&q, 0, sizeof q);
+            q.gridDim = dim3(sms);
+            q.blockDim = dim3(tc::kThreads);
+            q.dynamicSmemBytes = smem;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = 2;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, (const void*)tc::tc_linear_kernel<2>, &q) != cudaSuccess || nc <= 0)
+                nc = sms / 2;
+            max_pairs = nc;
+            if (std::getenv("DASH_TC_VERBOSE")) fprintf(stderr, "tc_linear: %d resident CTA pairs\n", nc);
+        }
+        const uint32_t pairs = std::min<uint32_t>(tiles, (uint32_t)max_pairs);
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(tc::kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = S(st);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        ck(cudaLaunchKernelEx(&cfg, tc::tc_linear_kernel<2>, map, P, rmaps), "tc_linear pair launch");
+    } else {
+        smem_attr((const void*)tc::tc_linear_kernel<1>, smem);
+        const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)sms);  // persistent: one CTA per SM
+        tc::tc_linear_kernel<1><<<grid, tc::kThreads, smem, S(st)>>>(map, P, rmaps);
+    }
     dev::check();
 }
 

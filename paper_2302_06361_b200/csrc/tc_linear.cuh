@@ -31,7 +31,7 @@
 // registers, mod p, + z*zero, - b*R, pack, store); one MMA warp whose lane 0
 // issues tcgen05.mma (M = 128, N = BN, K = 32 bytes per instruction) into two
 // TMEM accumulators; one warp streams weight tiles with TMA.  Stages are
-// tracked with mbarriers (full: 32 kProd producer arrivals + 1 TMA
+// tracked with mbarriers (full: one arrival per producer warp + 1 TMA
 // transaction; empty: tcgen05.commit).  One persistent CTA per SM.
 #pragma once
 
@@ -237,14 +237,73 @@ struct TileId {
     int li;
     uint32_t mt, nt;
 };
-__device__ __forceinline__ TileId tile_of(const TcParams& P, uint32_t t) {
+// With CTA pairs (CG = 2) a tile is a pair of row tiles: CTA rank c of the
+// pair takes row tile CG * (t / tiles_n) + c.
+__device__ __forceinline__ TileId tile_of(const TcParams& P, uint32_t t, uint32_t CG = 1, uint32_t crank = 0) {
     TileId r;
     r.li = 0;
     while (r.li + 1 < P.nl && t >= P.L[r.li + 1].tile_base) ++r.li;
     t -= P.L[r.li].tile_base;
-    r.mt = t / P.tiles_n;
-    r.nt = t - r.mt * P.tiles_n;
+    const uint32_t mp = t / P.tiles_n;
+    r.nt = t - mp * P.tiles_n;
+    r.mt = mp * CG + crank;
     return r;
+}
+
+// ---- CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    while (!mbar_try_cluster(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// weight half-tile of this CTA; completion is counted on the leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* map, uint32_t leader_bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(leader_bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mma_u8_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
 }
 
 // Row group g of lane L: (b, w, pos) -> first word of its window in the plane
@@ -267,6 +326,12 @@ __device__ __forceinline__ Group group_of(const TcParams& P, const TcLane& L, ui
 // Persistent, warp-specialized: CTA c takes tiles c, c + grid, ...; the
 // producers run ahead across tile boundaries, the MMA warp alternates two
 // TMEM accumulators so the epilogue of one tile overlaps the MMAs of the next.
+// CG = 2: CTA pairs (launched as clusters of two).  Each CTA builds its own
+// 128-row A tile and loads half of the BN weight rows; the leader (rank 0)
+// issues tcgen05.mma.cta_group::2 (M = 256) whose commits arrive on both
+// CTAs' barriers; producers, weight TMAs and epilogues of both CTAs report to
+// the leader's full / tempty barriers.
+template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_linear_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ TcParams P,
                      const __grid_constant__ TcRawMaps rmaps) {
@@ -277,10 +342,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // TMEM columns per accumulator: SUB row tiles x BN columns (power of two >= 32)
     uint32_t tcols = 32;
     while (tcols < SUB * BN) tcols <<= 1;
+    const uint32_t crank = CG == 2 ? cluster_rank() : 0u;
+    const bool leader = crank == 0;
+    const uint32_t t0 = blockIdx.x / CG, tstep = gridDim.x / CG;  // pair-tile schedule
+    const uint32_t BNc = BN / CG;                                 // weight rows held by this CTA
 
     const uint32_t sA = smem_u32(base);                     // S x [128 rows][128 B], swizzled
-    const uint32_t sB = sA + S * kAStage;                   // S x [BN rows][128 B], swizzled (TMA)
-    const uint32_t sRaw = sB + S * BN * BKB;                // RS x [32 rows][132 words]
+    const uint32_t sB = sA + S * kAStage;                   // S x [BN / CG rows][128 B], swizzled (TMA)
+    const uint32_t sRaw = sB + S * BNc * BKB;               // RS x [32 rows][132 words]
     const uint32_t rstage = P.a_tma ? kRawStageT : kRawStage;
     const uint32_t sStg = sRaw + RS * rstage;               // epilogue staging [BN][32] words
     const uint32_t sZB = sStg + 4 * 32 * (BN / 4 + 1) * 4;  // 2 x [z residues | bias residues] of a column tile
@@ -293,16 +362,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (tid == 0) {
         for (uint32_t s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, 32 * kProd + 1);  // producer arrivals + the weight TMA
+            mbar_init(full0 + 8 * s, CG * kProd + 1);  // one arrival per producer warp (both CTAs) + the weight TMA
             mbar_init(empty0 + 8 * s, 1);   // tcgen05.commit
         }
         for (uint32_t r = 0; r < RS; ++r) {
             mbar_init(rfull0 + 8 * r, 1);              // window TMA transaction
-            mbar_init(rempty0 + 8 * r, 32 * kProd);    // producers read the window stage
+            mbar_init(rempty0 + 8 * r, kProd);         // producer warps read the window stage
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(tfull0 + 8 * i, 1);     // last MMA of a tile committed
-            mbar_init(tempty0 + 8 * i, 32 * kEpiW);  // epilogue warps drained the accumulator
+            mbar_init(tempty0 + 8 * i, CG * kEpiW);  // epilogue warps (both CTAs) drained the accumulator
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
@@ -310,18 +379,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < P.nl; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"(&rmaps.m[i]) : "memory");
     }
     if (warp == kMmaWarp) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                     "r"(2 * tcols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                         "r"(2 * tcols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                         "r"(2 * tcols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     // the window offsets are read by every producer lane for every element:
     // shared memory, not L1 (which the streamed 4-byte window copies evict)
     for (uint32_t i = tid; i < koff_bytes / 4; i += kThreads)
         asm volatile("st.shared.s32 [%0], %1;" ::"r"(sKoff + 4 * i), "r"(__ldg(P.koff + i)) : "memory");
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();  // both CTAs' barriers initialized before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    // the leader's full / tempty barriers as seen from this CTA
+    const uint32_t full_l = CG == 2 ? mapa_shared(full0, 0) : full0, tempty_l = CG == 2 ? mapa_shared(tempty0, 0) : tempty0;
     const uint32_t nk = P.kblocks;
 
     if (warp < kProd) {
@@ -336,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t st = (kEW * warp) / KS, ko0 = (kEW * warp) % KS;
         uint32_t f = 0;  // flat stage counter over (tile, kb)
         Ring ri_(RS), rs_(S), rr_(RS);  // cp.async issue slot, A/B stage, window stage
-        uint32_t it_tile = blockIdx.x, it_kb = 0;  // issue iterator
+        uint32_t it_tile = t0, it_kb = 0;  // issue iterator
         Group ig;
         bool ig_valid = false;
         uint32_t ig_g0 = 0, ig_groups = 0, ig_nw = 1, ig_b = 0, ig_w = 0;
@@ -344,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue = [&]() {  // cp.async of the next stage (or an empty group)
             if (!(DASH_TC_DBG & 16) && it_tile < P.tiles) {
                 if (!ig_valid) {
-                    const TileId ti = tile_of(P, it_tile);
+                    const TileId ti = tile_of(P, it_tile, CG, crank);
                     const TcLane L = P.L[ti.li];
                     ig_g0 = (ti.mt * SUB + st) * GM;
                     ig = group_of(P, L, ig_g0 + lane);
@@ -399,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (++it_kb == nk) {
                     it_kb = 0;
-                    it_tile += gridDim.x;
+                    it_tile += tstep;
                     ig_valid = false;
                 }
             }
@@ -411,12 +489,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // TMA window path: this warp's bytes [4 kEW warp, 4 kEW (warp + 1)) of
         // each swizzled 512-byte row live in box q at 16-byte chunks c0 + c
         const uint32_t tb0 = 4 * kEW * warp, tq = tb0 / 128, tc0 = (tb0 % 128) / 16;
-        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
+        for (uint32_t t = t0; t < P.tiles; t += tstep) {
             for (uint32_t kb = 0; kb < nk; ++kb, ++f, rs_.next(), rr_.next()) {
                 if (DASH_TC_DBG & 2) {
                     const uint32_t s = rs_.i;
                     if (rs_.warm) mbar_wait(empty0 + 8 * s, rs_.ph ^ 1);
-                    mbar_arrive(full0 + 8 * s);
+                    if (lane == 0) {
+                        if (CG == 2) mbar_arrive_cluster(full_l + 8 * s);
+                        else mbar_arrive(full0 + 8 * s);
+                    }
                     continue;
                 }
                 if (P.a_tma) {
@@ -446,9 +527,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                          "r"(y[j][0]), "r"(y[j][1]), "r"(y[j][2]), "r"(y[j][3])
                                          : "memory");
                     }
-                    mbar_arrive(rempty0 + 8 * r);  // window stage consumed (values are in registers)
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_arrive(full0 + 8 * s);
+                    __syncwarp();  // the warp's reads and tile stores are done: one arrival per warp
+                    if (lane == 0) {
+                        mbar_arrive(rempty0 + 8 * r);  // window stage consumed (values are in registers)
+                        if (CG == 2) mbar_arrive_cluster(full_l + 8 * s);
+                        else mbar_arrive(full0 + 8 * s);
+                    }
                     continue;
                 }
                 issue();
@@ -481,7 +566,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : "memory");
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(full0 + 8 * s);
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster(full_l + 8 * s);
+                    else mbar_arrive(full0 + 8 * s);
+                }
             }
         }
         if (!P.a_tma) cp_wait<0>();
@@ -500,16 +589,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto zb_fetch = [&](uint32_t t, uint32_t slot) {
             if (e != 0) return;
             if (t < P.tiles && 16 * lane < (P.garbler ? 2 * BN : BN)) {  // the evaluator has no bias residues
-                const TileId tn = tile_of(P, t);
+                const TileId tn = tile_of(P, t, CG, crank);
                 const uint8_t* src = lane * 16 < BN ? P.L[tn.li].zt + tn.nt * BN + 16 * lane
                                                     : P.L[tn.li].bres + tn.nt * BN + 16 * lane - BN;
                 cp_async16(sZB + slot * 2 * BN + 16 * lane, src, true);
             }
             cp_commit();
         };
-        zb_fetch(blockIdx.x, 0);
-        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++n) {
-            const TileId ti = tile_of(P, t);
+        zb_fetch(t0, 0);
+        for (uint32_t t = t0; t < P.tiles; t += tstep, ++n) {
+            const TileId ti = tile_of(P, t, CG, crank);
             const TcLane L = P.L[ti.li];  // by value: registers, not reloaded around the asm below
             const uint32_t buf = n & 1;
             // this tile's first row tile: zero-wire / R_p words fetched before the accumulator wait
@@ -522,7 +611,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (DASH_TC_DBG & 8) {
                 tc_fence_before();
-                mbar_arrive(tempty0 + 8 * buf);
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster(tempty_l + 8 * buf);
+                    else mbar_arrive(tempty0 + 8 * buf);
+                }
                 continue;
             }
             for (uint32_t sb = 0; sb < SUB; ++sb) {
@@ -541,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // loads are both conflict-free)
             const uint32_t QP = BN / 4 + 1, plane = sStg + j * 32 * QP * 4;
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiW) : "memory");  // staging free (previous tile stored)
-            if (sb == 0) zb_fetch(t + gridDim.x, buf ^ 1);  // the other buffer's tile is done
+            if (sb == 0) zb_fetch(t + tstep, buf ^ 1);  // the other buffer's tile is done
             // 32 accumulator columns per TMEM round trip (two x16 loads, one wait)
             for (uint32_t c0 = cbeg; cols && !(DASH_TC_DBG & 256) && c0 < cbeg + CW; c0 += 32) {
                 uint32_t v2[32];
@@ -616,7 +709,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (sb + 1 == SUB) {
                 tc_fence_before();
-                mbar_arrive(tempty0 + 8 * buf);  // accumulator drained: the MMA warp may reuse it
+                __syncwarp();  // the warp's TMEM reads are done: one arrival per warp
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster(tempty_l + 8 * buf);  // accumulator drained: the MMA warp may reuse it
+                    else mbar_arrive(tempty0 + 8 * buf);
+                }
             }
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiW) : "memory");
             // output phase: warp e stores row groups [e R, e R + R), lane = column
@@ -654,35 +751,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == kMmaWarp && lane == 0) {
         // ---------------- MMA issue (one thread), two TMEM accumulators
-        const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+        // M = 128 (one CTA) or 256 (CTA pair: the peer's A tile and weight half
+        // sit at the same shared-memory offsets)
+        const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)((CG * BM) >> 4) << 24);
         uint32_t n = 0;
         Ring ms_(S);
-        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++n) {
+        for (uint32_t t = t0; leader && t < P.tiles; t += tstep, ++n) {
             const uint32_t buf = n & 1, d = tmem + buf * tcols;  // row tile sb at columns sb * BN
-            if (n >= 2) mbar_wait(tempty0 + 8 * buf, ((n >> 1) & 1) ^ 1);
+            if (n >= 2) {
+                if (CG == 2) mbar_wait_cluster(tempty0 + 8 * buf, ((n >> 1) & 1) ^ 1);
+                else mbar_wait(tempty0 + 8 * buf, ((n >> 1) & 1) ^ 1);
+            }
             tc_fence_after();
             for (uint32_t kb = 0; kb < nk; ++kb, ms_.next()) {
                 const uint32_t s = ms_.i;
-                mbar_wait(full0 + 8 * s, ms_.ph);
+                if (CG == 2) mbar_wait_cluster(full0 + 8 * s, ms_.ph);
+                else mbar_wait(full0 + 8 * s, ms_.ph);
                 tc_fence_after();
-                const uint32_t a = sA + s * kAStage, bsm = sB + s * BN * BKB;
+                const uint32_t a = sA + s * kAStage, bsm = sB + s * BNc * BKB;
                 for (uint32_t sb = 0; sb < SUB; ++sb)
-                    for (uint32_t kk = 0; kk < KS / 32; ++kk)
-                        if (!(DASH_TC_DBG & 1)) mma_u8(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
-                               (kb | kk) != 0);
-                mma_commit(empty0 + 8 * s);
+                    for (uint32_t kk = 0; kk < KS / 32; ++kk) {
+                        if (DASH_TC_DBG & 1) continue;
+                        if (CG == 2)
+                            mma_u8_pair(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
+                                        (kb | kk) != 0);
+                        else
+                            mma_u8(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
+                                   (kb | kk) != 0);
+                    }
+                if (CG == 2) mma_commit_pair(empty0 + 8 * s);
+                else mma_commit(empty0 + 8 * s);
             }
-            mma_commit(tfull0 + 8 * buf);
+            if (CG == 2) mma_commit_pair(tfull0 + 8 * buf);
+            else mma_commit(tfull0 + 8 * buf);
         }
     } else if (warp == kTmaWarp && lane == 0) {
         // ---------------- weight tiles by TMA, S stages ahead of the MMAs
         Ring ws_(S);
-        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
-            const TileId ti = tile_of(P, t);
-            const uint32_t wrow = P.L[ti.li].wrow + ti.nt * BN;
+        for (uint32_t t = t0; t < P.tiles; t += tstep) {
+            const TileId ti = tile_of(P, t, CG, crank);
+            const uint32_t wrow = P.L[ti.li].wrow + ti.nt * BN + crank * BNc;  // this CTA's weight rows
             for (uint32_t kb = 0; kb < nk; ++kb, ws_.next()) {
                 const uint32_t s = ws_.i;
                 if (ws_.warm) mbar_wait(empty0 + 8 * s, ws_.ph ^ 1);
+                if (CG == 2) {
+                    // the leader expects both halves' bytes; each CTA's half completes on it
+                    if (leader) mbar_expect_tx(full0 + 8 * s, BN * BKB);
+                    tma_load_2d_pair(sB + s * BNc * BKB, &wmap, full_l + 8 * s, (int)(kb * BKB), (int)wrow);
+                    continue;
+                }
                 if (DASH_TC_DBG & 4) {
                     mbar_arrive(full0 + 8 * s);
                     continue;
@@ -696,8 +813,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // row groups [32 mt, 32 mt + 32) x window words [128 kb, 128 kb + 128)
         // of the lane's plane, four 128-byte swizzled boxes per stage
         Ring q_(RS);
-        for (uint32_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
-            const TileId ti = tile_of(P, t);
+        for (uint32_t t = t0; t < P.tiles; t += tstep) {
+            const TileId ti = tile_of(P, t, CG, crank);
             const CUtensorMap* m = &rmaps.m[ti.li];
             const int g0 = (int)(ti.mt * GM);
             for (uint32_t kb = 0; kb < nk; ++kb, q_.next()) {
@@ -711,10 +828,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();  // the peer's MMAs and remote arrivals are done
+    else __syncthreads();
     if (warp == kMmaWarp) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tcols));
+        if (CG == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tcols));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * tcols));
     }
 }
 
@@ -733,15 +852,15 @@ inline uint32_t raw_stages(bool tma) {
 }
 inline uint32_t stg_bytes(uint32_t BN) { return 4 * 32 * (BN / 4 + 1) * 4; }  // epilogue staging planes
 inline uint32_t raw_bytes(bool tma) { return raw_stages(tma) * (tma ? kRawStageT : kRawStage); }
-inline uint32_t stages_for(uint32_t BN, uint32_t koff_bytes, bool tma) {
+inline uint32_t stages_for(uint32_t BN, uint32_t koff_bytes, bool tma, uint32_t CG = 1) {
     const uint32_t fixed = 1024 + raw_bytes(tma) + stg_bytes(BN) + 4 * BN + koff_bytes + 256;
-    const uint32_t per = kAStage + BN * BKB;
+    const uint32_t per = kAStage + BN / CG * BKB;
     uint32_t S = (225u * 1024u - fixed) / per;
     if (S > 8) S = 8;
     return S < 2 ? 2 : S;
 }
-inline size_t smem_bytes(uint32_t BN, uint32_t S, uint32_t koff_bytes, bool tma) {
-    return 1024 + (size_t)S * (kAStage + BN * BKB) + raw_bytes(tma) + stg_bytes(BN) + 4 * BN + koff_bytes +
+inline size_t smem_bytes(uint32_t BN, uint32_t S, uint32_t koff_bytes, bool tma, uint32_t CG = 1) {
+    return 1024 + (size_t)S * (kAStage + BN / CG * BKB) + raw_bytes(tma) + stg_bytes(BN) + 4 * BN + koff_bytes +
            8 * (2 * S + 4 + 2 * raw_stages(tma)) + 16;
 }
 

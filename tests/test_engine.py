@@ -327,6 +327,15 @@ def test_tensor_core_linear_vs_oracle(eng, oracle, kind):
         assert out[i].tolist() == g.plain_forward(x[i]).tolist()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["wide", "ntiles", "deep"])
+def test_tensor_core_linear_cta_pairs_vs_oracle(gpu, oracle, monkeypatch, kind):
+    # the opt-in CTA-pair digit-row kernel (tcgen05.mma.cta_group::2, M = 256,
+    # each CTA holding half of the weight tile) gives the same bytes
+    monkeypatch.setenv("DASH_TC_CG", "2")
+    test_tensor_core_linear_vs_oracle(gpu, oracle, kind)
+
+
 # ------------------------------------------------------- streamed sweep layers
 
 @pytest.mark.parametrize("name,k,chunk", [("relu3000", 4, 1024), ("sign777", 5, 100), ("relu300", 8, 300)])
