@@ -884,6 +884,22 @@ DASH_HD void rows_batched(const uint32_t* p, uint64_t stride, int nw, F&& f) {
     }
 }
 
+// Power-of-two labels: a word of four byte digits (each < 2^e) <-> the
+// 4e-bit field of the packed form (digit j at bit e j)
+DASH_HD uint32_t pack_digits(uint32_t x, uint32_t e) {
+    if (e == 1) return ((x & 0x01010101u) * 0x10204080u) >> 28;  // bit 8j -> bit 28 + j, no carries
+    return (x & 0xffu) | (((x >> 8) & 0xffu) << e) | (((x >> 16) & 0xffu) << (2 * e)) | ((x >> 24) << (3 * e));
+}
+DASH_HD uint32_t unpack_digits(uint32_t c, uint32_t e, uint32_t mask) {
+    if (e == 1) return ((c & 0xfu) * 0x00204081u) & 0x01010101u;  // bit j -> bit 8j
+    return (c & mask) | (((c >> e) & mask) << 8) | (((c >> (2 * e)) & mask) << 16) | (((c >> (3 * e)) & mask) << 24);
+}
+// byte mask of the digits of word w that exist (i < n)
+DASH_HD uint32_t live_bytes(int w, const ModC& M) {
+    const int left = M.n - 4 * w;
+    return left >= 4 ? 0xffffffffu : (1u << (8 * left)) - 1u;
+}
+
 template <int NB = kRowBatch>
 DASH_HD void lb_load_rows(LB L, const uint32_t* p, uint64_t stride, const ModC& M) {
     if (!M.pow2) {
@@ -893,14 +909,9 @@ DASH_HD void lb_load_rows(LB L, const uint32_t* p, uint64_t stride, const ModC& 
     U4 acc;
     acc.x[0] = acc.x[1] = acc.x[2] = acc.x[3] = 0;
     rows_batched<NB>(p, stride, M.nw, [&](int w, uint32_t x) {
-        for (int j = 0; j < 4; ++j) {
-            const int i = 4 * w + j;
-            if (i < M.n) {
-                const uint32_t d = (x >> (8 * j)) & 0xffu;
-                u4_or_shl(acc, d, (uint32_t)(M.e * i));
-            }
-        }
+        u4_or_shl(acc, pack_digits(x & live_bytes(w, M), M.e), (uint32_t)(4 * M.e * w));
     });
+    for (int i = 0; i < 4; ++i) acc.x[i] &= M.bits[i];
     lb_set_u4(L, acc);
 }
 
@@ -911,14 +922,8 @@ DASH_HD void lb_store_rows(LB L, uint32_t* p, uint64_t stride, const ModC& M) {
     }
     const U4 v = lb_u4(L);
     const uint32_t mask = M.m - 1u;
-    for (int w = 0; w < M.nw; ++w) {
-        uint32_t x = 0;
-        for (int j = 0; j < 4; ++j) {
-            const int i = 4 * w + j;
-            if (i < M.n) x |= (u4_shr_low(v, (uint32_t)(M.e * i)) & mask) << (8 * j);
-        }
-        p[(uint64_t)w * stride] = x;
-    }
+    for (int w = 0; w < M.nw; ++w)
+        p[(uint64_t)w * stride] = unpack_digits(u4_shr_low(v, (uint32_t)(4 * M.e * w)), M.e, mask) & live_bytes(w, M);
 }
 
 // LabelPrf::draw (prf.cpp:11-27): digit i = (u32 word i of
@@ -941,10 +946,12 @@ DASH_HD void lb_prf(LB L, uint64_t wire, uint32_t stream, const ModC& M, const u
                 if (4 * b + j < M.n) x |= mod32(o.x[j], M) << (8 * j);
             L[b] = x;
         } else {
-            for (int j = 0; j < 4; ++j) {
-                const int i = 4 * b + j;
-                if (i < M.n) u4_or_shl(acc, o.x[j] & mask, (uint32_t)(M.e * i));
-            }
+            // four e-bit digits (words of the block mod 2^e) -> one 4e-bit field;
+            // digits past n fall beyond bit 128 or under the final mask
+            const uint32_t e = M.e;
+            const uint32_t c = (o.x[0] & mask) | ((o.x[1] & mask) << e) | ((o.x[2] & mask) << (2 * e)) |
+                               ((o.x[3] & mask) << (3 * e));
+            u4_or_shl(acc, c, (uint32_t)(4 * e * b));
         }
     }
     if (M.pow2) {

@@ -8,7 +8,7 @@ for i, line in enumerate(open(fn_file), 1):
     if m: funcs.append((i, m.group(2)))
 starts = [f[0] for f in funcs]
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "--kernel-name", "regex:.",
-                      "--launch-skip", "0", "--launch-count", "1"], capture_output=True, text=True).stdout
+                      "--launch-skip", sys.argv[2] if len(sys.argv) > 2 else "0", "--launch-count", "1"], capture_output=True, text=True).stdout
 cur = None; hdr = None; agg = {}
 for r in csv.reader(io.StringIO(src)):
     if not r: continue
