@@ -478,6 +478,12 @@ def run_sweep(args):
                         line["roofline"] = {"bound": "tensor", "achieved": ach, "peak": i8, "unit": "TOPS (int8)",
                                             "frac": ach / i8, "peak_source": i8_src,
                                             "kernel": "tc_linear_kernel (digit rows, tcgen05.mma kind::i8)"}
+                        tp = os.path.join(ROOT, "profiles", "tc_dense_pipe.json")
+                        if os.path.exists(tp):  # ncu of the same kernel (k = 8, 4096 inferences, one pass)
+                            tj = json.load(open(tp))
+                            line["roofline"]["tensor_pipe_ncu"] = {
+                                key: tj.get(key) for key in ("tensor_pipe_active_pct", "imma_subpipe_inst_pct",
+                                                             "issue_active_pct", "source")}
                 if rank == 0:
                     print(json.dumps(line), flush=True)
     if world > 1:
