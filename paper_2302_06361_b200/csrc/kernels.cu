@@ -428,6 +428,9 @@ static void launch_linear_exp(const LinParams* Ls, int n, const TcLinear& T, voi
     P.E_in = L0.E_in;
     P.M = L0.M;
     P.stages = tcx::stages_for(T.BN);
+    P.nowrap = 1;  // the accumulator, z zero and (p - b) R sum below 2^31: no wrap handling
+    for (int i = 0; i < n; ++i)
+        if ((uint64_t)(L0.K + 3) * Ls[i].p * Ls[i].p >= (1ull << 31)) P.nowrap = 0;
     P.zstride = L0.zstride;
     P.garbler = L0.garbler;
     P.koff = T.koff;

@@ -71,6 +71,7 @@ struct TcParams {
     uint32_t P, OW, s, W, E_in, M, nout, tiles_n, BN, stages, zstride;
     int garbler;
     int a_tma;            // dense layer whose planes are TMA-able: A tiles by TMA, no gather
+    int nowrap;           // (K + 3) p^2 < 2^31 for every lane: acc + z zero + (p - b) R in one reduction
     const int32_t* koff;  // [kblocks * KWS] element offset of window index i, -1 = padding
 };
 
@@ -260,7 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // (layer.cpp:116-118); the s32 MMA accumulator wraps the
                     // same way, and the 31-bit-exact magic sees its low 31
                     // bits plus bit 31's residue (2^31 mod p, in [1, p])
-                    const uint32_t s0 = modp(v[g * 4 + j] & 0x7fffffffu, L.p, L.mag, L.sh) + (v[g * 4 + j] >> 31) * c31;
+                    const uint32_t s0 = P.nowrap ? v[g * 4 + j]
+                                                 : modp(v[g * 4 + j] & 0x7fffffffu, L.p, L.mag, L.sh) +
+                                                       (v[g * 4 + j] >> 31) * c31;
                     const uint32_t t1 = s0 + z * ((zw >> (8 * j)) & 0xffu) + nb * ((rw >> (8 * j)) & 0xffu);
                     o |= modp(t1, L.p, L.mag, L.sh) << (8 * j);
                 }
