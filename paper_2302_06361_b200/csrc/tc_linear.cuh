@@ -60,6 +60,7 @@ constexpr int kProd = DASH_TC_PROD;
 #ifndef DASH_TC_DBG
 #define DASH_TC_DBG 0
 #endif
+
 constexpr int kEW = BKB / kProd;                 // window elements (K bytes) per producer warp and stage
 // epilogue warps: 4 or 8 (-DDASH_TC_EPI=4); warp kEpi0 + e reads TMEM lane
 // quarter e mod 4 (its digit j) and column half e / 4 of the tile
@@ -493,6 +494,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (uint32_t kb = 0; kb < nk; ++kb, ++f, rs_.next(), rr_.next()) {
                 if (DASH_TC_DBG & 2) {
                     const uint32_t s = rs_.i;
+                    if (P.a_tma) {  // keep the window ring turning
+                        mbar_wait(rfull0 + 8 * rr_.i, rr_.ph);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(rempty0 + 8 * rr_.i);
+                    }
                     if (rs_.warm) mbar_wait(empty0 + 8 * s, rs_.ph ^ 1);
                     if (lane == 0) {
                         if (CG == 2) mbar_arrive_cluster(full_l + 8 * s);
