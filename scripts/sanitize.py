@@ -8,7 +8,7 @@ sys.path.insert(0, ROOT)
 from paper_2302_06361_b200.engine import Dash  # noqa: E402
 E = Dash(0)
 for name, B in [(a, int(b)) for a, b in (t.split(":") for t in (sys.argv[1:] or ["model_a:1", "model_tiny:3"]))]:
-    g = E.model(name, 1000, 8)
+    g = E.model(name, 0 if name == "dense1024" else 1000, 8)
     seeds = b"".join(int(0x5A00 + b).to_bytes(16, "big") for b in range(B))
     x = np.stack([g.random_input(10 + b, -3, 3) for b in range(B)])
     out, _ = E.infer(g, seeds, x)
