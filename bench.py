@@ -778,7 +778,11 @@ def run_ours(args, rank, world, local):
         cpu = None
         sample = args.cpu_sample or min(B, max(8, os.cpu_count() or 8))
         try:
-            cpu = None if args.no_cpu else cpu_baseline(reference_circuit(args.model, args.k), n_in, n_out, sample)
+            if world > 1:  # the CPU baseline is an N = 1 figure (taken on rank 0 of a 1-GPU run)
+                cpu = {"value": None, "unit": "inferences/s", "cores": os.cpu_count(), "kind": "skipped",
+                       "sample": "reported by the N = 1 run only"}
+            elif not args.no_cpu:
+                cpu = cpu_baseline(reference_circuit(args.model, args.k), n_in, n_out, sample)
         except (Exception, SystemExit) as e:  # the CPU baseline must not hide the GPU line
             cpu = {"value": None, "unit": "inferences/s", "cores": os.cpu_count(), "kind": "unavailable",
                    "sample": str(e)[:200]}
