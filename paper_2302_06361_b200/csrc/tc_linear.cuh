@@ -189,6 +189,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "memory");
 }
 
+// tcgen05.ld of 32 columns without the wait, and the wait as a data
+// dependency of those 32 registers (their uses cannot move above it)
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait32(uint32_t (&v)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                   "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                   "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                   "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+                 :
+                 : "memory");
+}
+
 __device__ __forceinline__ uint32_t modp(uint32_t x, uint32_t p, uint32_t mag, uint32_t sh) {
     return x - (__umulhi(x, mag) >> sh) * p;
 }
@@ -641,8 +664,50 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t QP = BN / 4 + 1, plane = sStg + j * 32 * QP * 4;
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiW) : "memory");  // staging free (previous tile stored)
             if (sb == 0) zb_fetch(t + tstep, buf ^ 1);  // the other buffer's tile is done
+            // no-wrap tiles of whole 64-column spans: the next 32-column TMEM
+            // load is in flight while this one is reduced (two register sets)
+            const bool fast = P.nowrap && !P.fold && cols && (CW % 64) == 0 && !(DASH_TC_DBG & 256);
+            auto reduce32 = [&](uint32_t (&v)[32], uint32_t c0) {
+                const uint32_t pp = p * 0x01010101u;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint32_t cc = c0 / 16 + hh;
+                    uint32_t zw4[4], bw4[4];
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(zw4[0]), "=r"(zw4[1]), "=r"(zw4[2]), "=r"(zw4[3]) : "r"(zbs + cc * 16));
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(bw4[0]), "=r"(bw4[1]), "=r"(bw4[2]), "=r"(bw4[3]) : "r"(zbs + BN + cc * 16));
+#pragma unroll
+                    for (int g4 = 0; g4 < 4; ++g4) {
+                        const uint32_t nbw = P.garbler ? pp - bw4[g4] : 0u;
+                        const uint32_t lo = __byte_perm(zw4[g4], nbw, 0x5140), hi = __byte_perm(zw4[g4], nbw, 0x7362);
+                        const uint32_t* x = v + 16 * hh + 4 * g4;
+                        uint32_t word = modp(__dp2a_lo(zr, lo, x[0]), p, mag, sh);
+                        word |= modp(__dp2a_hi(zr, lo, x[1]), p, mag, sh) << 8;
+                        word |= modp(__dp2a_lo(zr, hi, x[2]), p, mag, sh) << 16;
+                        word |= modp(__dp2a_hi(zr, hi, x[3]), p, mag, sh) << 24;
+                        if (!live) word = 0;
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + cc * 4 + g4) * 4), "r"(word));
+                    }
+                }
+            };
+            if (fast) {
+                const uint32_t tb = tmem + buf * tcols + sb * BN + ((j * 32) << 16);
+                uint32_t va[32], vb[32];
+                tmem_ld32_issue(tb + cbeg, va);
+                tmem_wait32(va);
+                for (uint32_t c0 = cbeg; c0 < cbeg + CW; c0 += 64) {
+                    const bool more = c0 + 64 < cbeg + CW;
+                    tmem_ld32_issue(tb + c0 + 32, vb);
+                    reduce32(va, c0);
+                    tmem_wait32(vb);
+                    if (more) tmem_ld32_issue(tb + c0 + 64, va);
+                    reduce32(vb, c0 + 32);
+                    if (more) tmem_wait32(va);
+                }
+            }
             // 32 accumulator columns per TMEM round trip (two x16 loads, one wait)
-            for (uint32_t c0 = cbeg; cols && !(DASH_TC_DBG & 256) && c0 < cbeg + CW; c0 += 32) {
+            for (uint32_t c0 = cbeg; !fast && cols && !(DASH_TC_DBG & 256) && c0 < cbeg + CW; c0 += 32) {
                 uint32_t v2[32];
                 const uint32_t taddr = tmem + buf * tcols + sb * BN + ((j * 32) << 16) + c0;
                 const bool two = c0 + 16 < cbeg + CW;
