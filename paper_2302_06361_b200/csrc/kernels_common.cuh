@@ -24,7 +24,10 @@ namespace dashgpu {
 #define DASH_GARBLE_WARPS 28
 #endif
 constexpr int kActWarpsGarble = DASH_GARBLE_WARPS;
-constexpr int kActWarpsEval = 24;
+#ifndef DASH_EVAL_WARPS
+#define DASH_EVAL_WARPS 24
+#endif
+constexpr int kActWarpsEval = DASH_EVAL_WARPS;
 constexpr int kTWords = 256 * 32;
 
 inline void ck(cudaError_t e, const char* what) {
