@@ -108,15 +108,12 @@ __global__ void __launch_bounds__(kPrivWarps * 32, 1) private_kernel(const __gri
     const AesTab t = make_tab(nullptr, lane);
     const ModC& M = c_mod[P.p];
     const uint32_t p = P.p, total = P.B * P.M;
-    const uint32_t* Rp = G ? P.mult + ((uint64_t)c_modslot[p] * 128u + 1) * NWMAX : nullptr;
     uint32_t item = warp * gridDim.x + blockIdx.x;
     const uint32_t first = kPrivWarps * gridDim.x;
     while (item < total) {
         const uint32_t b = item / P.M, u = item - b * P.M;
         const uint32_t* rk = P.rk + (uint64_t)b * 44;
         const uint32_t* mult = P.mult + (uint64_t)b * P.mult_stride;
-        const uint32_t* Rb = G ? mult + ((uint64_t)c_modslot[p] * 128u + 1) * NWMAX : nullptr;
-        (void)Rp;
         uint32_t oc = 0, oy = 0, ox = 0;
         if (P.conv) {
             oc = u / (P.OH * P.OW);
@@ -143,17 +140,11 @@ __global__ void __launch_bounds__(kPrivWarps * 32, 1) private_kernel(const __gri
                 U4* R = P.blob + (uint64_t)b * P.blob_stride + ((uint64_t)u * P.win + j) * p;
                 const uint32_t c = lb_color(X, M);
                 if (G) {
-                    lb_prf(T, P.wire_base + (uint64_t)u * P.win + j, 0, M, rk, t);
-                    const uint32_t wv = wr[j];
-                    const uint32_t* mrow = mult + (uint64_t)c_modslot[p] * 128u * NWMAX;
-                    uint32_t row = c, v = 0;  // row (c + a) mod p carries payload (w a mod p) R_p
-                    for (uint32_t a = 0; a < p; ++a) {
-                        const U4 H = hash_tw(lb_key_step(X, Rb, M), g, row, 0, t);
-                        R[row] = lb_enc(H, T, mrow + (uint64_t)v * NWMAX, nullptr, 0, M);
-                        row = row + 1 == p ? 0 : row + 1;
-                        v += wv;
-                        v = v >= p ? v - p : v;
-                    }
+                    // fresh output label, then the projection x -> w x mod p: row
+                    // (c + a) mod p carries payload (w a mod p) R_p -- the act
+                    // kernels' single-copy row loop (garble_rows_n, phi = nullptr)
+                    prf_n(T, P.wire_base + (uint64_t)u * P.win + j, 0, p, rk, t);
+                    garble_rows_n(X, T, t, mult, p, p, c, g, nullptr, wr[j], R, 0, 1);
                 } else {
                     lb_dec(T, R[c], hash_tw(lb_compress(X, M), g, c, 0, t), M);
                 }
