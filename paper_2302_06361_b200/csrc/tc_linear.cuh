@@ -56,7 +56,7 @@ constexpr int kProd = DASH_TC_PROD;
 // timing experiments only (results are wrong): 1 = no MMAs, 2 = producers
 // skip the window copies and transposes, 4 = no weight TMA, 8 = no epilogue,
 // 16 = no window copies (transposes of stale data), 128 = no output stores,
-// 256 = no accumulator reduction
+// 256 = no accumulator reduction, 512 = no window TMA (with 2)
 #ifndef DASH_TC_DBG
 #define DASH_TC_DBG 0
 #endif
@@ -162,6 +162,24 @@ __device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t a, uint64_t b, 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
+// Warp-wide forms: the whole (converged) MMA warp runs the issue loop with
+// warp-uniform operands, one elected lane executes the instruction, so the
+// operands stay in uniform registers (no per-issue election loop).
+__device__ __forceinline__ void mma_u8_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_w(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -214,6 +232,12 @@ __device__ __forceinline__ void tmem_wait32(uint32_t (&v)[32]) {
 
 __device__ __forceinline__ uint32_t modp(uint32_t x, uint32_t p, uint32_t mag, uint32_t sh) {
     return x - (__umulhi(x, mag) >> sh) * p;
+}
+// x mod p with negp = -p: q * negp + x as one multiply-add
+__device__ __forceinline__ uint32_t modpn(uint32_t x, uint32_t negp, uint32_t mag, uint32_t sh) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(__umulhi(x, mag) >> sh), "r"(negp), "r"(x));
+    return r;
 }
 
 // 4x4 byte transpose: x[c] holds digits (0..3) of window element c; y[j]
@@ -321,6 +345,22 @@ __device__ __forceinline__ void mma_u8_pair(uint32_t tmem_d, uint64_t a, uint64_
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_u8_pair_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair_w(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
 }
 // commit to the barrier at the same offset in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
@@ -517,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (uint32_t kb = 0; kb < nk; ++kb, ++f, rs_.next(), rr_.next()) {
                 if (DASH_TC_DBG & 2) {
                     const uint32_t s = rs_.i;
-                    if (P.a_tma) {  // keep the window ring turning
+                    if (P.a_tma && !(DASH_TC_DBG & 512)) {  // keep the window ring turning
                         mbar_wait(rfull0 + 8 * rr_.i, rr_.ph);
                         __syncwarp();
                         if (lane == 0) mbar_arrive(rempty0 + 8 * rr_.i);
@@ -655,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t zj = (zword >> (8 * j)) & 0xffu, rj = (rword >> (8 * j)) & 0xffu;
             const bool live = 4 * w + j < L.n;  // digits beyond n_p stay zero
             const uint32_t zr = zj | (rj << 16);  // dp2a operand (zero_j, R_j)
-            const uint32_t p = L.p, mag = L.mag, sh = L.sh;
+            const uint32_t p = L.p, mag = L.mag, sh = L.sh, negp = 0u - L.p;
             const uint32_t c31 = modp(0x7fffffffu, p, mag, sh) + 1u;  // == 2^31 mod p (up to one p)
             const uint32_t zbs = sZB + buf * 2 * BN;  // [z residues of the BN columns | bias residues]
             // staging plane j: [32 row groups][BN / 4 + 1] words (odd row pitch: the
@@ -682,10 +722,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t nbw = P.garbler ? pp - bw4[g4] : 0u;
                         const uint32_t lo = __byte_perm(zw4[g4], nbw, 0x5140), hi = __byte_perm(zw4[g4], nbw, 0x7362);
                         const uint32_t* x = v + 16 * hh + 4 * g4;
-                        uint32_t word = modp(__dp2a_lo(zr, lo, x[0]), p, mag, sh);
-                        word |= modp(__dp2a_hi(zr, lo, x[1]), p, mag, sh) << 8;
-                        word |= modp(__dp2a_lo(zr, hi, x[2]), p, mag, sh) << 16;
-                        word |= modp(__dp2a_hi(zr, hi, x[3]), p, mag, sh) << 24;
+                        uint32_t word = modpn(__dp2a_lo(zr, lo, x[0]), negp, mag, sh);
+                        word |= modpn(__dp2a_hi(zr, lo, x[1]), negp, mag, sh) << 8;
+                        word |= modpn(__dp2a_lo(zr, hi, x[2]), negp, mag, sh) << 16;
+                        word |= modpn(__dp2a_hi(zr, hi, x[3]), negp, mag, sh) << 24;
                         if (!live) word = 0;
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + cc * 4 + g4) * 4), "r"(word));
                     }
@@ -749,10 +789,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int g4 = 0; g4 < 4; ++g4) {
                         const uint32_t nbw = pp - bw4[g4];
                         const uint32_t lo = __byte_perm(zw4[g4], nbw, 0x5140), hi = __byte_perm(zw4[g4], nbw, 0x7362);
-                        uint32_t word = modp(__dp2a_lo(zr, lo, v[4 * g4]), p, mag, sh);
-                        word |= modp(__dp2a_hi(zr, lo, v[4 * g4 + 1]), p, mag, sh) << 8;
-                        word |= modp(__dp2a_lo(zr, hi, v[4 * g4 + 2]), p, mag, sh) << 16;
-                        word |= modp(__dp2a_hi(zr, hi, v[4 * g4 + 3]), p, mag, sh) << 24;
+                        uint32_t word = modpn(__dp2a_lo(zr, lo, v[4 * g4]), negp, mag, sh);
+                        word |= modpn(__dp2a_hi(zr, lo, v[4 * g4 + 1]), negp, mag, sh) << 8;
+                        word |= modpn(__dp2a_lo(zr, hi, v[4 * g4 + 2]), negp, mag, sh) << 16;
+                        word |= modpn(__dp2a_hi(zr, hi, v[4 * g4 + 3]), negp, mag, sh) << 24;
                         if (!live) word = 0;
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + cc * 4 + g4) * 4), "r"(word));
                     }
@@ -820,10 +860,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             }
         }
-    } else if (warp == kMmaWarp && lane == 0) {
+    } else if (warp == kMmaWarp) {
         // ---------------- MMA issue (one thread), two TMEM accumulators
-        // M = 128 (one CTA) or 256 (CTA pair: the peer's A tile and weight half
-        // sit at the same shared-memory offsets)
+        // the whole warp runs this loop (warp-uniform values), one elected lane
+        // issues each MMA / commit.  M = 128 (one CTA) or 256 (CTA pair: the
+        // peer's A tile and weight half sit at the same shared-memory offsets)
         const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)((CG * BM) >> 4) << 24);
         uint32_t n = 0;
         Ring ms_(S);
@@ -844,17 +885,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (uint32_t kk = 0; kk < KS / 32; ++kk) {
                         if (DASH_TC_DBG & 1) continue;
                         if (CG == 2)
-                            mma_u8_pair(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
+                            mma_u8_pair_w(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
                                         (kb | kk) != 0);
                         else
-                            mma_u8(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
+                            mma_u8_w(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
                                    (kb | kk) != 0);
                     }
-                if (CG == 2) mma_commit_pair(empty0 + 8 * s);
-                else mma_commit(empty0 + 8 * s);
+                if (CG == 2) mma_commit_pair_w(empty0 + 8 * s);
+                else mma_commit_w(empty0 + 8 * s);
             }
-            if (CG == 2) mma_commit_pair(tfull0 + 8 * buf);
-            else mma_commit(tfull0 + 8 * buf);
+            if (CG == 2) mma_commit_pair_w(tfull0 + 8 * buf);
+            else mma_commit_w(tfull0 + 8 * buf);
         }
     } else if (warp == kTmaWarp && lane == 0) {
         // ---------------- weight tiles by TMA, S stages ahead of the MMAs
@@ -879,7 +920,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d(sB + s * BN * BKB, &wmap, full0 + 8 * s, (int)(kb * BKB), (int)wrow);
             }
         }
-    } else if (warp == kRawWarp && lane == 0 && P.a_tma) {
+    } else if (warp == kRawWarp && lane == 0 && P.a_tma && !(DASH_TC_DBG & 512)) {
         // ---------------- window words by TMA, RS stages ahead of the producers:
         // row groups [32 mt, 32 mt + 32) x window words [128 kb, 128 kb + 128)
         // of the lane's plane, four 128-byte swizzled boxes per stage
