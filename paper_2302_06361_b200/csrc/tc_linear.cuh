@@ -234,6 +234,10 @@ __device__ __forceinline__ uint32_t modp(uint32_t x, uint32_t p, uint32_t mag, u
     return x - (__umulhi(x, mag) >> sh) * p;
 }
 // x mod p with negp = -p: q * negp + x as one multiply-add
+// bytes 0 of four values -> one word (three PRMT)
+__device__ __forceinline__ uint32_t pack4b(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    return __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
+}
 __device__ __forceinline__ uint32_t modpn(uint32_t x, uint32_t negp, uint32_t mag, uint32_t sh) {
     uint32_t r;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(__umulhi(x, mag) >> sh), "r"(negp), "r"(x));
@@ -722,10 +726,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t nbw = P.garbler ? pp - bw4[g4] : 0u;
                         const uint32_t lo = __byte_perm(zw4[g4], nbw, 0x5140), hi = __byte_perm(zw4[g4], nbw, 0x7362);
                         const uint32_t* x = v + 16 * hh + 4 * g4;
-                        uint32_t word = modpn(__dp2a_lo(zr, lo, x[0]), negp, mag, sh);
-                        word |= modpn(__dp2a_hi(zr, lo, x[1]), negp, mag, sh) << 8;
-                        word |= modpn(__dp2a_lo(zr, hi, x[2]), negp, mag, sh) << 16;
-                        word |= modpn(__dp2a_hi(zr, hi, x[3]), negp, mag, sh) << 24;
+                        uint32_t word = pack4b(modpn(__dp2a_lo(zr, lo, x[0]), negp, mag, sh),
+                                               modpn(__dp2a_hi(zr, lo, x[1]), negp, mag, sh),
+                                               modpn(__dp2a_lo(zr, hi, x[2]), negp, mag, sh),
+                                               modpn(__dp2a_hi(zr, hi, x[3]), negp, mag, sh));
                         if (!live) word = 0;
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + cc * 4 + g4) * 4), "r"(word));
                     }
@@ -789,10 +793,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int g4 = 0; g4 < 4; ++g4) {
                         const uint32_t nbw = pp - bw4[g4];
                         const uint32_t lo = __byte_perm(zw4[g4], nbw, 0x5140), hi = __byte_perm(zw4[g4], nbw, 0x7362);
-                        uint32_t word = modpn(__dp2a_lo(zr, lo, v[4 * g4]), negp, mag, sh);
-                        word |= modpn(__dp2a_hi(zr, lo, v[4 * g4 + 1]), negp, mag, sh) << 8;
-                        word |= modpn(__dp2a_lo(zr, hi, v[4 * g4 + 2]), negp, mag, sh) << 16;
-                        word |= modpn(__dp2a_hi(zr, hi, v[4 * g4 + 3]), negp, mag, sh) << 24;
+                        uint32_t word = pack4b(modpn(__dp2a_lo(zr, lo, v[4 * g4]), negp, mag, sh),
+                                               modpn(__dp2a_hi(zr, lo, v[4 * g4 + 1]), negp, mag, sh),
+                                               modpn(__dp2a_lo(zr, hi, v[4 * g4 + 2]), negp, mag, sh),
+                                               modpn(__dp2a_hi(zr, hi, v[4 * g4 + 3]), negp, mag, sh));
                         if (!live) word = 0;
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + cc * 4 + g4) * 4), "r"(word));
                     }
