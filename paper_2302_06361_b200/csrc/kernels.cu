@@ -498,9 +498,12 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
     P.koff = T.koff;
     P.dense_vec = !L0.conv && (L0.E_in % 4) == 0;
     P.fold = T.fold;
-    P.nowrap = 1;
-    for (int i = 0; i < n; ++i)
-        if ((uint64_t)(L0.K + 3) * Ls[i].p * Ls[i].p >= (1ull << 31)) P.nowrap = 0;  // acc + z zero + nb R
+    P.nowrap = 2;
+    for (int i = 0; i < n; ++i) {
+        const uint64_t p = Ls[i].p, bound = (uint64_t)(L0.K + 3) * p * p;  // acc + z zero + nb R
+        if (bound >= (1ull << 31)) P.nowrap = 0;
+        else if (bound * p >= (1ull << 32) && P.nowrap == 2) P.nowrap = 1;
+    }
     // small windows: SUB row tiles share one 128-byte K stage (TMEM: SUB * BN <= 256 columns per buffer)
     P.sub = 1;
     if (T.kblocks == 1) {
@@ -536,6 +539,7 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
         l.nw = L.nw;
         l.mag = L.mag;
         l.sh = L.sh;
+        l.mag0 = (uint32_t)((0xffffffffull + L.p) / L.p);  // ceil(2^32 / p)
         l.groups = L.B * L.nw * P.P;
         l.tile_base = tiles;
         l.wrow = (uint32_t)i * T.Npad;

@@ -38,6 +38,7 @@
 #include <cuda.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace dashgpu {
 namespace tc {
@@ -89,6 +90,7 @@ struct TcLane {
     const uint32_t* zero; // zero-wire label words, inference b at zero[b*zstride]
     const uint32_t* R;    // offset R_p words (garbler)
     uint32_t p, n, nw, mag, sh;
+    uint32_t mag0;        // ceil(2^32 / p): x mod p = x - umulhi(x, mag0) p for x < 2^32 / p
     uint32_t groups;      // B * nw * P row groups
     uint32_t tile_base;   // first tile of this lane
     uint32_t wrow;        // first row of this lane in the weight tensor
@@ -107,7 +109,8 @@ struct TcParams {
     uint32_t tiles;       // all tiles of the launch (persistent CTAs stride over them)
     int garbler;
     int fold;             // window columns K, K + 1 carry the zero-wire label / R_p (x z_oc, x (p - b_oc))
-    int nowrap;           // (K + 3) p^2 < 2^31 for every lane: acc + z zero + (p - b) R is one 31-bit reduction
+    int nowrap;           // (K + 3) p^2 < 2^31 for every lane: acc + z zero + (p - b) R is one 31-bit reduction;
+                          // 2: also (K + 3) p^3 < 2^32, the reduction needs no shift (TcLane::mag0)
     int dense_vec;        // dense layer, E_in % 4 == 0: window words loaded 4 at a time (16 B)
     int koff_smem;        // the offset table is copied to shared memory (all but huge windows)
     const int32_t* koff;  // [kblocks * BKB] element offset of window index i, -1 = padding
@@ -237,6 +240,12 @@ __device__ __forceinline__ uint32_t modp(uint32_t x, uint32_t p, uint32_t mag, u
 // bytes 0 of four values -> one word (three PRMT)
 __device__ __forceinline__ uint32_t pack4b(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
     return __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
+}
+// x mod p for x < 2^32 / p: q = umulhi(x, ceil(2^32 / p)) is exact, no shift
+__device__ __forceinline__ uint32_t modpn0(uint32_t x, uint32_t negp, uint32_t mag0) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(__umulhi(x, mag0)), "r"(negp), "r"(x));
+    return r;
 }
 __device__ __forceinline__ uint32_t modpn(uint32_t x, uint32_t negp, uint32_t mag, uint32_t sh) {
     uint32_t r;
@@ -711,8 +720,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             // no-wrap tiles of whole 64-column spans: the next 32-column TMEM
             // load is in flight while this one is reduced (two register sets)
             const bool fast = P.nowrap && !P.fold && cols && (CW % 64) == 0 && !(DASH_TC_DBG & 256);
-            auto reduce32 = [&](uint32_t (&v)[32], uint32_t c0) {
-                const uint32_t pp = p * 0x01010101u;
+            auto reduce32 = [&](auto NS, uint32_t (&v)[32], uint32_t c0) {
+                const uint32_t pp = p * 0x01010101u, m0 = L.mag0;
+                auto red = [&](uint32_t x) {
+                    return decltype(NS)::value ? modpn0(x, negp, m0) : modpn(x, negp, mag, sh);
+                };
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     const uint32_t cc = c0 / 16 + hh;
@@ -726,16 +738,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t nbw = P.garbler ? pp - bw4[g4] : 0u;
                         const uint32_t lo = __byte_perm(zw4[g4], nbw, 0x5140), hi = __byte_perm(zw4[g4], nbw, 0x7362);
                         const uint32_t* x = v + 16 * hh + 4 * g4;
-                        uint32_t word = pack4b(modpn(__dp2a_lo(zr, lo, x[0]), negp, mag, sh),
-                                               modpn(__dp2a_hi(zr, lo, x[1]), negp, mag, sh),
-                                               modpn(__dp2a_lo(zr, hi, x[2]), negp, mag, sh),
-                                               modpn(__dp2a_hi(zr, hi, x[3]), negp, mag, sh));
+                        uint32_t word = pack4b(red(__dp2a_lo(zr, lo, x[0])), red(__dp2a_hi(zr, lo, x[1])),
+                                               red(__dp2a_lo(zr, hi, x[2])), red(__dp2a_hi(zr, hi, x[3])));
                         if (!live) word = 0;
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(plane + (lane * QP + cc * 4 + g4) * 4), "r"(word));
                     }
                 }
             };
-            if (fast) {
+            auto run_fast = [&](auto NS) {
                 const uint32_t tb = tmem + buf * tcols + sb * BN + ((j * 32) << 16);
                 uint32_t va[32], vb[32];
                 tmem_ld32_issue(tb + cbeg, va);
@@ -743,12 +753,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (uint32_t c0 = cbeg; c0 < cbeg + CW; c0 += 64) {
                     const bool more = c0 + 64 < cbeg + CW;
                     tmem_ld32_issue(tb + c0 + 32, vb);
-                    reduce32(va, c0);
+                    reduce32(NS, va, c0);
                     tmem_wait32(vb);
                     if (more) tmem_ld32_issue(tb + c0 + 64, va);
-                    reduce32(vb, c0 + 32);
+                    reduce32(NS, vb, c0 + 32);
                     if (more) tmem_wait32(va);
                 }
+            };
+            if (fast) {
+                if (P.nowrap == 2) run_fast(std::true_type{});
+                else run_fast(std::false_type{});
             }
             // 32 accumulator columns per TMEM round trip (two x16 loads, one wait)
             for (uint32_t c0 = cbeg; !fast && cols && !(DASH_TC_DBG & 256) && c0 < cbeg + CW; c0 += 32) {
