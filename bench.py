@@ -478,6 +478,10 @@ def run_sweep(args):
                         line["roofline"] = {"bound": "tensor", "achieved": ach, "peak": i8, "unit": "TOPS (int8)",
                                             "frac": ach / i8, "peak_source": i8_src,
                                             "kernel": "tc_linear_kernel (digit rows, tcgen05.mma kind::i8)"}
+                        pk = json.load(open(os.path.join(ROOT, "profiles", "int8_peak.json"))).get("tcgen05_issue_peak")
+                        if pk:  # the tensor pipe's own ceiling (back-to-back MMAs), beside the cuBLASLt yardstick
+                            line["roofline"]["frac_of_mma_issue_peak"] = ach / pk["tops"]
+                            line["roofline"]["mma_issue_peak"] = pk["tops"]
                         tp = os.path.join(ROOT, "profiles", "tc_dense_pipe.json")
                         if os.path.exists(tp):  # ncu of the same kernel (k = 8, 4096 inferences, one pass)
                             tj = json.load(open(tp))
