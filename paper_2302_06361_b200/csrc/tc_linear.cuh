@@ -886,6 +886,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t idesc = (2u << 4) | ((BN >> 3) << 17) | ((uint32_t)((CG * BM) >> 4) << 24);
         uint32_t n = 0;
         Ring ms_(S);
+        const uint64_t dA0 = sw128_desc(sA), dB0 = sw128_desc(sB);
         for (uint32_t t = t0; leader && t < P.tiles; t += tstep, ++n) {
             const uint32_t buf = n & 1, d = tmem + buf * tcols;  // row tile sb at columns sb * BN
             if (n >= 2) {
@@ -898,16 +899,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (CG == 2) mbar_wait_cluster(full0 + 8 * s, ms_.ph);
                 else mbar_wait(full0 + 8 * s, ms_.ph);
                 tc_fence_after();
-                const uint32_t a = sA + s * kAStage, bsm = sB + s * BNc * BKB;
+                // descriptors advance in their 16-byte address field (shared
+                // addresses < 2^18: no carry out of the 14-bit field)
+                const uint64_t da = dA0 + ((s * kAStage) >> 4), db = dB0 + ((s * BNc * BKB) >> 4);
                 for (uint32_t sb = 0; sb < SUB; ++sb)
                     for (uint32_t kk = 0; kk < KS / 32; ++kk) {
                         if (DASH_TC_DBG & 1) continue;
-                        if (CG == 2)
-                            mma_u8_pair_w(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
-                                        (kb | kk) != 0);
-                        else
-                            mma_u8_w(d + sb * BN, sw128_desc(a + sb * KS + kk * 32), sw128_desc(bsm + kk * 32), idesc,
-                                   (kb | kk) != 0);
+                        const uint64_t dak = da + ((sb * KS + kk * 32) >> 4), dbk = db + ((kk * 32) >> 4);
+                        if (CG == 2) mma_u8_pair_w(d + sb * BN, dak, dbk, idesc, (kb | kk) != 0);
+                        else mma_u8_w(d + sb * BN, dak, dbk, idesc, (kb | kk) != 0);
                     }
                 if (CG == 2) mma_commit_pair_w(empty0 + 8 * s);
                 else mma_commit_w(empty0 + 8 * s);
