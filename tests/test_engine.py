@@ -785,6 +785,31 @@ def test_linear_accumulator_wraps_like_the_reference(gpu):
     assert K * 52 * 52 >= 1 << 32 and (1 << 31) <= K * 46 * 46 < 1 << 32
 
 
+@pytest.mark.gpu
+def test_linear_mid_window_reduction_paths(gpu):
+    """Digit-row epilogue reduction paths by window size (tc_linear.cuh,
+    TcParams::nowrap): K = 100,000 at k = 16 sums below 2^31 but not below
+    2^32 / p for p = 53 (the shifted 31-bit reduction), K = 4,096 below 2^32 / p
+    for every lane (the shift-free one).  Weights +-1 (no zero residues),
+    random input digits; the evaluator's lane is sum (w mod p) x mod p."""
+    from paper_2302_06361_b200.circuit import Circuit, dense
+
+    k = 16
+    for K in (100_000, 4_096):
+        assert (K + 3) * 53 * 53 < 1 << 31
+        rng = np.random.default_rng(K)
+        w = rng.choice([-1, 1], size=(2, K)).astype(np.int64)
+        c = Circuit([K], k, [dense(K, 2, w, np.zeros(2, np.int64))])
+        g = gpu.circuit(c)
+        net = gpu.network_setup(g, seed_hex(0xACD))
+        lanes = [rng.integers(0, p, size=(1, K, _ndig(p))).astype(np.uint16) for p in PRIMES[:k]]
+        out = gpu.layer_eval(net, 0, gpu.bundle_from_labels(net, lanes))
+        for i, p in enumerate(PRIMES[:k]):
+            want = ((w % p) @ lanes[i][0].astype(np.int64)) % p  # [2 units][n_p digits]
+            got = out.labels(i)[0]
+            assert (got == want).all(), (K, p)
+
+
 def _ndig(m):
     n, v = 0, 1
     while v * m <= 1 << 128:
