@@ -393,6 +393,12 @@ __device__ __forceinline__ Group group_of(const TcParams& P, const TcLane& L, ui
     Group r;
     r.ok = g < L.groups;
     const uint32_t gg = r.ok ? g : 0;
+    if (P.P == 1) {  // dense layers (every use of this kernel today): no divisions
+        r.bw = gg;
+        r.pos = 0;
+        r.src = L.in + (uint64_t)gg * P.E_in;
+        return r;
+    }
     r.bw = gg / P.P;
     r.pos = gg - r.bw * P.P;
     const uint32_t oy = r.pos / P.OW, ox = r.pos - oy * P.OW;
