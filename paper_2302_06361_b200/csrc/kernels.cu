@@ -540,12 +540,19 @@ void launch_linear(const LinParams* Ls, int n, const TcLinear& T, void* st) {
         l.mag = L.mag;
         l.sh = L.sh;
         l.mag0 = (uint32_t)((0xffffffffull + L.p) / L.p);  // ceil(2^32 / p)
+        if (L.nw < 2) throw std::runtime_error("tc_linear: lanes of fewer than 5 digits");
+        l.nw_mag = (uint32_t)(0xffffffffull / L.nw + 1);
+        if ((uint64_t)L.B * L.nw * P.P >= (1ull << 22))
+            throw std::runtime_error("tc_linear: too many row groups per lane for the reciprocal decode");
         l.groups = L.B * L.nw * P.P;
         l.tile_base = tiles;
         l.wrow = (uint32_t)i * T.Npad;
         tiles += cdiv(cdiv(l.groups, tc::GM * P.sub), CG) * P.tiles_n;  // (pairs of) row tiles x column tiles
     }
     P.tiles = tiles;
+    P.tn_mag = P.tiles_n > 1 ? (uint32_t)(0xffffffffull / P.tiles_n + 1) : 0u;
+    // umulhi(x, floor(2^32 / d) + 1) == x / d whenever x * d < 2^32
+    if (tiles >= (1u << 22) || P.tiles_n >= 1024) throw std::runtime_error("tc_linear: tile grid too large for the reciprocal decode");
     P.raw_stages = tc::raw_stages(P.a_tma);
     const size_t smem = tc::smem_bytes(T.BN, P.stages, koff_bytes, P.a_tma, CG);
     CUtensorMap map;

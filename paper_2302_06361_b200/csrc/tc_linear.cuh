@@ -91,6 +91,7 @@ struct TcLane {
     const uint32_t* R;    // offset R_p words (garbler)
     uint32_t p, n, nw, mag, sh;
     uint32_t mag0;        // ceil(2^32 / p): x mod p = x - umulhi(x, mag0) p for x < 2^32 / p
+    uint32_t nw_mag;      // floor(2^32 / nw) + 1: bw / nw = umulhi(bw, nw_mag) for bw < 2^22 (nw > 1: n_p >= 22)
     uint32_t groups;      // B * nw * P row groups
     uint32_t tile_base;   // first tile of this lane
     uint32_t wrow;        // first row of this lane in the weight tensor
@@ -107,6 +108,7 @@ struct TcParams {
     uint32_t sub;         // row tiles per stage (windows of <= 32 / 64 bytes share the 128-byte K stage)
     uint32_t ksub;        // K bytes per row tile within a stage (128 / sub)
     uint32_t tiles;       // all tiles of the launch (persistent CTAs stride over them)
+    uint32_t tn_mag;      // floor(2^32 / tiles_n) + 1: t / tiles_n = umulhi(t, tn_mag) for t < 2^22 (tiles_n > 1)
     int garbler;
     int fold;             // window columns K, K + 1 carry the zero-wire label / R_p (x z_oc, x (p - b_oc))
     int nowrap;           // (K + 3) p^2 < 2^31 for every lane: acc + z zero + (p - b) R is one 31-bit reduction;
@@ -305,7 +307,7 @@ __device__ __forceinline__ TileId tile_of(const TcParams& P, uint32_t t, uint32_
     r.li = 0;
     while (r.li + 1 < P.nl && t >= P.L[r.li + 1].tile_base) ++r.li;
     t -= P.L[r.li].tile_base;
-    const uint32_t mp = t / P.tiles_n;
+    const uint32_t mp = P.tiles_n == 1 ? t : __umulhi(t, P.tn_mag);  // t / tiles_n
     r.nt = t - mp * P.tiles_n;
     r.mt = mp * CG + crank;
     return r;
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ig_in = L.in;
                     ig_zero = L.zero;
                     ig_R = L.R;
-                    ig_b = ig.bw / L.nw;
+                    ig_b = __umulhi(ig.bw, L.nw_mag);  // bw / nw
                     ig_w = ig.bw - ig_b * L.nw;
                     ig_valid = true;
                 }
@@ -691,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t buf = n & 1;
             // this tile's first row tile: zero-wire / R_p words fetched before the accumulator wait
             const Group G0 = group_of(P, L, ti.mt * SUB * GM + lane);
-            const uint32_t b0 = G0.bw / L.nw, w0 = G0.bw - b0 * L.nw;
+            const uint32_t b0 = __umulhi(G0.bw, L.nw_mag), w0 = G0.bw - b0 * L.nw;
             const uint32_t zpre = __ldg(L.zero + (uint64_t)b0 * P.zstride + w0);
             const uint32_t rpre = P.garbler ? __ldg(L.R + (uint64_t)b0 * P.zstride + w0) : 0u;
             if (e == 0) cp_wait<0>();  // this tile's z / bias residues (visible after the bar.sync below)
@@ -708,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             for (uint32_t sb = 0; sb < SUB; ++sb) {
             const Group G = group_of(P, L, (ti.mt * SUB + sb) * GM + lane);
-            const uint32_t b = G.bw / L.nw, w = G.bw - b * L.nw;
+            const uint32_t b = __umulhi(G.bw, L.nw_mag), w = G.bw - b * L.nw;
             const uint32_t zword = sb == 0 ? zpre : __ldg(L.zero + (uint64_t)b * P.zstride + w);
             const uint32_t rword = sb == 0 ? rpre : P.garbler ? __ldg(L.R + (uint64_t)b * P.zstride + w) : 0u;
             const uint32_t zj = (zword >> (8 * j)) & 0xffu, rj = (rword >> (8 * j)) & 0xffu;
