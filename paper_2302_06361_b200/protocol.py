@@ -726,7 +726,7 @@ def run_local_protocol(eng: Dash, quantized: Circuit, inputs, owners: int = 1,
 
 # ---------------------------------------------------------------- TCP transport (protocol.cpp:437-614)
 
-_RECV_CHUNK = 16384
+_RECV_CHUNK = 1 << 20  # GC_TRANSFER frames are ~10^8 bytes
 
 
 def _send_frame(sock: socket.socket, f: Frame):
