@@ -737,11 +737,12 @@ def run_ours(args, rank, world, local):
         eng.profile(False)
 
     # ---- e2e: host buffers through the C ABI (dashgpu_infer) ----
-    h2d = d2h = 0
+    h2d = d2h = sub_batches = layerwise = 0
     with Timer() as te:
         for i in range(args.steps):
             out_host, tm = eng.infer(g, steps_seeds[args.warmup + i], host_x)
             h2d, d2h = tm.h2d_bytes, tm.d2h_bytes
+            sub_batches, layerwise = tm.sub_batches, tm.layerwise
             if world > 1:
                 dist.all_gather_into_tensor(gathered, torch.from_numpy(out_host).to(dev))
     e2e = world * B * args.steps / (te.ms / 1e3)
@@ -770,7 +771,9 @@ def run_ours(args, rank, world, local):
                                f"synthetic inputs U[-7,7], batch {B} per GPU, fresh seed per inference per step",
                    "global_batch": world * B, "inferences_per_gpu": B, "parallelism": f"inference-sharded x{world}",
                    "l2": "per-step garbled tables (%.1f GB) exceed L2; no flush needed" % (info.cts * 16 * B / 1e9),
-                   "ciphertexts_per_inference": info.cts, "relu_elements_per_inference": info.relu_elements},
+                   "ciphertexts_per_inference": info.cts, "relu_elements_per_inference": info.relu_elements,
+                   "sub_batches_per_step": int(sub_batches),
+                   "schedule": "layer-windowed" if layerwise else "whole GC per sub-batch"},
         "gather": {"collective": "all_gather of decoded outputs (int64) once per step",
                    "bytes_per_step": world * B * n_out * 8, "verified": bool(gather_ok)},
         "e2e": {"value": e2e, "unit": "inferences/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},

@@ -72,6 +72,7 @@ typedef struct dashgpu_timing {
     double ms_garble, ms_encode, ms_evaluate, ms_decode, ms_total;
     uint64_t h2d_bytes, d2h_bytes;
     uint32_t sub_batches;
+    uint32_t layerwise; /* dashgpu_infer: 1 = layer-windowed sub-batches */
 } dashgpu_timing;
 
 const char* dashgpu_last_error(void);
@@ -203,9 +204,21 @@ int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint
 /* ---- fused pipeline: garble + garble_inputs + evaluate + decode_outputs ----
  * inputs [batch][n_in], outputs [batch][n_out].  on_device=0: host buffers
  * (copies inside the call); on_device=1: device pointers (seeds too).
- * Sub-batches automatically when the garbled circuits exceed free HBM. */
+ * Sub-batches automatically when the garbled circuits exceed free HBM; such
+ * sub-batches are garbled and evaluated layer by layer through a one-layer
+ * ciphertext window when that admits more inferences per pass
+ * (t->layerwise; DASHGPU_LAYERWISE=0/1 forces the schedule). */
 int dashgpu_infer(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch,
                   const int64_t* inputs, int64_t* outputs, int on_device, dashgpu_timing* t);
+
+/* Digest parity mode of streamed whole-network garbling:
+ * garbles the batch layer by layer through a one-layer ciphertext window
+ * (no whole GC is held) and writes, per inference and layer, the tree
+ * SHA-256 of the layer's ciphertexts in GarbledCircuit::cts order
+ * (garble.hpp:46-53): SHA-256 over the SHA-256 digests of its 64 KiB leaves;
+ * a layer without ciphertexts gets SHA-256 of the empty string.
+ * seeds [batch][16] (host), digests [batch][n_layers][32] (host). */
+int dashgpu_garble_digest(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch, uint8_t* digests);
 
 /* Streamed inference of a single activation-layer circuit (the label-ops
  * sweep: {input_shape={N}, layers={relu()}}, reference bench_main.cpp:156-162,

@@ -4,6 +4,7 @@
 #pragma once
 
 #include "dash_device.cuh"
+#include "sha256.hpp"
 
 namespace dashgpu {
 
@@ -502,6 +503,35 @@ DASH_HD void rows_permute_thread(const RowsPermuteParams& P, uint64_t r) {
     const uint64_t d = blk * 32 * P.uc + j * w + (e & 31);
     if (P.to_ref) P.dst[r] = P.src[d];
     else P.dst[d] = P.src[r];
+}
+
+// Streamed-garbling digest mode (sha256.hpp): one 64 KiB leaf of one
+// inference's layer rows, read in reference order straight from the garbling
+// window (activation rows through the rows_permute mapping above).
+struct DigestParams {
+    const U4* src;    // window: inference b's rows at src + b * stride
+    uint64_t stride;  // rows per inference in the window
+    uint64_t rows;    // ciphertext rows of the layer per inference
+    uint64_t E, uc;   // activation layer (device row order); uc == 0: reference order
+    uint32_t B, leaves;
+    uint32_t* out;    // [B][leaves][8] SHA-256 state words
+};
+
+DASH_HD void digest_leaf_thread(const DigestParams& P, uint32_t b, uint32_t leaf) {
+    const U4* src = P.src + (uint64_t)b * P.stride;
+    const uint64_t r0 = (uint64_t)leaf * kDigestLeafRows;
+    const uint64_t n = P.rows - r0 < kDigestLeafRows ? P.rows - r0 : kDigestLeafRows;
+    auto row = [&](uint64_t i, uint32_t* w) {
+        uint64_t r = r0 + i;
+        if (P.uc) {
+            const uint64_t e = r / P.uc, j = r - e * P.uc;
+            const uint64_t blk = e >> 5, left = P.E - (blk << 5), wd = left < 32 ? left : 32;
+            r = blk * 32 * P.uc + j * wd + (e & 31);
+        }
+        const U4 v = src[r];
+        for (int t = 0; t < 4; ++t) w[t] = v.x[t];
+    };
+    sha256_rows(n, row, P.out + ((uint64_t)b * P.leaves + leaf) * 8);
 }
 
 }  // namespace dashgpu

@@ -1420,6 +1420,13 @@ struct Network {
     void require_gc() const {
         if (gc_released) throw DataError("garbled circuit already released (dashgpu_network_release_gc)");
     }
+    // Layer-windowed garbling (infer_layerwise, garble_digest_into): `blob`
+    // holds one layer's rows for the batch at a time, [B][layer cts], instead
+    // of whole GCs [B][total_cts]
+    bool windowed = false;
+    size_t act_flushed = 0;  // activation layers whose garbling launch is enqueued
+    U4* layer_blob(const HLayer& l) const { return blob.as<U4>() + (windowed ? 0 : l.ct_base); }
+    uint64_t layer_blob_stride(const HLayer& l) const { return windowed ? l.cts : c->total_cts; }
     size_t slot_used = 0;  // U4 entries of `slots` handed out to garbled layers
     size_t mm_used = 0;    // U4 entries of `mmlab` handed out to garbled layers
     uint64_t mult_stride = 0;
@@ -1578,8 +1585,8 @@ static void run_layer(Network& n, size_t li, const HLayer& l, bool garbler, cons
             P.B = n.B;
             P.gate_base = l.gate_base + l.lane_gate_off[i];
             P.wire_base = l.wire_base + l.lane_wire_off[i];
-            P.blob = n.blob.as<U4>() + l.ct_base + l.lane_ct_off[i];
-            P.blob_stride = c.total_cts;
+            P.blob = n.layer_blob(l) + l.lane_ct_off[i];
+            P.blob_stride = n.layer_blob_stride(l);
             P.rk = n.rk.as<uint32_t>();
             P.mult = n.mult.as<uint32_t>();
             P.mult_stride = n.mult_stride;
@@ -1605,8 +1612,8 @@ static void run_layer(Network& n, size_t li, const HLayer& l, bool garbler, cons
     P.uc_cts = l.tape->cts;
     P.uc_gates = l.tape->gates;
     P.uc_wires = l.tape->wires;
-    P.blob = n.blob.as<U4>() + l.ct_base;
-    P.blob_stride = c.total_cts;
+    P.blob = n.layer_blob(l);
+    P.blob_stride = n.layer_blob_stride(l);
     for (int i = 0; i < k; ++i) {
         P.out[i] = out.lane[i]->as<uint32_t>();
         P.out_kind[i] = l.tape->out_kind[i];
@@ -1644,9 +1651,17 @@ static void run_layer(Network& n, size_t li, const HLayer& l, bool garbler, cons
     launch_act_multi(dp, pin, 1, false, g_stream, n.sched());
 }
 
-static void network_reserve(Network& n, uint32_t B) {
+static uint64_t max_layer_cts(const dashgpu_circuit& c) {
+    uint64_t m = 0;
+    for (const auto& l : c.layers) m = std::max<uint64_t>(m, l.cts);
+    return m;
+}
+
+static void network_reserve(Network& n, uint32_t B, bool windowed = false) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
+    n.windowed = windowed;
+    n.blob.ensure((size_t)B * std::max<uint64_t>(windowed ? max_layer_cts(c) : c.total_cts, 1) * 16);
     if (B <= n.cap && n.cap) {
         n.B = B;
         return;
@@ -1660,7 +1675,6 @@ static void network_reserve(Network& n, uint32_t B) {
     n.zero.ensure((size_t)B * k * LABW * 4);
     n.Rb.ensure((size_t)B * k * LABW * 4);
     n.commit.ensure((size_t)B * 16);
-    n.blob.ensure((size_t)B * std::max<uint64_t>(c.total_cts, 1) * 16);
     n.sum_p = 0;
     for (int p : c.base.primes) n.sum_p += (uint32_t)p;
     n.dec.ensure((size_t)B * c.n_out * n.sum_p * 16);
@@ -1699,37 +1713,44 @@ static void network_reserve(Network& n, uint32_t B) {
 
 // All layers of the circuit in order (DAG inputs per layer, see
 // dash_circuit_desc.h); returns the final output planes.
-static const Lanes* run_layers(Network& n, bool garbler, const Lanes& input) {
-    dashgpu_circuit& c = *n.c;
+static void outs_begin(Network& n, bool garbler, const Lanes& input) {
     Network::Outs& O = garbler ? n.gouts : n.eouts;
-    const size_t L = c.layers.size();
+    const size_t L = n.c->layers.size();
     O.own.resize(L + 1);
     O.at.assign(L + 1, nullptr);
     O.at[0] = &input;
-    for (size_t li = 0; li < L; ++li) {
-        const HLayer& l = c.layers[li];
-        const Lanes* src = O.at[src_index(li, l.src)];
-        if (l.kind == DASH_LAYER_FLATTEN) {  // metadata-only reshape: planes are already flat
-            O.at[li + 1] = src;
-            continue;
-        }
-        if (!O.own[li + 1]) O.own[li + 1] = std::make_unique<Lanes>();
-        const Lanes* src2 = l.kind == DASH_LAYER_ADD ? O.at[src_index(li, l.src2)] : nullptr;
-        run_layer(n, li, l, garbler, *src, src2, *O.own[li + 1]);
-        O.at[li + 1] = O.own[li + 1].get();
+}
+
+static void run_layer_at(Network& n, bool garbler, size_t li) {
+    Network::Outs& O = garbler ? n.gouts : n.eouts;
+    const HLayer& l = n.c->layers[li];
+    const Lanes* src = O.at[src_index(li, l.src)];
+    if (l.kind == DASH_LAYER_FLATTEN) {  // metadata-only reshape: planes are already flat
+        O.at[li + 1] = src;
+        return;
     }
-    return O.at[L];
+    if (!O.own[li + 1]) O.own[li + 1] = std::make_unique<Lanes>();
+    const Lanes* src2 = l.kind == DASH_LAYER_ADD ? O.at[src_index(li, l.src2)] : nullptr;
+    run_layer(n, li, l, garbler, *src, src2, *O.own[li + 1]);
+    O.at[li + 1] = O.own[li + 1].get();
+}
+
+static const Lanes* run_layers(Network& n, bool garbler, const Lanes& input) {
+    outs_begin(n, garbler, input);
+    const size_t L = n.c->layers.size();
+    for (size_t li = 0; li < L; ++li) run_layer_at(n, garbler, li);
+    return (garbler ? n.gouts : n.eouts).at[L];
 }
 
 // garble (garble.cpp:134-240), batched: inference b uses seeds[b].
 // garble_setup: offsets, multiples, zero-wire / input base labels, seed
 // commitment (garble.cpp:134-204 before the layer loop).
-static void garble_setup(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device) {
+static void garble_setup(Network& n, const uint8_t* seeds, uint32_t B, bool seeds_on_device, bool windowed = false) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
     if (c.eval_only) throw DataError("circuit is an evaluator copy (private weights withheld): it cannot garble");
     upload_circuit(c);
-    network_reserve(n, B);
+    network_reserve(n, B, windowed);
     // seeds -> device, AES key schedules expanded on the device (no host
     // round trip when the seeds are already in HBM)
     if (seeds_on_device) {
@@ -1759,6 +1780,7 @@ static void garble_setup(Network& n, const uint8_t* seeds, uint32_t B, bool seed
     S.commit = n.commit.as<U4>();
     launch_setup(S, g_stream);
     n.act_host.clear();
+    n.act_flushed = 0;
     n.slot_used = 0;
     n.mm_used = 0;
 }
@@ -1785,9 +1807,17 @@ static void garble_dectables(Network& n, const Lanes& fin) {
 // the deferred combined garbling launch of the activation layers recorded in act_host
 static void garble_act_flush(Network& n) {
     if (n.act_host.empty()) return;
-    std::memcpy(n.act_pin.p, n.act_host.data(), n.act_host.size() * sizeof(ActParams));
-    dev::h2d(n.act_dev.p, n.act_pin.p, n.act_host.size() * sizeof(ActParams), g_stream);
-    launch_act_multi(n.act_dev.as<ActParams>(), n.act_host.data(), (int)n.act_host.size(), true, g_stream, n.sched());
+    // a layer-windowed garbling flushes once per activation layer: each flush
+    // stages its parameters in its own pinned / device slot, since the async
+    // copy of an earlier flush may not have run yet
+    const size_t at = n.act_flushed, cnt = n.act_host.size();
+    if (at + cnt > n.nact) throw std::logic_error("activation launch staging overflow");
+    ActParams* pin = n.act_pin.as<ActParams>() + at;
+    ActParams* dp = n.act_dev.as<ActParams>() + at;
+    std::memcpy(pin, n.act_host.data(), cnt * sizeof(ActParams));
+    dev::h2d(dp, pin, cnt * sizeof(ActParams), g_stream);
+    launch_act_multi(dp, n.act_host.data(), (int)cnt, true, g_stream, n.sched());
+    n.act_flushed += cnt;
     n.act_host.clear();
     n.slot_used = 0;
     n.mm_used = 0;
@@ -1848,6 +1878,18 @@ static void encode_into(Network& n, const int64_t* values, bool on_device, Bundl
     encode_finish(n);
 }
 
+// copies the last layer's evaluator planes into the output bundle
+static void eval_output(Network& n, const Lanes& cur, Bundle& out) {
+    dashgpu_circuit& c = *n.c;
+    out.net = &n;
+    out.B = n.B;
+    out.output = true;
+    out.lanes.ensure(c.base, n.B, c.n_out);
+    for (int i = 0; i < c.k; ++i)
+        dev::d2d(out.lanes.lane[i]->p, cur.lane[i]->p,
+                 (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_out * 4, g_stream);
+}
+
 // evaluate (garble.cpp:265-312)
 static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
     dashgpu_circuit& c = *n.c;
@@ -1857,14 +1899,83 @@ static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
     if (in.net != &n || in.B != n.B || in.output) throw DataError("garbled input bundle does not match the network");
     if (in.lanes.E != c.n_in || in.lanes.lane.size() != (size_t)k) throw DataError("garbled input shape mismatch");
     n.require_gc();
-    const Lanes* cur = run_layers(n, false, in.lanes);
-    out.net = &n;
-    out.B = n.B;
-    out.output = true;
-    out.lanes.ensure(c.base, n.B, c.n_out);
-    for (int i = 0; i < k; ++i)
-        dev::d2d(out.lanes.lane[i]->p, cur->lane[i]->p,
-                 (size_t)n.B * ((n_digits_host(c.base.primes[i]) + 3) / 4) * c.n_out * 4, g_stream);
+    eval_output(n, *run_layers(n, false, in.lanes), out);
+}
+
+// Layer-windowed inference ("tables are streamed per
+// layer chunk, not materialised whole"): layer li of the whole sub-batch is
+// garbled into the window, evaluated from it, and the window is reused for
+// li + 1.  Rows, labels and outputs are those of garble_into + evaluate_into
+// (same kernels, same ids; only the row addresses change), but a pass holds
+// B x (largest layer) ciphertexts instead of B x (whole GC), so batches whose
+// GCs exceed HBM run in fewer, larger sub-batches.  The GC is never whole:
+// the network cannot be exported afterwards.
+static void infer_layerwise(Network& n, const uint8_t* seeds, uint32_t B, bool on_device, const int64_t* inputs,
+                            Bundle& in, Bundle& out) {
+    dashgpu_circuit& c = *n.c;
+    garble_setup(n, seeds, B, on_device, true);
+    n.gc_released = false;
+    encode_enqueue(n, inputs, on_device, in);
+    outs_begin(n, true, n.base);
+    outs_begin(n, false, in.lanes);
+    const size_t L = c.layers.size();
+    for (size_t li = 0; li < L; ++li) {
+        run_layer_at(n, true, li);
+        garble_act_flush(n);
+        run_layer_at(n, false, li);
+    }
+    garble_dectables(n, *n.gouts.at[L]);
+    eval_output(n, *n.eouts.at[L], out);
+    n.gc_released = true;
+}
+
+// Digest parity mode: garbles layer by layer into the
+// window and reduces each layer's rows to the tree SHA-256 of sha256.hpp
+// (the leaves on the device, read in the reference's cts order; the root on
+// the host).  digests: [B][layers][32].  A layer's digest equals the one of
+// the same layer's bytes in dashgpu_export_gc, so whole-GC parity at sizes
+// that never fit HBM reduces to comparing 32 bytes per layer.
+static void garble_digest_into(Network& n, const uint8_t* seeds, uint32_t B, uint8_t* digests) {
+    dashgpu_circuit& c = *n.c;
+    garble_setup(n, seeds, B, false, true);
+    n.gc_released = false;
+    outs_begin(n, true, n.base);
+    const size_t L = c.layers.size();
+    DevBuf leaves;
+    std::vector<uint32_t> hl;
+    std::vector<uint8_t> cat;
+    for (size_t li = 0; li < L; ++li) {
+        run_layer_at(n, true, li);
+        garble_act_flush(n);
+        const HLayer& l = c.layers[li];
+        DigestParams P;
+        std::memset(&P, 0, sizeof P);
+        P.src = n.blob.as<U4>();
+        P.stride = l.cts;
+        P.rows = l.cts;
+        P.E = l.tape ? l.E_out : 0;
+        P.uc = l.tape ? l.tape->cts : 0;
+        P.B = B;
+        P.leaves = (uint32_t)((l.cts + kDigestLeafRows - 1) / kDigestLeafRows);
+        if (P.leaves) {
+            leaves.ensure((size_t)B * P.leaves * 32);
+            P.out = leaves.as<uint32_t>();
+            launch_digest(P, g_stream);
+            hl.resize((size_t)B * P.leaves * 8);
+            dev::d2h(hl.data(), leaves.p, hl.size() * 4, g_stream);
+            dev::sync(g_stream);
+        }
+        for (uint32_t b = 0; b < B; ++b) {
+            cat.resize((size_t)P.leaves * 32);
+            for (size_t w = 0; w < (size_t)P.leaves * 8; ++w) {
+                const uint32_t v = hl[(size_t)b * P.leaves * 8 + w];
+                for (int q = 0; q < 4; ++q) cat[4 * w + q] = (uint8_t)(v >> (24 - 8 * q));
+            }
+            sha256_bytes(cat.data(), cat.size(), digests + ((size_t)b * L + li) * 32);
+        }
+    }
+    dev::sync(g_stream);
+    n.gc_released = true;
 }
 
 
@@ -3306,6 +3417,43 @@ int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint
     });
 }
 
+// device bytes one inference of dashgpu_infer needs: ciphertexts (whole GC,
+// or its largest layer when layer-windowed) + multiples + planes of every
+// layer for garbler and evaluator + gadget slots + decode table
+static uint64_t per_inference_bytes(const dashgpu_circuit& c, bool windowed) {
+    uint64_t planes = 0;
+    {
+        uint64_t sumE = 3 * c.n_in + 2 * c.n_out;
+        for (const auto& l : c.layers)
+            if (l.kind != DASH_LAYER_FLATTEN) sumE += 2 * l.E_out;
+        for (int p : c.base.primes) planes += (uint64_t)((n_digits_host(p) + 3) / 4) * sumE * 4;
+    }
+    uint64_t slots = 0;
+    for (const auto& l : c.layers)
+        if (l.tape) slots += (uint64_t)l.tape->nslots * l.E_out * 16;
+    return (windowed ? max_layer_cts(c) : c.total_cts) * 16 + (uint64_t)(MAXMOD - 1) * 128 * NWMAX * 4 + planes +
+           slots + c.n_out * 600 * 16 + 4096;
+}
+
+int dashgpu_garble_digest(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batch, uint8_t* digests) {
+    return guarded([&] {
+        auto* c = const_cast<dashgpu_circuit*>(cc);
+        {
+            std::lock_guard<std::mutex> lk(c->mu);
+            upload_circuit(*c);
+        }
+        Network n;
+        n.c = c;
+        const uint64_t per = per_inference_bytes(*c, true);
+        const uint32_t chunk =
+            (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(batch, (uint64_t)(dev::free_bytes() * 0.85) / per));
+        for (uint32_t b0 = 0; b0 < batch; b0 += chunk) {
+            const uint32_t B = std::min(chunk, batch - b0);
+            garble_digest_into(n, seeds + (size_t)16 * b0, B, digests + (size_t)b0 * c->layers.size() * 32);
+        }
+    });
+}
+
 int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batch, const int64_t* inputs,
                   int64_t* outputs, int on_device, dashgpu_timing* t) {
     return guarded([&] {
@@ -3323,20 +3471,6 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
         std::lock_guard<std::mutex> lk(wsp->mu);
         using clk = std::chrono::steady_clock;
         const auto t0 = clk::now();
-        // per-inference device bytes: ciphertexts + multiples + decode table + planes
-        // per-layer output planes of garbler and evaluator + input planes
-        uint64_t planes = 0;
-        {
-            uint64_t sumE = 3 * c->n_in + 2 * c->n_out;
-            for (const auto& l : c->layers)
-                if (l.kind != DASH_LAYER_FLATTEN) sumE += 2 * l.E_out;
-            for (int p : c->base.primes) planes += (uint64_t)((n_digits_host(p) + 3) / 4) * sumE * 4;
-        }
-        uint64_t slots = 0;
-        for (const auto& l : c->layers)
-            if (l.tape) slots += (uint64_t)l.tape->nslots * l.E_out * 16;
-        const uint64_t per = c->total_cts * 16 + (uint64_t)(MAXMOD - 1) * 128 * NWMAX * 4 + planes + slots +
-                             c->n_out * 600 * 16 + 4096;
         auto make_ws = [&](std::unique_ptr<Network>& ws) {
             if (!ws) {
                 ws = std::make_unique<Network>();
@@ -3353,10 +3487,26 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
         // CTAs hold 196-218 KB of shared memory, so the other stream's
         // kernels cannot co-reside and the halves serialize.)
         Network& n = *make_ws(wsp->net);
+        // Whole GCs per sub-batch, or layer-windowed (infer_layerwise) when
+        // the batch's GCs exceed the HBM budget and a window admits a larger
+        // sub-batch; DASHGPU_LAYERWISE=0/1 forces either schedule.
+        const char* force = std::getenv("DASHGPU_LAYERWISE");
         uint32_t chunk = batch;
-        if (n.cap < batch) {
-            const uint64_t budget = (uint64_t)(dev::free_bytes() * 0.85) + (uint64_t)n.cap * per;
-            chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(batch, budget / per));
+        bool layerwise = n.windowed;
+        if (n.cap < batch || force) {
+            // (cudaMemGetInfo is only asked when the workspace must grow: it
+            // costs far more than the rest of the host side of a call)
+            const uint64_t per = per_inference_bytes(*c, false), per_w = per_inference_bytes(*c, true);
+            // free HBM plus what this workspace already holds (its last schedule)
+            const uint64_t avail =
+                (uint64_t)(dev::free_bytes() * 0.85) + (uint64_t)n.cap * (n.windowed ? per_w : per);
+            auto fit = [&](uint64_t p) {
+                return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(batch, avail / p));
+            };
+            chunk = fit(per);
+            layerwise = chunk < batch && fit(per_w) > chunk;
+            if (force) layerwise = force[0] == '1';
+            if (layerwise) chunk = fit(per_w);
         }
         Bundle& in = *n.bin;
         Bundle& out = *n.bout;
@@ -3366,9 +3516,13 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
             // are checked after the sync)
             const uint32_t B = std::min(chunk, batch - b0);
             const auto a = clk::now();
-            garble_into(n, seeds + (size_t)16 * b0, B, on_device != 0);
-            encode_enqueue(n, inputs + (size_t)b0 * c->n_in, on_device != 0, in);
-            evaluate_into(n, in, out);
+            if (layerwise) {
+                infer_layerwise(n, seeds + (size_t)16 * b0, B, on_device != 0, inputs + (size_t)b0 * c->n_in, in, out);
+            } else {
+                garble_into(n, seeds + (size_t)16 * b0, B, on_device != 0);
+                encode_enqueue(n, inputs + (size_t)b0 * c->n_in, on_device != 0, in);
+                evaluate_into(n, in, out);
+            }
             decode_enqueue(n, out, on_device ? outputs + (size_t)b0 * c->n_out : nullptr);
             dev::sync(g_stream);
             encode_finish(n);
@@ -3376,6 +3530,7 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
             tm.ms_garble += std::chrono::duration<double, std::milli>(clk::now() - a).count();
             tm.sub_batches += 1;
         }
+        tm.layerwise = layerwise ? 1 : 0;
         if (!on_device) {
             // seeds + quantized inputs in, decoded outputs out (AES key
             // schedules are expanded on the device, launch parameters are

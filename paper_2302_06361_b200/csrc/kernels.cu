@@ -267,6 +267,11 @@ __global__ void __launch_bounds__(256) rows_permute_kernel(RowsPermuteParams P) 
         rows_permute_thread(P, r);
 }
 
+__global__ void __launch_bounds__(128) digest_kernel(DigestParams P) {
+    const uint32_t leaf = blockIdx.x * blockDim.x + threadIdx.x;
+    if (leaf < P.leaves) digest_leaf_thread(P, blockIdx.y, leaf);
+}
+
 __global__ void __launch_bounds__(128) prim_kernel(PrimParams P) {
     fill_T(g_T0);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -719,6 +724,13 @@ void launch_rows_permute(const RowsPermuteParams& P, void* st) {
     if (!n) return;
     ProfScope ps(K_MISC, S(st));
     rows_permute_kernel<<<(uint32_t)std::min<uint64_t>(cdiv(n, 256), 148ull * 16), 256, 0, S(st)>>>(P);
+    dev::check();
+}
+
+void launch_digest(const DigestParams& P, void* st) {
+    if (!P.leaves || !P.B) return;
+    ProfScope ps(K_MISC, S(st));
+    digest_kernel<<<dim3(cdiv(P.leaves, 128), P.B), 128, 0, S(st)>>>(P);
     dev::check();
 }
 

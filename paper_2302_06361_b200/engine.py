@@ -94,6 +94,7 @@ class Timing(ctypes.Structure):
         ("h2d_bytes", ctypes.c_uint64),
         ("d2h_bytes", ctypes.c_uint64),
         ("sub_batches", ctypes.c_uint32),
+        ("layerwise", ctypes.c_uint32),
     ]
 
 
@@ -129,6 +130,7 @@ def _declare(L):
     L.dashgpu_network_circuit.argtypes = [vp, ctypes.POINTER(vp)]
     L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
     L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
+    L.dashgpu_garble_digest.argtypes = [vp, u8p, ctypes.c_uint32, u8p]
     L.dashgpu_infer_stream.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
     L.dashgpu_infer_stream_range.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, ctypes.c_uint64,
                                              ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
@@ -206,6 +208,19 @@ class Dash:
         buf = (ctypes.c_uint8 * len(seeds)).from_buffer_copy(seeds)
         self._check(self.lib.dashgpu_garble(c.h, buf, len(seeds) // 16, ctypes.byref(h)))
         return GarbledNetwork(self, h, c, len(seeds) // 16)
+
+    def garble_digest(self, c: "GpuCircuit", seeds: bytes) -> np.ndarray:
+        """Digest parity mode of streamed garbling: [batch][n_layers][32] tree
+        SHA-256 of each layer's ciphertexts in the reference's cts order,
+        garbled through a one-layer window (csrc/sha256.hpp)."""
+        if len(seeds) == 0 or len(seeds) % 16:
+            raise DataError("seeds must be a non-empty multiple of 16 bytes")
+        batch = len(seeds) // 16
+        buf = (ctypes.c_uint8 * len(seeds)).from_buffer_copy(seeds)
+        out = np.zeros((batch, c.info.n_layers, 32), np.uint8)
+        self._check(self.lib.dashgpu_garble_digest(c.h, buf, batch,
+                                                   out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+        return out
 
     def garble_inputs(self, net: "GarbledNetwork", values) -> "Bundle":
         v = np.ascontiguousarray(values, np.int64).reshape(net.batch, net.circuit.info.n_in)
