@@ -71,8 +71,9 @@ def seeds_for(step, rank, world, batch):
 class ClockSampler:
     """SM clocks and throttle reasons during the timed region.
 
-    NVML (pynvml) is polled every 2 ms from a thread, so even a timed region
-    of a few milliseconds (Model A batch 1) gets samples; nvidia-smi -lms 100
+    NVML (pynvml) is polled every 2 ms from a thread for the first 250
+    samples, so even a timed region of a few milliseconds (Model A batch 1)
+    gets samples, and every 20 ms after that; nvidia-smi -lms 100
     is the fallback when NVML is unavailable."""
 
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
@@ -124,7 +125,9 @@ class ClockSampler:
                 self.rows.append((float(sm), float(mx), {n for n, b in bits.items() if r & b}))
             except Exception:
                 pass
-            if self._stop.wait(0.002):
+            # 2 ms for the first ~0.5 s (short regions get samples), then 20 ms:
+            # NVML queries take driver locks the CUDA host calls also need
+            if self._stop.wait(0.002 if len(self.rows) < 250 else 0.02):
                 return
 
     def _read(self):

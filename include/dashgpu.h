@@ -220,6 +220,18 @@ int dashgpu_infer(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch
  * seeds [batch][16] (host), digests [batch][n_layers][32] (host). */
 int dashgpu_garble_digest(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch, uint8_t* digests);
 
+/* Streamed serialize_garbled_circuit (garble.cpp:347-403):
+ * garbles the batch layer by layer through a one-layer ciphertext window and
+ * calls sink(user, b, data, len) with inference b's GC bytes in order --
+ * header, every layer's rows in GarbledCircuit::cts order, commitment -- so
+ * the concatenation for each b equals dashgpu_export_gc(net, b) of a whole
+ * garbling, while the device never holds a whole GC.  A nonzero sink return
+ * aborts with DASHGPU_ERR_DATA.  *out (optional) receives the network with
+ * its encoding / decoding material, as after dashgpu_network_release_gc. */
+typedef int (*dashgpu_gc_sink)(void* user, uint32_t b, const uint8_t* data, size_t len);
+int dashgpu_garble_stream(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch, dashgpu_gc_sink sink,
+                          void* user, dashgpu_network** out);
+
 /* Streamed inference of a single activation-layer circuit (the label-ops
  * sweep: {input_shape={N}, layers={relu()}}, reference bench_main.cpp:156-162,
  * garble_layer/eval_layer layer.hpp:85-97 over element ranges).  Element

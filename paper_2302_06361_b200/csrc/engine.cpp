@@ -1425,6 +1425,9 @@ struct Network {
     // of whole GCs [B][total_cts]
     bool windowed = false;
     size_t act_flushed = 0;  // activation layers whose garbling launch is enqueued
+    // dashgpu_infer's last sub-batch plan (batch size -> sub-batch, schedule)
+    uint32_t plan_batch = 0, plan_chunk = 0;
+    bool plan_layerwise = false;
     U4* layer_blob(const HLayer& l) const { return blob.as<U4>() + (windowed ? 0 : l.ct_base); }
     uint64_t layer_blob_stride(const HLayer& l) const { return windowed ? l.cts : c->total_cts; }
     size_t slot_used = 0;  // U4 entries of `slots` handed out to garbled layers
@@ -1661,7 +1664,25 @@ static void network_reserve(Network& n, uint32_t B, bool windowed = false) {
     dashgpu_circuit& c = *n.c;
     const int k = c.k;
     n.windowed = windowed;
+    // ciphertexts, gadget slots and mixed-modulus labels: every layer's
+    // region at once, or (windowed) the largest layer's, reused layer by
+    // layer.  Sized before the early return: they depend on the schedule.
     n.blob.ensure((size_t)B * std::max<uint64_t>(windowed ? max_layer_cts(c) : c.total_cts, 1) * 16);
+    {
+        size_t slot_total = 0, slot_eval = 0, mm_total = 0;
+        for (const auto& l : c.layers)
+            if (l.tape) {
+                const size_t sl = (size_t)act_slots(*l.tape, act_lv_ok(*l.tape, (uint64_t)B * l.E_out)) * B * l.E_out;
+                const size_t mm = (size_t)B * l.E_out * k * 2;
+                slot_total = windowed ? std::max(slot_total, sl) : slot_total + sl;
+                mm_total = windowed ? std::max(mm_total, mm) : mm_total + mm;
+                // warp-per-element evaluation of a small layer uses the level tape's slots
+                if ((uint64_t)B * l.E_out <= dev::lane_group_eval_max())
+                    slot_eval = std::max(slot_eval, (size_t)l.tape->nslots_lv * B * l.E_out);
+            }
+        n.slots.ensure(std::max<size_t>(std::max(slot_total, slot_eval), 1) * 16);
+        n.mmlab.ensure(std::max<size_t>(mm_total, 1) * 16);
+    }
     if (B <= n.cap && n.cap) {
         n.B = B;
         return;
@@ -1682,20 +1703,9 @@ static void network_reserve(Network& n, uint32_t B, bool windowed = false) {
     n.resid.ensure((size_t)B * c.n_out * k);
     n.err.ensure(16);
     n.base.ensure(c.base, B, c.n_in);
-    size_t slot_total = 0, nact = 0, slot_eval = 0;
+    size_t nact = 0;
     for (const auto& l : c.layers)
-        if (l.tape) {
-            slot_total += (size_t)act_slots(*l.tape, act_lv_ok(*l.tape, (uint64_t)B * l.E_out)) * B * l.E_out;
-            // warp-per-element evaluation of a small layer uses the level tape's slots
-            if ((uint64_t)B * l.E_out <= dev::lane_group_eval_max())
-                slot_eval = std::max(slot_eval, (size_t)l.tape->nslots_lv * B * l.E_out);
-            ++nact;
-        }
-    n.slots.ensure(std::max<size_t>(std::max(slot_total, slot_eval), 1) * 16);
-    size_t mm_total = 0;
-    for (const auto& l : c.layers)
-        if (l.tape) mm_total += (size_t)B * l.E_out * k * 2;
-    n.mmlab.ensure(std::max<size_t>(mm_total, 1) * 16);
+        if (l.tape) ++nact;
     n.nact = nact;
     n.act_cap = nact + c.layers.size();
     n.act_dev.ensure(n.act_cap * sizeof(ActParams));
@@ -1810,8 +1820,13 @@ static void garble_act_flush(Network& n) {
     // a layer-windowed garbling flushes once per activation layer: each flush
     // stages its parameters in its own pinned / device slot, since the async
     // copy of an earlier flush may not have run yet
-    const size_t at = n.act_flushed, cnt = n.act_host.size();
-    if (at + cnt > n.nact) throw std::logic_error("activation launch staging overflow");
+    const size_t cnt = n.act_host.size();
+    if (cnt > n.nact) throw std::logic_error("activation launch staging overflow");
+    if (n.act_flushed + cnt > n.nact) {  // slots exhausted (layer API reuse): drain, then restart
+        dev::sync(g_stream);
+        n.act_flushed = 0;
+    }
+    const size_t at = n.act_flushed;
     ActParams* pin = n.act_pin.as<ActParams>() + at;
     ActParams* dp = n.act_dev.as<ActParams>() + at;
     std::memcpy(pin, n.act_host.data(), cnt * sizeof(ActParams));
@@ -2390,12 +2405,10 @@ static size_t out_bytes(const std::vector<uint8_t>& v, uint8_t* buf, size_t cap,
     return v.size();
 }
 
-static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
-    const dashgpu_circuit& c = *n.c;
-    if (b >= n.B) throw DataError("inference index out of range");
-    n.require_gc();
-    Writer w;
-    w.b.reserve(c.total_cts * 16 + 4096);
+// serialize_garbled_circuit (garble.cpp:347-403) up to the ciphertext rows:
+// circuit description, zero-wire labels (zero = this inference's [k][LABW]
+// words), layer ciphertext bases and the row count
+static void gc_header(const dashgpu_circuit& c, const uint32_t* zero, Writer& w) {
     w.header(1);
     w.le((uint64_t)c.k, 1);
     w.shape(c.input_shape);
@@ -2427,6 +2440,19 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
             w.le(l.pad, 4);
         }
     }
+    for (int i = 0; i < c.k; ++i) w.u128v(host_compress(zero + (size_t)i * LABW, c.base.primes[i]));
+    w.le(c.layers.size() + 1, 8);
+    for (const auto& l : c.layers) w.le(l.ct_base, 8);
+    w.le(c.total_cts, 8);
+    w.le(c.total_cts, 8);
+}
+
+static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
+    const dashgpu_circuit& c = *n.c;
+    if (b >= n.B) throw DataError("inference index out of range");
+    n.require_gc();
+    Writer w;
+    w.b.reserve(c.total_cts * 16 + 4096);
     std::vector<uint32_t> zero((size_t)c.k * LABW);
     dev::d2h(zero.data(), n.zero.as<uint32_t>() + (uint64_t)b * c.k * LABW, zero.size() * 4, g_stream);
     // rows -> reference order on the device, then one D2H straight into the
@@ -2437,17 +2463,75 @@ static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
     U4 commit;
     dev::d2h(&commit, n.commit.as<U4>() + b, 16, g_stream);
     dev::sync(g_stream);
-    for (int i = 0; i < c.k; ++i) w.u128v(host_compress(zero.data() + (size_t)i * LABW, c.base.primes[i]));
-    w.le(c.layers.size() + 1, 8);
-    for (const auto& l : c.layers) w.le(l.ct_base, 8);
-    w.le(c.total_cts, 8);
-    w.le(c.total_cts, 8);
+    gc_header(c, zero.data(), w);
     const size_t at = w.b.size();
     w.b.resize(at + c.total_cts * 16);
     dev::d2h(w.b.data() + at, ref.p, c.total_cts * 16, g_stream);
     dev::sync(g_stream);
     w.u128v(u4_to_u128(commit));
     return w.b;
+}
+
+// Streamed serialize_garbled_circuit (SURVEY §8(f) row 1 at GC sizes beyond
+// HBM): garbles layer by layer through the one-layer window (§11.1) and hands
+// every inference's GC bytes to `sink` in order -- header, each layer's rows
+// in the reference's cts order, commitment -- so the concatenation per
+// inference is byte-identical to export_gc.  The network keeps its encoding
+// and decoding material (as after dashgpu_network_release_gc).
+static void garble_stream_into(Network& n, const uint8_t* seeds, uint32_t B, dashgpu_gc_sink sink, void* user) {
+    dashgpu_circuit& c = *n.c;
+    garble_setup(n, seeds, B, false, true);
+    n.gc_released = false;
+    auto emit = [&](uint32_t b, const void* p, size_t len) {
+        if (len && sink(user, b, static_cast<const uint8_t*>(p), len) != 0)
+            throw DataError("garbled-circuit sink aborted the stream");
+    };
+    std::vector<uint32_t> zero((size_t)B * c.k * LABW);
+    std::vector<U4> commit(B);
+    dev::d2h(zero.data(), n.zero.p, zero.size() * 4, g_stream);
+    dev::d2h(commit.data(), n.commit.p, (size_t)B * 16, g_stream);
+    dev::sync(g_stream);
+    for (uint32_t b = 0; b < B; ++b) {
+        Writer w;
+        gc_header(c, zero.data() + (size_t)b * c.k * LABW, w);
+        emit(b, w.b.data(), w.b.size());
+    }
+    outs_begin(n, true, n.base);
+    DevBuf ref;
+    HostBuf host;
+    for (size_t li = 0; li < c.layers.size(); ++li) {
+        run_layer_at(n, true, li);
+        garble_act_flush(n);
+        const HLayer& l = c.layers[li];
+        if (!l.cts) continue;
+        ref.ensure(l.cts * 16);
+        host.ensure(l.cts * 16);
+        for (uint32_t b = 0; b < B; ++b) {
+            const U4* src = n.blob.as<U4>() + (uint64_t)b * l.cts;
+            if (l.tape) {
+                RowsPermuteParams P;
+                P.src = src;
+                P.dst = ref.as<U4>();
+                P.E = l.E_out;
+                P.uc = l.tape->cts;
+                P.to_ref = 1;
+                launch_rows_permute(P, g_stream);
+                src = ref.as<U4>();
+            }
+            dev::d2h(host.p, src, l.cts * 16, g_stream);
+            dev::sync(g_stream);
+            emit(b, host.p, l.cts * 16);
+        }
+    }
+    for (uint32_t b = 0; b < B; ++b) {
+        Writer w;
+        w.u128v(u4_to_u128(commit[b]));
+        emit(b, w.b.data(), w.b.size());
+    }
+    garble_dectables(n, *n.gouts.at[c.layers.size()]);
+    dev::sync(g_stream);
+    for (DevBuf* d : {&n.blob, &n.slots, &n.mmlab}) d->reset();
+    n.gc_released = true;
 }
 
 static std::vector<U4> compress_lanes(const Lanes& L, const Crt& base, uint32_t B, uint32_t b) {
@@ -3109,6 +3193,19 @@ int dashgpu_garble(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batc
     });
 }
 
+int dashgpu_garble_stream(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch, dashgpu_gc_sink sink,
+                          void* user, dashgpu_network** out) {
+    return guarded([&] {
+        if (batch == 0) throw DataError("empty batch");
+        if (!sink) throw DataError("null sink");
+        auto n = std::make_unique<dashgpu_network>();
+        n->net = std::make_unique<Network>();
+        n->net->c = const_cast<dashgpu_circuit*>(c);
+        garble_stream_into(*n->net, seeds, batch, sink, user);
+        if (out) *out = n.release();
+    });
+}
+
 void dashgpu_network_destroy(dashgpu_network* n) { delete n; }
 
 // ---- layer level (layer.hpp:79-97) ----
@@ -3430,7 +3527,11 @@ static uint64_t per_inference_bytes(const dashgpu_circuit& c, bool windowed) {
     }
     uint64_t slots = 0;
     for (const auto& l : c.layers)
-        if (l.tape) slots += (uint64_t)l.tape->nslots * l.E_out * 16;
+        if (l.tape) {
+            const uint64_t sl = (uint64_t)std::max(l.tape->nslots, l.tape->nslots_lv) * l.E_out * 16 +
+                                (uint64_t)l.E_out * c.k * 2 * 16;  // + mixed-modulus labels
+            slots = windowed ? std::max(slots, sl) : slots + sl;
+        }
     return (windowed ? max_layer_cts(c) : c.total_cts) * 16 + (uint64_t)(MAXMOD - 1) * 128 * NWMAX * 4 + planes +
            slots + c.n_out * 600 * 16 + 4096;
 }
@@ -3493,7 +3594,10 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
         const char* force = std::getenv("DASHGPU_LAYERWISE");
         uint32_t chunk = batch;
         bool layerwise = n.windowed;
-        if (n.cap < batch || force) {
+        if (!force && n.plan_batch == batch && n.plan_chunk) {  // this batch size was planned before
+            chunk = n.plan_chunk;
+            layerwise = n.plan_layerwise;
+        } else if (n.cap < batch || force) {
             // (cudaMemGetInfo is only asked when the workspace must grow: it
             // costs far more than the rest of the host side of a call)
             const uint64_t per = per_inference_bytes(*c, false), per_w = per_inference_bytes(*c, true);
@@ -3508,6 +3612,9 @@ int dashgpu_infer(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batc
             if (force) layerwise = force[0] == '1';
             if (layerwise) chunk = fit(per_w);
         }
+        n.plan_batch = force ? 0 : batch;
+        n.plan_chunk = chunk;
+        n.plan_layerwise = layerwise;
         Bundle& in = *n.bin;
         Bundle& out = *n.bout;
         for (uint32_t b0 = 0; b0 < batch; b0 += chunk) {

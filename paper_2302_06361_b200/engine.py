@@ -84,6 +84,11 @@ class CircuitInfo(ctypes.Structure):
     ]
 
 
+# dashgpu_gc_sink: (user, inference, data, len) -> 0 to continue
+GC_SINK = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint8),
+                           ctypes.c_size_t)
+
+
 class Timing(ctypes.Structure):
     _fields_ = [
         ("ms_garble", ctypes.c_double),
@@ -131,6 +136,7 @@ def _declare(L):
     L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
     L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
     L.dashgpu_garble_digest.argtypes = [vp, u8p, ctypes.c_uint32, u8p]
+    L.dashgpu_garble_stream.argtypes = [vp, u8p, ctypes.c_uint32, GC_SINK, vp, ctypes.POINTER(vp)]
     L.dashgpu_infer_stream.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
     L.dashgpu_infer_stream_range.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, ctypes.c_uint64,
                                              ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
@@ -221,6 +227,32 @@ class Dash:
         self._check(self.lib.dashgpu_garble_digest(c.h, buf, batch,
                                                    out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
         return out
+
+    def garble_stream(self, c: "GpuCircuit", seeds: bytes, sink) -> "GarbledNetwork":
+        """Streamed serialize_garbled_circuit: sink(b, chunk: bytes) receives
+        inference b's GC bytes in order (their concatenation == export_gc(b));
+        the device holds one layer's ciphertexts at a time.  Returns the
+        network with encoding / decoding (its GC already released).  A sink
+        that returns a truthy value or raises aborts the stream (DataError)."""
+        if len(seeds) == 0 or len(seeds) % 16:
+            raise DataError("seeds must be a non-empty multiple of 16 bytes")
+        failure = []
+
+        def cb(_user, b, data, n):
+            try:
+                return 1 if sink(int(b), ctypes.string_at(data, n)) else 0
+            except BaseException as e:  # noqa: BLE001 -- re-raised below, never across the C frame
+                failure.append(e)
+                return 1
+
+        fn = GC_SINK(cb)
+        buf = (ctypes.c_uint8 * len(seeds)).from_buffer_copy(seeds)
+        h = vp()
+        rc = self.lib.dashgpu_garble_stream(c.h, buf, len(seeds) // 16, fn, None, ctypes.byref(h))
+        if failure:
+            raise failure[0]
+        self._check(rc)
+        return GarbledNetwork(self, h, c, len(seeds) // 16)
 
     def garble_inputs(self, net: "GarbledNetwork", values) -> "Bundle":
         v = np.ascontiguousarray(values, np.int64).reshape(net.batch, net.circuit.info.n_in)
