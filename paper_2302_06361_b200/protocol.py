@@ -364,11 +364,13 @@ class GarblerService:
         if owners > n_in:
             raise ProtocolError("more input owners than input elements")
         seed = self.cfg.seed if self.cfg.seed is not None else os.urandom(16)
-        net = self.eng.garble(self.eng.circuit(circuit), seed)
-        gc = net.export_gc(0)
-        # the GC has left: keep only encoding + decoding material in HBM, as the
-        # reference garbler keeps only EncodingInfo / DecodingInfo (protocol.cpp:211-226)
-        net.release_gc()
+        # streamed serialize_garbled_circuit: HBM holds one layer's rows at a
+        # time, and the network keeps only encoding + decoding material, as the
+        # reference garbler keeps only EncodingInfo / DecodingInfo
+        # (protocol.cpp:211-226)
+        chunks = []
+        net = self.eng.garble_stream(self.eng.circuit(circuit), seed, lambda b, data: chunks.append(data))
+        gc = b"".join(chunks)
         with self._mu:
             if f.session in self._sessions:
                 raise ProtocolError("session already exists")
