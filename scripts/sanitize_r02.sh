@@ -15,3 +15,8 @@ echo "memcheck dense1024 pairs: $(tail -1 gpurun_out/sanitizer/memcheck_dense102
 timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python scripts/sanitize.py lenet5:2 \
   > gpurun_out/sanitizer/memcheck_lenet5.txt 2>&1
 echo "memcheck lenet5: $(tail -1 gpurun_out/sanitizer/memcheck_lenet5.txt)"
+for tool in memcheck racecheck; do
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_stream.py \
+    > gpurun_out/sanitizer/${tool}_stream.txt 2>&1
+  echo "$tool stream: $(tail -1 gpurun_out/sanitizer/${tool}_stream.txt)"
+done
