@@ -2497,30 +2497,46 @@ static void garble_stream_into(Network& n, const uint8_t* seeds, uint32_t B, das
         emit(b, w.b.data(), w.b.size());
     }
     outs_begin(n, true, n.base);
-    DevBuf ref;
-    HostBuf host;
+    // double-buffered: inference b + 1's rows are permuted and copied while
+    // the sink consumes inference b's
+    DevBuf ref[2];
+    HostBuf host[2];
+    struct Ev {
+        void* e = dev::event_create();
+        ~Ev() { dev::event_destroy(e); }
+    } ev[2];
     for (size_t li = 0; li < c.layers.size(); ++li) {
         run_layer_at(n, true, li);
         garble_act_flush(n);
         const HLayer& l = c.layers[li];
         if (!l.cts) continue;
-        ref.ensure(l.cts * 16);
-        host.ensure(l.cts * 16);
-        for (uint32_t b = 0; b < B; ++b) {
-            const U4* src = n.blob.as<U4>() + (uint64_t)b * l.cts;
-            if (l.tape) {
-                RowsPermuteParams P;
-                P.src = src;
-                P.dst = ref.as<U4>();
-                P.E = l.E_out;
-                P.uc = l.tape->cts;
-                P.to_ref = 1;
-                launch_rows_permute(P, g_stream);
-                src = ref.as<U4>();
+        const size_t bytes = l.cts * 16;
+        for (int s = 0; s < 2; ++s) {
+            ref[s].ensure(bytes);
+            host[s].ensure(bytes);
+        }
+        for (uint32_t b = 0; b <= B; ++b) {
+            if (b < B) {
+                const int s = b & 1;
+                const U4* src = n.blob.as<U4>() + (uint64_t)b * l.cts;
+                if (l.tape) {
+                    RowsPermuteParams P;
+                    P.src = src;
+                    P.dst = ref[s].as<U4>();
+                    P.E = l.E_out;
+                    P.uc = l.tape->cts;
+                    P.to_ref = 1;
+                    launch_rows_permute(P, g_stream);
+                    src = ref[s].as<U4>();
+                }
+                dev::d2h(host[s].p, src, bytes, g_stream);
+                dev::event_record(ev[s].e, g_stream);
             }
-            dev::d2h(host.p, src, l.cts * 16, g_stream);
-            dev::sync(g_stream);
-            emit(b, host.p, l.cts * 16);
+            if (b > 0) {  // hand over inference b - 1 while b is in flight
+                const int s = (b - 1) & 1;
+                dev::event_sync(ev[s].e);
+                emit(b - 1, host[s].p, bytes);
+            }
         }
     }
     for (uint32_t b = 0; b < B; ++b) {
