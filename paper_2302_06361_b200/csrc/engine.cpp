@@ -2447,29 +2447,57 @@ static void gc_header(const dashgpu_circuit& c, const uint32_t* zero, Writer& w)
     w.le(c.total_cts, 8);
 }
 
-static std::vector<uint8_t> export_gc(const Network& n, uint32_t b) {
+// device rows -> host memory (pageable caller buffer) through two pinned
+// chunks: the copy of chunk i + 1 is in flight while chunk i is memcpy'd
+static void rows_to_host(const uint8_t* dsrc, size_t bytes, uint8_t* dst) {
+    constexpr size_t kChunk = 8u << 20;
+    static thread_local HostBuf stage[2];
+    struct Ev {
+        void* e = dev::event_create();
+        ~Ev() { dev::event_destroy(e); }
+    } ev[2];
+    const size_t n = (bytes + kChunk - 1) / kChunk;
+    for (size_t i = 0; i <= n; ++i) {
+        if (i < n) {
+            const size_t len = std::min(kChunk, bytes - i * kChunk);
+            stage[i & 1].ensure(kChunk);
+            dev::d2h(stage[i & 1].p, dsrc + i * kChunk, len, g_stream);
+            dev::event_record(ev[i & 1].e, g_stream);
+        }
+        if (i > 0) {
+            const size_t j = i - 1, len = std::min(kChunk, bytes - j * kChunk);
+            dev::event_sync(ev[j & 1].e);
+            std::memcpy(dst + j * kChunk, stage[j & 1].p, len);
+        }
+    }
+}
+
+// serialize_garbled_circuit (garble.cpp:347-403) of inference b straight into
+// buf (when cap suffices); *len = the GC's byte count either way
+static void export_gc_into(const Network& n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
     const dashgpu_circuit& c = *n.c;
     if (b >= n.B) throw DataError("inference index out of range");
     n.require_gc();
-    Writer w;
-    w.b.reserve(c.total_cts * 16 + 4096);
     std::vector<uint32_t> zero((size_t)c.k * LABW);
+    U4 commit;
     dev::d2h(zero.data(), n.zero.as<uint32_t>() + (uint64_t)b * c.k * LABW, zero.size() * 4, g_stream);
-    // rows -> reference order on the device, then one D2H straight into the
-    // writer's buffer (little-endian u128 rows == the U4 layout)
+    dev::d2h(&commit, n.commit.as<U4>() + b, 16, g_stream);
+    dev::sync(g_stream);
+    Writer w;
+    gc_header(c, zero.data(), w);
+    const size_t rows = c.total_cts * 16, total = w.b.size() + rows + 16;
+    if (len) *len = total;
+    if (!buf || cap < total) return;
+    std::memcpy(buf, w.b.data(), w.b.size());
+    // rows -> reference order on the device (little-endian u128 rows == the
+    // U4 layout), then to the caller's buffer
     DevBuf ref;
     ref.ensure(std::max<uint64_t>(c.total_cts, 1) * 16);
     blob_permute(c, n.blob.as<U4>() + (uint64_t)b * c.total_cts, ref.as<U4>(), true);
-    U4 commit;
-    dev::d2h(&commit, n.commit.as<U4>() + b, 16, g_stream);
-    dev::sync(g_stream);
-    gc_header(c, zero.data(), w);
-    const size_t at = w.b.size();
-    w.b.resize(at + c.total_cts * 16);
-    dev::d2h(w.b.data() + at, ref.p, c.total_cts * 16, g_stream);
-    dev::sync(g_stream);
-    w.u128v(u4_to_u128(commit));
-    return w.b;
+    rows_to_host(ref.as<uint8_t>(), rows, buf + w.b.size());
+    Writer t;
+    t.u128v(u4_to_u128(commit));
+    std::memcpy(buf + w.b.size() + rows, t.b.data(), 16);
 }
 
 // Streamed serialize_garbled_circuit (SURVEY §8(f) row 1 at GC sizes beyond
@@ -3403,7 +3431,7 @@ int dashgpu_decode_outputs(dashgpu_network* n, const dashgpu_bundle* out, int64_
 void dashgpu_bundle_destroy(dashgpu_bundle* b) { delete b; }
 
 int dashgpu_export_gc(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
-    return guarded([&] { export_cached(n, b, 1, buf, cap, len, [&] { return export_gc(*n->net, b); }); });
+    return guarded([&] { export_gc_into(*n->net, b, buf, cap, len); });
 }
 int dashgpu_export_encoding(const dashgpu_network* n, uint32_t b, uint8_t* buf, size_t cap, size_t* len) {
     return guarded([&] { export_cached(n, b, 2, buf, cap, len, [&] { return export_encoding(*n->net, b); }); });

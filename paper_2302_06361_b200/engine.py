@@ -513,9 +513,11 @@ class GarbledNetwork:
     def _export(self, fn, b: int) -> bytes:
         n = ctypes.c_size_t()
         self.eng._check(fn(self.h, b, None, 0, ctypes.byref(n)))
-        buf = (ctypes.c_uint8 * n.value)()
+        out = bytearray(n.value)
+        buf = (ctypes.c_uint8 * n.value).from_buffer(out)
         self.eng._check(fn(self.h, b, buf, n.value, ctypes.byref(n)))
-        return bytes(buf)
+        del buf  # release the export lock on `out`
+        return bytes(out)
 
     def export_gc(self, b: int = 0) -> bytes:
         """serialize_garbled_circuit (garble.cpp:347-370) of inference b."""
@@ -561,6 +563,8 @@ class Bundle:
         fn = self.eng.lib.dashgpu_export_bundle
         n = ctypes.c_size_t()
         self.eng._check(fn(self.h, b, None, 0, ctypes.byref(n)))
-        buf = (ctypes.c_uint8 * n.value)()
+        out = bytearray(n.value)
+        buf = (ctypes.c_uint8 * n.value).from_buffer(out)
         self.eng._check(fn(self.h, b, buf, n.value, ctypes.byref(n)))
-        return bytes(buf)
+        del buf  # release the export lock on `out`
+        return bytes(out)
