@@ -196,6 +196,12 @@ int dashgpu_import_bundle(dashgpu_network* n, const uint8_t* data, size_t len, i
  * evaluates them as inferences 0..batch-1 (garbling it returns
  * DASHGPU_ERR_DATA: private weights are not in a GC).  Owns its circuit. */
 int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t batch, dashgpu_network** out);
+/* The same with the ciphertexts kept in pinned HOST memory (reference cts
+ * order) instead of HBM: dashgpu_evaluate moves each layer's rows into a
+ * one-layer device window just before evaluating it, so an
+ * evaluator holds GCs larger than HBM.  Everything else is dashgpu_import_gc's
+ * (checks, export_gc, tamper, release). */
+int dashgpu_import_gc_host(const uint8_t* const* gcs, const size_t* lens, uint32_t batch, dashgpu_network** out);
 /* the circuit a network garbles / evaluates (borrowed: lives as long as the network) */
 int dashgpu_network_circuit(const dashgpu_network* n, const dashgpu_circuit** out);
 /* fault injection for tests: XOR `mask` (16 bytes) into ciphertext `index` of inference b */

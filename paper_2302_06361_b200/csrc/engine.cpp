@@ -956,6 +956,11 @@ struct HostBuf {
     HostBuf(const HostBuf&) = delete;
     HostBuf& operator=(const HostBuf&) = delete;
     ~HostBuf() { dev::host_release(p); }
+    void reset() {
+        dev::host_release(p);
+        p = nullptr;
+        n = 0;
+    }
     void ensure(size_t bytes) {
         if (bytes <= n && p) return;
         dev::host_release(p);
@@ -1424,6 +1429,11 @@ struct Network {
     // holds one layer's rows for the batch at a time, [B][layer cts], instead
     // of whole GCs [B][total_cts]
     bool windowed = false;
+    // host-resident GC (dashgpu_import_gc_host): rows in the reference's cts
+    // order, [B][total_cts] in pinned memory, moved to the window layer by
+    // layer during evaluation
+    bool host_gc = false;
+    HostBuf hblob;
     size_t act_flushed = 0;  // activation layers whose garbling launch is enqueued
     // dashgpu_infer's last sub-batch plan (batch size -> sub-batch, schedule)
     uint32_t plan_batch = 0, plan_chunk = 0;
@@ -1914,6 +1924,33 @@ static void evaluate_into(Network& n, const Bundle& in, Bundle& out) {
     if (in.net != &n || in.B != n.B || in.output) throw DataError("garbled input bundle does not match the network");
     if (in.lanes.E != c.n_in || in.lanes.lane.size() != (size_t)k) throw DataError("garbled input shape mismatch");
     n.require_gc();
+    if (n.host_gc) {  // host-resident GC: fill the window layer by layer
+        outs_begin(n, false, in.lanes);
+        DevBuf ref;
+        ref.ensure(std::max<uint64_t>(max_layer_cts(c), 1) * 16);
+        for (size_t li = 0; li < c.layers.size(); ++li) {
+            const HLayer& l = c.layers[li];
+            for (uint32_t b = 0; l.cts && b < n.B; ++b) {
+                const U4* h = n.hblob.as<U4>() + (uint64_t)b * c.total_cts + l.ct_base;
+                U4* w = n.blob.as<U4>() + (uint64_t)b * l.cts;
+                if (!l.tape) {  // private-weight rows are stored in reference order
+                    dev::h2d(w, h, l.cts * 16, g_stream);
+                    continue;
+                }
+                dev::h2d(ref.p, h, l.cts * 16, g_stream);
+                RowsPermuteParams P;
+                P.src = ref.as<U4>();
+                P.dst = w;
+                P.E = l.E_out;
+                P.uc = l.tape->cts;
+                P.to_ref = 0;
+                launch_rows_permute(P, g_stream);
+            }
+            run_layer_at(n, false, li);
+        }
+        eval_output(n, *n.eouts.at[c.layers.size()], out);
+        return;
+    }
     eval_output(n, *run_layers(n, false, in.lanes), out);
 }
 
@@ -2491,10 +2528,14 @@ static void export_gc_into(const Network& n, uint32_t b, uint8_t* buf, size_t ca
     std::memcpy(buf, w.b.data(), w.b.size());
     // rows -> reference order on the device (little-endian u128 rows == the
     // U4 layout), then to the caller's buffer
-    DevBuf ref;
-    ref.ensure(std::max<uint64_t>(c.total_cts, 1) * 16);
-    blob_permute(c, n.blob.as<U4>() + (uint64_t)b * c.total_cts, ref.as<U4>(), true);
-    rows_to_host(ref.as<uint8_t>(), rows, buf + w.b.size());
+    if (n.host_gc) {
+        std::memcpy(buf + w.b.size(), n.hblob.as<U4>() + (uint64_t)b * c.total_cts, rows);
+    } else {
+        DevBuf ref;
+        ref.ensure(std::max<uint64_t>(c.total_cts, 1) * 16);
+        blob_permute(c, n.blob.as<U4>() + (uint64_t)b * c.total_cts, ref.as<U4>(), true);
+        rows_to_host(ref.as<uint8_t>(), rows, buf + w.b.size());
+    }
     Writer t;
     t.u128v(u4_to_u128(commit));
     std::memcpy(buf + w.b.size() + rows, t.b.data(), 16);
@@ -3328,6 +3369,7 @@ int dashgpu_network_release_gc(dashgpu_network* n) {
         Network& N = *n->net;
         dev::sync(g_stream);  // nothing in flight may still read them
         for (DevBuf* b : {&N.blob, &N.slots, &N.mmlab, &N.act_dev, &N.qflags}) b->reset();
+        N.hblob.reset();
         N.gouts.own.clear();
         N.gouts.at.clear();
         N.eouts.own.clear();
@@ -3488,8 +3530,9 @@ int dashgpu_import_bundle(dashgpu_network* n, const uint8_t* data, size_t len, i
 // an evaluator network, one inference per GC; all GCs of a batch must carry
 // the same circuit.  The consistency checks of evaluate (garble.cpp:262-303)
 // run here, once.
-int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t batch, dashgpu_network** out) {
-    return guarded([&] {
+static void import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t batch, dashgpu_network** out,
+                      bool host) {
+    {
         if (!gcs || !lens || !out) throw DataError("null argument");
         if (batch == 0) throw DataError("empty batch");
         auto n = std::make_unique<dashgpu_network>();
@@ -3513,16 +3556,22 @@ int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t ba
         Network& N = *n->net;
         N.c = &c;
         upload_circuit(c);
-        network_reserve(N, batch);
+        network_reserve(N, batch, host);  // host-resident: a one-layer device window
+        N.host_gc = host;
         std::vector<uint32_t> zero((size_t)batch * c.k * LABW);
         std::vector<U4> commit(batch);
         DevBuf ref;  // one inference's rows in the reference order, then permuted on the device
-        ref.ensure(std::max<uint64_t>(c.total_cts, 1) * 16);
+        if (host) N.hblob.ensure(std::max<uint64_t>((uint64_t)batch * c.total_cts, 1) * 16);
+        else ref.ensure(std::max<uint64_t>(c.total_cts, 1) * 16);
         for (uint32_t b = 0; b < batch; ++b) {
             for (int i = 0; i < c.k; ++i)
                 host_decompress(gs[b].zero[i], c.base.primes[i], zero.data() + ((size_t)b * c.k + i) * LABW);
-            dev::h2d(ref.p, gs[b].cts, c.total_cts * 16, g_stream);
-            blob_permute(c, ref.as<U4>(), N.blob.as<U4>() + (uint64_t)b * c.total_cts, false);
+            if (host) {
+                std::memcpy(N.hblob.as<U4>() + (uint64_t)b * c.total_cts, gs[b].cts, c.total_cts * 16);
+            } else {
+                dev::h2d(ref.p, gs[b].cts, c.total_cts * 16, g_stream);
+                blob_permute(c, ref.as<U4>(), N.blob.as<U4>() + (uint64_t)b * c.total_cts, false);
+            }
             commit[b] = u128_to_u4(gs[b].commit);
         }
         dev::h2d(N.zero.p, zero.data(), zero.size() * 4, g_stream);
@@ -3532,7 +3581,15 @@ int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t ba
         dev::memset0(N.rk.p, N.rk.n, g_stream);
         dev::sync(g_stream);
         *out = n.release();
-    });
+    }
+}
+
+int dashgpu_import_gc(const uint8_t* const* gcs, const size_t* lens, uint32_t batch, dashgpu_network** out) {
+    return guarded([&] { import_gc(gcs, lens, batch, out, false); });
+}
+
+int dashgpu_import_gc_host(const uint8_t* const* gcs, const size_t* lens, uint32_t batch, dashgpu_network** out) {
+    return guarded([&] { import_gc(gcs, lens, batch, out, true); });
 }
 
 int dashgpu_network_circuit(const dashgpu_network* n, const dashgpu_circuit** out) {
@@ -3547,6 +3604,11 @@ int dashgpu_tamper_ct(dashgpu_network* n, uint32_t b, uint64_t index, const uint
         Network& N = *n->net;
         if (b >= N.B || index >= N.c->total_cts) throw DataError("ciphertext index out of range");
         N.require_gc();
+        if (N.host_gc) {
+            uint8_t* h = reinterpret_cast<uint8_t*>(N.hblob.as<U4>() + (uint64_t)b * N.c->total_cts + index);
+            for (int i = 0; i < 16; ++i) h[i] ^= mask16[i];
+            return;
+        }
         U4 v;
         U4* p = N.blob.as<U4>() + (uint64_t)b * N.c->total_cts + device_ct_index(*N.c, index);
         dev::d2h(&v, p, 16, g_stream);

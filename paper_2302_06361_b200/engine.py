@@ -132,6 +132,7 @@ def _declare(L):
     L.dashgpu_import_bundle.argtypes = [vp, u8p, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(vp)]
     L.dashgpu_import_gc.argtypes = [ctypes.POINTER(u8p), ctypes.POINTER(ctypes.c_size_t), ctypes.c_uint32,
                                     ctypes.POINTER(vp)]
+    L.dashgpu_import_gc_host.argtypes = L.dashgpu_import_gc.argtypes
     L.dashgpu_network_circuit.argtypes = [vp, ctypes.POINTER(vp)]
     L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
     L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
@@ -320,17 +321,20 @@ class Dash:
         self._check(self.lib.dashgpu_import_bundle(net.h, buf, len(payload), 1 if output else 0, ctypes.byref(h)))
         return Bundle(self, h, net, output)
 
-    def import_gc(self, gcs) -> "GarbledNetwork":
+    def import_gc(self, gcs, host_resident: bool = False) -> "GarbledNetwork":
         """parse_garbled_circuit (garble.cpp:368-403) on the evaluator side:
         serialized GCs of one circuit -> an evaluator network, inference b
-        evaluating gcs[b] (EvaluatorService GC_TRANSFER, protocol.cpp:309)."""
+        evaluating gcs[b] (EvaluatorService GC_TRANSFER, protocol.cpp:309).
+        host_resident: ciphertexts stay in pinned host memory and move to the
+        GPU one layer at a time during evaluate (GCs larger than HBM)."""
         if isinstance(gcs, (bytes, bytearray)):
             gcs = [gcs]
         gcs = [bytes(g) for g in gcs]  # no copy for bytes; pointers into them (kept alive below)
         ptrs = (u8p * len(gcs))(*[ctypes.cast(ctypes.c_char_p(g), u8p) for g in gcs])
         lens = (ctypes.c_size_t * len(gcs))(*[len(g) for g in gcs])
         h = vp()
-        self._check(self.lib.dashgpu_import_gc(ptrs, lens, len(gcs), ctypes.byref(h)))
+        fn = self.lib.dashgpu_import_gc_host if host_resident else self.lib.dashgpu_import_gc
+        self._check(fn(ptrs, lens, len(gcs), ctypes.byref(h)))
         ch = vp()
         self._check(self.lib.dashgpu_network_circuit(h, ctypes.byref(ch)))
         net = GarbledNetwork(self, h, GpuCircuit(self, ch, owned=False), len(gcs))
