@@ -472,11 +472,17 @@ class EvaluatorService:
     batch_timeout: seconds a batched group (handle_batch) waits for its
     members' GARBLED_INPUT frames; flush_expired() then evaluates the group
     with placeholder inputs for the missing members and answers those with
-    ERROR frames, so one stalled client cannot starve the others."""
+    ERROR frames, so one stalled client cannot starve the others.
 
-    def __init__(self, eng: Dash, batch_timeout: float = 30.0):
+    host_resident_gc: keep each session's ciphertexts in pinned host memory
+    and move them to the GPU one layer at a time at evaluation
+    (dashgpu_import_gc_host) -- for GCs that do not fit HBM, or many pending
+    sessions; the garbled outputs are the same."""
+
+    def __init__(self, eng: Dash, batch_timeout: float = 30.0, host_resident_gc: bool = False):
         self.eng = eng
         self.batch_timeout = batch_timeout
+        self.host_resident_gc = host_resident_gc
         self._mu = threading.Lock()
         self._sessions: Dict[int, _EvaluatorSession] = {}
         self._ready: List[Frame] = []  # replies of batched sessions not yet handed out
@@ -492,7 +498,7 @@ class EvaluatorService:
             return mine[0] if mine else None
         try:
             if f.type == FrameType.GC_TRANSFER:
-                net = self.eng.import_gc([f.payload])
+                net = self.eng.import_gc([f.payload], self.host_resident_gc)
                 info = net.circuit.info
                 mem = info.cts * 16 + info.k * 16 + 16 * info.k * info.n_in  # protocol.cpp:347-350
                 with self._mu:
@@ -593,7 +599,7 @@ class EvaluatorService:
         if len(fresh) < 2:
             return replies + [r for r in (self.handle(f) for f in fresh) if r is not None]
         try:
-            net = self.eng.import_gc([f.payload for f in fresh])
+            net = self.eng.import_gc([f.payload for f in fresh], self.host_resident_gc)
         except Error:  # bad file or mixed circuits: per-session imports attribute the errors
             return replies + [r for r in (self.handle(f) for f in fresh) if r is not None]
         info = net.circuit.info
@@ -667,7 +673,7 @@ LOOPBACK_SESSION = (0x44415348 << 64) | 1  # make_u128(0x44415348, 1) (protocol.
 
 
 def run_local_protocol(eng: Dash, quantized: Circuit, inputs, owners: int = 1,
-                       cfg: GarblerConfig = None) -> LocalRunResult:
+                       cfg: GarblerConfig = None, host_resident_gc: bool = False) -> LocalRunResult:
     """Both services in one process (protocol.cpp:355-435): model upload ->
     gNN transfer -> per-owner input uploads -> garbled input -> evaluation ->
     garbled output -> decode -> result request."""
@@ -676,7 +682,7 @@ def run_local_protocol(eng: Dash, quantized: Circuit, inputs, owners: int = 1,
         raise DataError("input size does not match the model")
     if owners == 0:
         raise DataError("at least one input owner required")
-    garbler, evaluator = GarblerService(eng, cfg), EvaluatorService(eng)
+    garbler, evaluator = GarblerService(eng, cfg), EvaluatorService(eng, host_resident_gc=host_resident_gc)
     session = LOOPBACK_SESSION
     res = LocalRunResult()
 

@@ -145,6 +145,17 @@ def test_gc_transfer_is_the_reference_gc(eng, oracle):
     assert outs[0].frame.payload == oracle.garble(c, oracle.seed_from_string("90a9")).gc_bytes()
 
 
+def test_host_resident_evaluator_gives_the_same_result(eng, oracle):
+    # EvaluatorService(host_resident_gc=True): GC rows in pinned host memory,
+    # moved to the GPU layer by layer; same garbled output frames
+    c = models.build("model_tiny", 1000, 8, private=True)
+    x = np.random.default_rng(907).integers(-7, 8, size=c.n_in)
+    a = P.run_local_protocol(eng, c, x, 2, _cfg(oracle, "90b1"))
+    b = P.run_local_protocol(eng, c, x, 2, _cfg(oracle, "90b1"), host_resident_gc=True)
+    assert b.outputs.tolist() == a.outputs.tolist() == oracle.plain_forward(c, x).tolist()
+    assert [(e.type, e.payload_bytes) for e in b.trace] == [(e.type, e.payload_bytes) for e in a.trace]
+
+
 def test_input_partitioning_does_not_change_garbled_input(eng, oracle):
     c = tiny()
     x = np.random.default_rng(901).integers(-7, 8, size=c.n_in)
