@@ -155,7 +155,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
                 "reasons": sorted(set().union(*(r[2] for r in self.rows))), "samples": len(self.rows),
-                "sampler": "nvml 2 ms" if self.nvml else "nvidia-smi 100 ms"}
+                "sampler": "nvml 2 ms x 250, then 20 ms" if self.nvml else "nvidia-smi 100 ms"}
 
 
 def cpu_baseline(circuit_desc_c, n_in, n_out, sample):
