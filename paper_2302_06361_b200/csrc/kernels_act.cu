@@ -343,8 +343,16 @@ uint64_t lane_group_eval_max() { return (uint64_t)sm_count() * kWpeEvalWarps * 3
 // warps per element of the level-parallel garbling launch (0: not used): the
 // largest power of two <= 8 whose warps still fit one wave of 16-warp CTAs
 uint32_t garble_lv_warps(uint64_t elements) {
-    uint32_t W = 8;
-    while (W >= 2 && elements * W > (uint64_t)sm_count() * kWpeWarps) W >>= 1;
+    static const uint32_t wmax = [] {  // DASH_LV_WARPS: A/B knob for the cap
+        const char* e = std::getenv("DASH_LV_WARPS");
+        return e ? (uint32_t)std::atoi(e) : 8u;
+    }();
+    static const uint32_t ctas = [] {  // DASH_LV_CTAS: resident 16-warp CTAs per SM assumed
+        const char* e = std::getenv("DASH_LV_CTAS");
+        return e ? (uint32_t)std::atoi(e) : 1u;
+    }();
+    uint32_t W = wmax;
+    while (W >= 2 && elements * W > (uint64_t)sm_count() * kWpeWarps * ctas) W >>= 1;
     return W >= 2 ? W : 0;
 }
 }  // namespace dev
