@@ -225,6 +225,10 @@ int dashgpu_infer(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch
  * a layer without ciphertexts gets SHA-256 of the empty string.
  * seeds [batch][16] (host), digests [batch][n_layers][32] (host). */
 int dashgpu_garble_digest(const dashgpu_circuit* c, const uint8_t* seeds, uint32_t batch, uint8_t* digests);
+/* The same digests of a network's held GC (garbled whole, or imported into
+ * HBM or host memory), inference b: digests [n_layers][32] (host).  An
+ * evaluator checks a received GC against the garbler's digest list. */
+int dashgpu_network_digest(const dashgpu_network* n, uint32_t b, uint8_t* digests);
 
 /* Streamed serialize_garbled_circuit (garble.cpp:347-403):
  * garbles the batch layer by layer through a one-layer ciphertext window and

@@ -3642,6 +3642,55 @@ static uint64_t per_inference_bytes(const dashgpu_circuit& c, bool windowed) {
            slots + c.n_out * 600 * 16 + 4096;
 }
 
+// per-layer tree digests of a network's held GC (whole-GC device blob or
+// host-resident rows): the evaluator's side of the digest parity mode
+static void network_digest(const Network& n, uint32_t b, uint8_t* digests) {
+    const dashgpu_circuit& c = *n.c;
+    if (b >= n.B) throw DataError("inference index out of range");
+    n.require_gc();
+    if (n.windowed && !n.host_gc) throw DataError("garbled circuit is not held whole");
+    DevBuf leaves, rows;
+    std::vector<uint32_t> hl;
+    std::vector<uint8_t> cat;
+    for (size_t li = 0; li < c.layers.size(); ++li) {
+        const HLayer& l = c.layers[li];
+        DigestParams P;
+        std::memset(&P, 0, sizeof P);
+        P.rows = l.cts;
+        P.stride = l.cts;
+        P.B = 1;
+        P.leaves = (uint32_t)((l.cts + kDigestLeafRows - 1) / kDigestLeafRows);
+        if (n.host_gc) {  // reference order already: copy the layer up
+            rows.ensure(std::max<uint64_t>(l.cts, 1) * 16);
+            dev::h2d(rows.p, n.hblob.as<U4>() + (uint64_t)b * c.total_cts + l.ct_base, l.cts * 16, g_stream);
+            P.src = rows.as<U4>();
+        } else {
+            P.src = n.blob.as<U4>() + (uint64_t)b * c.total_cts + l.ct_base;
+            P.E = l.tape ? l.E_out : 0;
+            P.uc = l.tape ? l.tape->cts : 0;
+        }
+        if (P.leaves) {
+            leaves.ensure((size_t)P.leaves * 32);
+            P.out = leaves.as<uint32_t>();
+            launch_digest(P, g_stream);
+            hl.resize((size_t)P.leaves * 8);
+            dev::d2h(hl.data(), leaves.p, hl.size() * 4, g_stream);
+            dev::sync(g_stream);
+        }
+        cat.resize((size_t)P.leaves * 32);
+        for (size_t w = 0; w < (size_t)P.leaves * 8; ++w)
+            for (int q = 0; q < 4; ++q) cat[4 * w + q] = (uint8_t)(hl[w] >> (24 - 8 * q));
+        sha256_bytes(cat.data(), cat.size(), digests + li * 32);
+    }
+}
+
+int dashgpu_network_digest(const dashgpu_network* n, uint32_t b, uint8_t* digests) {
+    return guarded([&] {
+        if (!n || !digests) throw DataError("null argument");
+        network_digest(*n->net, b, digests);
+    });
+}
+
 int dashgpu_garble_digest(const dashgpu_circuit* cc, const uint8_t* seeds, uint32_t batch, uint8_t* digests) {
     return guarded([&] {
         auto* c = const_cast<dashgpu_circuit*>(cc);

@@ -137,6 +137,7 @@ def _declare(L):
     L.dashgpu_tamper_ct.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, u8p]
     L.dashgpu_infer.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_int, ctypes.POINTER(Timing)]
     L.dashgpu_garble_digest.argtypes = [vp, u8p, ctypes.c_uint32, u8p]
+    L.dashgpu_network_digest.argtypes = [vp, ctypes.c_uint32, u8p]
     L.dashgpu_garble_stream.argtypes = [vp, u8p, ctypes.c_uint32, GC_SINK, vp, ctypes.POINTER(vp)]
     L.dashgpu_infer_stream.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, vp, ctypes.POINTER(Timing)]
     L.dashgpu_infer_stream_range.argtypes = [vp, vp, ctypes.c_uint32, vp, vp, ctypes.c_uint64, ctypes.c_uint64,
@@ -522,6 +523,14 @@ class GarbledNetwork:
         self.eng._check(fn(self.h, b, buf, n.value, ctypes.byref(n)))
         del buf  # release the export lock on `out`
         return bytes(out)
+
+    def digest(self, b: int = 0) -> np.ndarray:
+        """[n_layers][32] tree SHA-256 of inference b's layer ciphertexts
+        (dashgpu_network_digest; the same digests as Dash.garble_digest)."""
+        out = np.zeros((self.circuit.info.n_layers, 32), np.uint8)
+        self.eng._check(self.eng.lib.dashgpu_network_digest(self.h, b,
+                                                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+        return out
 
     def export_gc(self, b: int = 0) -> bytes:
         """serialize_garbled_circuit (garble.cpp:347-370) of inference b."""
