@@ -105,11 +105,11 @@ def test_lenet5_b64_bench_shape_vs_reference(gpu, golden_batch):
     # the bench's call: dashgpu_infer (garble + garble_inputs + evaluate + decode)
     out, t = gpu.infer(g, seeds, x)
     shape = gpu.last_act_launch(True)
+    for b in range(B):
+        assert out[b].tolist() == rec["inferences"][b]["decoded"], b
     assert shape["variant"] == "per-thread" and shape["nchunks"] == 8, shape
     assert shape["items"] > shape["grid"] * 28  # more warp items than garbling warps: chunk flags in play
     assert t.sub_batches == 1
-    for b in range(B):
-        assert out[b].tolist() == rec["inferences"][b]["decoded"], b
     # the same launch through the stepwise API, every artefact of every inference
     net = gpu.garble(g, seeds)
     assert gpu.last_act_launch(True)["nchunks"] == 8
