@@ -534,4 +534,16 @@ DASH_HD void digest_leaf_thread(const DigestParams& P, uint32_t b, uint32_t leaf
     sha256_rows(n, row, P.out + ((uint64_t)b * P.leaves + leaf) * 8);
 }
 
+// The root of one inference's layer: SHA-256 over its leaf digests as bytes
+// (state words big-endian), read as 16-byte rows: row i = half (i & 1) of
+// leaf i >> 1.  out: [B][8] state words.
+DASH_HD void digest_root_thread(const DigestParams& P, uint32_t b, uint32_t* out) {
+    const uint32_t* lv = P.out + (uint64_t)b * P.leaves * 8;
+    auto row = [&](uint64_t i, uint32_t* w) {
+        const uint32_t* d = lv + (i >> 1) * 8 + (i & 1) * 4;
+        for (int t = 0; t < 4; ++t) w[t] = sha_bswap(d[t]);
+    };
+    sha256_rows((uint64_t)P.leaves * 2, row, out + (uint64_t)b * 8);
+}
+
 }  // namespace dashgpu

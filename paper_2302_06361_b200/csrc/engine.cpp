@@ -1993,9 +1993,11 @@ static void garble_digest_into(Network& n, const uint8_t* seeds, uint32_t B, uin
     n.gc_released = false;
     outs_begin(n, true, n.base);
     const size_t L = c.layers.size();
-    DevBuf leaves;
-    std::vector<uint32_t> hl;
-    std::vector<uint8_t> cat;
+    // leaf digests of one layer at a time, roots of every layer: [L][B][8]
+    // words; one host sync for the whole network
+    DevBuf leaves, roots;
+    leaves.ensure(std::max<size_t>((size_t)B * ((max_layer_cts(c) + kDigestLeafRows - 1) / kDigestLeafRows), 1) * 32);
+    roots.ensure(std::max<size_t>(L, 1) * B * 32);
     for (size_t li = 0; li < L; ++li) {
         run_layer_at(n, true, li);
         garble_act_flush(n);
@@ -2009,24 +2011,17 @@ static void garble_digest_into(Network& n, const uint8_t* seeds, uint32_t B, uin
         P.uc = l.tape ? l.tape->cts : 0;
         P.B = B;
         P.leaves = (uint32_t)((l.cts + kDigestLeafRows - 1) / kDigestLeafRows);
-        if (P.leaves) {
-            leaves.ensure((size_t)B * P.leaves * 32);
-            P.out = leaves.as<uint32_t>();
-            launch_digest(P, g_stream);
-            hl.resize((size_t)B * P.leaves * 8);
-            dev::d2h(hl.data(), leaves.p, hl.size() * 4, g_stream);
-            dev::sync(g_stream);
-        }
-        for (uint32_t b = 0; b < B; ++b) {
-            cat.resize((size_t)P.leaves * 32);
-            for (size_t w = 0; w < (size_t)P.leaves * 8; ++w) {
-                const uint32_t v = hl[(size_t)b * P.leaves * 8 + w];
-                for (int q = 0; q < 4; ++q) cat[4 * w + q] = (uint8_t)(v >> (24 - 8 * q));
-            }
-            sha256_bytes(cat.data(), cat.size(), digests + ((size_t)b * L + li) * 32);
-        }
+        P.out = leaves.as<uint32_t>();
+        launch_digest(P, roots.as<uint32_t>() + li * B * 8, g_stream);
     }
+    std::vector<uint32_t> hr(L * B * 8);
+    dev::d2h(hr.data(), roots.p, hr.size() * 4, g_stream);
     dev::sync(g_stream);
+    for (size_t li = 0; li < L; ++li)
+        for (uint32_t b = 0; b < B; ++b)
+            for (int t = 0; t < 8; ++t)
+                for (int q = 0; q < 4; ++q)
+                    digests[((size_t)b * L + li) * 32 + 4 * t + q] = (uint8_t)(hr[(li * B + b) * 8 + t] >> (24 - 8 * q));
     n.gc_released = true;
 }
 
@@ -3649,10 +3644,12 @@ static void network_digest(const Network& n, uint32_t b, uint8_t* digests) {
     if (b >= n.B) throw DataError("inference index out of range");
     n.require_gc();
     if (n.windowed && !n.host_gc) throw DataError("garbled circuit is not held whole");
-    DevBuf leaves, rows;
-    std::vector<uint32_t> hl;
-    std::vector<uint8_t> cat;
-    for (size_t li = 0; li < c.layers.size(); ++li) {
+    const size_t L = c.layers.size();
+    DevBuf leaves, roots, rows;
+    leaves.ensure(std::max<size_t>((max_layer_cts(c) + kDigestLeafRows - 1) / kDigestLeafRows, 1) * 32);
+    roots.ensure(std::max<size_t>(L, 1) * 32);
+    if (n.host_gc) rows.ensure(std::max<uint64_t>(max_layer_cts(c), 1) * 16);
+    for (size_t li = 0; li < L; ++li) {
         const HLayer& l = c.layers[li];
         DigestParams P;
         std::memset(&P, 0, sizeof P);
@@ -3660,8 +3657,8 @@ static void network_digest(const Network& n, uint32_t b, uint8_t* digests) {
         P.stride = l.cts;
         P.B = 1;
         P.leaves = (uint32_t)((l.cts + kDigestLeafRows - 1) / kDigestLeafRows);
+        P.out = leaves.as<uint32_t>();
         if (n.host_gc) {  // reference order already: copy the layer up
-            rows.ensure(std::max<uint64_t>(l.cts, 1) * 16);
             dev::h2d(rows.p, n.hblob.as<U4>() + (uint64_t)b * c.total_cts + l.ct_base, l.cts * 16, g_stream);
             P.src = rows.as<U4>();
         } else {
@@ -3669,19 +3666,13 @@ static void network_digest(const Network& n, uint32_t b, uint8_t* digests) {
             P.E = l.tape ? l.E_out : 0;
             P.uc = l.tape ? l.tape->cts : 0;
         }
-        if (P.leaves) {
-            leaves.ensure((size_t)P.leaves * 32);
-            P.out = leaves.as<uint32_t>();
-            launch_digest(P, g_stream);
-            hl.resize((size_t)P.leaves * 8);
-            dev::d2h(hl.data(), leaves.p, hl.size() * 4, g_stream);
-            dev::sync(g_stream);
-        }
-        cat.resize((size_t)P.leaves * 32);
-        for (size_t w = 0; w < (size_t)P.leaves * 8; ++w)
-            for (int q = 0; q < 4; ++q) cat[4 * w + q] = (uint8_t)(hl[w] >> (24 - 8 * q));
-        sha256_bytes(cat.data(), cat.size(), digests + li * 32);
+        launch_digest(P, roots.as<uint32_t>() + li * 8, g_stream);
     }
+    std::vector<uint32_t> hr(L * 8);
+    dev::d2h(hr.data(), roots.p, hr.size() * 4, g_stream);
+    dev::sync(g_stream);
+    for (size_t i = 0; i < L * 8; ++i)
+        for (int q = 0; q < 4; ++q) digests[4 * i + q] = (uint8_t)(hr[i] >> (24 - 8 * q));
 }
 
 int dashgpu_network_digest(const dashgpu_network* n, uint32_t b, uint8_t* digests) {

@@ -727,10 +727,16 @@ void launch_rows_permute(const RowsPermuteParams& P, void* st) {
     dev::check();
 }
 
-void launch_digest(const DigestParams& P, void* st) {
-    if (!P.leaves || !P.B) return;
+__global__ void __launch_bounds__(32) digest_root_kernel(DigestParams P, uint32_t* roots) {
+    const uint32_t b = blockIdx.x * 32 + threadIdx.x;
+    if (b < P.B) digest_root_thread(P, b, roots);
+}
+
+void launch_digest(const DigestParams& P, uint32_t* roots, void* st) {
+    if (!P.B) return;
     ProfScope ps(K_MISC, S(st));
-    digest_kernel<<<dim3(cdiv(P.leaves, 128), P.B), 128, 0, S(st)>>>(P);
+    if (P.leaves) digest_kernel<<<dim3(cdiv(P.leaves, 128), P.B), 128, 0, S(st)>>>(P);
+    digest_root_kernel<<<cdiv(P.B, 32), 32, 0, S(st)>>>(P, roots);
     dev::check();
 }
 

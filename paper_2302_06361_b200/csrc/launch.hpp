@@ -115,7 +115,8 @@ void launch_decode(const DecodeParams& P, void* stream);
 void launch_compress(const CompressParams& P, void* stream);
 void launch_decompress(const CompressParams& P, uint32_t* lane_out, void* stream);
 void launch_rows_permute(const RowsPermuteParams& P, void* stream);  // GC export / import row order
-void launch_digest(const DigestParams& P, void* stream);  // streamed-garbling layer digests (leaves)
+// streamed-garbling layer digests: leaves into P.out, then the roots [B][8] state words
+void launch_digest(const DigestParams& P, uint32_t* roots, void* stream);
 
 // primitive kernels for parity tests: op 0 decompress+compress, 1 aes_pi,
 // 2 aes with key, 3 prf label, 4 encrypt_label, 5 decrypt_label

@@ -288,10 +288,11 @@ void launch_rows_permute(const RowsPermuteParams& P, void*) {
     for (int64_t r = 0; r < (int64_t)(P.E * P.uc); ++r) rows_permute_thread(P, (uint64_t)r);
 }
 
-void launch_digest(const DigestParams& P, void*) {
+void launch_digest(const DigestParams& P, uint32_t* roots, void*) {
 #pragma omp parallel for collapse(2)
     for (uint32_t b = 0; b < P.B; ++b)
         for (uint32_t l = 0; l < P.leaves; ++l) digest_leaf_thread(P, b, l);
+    for (uint32_t b = 0; b < P.B; ++b) digest_root_thread(P, b, roots);
 }
 
 void launch_prim(const PrimParams& P, void*) {
