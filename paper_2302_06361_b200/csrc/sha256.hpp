@@ -1,6 +1,6 @@
 // SHA-256 (FIPS 180-4) for the streamed-garbling digest mode: the compression
-// function is DASH_HD so the leaf kernel (dash_layers.cuh digest_leaf_thread)
-// and root kernels and the host hash share it.
+// function is DASH_HD so the leaf and root kernels (dash_layers.cuh
+// digest_leaf_thread / digest_root_thread) and the host hash share it.
 //
 // Layer digest: the layer's ciphertext bytes in the
 // reference's GarbledCircuit::cts order (garble.cpp:134-240, 16 little-endian

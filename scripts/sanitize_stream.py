@@ -30,4 +30,7 @@ for name, seed, k, priv in [("model_tiny", 1000, 8, True), ("model_f_dims", 1006
     for b in range(B):
         assert h[b].digest() == hashlib.sha256(net.export_gc(b)).digest(), name
     assert dg.shape == (B, g.info.n_layers, 32)
+    for b in range(B):
+        assert (net.digest(b) == dg[b]).all(), name
+        assert (E.import_gc([net.export_gc(b)], host_resident=True).digest(0) == dg[b]).all(), name
 print("sanitize stream workload ok")
