@@ -1,6 +1,6 @@
 // SHA-256 (FIPS 180-4) for the streamed-garbling digest mode: the compression
 // function is DASH_HD so the leaf and root kernels (dash_layers.cuh
-// digest_leaf_thread / digest_root_thread) and the host hash share it.
+// digest_leaf_thread / digest_root_thread) and the CPU emulation share it.
 //
 // Layer digest: the layer's ciphertext bytes in the
 // reference's GarbledCircuit::cts order (garble.cpp:134-240, 16 little-endian
@@ -9,7 +9,6 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
-#include <cstring>
 
 #include "dash_common.hpp"
 
@@ -87,35 +86,6 @@ DASH_HD void sha256_rows(uint64_t rows, Row row, uint32_t out[8]) {
     w[15] = (uint32_t)bits;
     sha256_block(s, w);
     for (int t = 0; t < 8; ++t) out[t] = s[t];
-}
-
-// host: SHA-256 of a byte string (root of the leaf digests)
-inline void sha256_bytes(const uint8_t* data, size_t n, uint8_t out[32]) {
-    uint32_t s[8], w[16];
-    sha256_init(s);
-    size_t i = 0;
-    auto load = [&](const uint8_t* p) {
-        for (int t = 0; t < 16; ++t)
-            w[t] = (uint32_t)p[4 * t] << 24 | (uint32_t)p[4 * t + 1] << 16 | (uint32_t)p[4 * t + 2] << 8 | p[4 * t + 3];
-    };
-    for (; i + 64 <= n; i += 64) {
-        load(data + i);
-        sha256_block(s, w);
-    }
-    uint8_t tail[128];
-    std::memset(tail, 0, sizeof tail);
-    const size_t left = n - i;
-    if (left) std::memcpy(tail, data + i, left);
-    tail[left] = 0x80;
-    const size_t tl = left + 9 <= 64 ? 64 : 128;
-    const uint64_t bits = (uint64_t)n * 8;
-    for (int t = 0; t < 8; ++t) tail[tl - 1 - t] = (uint8_t)(bits >> (8 * t));
-    for (size_t o = 0; o < tl; o += 64) {
-        load(tail + o);
-        sha256_block(s, w);
-    }
-    for (int t = 0; t < 8; ++t)
-        for (int q = 0; q < 4; ++q) out[4 * t + q] = (uint8_t)(s[t] >> (24 - 8 * q));
 }
 
 }  // namespace dashgpu
